@@ -1,0 +1,30 @@
+"""paper_2110_11738_b200 -- B200-native (sm_100a) DROT optimal-transport solver.
+
+A drop-in for the reference's solve path (drot::solve<T>, drot_step,
+FusedEngine; /root/reference/proj/core/include/drot/).  All computation runs
+in libdrotb200.so (hand-written CUDA kernels behind the C ABI of
+include/drotb.h); importing this package fails loudly if the library has not
+been built -- there is no CPU fallback.
+"""
+from . import _lib
+from .api import (DeviceError, DrotConfig, DrotState, DualCertificate, EngineKind, Errc,
+                  Error, FusedArray, FusedEngine, FusedPassOutput, GaussianSpec,
+                  MemoryCounters, Order, PassOptions, Precision, ResidualReport,
+                  SolveResult, SolveStatus, SolveTrace, TilePlan, TraceRow, TransportPlan,
+                  TransportProblem, check_problem, drot_step, dyadic_marginal,
+                  gen_gaussian_problem, gen_gaussian_problem_as, init_state,
+                  kernel_launches, plan_tiles, recover_duals, rho0_warmup_preset, solve)
+from .session import Session
+
+LIB_PATH = _lib.LIB_PATH
+_lib.load()
+
+__all__ = [
+    "DeviceError", "DrotConfig", "DrotState", "DualCertificate", "EngineKind", "Errc",
+    "Error", "FusedArray", "FusedEngine", "FusedPassOutput", "GaussianSpec",
+    "MemoryCounters", "Order", "PassOptions", "Precision", "ResidualReport", "SolveResult",
+    "SolveStatus", "SolveTrace", "TilePlan", "TraceRow", "TransportPlan",
+    "TransportProblem", "check_problem", "drot_step", "dyadic_marginal",
+    "gen_gaussian_problem", "gen_gaussian_problem_as", "init_state", "kernel_launches",
+    "plan_tiles", "recover_duals", "rho0_warmup_preset", "solve", "Session", "LIB_PATH",
+]

@@ -1,0 +1,165 @@
+// drotb_internal.hpp -- shared declarations of the B200 DROT engine
+// (device argument blocks, solver bookkeeping, kernel launchers).
+//
+// Device layout (column-major like the reference, matrix.hpp:56-59):
+//   X, C        ld x n, ld = round_up(m_rows, 32) (every column 128-B aligned;
+//               pad rows are zero and never enter a reduction)
+//   phi, a, r   ld-length row vectors;  varphi, b, s   n-length column vectors
+//   ustrip      grid_cols x ld     per-tile row-sum strips  (fused.hpp:194)
+//   vstrip      grid_rows64 x n    per-64-row-block column-sum strips (:195)
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace drotb {
+
+// Pass modes of the fused sweep (fused.hpp:244-289).
+enum PassMode : int {
+  kPlain0 = 0,  // fused_pass, parity 0: ((x+phi)+varphi) - rho c
+  kPlain1 = 1,  // fused_pass, parity 1: ((x - rho c)+phi)+varphi
+  kFold = 2,    // skip-C fold pass: parity 0, writes X+ - rho C
+  kSkip = 3,    // skip-C pass on a folded array: (x+phi)+varphi, no C read
+};
+
+constexpr int kWarpsPerCta = 4;
+constexpr int kChunkCols = 16;   // columns staged per warp for the v sums
+constexpr int kVBlockRows = 64;  // reference block_rows of the v strips
+
+template <class T>
+struct PassPartial {  // per-CTA partial reductions (fused.hpp:85-93)
+  T cost, prev, dual, dx, max_abs;
+  int bad;
+  int pad;
+};
+
+template <class T>
+struct PassArgs {
+  T* __restrict__ xy;
+  const T* __restrict__ cost;
+  const T* __restrict__ phi;
+  const T* __restrict__ varphi;
+  T rho;
+  int64_t m, n, ld;     // rows, cols, leading dimension
+  int64_t row_begin;    // global row of local row 0 (multi-GPU shards)
+  int64_t tc;           // tile columns (ws * bs)
+  T* __restrict__ ustrip;
+  T* __restrict__ vstrip;
+  PassPartial<T>* __restrict__ partials;
+  const int* stop;      // device stop flag (nullptr: never)
+};
+
+// Device-resident solver bookkeeping: every scalar of the solve loop
+// (solver.hpp:394-521) and of DrotState (solver.hpp:98-114).
+template <class T>
+struct Book {
+  // DrotState scalars
+  T alpha, beta, coef;
+  T nr2, ns2;  // vec_norm_sq(r), vec_norm_sq(s)
+  int64_t iter;        // iterations completed (state.iter)
+  int64_t iterations;  // result.trace.iterations
+  int32_t folded;
+  int32_t stop, converged, failed, confirm;
+  int32_t prev_pass_had_cost;
+  // pass totals of the last sweep (FusedPassOutput scalars)
+  T pass_cost, pass_prev, pass_dual, pass_dx, pass_max_abs;
+  int32_t pass_bad, pad0;
+  // solve-loop scalars
+  double last_cost, last_r_dual;
+  double erg_mean;
+  int64_t erg_count;
+  double r_primal, dual_value, gap, fp_residual;
+  double rep_r_primal, rep_r_dual, rep_gap, rep_objective;  // exact report
+  int64_t trace_rows;
+  int64_t gate_hits;
+  // configuration (written once)
+  int64_t max_iters, check_every, trace_every, trace_cap;
+  double tol_primal, tol_dual, tol_gap, primal_scale;
+  int32_t record_trace, relative;
+  unsigned int ticket_merge, ticket_update, ticket_report, pad1;
+};
+
+struct TraceRowDev {
+  int64_t iter;
+  double r_primal, r_dual, gap, objective, ergodic_objective,
+      fixed_point_residual;
+};
+
+template <class T>
+struct TailArgs {
+  int64_t m, n, ld;
+  int64_t m_global, n_global;  // problem sizes (rho, beta and inv_m/inv_n)
+  int32_t folded_after;        // fold state of the array after this pass
+  int32_t pad0;
+  int64_t grid_cols;    // number of u strips
+  int64_t grid_rows64;  // number of v strips (local)
+  const T* ustrip;
+  const T* vstrip;
+  const PassPartial<T>* pass_partials;
+  int64_t n_pass_partials;
+  const T* p;
+  const T* q;
+  T* u;        // merged row sums (engine API)
+  T* v;        // merged col sums
+  T* r_new;
+  T* s_new;
+  const T* r_old;
+  const T* s_old;
+  T* phi;
+  T* varphi;
+  T* a;
+  T* b;
+  T rho;
+  // pass properties
+  int32_t reads_cost, want_dual, want_dx;
+  int32_t solver;  // 0: engine pass only (no recursions)
+  // reduction scratch
+  double* dscratch;   // per-CTA double partials (update / report kernels)
+  T* tscratch;        // per-CTA T partials (merge kernel)
+  double* terms;      // exact mode per-element double terms (m+n)*3
+  Book<T>* book;
+  TraceRowDev* trace;
+  // exact-mode per-tile scalar chains (tile order)
+  const PassPartial<T>* tile_partials;
+  int64_t n_tiles;
+};
+
+// ---- kernel launchers (kernels.cu) ---------------------------------------
+template <class T>
+void launch_pass(const PassArgs<T>& a, int mode, bool want_dual, bool want_dx,
+                 cudaStream_t st);
+template <class T>
+void launch_tile_chains(const PassArgs<T>& a, int mode, bool want_dual,
+                        bool want_dx, int64_t bs, PassPartial<T>* tiles,
+                        cudaStream_t st);
+template <class T>
+void launch_merge(const TailArgs<T>& t, bool exact, cudaStream_t st);
+template <class T>
+void launch_update(const TailArgs<T>& t, bool exact, cudaStream_t st);
+template <class T>
+void launch_report(const T* xy, const T* cost, const TailArgs<T>& t,
+                   bool exact, bool always, cudaStream_t st);
+template <class T>
+void launch_init_x0(T* xy, const T* p, const T* q, int64_t m, int64_t n,
+                    int64_t ld, cudaStream_t st);
+template <class T>
+void launch_init_sums(const T* xy, const T* p, const T* q, T* a, T* b,
+                      int64_t m, int64_t n, int64_t ld, Book<T>* book,
+                      cudaStream_t st);
+template <class T>
+void launch_validate(const T* buf, int64_t m, int64_t n, int64_t ld,
+                     unsigned long long* first_nonfinite,
+                     unsigned long long* first_negative, cudaStream_t st);
+template <class T>
+void launch_materialize(const T* xy, const T* cost, T* out, T rho,
+                        int folded, int64_t m, int64_t n, int64_t ld,
+                        cudaStream_t st);
+
+int64_t kernel_launch_count();
+void count_launch(int64_t k = 1);
+
+inline int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace drotb

@@ -1,0 +1,1088 @@
+// kernels.cu -- sm_100a kernels of the B200 DROT engine.
+//
+//   K1  pass_kernel        one fused read-modify-write sweep per iteration
+//                          (FusedEngine<T>::run_pass, fused.hpp:206-357)
+//   K1x tile_chain_kernel  reference-order per-tile scalar chains (exact mode)
+//   K2  merge_kernel       strip merge -> u, v, r, s; scalar recursions
+//                          (fused.hpp:312-356; solver.hpp:268-278, 425-437)
+//   K3  update_kernel      phi/varphi/a/b recursions + gate
+//                          (solver.hpp:277-289, 443-504)
+//   K5  report_kernel      exact matched-pair report + confirm
+//                          (detail::state_report, solver.hpp:312-354, 503-519)
+//   K4  init_*             init_state (solver.hpp:143-186)
+//   K0  validate_kernel    check_problem's matrix scan (problem.hpp:129-133)
+//   K6  materialize_kernel materialize_plan (solver.hpp:204-217)
+//
+// Arithmetic contract: the library is compiled with -fmad=false, so every
+// expression below is evaluated exactly as written, in the association order
+// of the reference (no FMA contraction).  The fast-mode scalar reductions of
+// K1 use explicit fma() because their order is ours anyway.
+#include <cfloat>
+#include <cstdio>
+
+#include "drotb_internal.hpp"
+
+namespace drotb {
+
+// ---------------------------------------------------------------------------
+// small helpers
+// ---------------------------------------------------------------------------
+static int64_t g_launches = 0;
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) {
+  return a < b ? a : b;
+}
+int64_t kernel_launch_count() { return g_launches; }
+void count_launch(int64_t k) { g_launches += k; }
+
+template <class T>
+struct V16;
+template <>
+struct V16<float> {
+  using type = float4;
+};
+template <>
+struct V16<double> {
+  using type = double2;
+};
+
+__device__ __forceinline__ void unpack(const float4& v, float* o) {
+  o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+}
+__device__ __forceinline__ void unpack(const double2& v, double* o) {
+  o[0] = v.x; o[1] = v.y;
+}
+__device__ __forceinline__ float4 pack4(const float* o) {
+  return make_float4(o[0], o[1], o[2], o[3]);
+}
+__device__ __forceinline__ double2 pack4(const double* o) {
+  return make_double2(o[0], o[1]);
+}
+template <class T>
+__device__ __forceinline__ typename V16<T>::type vzero() {
+  typename V16<T>::type z;
+  T* p = reinterpret_cast<T*>(&z);
+#pragma unroll
+  for (int t = 0; t < int(16 / sizeof(T)); ++t) p[t] = T(0);
+  return z;
+}
+
+template <class T>
+__device__ __forceinline__ T max_finite();
+template <>
+__device__ __forceinline__ float max_finite<float>() { return FLT_MAX; }
+template <>
+__device__ __forceinline__ double max_finite<double>() { return DBL_MAX; }
+
+template <class T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <class T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Fixed-shape block tree reduction of K values (deterministic: the tree
+// depends only on blockDim).  Result valid in thread 0.
+template <class T, int K>
+__device__ __forceinline__ void block_sum(T (&v)[K], T* sh /* K*32 */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < K; ++k) sh[k * 32 + warp] = v[k];
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      T x = lane < nw ? sh[k * 32 + lane] : T(0);
+      v[k] = warp_sum(x);
+    }
+  }
+  __syncthreads();
+}
+
+// Grid-level "last block done" ticket (threadFenceReduction pattern).
+__device__ __forceinline__ bool last_block(unsigned int* ticket) {
+  __shared__ bool is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int t = atomicAdd(ticket, 1u);
+    is_last = (t == gridDim.x * gridDim.y - 1);
+  }
+  __syncthreads();
+  if (is_last) __threadfence();
+  return is_last;
+}
+
+// ---------------------------------------------------------------------------
+// K1: the fused sweep
+// ---------------------------------------------------------------------------
+// Thread mapping: a warp owns 32*R consecutive rows (R = 16 B / sizeof(T)
+// rows per lane, one 128-bit load per column) of one reference tile column
+// [c0, c0+tc).  Each lane walks the tile's columns in order, so its row
+// partials are exactly the reference's u strips (fused.hpp:267, tile-local
+// running sum from 0).  Column partials must be sequential over each
+// 64-row block (fused.hpp:268): the warp stages x+ of 16 columns in shared
+// memory (conflict-free swizzle) and one lane per (column, 64-row block)
+// sums the 64 values in row order.
+//
+// Swizzle: element (c, r) of a warp's [16 x 32R] staging tile lives at
+//   c*32R + R*((r/R) ^ H(c, r)) + ((r + c) mod R)
+// fp32 (R=4): H = (c>>2) | ((r>>6)<<2);  fp64 (R=2): H = (c>>1) & 7.
+// Writes (one 16-B vector per lane, components rotated by c) and the
+// row-order reads (lane = column/block) are both bank-conflict free.
+template <class T>
+__device__ __forceinline__ int stage_index(int c, int r) {
+  constexpr int R = 16 / sizeof(T);
+  constexpr int ROWS_W = 32 * R;
+  if constexpr (R == 4) {
+    const int h = (c >> 2) | ((r >> 6) << 2);
+    return c * ROWS_W + 4 * ((r >> 2) ^ h) + ((r + c) & 3);
+  } else {
+    const int h = (c >> 1) & 7;
+    return c * ROWS_W + 2 * ((r >> 1) ^ h) + ((r + c) & 1);
+  }
+}
+
+template <class T>
+struct PassAcc {
+  T cost, prev, dual, dx, mx;
+  bool bad;
+};
+
+template <class T, int MODE, bool DUAL, bool DX, bool MASK>
+__device__ __forceinline__ void pass_chunk(const PassArgs<T>& a, int64_t j0,
+                                           int cnt, int64_t row0, int nvalid,
+                                           const T (&ph)[16 / sizeof(T)],
+                                           T (&u)[16 / sizeof(T)],
+                                           PassAcc<T>& acc, T* wbuf,
+                                           int lane) {
+  using V = typename V16<T>::type;
+  constexpr int R = 16 / sizeof(T);
+  constexpr int CH = kChunkCols;
+  constexpr int G = 8;  // columns in flight per lane
+  constexpr bool RC = MODE != kSkip;
+  const bool live = !MASK || nvalid > 0;
+#pragma unroll
+  for (int g = 0; g < CH; g += G) {
+    V xv[G], cv[G];
+    T vj[G];
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      const int c = g + k;
+      xv[k] = vzero<T>();
+      cv[k] = vzero<T>();
+      vj[k] = T(0);
+      if (c < cnt) {
+        const int64_t off = (j0 + c) * a.ld + row0;
+        if (live) {
+          xv[k] = __ldcs(reinterpret_cast<const V*>(a.xy + off));
+          if (RC) cv[k] = __ldcs(reinterpret_cast<const V*>(a.cost + off));
+        }
+        vj[k] = __ldg(a.varphi + j0 + c);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      const int c = g + k;
+      if (c < cnt) {
+        T x[R], cc[R], xp[R], st[R];
+        unpack(xv[k], x);
+        unpack(cv[k], cc);
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+          T e = T(0), tv;
+          if (RC) {
+            e = a.rho * cc[t];
+            if (MODE == kPlain1)
+              tv = ((x[t] - e) + ph[t]) + vj[k];
+            else
+              tv = ((x[t] + ph[t]) + vj[k]) - e;
+          } else {
+            tv = (x[t] + ph[t]) + vj[k];
+          }
+          T p = tv > T(0) ? tv : T(0);
+          const bool valid = !MASK || t < nvalid;
+          if (MASK && !valid) {
+            p = T(0);
+            tv = T(0);
+          }
+          xp[t] = p;
+          st[t] = (MODE == kFold) ? p - e : p;
+          u[t] += p;
+          if (RC) {
+            acc.cost = fma(cc[t], p, acc.cost);
+            acc.prev = fma(cc[t], x[t], acc.prev);
+            if (DUAL) {
+              const T d = (ph[t] + vj[k]) - e;
+              if (valid && d > T(0)) acc.dual = fma(d, d, acc.dual);
+            }
+          }
+          if (DX) {
+            const T dd = p - x[t];
+            acc.dx = fma(dd, dd, acc.dx);
+          }
+          const T at = fabs(tv);
+          acc.mx = fmax(acc.mx, at);
+          acc.bad |= !(at <= max_finite<T>());
+        }
+        if (live) {
+          const int64_t off = (j0 + c) * a.ld + row0;
+          __stcs(reinterpret_cast<V*>(a.xy + off), pack4(st));
+        }
+        // stage x+ for the column sums, components rotated by c
+        T rot[R];
+#pragma unroll
+        for (int pp = 0; pp < R; ++pp) rot[pp] = xp[(pp - c) & (R - 1)];
+        int h;
+        if constexpr (R == 4)
+          h = (c >> 2) | ((lane >> 4) << 2);
+        else
+          h = (c >> 1) & 7;
+        *reinterpret_cast<V*>(wbuf + c * 32 * R + R * (lane ^ h)) = pack4(rot);
+      }
+    }
+  }
+}
+
+template <class T, int MODE, bool DUAL, bool DX>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+    pass_kernel(const PassArgs<T> a) {
+  using V = typename V16<T>::type;
+  constexpr int R = 16 / sizeof(T);
+  constexpr int ROWS_W = 32 * R;
+  constexpr int NB = ROWS_W / kVBlockRows;
+  constexpr int CH = kChunkCols;
+  __shared__ __align__(16) T sbuf[kWarpsPerCta][CH * ROWS_W];
+  __shared__ PassAcc<T> wacc[kWarpsPerCta];
+  if (a.stop != nullptr && *reinterpret_cast<const volatile int*>(a.stop)) return;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t wrow0 =
+      (static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + warp) * ROWS_W;
+  const int64_t row0 = wrow0 + static_cast<int64_t>(lane) * R;
+  const int64_t gc = blockIdx.y;
+  const int64_t c0 = gc * a.tc;
+  const int64_t c1 = min(a.n, c0 + a.tc);
+  int64_t nv = a.m - row0;
+  const int nvalid = nv <= 0 ? 0 : (nv >= R ? R : static_cast<int>(nv));
+  T* wbuf = sbuf[warp];
+
+  T ph[R], u[R];
+  if (nvalid > 0) {
+    unpack(*reinterpret_cast<const V*>(a.phi + row0), ph);
+  } else {
+#pragma unroll
+    for (int t = 0; t < R; ++t) ph[t] = T(0);
+  }
+#pragma unroll
+  for (int t = 0; t < R; ++t) u[t] = T(0);
+  PassAcc<T> acc{T(0), T(0), T(0), T(0), T(0), false};
+
+  for (int64_t j0 = c0; j0 < c1; j0 += CH) {
+    const int cnt = static_cast<int>(imin64(CH, c1 - j0));
+    if (nvalid == R)
+      pass_chunk<T, MODE, DUAL, DX, false>(a, j0, cnt, row0, nvalid, ph, u, acc,
+                                           wbuf, lane);
+    else
+      pass_chunk<T, MODE, DUAL, DX, true>(a, j0, cnt, row0, nvalid, ph, u, acc,
+                                          wbuf, lane);
+    __syncwarp();
+    if (lane < CH * NB) {
+      const int c = lane % CH, b = lane / CH;
+      const int64_t gb = wrow0 / kVBlockRows + b;
+      if (c < cnt && gb * kVBlockRows < a.m) {
+        T s = T(0);
+#pragma unroll 16
+        for (int i = 0; i < kVBlockRows; ++i)
+          s += wbuf[stage_index<T>(c, b * kVBlockRows + i)];
+        a.vstrip[gb * a.n + j0 + c] = s;
+      }
+    }
+    __syncwarp();
+  }
+  if (nvalid > 0)
+    *reinterpret_cast<V*>(a.ustrip + gc * a.ld + row0) = pack4(u);
+
+  // deterministic CTA partials: warp tree, then warps in order
+  acc.cost = warp_sum(acc.cost);
+  acc.prev = warp_sum(acc.prev);
+  acc.dual = warp_sum(acc.dual);
+  acc.dx = warp_sum(acc.dx);
+  acc.mx = warp_max(acc.mx);
+  const bool wbad = __any_sync(0xffffffffu, acc.bad);
+  if (lane == 0) {
+    acc.bad = wbad;
+    wacc[warp] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    PassPartial<T> out{T(0), T(0), T(0), T(0), T(0), 0, 0};
+#pragma unroll
+    for (int w = 0; w < kWarpsPerCta; ++w) {
+      out.cost += wacc[w].cost;
+      out.prev += wacc[w].prev;
+      out.dual += wacc[w].dual;
+      out.dx += wacc[w].dx;
+      out.max_abs = fmax(out.max_abs, wacc[w].mx);
+      out.bad |= wacc[w].bad ? 1 : 0;
+    }
+    a.partials[static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x] = out;
+  }
+}
+
+template <class T, int MODE, bool DUAL, bool DX>
+static void launch_pass_t(const PassArgs<T>& a, cudaStream_t st) {
+  constexpr int R = 16 / sizeof(T);
+  const int64_t rows_cta = int64_t(kWarpsPerCta) * 32 * R;
+  dim3 grid(static_cast<unsigned>((a.m + rows_cta - 1) / rows_cta),
+            static_cast<unsigned>((a.n + a.tc - 1) / a.tc));
+  pass_kernel<T, MODE, DUAL, DX><<<grid, kWarpsPerCta * 32, 0, st>>>(a);
+  count_launch();
+}
+
+template <class T>
+void launch_pass(const PassArgs<T>& a, int mode, bool want_dual, bool want_dx,
+                 cudaStream_t st) {
+#define DROTB_PASS_CASE(M)                                         \
+  case M:                                                          \
+    if (want_dual) {                                               \
+      if (want_dx) launch_pass_t<T, M, true, true>(a, st);         \
+      else launch_pass_t<T, M, true, false>(a, st);                \
+    } else {                                                       \
+      if (want_dx) launch_pass_t<T, M, false, true>(a, st);        \
+      else launch_pass_t<T, M, false, false>(a, st);               \
+    }                                                              \
+    break;
+  switch (mode) {
+    DROTB_PASS_CASE(kPlain0)
+    DROTB_PASS_CASE(kPlain1)
+    DROTB_PASS_CASE(kFold)
+    default:
+      launch_pass_t<T, kSkip, false, false>(a, st);
+  }
+#undef DROTB_PASS_CASE
+}
+
+// ---------------------------------------------------------------------------
+// K1x: reference-order tile scalar chains (exact mode only)
+// ---------------------------------------------------------------------------
+// One warp per reference tile (plan_tiles order: gc-major, gr-minor,
+// tiles.cpp:36-45); lanes 0..4 each run one of the serial chains of
+// fused.hpp:269-283 over the tile in j-outer / i-inner order, recomputing
+// x+ bit-identically from the pre-pass array.
+template <class T, int MODE, bool DUAL, bool DX>
+__global__ void tile_chain_kernel(const PassArgs<T> a, int64_t bs,
+                                  int64_t grid_rows, int64_t n_tiles,
+                                  PassPartial<T>* tiles) {
+  if (a.stop != nullptr && *reinterpret_cast<const volatile int*>(a.stop)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t tile =
+      static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (tile >= n_tiles || lane >= 5) return;
+  constexpr bool RC = MODE != kSkip;
+  const int64_t gcol = tile / grid_rows, grow = tile % grid_rows;
+  const int64_t r0 = grow * bs, r1 = min(a.m, r0 + bs);
+  const int64_t cb = gcol * a.tc, ce = min(a.n, cb + a.tc);
+  T acc = T(0);
+  bool bad = false;
+  for (int64_t j = cb; j < ce; ++j) {
+    const T vj = a.varphi[j];
+    const T* xc = a.xy + j * a.ld;
+    const T* ccol = a.cost + j * a.ld;
+    for (int64_t i = r0; i < r1; ++i) {
+      const T x = xc[i];
+      const T phi = a.phi[i];
+      T e = T(0), c = T(0), tv;
+      if (RC) {
+        c = ccol[i];
+        e = a.rho * c;
+        if (MODE == kPlain1)
+          tv = ((x - e) + phi) + vj;
+        else
+          tv = ((x + phi) + vj) - e;
+      } else {
+        tv = (x + phi) + vj;
+      }
+      const T xp = tv > T(0) ? tv : T(0);
+      switch (lane) {
+        case 0:
+          if (RC) acc += c * xp;
+          break;
+        case 1:
+          if (RC) acc += c * x;
+          break;
+        case 2:
+          if (RC && DUAL) {
+            const T d = (phi + vj) - e;
+            if (d > T(0)) acc += d * d;
+          }
+          break;
+        case 3:
+          if (DX) {
+            const T dx = xp - x;
+            acc += dx * dx;
+          }
+          break;
+        default: {
+          const T at = fabs(tv);
+          if (at > acc) acc = at;
+          if (!(at <= max_finite<T>())) bad = true;
+        }
+      }
+    }
+  }
+  PassPartial<T>& o = tiles[tile];
+  switch (lane) {
+    case 0: o.cost = acc; break;
+    case 1: o.prev = acc; break;
+    case 2: o.dual = acc; break;
+    case 3: o.dx = acc; break;
+    default:
+      o.max_abs = acc;
+      o.bad = bad ? 1 : 0;
+  }
+}
+
+template <class T, int MODE, bool DUAL, bool DX>
+static void launch_chain_t(const PassArgs<T>& a, int64_t bs,
+                           PassPartial<T>* tiles, cudaStream_t st) {
+  const int64_t grid_rows = (a.m + bs - 1) / bs;
+  const int64_t grid_cols = (a.n + a.tc - 1) / a.tc;
+  const int64_t n_tiles = grid_rows * grid_cols;
+  const int wpb = 4;
+  const unsigned blocks = static_cast<unsigned>((n_tiles + wpb - 1) / wpb);
+  tile_chain_kernel<T, MODE, DUAL, DX>
+      <<<blocks, wpb * 32, 0, st>>>(a, bs, grid_rows, n_tiles, tiles);
+  count_launch();
+}
+
+template <class T>
+void launch_tile_chains(const PassArgs<T>& a, int mode, bool want_dual,
+                        bool want_dx, int64_t bs, PassPartial<T>* tiles,
+                        cudaStream_t st) {
+#define DROTB_CHAIN_CASE(M)                                              \
+  case M:                                                                \
+    if (want_dual) {                                                     \
+      if (want_dx) launch_chain_t<T, M, true, true>(a, bs, tiles, st);   \
+      else launch_chain_t<T, M, true, false>(a, bs, tiles, st);          \
+    } else {                                                             \
+      if (want_dx) launch_chain_t<T, M, false, true>(a, bs, tiles, st);  \
+      else launch_chain_t<T, M, false, false>(a, bs, tiles, st);         \
+    }                                                                    \
+    break;
+  switch (mode) {
+    DROTB_CHAIN_CASE(kPlain0)
+    DROTB_CHAIN_CASE(kPlain1)
+    DROTB_CHAIN_CASE(kFold)
+    default:
+      launch_chain_t<T, kSkip, false, false>(a, bs, tiles, st);
+  }
+#undef DROTB_CHAIN_CASE
+}
+
+// ---------------------------------------------------------------------------
+// K2: merge strips, r/s, scalar recursions
+// ---------------------------------------------------------------------------
+constexpr int kTailThreads = 256;
+
+// Serial ascending-index sum / sum of squares (vec_sum, vec_norm_sq:
+// matrix.hpp:99-118), one thread.
+template <class T, bool SQUARE>
+__device__ T serial_sum(const T* x, int64_t len) {
+  T acc = T(0);
+  int64_t k = 0;
+  for (; k + 8 <= len; k += 8) {
+    T v[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) v[t] = x[k + t];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) acc += SQUARE ? v[t] * v[t] : v[t];
+  }
+  for (; k < len; ++k) acc += SQUARE ? x[k] * x[k] : x[k];
+  return acc;
+}
+
+template <class T>
+__device__ __forceinline__ void erg_update(Book<T>* bk, double value) {
+  bk->erg_count += 1;
+  bk->erg_mean += (value - bk->erg_mean) / static_cast<double>(bk->erg_count);
+}
+
+template <class T, bool EXACT>
+__global__ void __launch_bounds__(kTailThreads) merge_kernel(const TailArgs<T> t) {
+  Book<T>* bk = t.book;
+  if (t.solver && *reinterpret_cast<volatile int*>(&bk->stop)) return;
+  __shared__ T shT[4 * 32];
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  T part[3] = {T(0), T(0), T(0)};  // sum r, sum r^2, sum s^2
+  if (idx < t.m) {
+    T acc = T(0);
+    for (int64_t g = 0; g < t.grid_cols; ++g) acc += t.ustrip[g * t.ld + idx];
+    t.u[idx] = acc;
+    const T r = acc - t.p[idx];
+    t.r_new[idx] = r;
+    part[0] = r;
+    part[1] = r * r;
+  } else if (idx < t.m + t.n) {
+    const int64_t j = idx - t.m;
+    T acc = T(0);
+    for (int64_t g = 0; g < t.grid_rows64; ++g) acc += t.vstrip[g * t.n + j];
+    t.v[j] = acc;
+    const T s = acc - t.q[j];
+    t.s_new[j] = s;
+    part[2] = s * s;
+  }
+  if (!EXACT) {
+    block_sum<T, 3>(part, shT);
+    if (threadIdx.x == 0)
+      for (int k = 0; k < 3; ++k) t.tscratch[blockIdx.x * 3 + k] = part[k];
+  }
+  if (!last_block(&bk->ticket_merge)) return;
+
+  // ---- last block: totals in a fixed order ----
+  __shared__ T tot[8];
+  __shared__ int totbad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (EXACT) {
+    // tile order chains (fused.hpp:322-329) + sequential vec sums
+    if (warp == 0 && lane < 5) {
+      T acc = T(0);
+      int bad = 0;
+      for (int64_t k = 0; k < t.n_tiles; ++k) {
+        const PassPartial<T>& sc = t.tile_partials[k];
+        switch (lane) {
+          case 0: acc += sc.cost; break;
+          case 1: acc += sc.prev; break;
+          case 2: acc += sc.dual; break;
+          case 3: acc += sc.dx; break;
+          default:
+            if (sc.max_abs > acc) acc = sc.max_abs;
+            bad |= sc.bad;
+        }
+      }
+      tot[lane] = acc;
+      if (lane == 4) totbad = bad;
+    }
+    if (t.solver) {
+      if (warp == 1 && lane == 0) tot[5] = serial_sum<T, false>(t.r_new, t.m);
+      if (warp == 2 && lane == 0) tot[6] = serial_sum<T, true>(t.r_new, t.m);
+      if (warp == 3 && lane == 0) tot[7] = serial_sum<T, true>(t.s_new, t.n);
+    }
+    __syncthreads();
+  } else {
+    T v4[4] = {T(0), T(0), T(0), T(0)};
+    T mx = T(0);
+    int bad = 0;
+    for (int64_t k = tid; k < t.n_pass_partials; k += blockDim.x) {
+      const PassPartial<T>& sc = t.pass_partials[k];
+      v4[0] += sc.cost;
+      v4[1] += sc.prev;
+      v4[2] += sc.dual;
+      v4[3] += sc.dx;
+      mx = fmax(mx, sc.max_abs);
+      bad |= sc.bad;
+    }
+    T s3[3] = {T(0), T(0), T(0)};
+    for (int64_t k = tid; k < gridDim.x; k += blockDim.x)
+      for (int q = 0; q < 3; ++q) s3[q] += t.tscratch[k * 3 + q];
+    block_sum<T, 4>(v4, shT);
+    block_sum<T, 3>(s3, shT);
+    mx = warp_max(mx);
+    __shared__ T shm[32];
+    __shared__ int shb[32];
+    bad = __any_sync(0xffffffffu, bad) ? 1 : 0;
+    if (lane == 0) {
+      shm[warp] = mx;
+      shb[warp] = bad;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      T m2 = T(0);
+      int b2 = 0;
+      for (int w = 0; w < (blockDim.x >> 5); ++w) {
+        m2 = fmax(m2, shm[w]);
+        b2 |= shb[w];
+      }
+      for (int k = 0; k < 4; ++k) tot[k] = v4[k];
+      tot[4] = m2;
+      totbad = b2;
+      tot[5] = s3[0];
+      tot[6] = s3[1];
+      tot[7] = s3[2];
+    }
+    __syncthreads();
+  }
+  if (tid != 0) return;
+  bk->ticket_merge = 0u;
+  bk->pass_cost = tot[0];
+  bk->pass_prev = tot[1];
+  bk->pass_dual = tot[2];
+  bk->pass_dx = tot[3];
+  bk->pass_max_abs = tot[4];
+  bk->pass_bad = totbad;
+  if (!t.solver) return;
+  const int64_t k = bk->iter;
+  bk->folded = t.folded_after;
+  if (totbad) {  // solver.hpp:266, 418-422
+    bk->failed = 1;
+    bk->iterations = k + 1;
+    bk->stop = 1;
+    return;
+  }
+  // step_impl recursions (solver.hpp:273-277)
+  const T beta = tot[5] / static_cast<T>(t.m_global + t.n_global);
+  bk->beta = beta;
+  bk->coef = T(2) * beta - bk->alpha;
+  bk->nr2 = tot[6];
+  bk->ns2 = tot[7];
+  bk->iterations = k + 1;
+  // objective bookkeeping (solver.hpp:428-437)
+  const bool cost_valid = t.reads_cost != 0;
+  const bool dual_valid = t.reads_cost && t.want_dual;
+  if (!bk->prev_pass_had_cost && cost_valid)
+    erg_update(bk, static_cast<double>(tot[1]));
+  if (cost_valid) {
+    bk->last_cost = static_cast<double>(tot[0]);
+    erg_update(bk, bk->last_cost);
+  }
+  bk->prev_pass_had_cost = cost_valid ? 1 : 0;
+  if (dual_valid)
+    bk->last_r_dual =
+        sqrt(static_cast<double>(tot[2])) / static_cast<double>(t.rho);
+}
+
+template <class T>
+void launch_merge(const TailArgs<T>& t, bool exact, cudaStream_t st) {
+  const unsigned blocks =
+      static_cast<unsigned>((t.m + t.n + kTailThreads - 1) / kTailThreads);
+  if (exact)
+    merge_kernel<T, true><<<blocks, kTailThreads, 0, st>>>(t);
+  else
+    merge_kernel<T, false><<<blocks, kTailThreads, 0, st>>>(t);
+  count_launch();
+}
+
+// ---------------------------------------------------------------------------
+// K3: shift / defect recursions, dual value, trace row, gate
+// ---------------------------------------------------------------------------
+template <class T, bool EXACT>
+__global__ void __launch_bounds__(kTailThreads) update_kernel(const TailArgs<T> t) {
+  Book<T>* bk = t.book;
+  if (*reinterpret_cast<volatile int*>(&bk->stop)) return;
+  __shared__ double shD[6 * 32];
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const T coef = bk->coef;
+  const T inv_n = T(1) / static_cast<T>(t.n_global);
+  const T inv_m = T(1) / static_cast<T>(t.m_global);
+  const double drho = static_cast<double>(t.rho);
+  const bool fp = bk->record_trace != 0;
+  // 0 dual value, 1 dphi^2, 2 sum dphi, 3 dvarphi^2, 4 sum dvarphi, 5 cross
+  double part[6] = {0, 0, 0, 0, 0, 0};
+  const int64_t mn = t.m + t.n;
+  if (idx < t.m) {
+    const T r = t.r_new[idx];
+    const T ph_old = t.phi[idx];
+    const T ph = (t.a[idx] - T(2) * r + coef) * inv_n;
+    t.phi[idx] = ph;
+    t.a[idx] = t.a[idx] - r;
+    part[0] = static_cast<double>(t.p[idx]) * static_cast<double>(ph) / drho;
+    if (fp) {
+      const double d = static_cast<double>(ph) - static_cast<double>(ph_old);
+      part[1] = d * d;
+      part[2] = d;
+      part[5] = d * (static_cast<double>(r) - static_cast<double>(t.r_old[idx]));
+    }
+    if (EXACT) {
+      t.terms[idx] = part[0];
+      t.terms[mn + idx] = part[2];
+      t.terms[2 * mn + idx] = part[5];
+    }
+  } else if (idx < mn) {
+    const int64_t j = idx - t.m;
+    const T s = t.s_new[j];
+    const T vp_old = t.varphi[j];
+    const T vp = (t.b[j] - T(2) * s + coef) * inv_m;
+    t.varphi[j] = vp;
+    t.b[j] = t.b[j] - s;
+    part[0] = static_cast<double>(t.q[j]) * static_cast<double>(vp) / drho;
+    if (fp) {
+      const double d = static_cast<double>(vp) - static_cast<double>(vp_old);
+      part[3] = d * d;
+      part[4] = d;
+      part[5] = d * (static_cast<double>(s) - static_cast<double>(t.s_old[j]));
+    }
+    if (EXACT) {
+      t.terms[idx] = part[0];
+      t.terms[mn + idx] = part[4];
+      t.terms[2 * mn + idx] = part[5];
+    }
+  }
+  if (!EXACT) {
+    block_sum<double, 6>(part, shD);
+    if (threadIdx.x == 0)
+      for (int k = 0; k < 6; ++k) t.dscratch[blockIdx.x * 6 + k] = part[k];
+  }
+  if (!last_block(&bk->ticket_update)) return;
+
+  __shared__ double tot[6];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (EXACT) {
+    // one serial chain per quantity, in the reference's loop order
+    // (solver.hpp:450-465 and :479-486)
+    if (lane == 0 && warp < 6) {
+      double acc = 0;
+      const double* d = t.terms + mn;
+      switch (warp) {
+        case 0:
+          for (int64_t k = 0; k < mn; ++k) acc += t.terms[k];
+          break;
+        case 1:
+          if (fp) for (int64_t k = 0; k < t.m; ++k) acc += d[k] * d[k];
+          break;
+        case 2:
+          if (fp) for (int64_t k = 0; k < t.m; ++k) acc += d[k];
+          break;
+        case 3:
+          if (fp) for (int64_t k = t.m; k < mn; ++k) acc += d[k] * d[k];
+          break;
+        case 4:
+          if (fp) for (int64_t k = t.m; k < mn; ++k) acc += d[k];
+          break;
+        default:
+          if (fp) for (int64_t k = 0; k < mn; ++k) acc += t.terms[2 * mn + k];
+      }
+      tot[warp] = acc;
+    }
+    __syncthreads();
+  } else {
+    double s6[6] = {0, 0, 0, 0, 0, 0};
+    for (int64_t k = tid; k < gridDim.x; k += blockDim.x)
+      for (int q = 0; q < 6; ++q) s6[q] += t.dscratch[k * 6 + q];
+    block_sum<double, 6>(s6, shD);
+    if (tid == 0)
+      for (int q = 0; q < 6; ++q) tot[q] = s6[q];
+    __syncthreads();
+  }
+  if (tid != 0) return;
+  bk->ticket_update = 0u;
+  bk->alpha = bk->alpha - bk->beta;  // solver.hpp:289
+  const int64_t k = bk->iter;
+  bk->iter = k + 1;
+
+  // fixed-point residual via the rank-two identity (solver.hpp:443-472)
+  double fp_residual = __longlong_as_double(0x7ff8000000000000ULL);
+  if (fp) {
+    double fp_sq = static_cast<double>(t.n_global) * tot[1] +
+                   static_cast<double>(t.m_global) * tot[3] +
+                   2.0 * tot[2] * tot[4];
+    if (t.reads_cost && t.want_dx) fp_sq += static_cast<double>(bk->pass_dx) + 2.0 * tot[5];
+    fp_residual = sqrt(fmax(fp_sq, 0.0));
+  }
+  bk->fp_residual = fp_residual;
+  // gated quantities (solver.hpp:474-490)
+  const double r_primal = sqrt(static_cast<double>(bk->nr2) + static_cast<double>(bk->ns2));
+  const double dual_value = tot[0];
+  const double gap = fabs(bk->last_cost - dual_value);
+  const double gap_scale = bk->relative ? 1.0 / (1.0 + fabs(bk->last_cost)) : 1.0;
+  bk->r_primal = r_primal;
+  bk->dual_value = dual_value;
+  bk->gap = gap;
+  const bool check = ((k + 1) % bk->check_every) == 0;
+  const bool trace_row = bk->record_trace && ((k + 1) % bk->trace_every) == 0;
+  if (trace_row) {
+    if (bk->trace_rows < bk->trace_cap) {
+      TraceRowDev& row = t.trace[bk->trace_rows];
+      row.iter = k + 1;
+      row.r_primal = r_primal;
+      row.r_dual = bk->last_r_dual;
+      row.gap = gap;
+      row.objective = bk->last_cost;
+      row.ergodic_objective = bk->erg_mean;
+      row.fixed_point_residual = fp_residual;
+    }
+    bk->trace_rows += 1;
+  }
+  if (check && r_primal * bk->primal_scale <= bk->tol_primal &&
+      bk->last_r_dual <= bk->tol_dual && gap * gap_scale <= bk->tol_gap) {
+    bk->confirm = 1;
+    bk->gate_hits += 1;
+  } else if (k + 1 >= bk->max_iters) {
+    bk->stop = 1;
+  }
+}
+
+template <class T>
+void launch_update(const TailArgs<T>& t, bool exact, cudaStream_t st) {
+  const unsigned blocks =
+      static_cast<unsigned>((t.m + t.n + kTailThreads - 1) / kTailThreads);
+  if (exact)
+    update_kernel<T, true><<<blocks, kTailThreads, 0, st>>>(t);
+  else
+    update_kernel<T, false><<<blocks, kTailThreads, 0, st>>>(t);
+  count_launch();
+}
+
+// ---------------------------------------------------------------------------
+// K5: exact matched-pair report (detail::state_report) + confirm
+// ---------------------------------------------------------------------------
+template <class T>
+__device__ __forceinline__ void report_elem(T xv, T cv, T phi_i, double nu_j,
+                                            double drho, T rho, bool folded,
+                                            double& obj, double& dsq) {
+  const double c = static_cast<double>(cv);
+  double x = static_cast<double>(xv);
+  if (folded) {
+    x += static_cast<double>(rho) * c;
+    if (x < 0) x = 0;
+  }
+  obj += c * x;
+  const double slack = static_cast<double>(phi_i) / drho + nu_j - c;
+  if (slack > 0) dsq += slack * slack;
+}
+
+template <class T, bool EXACT>
+__global__ void __launch_bounds__(kTailThreads)
+    report_kernel(const T* __restrict__ xy, const T* __restrict__ cost,
+                  const TailArgs<T> t, int always) {
+  Book<T>* bk = t.book;
+  if (!always) {
+    if (*reinterpret_cast<volatile int*>(&bk->stop) ||
+        !*reinterpret_cast<volatile int*>(&bk->confirm))
+      return;
+  }
+  __shared__ double shD[2 * 32];
+  const bool folded = bk->folded != 0;
+  const double drho = static_cast<double>(t.rho);
+  double part[2] = {0, 0};
+  if (EXACT) {
+    // single serial chain in storage order (solver.hpp:322-337)
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      for (int64_t j = 0; j < t.n; ++j) {
+        const double nu_j = static_cast<double>(t.varphi[j]) / drho;
+        const T* xc = xy + j * t.ld;
+        const T* cc = cost + j * t.ld;
+        for (int64_t i = 0; i < t.m; ++i)
+          report_elem<T>(xc[i], cc[i], t.phi[i], nu_j, drho, t.rho, folded,
+                         part[0], part[1]);
+      }
+    }
+  } else {
+    // blocks stride over columns, threads over rows
+    for (int64_t j = blockIdx.x; j < t.n; j += gridDim.x) {
+      const double nu_j = static_cast<double>(t.varphi[j]) / drho;
+      const T* xc = xy + j * t.ld;
+      const T* cc = cost + j * t.ld;
+      for (int64_t i = threadIdx.x; i < t.m; i += blockDim.x)
+        report_elem<T>(xc[i], cc[i], t.phi[i], nu_j, drho, t.rho, folded,
+                       part[0], part[1]);
+    }
+    block_sum<double, 2>(part, shD);
+  }
+  if (threadIdx.x == 0) {
+    t.dscratch[blockIdx.x * 2 + 0] = part[0];
+    t.dscratch[blockIdx.x * 2 + 1] = part[1];
+  }
+  if (!last_block(&bk->ticket_report)) return;
+  double s2[2] = {0, 0};
+  for (int64_t k = threadIdx.x; k < gridDim.x; k += blockDim.x) {
+    s2[0] += t.dscratch[k * 2 + 0];
+    s2[1] += t.dscratch[k * 2 + 1];
+  }
+  block_sum<double, 2>(s2, shD);
+  if (threadIdx.x != 0) return;
+  bk->ticket_report = 0u;
+  const double obj = s2[0];
+  const double r_primal =
+      sqrt(static_cast<double>(bk->nr2) + static_cast<double>(bk->ns2));
+  const double r_dual = sqrt(s2[1]);
+  const double gap = fabs(obj - bk->dual_value);
+  bk->rep_objective = obj;
+  bk->rep_r_primal = r_primal;
+  bk->rep_r_dual = r_dual;
+  bk->rep_gap = gap;
+  if (always) return;
+  const double egs = bk->relative ? 1.0 / (1.0 + fabs(obj)) : 1.0;
+  if (r_primal * bk->primal_scale <= bk->tol_primal && r_dual <= bk->tol_dual &&
+      gap * egs <= bk->tol_gap) {
+    bk->converged = 1;
+    bk->stop = 1;
+  } else {
+    bk->confirm = 0;
+    if (bk->iter >= bk->max_iters) bk->stop = 1;
+  }
+}
+
+template <class T>
+void launch_report(const T* xy, const T* cost, const TailArgs<T>& t,
+                   bool exact, bool always, cudaStream_t st) {
+  if (exact) {
+    report_kernel<T, true><<<1, kTailThreads, 0, st>>>(xy, cost, t, always ? 1 : 0);
+  } else {
+    const int64_t blocks = imin64(t.n, 148 * 8);
+    report_kernel<T, false>
+        <<<static_cast<unsigned>(blocks), kTailThreads, 0, st>>>(xy, cost, t,
+                                                                 always ? 1 : 0);
+  }
+  count_launch();
+}
+
+// ---------------------------------------------------------------------------
+// K4: init_state
+// ---------------------------------------------------------------------------
+template <class T>
+__global__ void init_x0_kernel(T* xy, const T* p, const T* q, int64_t m,
+                               int64_t n, int64_t ld) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= ld) return;
+  const T pi = i < m ? p[i] : T(0);
+  for (int64_t j = blockIdx.y; j < n; j += gridDim.y)
+    xy[j * ld + i] = i < m ? pi * q[j] : T(0);  // solver.hpp:165
+}
+
+template <class T>
+void launch_init_x0(T* xy, const T* p, const T* q, int64_t m, int64_t n,
+                    int64_t ld, cudaStream_t st) {
+  dim3 grid(static_cast<unsigned>((ld + 255) / 256),
+            static_cast<unsigned>(imin64(n, 1024)));
+  init_x0_kernel<T><<<grid, 256, 0, st>>>(xy, p, q, m, n, ld);
+  count_launch();
+}
+
+// a = row_sums(X0) - p (untiled, sequential over columns, matrix.hpp:128-136)
+template <class T>
+__global__ void init_rows_kernel(const T* xy, const T* p, T* a, int64_t m,
+                                 int64_t n, int64_t ld) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  T acc = T(0);
+  for (int64_t j = 0; j < n; ++j) acc += xy[j * ld + i];
+  a[i] = acc - p[i];
+}
+
+// b = col_sums(X0) - q (sequential over rows, matrix.hpp:139-149)
+template <class T>
+__global__ void init_cols_kernel(const T* xy, const T* q, T* b, int64_t m,
+                                 int64_t n, int64_t ld) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const T* c = xy + j * ld;
+  T acc = T(0);
+  for (int64_t i = 0; i < m; ++i) acc += c[i];
+  b[j] = acc - q[j];
+}
+
+template <class T>
+__global__ void init_alpha_kernel(const T* a, const T* b, int64_t m, int64_t n,
+                                  int64_t mn_global, Book<T>* bk) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const T alpha = serial_sum<T, false>(a, m) / static_cast<T>(mn_global);
+  bk->alpha = alpha;  // solver.hpp:177-178
+  bk->beta = alpha;   // solver.hpp:183
+  bk->nr2 = serial_sum<T, true>(a, m);  // r = a, s = b (solver.hpp:181-182)
+  bk->ns2 = serial_sum<T, true>(b, n);
+}
+
+template <class T>
+void launch_init_sums(const T* xy, const T* p, const T* q, T* a, T* b,
+                      int64_t m, int64_t n, int64_t ld, Book<T>* book,
+                      cudaStream_t st) {
+  init_rows_kernel<T><<<static_cast<unsigned>((m + 127) / 128), 128, 0, st>>>(
+      xy, p, a, m, n, ld);
+  init_cols_kernel<T><<<static_cast<unsigned>((n + 127) / 128), 128, 0, st>>>(
+      xy, q, b, m, n, ld);
+  init_alpha_kernel<T><<<1, 32, 0, st>>>(a, b, m, n, m + n, book);
+  count_launch(3);
+}
+
+// ---------------------------------------------------------------------------
+// K0: check_problem's matrix scan: first non-finite / first negative entry
+// in reference flat order (problem.hpp:129-133; also init_state's x0 check)
+// ---------------------------------------------------------------------------
+template <class T>
+__global__ void validate_kernel(const T* buf, int64_t m, int64_t n, int64_t ld,
+                                unsigned long long* first_nonfinite,
+                                unsigned long long* first_negative) {
+  for (int64_t j = blockIdx.y; j < n; j += gridDim.y) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= m) continue;
+    const T v = buf[j * ld + i];
+    const unsigned long long flat = static_cast<unsigned long long>(j * m + i);
+    if (!(fabs(v) <= max_finite<T>())) atomicMin(first_nonfinite, flat);
+    else if (v < T(0)) atomicMin(first_negative, flat);
+  }
+}
+
+template <class T>
+void launch_validate(const T* buf, int64_t m, int64_t n, int64_t ld,
+                     unsigned long long* first_nonfinite,
+                     unsigned long long* first_negative, cudaStream_t st) {
+  dim3 grid(static_cast<unsigned>((m + 255) / 256),
+            static_cast<unsigned>(imin64(n, 2048)));
+  validate_kernel<T><<<grid, 256, 0, st>>>(buf, m, n, ld, first_nonfinite,
+                                           first_negative);
+  count_launch();
+}
+
+// ---------------------------------------------------------------------------
+// K6: materialize_plan (solver.hpp:204-217); out is a dense m x n array
+// ---------------------------------------------------------------------------
+template <class T>
+__global__ void materialize_kernel(const T* xy, const T* cost, T* out, T rho,
+                                   int folded, int64_t m, int64_t n,
+                                   int64_t ld) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  for (int64_t j = blockIdx.y; j < n; j += gridDim.y) {
+    const T x = xy[j * ld + i];
+    if (folded) {
+      const T v = x + rho * cost[j * ld + i];
+      out[j * ld + i] = v > T(0) ? v : T(0);
+    } else {
+      out[j * ld + i] = x;
+    }
+  }
+}
+
+template <class T>
+void launch_materialize(const T* xy, const T* cost, T* out, T rho, int folded,
+                        int64_t m, int64_t n, int64_t ld, cudaStream_t st) {
+  dim3 grid(static_cast<unsigned>((m + 255) / 256),
+            static_cast<unsigned>(imin64(n, 2048)));
+  materialize_kernel<T><<<grid, 256, 0, st>>>(xy, cost, out, rho, folded, m, n, ld);
+  count_launch();
+}
+
+// ---- explicit instantiations ----------------------------------------------
+#define DROTB_INST(T)                                                          \
+  template void launch_pass<T>(const PassArgs<T>&, int, bool, bool,            \
+                               cudaStream_t);                                  \
+  template void launch_tile_chains<T>(const PassArgs<T>&, int, bool, bool,     \
+                                      int64_t, PassPartial<T>*, cudaStream_t); \
+  template void launch_merge<T>(const TailArgs<T>&, bool, cudaStream_t);       \
+  template void launch_update<T>(const TailArgs<T>&, bool, cudaStream_t);      \
+  template void launch_report<T>(const T*, const T*, const TailArgs<T>&, bool, \
+                                 bool, cudaStream_t);                          \
+  template void launch_init_x0<T>(T*, const T*, const T*, int64_t, int64_t,    \
+                                  int64_t, cudaStream_t);                      \
+  template void launch_init_sums<T>(const T*, const T*, const T*, T*, T*,      \
+                                    int64_t, int64_t, int64_t, Book<T>*,       \
+                                    cudaStream_t);                             \
+  template void launch_validate<T>(const T*, int64_t, int64_t, int64_t,        \
+                                   unsigned long long*, unsigned long long*,   \
+                                   cudaStream_t);                              \
+  template void launch_materialize<T>(const T*, const T*, T*, T, int, int64_t, \
+                                      int64_t, int64_t, cudaStream_t);
+DROTB_INST(float)
+DROTB_INST(double)
+
+}  // namespace drotb

@@ -1,0 +1,1219 @@
+// session.cu -- host driver of the B200 DROT solver and the C ABI of
+// libdrotb200.so (include/drotb.h).
+//
+// The driver owns the device-resident DrotState (solver.hpp:98-114) and runs
+// the solve loop of drot::solve<T> (solver.hpp:372-540) as a fixed sequence
+// of kernels per iteration, captured as CUDA graphs (one graph = one
+// even/odd iteration pair, which fixes the pass modes and the r/s
+// ping-pong buffers).  All per-iteration decisions (recursions, ergodic
+// mean, gate, exact confirm, max_iters) are taken on the device; the host
+// only polls a stop flag once per batch of graphs, one batch behind.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "drotb_host.hpp"
+#include "drotb_internal.hpp"
+
+namespace drotb {
+
+// ---------------------------------------------------------------------------
+// errors (errors.hpp:48-88)
+// ---------------------------------------------------------------------------
+namespace {
+thread_local std::string g_err;
+const char* const kErrcNames[] = {
+    "negative_cost",  "marginal_not_simplex", "empty_dimension",
+    "non_finite_entry", "shape_mismatch",     "non_positive_rho",
+    "invalid_initial_plan", "non_finite_iterate", "zero_marginal",
+    "too_large",      "degenerate_cost",      "dimension_mismatch",
+    "fold_state_mismatch", "bad_magic",       "version_unsupported",
+    "size_mismatch",  "ragged_csv",           "empty_image",
+    "k_too_large",    "io_error",             "bad_config"};
+}  // namespace
+
+const char* errc_name(int errc) {
+  if (errc < 0 || errc >= static_cast<int>(sizeof(kErrcNames) / sizeof(kErrcNames[0])))
+    return "unknown";
+  return kErrcNames[errc];
+}
+int set_error(int errc, const std::string& what) {
+  g_err = std::string(errc_name(errc)) + ": " + what;
+  return 1 + errc;
+}
+int set_cuda_error(int code, const std::string& what) {
+  g_err = what;
+  return code;
+}
+void clear_error() { g_err.clear(); }
+const char* last_error_cstr() { return g_err.c_str(); }
+
+#define CUDA_TRY(expr)                                                       \
+  do {                                                                       \
+    cudaError_t e_ = (expr);                                                 \
+    if (e_ != cudaSuccess)                                                   \
+      return ::drotb::set_cuda_error(DROTB_ERR_CUDA + static_cast<int>(e_),  \
+                            std::string("cuda: ") + #expr + ": " +           \
+                                cudaGetErrorString(e_));                     \
+  } while (0)
+
+#define RC_TRY(expr)          \
+  do {                        \
+    int rc_ = (expr);         \
+    if (rc_) return rc_;      \
+  } while (0)
+
+template <class P>
+static int dev_alloc(P** ptr, size_t count) {
+  *ptr = nullptr;
+  if (count == 0) count = 1;
+  CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(ptr), count * sizeof(P)));
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Session<T>
+// ---------------------------------------------------------------------------
+template <class T>
+struct Session {
+  int64_t m = 0, n = 0, ld = 0, m_global = 0, n_global = 0, row_begin = 0;
+  drotb_config cfg{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+
+  T *X = nullptr, *C = nullptr, *Xout = nullptr;
+  T *phi = nullptr, *varphi = nullptr, *a = nullptr, *b = nullptr;
+  T *rb[2] = {nullptr, nullptr}, *sb[2] = {nullptr, nullptr};
+  T *p = nullptr, *q = nullptr, *u = nullptr, *v = nullptr;
+  T *ustrip = nullptr, *vstrip = nullptr, *tscr = nullptr;
+  PassPartial<T>* partials = nullptr;
+  PassPartial<T>* tiles = nullptr;
+  double *dscr = nullptr, *terms = nullptr;
+  Book<T>* book = nullptr;
+  TraceRowDev* trace = nullptr;
+  unsigned long long* vflags = nullptr;
+  int32_t* h_stop = nullptr;  // pinned, 2 slots
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+
+  std::vector<T> hp, hq;
+  T rho = T(0);
+  double rho_d = 0;
+  int64_t bs = 64, tc = 256, grid_cols = 0, grid_rows64 = 0, n_partials = 0;
+  int64_t tile_grid_rows = 0, n_tiles = 0, tail_blocks = 0, report_blocks = 0;
+  int64_t trace_cap = 0;
+  bool exact = false, have_problem = false, initialized = false;
+  bool want_dual = true, want_dx = true, gate = true;
+  int64_t h_iter = 0;
+  bool h_folded = false;
+  cudaGraphExec_t pair_exec = nullptr;
+  int64_t launches_per_pair = 0;
+
+  ~Session() { release(); }
+
+  void release() {
+    if (pair_exec) cudaGraphExecDestroy(pair_exec);
+    pair_exec = nullptr;
+    void* bufs[] = {X, C, Xout, phi, varphi, a, b, rb[0], rb[1], sb[0], sb[1],
+                    p, q, u, v, ustrip, vstrip, tscr, partials, tiles, dscr,
+                    terms, book, trace, vflags};
+    for (void* ptr : bufs)
+      if (ptr) cudaFree(ptr);
+    X = C = Xout = phi = varphi = a = b = p = q = u = v = ustrip = vstrip =
+        tscr = nullptr;
+    rb[0] = rb[1] = sb[0] = sb[1] = nullptr;
+    partials = tiles = nullptr;
+    dscr = terms = nullptr;
+    book = nullptr;
+    trace = nullptr;
+    vflags = nullptr;
+    if (h_stop) cudaFreeHost(h_stop);
+    h_stop = nullptr;
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    ev[0] = ev[1] = nullptr;
+    if (own_stream && stream) cudaStreamDestroy(stream);
+    stream = nullptr;
+    own_stream = false;
+  }
+
+  int create(int64_t m_, int64_t n_, const drotb_config& c) {
+    if (m_ <= 0 || n_ <= 0)
+      return set_error(DROTB_ERRC_EMPTY_DIMENSION, "cost matrix has an empty dimension");
+    cfg = c;
+    m = m_global = m_;
+    n = n_global = n_;
+    if (cfg.device >= 0) CUDA_TRY(cudaSetDevice(cfg.device));
+    CUDA_TRY(cudaGetDevice(&device));
+    CUDA_TRY(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    own_stream = true;
+    exact = cfg.order == DROTB_ORDER_REFERENCE;
+    bs = std::max<int64_t>(1, cfg.block_rows);
+    tc = bs * std::max<int64_t>(1, cfg.work_size);
+    return allocate();
+  }
+
+  int allocate() {
+    ld = round_up(m, 32);
+    constexpr int R = 16 / sizeof(T);
+    const int64_t rows_cta = int64_t(kWarpsPerCta) * 32 * R;
+    grid_cols = (n + tc - 1) / tc;
+    grid_rows64 = (m + kVBlockRows - 1) / kVBlockRows;
+    n_partials = ((m + rows_cta - 1) / rows_cta) * grid_cols;
+    tile_grid_rows = (m + bs - 1) / bs;
+    n_tiles = tile_grid_rows * grid_cols;
+    tail_blocks = (m + n + 255) / 256;
+    report_blocks = std::min<int64_t>(n, 148 * 8);
+    const size_t mat = static_cast<size_t>(ld) * static_cast<size_t>(n);
+    RC_TRY(dev_alloc(&X, mat));
+    RC_TRY(dev_alloc(&C, mat));
+    RC_TRY(dev_alloc(&phi, ld));
+    RC_TRY(dev_alloc(&a, ld));
+    RC_TRY(dev_alloc(&rb[0], ld));
+    RC_TRY(dev_alloc(&rb[1], ld));
+    RC_TRY(dev_alloc(&p, ld));
+    RC_TRY(dev_alloc(&u, ld));
+    RC_TRY(dev_alloc(&varphi, n));
+    RC_TRY(dev_alloc(&b, n));
+    RC_TRY(dev_alloc(&sb[0], n));
+    RC_TRY(dev_alloc(&sb[1], n));
+    RC_TRY(dev_alloc(&q, n));
+    RC_TRY(dev_alloc(&v, n));
+    RC_TRY(dev_alloc(&ustrip, static_cast<size_t>(grid_cols) * ld));
+    RC_TRY(dev_alloc(&vstrip, static_cast<size_t>(grid_rows64) * n));
+    RC_TRY(dev_alloc(&tscr, static_cast<size_t>(tail_blocks) * 3));
+    RC_TRY(dev_alloc(&partials, static_cast<size_t>(n_partials)));
+    if (exact) {
+      RC_TRY(dev_alloc(&tiles, static_cast<size_t>(n_tiles)));
+      RC_TRY(dev_alloc(&terms, static_cast<size_t>(m + n) * 3));
+    }
+    RC_TRY(dev_alloc(&dscr, static_cast<size_t>(std::max(tail_blocks * 6, report_blocks * 2))));
+    RC_TRY(dev_alloc(&book, 1));
+    RC_TRY(dev_alloc(&vflags, 2));
+    CUDA_TRY(cudaMemsetAsync(book, 0, sizeof(Book<T>), stream));
+    CUDA_TRY(cudaMemsetAsync(phi, 0, sizeof(T) * ld, stream));
+    CUDA_TRY(cudaMemsetAsync(p, 0, sizeof(T) * ld, stream));
+    CUDA_TRY(cudaMemsetAsync(u, 0, sizeof(T) * ld, stream));
+    CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&h_stop), 2 * sizeof(int32_t)));
+    CUDA_TRY(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    return 0;
+  }
+
+  int set_stream(void* s) {
+    if (pair_exec) cudaGraphExecDestroy(pair_exec);
+    pair_exec = nullptr;
+    if (own_stream && stream) {
+      CUDA_TRY(cudaStreamSynchronize(stream));
+      cudaStreamDestroy(stream);
+    }
+    if (s) {
+      stream = static_cast<cudaStream_t>(s);
+      own_stream = false;
+    } else {
+      CUDA_TRY(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+      own_stream = true;
+    }
+    return 0;
+  }
+
+  // Upload a dense column-major m x n host/device array into an ld-pitched
+  // device array (pad rows zeroed).
+  int upload_matrix(T* dst, const T* src, bool is_device) {
+    CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(T) * static_cast<size_t>(ld) * n, stream));
+    CUDA_TRY(cudaMemcpy2DAsync(dst, sizeof(T) * ld, src, sizeof(T) * m,
+                               sizeof(T) * m, n,
+                               is_device ? cudaMemcpyDeviceToDevice
+                                         : cudaMemcpyHostToDevice,
+                               stream));
+    return 0;
+  }
+
+  int download_matrix(T* dst, const T* src) {
+    CUDA_TRY(cudaMemcpy2DAsync(dst, sizeof(T) * m, src, sizeof(T) * ld,
+                               sizeof(T) * m, n, cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    return 0;
+  }
+
+  // first_nonfinite / first_negative flat indices of an uploaded matrix
+  int scan_matrix(const T* buf, unsigned long long* nf, unsigned long long* ng) {
+    const unsigned long long init[2] = {~0ull, ~0ull};
+    CUDA_TRY(cudaMemcpyAsync(vflags, init, sizeof(init), cudaMemcpyHostToDevice, stream));
+    launch_validate<T>(buf, m, n, ld, vflags, vflags + 1, stream);
+    CUDA_TRY(cudaGetLastError());
+    unsigned long long res[2];
+    CUDA_TRY(cudaMemcpyAsync(res, vflags, sizeof(res), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    *nf = res[0];
+    *ng = res[1];
+    return 0;
+  }
+
+  // check_marginal (problem.hpp:103-117), host: sequential double sum
+  static int check_marginal(const std::vector<T>& vv, const char* name) {
+    if (vv.empty()) return set_error(DROTB_ERRC_EMPTY_DIMENSION, std::string(name) + " is empty");
+    double sum = 0;
+    for (T e : vv) {
+      if (!std::isfinite(static_cast<double>(e)))
+        return set_error(DROTB_ERRC_NON_FINITE_ENTRY, std::string(name) + " has a non-finite entry");
+      if (e < T(0))
+        return set_error(DROTB_ERRC_MARGINAL_NOT_SIMPLEX, std::string(name) + " has a negative entry");
+      sum += static_cast<double>(e);
+    }
+    if (std::abs(sum - 1.0) > 1e-12)
+      return set_error(DROTB_ERRC_MARGINAL_NOT_SIMPLEX,
+                       std::string(name) + " sums to " + std::to_string(sum));
+    return 0;
+  }
+
+  // set_problem + check_problem (problem.hpp:122-136)
+  int set_problem(const T* C_, const T* p_, const T* q_, bool is_device,
+                  bool validate) {
+    RC_TRY(upload_matrix(C, C_, is_device));
+    hp.assign(static_cast<size_t>(m), T(0));
+    hq.assign(static_cast<size_t>(n), T(0));
+    const cudaMemcpyKind k = is_device ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost;
+    CUDA_TRY(cudaMemcpyAsync(hp.data(), p_, sizeof(T) * m, k, stream));
+    CUDA_TRY(cudaMemcpyAsync(hq.data(), q_, sizeof(T) * n, k, stream));
+    CUDA_TRY(cudaMemcpyAsync(p, hp.data(), sizeof(T) * m, cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaMemcpyAsync(q, hq.data(), sizeof(T) * n, cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    have_problem = true;
+    initialized = false;
+    if (!validate) return 0;
+    unsigned long long nf, ng;
+    RC_TRY(scan_matrix(C, &nf, &ng));
+    if (nf != ~0ull || ng != ~0ull) {
+      if (nf < ng)
+        return set_error(DROTB_ERRC_NON_FINITE_ENTRY, "cost matrix has a non-finite entry");
+      return set_error(DROTB_ERRC_NEGATIVE_COST, "cost matrix has a negative entry");
+    }
+    RC_TRY(check_marginal(hp, "p"));
+    RC_TRY(check_marginal(hq, "q"));
+    return 0;
+  }
+
+  int resolve_rho() {  // DrotConfig::resolved_rho, solver.hpp:77-83
+    const double r = cfg.has_rho_override
+                         ? cfg.rho_override
+                         : cfg.rho0 / static_cast<double>(m_global + n_global);
+    if (!(r > 0) || !std::isfinite(r))
+      return set_error(DROTB_ERRC_NON_POSITIVE_RHO, "resolved rho must be positive");
+    rho_d = r;
+    rho = static_cast<T>(r);
+    return 0;
+  }
+
+  static T host_norm_sq(const std::vector<T>& x) {  // vec_norm_sq
+    T acc = T(0);
+    for (T e : x) acc += e * e;
+    return acc;
+  }
+
+  // init_state (solver.hpp:143-186) + solve-loop bookkeeping reset
+  // (solver.hpp:387-404).
+  int init(const T* x0, bool x0_is_device = false) {
+    if (!have_problem) return set_error(DROTB_ERRC_BAD_CONFIG, "no problem set");
+    RC_TRY(resolve_rho());
+    if (x0) {
+      RC_TRY(upload_matrix(X, x0, x0_is_device));
+      unsigned long long nf, ng;
+      RC_TRY(scan_matrix(X, &nf, &ng));
+      if (nf != ~0ull || ng != ~0ull)
+        return set_error(DROTB_ERRC_INVALID_INITIAL_PLAN,
+                         "initial plan must be nonnegative and finite");
+    } else {
+      launch_init_x0<T>(X, p, q, m, n, ld, stream);
+    }
+    CUDA_TRY(cudaMemsetAsync(phi, 0, sizeof(T) * ld, stream));
+    CUDA_TRY(cudaMemsetAsync(varphi, 0, sizeof(T) * n, stream));
+    CUDA_TRY(cudaMemsetAsync(a, 0, sizeof(T) * ld, stream));
+    CUDA_TRY(cudaMemsetAsync(rb[0], 0, sizeof(T) * ld, stream));
+    CUDA_TRY(cudaMemsetAsync(rb[1], 0, sizeof(T) * ld, stream));
+
+    // bookkeeping
+    if (cfg.record_trace) {
+      const int64_t te = std::max<int64_t>(1, cfg.trace_every);
+      trace_cap = std::min<int64_t>(std::max<int64_t>(cfg.max_iters, 0) / te + 1, int64_t(1) << 23);
+      if (trace) cudaFree(trace);
+      RC_TRY(dev_alloc(&trace, static_cast<size_t>(trace_cap)));
+    } else {
+      trace_cap = 0;
+    }
+    Book<T> hb;
+    std::memset(&hb, 0, sizeof(hb));
+    hb.last_cost = std::numeric_limits<double>::quiet_NaN();
+    hb.last_r_dual = std::numeric_limits<double>::infinity();
+    hb.prev_pass_had_cost = 1;
+    hb.dual_value = 0.0;  // phi = varphi = 0
+    hb.max_iters = cfg.max_iters;
+    hb.check_every = std::max<int64_t>(1, cfg.check_every);
+    hb.trace_every = std::max<int64_t>(1, cfg.trace_every);
+    hb.trace_cap = trace_cap;
+    hb.tol_primal = cfg.tol_primal;
+    hb.tol_dual = cfg.tol_dual;
+    hb.tol_gap = cfg.tol_gap;
+    const double p_norm = std::sqrt(static_cast<double>(host_norm_sq(hp)));
+    const double q_norm = std::sqrt(static_cast<double>(host_norm_sq(hq)));
+    hb.primal_scale = cfg.relative_tolerances ? 1.0 / (1.0 + p_norm + q_norm) : 1.0;
+    hb.record_trace = cfg.record_trace ? 1 : 0;
+    hb.relative = cfg.relative_tolerances ? 1 : 0;
+    if (cfg.max_iters <= 0) hb.stop = 1;
+    CUDA_TRY(cudaMemcpyAsync(book, &hb, sizeof(hb), cudaMemcpyHostToDevice, stream));
+    launch_init_sums<T>(X, p, q, a, b, m, n, ld, book, stream);
+    CUDA_TRY(cudaMemcpyAsync(rb[0], a, sizeof(T) * ld, cudaMemcpyDeviceToDevice, stream));
+    CUDA_TRY(cudaMemcpyAsync(sb[0], b, sizeof(T) * n, cudaMemcpyDeviceToDevice, stream));
+    CUDA_TRY(cudaGetLastError());
+    want_dual = true;
+    want_dx = cfg.record_trace != 0;
+    gate = true;
+    h_iter = 0;
+    h_folded = false;
+    initialized = true;
+    return 0;
+  }
+
+  int pass_mode(int64_t k, bool folded, int* mode, bool* folded_after) const {
+    if (cfg.engine == DROTB_ENGINE_REFERENCE) {
+      if (folded) return set_error(DROTB_ERRC_FOLD_STATE_MISMATCH, "reference pass on a folded array");
+      *mode = (k & 1) ? kPlain1 : kPlain0;
+      *folded_after = false;
+    } else if (cfg.skip_cost) {
+      *mode = folded ? kSkip : kFold;
+      *folded_after = !folded;
+    } else {
+      *mode = (k & 1) ? kPlain1 : kPlain0;
+      *folded_after = folded;  // a plain pass on a folded array is not reachable
+    }
+    return 0;
+  }
+
+  PassArgs<T> pass_args() {
+    PassArgs<T> pa;
+    pa.xy = X;
+    pa.cost = C;
+    pa.phi = phi;
+    pa.varphi = varphi;
+    pa.rho = rho;
+    pa.m = m;
+    pa.n = n;
+    pa.ld = ld;
+    pa.row_begin = row_begin;
+    pa.tc = tc;
+    pa.ustrip = ustrip;
+    pa.vstrip = vstrip;
+    pa.partials = partials;
+    pa.stop = &book->stop;
+    return pa;
+  }
+
+  TailArgs<T> tail_args(int64_t k, int mode, bool folded_after, bool solver) {
+    TailArgs<T> t;
+    std::memset(&t, 0, sizeof(t));
+    t.m = m;
+    t.n = n;
+    t.ld = ld;
+    t.m_global = m_global;
+    t.n_global = n_global;
+    t.folded_after = folded_after ? 1 : 0;
+    t.grid_cols = grid_cols;
+    t.grid_rows64 = grid_rows64;
+    t.ustrip = ustrip;
+    t.vstrip = vstrip;
+    t.pass_partials = partials;
+    t.n_pass_partials = n_partials;
+    t.p = p;
+    t.q = q;
+    t.u = u;
+    t.v = v;
+    t.r_old = rb[k & 1];
+    t.r_new = rb[(k + 1) & 1];
+    t.s_old = sb[k & 1];
+    t.s_new = sb[(k + 1) & 1];
+    t.phi = phi;
+    t.varphi = varphi;
+    t.a = a;
+    t.b = b;
+    t.rho = rho;
+    t.reads_cost = mode != kSkip;
+    t.want_dual = want_dual;
+    t.want_dx = want_dx;
+    t.solver = solver ? 1 : 0;
+    t.dscratch = dscr;
+    t.tscratch = tscr;
+    t.terms = terms;
+    t.book = book;
+    t.trace = trace;
+    t.tile_partials = tiles;
+    t.n_tiles = n_tiles;
+    return t;
+  }
+
+  // One solve-loop iteration: step_impl (solver.hpp:238-307) + the
+  // bookkeeping and gate of solve (solver.hpp:406-521).
+  int enqueue_iteration() {
+    const int64_t k = h_iter;
+    int mode;
+    bool folded_after;
+    RC_TRY(pass_mode(k, h_folded, &mode, &folded_after));
+    PassArgs<T> pa = pass_args();
+    if (exact) launch_tile_chains<T>(pa, mode, want_dual, want_dx, bs, tiles, stream);
+    launch_pass<T>(pa, mode, want_dual, want_dx, stream);
+    TailArgs<T> ta = tail_args(k, mode, folded_after, true);
+    launch_merge<T>(ta, exact, stream);
+    launch_update<T>(ta, exact, stream);
+    if (gate) launch_report<T>(X, C, ta, exact, false, stream);
+    h_iter = k + 1;
+    h_folded = folded_after;
+    return 0;
+  }
+
+  int capture_pair() {
+    if (pair_exec) return 0;
+    const int64_t save_iter = h_iter;
+    const bool save_folded = h_folded;
+    const int64_t before = kernel_launch_count();
+    cudaGraph_t graph = nullptr;
+    CUDA_TRY(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+    int rc = enqueue_iteration();
+    if (!rc) rc = enqueue_iteration();
+    cudaError_t e = cudaStreamEndCapture(stream, &graph);
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    CUDA_TRY(e);
+    CUDA_TRY(cudaGraphInstantiate(&pair_exec, graph, 0));
+    cudaGraphDestroy(graph);
+    launches_per_pair = kernel_launch_count() - before;
+    count_launch(-launches_per_pair);  // captured, not launched
+    h_iter = save_iter;
+    h_folded = save_folded;
+    return 0;
+  }
+
+  int enqueue(int64_t n_iters) {
+    if (!initialized) return set_error(DROTB_ERRC_BAD_CONFIG, "session not initialized");
+    while (n_iters > 0) {
+      if (cfg.use_graphs && n_iters >= 2 && (h_iter & 1) == 0 && !h_folded) {
+        RC_TRY(capture_pair());
+        CUDA_TRY(cudaGraphLaunch(pair_exec, stream));
+        count_launch(launches_per_pair);
+        h_iter += 2;
+        n_iters -= 2;
+      } else {
+        RC_TRY(enqueue_iteration());
+        n_iters -= 1;
+      }
+    }
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
+
+  int64_t batch_iters() const {
+    // ~1 ms of pass traffic per batch at ~6 TB/s, at least 8 iterations
+    const double bytes = 3.0 * sizeof(T) * static_cast<double>(m) * n;
+    const double t_iter = bytes / 6.0e12 + 20e-6;
+    int64_t bi = static_cast<int64_t>(1e-3 / t_iter) + 1;
+    bi = std::max<int64_t>(8, std::min<int64_t>(bi, 256));
+    return bi + (bi & 1);
+  }
+
+  // Runs the loop until the device raises its stop flag (converged,
+  // max_iters, numerical failure).  The host polls one batch behind so the
+  // GPU queue never drains.
+  int run() {
+    if (!initialized) return set_error(DROTB_ERRC_BAD_CONFIG, "session not initialized");
+    const int64_t bi = batch_iters();
+    int slot = 0;
+    bool pending = false;
+    const int64_t limit = std::max<int64_t>(cfg.max_iters, 0) + 4 * bi + 4;
+    while (true) {
+      RC_TRY(enqueue(bi));
+      CUDA_TRY(cudaMemcpyAsync(&h_stop[slot], &book->stop, sizeof(int32_t),
+                               cudaMemcpyDeviceToHost, stream));
+      CUDA_TRY(cudaEventRecord(ev[slot], stream));
+      if (pending) {
+        CUDA_TRY(cudaEventSynchronize(ev[slot ^ 1]));
+        if (h_stop[slot ^ 1]) break;
+      }
+      pending = true;
+      slot ^= 1;
+      if (h_iter > limit) break;  // the device sets stop at max_iters
+    }
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    return 0;
+  }
+
+  int read_book(Book<T>* hb) {
+    CUDA_TRY(cudaMemcpyAsync(hb, book, sizeof(Book<T>), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    return 0;
+  }
+
+  // Final status and report (solver.hpp:527-538).
+  int finish(int32_t* status, int64_t* iterations, drotb_report* rep) {
+    Book<T> hb;
+    RC_TRY(read_book(&hb));
+    int32_t st = DROTB_MAX_ITERS;
+    if (hb.converged) st = DROTB_CONVERGED;
+    if (hb.failed) st = DROTB_NUMERICAL_FAILURE;
+    if (st == DROTB_MAX_ITERS) {
+      TailArgs<T> ta = tail_args(hb.iter, kPlain0, hb.folded != 0, true);
+      launch_report<T>(X, C, ta, exact, true, stream);
+      CUDA_TRY(cudaGetLastError());
+      RC_TRY(read_book(&hb));
+    }
+    if (status) *status = st;
+    if (iterations) *iterations = hb.iterations;
+    if (rep) {
+      if (st == DROTB_NUMERICAL_FAILURE) {
+        const double nan = std::numeric_limits<double>::quiet_NaN();
+        rep->r_primal = rep->r_dual = rep->gap = rep->objective = nan;
+      } else {
+        rep->r_primal = hb.rep_r_primal;
+        rep->r_dual = hb.rep_r_dual;
+        rep->gap = hb.rep_gap;
+        rep->objective = hb.rep_objective;
+      }
+    }
+    return 0;
+  }
+
+  // materialize_plan + recover_duals (solver.hpp:188-217)
+  int get_plan(T* plan, T* mu, T* nu) {
+    Book<T> hb;
+    RC_TRY(read_book(&hb));
+    if (plan) {
+      if (!Xout) RC_TRY(dev_alloc(&Xout, static_cast<size_t>(ld) * n));
+      launch_materialize<T>(X, C, Xout, rho, hb.folded, m, n, ld, stream);
+      CUDA_TRY(cudaGetLastError());
+      RC_TRY(download_matrix(plan, Xout));
+    }
+    if (mu || nu) {
+      std::vector<T> hphi(static_cast<size_t>(m)), hvar(static_cast<size_t>(n));
+      CUDA_TRY(cudaMemcpyAsync(hphi.data(), phi, sizeof(T) * m, cudaMemcpyDeviceToHost, stream));
+      CUDA_TRY(cudaMemcpyAsync(hvar.data(), varphi, sizeof(T) * n, cudaMemcpyDeviceToHost, stream));
+      CUDA_TRY(cudaStreamSynchronize(stream));
+      if (mu)
+        for (int64_t i = 0; i < m; ++i) mu[i] = hphi[i] / rho;
+      if (nu)
+        for (int64_t j = 0; j < n; ++j) nu[j] = hvar[j] / rho;
+    }
+    return 0;
+  }
+
+  int get_trace(drotb_trace_row* out, int64_t cap, int64_t* len) {
+    Book<T> hb;
+    RC_TRY(read_book(&hb));
+    if (len) *len = hb.trace_rows;
+    if (out && cap > 0 && trace) {
+      const int64_t cnt = std::min<int64_t>({cap, hb.trace_rows, trace_cap});
+      static_assert(sizeof(TraceRowDev) == sizeof(drotb_trace_row), "trace row");
+      if (cnt > 0) {
+        CUDA_TRY(cudaMemcpyAsync(out, trace, sizeof(TraceRowDev) * cnt,
+                                 cudaMemcpyDeviceToHost, stream));
+        CUDA_TRY(cudaStreamSynchronize(stream));
+      }
+    }
+    return 0;
+  }
+
+  // ---- external-state single step (drot_step, solver.hpp:361-370) --------
+  int load_state(const T* xy, int32_t folded, const T* rs, const T* cs,
+                 const T* ya, const T* yb, T alpha, const T* r, const T* s,
+                 T beta, int64_t iter) {
+    RC_TRY(resolve_rho());
+    RC_TRY(upload_matrix(X, xy, false));
+    CUDA_TRY(cudaMemcpyAsync(phi, rs, sizeof(T) * m, cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaMemcpyAsync(varphi, cs, sizeof(T) * n, cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaMemcpyAsync(a, ya, sizeof(T) * m, cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaMemcpyAsync(b, yb, sizeof(T) * n, cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaMemcpyAsync(rb[iter & 1], r, sizeof(T) * m, cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaMemcpyAsync(sb[iter & 1], s, sizeof(T) * n, cudaMemcpyHostToDevice, stream));
+    Book<T> hb;
+    std::memset(&hb, 0, sizeof(hb));
+    hb.alpha = alpha;
+    hb.beta = beta;
+    hb.iter = iter;
+    hb.folded = folded;
+    hb.last_cost = std::numeric_limits<double>::quiet_NaN();
+    hb.last_r_dual = std::numeric_limits<double>::infinity();
+    hb.prev_pass_had_cost = 1;
+    hb.max_iters = std::numeric_limits<int64_t>::max();
+    hb.check_every = 1;
+    hb.trace_every = 1;
+    hb.tol_primal = hb.tol_dual = hb.tol_gap = -1.0;
+    CUDA_TRY(cudaMemcpyAsync(book, &hb, sizeof(hb), cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    want_dual = false;  // default PassOptions (solver.hpp:367)
+    want_dx = false;
+    gate = false;
+    h_iter = iter;
+    h_folded = folded != 0;
+    initialized = true;
+    return 0;
+  }
+
+  int store_state(T* xy, int32_t* folded, T* rs, T* cs, T* ya, T* yb, T* alpha,
+                  T* r, T* s, T* beta, int64_t* iter, bool full) {
+    Book<T> hb;
+    RC_TRY(read_book(&hb));
+    RC_TRY(download_matrix(xy, X));
+    *folded = hb.folded;
+    if (!full) return 0;
+    CUDA_TRY(cudaMemcpyAsync(rs, phi, sizeof(T) * m, cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaMemcpyAsync(cs, varphi, sizeof(T) * n, cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaMemcpyAsync(ya, a, sizeof(T) * m, cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaMemcpyAsync(yb, b, sizeof(T) * n, cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaMemcpyAsync(r, rb[hb.iter & 1], sizeof(T) * m, cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaMemcpyAsync(s, sb[hb.iter & 1], sizeof(T) * n, cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    *alpha = hb.alpha;
+    *beta = hb.beta;
+    *iter = hb.iter;
+    return 0;
+  }
+
+  // ---- engine pass (FusedEngine<T>, fused.hpp:127-165) -------------------
+  int engine_pass(T* xy, const T* cost, const T* rs, const T* cs, T rho_,
+                  int mode, bool dual, bool dx, bool deterministic, T* row_sums,
+                  T* col_sums, drotb_pass_out* out) {
+    RC_TRY(upload_matrix(X, xy, false));
+    RC_TRY(upload_matrix(C, cost, false));
+    CUDA_TRY(cudaMemcpyAsync(phi, rs, sizeof(T) * m, cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaMemcpyAsync(varphi, cs, sizeof(T) * n, cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaMemsetAsync(book, 0, sizeof(Book<T>), stream));
+    rho = rho_;
+    const bool ex = deterministic;
+    if (ex && !tiles) RC_TRY(dev_alloc(&tiles, static_cast<size_t>(n_tiles)));
+    PassArgs<T> pa = pass_args();
+    pa.stop = nullptr;
+    const bool rc = mode != kSkip;
+    if (ex) launch_tile_chains<T>(pa, mode, dual && rc, dx && rc, bs, tiles, stream);
+    launch_pass<T>(pa, mode, dual && rc, dx && rc, stream);
+    TailArgs<T> ta = tail_args(0, mode, false, false);
+    ta.want_dual = dual;
+    ta.want_dx = dx;
+    ta.tile_partials = tiles;
+    launch_merge<T>(ta, ex, stream);
+    CUDA_TRY(cudaGetLastError());
+    RC_TRY(download_matrix(xy, X));
+    Book<T> hb;
+    RC_TRY(read_book(&hb));
+    if (row_sums) CUDA_TRY(cudaMemcpy(row_sums, u, sizeof(T) * m, cudaMemcpyDeviceToHost));
+    if (col_sums) CUDA_TRY(cudaMemcpy(col_sums, v, sizeof(T) * n, cudaMemcpyDeviceToHost));
+    if (out) {
+      out->cost_dot = rc ? static_cast<double>(hb.pass_cost) : 0.0;
+      out->prev_cost_dot = rc ? static_cast<double>(hb.pass_prev) : 0.0;
+      out->dual_sq = (rc && dual) ? static_cast<double>(hb.pass_dual) : 0.0;
+      out->dx_sq = (rc && dx) ? static_cast<double>(hb.pass_dx) : 0.0;
+      out->max_abs = static_cast<double>(hb.pass_max_abs);
+      out->nonfinite = hb.pass_bad ? 1 : 0;
+      out->cost_valid = rc;
+      out->prev_cost_valid = rc;
+      out->dual_valid = rc && dual;
+      out->dx_valid = rc && dx;
+      out->pad_ = 0;
+    }
+    return 0;
+  }
+};
+
+template <class T>
+static Session<T>* as_session(void* s) {
+  return static_cast<Session<T>*>(s);
+}
+
+}  // namespace drotb
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+using drotb::Session;
+
+struct drotb_session {
+  int32_t precision;
+  void* impl;
+};
+struct drotb_engine {
+  int32_t precision;
+  void* impl;
+};
+
+namespace {
+
+int guard_exceptions(const std::exception& e) {
+  return drotb::set_cuda_error(DROTB_ERR_CUDA, std::string("exception: ") + e.what());
+}
+
+drotb_config effective(const drotb_config* cfg) {
+  drotb_config c;
+  drotb_config_default(&c);
+  if (cfg) c = *cfg;
+  return c;
+}
+
+template <class T>
+int solve_t(const T* C, int64_t m, int64_t n, const T* p, const T* q,
+            const drotb_config* cfgp, const T* x0, T* plan, T* mu, T* nu,
+            T* rho_out, drotb_report* rep, drotb_trace_row* trace,
+            int64_t trace_cap, int64_t* trace_len, int64_t* iters,
+            int32_t* status, double* wall) {
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
+  drotb::clear_error();
+  const drotb_config cfg = effective(cfgp);
+  try {
+    std::unique_ptr<Session<T>> s(new Session<T>());
+    RC_TRY(s->create(m, n, cfg));
+    RC_TRY(s->set_problem(C, p, q, false, true));
+    RC_TRY(s->init(x0));
+    RC_TRY(s->run());
+    const auto t1 = clk::now();
+    RC_TRY(s->finish(status, iters, rep));
+    RC_TRY(s->get_plan(plan, mu, nu));
+    RC_TRY(s->get_trace(trace, trace_cap, trace_len));
+    if (rho_out) *rho_out = s->rho;
+    if (wall) *wall = std::chrono::duration<double>(t1 - t0).count();
+    return 0;
+  } catch (const std::exception& e) {
+    return guard_exceptions(e);
+  }
+}
+
+template <class T>
+int step_t(T* xy, int32_t* folded, T* rs, T* cs, T* ya, T* yb, T* alpha, T* r,
+           T* s, T* beta, int64_t* iter, const T* C, int64_t m, int64_t n,
+           const T* p, const T* q, const drotb_config* cfgp) {
+  drotb::clear_error();
+  const drotb_config cfg = effective(cfgp);
+  try {
+    std::unique_ptr<Session<T>> ss(new Session<T>());
+    RC_TRY(ss->create(m, n, cfg));
+    RC_TRY(ss->set_problem(C, p, q, false, false));
+    RC_TRY(ss->load_state(xy, *folded, rs, cs, ya, yb, *alpha, r, s, *beta, *iter));
+    RC_TRY(ss->enqueue_iteration());
+    CUDA_TRY(cudaGetLastError());
+    drotb::Book<T> hb;
+    RC_TRY(ss->read_book(&hb));
+    if (hb.pass_bad) {
+      RC_TRY(ss->store_state(xy, folded, rs, cs, ya, yb, alpha, r, s, beta, iter, false));
+      return drotb::set_error(DROTB_ERRC_NON_FINITE_ITERATE,
+                              "non-finite value in iterate update");
+    }
+    return ss->store_state(xy, folded, rs, cs, ya, yb, alpha, r, s, beta, iter, true);
+  } catch (const std::exception& e) {
+    return guard_exceptions(e);
+  }
+}
+
+template <class T>
+int init_state_t(T* xy, int32_t* folded, T* rs, T* cs, T* ya, T* yb, T* alpha,
+                 T* r, T* s, T* beta, int64_t* iter, const T* C, int64_t m,
+                 int64_t n, const T* p, const T* q, const T* x0,
+                 const drotb_config* cfgp) {
+  drotb::clear_error();
+  drotb_config cfg = effective(cfgp);
+  try {
+    std::unique_ptr<Session<T>> ss(new Session<T>());
+    RC_TRY(ss->create(m, n, cfg));
+    RC_TRY(ss->set_problem(C, p, q, false, false));
+    RC_TRY(ss->init(x0));
+    return ss->store_state(xy, folded, rs, cs, ya, yb, alpha, r, s, beta, iter, true);
+  } catch (const std::exception& e) {
+    return guard_exceptions(e);
+  }
+}
+
+template <class T>
+int engine_pass_t(drotb_engine* eng, T* xy, const T* C, const T* rs,
+                  const T* cs, T rho, int32_t kind, int32_t fold,
+                  int32_t* cost_folded, int32_t parity, int32_t want_dual,
+                  int32_t want_dx, int32_t deterministic, T* row_sums,
+                  T* col_sums, drotb_pass_out* out, drotb_counters* counters) {
+  drotb::clear_error();
+  if (!eng) return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "null engine");
+  if ((eng->precision == 0) != (sizeof(T) == 4))
+    return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "engine precision mismatch");
+  auto* s = static_cast<Session<T>*>(eng->impl);
+  int mode;
+  bool fold_write = false;
+  if (kind == DROTB_PASS_SKIP_COST) {
+    if (!cost_folded) return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "cost_folded required");
+    if ((fold != 0) == (*cost_folded != 0))
+      return drotb::set_error(DROTB_ERRC_FOLD_STATE_MISMATCH,
+                              fold ? "array already stores X - rho C"
+                                   : "array does not store X - rho C");
+    mode = fold ? drotb::kFold : drotb::kSkip;
+    fold_write = fold != 0;
+  } else {
+    mode = parity ? drotb::kPlain1 : drotb::kPlain0;
+  }
+  try {
+    const bool dual = want_dual != 0;
+    const bool dx = want_dx != 0;
+    RC_TRY(s->engine_pass(xy, C, rs, cs, rho, mode, dual, dx, deterministic != 0,
+                          row_sums, col_sums, out));
+  } catch (const std::exception& e) {
+    return guard_exceptions(e);
+  }
+  if (kind == DROTB_PASS_SKIP_COST) *cost_folded = fold_write ? 1 : 0;
+  if (kind == DROTB_PASS_UNFUSED && out) {
+    out->dual_valid = want_dual != 0;
+    out->dx_valid = want_dx != 0;
+  }
+  if (counters) {  // MemoryCounters (fused.hpp:305-310, 423-519)
+    const uint64_t cells = static_cast<uint64_t>(s->m) * static_cast<uint64_t>(s->n);
+    counters->passes += 1;
+    if (kind == DROTB_PASS_UNFUSED) {
+      counters->xy_elems_read += 4 * cells;
+      counters->xy_elems_written += cells;
+      counters->cost_elems_read += 2 * cells;
+    } else {
+      counters->xy_elems_read += cells;
+      counters->xy_elems_written += cells;
+      if (mode != drotb::kSkip) counters->cost_elems_read += cells;
+    }
+  }
+  return 0;
+}
+
+template <class T>
+int check_problem_t(const T* C, int64_t m, int64_t n, const T* p, const T* q) {
+  drotb::clear_error();
+  drotb_config cfg;
+  drotb_config_default(&cfg);
+  try {
+    std::unique_ptr<Session<T>> s(new Session<T>());
+    RC_TRY(s->create(m, n, cfg));
+    return s->set_problem(C, p, q, false, true);
+  } catch (const std::exception& e) {
+    return guard_exceptions(e);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t drotb_abi_version(void) { return DROTB_ABI_VERSION; }
+const char* drotb_last_error(void) { return drotb::last_error_cstr(); }
+const char* drotb_errc_name(int32_t errc) { return drotb::errc_name(errc); }
+int64_t drotb_kernel_launches(void) { return drotb::kernel_launch_count(); }
+
+void drotb_config_default(drotb_config* c) {  // DrotConfig{} (solver.hpp:51-88)
+  std::memset(c, 0, sizeof(*c));
+  c->rho0 = 2.0;
+  c->has_rho_override = 0;
+  c->relative_tolerances = 0;
+  c->rho_override = 0.0;
+  c->tol_primal = c->tol_dual = c->tol_gap = 1e-4;
+  c->max_iters = 100000;
+  c->check_every = 1;
+  c->engine = DROTB_ENGINE_FUSED;
+  c->skip_cost = 1;
+  c->deterministic = 1;
+  c->record_trace = 1;
+  c->workers = 0;
+  c->block_rows = 64;
+  c->work_size = 4;
+  c->trace_every = 1;
+  c->precision = 1;
+  c->device = -1;
+  c->order = DROTB_ORDER_FAST;
+  c->use_graphs = 1;
+}
+
+int drotb_solve_f32(const float* C, int64_t m, int64_t n, const float* p,
+                    const float* q, const drotb_config* cfg, const float* x0,
+                    float* plan, float* mu, float* nu, float* rho_out,
+                    drotb_report* rep, drotb_trace_row* trace,
+                    int64_t trace_cap, int64_t* trace_len, int64_t* iters,
+                    int32_t* status, double* wall) {
+  return solve_t<float>(C, m, n, p, q, cfg, x0, plan, mu, nu, rho_out, rep,
+                        trace, trace_cap, trace_len, iters, status, wall);
+}
+int drotb_solve_f64(const double* C, int64_t m, int64_t n, const double* p,
+                    const double* q, const drotb_config* cfg, const double* x0,
+                    double* plan, double* mu, double* nu, double* rho_out,
+                    drotb_report* rep, drotb_trace_row* trace,
+                    int64_t trace_cap, int64_t* trace_len, int64_t* iters,
+                    int32_t* status, double* wall) {
+  return solve_t<double>(C, m, n, p, q, cfg, x0, plan, mu, nu, rho_out, rep,
+                         trace, trace_cap, trace_len, iters, status, wall);
+}
+
+int drotb_step_f32(float* xy, int32_t* folded, float* rs, float* cs, float* ya,
+                   float* yb, float* alpha, float* r, float* s, float* beta,
+                   int64_t* iter, const float* C, int64_t m, int64_t n,
+                   const float* p, const float* q, const drotb_config* cfg) {
+  return step_t<float>(xy, folded, rs, cs, ya, yb, alpha, r, s, beta, iter, C,
+                       m, n, p, q, cfg);
+}
+int drotb_step_f64(double* xy, int32_t* folded, double* rs, double* cs,
+                   double* ya, double* yb, double* alpha, double* r, double* s,
+                   double* beta, int64_t* iter, const double* C, int64_t m,
+                   int64_t n, const double* p, const double* q,
+                   const drotb_config* cfg) {
+  return step_t<double>(xy, folded, rs, cs, ya, yb, alpha, r, s, beta, iter, C,
+                        m, n, p, q, cfg);
+}
+int drotb_init_state_f32(float* xy, int32_t* folded, float* rs, float* cs,
+                         float* ya, float* yb, float* alpha, float* r, float* s,
+                         float* beta, int64_t* iter, const float* C, int64_t m,
+                         int64_t n, const float* p, const float* q,
+                         const float* x0, const drotb_config* cfg) {
+  return init_state_t<float>(xy, folded, rs, cs, ya, yb, alpha, r, s, beta,
+                             iter, C, m, n, p, q, x0, cfg);
+}
+int drotb_init_state_f64(double* xy, int32_t* folded, double* rs, double* cs,
+                         double* ya, double* yb, double* alpha, double* r,
+                         double* s, double* beta, int64_t* iter,
+                         const double* C, int64_t m, int64_t n, const double* p,
+                         const double* q, const double* x0,
+                         const drotb_config* cfg) {
+  return init_state_t<double>(xy, folded, rs, cs, ya, yb, alpha, r, s, beta,
+                              iter, C, m, n, p, q, x0, cfg);
+}
+
+int drotb_engine_create(drotb_engine** eng, int64_t m, int64_t n,
+                        int64_t block_rows, int64_t work_size,
+                        int32_t precision, int32_t device) {
+  drotb::clear_error();
+  *eng = nullptr;
+  drotb_config cfg;
+  drotb_config_default(&cfg);
+  cfg.block_rows = block_rows;
+  cfg.work_size = work_size;
+  cfg.device = device;
+  cfg.order = DROTB_ORDER_FAST;
+  try {
+    std::unique_ptr<drotb_engine> e(new drotb_engine{precision, nullptr});
+    if (precision == 0) {
+      std::unique_ptr<Session<float>> s(new Session<float>());
+      RC_TRY(s->create(m, n, cfg));
+      e->impl = s.release();
+    } else {
+      std::unique_ptr<Session<double>> s(new Session<double>());
+      RC_TRY(s->create(m, n, cfg));
+      e->impl = s.release();
+    }
+    *eng = e.release();
+    return 0;
+  } catch (const std::exception& ex) {
+    return guard_exceptions(ex);
+  }
+}
+
+void drotb_engine_destroy(drotb_engine* eng) {
+  if (!eng) return;
+  if (eng->precision == 0)
+    delete static_cast<Session<float>*>(eng->impl);
+  else
+    delete static_cast<Session<double>*>(eng->impl);
+  delete eng;
+}
+
+int drotb_engine_pass_f32(drotb_engine* eng, float* xy, const float* C,
+                          const float* rs, const float* cs, float rho,
+                          int32_t kind, int32_t fold, int32_t* cost_folded,
+                          int32_t parity, int32_t want_dual, int32_t want_dx,
+                          int32_t deterministic, float* row_sums,
+                          float* col_sums, drotb_pass_out* out,
+                          drotb_counters* counters) {
+  return engine_pass_t<float>(eng, xy, C, rs, cs, rho, kind, fold, cost_folded,
+                              parity, want_dual, want_dx, deterministic,
+                              row_sums, col_sums, out, counters);
+}
+int drotb_engine_pass_f64(drotb_engine* eng, double* xy, const double* C,
+                          const double* rs, const double* cs, double rho,
+                          int32_t kind, int32_t fold, int32_t* cost_folded,
+                          int32_t parity, int32_t want_dual, int32_t want_dx,
+                          int32_t deterministic, double* row_sums,
+                          double* col_sums, drotb_pass_out* out,
+                          drotb_counters* counters) {
+  return engine_pass_t<double>(eng, xy, C, rs, cs, rho, kind, fold,
+                               cost_folded, parity, want_dual, want_dx,
+                               deterministic, row_sums, col_sums, out,
+                               counters);
+}
+
+int drotb_check_problem_f32(const float* C, int64_t m, int64_t n,
+                            const float* p, const float* q) {
+  return check_problem_t<float>(C, m, n, p, q);
+}
+int drotb_check_problem_f64(const double* C, int64_t m, int64_t n,
+                            const double* p, const double* q) {
+  return check_problem_t<double>(C, m, n, p, q);
+}
+
+// ---- sessions ----------------------------------------------------------------
+#define DROTB_DISPATCH(s, call)                                  \
+  ((s)->precision == 0 ? drotb::as_session<float>((s)->impl)->call \
+                       : drotb::as_session<double>((s)->impl)->call)
+
+int drotb_session_create(drotb_session** s, int64_t m, int64_t n,
+                         int32_t precision, const drotb_config* cfgp) {
+  drotb::clear_error();
+  *s = nullptr;
+  const drotb_config cfg = effective(cfgp);
+  try {
+    std::unique_ptr<drotb_session> h(new drotb_session{precision, nullptr});
+    if (precision == 0) {
+      std::unique_ptr<Session<float>> ss(new Session<float>());
+      RC_TRY(ss->create(m, n, cfg));
+      h->impl = ss.release();
+    } else {
+      std::unique_ptr<Session<double>> ss(new Session<double>());
+      RC_TRY(ss->create(m, n, cfg));
+      h->impl = ss.release();
+    }
+    *s = h.release();
+    return 0;
+  } catch (const std::exception& e) {
+    return guard_exceptions(e);
+  }
+}
+
+void drotb_session_destroy(drotb_session* s) {
+  if (!s) return;
+  if (s->precision == 0)
+    delete drotb::as_session<float>(s->impl);
+  else
+    delete drotb::as_session<double>(s->impl);
+  delete s;
+}
+
+int drotb_session_set_stream(drotb_session* s, void* stream) {
+  drotb::clear_error();
+  return DROTB_DISPATCH(s, set_stream(stream));
+}
+
+int drotb_session_set_problem(drotb_session* s, const void* C, const void* p,
+                              const void* q, int32_t is_device) {
+  drotb::clear_error();
+  if (s->precision == 0)
+    return drotb::as_session<float>(s->impl)->set_problem(
+        static_cast<const float*>(C), static_cast<const float*>(p),
+        static_cast<const float*>(q), is_device != 0, true);
+  return drotb::as_session<double>(s->impl)->set_problem(
+      static_cast<const double*>(C), static_cast<const double*>(p),
+      static_cast<const double*>(q), is_device != 0, true);
+}
+
+int drotb_session_gen_gaussian(drotb_session* s, double sigma_t, uint64_t seed,
+                               int32_t marginals) {
+  drotb::clear_error();
+  auto go = [&](auto* ss) -> int {
+    using T = typename std::remove_pointer<decltype(ss->X)>::type;
+    const int64_t m = ss->m, n = ss->n;
+    T* hostC = nullptr;
+    CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&hostC), sizeof(T) * m * n));
+    std::unique_ptr<T, decltype(&cudaFreeHost)> hold(hostC, &cudaFreeHost);
+    RC_TRY(drotb::gen_gaussian_cost<T>(m, n, sigma_t, seed, hostC));
+    std::vector<T> p(static_cast<size_t>(m)), q(static_cast<size_t>(n));
+    if (marginals == 1) {
+      RC_TRY(drotb::dyadic_marginal<T>(m, p.data()));
+      RC_TRY(drotb::dyadic_marginal<T>(n, q.data()));
+    } else if (marginals == 2) {
+      std::vector<double> pd(static_cast<size_t>(m)), qd(static_cast<size_t>(n));
+      drotb::dirichlet_marginal(seed, 4, m, pd.data());
+      drotb::dirichlet_marginal(seed, 5, n, qd.data());
+      for (int64_t i = 0; i < m; ++i) p[i] = static_cast<T>(pd[i]);
+      for (int64_t j = 0; j < n; ++j) q[j] = static_cast<T>(qd[j]);
+    } else {
+      for (int64_t i = 0; i < m; ++i) p[i] = static_cast<T>(1.0 / static_cast<double>(m));
+      for (int64_t j = 0; j < n; ++j) q[j] = static_cast<T>(1.0 / static_cast<double>(n));
+    }
+    return ss->set_problem(hostC, p.data(), q.data(), false, true);
+  };
+  try {
+    if (s->precision == 0) return go(drotb::as_session<float>(s->impl));
+    return go(drotb::as_session<double>(s->impl));
+  } catch (const std::exception& e) {
+    return guard_exceptions(e);
+  }
+}
+
+int drotb_session_init(drotb_session* s, const void* x0) {
+  drotb::clear_error();
+  if (s->precision == 0)
+    return drotb::as_session<float>(s->impl)->init(static_cast<const float*>(x0));
+  return drotb::as_session<double>(s->impl)->init(static_cast<const double*>(x0));
+}
+
+int drotb_session_enqueue(drotb_session* s, int64_t n_iters) {
+  drotb::clear_error();
+  return DROTB_DISPATCH(s, enqueue(n_iters));
+}
+
+int drotb_session_run(drotb_session* s) {
+  drotb::clear_error();
+  return DROTB_DISPATCH(s, run());
+}
+
+int drotb_session_synchronize(drotb_session* s) {
+  drotb::clear_error();
+  void* st = DROTB_DISPATCH(s, stream);
+  CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(st)));
+  return 0;
+}
+
+int drotb_session_status(drotb_session* s, int32_t* status, int64_t* iterations,
+                         drotb_report* report) {
+  drotb::clear_error();
+  return DROTB_DISPATCH(s, finish(status, iterations, report));
+}
+
+int drotb_session_get_plan(drotb_session* s, void* plan, void* mu, void* nu) {
+  drotb::clear_error();
+  if (s->precision == 0)
+    return drotb::as_session<float>(s->impl)->get_plan(
+        static_cast<float*>(plan), static_cast<float*>(mu), static_cast<float*>(nu));
+  return drotb::as_session<double>(s->impl)->get_plan(
+      static_cast<double*>(plan), static_cast<double*>(mu), static_cast<double*>(nu));
+}
+
+void* drotb_session_device_xy(drotb_session* s) {
+  return s->precision == 0 ? static_cast<void*>(drotb::as_session<float>(s->impl)->X)
+                           : static_cast<void*>(drotb::as_session<double>(s->impl)->X);
+}
+
+void* drotb_session_stream(drotb_session* s) {
+  return s->precision == 0 ? static_cast<void*>(drotb::as_session<float>(s->impl)->stream)
+                           : static_cast<void*>(drotb::as_session<double>(s->impl)->stream);
+}
+
+int drotb_session_pass_bytes(drotb_session* s, double* bytes_fold,
+                             double* bytes_skip) {
+  const double cells = s->precision == 0
+                           ? static_cast<double>(drotb::as_session<float>(s->impl)->m) *
+                                 drotb::as_session<float>(s->impl)->n
+                           : static_cast<double>(drotb::as_session<double>(s->impl)->m) *
+                                 drotb::as_session<double>(s->impl)->n;
+  const double sz = s->precision == 0 ? 4.0 : 8.0;
+  if (bytes_fold) *bytes_fold = 3.0 * sz * cells;  // read X, C; write X
+  if (bytes_skip) *bytes_skip = 2.0 * sz * cells;  // read X; write X
+  return 0;
+}
+
+int drotb_nccl_unique_id(char* out128) {
+  (void)out128;
+  return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "multi-GPU sharding not built");
+}
+
+int drotb_session_shard(drotb_session* s, int32_t rank, int32_t world_size,
+                        const char* nccl_id128, int64_t row_begin,
+                        int64_t row_end) {
+  (void)s; (void)rank; (void)world_size; (void)nccl_id128; (void)row_begin; (void)row_end;
+  return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "multi-GPU sharding not built");
+}
+
+}  // extern "C"

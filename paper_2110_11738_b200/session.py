@@ -1,0 +1,103 @@
+"""Device-resident solve session (benchmarks, multi-GPU shards).
+
+A Session owns the device copies of C, p, q and the DrotState and runs the
+same iteration as drot::solve (solver.hpp:372-540), enqueued as CUDA graphs
+on one stream.  It is the B200 replacement of keeping a FusedEngine alive
+and calling detail::step_impl in a loop (solver.hpp:358-360).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .api import (DrotConfig, Error, Errc, ResidualReport, SolveStatus, _check, _cm,
+                  _p, _vec)
+from ._lib import drotb_report
+
+
+class Session:
+    MARGINALS = {"uniform": 0, "dyadic": 1, "dirichlet": 2}
+
+    def __init__(self, m: int, n: int, dtype=np.float32, cfg: Optional[DrotConfig] = None):
+        self.m, self.n = int(m), int(n)
+        self.dtype = np.dtype(dtype)
+        self.cfg = cfg or DrotConfig()
+        lib = _lib.load()
+        h = C.c_void_p()
+        ccfg = self.cfg.to_c()
+        _check(lib.drotb_session_create(C.byref(h), self.m, self.n,
+                                        0 if self.dtype == np.float32 else 1, C.byref(ccfg)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.load().drotb_session_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_stream(self, stream_ptr: Optional[int]):
+        _check(_lib.load().drotb_session_set_stream(self._h, stream_ptr))
+
+    @property
+    def stream(self) -> int:
+        return _lib.load().drotb_session_stream(self._h)
+
+    def set_problem(self, cost: np.ndarray, p: np.ndarray, q: np.ndarray):
+        dt = self.dtype
+        cm = _cm(cost, dt)
+        _check(_lib.load().drotb_session_set_problem(
+            self._h, _p(cm), _p(_vec(p, dt)), _p(_vec(q, dt)), 0))
+
+    def set_problem_device(self, cost_ptr: int, p_ptr: int, q_ptr: int):
+        _check(_lib.load().drotb_session_set_problem(self._h, cost_ptr, p_ptr, q_ptr, 1))
+
+    def gen_gaussian(self, sigma_t: float = 5.0, seed: int = 0, marginals: str = "dyadic"):
+        _check(_lib.load().drotb_session_gen_gaussian(self._h, sigma_t, seed,
+                                                      self.MARGINALS[marginals]))
+
+    def init(self, x0: Optional[np.ndarray] = None):
+        x = None if x0 is None else _cm(x0, self.dtype)
+        _check(_lib.load().drotb_session_init(self._h, _p(x)))
+
+    def enqueue(self, iters: int):
+        _check(_lib.load().drotb_session_enqueue(self._h, int(iters)))
+
+    def run(self):
+        _check(_lib.load().drotb_session_run(self._h))
+
+    def synchronize(self):
+        _check(_lib.load().drotb_session_synchronize(self._h))
+
+    def status(self):
+        st, it = C.c_int32(0), C.c_int64(0)
+        rep = drotb_report()
+        _check(_lib.load().drotb_session_status(self._h, C.byref(st), C.byref(it), C.byref(rep)))
+        return (SolveStatus(st.value), int(it.value),
+                ResidualReport(rep.r_primal, rep.r_dual, rep.gap, rep.objective))
+
+    def plan(self):
+        plan = np.empty((self.m, self.n), self.dtype, order="F")
+        mu = np.empty(self.m, self.dtype)
+        nu = np.empty(self.n, self.dtype)
+        _check(_lib.load().drotb_session_get_plan(self._h, _p(plan), _p(mu), _p(nu)))
+        return plan, mu, nu
+
+    def pass_bytes(self):
+        a, b = C.c_double(0), C.c_double(0)
+        _check(_lib.load().drotb_session_pass_bytes(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def device_xy(self) -> int:
+        return _lib.load().drotb_session_device_xy(self._h)

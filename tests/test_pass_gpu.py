@@ -1,0 +1,298 @@
+"""Pass-level parity of the sm_100a fused sweep against the reference engine.
+
+Ports every case of the reference's tests/test_fused.cpp (the only tests that
+pin the hot path) and adds direct GPU-vs-reference comparisons:
+the reference FusedEngine<T> (oracle/_ref, the unmodified reference
+library) runs on the same inputs and the GPU must match it
+
+  * X bitwise (elementwise update, fused.hpp:252-265),
+  * u bitwise for every tiling (tile-column order, fused.hpp:267/314-317),
+  * v bitwise when block_rows == 64 (the GPU's fixed 64-row v blocks),
+    else within 1e-12 (the reference's own tiling tolerance,
+    test_fused.cpp:162-167),
+  * cost / prev-cost / dual^2 / dx^2 / max|t| / nonfinite bitwise in
+    deterministic mode (reference tile-chain order, fused.hpp:322-329).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+F64, F32 = np.float64, np.float32
+
+
+def fixture(ref, m, n, seed, dt=F64):
+    """Fixture::random (test_fused.cpp:18-34)."""
+    xy = ref.random_unit(seed, m * n, -0.5, 1.0).reshape((m, n), order="F")
+    cost = ref.random_unit(seed ^ 0xC0C0, m * n).reshape((m, n), order="F")
+    sh = ref.random_unit(seed ^ 0xFEED, m + n) - 0.5
+    return (np.asfortranarray(xy.astype(dt)), np.asfortranarray(cost.astype(dt)),
+            sh[:m].astype(dt), sh[m:].astype(dt))
+
+
+def gpu_pass(drot, xy, cost, phi, varphi, rho, kind=0, fold=False, folded=False, parity=0,
+             bs=64, ws=4, dual=True, dx=True, det=True, counters=None):
+    m, n = xy.shape
+    eng = drot.FusedEngine(drot.plan_tiles(m, n, bs, ws), xy.dtype)
+    x = np.asfortranarray(xy.copy())
+    opts = drot.PassOptions(parity=parity, want_dual=dual, want_dx=dx, deterministic=det,
+                            counters=counters)
+    if kind == 1:
+        arr = drot.FusedArray(x, folded)
+        out = eng.fused_pass_skip_cost(arr, cost, phi, varphi, rho, fold, opts)
+        return out, arr.values, arr.cost_folded
+    if kind == 2:
+        return eng.unfused_pass(x, cost, phi, varphi, rho, opts), x, False
+    return eng.fused_pass(x, cost, phi, varphi, rho, opts), x, False
+
+
+def ref_pass(ref, xy, cost, phi, varphi, rho, kind=0, fold=False, folded=False, parity=0,
+             bs=64, ws=4, dual=True, dx=True, det=True):
+    m, n = xy.shape
+    r = ref.fused_pass(xy.ravel(order="F"), cost.ravel(order="F"), phi, varphi, rho, m, n,
+                       bs=bs, ws=ws, workers=3, kind=kind, fold=fold, folded=folded,
+                       parity=parity, want_dual=dual, want_dx=dx, deterministic=det)
+    return r
+
+
+SCALARS = ["cost_dot", "prev_cost_dot", "dual_sq", "dx_sq", "max_abs"]
+FLAGS = ["cost_valid", "prev_cost_valid", "dual_valid", "dx_valid", "nonfinite"]
+
+
+def assert_match(out, x, r, bs, exact_scalars=True, vtol=1e-12):
+    m, n = x.shape
+    np.testing.assert_array_equal(x.ravel(order="F"), r["xy"])
+    np.testing.assert_array_equal(out.row_sums, r["row_sums"])
+    if bs == 64:
+        np.testing.assert_array_equal(out.col_sums, r["col_sums"])
+    else:
+        np.testing.assert_allclose(out.col_sums, r["col_sums"], rtol=vtol, atol=1e-300)
+    for f in FLAGS:
+        assert bool(getattr(out, f)) == bool(r[f]), f
+    for f in SCALARS:
+        g, w = getattr(out, f), r[f]
+        if exact_scalars:
+            assert g == w or (np.isnan(g) and np.isnan(w)), (f, g, w)
+        else:
+            assert abs(g - w) <= vtol * max(1.0, abs(w)), (f, g, w)
+
+
+# ---- ports of test_fused.cpp ---------------------------------------------------
+def test_identity_pass(drot, ref):  # test_fused.cpp:66-87
+    xy, cost, _, _ = fixture(ref, 6, 4, 1)
+    xy = np.abs(xy)
+    phi, varphi = np.zeros(6), np.zeros(4)
+    out, x, _ = gpu_pass(drot, xy, cost, phi, varphi, 0.0, bs=2, ws=1, dual=False, dx=False)
+    np.testing.assert_array_equal(x, xy)
+    np.testing.assert_allclose(out.row_sums, xy.sum(axis=1), rtol=1e-12)
+    np.testing.assert_allclose(out.col_sums, xy.sum(axis=0), rtol=1e-12)
+    assert out.cost_dot == pytest.approx(float((cost * xy).sum()), rel=1e-12)
+    assert_match(out, x, ref_pass(ref, xy, cost, phi, varphi, 0.0, bs=2, ws=1, dual=False,
+                                  dx=False), 2)
+
+
+def test_full_clamp(drot, ref):  # test_fused.cpp:89-101
+    xy, cost, _, _ = fixture(ref, 3, 3, 2)
+    xy = -1.0 - np.abs(xy)
+    phi, varphi = -np.ones(3), -np.ones(3)
+    out, x, _ = gpu_pass(drot, np.asfortranarray(xy), cost, phi, varphi, 0.2)
+    assert (x == 0).all() and (out.row_sums == 0).all() and (out.col_sums == 0).all()
+    assert out.cost_dot == 0.0
+    assert not np.signbit(x).any()  # +0, not -0 (t > 0 ? t : 0)
+
+
+@pytest.mark.parametrize("dt", [F64, F32])
+def test_fused_vs_model_and_unfused(drot, ref, dt):  # test_fused.cpp:103-138
+    xy, cost, phi, varphi = fixture(ref, 7, 5, 3, dt)
+    rho = dt(0.2)
+    fo, xf, _ = gpu_pass(drot, xy, cost, phi, varphi, rho, bs=2, ws=1)
+    uo, xu, _ = gpu_pass(drot, xy, cost, phi, varphi, rho, kind=2, bs=2, ws=1)
+    # double-loop model (value check)
+    e = rho * cost
+    t = ((xy + phi[:, None]) + varphi[None, :]) - e
+    xp = np.where(t > 0, t, 0)
+    np.testing.assert_allclose(xf, xp, rtol=1e-12 if dt == F64 else 1e-6)
+    np.testing.assert_array_equal(xf, xu)
+    for f in ["row_sums", "col_sums"]:
+        np.testing.assert_array_equal(getattr(fo, f), getattr(uo, f))
+    for f in SCALARS:
+        assert getattr(fo, f) == getattr(uo, f)
+    assert_match(fo, xf, ref_pass(ref, xy, cost, phi, varphi, rho, bs=2, ws=1), 2)
+    assert_match(uo, xu, ref_pass(ref, xy, cost, phi, varphi, rho, kind=2, bs=2, ws=1), 2)
+
+
+@pytest.mark.parametrize("cfg", [(1, 1), (2, 3), (5, 1), (8, 2), (64, 4), (64, 1), (64, 7)])
+def test_tiling_independence(drot, ref, cfg):  # test_fused.cpp:140-188
+    bs, ws = cfg
+    xy, cost, phi, varphi = fixture(ref, 23, 17, 4)
+    base, xb, _ = gpu_pass(drot, xy, cost, phi, varphi, 0.2, bs=64, ws=4)
+    out, x, _ = gpu_pass(drot, xy, cost, phi, varphi, 0.2, bs=bs, ws=ws)
+    np.testing.assert_array_equal(x, xb)
+    np.testing.assert_allclose(out.row_sums, base.row_sums, rtol=1e-12)
+    np.testing.assert_allclose(out.col_sums, base.col_sums, rtol=1e-12)
+    assert out.cost_dot == pytest.approx(base.cost_dot, rel=1e-12)
+    assert_match(out, x, ref_pass(ref, xy, cost, phi, varphi, 0.2, bs=bs, ws=ws), bs)
+    # repeatability (deterministic): identical bits on every launch
+    again, x2, _ = gpu_pass(drot, xy, cost, phi, varphi, 0.2, bs=bs, ws=ws)
+    np.testing.assert_array_equal(again.col_sums, out.col_sums)
+    assert again.cost_dot == out.cost_dot
+
+
+def test_row_col_mass(drot, ref):  # test_fused.cpp:190-204
+    rs = np.random.default_rng(55)
+    for _ in range(6):
+        m, n = int(rs.integers(4, 24)), int(rs.integers(3, 23))
+        xy, cost, phi, varphi = fixture(ref, m, n, int(rs.integers(1 << 62)))
+        out, _, _ = gpu_pass(drot, xy, cost, phi, varphi, 0.2, bs=4, ws=2)
+        assert out.total_mass() == pytest.approx(out.col_sums.sum(), rel=1e-9)
+        assert (out.row_sums >= 0).all() and (out.col_sums >= 0).all()
+
+
+@pytest.mark.parametrize("dt", [F64, F32])
+def test_skip_cost_alternation_bitwise(drot, ref, dt):  # test_fused.cpp:206-258
+    m = n = 6
+    xy, cost, phi, varphi = fixture(ref, m, n, 6, dt)
+    xy = np.abs(xy)
+    rho = dt(0.2)
+    eng = drot.FusedEngine(drot.plan_tiles(m, n, 2, 2), dt)
+    x_plain = np.asfortranarray(xy.copy())
+    plain = [eng.fused_pass(x_plain, cost, phi, varphi, rho, drot.PassOptions(parity=k % 2))
+             for k in range(100)]
+    arr = drot.FusedArray(np.asfortranarray(xy.copy()), False)
+    ctr = drot.MemoryCounters()
+    skip = [eng.fused_pass_skip_cost(arr, cost, phi, varphi, rho, not arr.cost_folded,
+                                     drot.PassOptions(counters=ctr)) for _ in range(100)]
+    for a, b in zip(skip, plain):
+        np.testing.assert_array_equal(a.row_sums, b.row_sums)
+        np.testing.assert_array_equal(a.col_sums, b.col_sums)
+        if a.cost_valid:
+            assert a.cost_dot == b.cost_dot
+    assert not arr.cost_folded
+    np.testing.assert_array_equal(arr.values, x_plain)
+    cells = 36
+    assert ctr.passes == 100
+    assert ctr.xy_elems_read == cells * 100 and ctr.xy_elems_written == cells * 100
+    assert ctr.cost_elems_read == cells * 50
+    # and the same trajectory through the reference engine
+    x = xy.ravel(order="F").copy()
+    folded = False
+    for k in range(100):
+        r = ref.fused_pass(x, cost.ravel(order="F"), phi, varphi, rho, m, n, bs=2, ws=2,
+                           kind=1, fold=not folded, folded=folded)
+        x, folded = r["xy"], r["folded"]
+        np.testing.assert_array_equal(r["row_sums"], skip[k].row_sums)
+        np.testing.assert_array_equal(r["col_sums"], skip[k].col_sums)
+    np.testing.assert_array_equal(x, arr.values.ravel(order="F"))
+
+
+def test_prev_cost_recovery(drot, ref):  # test_fused.cpp:260-284
+    xy, cost, phi, varphi = fixture(ref, 5, 4, 7)
+    xy = np.abs(xy)
+    eng = drot.FusedEngine(drot.plan_tiles(5, 4, 64, 4), F64)
+    arr = drot.FusedArray(np.asfortranarray(xy.copy()), False)
+    o1 = eng.fused_pass_skip_cost(arr, cost, phi, varphi, 0.2, True)
+    assert o1.cost_valid
+    o2 = eng.fused_pass_skip_cost(arr, cost, phi, varphi, 0.2, False)
+    assert not o2.cost_valid
+    x2 = arr.values.copy()
+    o3 = eng.fused_pass_skip_cost(arr, cost, phi, varphi, 0.2, True)
+    assert o3.prev_cost_valid
+    assert o3.prev_cost_dot == pytest.approx(float((cost * x2).sum()), rel=1e-12)
+
+
+def test_zero_rho_fold_noop(drot, ref):  # test_fused.cpp:286-302
+    xy, cost, phi, varphi = fixture(ref, 4, 4, 8)
+    xy = np.abs(xy)
+    _, xa, _ = gpu_pass(drot, xy, cost, phi, varphi, 0.0, bs=2, ws=1)
+    _, xb, fl = gpu_pass(drot, xy, cost, phi, varphi, 0.0, kind=1, fold=True, bs=2, ws=1)
+    assert fl
+    np.testing.assert_array_equal(xa, xb)
+
+
+def test_wrong_fold_flag(drot, ref):  # test_fused.cpp:304-319
+    xy, cost, phi, varphi = fixture(ref, 3, 3, 9)
+    eng = drot.FusedEngine(drot.plan_tiles(3, 3, 2, 1), F64)
+    arr = drot.FusedArray(np.asfortranarray(xy.copy()), False)
+    with pytest.raises(drot.Error) as ei:
+        eng.fused_pass_skip_cost(arr, cost, phi, varphi, 0.2, False)
+    assert ei.value.code == drot.Errc.fold_state_mismatch
+    assert str(ei.value).startswith("fold_state_mismatch: ")
+    eng.fused_pass_skip_cost(arr, cost, phi, varphi, 0.2, True)
+    with pytest.raises(drot.Error):
+        eng.fused_pass_skip_cost(arr, cost, phi, varphi, 0.2, True)
+
+
+def test_unfused_counters(drot, ref):  # test_fused.cpp:321-332
+    xy, cost, phi, varphi = fixture(ref, 8, 8, 10)
+    ctr = drot.MemoryCounters()
+    gpu_pass(drot, xy, cost, phi, varphi, 0.2, kind=2, bs=4, ws=1, counters=ctr)
+    assert ctr.xy_elems_read == 64 * 4 and ctr.xy_elems_written == 64
+    assert ctr.cost_elems_read == 64 * 2
+
+
+@pytest.mark.parametrize("dt", [F64, F32])
+def test_nonfinite_flag(drot, ref, dt):  # test_fused.cpp:334-342
+    xy, cost, phi, varphi = fixture(ref, 3, 3, 11, dt)
+    big = np.finfo(dt).max
+    xy[1, 1] = big
+    phi[:] = big
+    out, x, _ = gpu_pass(drot, xy, cost, phi, varphi, dt(0.2))
+    assert out.nonfinite
+    r = ref_pass(ref, xy, cost, phi, varphi, dt(0.2))
+    assert r["nonfinite"]
+    np.testing.assert_array_equal(x.ravel(order="F"), r["xy"])
+
+
+def test_nan_flag(drot, ref):
+    xy, cost, phi, varphi = fixture(ref, 70, 9, 12)
+    xy[65, 3] = np.nan  # NaN clamps to 0 but must raise the flag
+    out, x, _ = gpu_pass(drot, xy, cost, phi, varphi, 0.2)
+    assert out.nonfinite and x[65, 3] == 0.0
+    assert_match(out, x, ref_pass(ref, xy, cost, phi, varphi, 0.2), 64)
+
+
+def test_free_order_within_noise(drot, ref):  # test_fused.cpp:344-360
+    xy, cost, phi, varphi = fixture(ref, 33, 29, 12)
+    det, xd, _ = gpu_pass(drot, xy, cost, phi, varphi, 0.2, bs=4, ws=2, det=True)
+    fr, xf, _ = gpu_pass(drot, xy, cost, phi, varphi, 0.2, bs=4, ws=2, det=False)
+    np.testing.assert_array_equal(xd, xf)
+    np.testing.assert_allclose(fr.row_sums, det.row_sums, rtol=1e-12)
+    assert fr.cost_dot == pytest.approx(det.cost_dot, rel=1e-12)
+
+
+# ---- larger shapes, every mode, both precisions ----------------------------------
+MODES = [  # (kind, fold, folded, parity)
+    (0, False, False, 0), (0, False, False, 1), (1, True, False, 0), (1, False, True, 1),
+    (2, False, False, 1)]
+
+
+@pytest.mark.parametrize("dt", [F64, F32])
+@pytest.mark.parametrize("shape", [(1000, 700), (777, 333), (1, 1), (129, 300), (4096, 20),
+                                   (50, 2000)])
+@pytest.mark.parametrize("mode", MODES)
+def test_gpu_matches_reference_engine(drot, ref, dt, shape, mode):
+    m, n = shape
+    kind, fold, folded, parity = mode
+    xy, cost, phi, varphi = fixture(ref, m, n, 1234 + m + n, dt)
+    rho = dt(0.7 / (m + n) * 50)
+    out, x, fl = gpu_pass(drot, xy, cost, phi, varphi, rho, kind, fold, folded, parity)
+    r = ref_pass(ref, xy, cost, phi, varphi, rho, kind, fold, folded, parity)
+    assert_match(out, x, r, 64)
+    if kind == 1:
+        assert fl == r["folded"]
+
+
+@pytest.mark.parametrize("dt", [F64, F32])
+def test_fast_order_scalars(drot, ref, dt):
+    """deterministic=False selects the fast tree reductions: X, u, v stay
+    bitwise; scalars agree to summation-order noise."""
+    xy, cost, phi, varphi = fixture(ref, 1000, 900, 99, dt)
+    out, x, _ = gpu_pass(drot, xy, cost, phi, varphi, dt(0.05), det=False)
+    r = ref_pass(ref, xy, cost, phi, varphi, dt(0.05))
+    np.testing.assert_array_equal(x.ravel(order="F"), r["xy"])
+    np.testing.assert_array_equal(out.row_sums, r["row_sums"])
+    np.testing.assert_array_equal(out.col_sums, r["col_sums"])
+    tol = 1e-12 if dt == F64 else 2e-4
+    for f in ["cost_dot", "prev_cost_dot", "dual_sq", "dx_sq"]:
+        assert abs(getattr(out, f) - r[f]) <= tol * abs(r[f]) + 1e-30, f
+    assert out.max_abs == r["max_abs"]
