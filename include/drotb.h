@@ -294,6 +294,16 @@ void* drotb_session_stream(drotb_session* s);
 int drotb_session_pass_bytes(drotb_session* s, double* bytes_fold,
                              double* bytes_skip);
 
+/* Run exactly n_iters iterations eagerly, bracketed by CUDA events on the
+ * session stream, with an event pair around every fused-sweep launch.
+ * total_ms: first-to-last event; pass_ms: summed sweep durations; n_pass:
+ * sweeps timed; pass_bytes: their algorithmic bytes (3*s*m*n per C-reading
+ * sweep, 2*s*m*n per skip sweep); launches: kernels launched.
+ * Synchronizes. */
+int drotb_session_run_timed(drotb_session* s, int64_t n_iters, double* total_ms,
+                            double* pass_ms, int64_t* n_pass, double* pass_bytes,
+                            int64_t* launches);
+
 /* ---- multi-GPU (row sharding, NCCL) ------------------------------------- */
 #define DROTB_NCCL_ID_BYTES 128
 int drotb_nccl_unique_id(char* out128);

@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libdrotb200.so")
+LIB_PATH = os.environ.get("DROTB_LIB") or os.path.join(PKG, "libdrotb200.so")
 
 
 class drotb_config(C.Structure):
@@ -104,6 +104,7 @@ SIGNATURES = {
     "drotb_session_device_xy": (vp, [vp]),
     "drotb_session_stream": (vp, [vp]),
     "drotb_session_pass_bytes": (C.c_int, [vp, P(f64), P(f64)]),
+    "drotb_session_run_timed": (C.c_int, [vp, i64, P(f64), P(f64), P(i64), P(f64), P(i64)]),
     "drotb_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "drotb_session_shard": (C.c_int, [vp, i32, i32, C.c_char_p, i64, i64]),
 }

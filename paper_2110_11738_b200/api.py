@@ -262,8 +262,8 @@ def check_problem(problem: TransportProblem) -> None:
                     "shape_mismatch: marginal lengths do not match the cost matrix")
     lib = _lib.load()
     cm = _cm(problem.cost, dt)
-    _check(getattr(lib, "drotb_check_problem_" + _sfx(dt))(
-        _p(cm), m, n, _p(_vec(problem.p, dt)), _p(_vec(problem.q, dt))))
+    pv, qv = _vec(problem.p, dt), _vec(problem.q, dt)  # keep alive across the call
+    _check(getattr(lib, "drotb_check_problem_" + _sfx(dt))(_p(cm), m, n, _p(pv), _p(qv)))
 
 
 def solve(problem: TransportProblem, cfg: Optional[DrotConfig] = None,
@@ -343,12 +343,21 @@ def _state_call(fn_name, problem, cfg, st: DrotState, x0=None):
     folded = C.c_int32(int(st.xy.cost_folded))
     alpha, beta = ct(st.y_mass_gap), ct(st.x_mass_gap)
     it = C.c_int64(st.iter)
+    for name in ("row_shift", "col_shift", "y_row_defect", "y_col_defect", "row_residual",
+                 "col_residual"):
+        arr = getattr(st, name)
+        if not (isinstance(arr, np.ndarray) and arr.dtype == dt and arr.flags.c_contiguous):
+            raise Error(Errc.bad_config, f"bad_config: state.{name} must be a contiguous {dt} array")
+    if not (st.xy.values.dtype == dt and st.xy.values.flags.f_contiguous):
+        raise Error(Errc.bad_config, "bad_config: state.xy must be a Fortran-ordered array")
+    keep = [_cm(problem.cost, dt), _vec(problem.p, dt), _vec(problem.q, dt),
+            None if x0 is None else _cm(x0, dt)]  # alive across the call
     args = [_p(st.xy.values), C.byref(folded), _p(st.row_shift), _p(st.col_shift),
             _p(st.y_row_defect), _p(st.y_col_defect), C.byref(alpha), _p(st.row_residual),
             _p(st.col_residual), C.byref(beta), C.byref(it),
-            _p(_cm(problem.cost, dt)), m, n, _p(_vec(problem.p, dt)), _p(_vec(problem.q, dt))]
+            _p(keep[0]), m, n, _p(keep[1]), _p(keep[2])]
     if x0 is not None or fn_name.startswith("drotb_init_state"):
-        args.append(_p(None if x0 is None else _cm(x0, dt)))
+        args.append(_p(keep[3]))
     ccfg = cfg.to_c()
     args.append(C.byref(ccfg))
     rc = getattr(lib, fn_name + "_" + _sfx(dt))(*args)
@@ -505,9 +514,10 @@ class FusedEngine:
             ctr.xy_elems_written, ctr.cost_elems_read = c.xy_elems_written, c.cost_elems_read
         fl = C.c_int32(int(folded))
         lib = _lib.load()
+        keep = [_cm(cost, dt), _vec(row_shift, dt), _vec(col_shift, dt)]
         _check(getattr(lib, "drotb_engine_pass_" + _sfx(dt))(
-            self._h, _p(xy), _p(_cm(cost, dt)), _p(_vec(row_shift, dt)),
-            _p(_vec(col_shift, dt)), _ctype(dt)(rho), kind, int(fold), C.byref(fl),
+            self._h, _p(xy), _p(keep[0]), _p(keep[1]),
+            _p(keep[2]), _ctype(dt)(rho), kind, int(fold), C.byref(fl),
             int(opts.parity), int(opts.want_dual), int(opts.want_dx),
             int(opts.deterministic), _p(row), _p(col), C.byref(out), C.byref(ctr)))
         if opts.counters is not None:

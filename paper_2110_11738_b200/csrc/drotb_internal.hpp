@@ -124,6 +124,10 @@ struct TailArgs {
   // exact-mode per-tile scalar chains (tile order)
   const PassPartial<T>* tile_partials;
   int64_t n_tiles;
+  // CUDA-graph IF node guarding the confirm report of this iteration
+  unsigned long long cond;
+  int32_t use_cond;
+  int32_t pad1;
 };
 
 // ---- kernel launchers (kernels.cu) ---------------------------------------

@@ -127,141 +127,197 @@ __device__ __forceinline__ bool last_block(unsigned int* ticket) {
 // K1: the fused sweep
 // ---------------------------------------------------------------------------
 // Thread mapping: a warp owns 32*R consecutive rows (R = 16 B / sizeof(T)
-// rows per lane, one 128-bit load per column) of one reference tile column
+// rows per lane, one 128-bit load per column) of one tile column
 // [c0, c0+tc).  Each lane walks the tile's columns in order, so its row
 // partials are exactly the reference's u strips (fused.hpp:267, tile-local
 // running sum from 0).  Column partials must be sequential over each
 // 64-row block (fused.hpp:268): the warp stages x+ of 16 columns in shared
-// memory (conflict-free swizzle) and one lane per (column, 64-row block)
-// sums the 64 values in row order.
+// memory and one lane per (column, 64-row block) sums the 64 values in row
+// order with 128-bit shared loads.
 //
-// Swizzle: element (c, r) of a warp's [16 x 32R] staging tile lives at
-//   c*32R + R*((r/R) ^ H(c, r)) + ((r + c) mod R)
-// fp32 (R=4): H = (c>>2) | ((r>>6)<<2);  fp64 (R=2): H = (c>>1) & 7.
-// Writes (one 16-B vector per lane, components rotated by c) and the
-// row-order reads (lane = column/block) are both bank-conflict free.
-template <class T>
-__device__ __forceinline__ int stage_index(int c, int r) {
-  constexpr int R = 16 / sizeof(T);
-  constexpr int ROWS_W = 32 * R;
-  if constexpr (R == 4) {
-    const int h = (c >> 2) | ((r >> 6) << 2);
-    return c * ROWS_W + 4 * ((r >> 2) ^ h) + ((r + c) & 3);
-  } else {
-    const int h = (c >> 1) & 7;
-    return c * ROWS_W + 2 * ((r >> 1) ^ h) + ((r + c) & 1);
-  }
-}
-
+// Staging layout (per warp, 16 columns x 32R rows, 16-B chunks): chunk q
+// (rows qR..qR+R-1) of column c lives at chunk slot c*32 + (q ^ (c & 7)).
+// The STS.128 of a column (lane l writes chunk l) and the LDS.128 of the
+// row-order reads (lane = column [+16 * block], same q across lanes) both
+// touch 8 distinct 16-B bank groups per 8-lane phase: conflict free.
+//
+// Memory pipeline: columns are processed in groups of G with register
+// double buffering -- the loads of group g+1 (and of the next chunk's first
+// group, across the v-phase) are in flight while group g is computed.
 template <class T>
 struct PassAcc {
   T cost, prev, dual, dx, mx;
   bool bad;
 };
 
-template <class T, int MODE, bool DUAL, bool DX, bool MASK>
-__device__ __forceinline__ void pass_chunk(const PassArgs<T>& a, int64_t j0,
-                                           int cnt, int64_t row0, int nvalid,
-                                           const T (&ph)[16 / sizeof(T)],
-                                           T (&u)[16 / sizeof(T)],
-                                           PassAcc<T>& acc, T* wbuf,
-                                           int lane) {
+template <class T, int G>
+struct ColGroup {
+  typename V16<T>::type x[G], c[G];
+  T v[G];
+};
+
+template <class T, int MODE, int G>
+__device__ __forceinline__ void load_group(const PassArgs<T>& a, ColGroup<T, G>& g,
+                                           int64_t j, int64_t c1, int64_t row0,
+                                           bool live) {
   using V = typename V16<T>::type;
-  constexpr int R = 16 / sizeof(T);
-  constexpr int CH = kChunkCols;
-  constexpr int G = 8;  // columns in flight per lane
   constexpr bool RC = MODE != kSkip;
-  const bool live = !MASK || nvalid > 0;
 #pragma unroll
-  for (int g = 0; g < CH; g += G) {
-    V xv[G], cv[G];
-    T vj[G];
-#pragma unroll
-    for (int k = 0; k < G; ++k) {
-      const int c = g + k;
-      xv[k] = vzero<T>();
-      cv[k] = vzero<T>();
-      vj[k] = T(0);
-      if (c < cnt) {
-        const int64_t off = (j0 + c) * a.ld + row0;
-        if (live) {
-          xv[k] = __ldcs(reinterpret_cast<const V*>(a.xy + off));
-          if (RC) cv[k] = __ldcs(reinterpret_cast<const V*>(a.cost + off));
-        }
-        vj[k] = __ldg(a.varphi + j0 + c);
+  for (int k = 0; k < G; ++k) {
+    if (j + k < c1) {
+      const int64_t off = (j + k) * a.ld + row0;
+      if (live) {
+        g.x[k] = __ldcs(reinterpret_cast<const V*>(a.xy + off));
+        if (RC) g.c[k] = __ldcs(reinterpret_cast<const V*>(a.cost + off));
       }
-    }
-#pragma unroll
-    for (int k = 0; k < G; ++k) {
-      const int c = g + k;
-      if (c < cnt) {
-        T x[R], cc[R], xp[R], st[R];
-        unpack(xv[k], x);
-        unpack(cv[k], cc);
-#pragma unroll
-        for (int t = 0; t < R; ++t) {
-          T e = T(0), tv;
-          if (RC) {
-            e = a.rho * cc[t];
-            if (MODE == kPlain1)
-              tv = ((x[t] - e) + ph[t]) + vj[k];
-            else
-              tv = ((x[t] + ph[t]) + vj[k]) - e;
-          } else {
-            tv = (x[t] + ph[t]) + vj[k];
-          }
-          T p = tv > T(0) ? tv : T(0);
-          const bool valid = !MASK || t < nvalid;
-          if (MASK && !valid) {
-            p = T(0);
-            tv = T(0);
-          }
-          xp[t] = p;
-          st[t] = (MODE == kFold) ? p - e : p;
-          u[t] += p;
-          if (RC) {
-            acc.cost = fma(cc[t], p, acc.cost);
-            acc.prev = fma(cc[t], x[t], acc.prev);
-            if (DUAL) {
-              const T d = (ph[t] + vj[k]) - e;
-              if (valid && d > T(0)) acc.dual = fma(d, d, acc.dual);
-            }
-          }
-          if (DX) {
-            const T dd = p - x[t];
-            acc.dx = fma(dd, dd, acc.dx);
-          }
-          const T at = fabs(tv);
-          acc.mx = fmax(acc.mx, at);
-          acc.bad |= !(at <= max_finite<T>());
-        }
-        if (live) {
-          const int64_t off = (j0 + c) * a.ld + row0;
-          __stcs(reinterpret_cast<V*>(a.xy + off), pack4(st));
-        }
-        // stage x+ for the column sums, components rotated by c
-        T rot[R];
-#pragma unroll
-        for (int pp = 0; pp < R; ++pp) rot[pp] = xp[(pp - c) & (R - 1)];
-        int h;
-        if constexpr (R == 4)
-          h = (c >> 2) | ((lane >> 4) << 2);
-        else
-          h = (c >> 1) & 7;
-        *reinterpret_cast<V*>(wbuf + c * 32 * R + R * (lane ^ h)) = pack4(rot);
-      }
+      g.v[k] = __ldg(a.varphi + j + k);
     }
   }
 }
 
-template <class T, int MODE, bool DUAL, bool DX>
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
-    pass_kernel(const PassArgs<T> a) {
+template <class T, int MODE, bool DUAL, bool DX, bool MASK, int G>
+__device__ __forceinline__ void compute_group(const PassArgs<T>& a,
+                                              const ColGroup<T, G>& g, int64_t j,
+                                              int cbase, int64_t c1, int64_t row0,
+                                              int nvalid, const T (&ph)[16 / sizeof(T)],
+                                              T (&u)[16 / sizeof(T)], PassAcc<T>& acc,
+                                              T* wbuf, int lane) {
+  using V = typename V16<T>::type;
+  constexpr int R = 16 / sizeof(T);
+  constexpr bool RC = MODE != kSkip;
+  const bool live = !MASK || nvalid > 0;
+#pragma unroll
+  for (int k = 0; k < G; ++k) {
+    const int c = cbase + k;
+    if (j + k < c1) {
+      T x[R], cc[R], xp[R], st[R];
+      if (live) {
+        unpack(g.x[k], x);
+        if (RC) unpack(g.c[k], cc);
+      } else {
+#pragma unroll
+        for (int t = 0; t < R; ++t) x[t] = cc[t] = T(0);
+      }
+      const T vj = g.v[k];
+#pragma unroll
+      for (int t = 0; t < R; ++t) {
+        T e = T(0), tv;
+        if (RC) {
+          e = a.rho * cc[t];
+          if (MODE == kPlain1)
+            tv = ((x[t] - e) + ph[t]) + vj;
+          else
+            tv = ((x[t] + ph[t]) + vj) - e;
+        } else {
+          tv = (x[t] + ph[t]) + vj;
+        }
+        T p = tv > T(0) ? tv : T(0);
+        const bool valid = !MASK || t < nvalid;
+        if (MASK && !valid) {
+          p = T(0);
+          tv = T(0);
+        }
+        xp[t] = p;
+        st[t] = (MODE == kFold) ? p - e : p;
+        u[t] += p;
+        if (RC) {
+          acc.cost = fma(cc[t], p, acc.cost);
+          acc.prev = fma(cc[t], x[t], acc.prev);
+          if (DUAL) {
+            T d = (ph[t] + vj) - e;
+            d = d > T(0) ? d : T(0);
+            if (MASK && !valid) d = T(0);
+            acc.dual = fma(d, d, acc.dual);
+          }
+        }
+        if (DX) {
+          const T dd = p - x[t];
+          acc.dx = fma(dd, dd, acc.dx);
+        }
+        const T at = fabs(tv);
+        acc.mx = fmax(acc.mx, at);
+        acc.bad |= !(at <= max_finite<T>());
+      }
+      if (live) {
+        const int64_t off = (j + k) * a.ld + row0;
+        __stcs(reinterpret_cast<V*>(a.xy + off), pack4(st));
+      }
+      *reinterpret_cast<V*>(wbuf + (c * 32 + (lane ^ (c & 7))) * R) = pack4(xp);
+    }
+  }
+}
+
+template <class T, int MODE, bool DUAL, bool DX, bool MASK, int G>
+__device__ __forceinline__ void pass_tile(const PassArgs<T>& a, int64_t c0, int64_t c1,
+                                          int64_t wrow0, int64_t row0, int nvalid,
+                                          const T (&ph)[16 / sizeof(T)],
+                                          T (&u)[16 / sizeof(T)], PassAcc<T>& acc,
+                                          T* wbuf, int lane) {
   using V = typename V16<T>::type;
   constexpr int R = 16 / sizeof(T);
   constexpr int ROWS_W = 32 * R;
   constexpr int NB = ROWS_W / kVBlockRows;
   constexpr int CH = kChunkCols;
+  constexpr int NG = CH / G;
+  static_assert(NG % 2 == 0, "groups per chunk must be even (ping-pong)");
+  const bool live = !MASK || nvalid > 0;
+  ColGroup<T, G> A, B;
+#pragma unroll
+  for (int k = 0; k < G; ++k) {
+    A.x[k] = B.x[k] = A.c[k] = B.c[k] = vzero<T>();
+    A.v[k] = B.v[k] = T(0);
+  }
+  load_group<T, MODE, G>(a, A, c0, c1, row0, live);
+  for (int64_t j0 = c0; j0 < c1; j0 += CH) {
+#pragma unroll
+    for (int gi = 0; gi < NG; gi += 2) {
+      load_group<T, MODE, G>(a, B, j0 + (gi + 1) * G, c1, row0, live);
+      compute_group<T, MODE, DUAL, DX, MASK, G>(a, A, j0 + gi * G, gi * G, c1, row0,
+                                                nvalid, ph, u, acc, wbuf, lane);
+      load_group<T, MODE, G>(a, A, j0 + (gi + 2) * G, c1, row0, live);
+      compute_group<T, MODE, DUAL, DX, MASK, G>(a, B, j0 + (gi + 1) * G, (gi + 1) * G,
+                                                c1, row0, nvalid, ph, u, acc, wbuf, lane);
+    }
+    // v-phase: lane (c, b) sums the 64 rows of block b of column c in order
+    __syncwarp();
+    const int cnt = static_cast<int>(imin64(CH, c1 - j0));
+    if (lane < CH * NB) {
+      const int c = lane % CH, b = lane / CH;
+      const int64_t gb = wrow0 / kVBlockRows + b;
+      if (c < cnt && gb * kVBlockRows < a.m) {
+        const V* col = reinterpret_cast<const V*>(wbuf) + c * 32;
+        const int g7 = c & 7;
+        constexpr int QB = kVBlockRows / R;  // chunks per 64-row block
+        T s = T(0);
+#pragma unroll
+        for (int qq = 0; qq < QB; ++qq) {
+          T v4[R];
+          unpack(col[(b * QB + qq) ^ g7], v4);
+#pragma unroll
+          for (int t = 0; t < R; ++t) s += v4[t];
+        }
+        a.vstrip[gb * a.n + j0 + c] = s;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+#ifndef DROTB_PASS_G
+#define DROTB_PASS_G 4  // columns per load group (two groups in flight)
+#endif
+#ifndef DROTB_PASS_MINB
+#define DROTB_PASS_MINB 4  // resident CTAs per SM the register budget targets
+#endif
+
+template <class T, int MODE, bool DUAL, bool DX>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_PASS_MINB)
+    pass_kernel(const PassArgs<T> a) {
+  using V = typename V16<T>::type;
+  constexpr int R = 16 / sizeof(T);
+  constexpr int ROWS_W = 32 * R;
+  constexpr int CH = kChunkCols;
+  constexpr int G = DROTB_PASS_G;
   __shared__ __align__(16) T sbuf[kWarpsPerCta][CH * ROWS_W];
   __shared__ PassAcc<T> wacc[kWarpsPerCta];
   if (a.stop != nullptr && *reinterpret_cast<const volatile int*>(a.stop)) return;
@@ -272,8 +328,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
   const int64_t row0 = wrow0 + static_cast<int64_t>(lane) * R;
   const int64_t gc = blockIdx.y;
   const int64_t c0 = gc * a.tc;
-  const int64_t c1 = min(a.n, c0 + a.tc);
-  int64_t nv = a.m - row0;
+  const int64_t c1 = imin64(a.n, c0 + a.tc);
+  const int64_t nv = a.m - row0;
   const int nvalid = nv <= 0 ? 0 : (nv >= R ? R : static_cast<int>(nv));
   T* wbuf = sbuf[warp];
 
@@ -288,28 +344,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
   for (int t = 0; t < R; ++t) u[t] = T(0);
   PassAcc<T> acc{T(0), T(0), T(0), T(0), T(0), false};
 
-  for (int64_t j0 = c0; j0 < c1; j0 += CH) {
-    const int cnt = static_cast<int>(imin64(CH, c1 - j0));
-    if (nvalid == R)
-      pass_chunk<T, MODE, DUAL, DX, false>(a, j0, cnt, row0, nvalid, ph, u, acc,
+  if (__all_sync(0xffffffffu, nvalid == R))
+    pass_tile<T, MODE, DUAL, DX, false, G>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc,
                                            wbuf, lane);
-    else
-      pass_chunk<T, MODE, DUAL, DX, true>(a, j0, cnt, row0, nvalid, ph, u, acc,
+  else
+    pass_tile<T, MODE, DUAL, DX, true, G>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc,
                                           wbuf, lane);
-    __syncwarp();
-    if (lane < CH * NB) {
-      const int c = lane % CH, b = lane / CH;
-      const int64_t gb = wrow0 / kVBlockRows + b;
-      if (c < cnt && gb * kVBlockRows < a.m) {
-        T s = T(0);
-#pragma unroll 16
-        for (int i = 0; i < kVBlockRows; ++i)
-          s += wbuf[stage_index<T>(c, b * kVBlockRows + i)];
-        a.vstrip[gb * a.n + j0 + c] = s;
-      }
-    }
-    __syncwarp();
-  }
   if (nvalid > 0)
     *reinterpret_cast<V*>(a.ustrip + gc * a.ld + row0) = pack4(u);
 
@@ -377,79 +417,99 @@ void launch_pass(const PassArgs<T>& a, int mode, bool want_dual, bool want_dx,
 // K1x: reference-order tile scalar chains (exact mode only)
 // ---------------------------------------------------------------------------
 // One warp per reference tile (plan_tiles order: gc-major, gr-minor,
-// tiles.cpp:36-45); lanes 0..4 each run one of the serial chains of
-// fused.hpp:269-283 over the tile in j-outer / i-inner order, recomputing
-// x+ bit-identically from the pre-pass array.
+// tiles.cpp:36-45).  The warp walks the tile in the reference's j-outer /
+// i-inner order in chunks of up to kChainChunk elements: all 32 lanes load
+// the chunk coalesced, recompute x+ bit-identically from the pre-pass array
+// and write the per-element terms of fused.hpp:270-280 to shared memory;
+// lanes 0..3 then extend the four serial chains (cost, prev-cost, dual^2,
+// dx^2) in element order.  max|t| and the non-finite flag are order-free.
+constexpr int kChainChunk = 256;
+constexpr int kChainWarps = 4;
+
 template <class T, int MODE, bool DUAL, bool DX>
-__global__ void tile_chain_kernel(const PassArgs<T> a, int64_t bs,
-                                  int64_t grid_rows, int64_t n_tiles,
-                                  PassPartial<T>* tiles) {
+__global__ void __launch_bounds__(kChainWarps * 32)
+    tile_chain_kernel(const PassArgs<T> a, int64_t bs, int64_t grid_rows,
+                      int64_t n_tiles, PassPartial<T>* tiles) {
+  __shared__ T terms[kChainWarps][4][kChainChunk];
   if (a.stop != nullptr && *reinterpret_cast<const volatile int*>(a.stop)) return;
-  const int lane = threadIdx.x & 31;
-  const int64_t tile =
-      static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (tile >= n_tiles || lane >= 5) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t tile = static_cast<int64_t>(blockIdx.x) * kChainWarps + warp;
+  if (tile >= n_tiles) return;
   constexpr bool RC = MODE != kSkip;
   const int64_t gcol = tile / grid_rows, grow = tile % grid_rows;
-  const int64_t r0 = grow * bs, r1 = min(a.m, r0 + bs);
-  const int64_t cb = gcol * a.tc, ce = min(a.n, cb + a.tc);
-  T acc = T(0);
+  const int64_t r0 = grow * bs, r1 = imin64(a.m, r0 + bs);
+  const int64_t cb = gcol * a.tc, ce = imin64(a.n, cb + a.tc);
+  const int64_t rows = r1 - r0;
+  const int64_t total = rows * (ce - cb);
+  T (*tm)[kChainChunk] = terms[warp];
+  T chain = T(0);  // lanes 0..3: cost, prev, dual, dx
+  T mx = T(0);
   bool bad = false;
-  for (int64_t j = cb; j < ce; ++j) {
-    const T vj = a.varphi[j];
-    const T* xc = a.xy + j * a.ld;
-    const T* ccol = a.cost + j * a.ld;
-    for (int64_t i = r0; i < r1; ++i) {
-      const T x = xc[i];
-      const T phi = a.phi[i];
-      T e = T(0), c = T(0), tv;
+  for (int64_t e0 = 0; e0 < total; e0 += kChainChunk) {
+    const int cnt = static_cast<int>(imin64(kChainChunk, total - e0));
+    for (int k = lane; k < cnt; k += 32) {
+      const int64_t e = e0 + k;
+      const int64_t j = cb + e / rows, i = r0 + e % rows;
+      const T x = a.xy[j * a.ld + i];
+      const T phi = a.phi[i], vj = a.varphi[j];
+      T ec = T(0), c = T(0), tv;
       if (RC) {
-        c = ccol[i];
-        e = a.rho * c;
+        c = a.cost[j * a.ld + i];
+        ec = a.rho * c;
         if (MODE == kPlain1)
-          tv = ((x - e) + phi) + vj;
+          tv = ((x - ec) + phi) + vj;
         else
-          tv = ((x + phi) + vj) - e;
+          tv = ((x + phi) + vj) - ec;
       } else {
         tv = (x + phi) + vj;
       }
       const T xp = tv > T(0) ? tv : T(0);
-      switch (lane) {
-        case 0:
-          if (RC) acc += c * xp;
-          break;
-        case 1:
-          if (RC) acc += c * x;
-          break;
-        case 2:
-          if (RC && DUAL) {
-            const T d = (phi + vj) - e;
-            if (d > T(0)) acc += d * d;
-          }
-          break;
-        case 3:
-          if (DX) {
-            const T dx = xp - x;
-            acc += dx * dx;
-          }
-          break;
-        default: {
-          const T at = fabs(tv);
-          if (at > acc) acc = at;
-          if (!(at <= max_finite<T>())) bad = true;
+      T t0 = T(0), t1 = T(0), t2 = T(0), t3 = T(0);
+      if (RC) {
+        t0 = c * xp;
+        t1 = c * x;
+        if (DUAL) {
+          const T d = (phi + vj) - ec;
+          if (d > T(0)) t2 = d * d;
         }
       }
+      if (DX) {
+        const T dx = xp - x;
+        t3 = dx * dx;
+      }
+      tm[0][k] = t0;
+      tm[1][k] = t1;
+      tm[2][k] = t2;
+      tm[3][k] = t3;
+      const T at = fabs(tv);
+      if (at > mx) mx = at;
+      if (!(at <= max_finite<T>())) bad = true;
     }
+    __syncwarp();
+    if (lane < 4) {
+      const T* src = tm[lane];
+      int k = 0;
+      for (; k + 8 <= cnt; k += 8) {
+        T v[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) v[t] = src[k + t];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) chain += v[t];
+      }
+      for (; k < cnt; ++k) chain += src[k];
+    }
+    __syncwarp();
   }
+  mx = warp_max(mx);
+  bad = __any_sync(0xffffffffu, bad);
   PassPartial<T>& o = tiles[tile];
-  switch (lane) {
-    case 0: o.cost = acc; break;
-    case 1: o.prev = acc; break;
-    case 2: o.dual = acc; break;
-    case 3: o.dx = acc; break;
-    default:
-      o.max_abs = acc;
-      o.bad = bad ? 1 : 0;
+  if (lane == 0) o.cost = chain;
+  if (lane == 1) o.prev = chain;
+  if (lane == 2) o.dual = chain;
+  if (lane == 3) o.dx = chain;
+  if (lane == 4) {
+    o.max_abs = mx;
+    o.bad = bad ? 1 : 0;
   }
 }
 
@@ -459,10 +519,10 @@ static void launch_chain_t(const PassArgs<T>& a, int64_t bs,
   const int64_t grid_rows = (a.m + bs - 1) / bs;
   const int64_t grid_cols = (a.n + a.tc - 1) / a.tc;
   const int64_t n_tiles = grid_rows * grid_cols;
-  const int wpb = 4;
-  const unsigned blocks = static_cast<unsigned>((n_tiles + wpb - 1) / wpb);
+  const unsigned blocks =
+      static_cast<unsigned>((n_tiles + kChainWarps - 1) / kChainWarps);
   tile_chain_kernel<T, MODE, DUAL, DX>
-      <<<blocks, wpb * 32, 0, st>>>(a, bs, grid_rows, n_tiles, tiles);
+      <<<blocks, kChainWarps * 32, 0, st>>>(a, bs, grid_rows, n_tiles, tiles);
   count_launch();
 }
 
@@ -512,6 +572,43 @@ __device__ T serial_sum(const T* x, int64_t len) {
   return acc;
 }
 
+// K serial ascending-index chains over len terms, staged through shared
+// memory by the whole block (coalesced loads); chain k is carried by lane 0
+// of warp k, so the K chains advance concurrently.  out[k] (shared) receives
+// the chain totals.  Matches a sequential `acc += term(k, e)` loop bitwise.
+constexpr int kStage = 1024;
+
+template <class T, int K, class F>
+__device__ void staged_chains(int64_t len, F term, T* sbuf /* K*kStage */,
+                              T* out /* K, shared */) {
+  const int tid = threadIdx.x;
+  const bool owner = (tid & 31) == 0 && (tid >> 5) < K;
+  const int kk = tid >> 5;
+  T acc = T(0);
+  for (int64_t base = 0; base < len; base += kStage) {
+    const int cnt = static_cast<int>(imin64(kStage, len - base));
+    for (int e = tid; e < cnt; e += blockDim.x)
+#pragma unroll
+      for (int k = 0; k < K; ++k) sbuf[k * kStage + e] = term(k, base + e);
+    __syncthreads();
+    if (owner) {
+      const T* src = sbuf + kk * kStage;
+      int e = 0;
+      for (; e + 8 <= cnt; e += 8) {
+        T v[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) v[t] = src[e + t];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) acc += v[t];
+      }
+      for (; e < cnt; ++e) acc += src[e];
+    }
+    __syncthreads();
+  }
+  if (owner) out[kk] = acc;
+  __syncthreads();
+}
+
 template <class T>
 __device__ __forceinline__ void erg_update(Book<T>* bk, double value) {
   bk->erg_count += 1;
@@ -527,7 +624,15 @@ __global__ void __launch_bounds__(kTailThreads) merge_kernel(const TailArgs<T> t
   T part[3] = {T(0), T(0), T(0)};  // sum r, sum r^2, sum s^2
   if (idx < t.m) {
     T acc = T(0);
-    for (int64_t g = 0; g < t.grid_cols; ++g) acc += t.ustrip[g * t.ld + idx];
+    int64_t g = 0;
+    for (; g + 8 <= t.grid_cols; g += 8) {
+      T v8[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v8[q] = t.ustrip[(g + q) * t.ld + idx];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc += v8[q];
+    }
+    for (; g < t.grid_cols; ++g) acc += t.ustrip[g * t.ld + idx];
     t.u[idx] = acc;
     const T r = acc - t.p[idx];
     t.r_new[idx] = r;
@@ -536,7 +641,15 @@ __global__ void __launch_bounds__(kTailThreads) merge_kernel(const TailArgs<T> t
   } else if (idx < t.m + t.n) {
     const int64_t j = idx - t.m;
     T acc = T(0);
-    for (int64_t g = 0; g < t.grid_rows64; ++g) acc += t.vstrip[g * t.n + j];
+    int64_t g = 0;
+    for (; g + 8 <= t.grid_rows64; g += 8) {
+      T v8[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v8[q] = t.vstrip[(g + q) * t.n + j];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc += v8[q];
+    }
+    for (; g < t.grid_rows64; ++g) acc += t.vstrip[g * t.n + j];
     t.v[j] = acc;
     const T s = acc - t.q[j];
     t.s_new[j] = s;
@@ -554,29 +667,59 @@ __global__ void __launch_bounds__(kTailThreads) merge_kernel(const TailArgs<T> t
   __shared__ int totbad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (EXACT) {
-    // tile order chains (fused.hpp:322-329) + sequential vec sums
-    if (warp == 0 && lane < 5) {
-      T acc = T(0);
-      int bad = 0;
-      for (int64_t k = 0; k < t.n_tiles; ++k) {
-        const PassPartial<T>& sc = t.tile_partials[k];
-        switch (lane) {
-          case 0: acc += sc.cost; break;
-          case 1: acc += sc.prev; break;
-          case 2: acc += sc.dual; break;
-          case 3: acc += sc.dx; break;
-          default:
-            if (sc.max_abs > acc) acc = sc.max_abs;
-            bad |= sc.bad;
-        }
-      }
-      tot[lane] = acc;
-      if (lane == 4) totbad = bad;
+    // tile-order chains (fused.hpp:322-329) + sequential vec sums
+    // (solver.hpp:273, 475-477)
+    __shared__ double sraw[4 * kStage];
+    __shared__ T chains[4];
+    __shared__ T mxs[32];
+    __shared__ int bads[32];
+    T* sb = reinterpret_cast<T*>(sraw);
+    const PassPartial<T>* tp = t.tile_partials;
+    staged_chains<T, 4>(
+        t.n_tiles,
+        [&](int k, int64_t e) {
+          const PassPartial<T>& sc = tp[e];
+          return k == 0 ? sc.cost : k == 1 ? sc.prev : k == 2 ? sc.dual : sc.dx;
+        },
+        sb, chains);
+    T mx = T(0);
+    int bad = 0;
+    for (int64_t k = tid; k < t.n_tiles; k += blockDim.x) {
+      mx = fmax(mx, tp[k].max_abs);
+      bad |= tp[k].bad;
     }
+    mx = warp_max(mx);
+    bad = __any_sync(0xffffffffu, bad) ? 1 : 0;
+    if (lane == 0) {
+      mxs[warp] = mx;
+      bads[warp] = bad;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      T m2 = T(0);
+      int b2 = 0;
+      for (int w = 0; w < (blockDim.x >> 5); ++w) {
+        m2 = fmax(m2, mxs[w]);
+        b2 |= bads[w];
+      }
+      for (int k = 0; k < 4; ++k) tot[k] = chains[k];
+      tot[4] = m2;
+      totbad = b2;
+    }
+    __syncthreads();
     if (t.solver) {
-      if (warp == 1 && lane == 0) tot[5] = serial_sum<T, false>(t.r_new, t.m);
-      if (warp == 2 && lane == 0) tot[6] = serial_sum<T, true>(t.r_new, t.m);
-      if (warp == 3 && lane == 0) tot[7] = serial_sum<T, true>(t.s_new, t.n);
+      const T* rn = t.r_new;
+      const T* sn = t.s_new;
+      staged_chains<T, 2>(
+          t.m, [&](int k, int64_t e) { const T r = rn[e]; return k == 0 ? r : r * r; }, sb,
+          chains);
+      if (tid == 0) {
+        tot[5] = chains[0];
+        tot[6] = chains[1];
+      }
+      staged_chains<T, 1>(
+          t.n, [&](int, int64_t e) { const T v = sn[e]; return v * v; }, sb, chains);
+      if (tid == 0) tot[7] = chains[0];
     }
     __syncthreads();
   } else {
@@ -739,29 +882,34 @@ __global__ void __launch_bounds__(kTailThreads) update_kernel(const TailArgs<T> 
   if (EXACT) {
     // one serial chain per quantity, in the reference's loop order
     // (solver.hpp:450-465 and :479-486)
-    if (lane == 0 && warp < 6) {
-      double acc = 0;
+    __shared__ double sb[2 * kStage];
+    __shared__ double chains[2];
+    const double* tv = t.terms;
+    staged_chains<double, 2>(
+        mn, [&](int k, int64_t e) { return k == 0 ? tv[e] : tv[2 * mn + e]; }, sb, chains);
+    if (tid == 0) {
+      tot[0] = chains[0];
+      tot[5] = fp ? chains[1] : 0.0;
+    }
+    if (fp) {
       const double* d = t.terms + mn;
-      switch (warp) {
-        case 0:
-          for (int64_t k = 0; k < mn; ++k) acc += t.terms[k];
-          break;
-        case 1:
-          if (fp) for (int64_t k = 0; k < t.m; ++k) acc += d[k] * d[k];
-          break;
-        case 2:
-          if (fp) for (int64_t k = 0; k < t.m; ++k) acc += d[k];
-          break;
-        case 3:
-          if (fp) for (int64_t k = t.m; k < mn; ++k) acc += d[k] * d[k];
-          break;
-        case 4:
-          if (fp) for (int64_t k = t.m; k < mn; ++k) acc += d[k];
-          break;
-        default:
-          if (fp) for (int64_t k = 0; k < mn; ++k) acc += t.terms[2 * mn + k];
+      staged_chains<double, 2>(
+          t.m, [&](int k, int64_t e) { const double x = d[e]; return k == 0 ? x * x : x; },
+          sb, chains);
+      if (tid == 0) {
+        tot[1] = chains[0];
+        tot[2] = chains[1];
       }
-      tot[warp] = acc;
+      staged_chains<double, 2>(
+          t.n,
+          [&](int k, int64_t e) { const double x = d[t.m + e]; return k == 0 ? x * x : x; },
+          sb, chains);
+      if (tid == 0) {
+        tot[3] = chains[0];
+        tot[4] = chains[1];
+      }
+    } else if (tid == 0) {
+      tot[1] = tot[2] = tot[3] = tot[4] = 0.0;
     }
     __syncthreads();
   } else {
@@ -812,13 +960,16 @@ __global__ void __launch_bounds__(kTailThreads) update_kernel(const TailArgs<T> 
     }
     bk->trace_rows += 1;
   }
-  if (check && r_primal * bk->primal_scale <= bk->tol_primal &&
-      bk->last_r_dual <= bk->tol_dual && gap * gap_scale <= bk->tol_gap) {
+  const bool fire = check && r_primal * bk->primal_scale <= bk->tol_primal &&
+                    bk->last_r_dual <= bk->tol_dual && gap * gap_scale <= bk->tol_gap;
+  if (fire) {
     bk->confirm = 1;
     bk->gate_hits += 1;
   } else if (k + 1 >= bk->max_iters) {
     bk->stop = 1;
   }
+  // the confirm report runs only when the gate fires (graph IF node)
+  if (t.use_cond) cudaGraphSetConditional(t.cond, fire ? 1u : 0u);
 }
 
 template <class T>
@@ -865,17 +1016,35 @@ __global__ void __launch_bounds__(kTailThreads)
   const double drho = static_cast<double>(t.rho);
   double part[2] = {0, 0};
   if (EXACT) {
-    // single serial chain in storage order (solver.hpp:322-337)
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      for (int64_t j = 0; j < t.n; ++j) {
-        const double nu_j = static_cast<double>(t.varphi[j]) / drho;
-        const T* xc = xy + j * t.ld;
-        const T* cc = cost + j * t.ld;
-        for (int64_t i = 0; i < t.m; ++i)
-          report_elem<T>(xc[i], cc[i], t.phi[i], nu_j, drho, t.rho, folded,
-                         part[0], part[1]);
-      }
-    }
+    // two serial double chains in storage order (solver.hpp:322-337),
+    // staged: terms are formed in parallel, then added in order
+    __shared__ double sb[2 * kStage];
+    __shared__ double chains[2];
+    const int64_t m = t.m;
+    const T rho = t.rho;
+    const T* ph = t.phi;
+    const T* vp = t.varphi;
+    const int64_t ld = t.ld;
+    staged_chains<double, 2>(
+        t.m * t.n,
+        [&](int k, int64_t e) {
+          const int64_t j = e / m, i = e - j * m;
+          const double c = static_cast<double>(cost[j * ld + i]);
+          if (k == 0) {
+            double x = static_cast<double>(xy[j * ld + i]);
+            if (folded) {
+              x += static_cast<double>(rho) * c;
+              if (x < 0) x = 0;
+            }
+            return c * x;
+          }
+          const double nu_j = static_cast<double>(vp[j]) / drho;
+          const double slack = static_cast<double>(ph[i]) / drho + nu_j - c;
+          return slack > 0 ? slack * slack : 0.0;
+        },
+        sb, chains);
+    part[0] = chains[0];
+    part[1] = chains[1];
   } else {
     // blocks stride over columns, threads over rows
     for (int64_t j = blockIdx.x; j < t.n; j += gridDim.x) {
@@ -928,7 +1097,7 @@ void launch_report(const T* xy, const T* cost, const TailArgs<T>& t,
   if (exact) {
     report_kernel<T, true><<<1, kTailThreads, 0, st>>>(xy, cost, t, always ? 1 : 0);
   } else {
-    const int64_t blocks = imin64(t.n, 148 * 8);
+    const int64_t blocks = imin64(t.n, 148 * 2);
     report_kernel<T, false>
         <<<static_cast<unsigned>(blocks), kTailThreads, 0, st>>>(xy, cost, t,
                                                                  always ? 1 : 0);

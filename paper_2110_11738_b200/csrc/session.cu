@@ -111,14 +111,14 @@ struct Session {
   bool want_dual = true, want_dx = true, gate = true;
   int64_t h_iter = 0;
   bool h_folded = false;
-  cudaGraphExec_t pair_exec = nullptr;
-  int64_t launches_per_pair = 0;
 
-  ~Session() { release(); }
+  ~Session() {
+    drop_graphs();
+    for (auto e : tev) cudaEventDestroy(e);
+    release();
+  }
 
   void release() {
-    if (pair_exec) cudaGraphExecDestroy(pair_exec);
-    pair_exec = nullptr;
     void* bufs[] = {X, C, Xout, phi, varphi, a, b, rb[0], rb[1], sb[0], sb[1],
                     p, q, u, v, ustrip, vstrip, tscr, partials, tiles, dscr,
                     terms, book, trace, vflags};
@@ -142,7 +142,7 @@ struct Session {
     own_stream = false;
   }
 
-  int create(int64_t m_, int64_t n_, const drotb_config& c) {
+  int create(int64_t m_, int64_t n_, const drotb_config& c, bool engine = false) {
     if (m_ <= 0 || n_ <= 0)
       return set_error(DROTB_ERRC_EMPTY_DIMENSION, "cost matrix has an empty dimension");
     cfg = c;
@@ -155,7 +155,21 @@ struct Session {
     exact = cfg.order == DROTB_ORDER_REFERENCE;
     bs = std::max<int64_t>(1, cfg.block_rows);
     tc = bs * std::max<int64_t>(1, cfg.work_size);
+    if (!exact && !engine) tc = fast_tile_cols();
     return allocate();
+  }
+
+  // Fast order is free to pick the u-strip width: enough column tiles for
+  // ~6 waves of 4 CTAs on each of the 148 SMs (wave-quantization and
+  // latency), in multiples of the 16-column staging chunk, at most 256.
+  int64_t fast_tile_cols() const {
+    constexpr int R = 16 / sizeof(T);
+    const int64_t rows_cta = int64_t(kWarpsPerCta) * 32 * R;
+    const int64_t row_ctas = (m + rows_cta - 1) / rows_cta;
+    const int64_t target = 148 * 4 * 6;
+    const int64_t col_tiles = std::max<int64_t>(1, (target + row_ctas - 1) / row_ctas);
+    const int64_t w = round_up((n + col_tiles - 1) / col_tiles, kChunkCols);
+    return std::min<int64_t>(256, std::max<int64_t>(kChunkCols, w));
   }
 
   int allocate() {
@@ -168,7 +182,7 @@ struct Session {
     tile_grid_rows = (m + bs - 1) / bs;
     n_tiles = tile_grid_rows * grid_cols;
     tail_blocks = (m + n + 255) / 256;
-    report_blocks = std::min<int64_t>(n, 148 * 8);
+    report_blocks = std::min<int64_t>(n, 148 * 2);
     const size_t mat = static_cast<size_t>(ld) * static_cast<size_t>(n);
     RC_TRY(dev_alloc(&X, mat));
     RC_TRY(dev_alloc(&C, mat));
@@ -206,8 +220,7 @@ struct Session {
   }
 
   int set_stream(void* s) {
-    if (pair_exec) cudaGraphExecDestroy(pair_exec);
-    pair_exec = nullptr;
+    drop_graphs();
     if (own_stream && stream) {
       CUDA_TRY(cudaStreamSynchronize(stream));
       cudaStreamDestroy(stream);
@@ -457,54 +470,158 @@ struct Session {
 
   // One solve-loop iteration: step_impl (solver.hpp:238-307) + the
   // bookkeeping and gate of solve (solver.hpp:406-521).
-  int enqueue_iteration() {
+  int enqueue_iteration(cudaEvent_t pass_begin = nullptr,
+                        cudaEvent_t pass_end = nullptr, int* mode_out = nullptr,
+                        unsigned long long* cond_out = nullptr,
+                        TailArgs<T>* report_args = nullptr) {
     const int64_t k = h_iter;
     int mode;
     bool folded_after;
     RC_TRY(pass_mode(k, h_folded, &mode, &folded_after));
+    if (mode_out) *mode_out = mode;
     PassArgs<T> pa = pass_args();
     if (exact) launch_tile_chains<T>(pa, mode, want_dual, want_dx, bs, tiles, stream);
+    if (pass_begin) CUDA_TRY(cudaEventRecord(pass_begin, stream));
     launch_pass<T>(pa, mode, want_dual, want_dx, stream);
+    if (pass_end) CUDA_TRY(cudaEventRecord(pass_end, stream));
     TailArgs<T> ta = tail_args(k, mode, folded_after, true);
     launch_merge<T>(ta, exact, stream);
-    launch_update<T>(ta, exact, stream);
-    if (gate) launch_report<T>(X, C, ta, exact, false, stream);
+    if (cond_out) {  // graph build: the report goes into an IF node body
+      ta.cond = *cond_out;
+      ta.use_cond = 1;
+      launch_update<T>(ta, exact, stream);
+      *report_args = ta;
+    } else {
+      launch_update<T>(ta, exact, stream);
+      if (gate) launch_report<T>(X, C, ta, exact, false, stream);
+    }
     h_iter = k + 1;
     h_folded = folded_after;
     return 0;
   }
 
-  int capture_pair() {
-    if (pair_exec) return 0;
+  // Graph of n_iters (even) iterations from an even, unfolded state: per
+  // iteration the sweep, merge and update kernels, then an IF node whose
+  // body (the exact confirm report) runs only when the update kernel's gate
+  // fired.  Optional timing events bracket the graph and every sweep.
+  int build_graph(int64_t n_iters, bool timed, cudaGraphExec_t* exec_out,
+                  int64_t* launches_out) {
     const int64_t save_iter = h_iter;
     const bool save_folded = h_folded;
     const int64_t before = kernel_launch_count();
-    cudaGraph_t graph = nullptr;
-    CUDA_TRY(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-    int rc = enqueue_iteration();
-    if (!rc) rc = enqueue_iteration();
-    cudaError_t e = cudaStreamEndCapture(stream, &graph);
-    if (rc) {
-      if (graph) cudaGraphDestroy(graph);
-      return rc;
+    if (timed) RC_TRY(ensure_events(static_cast<size_t>(2 * n_iters + 2)));
+    cudaGraph_t g = nullptr;
+    CUDA_TRY(cudaGraphCreate(&g, 0));
+    std::unique_ptr<CUgraph_st, decltype(&cudaGraphDestroy)> hold(g, &cudaGraphDestroy);
+    std::vector<cudaGraphNode_t> deps;
+    const cudaStreamCaptureMode cm = cudaStreamCaptureModeThreadLocal;
+    int rc = 0;
+    for (int64_t it = 0; it < n_iters && rc == 0; ++it) {
+      cudaGraphConditionalHandle h = 0;
+      if (gate) CUDA_TRY(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+      CUDA_TRY(cudaStreamBeginCaptureToGraph(stream, g, deps.empty() ? nullptr : deps.data(),
+                                             nullptr, deps.size(), cm));
+      if (timed && it == 0) CUDA_TRY(cudaEventRecord(tev[0], stream));
+      TailArgs<T> ra;
+      unsigned long long hv = static_cast<unsigned long long>(h);
+      rc = enqueue_iteration(timed ? tev[2 + 2 * it] : nullptr,
+                             timed ? tev[3 + 2 * it] : nullptr, nullptr,
+                             gate ? &hv : nullptr, &ra);
+      if (timed && it + 1 == n_iters && !gate) CUDA_TRY(cudaEventRecord(tev[1], stream));
+      cudaStreamCaptureStatus cs;
+      const cudaGraphNode_t* d = nullptr;
+      size_t nd = 0;
+      CUDA_TRY(cudaStreamGetCaptureInfo(stream, &cs, nullptr, nullptr, &d, &nd));
+      deps.assign(d, d + nd);
+      cudaGraph_t tmp;
+      CUDA_TRY(cudaStreamEndCapture(stream, &tmp));
+      if (rc || !gate) continue;
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = h;
+      cp.conditional.type = cudaGraphCondTypeIf;
+      cp.conditional.size = 1;
+      cudaGraphNode_t cn;
+      CUDA_TRY(cudaGraphAddNode(&cn, g, deps.data(), deps.size(), &cp));
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      CUDA_TRY(cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0, cm));
+      launch_report<T>(X, C, ra, exact, false, stream);
+      CUDA_TRY(cudaStreamEndCapture(stream, &tmp));
+      deps.assign(1, cn);
+      if (timed && it + 1 == n_iters) {
+        CUDA_TRY(cudaStreamBeginCaptureToGraph(stream, g, deps.data(), nullptr, deps.size(), cm));
+        CUDA_TRY(cudaEventRecord(tev[1], stream));
+        CUDA_TRY(cudaStreamEndCapture(stream, &tmp));
+      }
     }
-    CUDA_TRY(e);
-    CUDA_TRY(cudaGraphInstantiate(&pair_exec, graph, 0));
-    cudaGraphDestroy(graph);
-    launches_per_pair = kernel_launch_count() - before;
-    count_launch(-launches_per_pair);  // captured, not launched
     h_iter = save_iter;
     h_folded = save_folded;
+    if (rc) return rc;
+    CUDA_TRY(cudaGraphInstantiate(exec_out, g, 0));
+    *launches_out = kernel_launch_count() - before;
+    count_launch(-*launches_out);  // captured, not launched
     return 0;
+  }
+
+  int ensure_events(size_t need) {
+    while (tev.size() < need) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreate(&e));
+      tev.push_back(e);
+    }
+    return 0;
+  }
+
+  // cached graphs: batch graphs (untimed) and timed graphs, keyed by length
+  std::vector<std::pair<int64_t, cudaGraphExec_t>> graphs, tgraphs;
+  std::vector<int64_t> graph_launches, tgraph_launches;
+
+  int get_graph(int64_t len, bool timed, cudaGraphExec_t* ex, int64_t* nl) {
+    auto& gs = timed ? tgraphs : graphs;
+    auto& ls = timed ? tgraph_launches : graph_launches;
+    for (size_t k = 0; k < gs.size(); ++k)
+      if (gs[k].first == len) {
+        *ex = gs[k].second;
+        *nl = ls[k];
+        return 0;
+      }
+    RC_TRY(build_graph(len, timed, ex, nl));
+    gs.emplace_back(len, *ex);
+    ls.push_back(*nl);
+    return 0;
+  }
+
+  void drop_graphs() {
+    for (auto& g : graphs) cudaGraphExecDestroy(g.second);
+    for (auto& g : tgraphs) cudaGraphExecDestroy(g.second);
+    graphs.clear();
+    tgraphs.clear();
+    graph_launches.clear();
+    tgraph_launches.clear();
+  }
+
+  bool graph_ok(int64_t len) const {
+    return cfg.use_graphs && len >= 2 && (len & 1) == 0 && (h_iter & 1) == 0 && !h_folded;
   }
 
   int enqueue(int64_t n_iters) {
     if (!initialized) return set_error(DROTB_ERRC_BAD_CONFIG, "session not initialized");
+    const int64_t bi = batch_iters();
     while (n_iters > 0) {
-      if (cfg.use_graphs && n_iters >= 2 && (h_iter & 1) == 0 && !h_folded) {
-        RC_TRY(capture_pair());
-        CUDA_TRY(cudaGraphLaunch(pair_exec, stream));
-        count_launch(launches_per_pair);
+      if (n_iters >= bi && graph_ok(bi)) {
+        cudaGraphExec_t ex;
+        int64_t nl;
+        RC_TRY(get_graph(bi, false, &ex, &nl));
+        CUDA_TRY(cudaGraphLaunch(ex, stream));
+        count_launch(nl);
+        h_iter += bi;
+        n_iters -= bi;
+      } else if (n_iters >= 2 && graph_ok(2)) {
+        cudaGraphExec_t ex;
+        int64_t nl;
+        RC_TRY(get_graph(2, false, &ex, &nl));
+        CUDA_TRY(cudaGraphLaunch(ex, stream));
+        count_launch(nl);
         h_iter += 2;
         n_iters -= 2;
       } else {
@@ -513,6 +630,58 @@ struct Session {
       }
     }
     CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
+
+  // Eager run of exactly n_iters iterations bracketed by CUDA events on the
+  // session stream, with an event pair around every fused-sweep launch:
+  // the live measurement behind bench.py's value and roofline.
+  std::vector<cudaEvent_t> tev;
+  int run_timed(int64_t n_iters, double* total_ms, double* pass_ms,
+                int64_t* n_pass, double* pass_bytes, int64_t* launches) {
+    if (!initialized) return set_error(DROTB_ERRC_BAD_CONFIG, "session not initialized");
+    RC_TRY(ensure_events(static_cast<size_t>(2 * n_iters + 2)));
+    const int64_t before = kernel_launch_count();
+    std::vector<int> modes(static_cast<size_t>(n_iters));
+    {  // modes of the iterations about to run (host-side symbolic state)
+      int64_t k = h_iter;
+      bool f = h_folded;
+      for (int64_t it = 0; it < n_iters; ++it, ++k) {
+        bool fa;
+        RC_TRY(pass_mode(k, f, &modes[it], &fa));
+        f = fa;
+      }
+    }
+    if (graph_ok(n_iters)) {
+      cudaGraphExec_t ex;
+      int64_t nl;
+      RC_TRY(get_graph(n_iters, true, &ex, &nl));
+      CUDA_TRY(cudaGraphLaunch(ex, stream));
+      count_launch(nl);
+      h_iter += n_iters;
+    } else {
+      CUDA_TRY(cudaEventRecord(tev[0], stream));
+      for (int64_t it = 0; it < n_iters; ++it)
+        RC_TRY(enqueue_iteration(tev[2 + 2 * it], tev[3 + 2 * it]));
+      CUDA_TRY(cudaEventRecord(tev[1], stream));
+    }
+    CUDA_TRY(cudaEventSynchronize(tev[1]));
+    CUDA_TRY(cudaGetLastError());
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, tev[0], tev[1]));
+    double psum = 0, bsum = 0;
+    const double cells = static_cast<double>(m) * static_cast<double>(n);
+    for (int64_t it = 0; it < n_iters; ++it) {
+      float pm = 0;
+      CUDA_TRY(cudaEventElapsedTime(&pm, tev[2 + 2 * it], tev[3 + 2 * it]));
+      psum += pm;
+      bsum += (modes[it] == kSkip ? 2.0 : 3.0) * sizeof(T) * cells;
+    }
+    if (total_ms) *total_ms = ms;
+    if (pass_ms) *pass_ms = psum;
+    if (n_pass) *n_pass = n_iters;
+    if (pass_bytes) *pass_bytes = bsum;
+    if (launches) *launches = kernel_launch_count() - before;
     return 0;
   }
 
@@ -998,11 +1167,11 @@ int drotb_engine_create(drotb_engine** eng, int64_t m, int64_t n,
     std::unique_ptr<drotb_engine> e(new drotb_engine{precision, nullptr});
     if (precision == 0) {
       std::unique_ptr<Session<float>> s(new Session<float>());
-      RC_TRY(s->create(m, n, cfg));
+      RC_TRY(s->create(m, n, cfg, true));
       e->impl = s.release();
     } else {
       std::unique_ptr<Session<double>> s(new Session<double>());
-      RC_TRY(s->create(m, n, cfg));
+      RC_TRY(s->create(m, n, cfg, true));
       e->impl = s.release();
     }
     *eng = e.release();
@@ -1202,6 +1371,13 @@ int drotb_session_pass_bytes(drotb_session* s, double* bytes_fold,
   if (bytes_fold) *bytes_fold = 3.0 * sz * cells;  // read X, C; write X
   if (bytes_skip) *bytes_skip = 2.0 * sz * cells;  // read X; write X
   return 0;
+}
+
+int drotb_session_run_timed(drotb_session* s, int64_t n_iters, double* total_ms,
+                            double* pass_ms, int64_t* n_pass, double* pass_bytes,
+                            int64_t* launches) {
+  drotb::clear_error();
+  return DROTB_DISPATCH(s, run_timed(n_iters, total_ms, pass_ms, n_pass, pass_bytes, launches));
 }
 
 int drotb_nccl_unique_id(char* out128) {

@@ -56,9 +56,8 @@ class Session:
 
     def set_problem(self, cost: np.ndarray, p: np.ndarray, q: np.ndarray):
         dt = self.dtype
-        cm = _cm(cost, dt)
-        _check(_lib.load().drotb_session_set_problem(
-            self._h, _p(cm), _p(_vec(p, dt)), _p(_vec(q, dt)), 0))
+        cm, pv, qv = _cm(cost, dt), _vec(p, dt), _vec(q, dt)  # alive across the call
+        _check(_lib.load().drotb_session_set_problem(self._h, _p(cm), _p(pv), _p(qv), 0))
 
     def set_problem_device(self, cost_ptr: int, p_ptr: int, q_ptr: int):
         _check(_lib.load().drotb_session_set_problem(self._h, cost_ptr, p_ptr, q_ptr, 1))
@@ -98,6 +97,17 @@ class Session:
         a, b = C.c_double(0), C.c_double(0)
         _check(_lib.load().drotb_session_pass_bytes(self._h, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+    def run_timed(self, iters: int) -> dict:
+        """Exactly `iters` eager iterations with CUDA events around the whole
+        region and around every fused-sweep launch (bench.py's live timing)."""
+        tot, pms, pb = C.c_double(0), C.c_double(0), C.c_double(0)
+        npass, launches = C.c_int64(0), C.c_int64(0)
+        _check(_lib.load().drotb_session_run_timed(
+            self._h, int(iters), C.byref(tot), C.byref(pms), C.byref(npass), C.byref(pb),
+            C.byref(launches)))
+        return dict(total_ms=tot.value, pass_ms=pms.value, n_pass=npass.value,
+                    pass_bytes=pb.value, launches=launches.value)
 
     def device_xy(self) -> int:
         return _lib.load().drotb_session_device_xy(self._h)

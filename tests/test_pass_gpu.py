@@ -59,8 +59,10 @@ SCALARS = ["cost_dot", "prev_cost_dot", "dual_sq", "dx_sq", "max_abs"]
 FLAGS = ["cost_valid", "prev_cost_valid", "dual_valid", "dx_valid", "nonfinite"]
 
 
-def assert_match(out, x, r, bs, exact_scalars=True, vtol=1e-12):
+def assert_match(out, x, r, bs, exact_scalars=True, vtol=None):
     m, n = x.shape
+    if vtol is None:
+        vtol = 1e-12 if x.dtype == F64 else 2e-6
     np.testing.assert_array_equal(x.ravel(order="F"), r["xy"])
     np.testing.assert_array_equal(out.row_sums, r["row_sums"])
     if bs == 64:
