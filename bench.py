@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""bench.py -- DROT iterations/s and HBM GB/s at m = n = 10 000 fp32.
+
+Metric (BASELINE.json): "DROT iters/sec & HBM GB/s (m=n=10k fp32);
+time-to-1e-4 at 1/2/4/8 GPU".  One *step* is one DROT iteration of the
+reference's solve loop (solver.hpp:406-521): the fused sweep over X (and C
+on C-reading passes), the strip merge and recursions, the gate and -- when
+the gate fires -- the exact confirm report.  Workload = config C2 (SURVEY
+§8(d)): gen_gaussian_problem(m=n=10000, sigma_t=5, seed 0) cast to fp32,
+dyadic-uniform marginals (the fp32 inputs the reference's simplex check
+accepts), rho0 = 2, tol 1e-4, skip_cost and record_trace on
+(the reference defaults).
+
+  python bench.py [--gpus N --steps K --warmup W]          # B200 arm
+  python bench.py --impl reference [--steps K --warmup W]  # reference CPU arm
+
+Under torchrun (N > 1) every rank runs its own 10k x 10k instance
+(weak scaling, one process per GPU); rank 0 prints the JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DROT iterations/s (m=n=10000 fp32, Gaussian squared-Euclidean cost)"
+UNIT = "iter/s"
+
+
+def workload_config(m, n, order, extra=None):
+    cfg = {
+        "workload": f"C2: m=n={m} fp32 DROT solve loop on gen_gaussian_problem(seed=0, "
+                    "sigma_t=5) cost, dyadic-uniform marginals, rho0=2, tol 1e-4, "
+                    "skip_cost=true, record_trace=true (reference defaults)",
+        "m": m, "n": n, "reduction_order": order,
+        "l2_policy": "inputs larger than L2 (X + C = %.0f MB vs 126 MB L2)" % (8.0 * m * n / 1e6),
+    }
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+# ---------------------------------------------------------------------------
+# clocks (B200_PROFILING.md: sample nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + self.Q,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_hbm_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(m, n, dtype):
+    """DRAM bytes per sweep launch from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_pass_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        key = f"{m}x{n}_{dtype}"
+        return d[key]["dram_bytes_per_launch_avg"]
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# reference CPU timing (oracle/_ref: the unmodified reference, compiled here)
+# ---------------------------------------------------------------------------
+def reference_problem(m, n):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from pyoracle import LIB_PATHS, Oracle, default_config, dyadic_marginal
+    kind = "reference" if os.path.exists(LIB_PATHS["ref"]) else "port"
+    orc = Oracle("ref" if kind == "reference" else "orc")
+    C, _, _ = orc.gen_gaussian(m, n, seed=0)
+    C = C.astype(np.float32)
+    p = dyadic_marginal(m, np.float32)
+    q = dyadic_marginal(n, np.float32)
+    return orc, kind, C, p, q, default_config
+
+
+def reference_iters_per_s(m, n, iters, warm):
+    """Per-iteration wall time of the reference solve<float> loop on all host
+    threads: solve(max_iters=warm) and solve(max_iters=warm+iters) with
+    unreachable tolerances; the difference isolates `iters` iterations."""
+    orc, kind, C, p, q, default_config = reference_problem(m, n)
+    cores = orc.hardware_workers() if kind == "reference" else 1
+    cfg = default_config(tol_primal=-1.0, tol_dual=-1.0, tol_gap=-1.0, record_trace=1)
+    if kind == "reference":
+        spi, tot = orc.time_iters(C, p, q, m, n, iters, cfg)
+        return 1.0 / spi, cores, kind, iters, tot
+    t0 = time.perf_counter()
+    cfg.max_iters = warm
+    orc.solve(C, p, q, m, n, cfg, trace_cap=0)
+    t1 = time.perf_counter()
+    cfg.max_iters = warm + iters
+    orc.solve(C, p, q, m, n, cfg, trace_cap=0)
+    t2 = time.perf_counter()
+    return iters / ((t2 - t1) - (t1 - t0)), cores, kind, iters, t2 - t0
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    m = n = args.size
+    est = 0.3  # s/iter, conservative for 10k^2 fp32 on a multi-core host
+    k = max(1, min(args.steps, int(150 / est)))
+    ips, cores, kind, k_run, total = reference_iters_per_s(m, n, k, 1)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": ips, "unit": UNIT,
+        "n_gpus": world, "steps": k_run, "warmup": 1, "ms_per_step": 1e3 / ips,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (reference gen_gaussian_problem, seed 0)",
+        "config": workload_config(m, n, "reference CPU deterministic tile order"),
+        "cpu_baseline": {"value": ips, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"{k_run} solve-loop iterations (difference of solve(max_iters=1) "
+                                   f"and solve(max_iters={1 + k_run})), {total:.1f} s wall"},
+        "e2e": {"value": ips, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+def run_b200(args, rank, world, local_rank):
+    import torch
+    import paper_2110_11738_b200 as drot
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    m = n = args.size
+    dt = np.float32
+    order = args.order
+    cfg = drot.DrotConfig(order=drot.Order[order], tol_primal=-1.0, max_iters=10 ** 12,
+                          device=local_rank)
+    sess = drot.Session(m, n, dt, cfg)
+    stream = torch.cuda.current_stream(dev)
+    sess.set_stream(stream.cuda_stream)
+    sess.gen_gaussian(5.0, 0, "dyadic")
+    sess.init()
+    # warmup: W iterations (graphs captured, clocks up)
+    w = max(args.warmup, 3)
+    sess.run_timed(w)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize()
+    r = sess.run_timed(args.steps)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+
+    ms = r["total_ms"]
+    if dist is not None:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * args.steps / (ms / 1e3)
+    pass_avg_ms = r["pass_ms"] / r["n_pass"]
+    bytes_avg = r["pass_bytes"] / r["n_pass"]
+    achieved = bytes_avg / (pass_avg_ms / 1e3) / 1e9
+    peak, peak_src = measured_hbm_peak()
+    step_bytes_gbs = r["pass_bytes"] / (r["total_ms"] / 1e3) / 1e9
+    st, it_done, _ = sess.status()
+    sess.close()
+    del sess
+
+    out = None
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": w, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic (gen_gaussian_problem seed 0 regenerated bit-identically on the "
+                    "host, uploaded once; inputs resident in HBM)",
+            "config": workload_config(m, n, order, {
+                "parallelism": f"{world} independent row-complete instances (one per GPU)"
+                if world > 1 else "1 GPU"}),
+            "hbm_gbs_step": step_bytes_gbs,
+            "roofline": {
+                "bound": "hbm", "kernel": "pass_kernel (fused DROT sweep, K1)",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": bytes_avg,
+                "bytes_model": "3*4*m*n on C-reading (fold) sweeps, 2*4*m*n on skip sweeps "
+                               "(SURVEY §8(d)); averaged over the timed launches",
+                "kernel_ms_avg": pass_avg_ms,
+                "kernel_share_of_step": r["pass_ms"] / r["total_ms"],
+                "traffic": ncu_traffic(m, n, "f32"),
+            },
+            "clocks": clk,
+            "gpu_launches": r["launches"],
+        }
+    # ---- e2e through the public API with host buffers -----------------------
+    if not args.no_e2e:
+        e2e = run_e2e(args, drot, torch, m, n, local_rank)
+        if out is not None:
+            out["e2e"] = e2e
+    # ---- CPU baseline (rank 0, N = 1 only) ----------------------------------
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ips, cores, kind, k_run, total = reference_iters_per_s(m, n, args.cpu_iters, 1)
+        out["cpu_baseline"] = {
+            "value": ips, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{k_run} iterations of reference solve<float> on the same 10k x 10k fp32 "
+                      f"instance (difference of solve(max_iters=1) and solve(max_iters="
+                      f"{1 + k_run})), {total:.1f} s wall, {cores} host threads"}
+    # ---- time to tolerance (C1: 1000x1000 fp64, the results-oracle config) --
+    if rank == 0 and not args.no_ttt:
+        out["time_to_tol"] = time_to_tol(drot)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(args, drot, torch, m, n, local_rank):
+    """Same metric through drot.solve() on pinned host buffers: each e2e step
+    is one solve call of S iterations (H2D of C, p, q; S iterations with
+    gating; final report; D2H of plan, duals and trace)."""
+    S = args.e2e_iters
+    prob = drot.gen_gaussian_problem_as(drot.GaussianSpec(m, n, 5.0, 0), np.float32)
+    pin = torch.empty((n, m), dtype=torch.float32, pin_memory=True)
+    cost = pin.numpy().T  # (m, n) column-major view of pinned memory
+    cost[...] = prob.cost
+    p = torch.from_numpy(drot.dyadic_marginal(m, np.float32)).pin_memory().numpy()
+    q = torch.from_numpy(drot.dyadic_marginal(n, np.float32)).pin_memory().numpy()
+    plan = torch.empty((n, m), dtype=torch.float32, pin_memory=True).numpy().T
+    problem = drot.TransportProblem(cost, p, q)
+    cfg = drot.DrotConfig(tol_primal=-1.0, max_iters=S, device=local_rank)
+    times = []
+    for rep in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = drot.solve(problem, cfg, plan_out=plan)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+        assert res.trace.iterations == S
+    t = statistics.median(times[1:])
+    h2d = 4 * m * n + 4 * m + 4 * n
+    d2h = 4 * m * n + 4 * m + 4 * n + 56 * S
+    return {"value": S / t, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h,
+            "step": f"one drot.solve() call of {S} iterations from pinned host buffers "
+                    f"(validation, init, {S} gated iterations, final report, plan/duals/trace "
+                    f"download); median of 2 after 1 warm call, {t*1e3:.1f} ms/call"}
+
+
+def time_to_tol(drot):
+    """C1: 1000x1000 CounterRng(1) cost, uniform marginals,
+    fp64, reference defaults -> reference: 36 041 iterations."""
+    m = n = 1000
+    C = drot.counter_uniform(1, m * n)  # CounterRng(1) in storage order
+    prob = drot.TransportProblem(C.reshape((m, n), order="F"), np.full(m, 1.0 / m),
+                                 np.full(n, 1.0 / n))
+    out = {}
+    for order in ("fast", "reference"):
+        t0 = time.perf_counter()
+        res = drot.solve(prob, drot.DrotConfig(order=drot.Order[order]))
+        t = time.perf_counter() - t0
+        out[order] = {"seconds": t, "iterations": res.trace.iterations,
+                      "status": res.status.name, "objective": res.report.objective}
+    gold = {}
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as f:
+            g = json.load(f)["c1_f64"]
+        gold = {"iterations": g["iterations"], "objective": g["report_float"]["objective"],
+                "seconds_8_threads_build_container": g["wall_s_ref_8threads"]}
+    except Exception:
+        pass
+    return {"config": "C1: m=n=1000 fp64, C=CounterRng(1) uniform, p=q=uniform, tol 1e-4 "
+                      "(reference defaults), 1 GPU, wall clock of drot.solve()",
+            "b200": out, "reference_golden": gold}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--size", type=int, default=10000)
+    ap.add_argument("--order", default="fast", choices=["fast", "reference"])
+    ap.add_argument("--e2e-iters", type=int, default=200)
+    ap.add_argument("--cpu-iters", type=int, default=20)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ttt", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" not in os.environ:
+        world = 1
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+    else:
+        run_b200(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

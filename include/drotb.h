@@ -250,6 +250,11 @@ int drotb_gen_gaussian(int64_t m, int64_t n, double sigma_t, uint64_t seed,
  * matrix. */
 int drotb_gen_gaussian_f32(int64_t m, int64_t n, double sigma_t,
                            uint64_t seed, float* C);
+/* lo + (hi - lo) * CounterRng(seed).next_unit() for outputs 1..count
+ * (rng.hpp:49-57): the reference's random_matrix fixture in storage order
+ * (tests/support/oracles.hpp:128-135), used for the C1 / C3 cost matrices. */
+int drotb_counter_uniform(uint64_t seed, int64_t count, double lo, double hi,
+                          double* out);
 /* Simplex vector of exact dyadic entries k_i * 2^-K summing to exactly 1,
  * as uniform as the format allows (the inputs the reference's 1e-12 simplex
  * check accepts at every size; B200 extension). */

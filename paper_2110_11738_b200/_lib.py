@@ -88,6 +88,7 @@ SIGNATURES = {
     "drotb_check_problem_f64": (C.c_int, [vp, i64, i64, vp, vp]),
     "drotb_gen_gaussian": (C.c_int, [i64, i64, f64, u64, i32, vp, vp, vp]),
     "drotb_gen_gaussian_f32": (C.c_int, [i64, i64, f64, u64, vp]),
+    "drotb_counter_uniform": (C.c_int, [u64, i64, f64, f64, vp]),
     "drotb_dyadic_marginal_f32": (C.c_int, [i64, vp]),
     "drotb_dyadic_marginal_f64": (C.c_int, [i64, vp]),
     "drotb_session_create": (C.c_int, [P(vp), i64, i64, i32, P(drotb_config)]),

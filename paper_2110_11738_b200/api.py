@@ -267,8 +267,10 @@ def check_problem(problem: TransportProblem) -> None:
 
 
 def solve(problem: TransportProblem, cfg: Optional[DrotConfig] = None,
-          x0: Optional[np.ndarray] = None) -> SolveResult:
-    """drot::solve<T> (solver.hpp:372-540) on the B200."""
+          x0: Optional[np.ndarray] = None,
+          plan_out: Optional[np.ndarray] = None) -> SolveResult:
+    """drot::solve<T> (solver.hpp:372-540) on the B200.  plan_out: optional
+    caller-owned (m, n) Fortran-ordered buffer (e.g. pinned) for the plan."""
     cfg = cfg or DrotConfig()
     dt = _dtype_of(problem)
     m, n = problem.m, problem.n
@@ -284,7 +286,13 @@ def solve(problem: TransportProblem, cfg: Optional[DrotConfig] = None,
     cm = _cm(problem.cost, dt)
     pv, qv = _vec(problem.p, dt), _vec(problem.q, dt)
     x0m = None if x0 is None else _cm(x0, dt)
-    plan = np.empty((m, n), dtype=dt, order="F")
+    if plan_out is not None:
+        if plan_out.shape != (m, n) or plan_out.dtype != dt or not plan_out.flags.f_contiguous:
+            raise Error(Errc.bad_config, "bad_config: plan_out must be a Fortran-ordered "
+                        "(m, n) array of the problem dtype")
+        plan = plan_out
+    else:
+        plan = np.empty((m, n), dtype=dt, order="F")
     mu = np.empty(m, dtype=dt)
     nu = np.empty(n, dtype=dt)
     rho = _ctype(dt)(0)
@@ -589,6 +597,19 @@ def gen_gaussian_problem_as(spec: GaussianSpec, dtype) -> TransportProblem:
     p = np.full(spec.m, 1.0 / spec.m).astype(dt)
     q = np.full(spec.n, 1.0 / spec.n).astype(dt)
     return TransportProblem(cost, p, q)
+
+
+def counter_uniform(seed: int, count: int, lo: float = 0.0, hi: float = 1.0) -> np.ndarray:
+    """lo + (hi-lo) * CounterRng(seed).next_unit(), outputs 1..count (rng.hpp:49-57)."""
+    out = np.empty(count, np.float64)
+    _check(_lib.load().drotb_counter_uniform(seed, count, lo, hi, _p(out)))
+    return out
+
+
+def random_matrix(m: int, n: int, seed: int, lo: float = 0.0, hi: float = 1.0) -> np.ndarray:
+    """The reference fixture random_matrix (tests/support/oracles.hpp:128-135),
+    column-major (m, n)."""
+    return counter_uniform(seed, m * n, lo, hi).reshape((m, n), order="F")
 
 
 def dyadic_marginal(length: int, dtype=np.float64) -> np.ndarray:

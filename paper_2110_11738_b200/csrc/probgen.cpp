@@ -21,15 +21,25 @@
 
 namespace drotb {
 
-namespace {
-
-constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+template <class F>
+void parallel_range(int64_t n, F&& fn) {
+  unsigned hc = std::thread::hardware_concurrency();
+  const int64_t nt = std::max<int64_t>(1, std::min<int64_t>(hc ? hc : 1, n / 65536 + 1));
+  std::vector<std::thread> th;
+  for (int64_t t = 0; t < nt; ++t)
+    th.emplace_back([&, t] { fn(n * t / nt, n * (t + 1) / nt); });
+  for (auto& x : th) x.join();
+}
 
 inline uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   return z ^ (z >> 31);
 }
+
+namespace {
+
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
 
 struct Stream {
   uint64_t key, ctr = 0;
@@ -215,6 +225,21 @@ int drotb_gen_gaussian_f32(int64_t m, int64_t n, double sigma_t, uint64_t seed,
                            float* C) {
   drotb::clear_error();
   return drotb::gen_gaussian_cost<float>(m, n, sigma_t, seed, C);
+}
+
+int drotb_counter_uniform(uint64_t seed, int64_t count, double lo, double hi,
+                          double* out) {
+  // lo + (hi - lo) * CounterRng(seed).next_unit() for outputs 1..count
+  // (rng.hpp:49-57; the reference fixture random_matrix, oracles.hpp:128-135)
+  drotb::clear_error();
+  if (count < 0) return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "negative count");
+  drotb::parallel_range(count, [&](int64_t k0, int64_t k1) {
+    for (int64_t k = k0; k < k1; ++k) {
+      const uint64_t z = drotb::mix64(seed + static_cast<uint64_t>(k + 1) * 0x9E3779B97F4A7C15ull);
+      out[k] = lo + (hi - lo) * (static_cast<double>(z >> 11) * 0x1.0p-53);
+    }
+  });
+  return 0;
 }
 
 int drotb_dyadic_marginal_f32(int64_t len, float* out) {

@@ -481,9 +481,10 @@ struct Session {
     if (mode_out) *mode_out = mode;
     PassArgs<T> pa = pass_args();
     if (exact) launch_tile_chains<T>(pa, mode, want_dual, want_dx, bs, tiles, stream);
-    if (pass_begin) CUDA_TRY(cudaEventRecord(pass_begin, stream));
+    // external records: they become event nodes when captured into a graph
+    if (pass_begin) CUDA_TRY(cudaEventRecordWithFlags(pass_begin, stream, cudaEventRecordExternal));
     launch_pass<T>(pa, mode, want_dual, want_dx, stream);
-    if (pass_end) CUDA_TRY(cudaEventRecord(pass_end, stream));
+    if (pass_end) CUDA_TRY(cudaEventRecordWithFlags(pass_end, stream, cudaEventRecordExternal));
     TailArgs<T> ta = tail_args(k, mode, folded_after, true);
     launch_merge<T>(ta, exact, stream);
     if (cond_out) {  // graph build: the report goes into an IF node body
@@ -521,13 +522,15 @@ struct Session {
       if (gate) CUDA_TRY(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
       CUDA_TRY(cudaStreamBeginCaptureToGraph(stream, g, deps.empty() ? nullptr : deps.data(),
                                              nullptr, deps.size(), cm));
-      if (timed && it == 0) CUDA_TRY(cudaEventRecord(tev[0], stream));
+      if (timed && it == 0)
+        CUDA_TRY(cudaEventRecordWithFlags(tev[0], stream, cudaEventRecordExternal));
       TailArgs<T> ra;
       unsigned long long hv = static_cast<unsigned long long>(h);
       rc = enqueue_iteration(timed ? tev[2 + 2 * it] : nullptr,
                              timed ? tev[3 + 2 * it] : nullptr, nullptr,
                              gate ? &hv : nullptr, &ra);
-      if (timed && it + 1 == n_iters && !gate) CUDA_TRY(cudaEventRecord(tev[1], stream));
+      if (timed && it + 1 == n_iters && !gate)
+        CUDA_TRY(cudaEventRecordWithFlags(tev[1], stream, cudaEventRecordExternal));
       cudaStreamCaptureStatus cs;
       const cudaGraphNode_t* d = nullptr;
       size_t nd = 0;
@@ -550,7 +553,7 @@ struct Session {
       deps.assign(1, cn);
       if (timed && it + 1 == n_iters) {
         CUDA_TRY(cudaStreamBeginCaptureToGraph(stream, g, deps.data(), nullptr, deps.size(), cm));
-        CUDA_TRY(cudaEventRecord(tev[1], stream));
+        CUDA_TRY(cudaEventRecordWithFlags(tev[1], stream, cudaEventRecordExternal));
         CUDA_TRY(cudaStreamEndCapture(stream, &tmp));
       }
     }
