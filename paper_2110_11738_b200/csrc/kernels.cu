@@ -19,6 +19,7 @@
 // K1 use explicit fma() because their order is ours anyway.
 #include <cfloat>
 #include <cstdio>
+#include <cstdlib>
 
 #include "drotb_internal.hpp"
 
@@ -175,6 +176,63 @@ __device__ __forceinline__ void load_group(const PassArgs<T>& a, ColGroup<T, G>&
   }
 }
 
+// The elementwise update of one column slice (R rows) and its reductions
+// (fused.hpp:249-284).  c = column index within the 16-column staging chunk.
+template <class T, int MODE, bool DUAL, bool DX, bool MASK>
+__device__ __forceinline__ void compute_col(const PassArgs<T>& a, const T (&x)[16 / sizeof(T)],
+                                            const T (&cc)[16 / sizeof(T)], T vj, int64_t col,
+                                            int c, int64_t row0, int nvalid,
+                                            const T (&ph)[16 / sizeof(T)],
+                                            T (&u)[16 / sizeof(T)], PassAcc<T>& acc, T* wbuf,
+                                            int lane) {
+  using V = typename V16<T>::type;
+  constexpr int R = 16 / sizeof(T);
+  constexpr bool RC = MODE != kSkip;
+  const bool live = !MASK || nvalid > 0;
+  T xp[R], st[R];
+#pragma unroll
+  for (int t = 0; t < R; ++t) {
+    T e = T(0), tv;
+    if (RC) {
+      e = a.rho * cc[t];
+      if (MODE == kPlain1)
+        tv = ((x[t] - e) + ph[t]) + vj;
+      else
+        tv = ((x[t] + ph[t]) + vj) - e;
+    } else {
+      tv = (x[t] + ph[t]) + vj;
+    }
+    T p = tv > T(0) ? tv : T(0);
+    const bool valid = !MASK || t < nvalid;
+    if (MASK && !valid) {
+      p = T(0);
+      tv = T(0);
+    }
+    xp[t] = p;
+    st[t] = (MODE == kFold) ? p - e : p;
+    u[t] += p;
+    if (RC) {
+      acc.cost = fma(cc[t], p, acc.cost);
+      acc.prev = fma(cc[t], x[t], acc.prev);
+      if (DUAL) {
+        T d = (ph[t] + vj) - e;
+        d = d > T(0) ? d : T(0);
+        if (MASK && !valid) d = T(0);
+        acc.dual = fma(d, d, acc.dual);
+      }
+    }
+    if (DX) {
+      const T dd = p - x[t];
+      acc.dx = fma(dd, dd, acc.dx);
+    }
+    const T at = fabs(tv);
+    acc.mx = fmax(acc.mx, at);
+    acc.bad |= !(at <= max_finite<T>());
+  }
+  if (live) __stcs(reinterpret_cast<V*>(a.xy + col * a.ld + row0), pack4(st));
+  *reinterpret_cast<V*>(wbuf + (c * 32 + (lane ^ (c & 7))) * R) = pack4(xp);
+}
+
 template <class T, int MODE, bool DUAL, bool DX, bool MASK, int G>
 __device__ __forceinline__ void compute_group(const PassArgs<T>& a,
                                               const ColGroup<T, G>& g, int64_t j,
@@ -182,67 +240,50 @@ __device__ __forceinline__ void compute_group(const PassArgs<T>& a,
                                               int nvalid, const T (&ph)[16 / sizeof(T)],
                                               T (&u)[16 / sizeof(T)], PassAcc<T>& acc,
                                               T* wbuf, int lane) {
-  using V = typename V16<T>::type;
   constexpr int R = 16 / sizeof(T);
   constexpr bool RC = MODE != kSkip;
   const bool live = !MASK || nvalid > 0;
 #pragma unroll
   for (int k = 0; k < G; ++k) {
-    const int c = cbase + k;
     if (j + k < c1) {
-      T x[R], cc[R], xp[R], st[R];
+      T x[R], cc[R];
+#pragma unroll
+      for (int t = 0; t < R; ++t) x[t] = cc[t] = T(0);
       if (live) {
         unpack(g.x[k], x);
         if (RC) unpack(g.c[k], cc);
-      } else {
+      }
+      compute_col<T, MODE, DUAL, DX, MASK>(a, x, cc, g.v[k], j + k, cbase + k, row0, nvalid,
+                                           ph, u, acc, wbuf, lane);
+    }
+  }
+}
+
+// v-phase: lane (c, b) sums the 64 rows of block b of staged column c in
+// row order (fused.hpp:268) and writes the v strip entry.
+template <class T>
+__device__ __forceinline__ void v_phase(const PassArgs<T>& a, const T* wbuf, int64_t j0,
+                                        int cnt, int64_t wrow0, int lane) {
+  using V = typename V16<T>::type;
+  constexpr int R = 16 / sizeof(T);
+  constexpr int NB = 32 * R / kVBlockRows;
+  constexpr int CH = kChunkCols;
+  if (lane < CH * NB) {
+    const int c = lane % CH, b = lane / CH;
+    const int64_t gb = wrow0 / kVBlockRows + b;
+    if (c < cnt && gb * kVBlockRows < a.m) {
+      const V* col = reinterpret_cast<const V*>(wbuf) + c * 32;
+      const int g7 = c & 7;
+      constexpr int QB = kVBlockRows / R;  // chunks per 64-row block
+      T s = T(0);
 #pragma unroll
-        for (int t = 0; t < R; ++t) x[t] = cc[t] = T(0);
-      }
-      const T vj = g.v[k];
+      for (int qq = 0; qq < QB; ++qq) {
+        T v4[R];
+        unpack(col[(b * QB + qq) ^ g7], v4);
 #pragma unroll
-      for (int t = 0; t < R; ++t) {
-        T e = T(0), tv;
-        if (RC) {
-          e = a.rho * cc[t];
-          if (MODE == kPlain1)
-            tv = ((x[t] - e) + ph[t]) + vj;
-          else
-            tv = ((x[t] + ph[t]) + vj) - e;
-        } else {
-          tv = (x[t] + ph[t]) + vj;
-        }
-        T p = tv > T(0) ? tv : T(0);
-        const bool valid = !MASK || t < nvalid;
-        if (MASK && !valid) {
-          p = T(0);
-          tv = T(0);
-        }
-        xp[t] = p;
-        st[t] = (MODE == kFold) ? p - e : p;
-        u[t] += p;
-        if (RC) {
-          acc.cost = fma(cc[t], p, acc.cost);
-          acc.prev = fma(cc[t], x[t], acc.prev);
-          if (DUAL) {
-            T d = (ph[t] + vj) - e;
-            d = d > T(0) ? d : T(0);
-            if (MASK && !valid) d = T(0);
-            acc.dual = fma(d, d, acc.dual);
-          }
-        }
-        if (DX) {
-          const T dd = p - x[t];
-          acc.dx = fma(dd, dd, acc.dx);
-        }
-        const T at = fabs(tv);
-        acc.mx = fmax(acc.mx, at);
-        acc.bad |= !(at <= max_finite<T>());
+        for (int t = 0; t < R; ++t) s += v4[t];
       }
-      if (live) {
-        const int64_t off = (j + k) * a.ld + row0;
-        __stcs(reinterpret_cast<V*>(a.xy + off), pack4(st));
-      }
-      *reinterpret_cast<V*>(wbuf + (c * 32 + (lane ^ (c & 7))) * R) = pack4(xp);
+      a.vstrip[gb * a.n + j0 + c] = s;
     }
   }
 }
@@ -278,27 +319,8 @@ __device__ __forceinline__ void pass_tile(const PassArgs<T>& a, int64_t c0, int6
       compute_group<T, MODE, DUAL, DX, MASK, G>(a, B, j0 + (gi + 1) * G, (gi + 1) * G,
                                                 c1, row0, nvalid, ph, u, acc, wbuf, lane);
     }
-    // v-phase: lane (c, b) sums the 64 rows of block b of column c in order
     __syncwarp();
-    const int cnt = static_cast<int>(imin64(CH, c1 - j0));
-    if (lane < CH * NB) {
-      const int c = lane % CH, b = lane / CH;
-      const int64_t gb = wrow0 / kVBlockRows + b;
-      if (c < cnt && gb * kVBlockRows < a.m) {
-        const V* col = reinterpret_cast<const V*>(wbuf) + c * 32;
-        const int g7 = c & 7;
-        constexpr int QB = kVBlockRows / R;  // chunks per 64-row block
-        T s = T(0);
-#pragma unroll
-        for (int qq = 0; qq < QB; ++qq) {
-          T v4[R];
-          unpack(col[(b * QB + qq) ^ g7], v4);
-#pragma unroll
-          for (int t = 0; t < R; ++t) s += v4[t];
-        }
-        a.vstrip[gb * a.n + j0 + c] = s;
-      }
-    }
+    v_phase<T>(a, wbuf, j0, static_cast<int>(imin64(CH, c1 - j0)), wrow0, lane);
     __syncwarp();
   }
 }
@@ -380,13 +402,200 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_PASS_MINB)
   }
 }
 
+// ---------------------------------------------------------------------------
+// K1 (async): the same sweep with a per-lane cp.async ring in shared memory.
+// Each lane copies its own 16-B slices of X and C for kAsyncStages-1 column
+// groups ahead (LDGSTS, no register cost for data in flight) and consumes
+// them in order; completion is per-thread (cp.async.wait_group), so no
+// cross-lane synchronisation is needed for the ring.
+// ---------------------------------------------------------------------------
+#ifndef DROTB_ASYNC_S
+#define DROTB_ASYNC_S 4  // ring stages (S-1 groups in flight)
+#endif
+#ifndef DROTB_ASYNC_G
+#define DROTB_ASYNC_G 2  // columns per stage
+#endif
+constexpr int kAsyncS = DROTB_ASYNC_S;
+constexpr int kAsyncG = DROTB_ASYNC_G;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <class T>
+constexpr size_t async_smem_bytes() {
+  // per warp: ring [S][2][G][32 lanes] x 16 B + staging [16 cols][32 R] x sizeof(T)
+  return static_cast<size_t>(kWarpsPerCta) *
+         (static_cast<size_t>(kAsyncS) * 2 * kAsyncG * 32 * 16 +
+          static_cast<size_t>(kChunkCols) * 32 * 16);
+}
+
+template <class T, int MODE, bool DUAL, bool DX, bool MASK>
+__device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0, int64_t c1,
+                                                int64_t wrow0, int64_t row0, int nvalid,
+                                                const T (&ph)[16 / sizeof(T)],
+                                                T (&u)[16 / sizeof(T)], PassAcc<T>& acc,
+                                                T* wbuf, typename V16<T>::type* ring,
+                                                int lane) {
+  using V = typename V16<T>::type;
+  constexpr int R = 16 / sizeof(T);
+  constexpr int S = kAsyncS, G = kAsyncG, CH = kChunkCols;
+  constexpr int NG = CH / G;
+  static_assert(NG % S == 0, "stages must divide the groups of a chunk");
+  constexpr bool RC = MODE != kSkip;
+  const bool live = !MASK || nvalid > 0;
+  T vb[S][G];
+  auto issue = [&](int st, int64_t jg) {
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      const int64_t col = jg + k;
+      vb[st][k] = T(0);
+      if (col < c1) {
+        if (live) {
+          const int64_t off = col * a.ld + row0;
+          cp_async16(ring + ((st * 2 + 0) * G + k) * 32 + lane, a.xy + off);
+          if (RC) cp_async16(ring + ((st * 2 + 1) * G + k) * 32 + lane, a.cost + off);
+        }
+        vb[st][k] = __ldg(a.varphi + col);
+      }
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int st = 0; st < S - 1; ++st) issue(st, c0 + st * G);
+  for (int64_t j0 = c0; j0 < c1; j0 += CH) {
+#pragma unroll
+    for (int gg = 0; gg < NG; ++gg) {
+      const int st = gg % S;
+      issue((gg + S - 1) % S, j0 + (gg + S - 1) * G);
+      cp_async_wait<S - 1>();
+#pragma unroll
+      for (int k = 0; k < G; ++k) {
+        const int64_t col = j0 + gg * G + k;
+        if (col < c1) {
+          T x[R], cc[R];
+#pragma unroll
+          for (int t = 0; t < R; ++t) x[t] = cc[t] = T(0);
+          if (live) {
+            unpack(ring[((st * 2 + 0) * G + k) * 32 + lane], x);
+            if (RC) unpack(ring[((st * 2 + 1) * G + k) * 32 + lane], cc);
+          }
+          compute_col<T, MODE, DUAL, DX, MASK>(a, x, cc, vb[st][k], col, gg * G + k, row0,
+                                               nvalid, ph, u, acc, wbuf, lane);
+        }
+      }
+    }
+    __syncwarp();
+    v_phase<T>(a, wbuf, j0, static_cast<int>(imin64(CH, c1 - j0)), wrow0, lane);
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+}
+
+template <class T, int MODE, bool DUAL, bool DX>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+    pass_kernel_async(const PassArgs<T> a) {
+  using V = typename V16<T>::type;
+  constexpr int R = 16 / sizeof(T);
+  constexpr int ROWS_W = 32 * R;
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  __shared__ PassAcc<T> wacc[kWarpsPerCta];
+  if (a.stop != nullptr && *reinterpret_cast<const volatile int*>(a.stop)) return;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr size_t ring_v = static_cast<size_t>(kAsyncS) * 2 * kAsyncG * 32;  // V per warp
+  V* ring = reinterpret_cast<V*>(dyn_smem) + warp * ring_v;
+  T* wbuf = reinterpret_cast<T*>(reinterpret_cast<V*>(dyn_smem) + kWarpsPerCta * ring_v) +
+            warp * kChunkCols * ROWS_W;
+  const int64_t wrow0 =
+      (static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + warp) * ROWS_W;
+  const int64_t row0 = wrow0 + static_cast<int64_t>(lane) * R;
+  const int64_t gc = blockIdx.y;
+  const int64_t c0 = gc * a.tc;
+  const int64_t c1 = imin64(a.n, c0 + a.tc);
+  const int64_t nv = a.m - row0;
+  const int nvalid = nv <= 0 ? 0 : (nv >= R ? R : static_cast<int>(nv));
+
+  T ph[R], u[R];
+  if (nvalid > 0) {
+    unpack(*reinterpret_cast<const V*>(a.phi + row0), ph);
+  } else {
+#pragma unroll
+    for (int t = 0; t < R; ++t) ph[t] = T(0);
+  }
+#pragma unroll
+  for (int t = 0; t < R; ++t) u[t] = T(0);
+  PassAcc<T> acc{T(0), T(0), T(0), T(0), T(0), false};
+  if (__all_sync(0xffffffffu, nvalid == R))
+    pass_tile_async<T, MODE, DUAL, DX, false>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc, wbuf,
+                                              ring, lane);
+  else
+    pass_tile_async<T, MODE, DUAL, DX, true>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc, wbuf,
+                                             ring, lane);
+  if (nvalid > 0)
+    *reinterpret_cast<V*>(a.ustrip + gc * a.ld + row0) = pack4(u);
+
+  acc.cost = warp_sum(acc.cost);
+  acc.prev = warp_sum(acc.prev);
+  acc.dual = warp_sum(acc.dual);
+  acc.dx = warp_sum(acc.dx);
+  acc.mx = warp_max(acc.mx);
+  const bool wbad = __any_sync(0xffffffffu, acc.bad);
+  if (lane == 0) {
+    acc.bad = wbad;
+    wacc[warp] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    PassPartial<T> out{T(0), T(0), T(0), T(0), T(0), 0, 0};
+#pragma unroll
+    for (int w = 0; w < kWarpsPerCta; ++w) {
+      out.cost += wacc[w].cost;
+      out.prev += wacc[w].prev;
+      out.dual += wacc[w].dual;
+      out.dx += wacc[w].dx;
+      out.max_abs = fmax(out.max_abs, wacc[w].mx);
+      out.bad |= wacc[w].bad ? 1 : 0;
+    }
+    a.partials[static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x] = out;
+  }
+}
+
+static int k1_impl() {  // 0 = register double buffer, 1 = cp.async ring
+  static int impl = [] {
+    const char* e = std::getenv("DROTB_K1");
+    if (e && e[0] == 'r') return 0;
+    return 1;
+  }();
+  return impl;
+}
+
 template <class T, int MODE, bool DUAL, bool DX>
 static void launch_pass_t(const PassArgs<T>& a, cudaStream_t st) {
   constexpr int R = 16 / sizeof(T);
   const int64_t rows_cta = int64_t(kWarpsPerCta) * 32 * R;
   dim3 grid(static_cast<unsigned>((a.m + rows_cta - 1) / rows_cta),
             static_cast<unsigned>((a.n + a.tc - 1) / a.tc));
-  pass_kernel<T, MODE, DUAL, DX><<<grid, kWarpsPerCta * 32, 0, st>>>(a);
+  if (k1_impl() == 1) {
+    constexpr size_t smem = async_smem_bytes<T>();
+    static bool attr = [] {
+      cudaFuncSetAttribute(pass_kernel_async<T, MODE, DUAL, DX>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      return true;
+    }();
+    (void)attr;
+    pass_kernel_async<T, MODE, DUAL, DX><<<grid, kWarpsPerCta * 32, smem, st>>>(a);
+  } else {
+    pass_kernel<T, MODE, DUAL, DX><<<grid, kWarpsPerCta * 32, 0, st>>>(a);
+  }
   count_launch();
 }
 
@@ -615,45 +824,69 @@ __device__ __forceinline__ void erg_update(Book<T>* bk, double value) {
   bk->erg_mean += (value - bk->erg_mean) / static_cast<double>(bk->erg_count);
 }
 
+// Strip merge.  Exact order: one thread per row / column, sequential over
+// the strips (fused.hpp:314-321).  Fast order: kMergeLanes threads per row /
+// column sum interleaved strip subsets, combined by a fixed shuffle tree.
+constexpr int kMergeLanes = 8;
+
+template <class T, bool EXACT>
+__device__ __forceinline__ T strip_sum(const T* strips, int64_t count, int64_t stride,
+                                       int64_t idx, int sub) {
+  T acc = T(0);
+  if (EXACT) {
+    int64_t g = 0;
+    for (; g + 8 <= count; g += 8) {
+      T v8[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v8[q] = strips[(g + q) * stride + idx];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc += v8[q];
+    }
+    for (; g < count; ++g) acc += strips[g * stride + idx];
+  } else {
+    int64_t g = sub;
+    for (; g + 3 * kMergeLanes < count; g += 4 * kMergeLanes) {
+      T v4[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v4[q] = strips[(g + q * kMergeLanes) * stride + idx];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc += v4[q];
+    }
+    for (; g < count; g += kMergeLanes) acc += strips[g * stride + idx];
+#pragma unroll
+    for (int o = kMergeLanes / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  }
+  return acc;
+}
+
 template <class T, bool EXACT>
 __global__ void __launch_bounds__(kTailThreads) merge_kernel(const TailArgs<T> t) {
   Book<T>* bk = t.book;
   if (t.solver && *reinterpret_cast<volatile int*>(&bk->stop)) return;
   __shared__ T shT[4 * 32];
-  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  constexpr int L = EXACT ? 1 : kMergeLanes;
+  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t idx = gtid / L;
+  const int sub = static_cast<int>(gtid % L);
   T part[3] = {T(0), T(0), T(0)};  // sum r, sum r^2, sum s^2
   if (idx < t.m) {
-    T acc = T(0);
-    int64_t g = 0;
-    for (; g + 8 <= t.grid_cols; g += 8) {
-      T v8[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) v8[q] = t.ustrip[(g + q) * t.ld + idx];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) acc += v8[q];
+    const T acc = strip_sum<T, EXACT>(t.ustrip, t.grid_cols, t.ld, idx, sub);
+    if (sub == 0) {
+      t.u[idx] = acc;
+      const T r = acc - t.p[idx];
+      t.r_new[idx] = r;
+      part[0] = r;
+      part[1] = r * r;
     }
-    for (; g < t.grid_cols; ++g) acc += t.ustrip[g * t.ld + idx];
-    t.u[idx] = acc;
-    const T r = acc - t.p[idx];
-    t.r_new[idx] = r;
-    part[0] = r;
-    part[1] = r * r;
   } else if (idx < t.m + t.n) {
     const int64_t j = idx - t.m;
-    T acc = T(0);
-    int64_t g = 0;
-    for (; g + 8 <= t.grid_rows64; g += 8) {
-      T v8[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) v8[q] = t.vstrip[(g + q) * t.n + j];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) acc += v8[q];
+    const T acc = strip_sum<T, EXACT>(t.vstrip, t.grid_rows64, t.n, j, sub);
+    if (sub == 0) {
+      t.v[j] = acc;
+      const T s = acc - t.q[j];
+      t.s_new[j] = s;
+      part[2] = s * s;
     }
-    for (; g < t.grid_rows64; ++g) acc += t.vstrip[g * t.n + j];
-    t.v[j] = acc;
-    const T s = acc - t.q[j];
-    t.s_new[j] = s;
-    part[2] = s * s;
   }
   if (!EXACT) {
     block_sum<T, 3>(part, shT);
@@ -806,8 +1039,9 @@ __global__ void __launch_bounds__(kTailThreads) merge_kernel(const TailArgs<T> t
 
 template <class T>
 void launch_merge(const TailArgs<T>& t, bool exact, cudaStream_t st) {
+  const int64_t L = exact ? 1 : kMergeLanes;
   const unsigned blocks =
-      static_cast<unsigned>((t.m + t.n + kTailThreads - 1) / kTailThreads);
+      static_cast<unsigned>(((t.m + t.n) * L + kTailThreads - 1) / kTailThreads);
   if (exact)
     merge_kernel<T, true><<<blocks, kTailThreads, 0, st>>>(t);
   else
@@ -1097,7 +1331,7 @@ void launch_report(const T* xy, const T* cost, const TailArgs<T>& t,
   if (exact) {
     report_kernel<T, true><<<1, kTailThreads, 0, st>>>(xy, cost, t, always ? 1 : 0);
   } else {
-    const int64_t blocks = imin64(t.n, 148 * 2);
+    const int64_t blocks = imin64(t.n, 148 * 4);
     report_kernel<T, false>
         <<<static_cast<unsigned>(blocks), kTailThreads, 0, st>>>(xy, cost, t,
                                                                  always ? 1 : 0);

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -146,6 +147,8 @@ struct Session {
     if (m_ <= 0 || n_ <= 0)
       return set_error(DROTB_ERRC_EMPTY_DIMENSION, "cost matrix has an empty dimension");
     cfg = c;
+    if (const char* e = std::getenv("DROTB_NO_GRAPHS"))  // profiling aid (ncu)
+      if (e[0] == '1') cfg.use_graphs = 0;
     m = m_global = m_;
     n = n_global = n_;
     if (cfg.device >= 0) CUDA_TRY(cudaSetDevice(cfg.device));
@@ -182,7 +185,7 @@ struct Session {
     tile_grid_rows = (m + bs - 1) / bs;
     n_tiles = tile_grid_rows * grid_cols;
     tail_blocks = (m + n + 255) / 256;
-    report_blocks = std::min<int64_t>(n, 148 * 2);
+    report_blocks = std::min<int64_t>(n, 148 * 4);
     const size_t mat = static_cast<size_t>(ld) * static_cast<size_t>(n);
     RC_TRY(dev_alloc(&X, mat));
     RC_TRY(dev_alloc(&C, mat));
@@ -200,7 +203,7 @@ struct Session {
     RC_TRY(dev_alloc(&v, n));
     RC_TRY(dev_alloc(&ustrip, static_cast<size_t>(grid_cols) * ld));
     RC_TRY(dev_alloc(&vstrip, static_cast<size_t>(grid_rows64) * n));
-    RC_TRY(dev_alloc(&tscr, static_cast<size_t>(tail_blocks) * 3));
+    RC_TRY(dev_alloc(&tscr, static_cast<size_t>(tail_blocks) * 8 * 3));  // merge: 8 lanes per index
     RC_TRY(dev_alloc(&partials, static_cast<size_t>(n_partials)));
     if (exact) {
       RC_TRY(dev_alloc(&tiles, static_cast<size_t>(n_tiles)));
@@ -481,10 +484,13 @@ struct Session {
     if (mode_out) *mode_out = mode;
     PassArgs<T> pa = pass_args();
     if (exact) launch_tile_chains<T>(pa, mode, want_dual, want_dx, bs, tiles, stream);
-    // external records: they become event nodes when captured into a graph
-    if (pass_begin) CUDA_TRY(cudaEventRecordWithFlags(pass_begin, stream, cudaEventRecordExternal));
+    // while capturing, external records become event nodes of the graph
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (pass_begin || pass_end) CUDA_TRY(cudaStreamIsCapturing(stream, &cap));
+    const unsigned evf = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
+    if (pass_begin) CUDA_TRY(cudaEventRecordWithFlags(pass_begin, stream, evf));
     launch_pass<T>(pa, mode, want_dual, want_dx, stream);
-    if (pass_end) CUDA_TRY(cudaEventRecordWithFlags(pass_end, stream, cudaEventRecordExternal));
+    if (pass_end) CUDA_TRY(cudaEventRecordWithFlags(pass_end, stream, evf));
     TailArgs<T> ta = tail_args(k, mode, folded_after, true);
     launch_merge<T>(ta, exact, stream);
     if (cond_out) {  // graph build: the report goes into an IF node body

@@ -6,7 +6,7 @@ import paper_2110_11738_b200 as drot
 m = n = int(sys.argv[1]) if len(sys.argv) > 1 else 10000
 dt = np.float32 if (len(sys.argv) < 3 or sys.argv[2] == "f32") else np.float64
 iters = int(sys.argv[3]) if len(sys.argv) > 3 else 8
-cfg = drot.DrotConfig(tol_primal=-1.0, max_iters=10**9)
+cfg = drot.DrotConfig(tol_primal=-1.0, max_iters=10**9, use_graphs=False)  # ncu cannot profile kernels inside graphs with conditional nodes
 s = drot.Session(m, n, dt, cfg)
 s.gen_gaussian(5.0, 0, "dyadic")
 s.init()
