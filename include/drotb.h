@@ -311,13 +311,24 @@ int drotb_session_run_timed(drotb_session* s, int64_t n_iters, double* total_ms,
 
 /* ---- multi-GPU (row sharding, NCCL) ------------------------------------- */
 #define DROTB_NCCL_ID_BYTES 128
+/* ncclGetUniqueId for rank 0 to broadcast (e.g. over torch.distributed). */
 int drotb_nccl_unique_id(char* out128);
-/* Attach a row shard [row_begin, row_end) of a world_size-rank job to the
- * session before set_problem; the session then holds only its rows of C/X
- * and allreduces the column sums and scalars every iteration. */
-int drotb_session_shard(drotb_session* s, int32_t rank, int32_t world_size,
-                        const char* nccl_id128, int64_t row_begin,
-                        int64_t row_end);
+/* Row range of `rank` in a world_size-way split of m rows: contiguous,
+ * aligned to the 64-row v blocks, as even as possible. */
+int drotb_shard_rows(int64_t m, int32_t world_size, int32_t rank,
+                     int64_t* row_begin, int64_t* row_end);
+/* A session holding rows [row_begin, row_end) of an m_global x n problem,
+ * one process per GPU.  X, C, phi, a, r, p are local; varphi, b, s, q are
+ * replicated.  Per iteration: one NCCL allreduce of [v partial (n) | pass
+ * scalars], one of the row-side dual/trace sums, and -- only when the gate
+ * fires -- one of the exact-report sums.  set_problem then
+ * takes the local rows of C (row_end-row_begin x n, column-major), the local
+ * p and the full q; get_plan returns the local rows.  order must be fast. */
+int drotb_session_create_sharded(drotb_session** s, int64_t m_global, int64_t n,
+                                 int32_t precision, const drotb_config* cfg,
+                                 int32_t rank, int32_t world_size,
+                                 const char* nccl_id128, int64_t row_begin,
+                                 int64_t row_end);
 
 #ifdef __cplusplus
 }

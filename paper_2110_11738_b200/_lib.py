@@ -107,7 +107,9 @@ SIGNATURES = {
     "drotb_session_pass_bytes": (C.c_int, [vp, P(f64), P(f64)]),
     "drotb_session_run_timed": (C.c_int, [vp, i64, P(f64), P(f64), P(i64), P(f64), P(i64)]),
     "drotb_nccl_unique_id": (C.c_int, [C.c_char_p]),
-    "drotb_session_shard": (C.c_int, [vp, i32, i32, C.c_char_p, i64, i64]),
+    "drotb_shard_rows": (C.c_int, [i64, i32, i32, P(i64), P(i64)]),
+    "drotb_session_create_sharded": (C.c_int, [P(vp), i64, i64, i32, P(drotb_config), i32, i32,
+                                               C.c_char_p, i64, i64]),
 }
 
 _lib = None

@@ -25,6 +25,9 @@ int gen_gaussian_points(int64_t m, int64_t n, double sigma_t, uint64_t seed,
 template <class T>
 int gen_gaussian_cost(int64_t m, int64_t n, double sigma_t, uint64_t seed,
                       T* C);
+template <class T>
+int gen_gaussian_cost_rows(int64_t m, int64_t n, double sigma_t, uint64_t seed,
+                           int64_t row_begin, int64_t row_end, T* C);
 void dirichlet_marginal(uint64_t seed, uint64_t stream, int64_t count,
                         double* w);
 template <class T>

@@ -79,6 +79,7 @@ struct Book {
   double tol_primal, tol_dual, tol_gap, primal_scale;
   int32_t record_trace, relative;
   unsigned int ticket_merge, ticket_update, ticket_report, pad1;
+  double jpart[4];  // sharded: replicated column-side partials of the update
 };
 
 struct TraceRowDev {
@@ -127,7 +128,12 @@ struct TailArgs {
   // CUDA-graph IF node guarding the confirm report of this iteration
   unsigned long long cond;
   int32_t use_cond;
-  int32_t pad1;
+  // row-sharded multi-GPU (0: single device): merge/update/report write
+  // their rank-local partials to these buffers for the NCCL allreduces
+  int32_t sharded;
+  T* pack;       // [v (n) | sum r, sum r^2, cost, prev, dual, dx]  (sum)
+  T* pmax;       // [max|t| or +inf if non-finite]                   (max)
+  double* dpack; // [dual_i, dphi^2, dphi, cross_i | obj, dual^2]    (sum)
 };
 
 // ---- kernel launchers (kernels.cu) ---------------------------------------
@@ -146,12 +152,21 @@ template <class T>
 void launch_report(const T* xy, const T* cost, const TailArgs<T>& t,
                    bool exact, bool always, cudaStream_t st);
 template <class T>
+void launch_finish(const TailArgs<T>& t, cudaStream_t st);
+template <class T>
+void launch_gate(const TailArgs<T>& t, cudaStream_t st);
+template <class T>
+void launch_report_final(const TailArgs<T>& t, bool always, cudaStream_t st);
+template <class T>
+void launch_init_sharded_finish(T* b, const T* q, int64_t n, const T* pack,
+                                int64_t mn_global, Book<T>* book, cudaStream_t st);
+template <class T>
 void launch_init_x0(T* xy, const T* p, const T* q, int64_t m, int64_t n,
                     int64_t ld, cudaStream_t st);
 template <class T>
 void launch_init_sums(const T* xy, const T* p, const T* q, T* a, T* b,
                       int64_t m, int64_t n, int64_t ld, Book<T>* book,
-                      cudaStream_t st);
+                      cudaStream_t st, T* shard_pack = nullptr);
 template <class T>
 void launch_validate(const T* buf, int64_t m, int64_t n, int64_t ld,
                      unsigned long long* first_nonfinite,

@@ -859,6 +859,46 @@ __device__ __forceinline__ T strip_sum(const T* strips, int64_t count, int64_t s
   return acc;
 }
 
+// Pass totals -> FusedPassOutput scalars, step_impl recursions and the
+// objective bookkeeping of solve (fused.hpp:346-356; solver.hpp:266,
+// 273-277, 418-437).  tot = {cost, prev, dual, dx, max|t|, sum r, |r|^2, |s|^2}.
+template <class T>
+__device__ void merge_scalars(Book<T>* bk, const TailArgs<T>& t, const T (&tot)[8],
+                              int totbad) {
+  bk->pass_cost = tot[0];
+  bk->pass_prev = tot[1];
+  bk->pass_dual = tot[2];
+  bk->pass_dx = tot[3];
+  bk->pass_max_abs = tot[4];
+  bk->pass_bad = totbad;
+  if (!t.solver) return;
+  const int64_t k = bk->iter;
+  bk->folded = t.folded_after;
+  if (totbad) {  // solver.hpp:266, 418-422
+    bk->failed = 1;
+    bk->iterations = k + 1;
+    bk->stop = 1;
+    return;
+  }
+  const T beta = tot[5] / static_cast<T>(t.m_global + t.n_global);
+  bk->beta = beta;
+  bk->coef = T(2) * beta - bk->alpha;
+  bk->nr2 = tot[6];
+  bk->ns2 = tot[7];
+  bk->iterations = k + 1;
+  const bool cost_valid = t.reads_cost != 0;
+  const bool dual_valid = t.reads_cost && t.want_dual;
+  if (!bk->prev_pass_had_cost && cost_valid)
+    erg_update(bk, static_cast<double>(tot[1]));
+  if (cost_valid) {
+    bk->last_cost = static_cast<double>(tot[0]);
+    erg_update(bk, bk->last_cost);
+  }
+  bk->prev_pass_had_cost = cost_valid ? 1 : 0;
+  if (dual_valid)
+    bk->last_r_dual = sqrt(static_cast<double>(tot[2])) / static_cast<double>(t.rho);
+}
+
 template <class T, bool EXACT>
 __global__ void __launch_bounds__(kTailThreads) merge_kernel(const TailArgs<T> t) {
   Book<T>* bk = t.book;
@@ -882,10 +922,12 @@ __global__ void __launch_bounds__(kTailThreads) merge_kernel(const TailArgs<T> t
     const int64_t j = idx - t.m;
     const T acc = strip_sum<T, EXACT>(t.vstrip, t.grid_rows64, t.n, j, sub);
     if (sub == 0) {
-      t.v[j] = acc;
-      const T s = acc - t.q[j];
-      t.s_new[j] = s;
-      part[2] = s * s;
+      t.v[j] = acc;  // sharded: v points at the allreduce pack
+      if (!t.sharded) {
+        const T s = acc - t.q[j];
+        t.s_new[j] = s;
+        part[2] = s * s;
+      }
     }
   }
   if (!EXACT) {
@@ -959,18 +1001,39 @@ __global__ void __launch_bounds__(kTailThreads) merge_kernel(const TailArgs<T> t
     T v4[4] = {T(0), T(0), T(0), T(0)};
     T mx = T(0);
     int bad = 0;
-    for (int64_t k = tid; k < t.n_pass_partials; k += blockDim.x) {
-      const PassPartial<T>& sc = t.pass_partials[k];
-      v4[0] += sc.cost;
-      v4[1] += sc.prev;
-      v4[2] += sc.dual;
-      v4[3] += sc.dx;
-      mx = fmax(mx, sc.max_abs);
-      bad |= sc.bad;
+    // fixed strided order, 8 independent loads in flight per thread
+    const int64_t np = t.n_pass_partials;
+    const int64_t bd = blockDim.x;
+    for (int64_t k0 = tid; k0 < np; k0 += 8 * bd) {
+      PassPartial<T> sc[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (k0 + q * bd < np) sc[q] = t.pass_partials[k0 + q * bd];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (k0 + q * bd < np) {
+          v4[0] += sc[q].cost;
+          v4[1] += sc[q].prev;
+          v4[2] += sc[q].dual;
+          v4[3] += sc[q].dx;
+          mx = fmax(mx, sc[q].max_abs);
+          bad |= sc[q].bad;
+        }
     }
     T s3[3] = {T(0), T(0), T(0)};
-    for (int64_t k = tid; k < gridDim.x; k += blockDim.x)
-      for (int q = 0; q < 3; ++q) s3[q] += t.tscratch[k * 3 + q];
+    const int64_t nb = gridDim.x;
+    for (int64_t k0 = tid; k0 < nb; k0 += 4 * bd) {
+      T v[4][3];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+          v[q][r] = k0 + q * bd < nb ? t.tscratch[(k0 + q * bd) * 3 + r] : T(0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int r = 0; r < 3; ++r) s3[r] += v[q][r];
+    }
     block_sum<T, 4>(v4, shT);
     block_sum<T, 3>(s3, shT);
     mx = warp_max(mx);
@@ -1000,41 +1063,14 @@ __global__ void __launch_bounds__(kTailThreads) merge_kernel(const TailArgs<T> t
   }
   if (tid != 0) return;
   bk->ticket_merge = 0u;
-  bk->pass_cost = tot[0];
-  bk->pass_prev = tot[1];
-  bk->pass_dual = tot[2];
-  bk->pass_dx = tot[3];
-  bk->pass_max_abs = tot[4];
-  bk->pass_bad = totbad;
-  if (!t.solver) return;
-  const int64_t k = bk->iter;
-  bk->folded = t.folded_after;
-  if (totbad) {  // solver.hpp:266, 418-422
-    bk->failed = 1;
-    bk->iterations = k + 1;
-    bk->stop = 1;
+  if (t.sharded) {  // rank-local totals -> allreduce -> finish_kernel
+    for (int k = 0; k < 4; ++k) t.pack[t.n + 2 + k] = tot[k];
+    t.pack[t.n + 0] = tot[5];
+    t.pack[t.n + 1] = tot[6];
+    t.pmax[0] = totbad ? __int_as_float(0x7f800000) : tot[4];
     return;
   }
-  // step_impl recursions (solver.hpp:273-277)
-  const T beta = tot[5] / static_cast<T>(t.m_global + t.n_global);
-  bk->beta = beta;
-  bk->coef = T(2) * beta - bk->alpha;
-  bk->nr2 = tot[6];
-  bk->ns2 = tot[7];
-  bk->iterations = k + 1;
-  // objective bookkeeping (solver.hpp:428-437)
-  const bool cost_valid = t.reads_cost != 0;
-  const bool dual_valid = t.reads_cost && t.want_dual;
-  if (!bk->prev_pass_had_cost && cost_valid)
-    erg_update(bk, static_cast<double>(tot[1]));
-  if (cost_valid) {
-    bk->last_cost = static_cast<double>(tot[0]);
-    erg_update(bk, bk->last_cost);
-  }
-  bk->prev_pass_had_cost = cost_valid ? 1 : 0;
-  if (dual_valid)
-    bk->last_r_dual =
-        sqrt(static_cast<double>(tot[2])) / static_cast<double>(t.rho);
+  merge_scalars<T>(bk, t, tot, totbad);
 }
 
 template <class T>
@@ -1049,131 +1085,65 @@ void launch_merge(const TailArgs<T>& t, bool exact, cudaStream_t st) {
   count_launch();
 }
 
+// Sharded continuation of K2 after the NCCL allreduce of the pack:
+// s = v - q (replicated), |s|^2, then the scalar recursions.
+template <class T>
+__global__ void __launch_bounds__(kTailThreads) finish_kernel(const TailArgs<T> t) {
+  Book<T>* bk = t.book;
+  if (*reinterpret_cast<volatile int*>(&bk->stop)) return;
+  __shared__ T shT[32];
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  T part[1] = {T(0)};
+  if (j < t.n) {
+    const T s = t.pack[j] - t.q[j];
+    t.s_new[j] = s;
+    part[0] = s * s;
+  }
+  block_sum<T, 1>(part, shT);
+  if (threadIdx.x == 0) t.tscratch[blockIdx.x] = part[0];
+  if (!last_block(&bk->ticket_merge)) return;
+  T s1[1] = {T(0)};
+  for (int64_t k = threadIdx.x; k < gridDim.x; k += blockDim.x) s1[0] += t.tscratch[k];
+  block_sum<T, 1>(s1, shT);
+  if (threadIdx.x != 0) return;
+  bk->ticket_merge = 0u;
+  const T mx = t.pmax[0];
+  const int bad = !(mx <= max_finite<T>());
+  const T tot[8] = {t.pack[t.n + 2], t.pack[t.n + 3], t.pack[t.n + 4], t.pack[t.n + 5],
+                    mx,              t.pack[t.n + 0], t.pack[t.n + 1], s1[0]};
+  merge_scalars<T>(bk, t, tot, bad);
+}
+
+template <class T>
+void launch_finish(const TailArgs<T>& t, cudaStream_t st) {
+  finish_kernel<T><<<static_cast<unsigned>((t.n + kTailThreads - 1) / kTailThreads),
+                     kTailThreads, 0, st>>>(t);
+  count_launch();
+}
+
 // ---------------------------------------------------------------------------
 // K3: shift / defect recursions, dual value, trace row, gate
 // ---------------------------------------------------------------------------
-template <class T, bool EXACT>
-__global__ void __launch_bounds__(kTailThreads) update_kernel(const TailArgs<T> t) {
-  Book<T>* bk = t.book;
-  if (*reinterpret_cast<volatile int*>(&bk->stop)) return;
-  __shared__ double shD[6 * 32];
-  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const T coef = bk->coef;
-  const T inv_n = T(1) / static_cast<T>(t.n_global);
-  const T inv_m = T(1) / static_cast<T>(t.m_global);
-  const double drho = static_cast<double>(t.rho);
+// Gate of solve (solver.hpp:439-504) given the O(m+n) sums of this iteration:
+// dual value sum_i p_i phi_i/rho + sum_j q_j varphi_j/rho and the rank-two
+// fixed-point terms.  Fires the confirm report (graph IF node, or a pause
+// when row-sharded) when the stale-dual gate passes.
+template <class T>
+__device__ void gate_logic(Book<T>* bk, const TailArgs<T>& t, double dual_value, double dphi2,
+                           double dphi, double dvarphi2, double dvarphi, double cross) {
   const bool fp = bk->record_trace != 0;
-  // 0 dual value, 1 dphi^2, 2 sum dphi, 3 dvarphi^2, 4 sum dvarphi, 5 cross
-  double part[6] = {0, 0, 0, 0, 0, 0};
-  const int64_t mn = t.m + t.n;
-  if (idx < t.m) {
-    const T r = t.r_new[idx];
-    const T ph_old = t.phi[idx];
-    const T ph = (t.a[idx] - T(2) * r + coef) * inv_n;
-    t.phi[idx] = ph;
-    t.a[idx] = t.a[idx] - r;
-    part[0] = static_cast<double>(t.p[idx]) * static_cast<double>(ph) / drho;
-    if (fp) {
-      const double d = static_cast<double>(ph) - static_cast<double>(ph_old);
-      part[1] = d * d;
-      part[2] = d;
-      part[5] = d * (static_cast<double>(r) - static_cast<double>(t.r_old[idx]));
-    }
-    if (EXACT) {
-      t.terms[idx] = part[0];
-      t.terms[mn + idx] = part[2];
-      t.terms[2 * mn + idx] = part[5];
-    }
-  } else if (idx < mn) {
-    const int64_t j = idx - t.m;
-    const T s = t.s_new[j];
-    const T vp_old = t.varphi[j];
-    const T vp = (t.b[j] - T(2) * s + coef) * inv_m;
-    t.varphi[j] = vp;
-    t.b[j] = t.b[j] - s;
-    part[0] = static_cast<double>(t.q[j]) * static_cast<double>(vp) / drho;
-    if (fp) {
-      const double d = static_cast<double>(vp) - static_cast<double>(vp_old);
-      part[3] = d * d;
-      part[4] = d;
-      part[5] = d * (static_cast<double>(s) - static_cast<double>(t.s_old[j]));
-    }
-    if (EXACT) {
-      t.terms[idx] = part[0];
-      t.terms[mn + idx] = part[4];
-      t.terms[2 * mn + idx] = part[5];
-    }
-  }
-  if (!EXACT) {
-    block_sum<double, 6>(part, shD);
-    if (threadIdx.x == 0)
-      for (int k = 0; k < 6; ++k) t.dscratch[blockIdx.x * 6 + k] = part[k];
-  }
-  if (!last_block(&bk->ticket_update)) return;
-
-  __shared__ double tot[6];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (EXACT) {
-    // one serial chain per quantity, in the reference's loop order
-    // (solver.hpp:450-465 and :479-486)
-    __shared__ double sb[2 * kStage];
-    __shared__ double chains[2];
-    const double* tv = t.terms;
-    staged_chains<double, 2>(
-        mn, [&](int k, int64_t e) { return k == 0 ? tv[e] : tv[2 * mn + e]; }, sb, chains);
-    if (tid == 0) {
-      tot[0] = chains[0];
-      tot[5] = fp ? chains[1] : 0.0;
-    }
-    if (fp) {
-      const double* d = t.terms + mn;
-      staged_chains<double, 2>(
-          t.m, [&](int k, int64_t e) { const double x = d[e]; return k == 0 ? x * x : x; },
-          sb, chains);
-      if (tid == 0) {
-        tot[1] = chains[0];
-        tot[2] = chains[1];
-      }
-      staged_chains<double, 2>(
-          t.n,
-          [&](int k, int64_t e) { const double x = d[t.m + e]; return k == 0 ? x * x : x; },
-          sb, chains);
-      if (tid == 0) {
-        tot[3] = chains[0];
-        tot[4] = chains[1];
-      }
-    } else if (tid == 0) {
-      tot[1] = tot[2] = tot[3] = tot[4] = 0.0;
-    }
-    __syncthreads();
-  } else {
-    double s6[6] = {0, 0, 0, 0, 0, 0};
-    for (int64_t k = tid; k < gridDim.x; k += blockDim.x)
-      for (int q = 0; q < 6; ++q) s6[q] += t.dscratch[k * 6 + q];
-    block_sum<double, 6>(s6, shD);
-    if (tid == 0)
-      for (int q = 0; q < 6; ++q) tot[q] = s6[q];
-    __syncthreads();
-  }
-  if (tid != 0) return;
-  bk->ticket_update = 0u;
   bk->alpha = bk->alpha - bk->beta;  // solver.hpp:289
   const int64_t k = bk->iter;
   bk->iter = k + 1;
-
-  // fixed-point residual via the rank-two identity (solver.hpp:443-472)
   double fp_residual = __longlong_as_double(0x7ff8000000000000ULL);
-  if (fp) {
-    double fp_sq = static_cast<double>(t.n_global) * tot[1] +
-                   static_cast<double>(t.m_global) * tot[3] +
-                   2.0 * tot[2] * tot[4];
-    if (t.reads_cost && t.want_dx) fp_sq += static_cast<double>(bk->pass_dx) + 2.0 * tot[5];
+  if (fp) {  // rank-two identity (solver.hpp:443-472)
+    double fp_sq = static_cast<double>(t.n_global) * dphi2 +
+                   static_cast<double>(t.m_global) * dvarphi2 + 2.0 * dphi * dvarphi;
+    if (t.reads_cost && t.want_dx) fp_sq += static_cast<double>(bk->pass_dx) + 2.0 * cross;
     fp_residual = sqrt(fmax(fp_sq, 0.0));
   }
   bk->fp_residual = fp_residual;
-  // gated quantities (solver.hpp:474-490)
   const double r_primal = sqrt(static_cast<double>(bk->nr2) + static_cast<double>(bk->ns2));
-  const double dual_value = tot[0];
   const double gap = fabs(bk->last_cost - dual_value);
   const double gap_scale = bk->relative ? 1.0 / (1.0 + fabs(bk->last_cost)) : 1.0;
   bk->r_primal = r_primal;
@@ -1199,11 +1169,157 @@ __global__ void __launch_bounds__(kTailThreads) update_kernel(const TailArgs<T> 
   if (fire) {
     bk->confirm = 1;
     bk->gate_hits += 1;
+    if (t.sharded) bk->stop = 2;  // pause: the host runs the collective confirm
   } else if (k + 1 >= bk->max_iters) {
     bk->stop = 1;
   }
   // the confirm report runs only when the gate fires (graph IF node)
   if (t.use_cond) cudaGraphSetConditional(t.cond, fire ? 1u : 0u);
+}
+
+template <class T, bool EXACT>
+__global__ void __launch_bounds__(kTailThreads) update_kernel(const TailArgs<T> t) {
+  Book<T>* bk = t.book;
+  if (*reinterpret_cast<volatile int*>(&bk->stop)) return;
+  __shared__ double shD[8 * 32];
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const T coef = bk->coef;
+  const T inv_n = T(1) / static_cast<T>(t.n_global);
+  const T inv_m = T(1) / static_cast<T>(t.m_global);
+  const double drho = static_cast<double>(t.rho);
+  const bool fp = bk->record_trace != 0;
+  // row side:    0 dual_i, 1 dphi^2, 2 sum dphi, 3 cross_i
+  // column side: 4 dual_j, 5 dvarphi^2, 6 sum dvarphi, 7 cross_j
+  double part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const int64_t mn = t.m + t.n;
+  if (idx < t.m) {
+    const T r = t.r_new[idx];
+    const T ph_old = t.phi[idx];
+    const T ph = (t.a[idx] - T(2) * r + coef) * inv_n;  // solver.hpp:280-282
+    t.phi[idx] = ph;
+    t.a[idx] = t.a[idx] - r;  // solver.hpp:287
+    part[0] = static_cast<double>(t.p[idx]) * static_cast<double>(ph) / drho;
+    if (fp) {
+      const double d = static_cast<double>(ph) - static_cast<double>(ph_old);
+      part[1] = d * d;
+      part[2] = d;
+      part[3] = d * (static_cast<double>(r) - static_cast<double>(t.r_old[idx]));
+    }
+    if (EXACT) {
+      t.terms[idx] = part[0];
+      t.terms[mn + idx] = part[2];
+      t.terms[2 * mn + idx] = part[3];
+    }
+  } else if (idx < mn) {
+    const int64_t j = idx - t.m;
+    const T s = t.s_new[j];
+    const T vp_old = t.varphi[j];
+    const T vp = (t.b[j] - T(2) * s + coef) * inv_m;  // solver.hpp:283-285
+    t.varphi[j] = vp;
+    t.b[j] = t.b[j] - s;  // solver.hpp:288
+    part[4] = static_cast<double>(t.q[j]) * static_cast<double>(vp) / drho;
+    if (fp) {
+      const double d = static_cast<double>(vp) - static_cast<double>(vp_old);
+      part[5] = d * d;
+      part[6] = d;
+      part[7] = d * (static_cast<double>(s) - static_cast<double>(t.s_old[j]));
+    }
+    if (EXACT) {
+      t.terms[idx] = part[4];
+      t.terms[mn + idx] = part[6];
+      t.terms[2 * mn + idx] = part[7];
+    }
+  }
+  if (!EXACT) {
+    block_sum<double, 8>(part, shD);
+    if (threadIdx.x == 0)
+      for (int k = 0; k < 8; ++k) t.dscratch[blockIdx.x * 8 + k] = part[k];
+  }
+  if (!last_block(&bk->ticket_update)) return;
+
+  __shared__ double tot[8];
+  const int tid = threadIdx.x;
+  if (EXACT) {
+    // one serial chain per quantity, in the reference's loop order
+    // (solver.hpp:450-465 and :479-486); dual value and cross run over
+    // rows then columns in one chain
+    __shared__ double sb[2 * kStage];
+    __shared__ double chains[2];
+    const double* tv = t.terms;
+    staged_chains<double, 2>(
+        mn, [&](int k, int64_t e) { return k == 0 ? tv[e] : tv[2 * mn + e]; }, sb, chains);
+    if (tid == 0) {
+      tot[0] = chains[0];
+      tot[3] = fp ? chains[1] : 0.0;
+    }
+    if (fp) {
+      const double* d = t.terms + mn;
+      staged_chains<double, 2>(
+          t.m, [&](int k, int64_t e) { const double x = d[e]; return k == 0 ? x * x : x; },
+          sb, chains);
+      if (tid == 0) {
+        tot[1] = chains[0];
+        tot[2] = chains[1];
+      }
+      staged_chains<double, 2>(
+          t.n,
+          [&](int k, int64_t e) { const double x = d[t.m + e]; return k == 0 ? x * x : x; },
+          sb, chains);
+      if (tid == 0) {
+        tot[5] = chains[0];
+        tot[6] = chains[1];
+      }
+    } else if (tid == 0) {
+      tot[1] = tot[2] = tot[5] = tot[6] = 0.0;
+    }
+    if (tid == 0) tot[4] = tot[7] = 0.0;  // folded into the single chains
+    __syncthreads();
+  } else {
+    double s8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const int64_t nb = gridDim.x, bd = blockDim.x;
+    for (int64_t k0 = tid; k0 < nb; k0 += 2 * bd) {
+      double v[2][8];
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int r = 0; r < 8; ++r) v[q][r] = k0 + q * bd < nb ? t.dscratch[(k0 + q * bd) * 8 + r] : 0.0;
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int r = 0; r < 8; ++r) s8[r] += v[q][r];
+    }
+    block_sum<double, 8>(s8, shD);
+    if (tid == 0)
+      for (int q = 0; q < 8; ++q) tot[q] = s8[q];
+    __syncthreads();
+  }
+  if (tid != 0) return;
+  bk->ticket_update = 0u;
+  if (t.sharded) {  // rank-local row sums -> allreduce -> gate_kernel
+    for (int q = 0; q < 4; ++q) {
+      t.dpack[q] = tot[q];
+      bk->jpart[q] = tot[4 + q];
+    }
+    return;
+  }
+  gate_logic<T>(bk, t, tot[0] + tot[4], tot[1], tot[2], tot[5], tot[6], tot[3] + tot[7]);
+}
+
+// Sharded continuation of K3 after the allreduce of the row-side sums.
+template <class T>
+__global__ void gate_kernel(const TailArgs<T> t) {
+  Book<T>* bk = t.book;
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (*reinterpret_cast<volatile int*>(&bk->stop)) return;
+  const double* d = t.dpack;
+  gate_logic<T>(bk, t, d[0] + bk->jpart[0], d[1], d[2], bk->jpart[1], bk->jpart[2],
+                d[3] + bk->jpart[3]);
+}
+
+template <class T>
+void launch_gate(const TailArgs<T>& t, cudaStream_t st) {
+  gate_kernel<T><<<1, 32, 0, st>>>(t);
+  count_launch();
 }
 
 template <class T>
@@ -1235,13 +1351,36 @@ __device__ __forceinline__ void report_elem(T xv, T cv, T phi_i, double nu_j,
   if (slack > 0) dsq += slack * slack;
 }
 
+// Exact report of the matched pair and the confirm decision
+// (solver.hpp:339-353, 508-519).  obj / dual_sq: the streamed sums.
+template <class T>
+__device__ void report_decide(Book<T>* bk, double obj, double dual_sq, int always) {
+  const double r_primal = sqrt(static_cast<double>(bk->nr2) + static_cast<double>(bk->ns2));
+  const double r_dual = sqrt(dual_sq);
+  const double gap = fabs(obj - bk->dual_value);
+  bk->rep_objective = obj;
+  bk->rep_r_primal = r_primal;
+  bk->rep_r_dual = r_dual;
+  bk->rep_gap = gap;
+  if (always) return;
+  const double egs = bk->relative ? 1.0 / (1.0 + fabs(obj)) : 1.0;
+  if (r_primal * bk->primal_scale <= bk->tol_primal && r_dual <= bk->tol_dual &&
+      gap * egs <= bk->tol_gap) {
+    bk->converged = 1;
+    bk->stop = 1;
+  } else {
+    bk->confirm = 0;
+    bk->stop = bk->iter >= bk->max_iters ? 1 : 0;  // also ends a sharded pause
+  }
+}
+
 template <class T, bool EXACT>
 __global__ void __launch_bounds__(kTailThreads)
     report_kernel(const T* __restrict__ xy, const T* __restrict__ cost,
                   const TailArgs<T> t, int always) {
   Book<T>* bk = t.book;
-  if (!always) {
-    if (*reinterpret_cast<volatile int*>(&bk->stop) ||
+  if (!always) {  // stop == 2 is the sharded pause that asked for this report
+    if (*reinterpret_cast<volatile int*>(&bk->stop) == 1 ||
         !*reinterpret_cast<volatile int*>(&bk->confirm))
       return;
   }
@@ -1304,25 +1443,24 @@ __global__ void __launch_bounds__(kTailThreads)
   block_sum<double, 2>(s2, shD);
   if (threadIdx.x != 0) return;
   bk->ticket_report = 0u;
-  const double obj = s2[0];
-  const double r_primal =
-      sqrt(static_cast<double>(bk->nr2) + static_cast<double>(bk->ns2));
-  const double r_dual = sqrt(s2[1]);
-  const double gap = fabs(obj - bk->dual_value);
-  bk->rep_objective = obj;
-  bk->rep_r_primal = r_primal;
-  bk->rep_r_dual = r_dual;
-  bk->rep_gap = gap;
-  if (always) return;
-  const double egs = bk->relative ? 1.0 / (1.0 + fabs(obj)) : 1.0;
-  if (r_primal * bk->primal_scale <= bk->tol_primal && r_dual <= bk->tol_dual &&
-      gap * egs <= bk->tol_gap) {
-    bk->converged = 1;
-    bk->stop = 1;
-  } else {
-    bk->confirm = 0;
-    if (bk->iter >= bk->max_iters) bk->stop = 1;
+  if (t.sharded) {  // rank-local sums -> allreduce -> report_final_kernel
+    t.dpack[4] = s2[0];
+    t.dpack[5] = s2[1];
+    return;
   }
+  report_decide<T>(bk, s2[0], s2[1], always);
+}
+
+template <class T>
+__global__ void report_final_kernel(const TailArgs<T> t, int always) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  report_decide<T>(t.book, t.dpack[4], t.dpack[5], always);
+}
+
+template <class T>
+void launch_report_final(const TailArgs<T>& t, bool always, cudaStream_t st) {
+  report_final_kernel<T><<<1, 32, 0, st>>>(t, always ? 1 : 0);
+  count_launch();
 }
 
 template <class T>
@@ -1372,22 +1510,28 @@ __global__ void init_rows_kernel(const T* xy, const T* p, T* a, int64_t m,
   a[i] = acc - p[i];
 }
 
-// b = col_sums(X0) - q (sequential over rows, matrix.hpp:139-149)
+// b = col_sums(X0) - q (sequential over rows, matrix.hpp:139-149); sharded
+// ranks write the local column partial (q subtracted after the allreduce)
 template <class T>
 __global__ void init_cols_kernel(const T* xy, const T* q, T* b, int64_t m,
-                                 int64_t n, int64_t ld) {
+                                 int64_t n, int64_t ld, int subtract) {
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const T* c = xy + j * ld;
   T acc = T(0);
   for (int64_t i = 0; i < m; ++i) acc += c[i];
-  b[j] = acc - q[j];
+  b[j] = subtract ? acc - q[j] : acc;
 }
 
 template <class T>
 __global__ void init_alpha_kernel(const T* a, const T* b, int64_t m, int64_t n,
-                                  int64_t mn_global, Book<T>* bk) {
+                                  int64_t mn_global, Book<T>* bk, T* shard_pack) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (shard_pack) {  // rank-local sums, finished after the allreduce
+    shard_pack[0] = serial_sum<T, false>(a, m);
+    shard_pack[1] = serial_sum<T, true>(a, m);
+    return;
+  }
   const T alpha = serial_sum<T, false>(a, m) / static_cast<T>(mn_global);
   bk->alpha = alpha;  // solver.hpp:177-178
   bk->beta = alpha;   // solver.hpp:183
@@ -1396,14 +1540,33 @@ __global__ void init_alpha_kernel(const T* a, const T* b, int64_t m, int64_t n,
 }
 
 template <class T>
+__global__ void init_sharded_finish_kernel(T* b, const T* q, int64_t n, const T* pack,
+                                           int64_t mn_global, Book<T>* bk) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int64_t j = 0; j < n; ++j) b[j] = b[j] - q[j];
+  const T alpha = pack[0] / static_cast<T>(mn_global);
+  bk->alpha = alpha;
+  bk->beta = alpha;
+  bk->nr2 = pack[1];
+  bk->ns2 = serial_sum<T, true>(b, n);
+}
+
+template <class T>
+void launch_init_sharded_finish(T* b, const T* q, int64_t n, const T* pack,
+                                int64_t mn_global, Book<T>* book, cudaStream_t st) {
+  init_sharded_finish_kernel<T><<<1, 32, 0, st>>>(b, q, n, pack, mn_global, book);
+  count_launch();
+}
+
+template <class T>
 void launch_init_sums(const T* xy, const T* p, const T* q, T* a, T* b,
                       int64_t m, int64_t n, int64_t ld, Book<T>* book,
-                      cudaStream_t st) {
+                      cudaStream_t st, T* shard_pack) {
   init_rows_kernel<T><<<static_cast<unsigned>((m + 127) / 128), 128, 0, st>>>(
       xy, p, a, m, n, ld);
   init_cols_kernel<T><<<static_cast<unsigned>((n + 127) / 128), 128, 0, st>>>(
-      xy, q, b, m, n, ld);
-  init_alpha_kernel<T><<<1, 32, 0, st>>>(a, b, m, n, m + n, book);
+      xy, q, b, m, n, ld, shard_pack ? 0 : 1);
+  init_alpha_kernel<T><<<1, 32, 0, st>>>(a, b, m, n, m + n, book, shard_pack);
   count_launch(3);
 }
 
@@ -1479,7 +1642,12 @@ void launch_materialize(const T* xy, const T* cost, T* out, T rho, int folded,
                                   int64_t, cudaStream_t);                      \
   template void launch_init_sums<T>(const T*, const T*, const T*, T*, T*,      \
                                     int64_t, int64_t, int64_t, Book<T>*,       \
-                                    cudaStream_t);                             \
+                                    cudaStream_t, T*);                         \
+  template void launch_finish<T>(const TailArgs<T>&, cudaStream_t);            \
+  template void launch_gate<T>(const TailArgs<T>&, cudaStream_t);              \
+  template void launch_report_final<T>(const TailArgs<T>&, bool, cudaStream_t);\
+  template void launch_init_sharded_finish<T>(T*, const T*, int64_t, const T*, \
+                                              int64_t, Book<T>*, cudaStream_t);\
   template void launch_validate<T>(const T*, int64_t, int64_t, int64_t,        \
                                    unsigned long long*, unsigned long long*,   \
                                    cudaStream_t);                              \

@@ -152,21 +152,34 @@ int gen_gaussian_points(int64_t m, int64_t n, double sigma_t, uint64_t seed,
   return 0;
 }
 
+// Rows [row_begin, row_end) of the m x n instance (column-major, leading
+// dimension row_end - row_begin); the normalization uses the global max.
 template <class T>
-int gen_gaussian_cost(int64_t m, int64_t n, double sigma_t, uint64_t seed,
-                      T* C) {
+int gen_gaussian_cost_rows(int64_t m, int64_t n, double sigma_t, uint64_t seed,
+                           int64_t row_begin, int64_t row_end, T* C) {
   std::vector<double> xs, xt;
   double cmax = 0;
   int rc = gen_gaussian_points(m, n, sigma_t, seed, xs, xt, &cmax);
   if (rc) return rc;
+  const int64_t ml = row_end - row_begin;
   parallel_cols(n, [&](int64_t j0, int64_t j1) {
     for (int64_t j = j0; j < j1; ++j) {
-      T* col = C + j * m;
-      for (int64_t i = 0; i < m; ++i)
-        col[i] = static_cast<T>(sqdist(&xs[2 * i], &xt[2 * j]) / cmax);
+      T* col = C + j * ml;
+      for (int64_t i = row_begin; i < row_end; ++i)
+        col[i - row_begin] = static_cast<T>(sqdist(&xs[2 * i], &xt[2 * j]) / cmax);
     }
   });
   return 0;
+}
+template int gen_gaussian_cost_rows<float>(int64_t, int64_t, double, uint64_t, int64_t,
+                                           int64_t, float*);
+template int gen_gaussian_cost_rows<double>(int64_t, int64_t, double, uint64_t, int64_t,
+                                            int64_t, double*);
+
+template <class T>
+int gen_gaussian_cost(int64_t m, int64_t n, double sigma_t, uint64_t seed,
+                      T* C) {
+  return gen_gaussian_cost_rows<T>(m, n, sigma_t, seed, 0, m, C);
 }
 template int gen_gaussian_cost<float>(int64_t, int64_t, double, uint64_t, float*);
 template int gen_gaussian_cost<double>(int64_t, int64_t, double, uint64_t, double*);

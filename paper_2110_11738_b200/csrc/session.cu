@@ -18,10 +18,49 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include "drotb_host.hpp"
 #include "drotb_internal.hpp"
 
 namespace drotb {
+
+// NCCL is bound at run time (dlopen "libnccl.so.2") and only when a sharded
+// session is created, so the library never pins a NCCL build: inside a
+// PyTorch process it shares the NCCL torch already loaded.
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+                            ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+  std::string err;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.err = std::string("dlopen libnccl.so.2: ") + dlerror();
+      return a;
+    }
+    a.getUniqueId = reinterpret_cast<decltype(a.getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    a.commInitRank = reinterpret_cast<decltype(a.commInitRank)>(dlsym(h, "ncclCommInitRank"));
+    a.allReduce = reinterpret_cast<decltype(a.allReduce)>(dlsym(h, "ncclAllReduce"));
+    a.commDestroy = reinterpret_cast<decltype(a.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+    a.getErrorString =
+        reinterpret_cast<decltype(a.getErrorString)>(dlsym(h, "ncclGetErrorString"));
+    a.ok = a.getUniqueId && a.commInitRank && a.allReduce && a.commDestroy && a.getErrorString;
+    if (!a.ok) a.err = "libnccl.so.2 lacks the expected symbols";
+    return a;
+  }();
+  return api;
+}
 
 // ---------------------------------------------------------------------------
 // errors (errors.hpp:48-88)
@@ -69,6 +108,20 @@ const char* last_error_cstr() { return g_err.c_str(); }
     if (rc_) return rc_;      \
   } while (0)
 
+#define NCCL_TRY(expr)                                                        \
+  do {                                                                        \
+    ncclResult_t r_ = (expr);                                                 \
+    if (r_ != ncclSuccess)                                                    \
+      return ::drotb::set_cuda_error(DROTB_ERR_NCCL + static_cast<int>(r_),   \
+                                     std::string("nccl: ") + #expr + ": " +   \
+                                         ::drotb::nccl().getErrorString(r_)); \
+  } while (0)
+
+template <class T>
+constexpr ncclDataType_t nccl_type() {
+  return sizeof(T) == 4 ? ncclFloat32 : ncclFloat64;
+}
+
 template <class P>
 static int dev_alloc(P** ptr, size_t count) {
   *ptr = nullptr;
@@ -102,6 +155,15 @@ struct Session {
   int32_t* h_stop = nullptr;  // pinned, 2 slots
   cudaEvent_t ev[2] = {nullptr, nullptr};
 
+  // row sharding (multi-GPU): this rank holds rows [row_begin, row_begin+m)
+  int rank = 0, world = 1;
+  bool sharded = false;
+  ncclComm_t comm = nullptr;
+  T* pack = nullptr;      // [v (n) | sum r, |r|^2, cost, prev, dual, dx]
+  T* pmax = nullptr;      // [max|t|]
+  double* dpack = nullptr;  // [row-side update sums (4) | report sums (2) | misc]
+  int32_t* dint = nullptr;
+
   std::vector<T> hp, hq;
   T rho = T(0);
   double rho_d = 0;
@@ -122,7 +184,12 @@ struct Session {
   void release() {
     void* bufs[] = {X, C, Xout, phi, varphi, a, b, rb[0], rb[1], sb[0], sb[1],
                     p, q, u, v, ustrip, vstrip, tscr, partials, tiles, dscr,
-                    terms, book, trace, vflags};
+                    terms, book, trace, vflags, pack, pmax, dpack, dint};
+    if (comm) nccl().commDestroy(comm);
+    comm = nullptr;
+    pack = pmax = nullptr;
+    dpack = nullptr;
+    dint = nullptr;
     for (void* ptr : bufs)
       if (ptr) cudaFree(ptr);
     X = C = Xout = phi = varphi = a = b = p = q = u = v = ustrip = vstrip =
@@ -160,6 +227,59 @@ struct Session {
     tc = bs * std::max<int64_t>(1, cfg.work_size);
     if (!exact && !engine) tc = fast_tile_cols();
     return allocate();
+  }
+
+  // Row shard [row_begin, row_end) of an m_global x n problem on `world`
+  // ranks (one process per GPU); collectives over NCCL.
+  int create_sharded(int64_t m_glob, int64_t n_, const drotb_config& c, int rk, int ws,
+                     const char* id128, int64_t r0, int64_t r1) {
+    if (ws < 1 || rk < 0 || rk >= ws || r0 < 0 || r1 <= r0 || r1 > m_glob)
+      return set_error(DROTB_ERRC_BAD_CONFIG, "invalid shard");
+    if (c.order == DROTB_ORDER_REFERENCE)
+      return set_error(DROTB_ERRC_BAD_CONFIG,
+                       "order=reference reproduces the single-threaded CPU tree; "
+                       "row sharding needs order=fast");
+    if (!nccl().ok) return set_error(DROTB_ERRC_BAD_CONFIG, "NCCL unavailable: " + nccl().err);
+    drotb_config c2 = c;
+    c2.use_graphs = 0;  // sharded iterations are enqueued eagerly (NCCL + pause)
+    RC_TRY(create(r1 - r0, n_, c2));
+    m_global = m_glob;
+    row_begin = r0;
+    rank = rk;
+    world = ws;
+    sharded = true;
+    RC_TRY(dev_alloc(&pack, static_cast<size_t>(n + 8)));
+    RC_TRY(dev_alloc(&pmax, 2));
+    RC_TRY(dev_alloc(&dpack, 16));
+    RC_TRY(dev_alloc(&dint, 2));
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    NCCL_TRY(nccl().commInitRank(&comm, world, id, rank));
+    return 0;
+  }
+
+  template <class U>
+  int allreduce(U* buf, size_t count, ncclRedOp_t op) {
+    ncclDataType_t dt = std::is_same<U, double>::value  ? ncclFloat64
+                        : std::is_same<U, float>::value ? ncclFloat32
+                                                        : ncclInt32;
+    NCCL_TRY(nccl().allReduce(buf, buf, count, dt, op, comm, stream));
+    return 0;
+  }
+
+  // Collective error agreement: every rank returns the same code.
+  int agree(int local_rc, const std::string& local_msg) {
+    if (!sharded) return local_rc;
+    int32_t v = local_rc;
+    CUDA_TRY(cudaMemcpyAsync(dint, &v, sizeof(v), cudaMemcpyHostToDevice, stream));
+    RC_TRY(allreduce(dint, 1, ncclMax));
+    CUDA_TRY(cudaMemcpyAsync(&v, dint, sizeof(v), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    if (v == 0) return 0;
+    if (v != local_rc) g_err = "rank " + std::to_string(rank) + ": another rank failed: " +
+                               std::string(v < DROTB_ERR_CUDA ? errc_name(v - 1) : "device error");
+    else g_err = local_msg;
+    return v;
   }
 
   // Fast order is free to pick the u-strip width: enough column tiles for
@@ -209,7 +329,7 @@ struct Session {
       RC_TRY(dev_alloc(&tiles, static_cast<size_t>(n_tiles)));
       RC_TRY(dev_alloc(&terms, static_cast<size_t>(m + n) * 3));
     }
-    RC_TRY(dev_alloc(&dscr, static_cast<size_t>(std::max(tail_blocks * 6, report_blocks * 2))));
+    RC_TRY(dev_alloc(&dscr, static_cast<size_t>(std::max(tail_blocks * 8, report_blocks * 2))));
     RC_TRY(dev_alloc(&book, 1));
     RC_TRY(dev_alloc(&vflags, 2));
     CUDA_TRY(cudaMemsetAsync(book, 0, sizeof(Book<T>), stream));
@@ -303,16 +423,44 @@ struct Session {
     have_problem = true;
     initialized = false;
     if (!validate) return 0;
+    if (!sharded) {
+      unsigned long long nf, ng;
+      RC_TRY(scan_matrix(C, &nf, &ng));
+      if (nf != ~0ull || ng != ~0ull) {
+        if (nf < ng)
+          return set_error(DROTB_ERRC_NON_FINITE_ENTRY, "cost matrix has a non-finite entry");
+        return set_error(DROTB_ERRC_NEGATIVE_COST, "cost matrix has a negative entry");
+      }
+      RC_TRY(check_marginal(hp, "p"));
+      RC_TRY(check_marginal(hq, "q"));
+      return 0;
+    }
+    // sharded: local scans, then a collective verdict (every rank agrees);
+    // the p sum is the allreduce of the rank-local sequential double sums
+    int rc = 0;
     unsigned long long nf, ng;
     RC_TRY(scan_matrix(C, &nf, &ng));
-    if (nf != ~0ull || ng != ~0ull) {
-      if (nf < ng)
-        return set_error(DROTB_ERRC_NON_FINITE_ENTRY, "cost matrix has a non-finite entry");
-      return set_error(DROTB_ERRC_NEGATIVE_COST, "cost matrix has a negative entry");
+    if (nf != ~0ull || ng != ~0ull)
+      rc = nf < ng ? set_error(DROTB_ERRC_NON_FINITE_ENTRY, "cost matrix has a non-finite entry")
+                   : set_error(DROTB_ERRC_NEGATIVE_COST, "cost matrix has a negative entry");
+    double psum = 0;
+    for (T e : hp) {
+      if (rc) break;
+      if (!std::isfinite(static_cast<double>(e)))
+        rc = set_error(DROTB_ERRC_NON_FINITE_ENTRY, "p has a non-finite entry");
+      else if (e < T(0))
+        rc = set_error(DROTB_ERRC_MARGINAL_NOT_SIMPLEX, "p has a negative entry");
+      psum += static_cast<double>(e);
     }
-    RC_TRY(check_marginal(hp, "p"));
-    RC_TRY(check_marginal(hq, "q"));
-    return 0;
+    const std::string msg = g_err;
+    RC_TRY(agree(rc, msg));
+    CUDA_TRY(cudaMemcpyAsync(dpack + 8, &psum, sizeof(double), cudaMemcpyHostToDevice, stream));
+    RC_TRY(allreduce(dpack + 8, 1, ncclSum));
+    CUDA_TRY(cudaMemcpyAsync(&psum, dpack + 8, sizeof(double), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    if (std::abs(psum - 1.0) > 1e-12)
+      return set_error(DROTB_ERRC_MARGINAL_NOT_SIMPLEX, "p sums to " + std::to_string(psum));
+    return check_marginal(hq, "q");
   }
 
   int resolve_rho() {  // DrotConfig::resolved_rho, solver.hpp:77-83
@@ -341,9 +489,12 @@ struct Session {
       RC_TRY(upload_matrix(X, x0, x0_is_device));
       unsigned long long nf, ng;
       RC_TRY(scan_matrix(X, &nf, &ng));
+      int rc = 0;
       if (nf != ~0ull || ng != ~0ull)
-        return set_error(DROTB_ERRC_INVALID_INITIAL_PLAN,
-                         "initial plan must be nonnegative and finite");
+        rc = set_error(DROTB_ERRC_INVALID_INITIAL_PLAN,
+                       "initial plan must be nonnegative and finite");
+      const std::string msg = g_err;
+      RC_TRY(agree(rc, msg));
     } else {
       launch_init_x0<T>(X, p, q, m, n, ld, stream);
     }
@@ -375,14 +526,28 @@ struct Session {
     hb.tol_primal = cfg.tol_primal;
     hb.tol_dual = cfg.tol_dual;
     hb.tol_gap = cfg.tol_gap;
-    const double p_norm = std::sqrt(static_cast<double>(host_norm_sq(hp)));
+    double p_norm2 = static_cast<double>(host_norm_sq(hp));
+    if (sharded) {  // global |p|^2 (allreduce of the rank-local T sums)
+      CUDA_TRY(cudaMemcpyAsync(dpack + 9, &p_norm2, sizeof(double), cudaMemcpyHostToDevice, stream));
+      RC_TRY(allreduce(dpack + 9, 1, ncclSum));
+      CUDA_TRY(cudaMemcpyAsync(&p_norm2, dpack + 9, sizeof(double), cudaMemcpyDeviceToHost, stream));
+      CUDA_TRY(cudaStreamSynchronize(stream));
+    }
+    const double p_norm = std::sqrt(p_norm2);
     const double q_norm = std::sqrt(static_cast<double>(host_norm_sq(hq)));
     hb.primal_scale = cfg.relative_tolerances ? 1.0 / (1.0 + p_norm + q_norm) : 1.0;
     hb.record_trace = cfg.record_trace ? 1 : 0;
     hb.relative = cfg.relative_tolerances ? 1 : 0;
     if (cfg.max_iters <= 0) hb.stop = 1;
     CUDA_TRY(cudaMemcpyAsync(book, &hb, sizeof(hb), cudaMemcpyHostToDevice, stream));
-    launch_init_sums<T>(X, p, q, a, b, m, n, ld, book, stream);
+    if (sharded) {  // column sums and sum(a) span all ranks
+      launch_init_sums<T>(X, p, q, a, b, m, n, ld, book, stream, pack);
+      RC_TRY(allreduce(b, static_cast<size_t>(n), ncclSum));
+      RC_TRY(allreduce(pack, 2, ncclSum));
+      launch_init_sharded_finish<T>(b, q, n, pack, m_global + n_global, book, stream);
+    } else {
+      launch_init_sums<T>(X, p, q, a, b, m, n, ld, book, stream);
+    }
     CUDA_TRY(cudaMemcpyAsync(rb[0], a, sizeof(T) * ld, cudaMemcpyDeviceToDevice, stream));
     CUDA_TRY(cudaMemcpyAsync(sb[0], b, sizeof(T) * n, cudaMemcpyDeviceToDevice, stream));
     CUDA_TRY(cudaGetLastError());
@@ -468,6 +633,11 @@ struct Session {
     t.trace = trace;
     t.tile_partials = tiles;
     t.n_tiles = n_tiles;
+    t.sharded = sharded ? 1 : 0;
+    t.pack = pack;
+    t.pmax = pmax;
+    t.dpack = dpack;
+    if (sharded) t.v = pack;  // the merge writes the local v partial into the pack
     return t;
   }
 
@@ -493,6 +663,17 @@ struct Session {
     if (pass_end) CUDA_TRY(cudaEventRecordWithFlags(pass_end, stream, evf));
     TailArgs<T> ta = tail_args(k, mode, folded_after, true);
     launch_merge<T>(ta, exact, stream);
+    if (sharded) {  // one exchange per phase; gate pauses for confirm
+      RC_TRY(allreduce(pack, static_cast<size_t>(n + 6), ncclSum));
+      RC_TRY(allreduce(pmax, 1, ncclMax));
+      launch_finish<T>(ta, stream);
+      launch_update<T>(ta, false, stream);
+      RC_TRY(allreduce(dpack, 4, ncclSum));
+      launch_gate<T>(ta, stream);
+      h_iter = k + 1;
+      h_folded = folded_after;
+      return 0;
+    }
     if (cond_out) {  // graph build: the report goes into an IF node body
       ta.cond = *cond_out;
       ta.use_cond = 1;
@@ -610,7 +791,7 @@ struct Session {
   }
 
   bool graph_ok(int64_t len) const {
-    return cfg.use_graphs && len >= 2 && (len & 1) == 0 && (h_iter & 1) == 0 && !h_folded;
+    return !sharded && cfg.use_graphs && len >= 2 && (len & 1) == 0 && (h_iter & 1) == 0 && !h_folded;
   }
 
   int enqueue(int64_t n_iters) {
@@ -706,8 +887,42 @@ struct Session {
   // Runs the loop until the device raises its stop flag (converged,
   // max_iters, numerical failure).  The host polls one batch behind so the
   // GPU queue never drains.
+  // Sharded confirm after a gate pause (stop == 2): the exact report's sums
+  // over all ranks, then the replicated decision (stop -> 1 or back to 0).
+  int sharded_report(bool always) {
+    Book<T> hb;
+    RC_TRY(read_book(&hb));
+    TailArgs<T> ta = tail_args(hb.iter, kPlain0, hb.folded != 0, true);
+    launch_report<T>(X, C, ta, false, always, stream);
+    RC_TRY(allreduce(dpack + 4, 2, ncclSum));
+    launch_report_final<T>(ta, always, stream);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
+
+  int run_sharded() {
+    const int64_t bi = batch_iters();
+    const int64_t limit = std::max<int64_t>(cfg.max_iters, 0) + 4 * bi + 4;
+    int64_t guard = 0;
+    while (true) {
+      RC_TRY(enqueue(bi));
+      Book<T> hb;
+      RC_TRY(read_book(&hb));
+      if (hb.stop == 2) {
+        RC_TRY(sharded_report(false));
+        RC_TRY(read_book(&hb));
+      }
+      h_iter = hb.iter;  // the batch may have run past a pause: resync
+      h_folded = hb.folded != 0;
+      if (hb.stop == 1) break;
+      if ((guard += bi) > limit) break;
+    }
+    return 0;
+  }
+
   int run() {
     if (!initialized) return set_error(DROTB_ERRC_BAD_CONFIG, "session not initialized");
+    if (sharded) return run_sharded();
     const int64_t bi = batch_iters();
     int slot = 0;
     bool pending = false;
@@ -743,9 +958,13 @@ struct Session {
     if (hb.converged) st = DROTB_CONVERGED;
     if (hb.failed) st = DROTB_NUMERICAL_FAILURE;
     if (st == DROTB_MAX_ITERS) {
-      TailArgs<T> ta = tail_args(hb.iter, kPlain0, hb.folded != 0, true);
-      launch_report<T>(X, C, ta, exact, true, stream);
-      CUDA_TRY(cudaGetLastError());
+      if (sharded) {
+        RC_TRY(sharded_report(true));
+      } else {
+        TailArgs<T> ta = tail_args(hb.iter, kPlain0, hb.folded != 0, true);
+        launch_report<T>(X, C, ta, exact, true, stream);
+        CUDA_TRY(cudaGetLastError());
+      }
       RC_TRY(read_book(&hb));
     }
     if (status) *status = st;
@@ -1295,22 +1514,23 @@ int drotb_session_gen_gaussian(drotb_session* s, double sigma_t, uint64_t seed,
     T* hostC = nullptr;
     CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&hostC), sizeof(T) * m * n));
     std::unique_ptr<T, decltype(&cudaFreeHost)> hold(hostC, &cudaFreeHost);
-    RC_TRY(drotb::gen_gaussian_cost<T>(m, n, sigma_t, seed, hostC));
-    std::vector<T> p(static_cast<size_t>(m)), q(static_cast<size_t>(n));
+    const int64_t mg = ss->m_global, r0 = ss->row_begin;
+    RC_TRY(drotb::gen_gaussian_cost_rows<T>(mg, n, sigma_t, seed, r0, r0 + m, hostC));
+    std::vector<T> pg(static_cast<size_t>(mg)), q(static_cast<size_t>(n));
     if (marginals == 1) {
-      RC_TRY(drotb::dyadic_marginal<T>(m, p.data()));
+      RC_TRY(drotb::dyadic_marginal<T>(mg, pg.data()));
       RC_TRY(drotb::dyadic_marginal<T>(n, q.data()));
     } else if (marginals == 2) {
-      std::vector<double> pd(static_cast<size_t>(m)), qd(static_cast<size_t>(n));
-      drotb::dirichlet_marginal(seed, 4, m, pd.data());
+      std::vector<double> pd(static_cast<size_t>(mg)), qd(static_cast<size_t>(n));
+      drotb::dirichlet_marginal(seed, 4, mg, pd.data());
       drotb::dirichlet_marginal(seed, 5, n, qd.data());
-      for (int64_t i = 0; i < m; ++i) p[i] = static_cast<T>(pd[i]);
+      for (int64_t i = 0; i < mg; ++i) pg[i] = static_cast<T>(pd[i]);
       for (int64_t j = 0; j < n; ++j) q[j] = static_cast<T>(qd[j]);
     } else {
-      for (int64_t i = 0; i < m; ++i) p[i] = static_cast<T>(1.0 / static_cast<double>(m));
+      for (int64_t i = 0; i < mg; ++i) pg[i] = static_cast<T>(1.0 / static_cast<double>(mg));
       for (int64_t j = 0; j < n; ++j) q[j] = static_cast<T>(1.0 / static_cast<double>(n));
     }
-    return ss->set_problem(hostC, p.data(), q.data(), false, true);
+    return ss->set_problem(hostC, pg.data() + r0, q.data(), false, true);
   };
   try {
     if (s->precision == 0) return go(drotb::as_session<float>(s->impl));
@@ -1390,15 +1610,54 @@ int drotb_session_run_timed(drotb_session* s, int64_t n_iters, double* total_ms,
 }
 
 int drotb_nccl_unique_id(char* out128) {
-  (void)out128;
-  return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "multi-GPU sharding not built");
+  drotb::clear_error();
+  if (!drotb::nccl().ok)
+    return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "NCCL unavailable: " + drotb::nccl().err);
+  ncclUniqueId id;
+  NCCL_TRY(drotb::nccl().getUniqueId(&id));
+  static_assert(sizeof(id) == DROTB_NCCL_ID_BYTES, "ncclUniqueId size");
+  std::memcpy(out128, &id, sizeof(id));
+  return 0;
 }
 
-int drotb_session_shard(drotb_session* s, int32_t rank, int32_t world_size,
-                        const char* nccl_id128, int64_t row_begin,
-                        int64_t row_end) {
-  (void)s; (void)rank; (void)world_size; (void)nccl_id128; (void)row_begin; (void)row_end;
-  return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "multi-GPU sharding not built");
+int drotb_session_create_sharded(drotb_session** s, int64_t m_global, int64_t n,
+                                 int32_t precision, const drotb_config* cfgp, int32_t rank,
+                                 int32_t world_size, const char* nccl_id128,
+                                 int64_t row_begin, int64_t row_end) {
+  drotb::clear_error();
+  *s = nullptr;
+  const drotb_config cfg = effective(cfgp);
+  try {
+    std::unique_ptr<drotb_session> h(new drotb_session{precision, nullptr});
+    if (precision == 0) {
+      std::unique_ptr<Session<float>> ss(new Session<float>());
+      RC_TRY(ss->create_sharded(m_global, n, cfg, rank, world_size, nccl_id128, row_begin,
+                                row_end));
+      h->impl = ss.release();
+    } else {
+      std::unique_ptr<Session<double>> ss(new Session<double>());
+      RC_TRY(ss->create_sharded(m_global, n, cfg, rank, world_size, nccl_id128, row_begin,
+                                row_end));
+      h->impl = ss.release();
+    }
+    *s = h.release();
+    return 0;
+  } catch (const std::exception& e) {
+    return guard_exceptions(e);
+  }
+}
+
+int drotb_shard_rows(int64_t m, int32_t world_size, int32_t rank, int64_t* row_begin,
+                     int64_t* row_end) {
+  // contiguous row blocks aligned to the 64-row v blocks, as even as possible
+  drotb::clear_error();
+  if (world_size < 1 || rank < 0 || rank >= world_size || m < 1)
+    return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "invalid shard request");
+  const int64_t blocks = (m + 63) / 64;
+  const int64_t b0 = blocks * rank / world_size, b1 = blocks * (rank + 1) / world_size;
+  *row_begin = std::min<int64_t>(m, b0 * 64);
+  *row_end = std::min<int64_t>(m, b1 * 64);
+  return 0;
 }
 
 }  // extern "C"

@@ -18,6 +18,19 @@ from .api import (DrotConfig, Error, Errc, ResidualReport, SolveStatus, _check, 
 from ._lib import drotb_report
 
 
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(_lib.load().drotb_nccl_unique_id(buf))
+    return buf.raw
+
+
+def shard_rows(m: int, world: int, rank: int):
+    """Row range of `rank` (contiguous, 64-row aligned, balanced)."""
+    r0, r1 = C.c_int64(0), C.c_int64(0)
+    _check(_lib.load().drotb_shard_rows(int(m), int(world), int(rank), C.byref(r0), C.byref(r1)))
+    return int(r0.value), int(r1.value)
+
+
 class Session:
     MARGINALS = {"uniform": 0, "dyadic": 1, "dirichlet": 2}
 
@@ -31,6 +44,24 @@ class Session:
         _check(lib.drotb_session_create(C.byref(h), self.m, self.n,
                                         0 if self.dtype == np.float32 else 1, C.byref(ccfg)))
         self._h = h
+
+    @classmethod
+    def sharded(cls, m_global: int, n: int, dtype, cfg: Optional[DrotConfig], rank: int,
+                world: int, nccl_id: bytes, row_begin: int, row_end: int) -> "Session":
+        """Row shard [row_begin, row_end) of an m_global x n problem (one process
+        per GPU, NCCL collectives)."""
+        self = cls.__new__(cls)
+        self.m, self.n = int(row_end - row_begin), int(n)
+        self.m_global, self.row_begin = int(m_global), int(row_begin)
+        self.dtype = np.dtype(dtype)
+        self.cfg = cfg or DrotConfig()
+        h = C.c_void_p()
+        ccfg = self.cfg.to_c()
+        _check(_lib.load().drotb_session_create_sharded(
+            C.byref(h), int(m_global), int(n), 0 if self.dtype == np.float32 else 1,
+            C.byref(ccfg), int(rank), int(world), nccl_id, int(row_begin), int(row_end)))
+        self._h = h
+        return self
 
     def close(self):
         if getattr(self, "_h", None):
