@@ -274,10 +274,20 @@ int drotb_session_set_stream(drotb_session* s, void* stream);
  * session's precision.  Validates exactly like check_problem. */
 int drotb_session_set_problem(drotb_session* s, const void* C, const void* p,
                               const void* q, int32_t is_device);
-/* Generate the Gaussian instance on the host generator and upload it with
- * uniform (0) or dyadic-uniform (1) or Dirichlet (2) marginals. */
+/* Generate gen_gaussian_problem(m_global, n, sigma_t, seed)'s cost ON THE
+ * DEVICE (K7, bit-identical to probgen.hpp:131-180 cast to the session's
+ * precision; a shard generates its rows, normalized by the global max), with
+ * marginals: 0 uniform 1/m, 1 dyadic-uniform, 2 Dirichlet (probgen.hpp:
+ * 115-127), 3 random_simplex(seed^0x1111 / seed^0x2222) (oracles.hpp:137-147).
+ * Validates like check_problem. */
 int drotb_session_gen_gaussian(drotb_session* s, double sigma_t, uint64_t seed,
                                int32_t marginals);
+/* random_matrix(m_global, n, seed, lo, hi) (oracles.hpp:128-135) generated on
+ * the device in the global column-major storage order; marginals as above. */
+int drotb_session_gen_uniform(drotb_session* s, uint64_t seed, double lo, double hi,
+                              int32_t marginals);
+/* Copy the session's (local) cost matrix to host, m x n column-major. */
+int drotb_session_get_cost(drotb_session* s, void* out);
 /* init_state (x0 host pointer or NULL); resets the solve bookkeeping. */
 int drotb_session_init(drotb_session* s, const void* x0);
 /* Enqueue up to n_iters iterations of the solve loop (gating included) on

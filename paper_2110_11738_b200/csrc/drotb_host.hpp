@@ -19,6 +19,9 @@ void clear_error();
 const char* last_error_cstr();
 const char* errc_name(int errc);
 
+int gaussian_points(int64_t m, int64_t n, double sigma_t, uint64_t seed,
+                    std::vector<double>& xs, std::vector<double>& xt);
+void random_simplex(int64_t count, uint64_t seed, double* w);
 int gen_gaussian_points(int64_t m, int64_t n, double sigma_t, uint64_t seed,
                         std::vector<double>& xs, std::vector<double>& xt,
                         double* cmax_out);

@@ -176,6 +176,17 @@ void launch_materialize(const T* xy, const T* cost, T* out, T rho,
                         int folded, int64_t m, int64_t n, int64_t ld,
                         cudaStream_t st);
 
+// ---- K7 on-device problem generation (probgen.cu) -------------------------
+void launch_gaussian_cmax(const double* xs, const double* xt, int64_t m, int64_t n,
+                          unsigned long long* cmax_bits, cudaStream_t st);
+template <class T>
+void launch_gaussian_cost(const double* xs_local, const double* xt, int64_t m, int64_t n,
+                          int64_t ld, const unsigned long long* cmax_bits, T* C,
+                          cudaStream_t st);
+template <class T>
+void launch_uniform_cost(uint64_t seed, double lo, double hi, int64_t m, int64_t m_global,
+                         int64_t row_begin, int64_t n, int64_t ld, T* C, cudaStream_t st);
+
 int64_t kernel_launch_count();
 void count_launch(int64_t k = 1);
 

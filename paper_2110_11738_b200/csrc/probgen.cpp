@@ -125,9 +125,10 @@ inline double sqdist(const double* a, const double* b) {
 
 }  // namespace
 
-int gen_gaussian_points(int64_t m, int64_t n, double sigma_t, uint64_t seed,
-                        std::vector<double>& xs, std::vector<double>& xt,
-                        double* cmax_out) {
+// The m source and n target points (probgen.hpp:150-153), interleaved
+// (x, y) per point.  O(m+n): the O(m*n) cost runs on the device (probgen.cu).
+int gaussian_points(int64_t m, int64_t n, double sigma_t, uint64_t seed,
+                    std::vector<double>& xs, std::vector<double>& xt) {
   if (m <= 0 || n <= 0)
     return set_error(DROTB_ERRC_EMPTY_DIMENSION, "gen_gaussian_problem");
   if (!(sigma_t > 0)) return set_error(DROTB_ERRC_BAD_CONFIG, "sigma_t must be positive");
@@ -135,6 +136,14 @@ int gen_gaussian_points(int64_t m, int64_t n, double sigma_t, uint64_t seed,
   const Cloud tgt = cloud_params(seed, 2, 3, 5.0, sigma_t);
   cloud_points(seed, src, m, 100, xs);
   cloud_points(seed, tgt, n, 100 + static_cast<uint64_t>(m), xt);
+  return 0;
+}
+
+int gen_gaussian_points(int64_t m, int64_t n, double sigma_t, uint64_t seed,
+                        std::vector<double>& xs, std::vector<double>& xt,
+                        double* cmax_out) {
+  int rc = gaussian_points(m, n, sigma_t, seed, xs, xt);
+  if (rc) return rc;
   // cmax = max_ij |C_ij| of the unnormalized cost (probgen.hpp:378-379)
   std::vector<double> colmax(static_cast<size_t>(n), 0.0);
   parallel_cols(n, [&](int64_t j0, int64_t j1) {
@@ -190,6 +199,18 @@ void dirichlet_marginal(uint64_t seed, uint64_t stream, int64_t count,
   double total = 0;
   for (int64_t k = 0; k < count; ++k) {
     w[k] = -std::log(s.unit_open());
+    total += w[k];
+  }
+  for (int64_t k = 0; k < count; ++k) w[k] /= total;
+}
+
+// drot_tests::random_simplex (oracles.hpp:137-147): 0.05 + next_unit(),
+// sequential double total, then w /= total.
+void random_simplex(int64_t count, uint64_t seed, double* w) {
+  double total = 0;
+  for (int64_t k = 0; k < count; ++k) {
+    const uint64_t z = mix64(seed + static_cast<uint64_t>(k + 1) * kGolden);
+    w[k] = 0.05 + static_cast<double>(z >> 11) * 0x1.0p-53;
     total += w[k];
   }
   for (int64_t k = 0; k < count; ++k) w[k] /= total;

@@ -411,7 +411,7 @@ struct Session {
   // set_problem + check_problem (problem.hpp:122-136)
   int set_problem(const T* C_, const T* p_, const T* q_, bool is_device,
                   bool validate) {
-    RC_TRY(upload_matrix(C, C_, is_device));
+    if (C_) RC_TRY(upload_matrix(C, C_, is_device));  // nullptr: C generated in place
     hp.assign(static_cast<size_t>(m), T(0));
     hq.assign(static_cast<size_t>(n), T(0));
     const cudaMemcpyKind k = is_device ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost;
@@ -1298,6 +1298,42 @@ int check_problem_t(const T* C, int64_t m, int64_t n, const T* p, const T* q) {
 
 }  // namespace
 
+// Marginals of the generated instances (rank-local slice of p, all of q).
+//   0 uniform 1/m (gen_gaussian_problem, probgen.hpp:163-164)
+//   1 dyadic-exact uniform (passes the 1e-12 check in fp32)
+//   2 Dirichlet(1..1) (probgen.hpp:115-127, substreams 4 and 5)
+//   3 random_simplex(seed ^ 0x1111), random_simplex(seed ^ 0x2222)
+//     (oracles.hpp:137-147, the pattern of test_reference.cpp:22-29)
+namespace drotb {
+template <class T>
+static int gen_marginals(int64_t mg, int64_t n, uint64_t seed, int32_t kind,
+                         std::vector<T>& pg, std::vector<T>& q) {
+  pg.assign(static_cast<size_t>(mg), T(0));
+  q.assign(static_cast<size_t>(n), T(0));
+  if (kind == 1) {
+    RC_TRY(dyadic_marginal<T>(mg, pg.data()));
+    RC_TRY(dyadic_marginal<T>(n, q.data()));
+  } else if (kind == 2 || kind == 3) {
+    std::vector<double> pd(static_cast<size_t>(mg)), qd(static_cast<size_t>(n));
+    if (kind == 2) {
+      dirichlet_marginal(seed, 4, mg, pd.data());
+      dirichlet_marginal(seed, 5, n, qd.data());
+    } else {
+      random_simplex(mg, seed ^ 0x1111u, pd.data());
+      random_simplex(n, seed ^ 0x2222u, qd.data());
+    }
+    for (int64_t i = 0; i < mg; ++i) pg[i] = static_cast<T>(pd[i]);
+    for (int64_t j = 0; j < n; ++j) q[j] = static_cast<T>(qd[j]);
+  } else if (kind == 0) {
+    for (int64_t i = 0; i < mg; ++i) pg[i] = static_cast<T>(1.0 / static_cast<double>(mg));
+    for (int64_t j = 0; j < n; ++j) q[j] = static_cast<T>(1.0 / static_cast<double>(n));
+  } else {
+    return set_error(DROTB_ERRC_BAD_CONFIG, "unknown marginal kind");
+  }
+  return 0;
+}
+}  // namespace drotb
+
 extern "C" {
 
 int32_t drotb_abi_version(void) { return DROTB_ABI_VERSION; }
@@ -1505,32 +1541,40 @@ int drotb_session_set_problem(drotb_session* s, const void* C, const void* p,
       static_cast<const double*>(q), is_device != 0, true);
 }
 
+// K7: the Gaussian instance generated on the device (probgen.cu); only the
+// O(m+n) points and marginals are drawn on the host.
 int drotb_session_gen_gaussian(drotb_session* s, double sigma_t, uint64_t seed,
                                int32_t marginals) {
   drotb::clear_error();
   auto go = [&](auto* ss) -> int {
     using T = typename std::remove_pointer<decltype(ss->X)>::type;
-    const int64_t m = ss->m, n = ss->n;
-    T* hostC = nullptr;
-    CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&hostC), sizeof(T) * m * n));
-    std::unique_ptr<T, decltype(&cudaFreeHost)> hold(hostC, &cudaFreeHost);
-    const int64_t mg = ss->m_global, r0 = ss->row_begin;
-    RC_TRY(drotb::gen_gaussian_cost_rows<T>(mg, n, sigma_t, seed, r0, r0 + m, hostC));
-    std::vector<T> pg(static_cast<size_t>(mg)), q(static_cast<size_t>(n));
-    if (marginals == 1) {
-      RC_TRY(drotb::dyadic_marginal<T>(mg, pg.data()));
-      RC_TRY(drotb::dyadic_marginal<T>(n, q.data()));
-    } else if (marginals == 2) {
-      std::vector<double> pd(static_cast<size_t>(mg)), qd(static_cast<size_t>(n));
-      drotb::dirichlet_marginal(seed, 4, mg, pd.data());
-      drotb::dirichlet_marginal(seed, 5, n, qd.data());
-      for (int64_t i = 0; i < mg; ++i) pg[i] = static_cast<T>(pd[i]);
-      for (int64_t j = 0; j < n; ++j) q[j] = static_cast<T>(qd[j]);
-    } else {
-      for (int64_t i = 0; i < mg; ++i) pg[i] = static_cast<T>(1.0 / static_cast<double>(mg));
-      for (int64_t j = 0; j < n; ++j) q[j] = static_cast<T>(1.0 / static_cast<double>(n));
-    }
-    return ss->set_problem(hostC, pg.data() + r0, q.data(), false, true);
+    const int64_t m = ss->m, n = ss->n, mg = ss->m_global, r0 = ss->row_begin;
+    std::vector<double> xs, xt;
+    RC_TRY(drotb::gaussian_points(mg, n, sigma_t, seed, xs, xt));
+    double* dpts = nullptr;
+    unsigned long long* dmax = nullptr;
+    CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&dpts), sizeof(double) * 2 * (mg + n) + 16));
+    std::unique_ptr<double, decltype(&cudaFree)> hold(dpts, &cudaFree);
+    dmax = reinterpret_cast<unsigned long long*>(dpts + 2 * (mg + n));
+    double* dxs = dpts;
+    double* dxt = dpts + 2 * mg;
+    CUDA_TRY(cudaMemcpyAsync(dxs, xs.data(), sizeof(double) * 2 * mg, cudaMemcpyHostToDevice,
+                             ss->stream));
+    CUDA_TRY(cudaMemcpyAsync(dxt, xt.data(), sizeof(double) * 2 * n, cudaMemcpyHostToDevice,
+                             ss->stream));
+    drotb::launch_gaussian_cmax(dxs, dxt, mg, n, dmax, ss->stream);
+    unsigned long long bits = 0;
+    CUDA_TRY(cudaMemcpyAsync(&bits, dmax, sizeof(bits), cudaMemcpyDeviceToHost, ss->stream));
+    CUDA_TRY(cudaStreamSynchronize(ss->stream));
+    double cmax;
+    std::memcpy(&cmax, &bits, sizeof(cmax));
+    if (!(cmax > 0)) return drotb::set_error(DROTB_ERRC_DEGENERATE_COST, "all samples coincide");
+    drotb::launch_gaussian_cost<T>(dxs + 2 * r0, dxt, m, n, ss->ld, dmax, ss->C, ss->stream);
+    CUDA_TRY(cudaGetLastError());
+    std::vector<T> pg, q;
+    RC_TRY(drotb::gen_marginals<T>(mg, n, seed, marginals, pg, q));
+    RC_TRY(ss->set_problem(nullptr, pg.data() + r0, q.data(), false, true));
+    return 0;
   };
   try {
     if (s->precision == 0) return go(drotb::as_session<float>(s->impl));
@@ -1538,6 +1582,41 @@ int drotb_session_gen_gaussian(drotb_session* s, double sigma_t, uint64_t seed,
   } catch (const std::exception& e) {
     return guard_exceptions(e);
   }
+}
+
+// K7: random_matrix(m, n, seed, lo, hi) (oracles.hpp:128-135) generated on
+// the device, in the global storage order (shards generate their rows).
+int drotb_session_gen_uniform(drotb_session* s, uint64_t seed, double lo, double hi,
+                              int32_t marginals) {
+  drotb::clear_error();
+  auto go = [&](auto* ss) -> int {
+    using T = typename std::remove_pointer<decltype(ss->X)>::type;
+    const int64_t m = ss->m, n = ss->n, mg = ss->m_global, r0 = ss->row_begin;
+    drotb::launch_uniform_cost<T>(seed, lo, hi, m, mg, r0, n, ss->ld, ss->C, ss->stream);
+    CUDA_TRY(cudaGetLastError());
+    std::vector<T> pg, q;
+    RC_TRY(drotb::gen_marginals<T>(mg, n, seed, marginals, pg, q));
+    RC_TRY(ss->set_problem(nullptr, pg.data() + r0, q.data(), false, true));
+    return 0;
+  };
+  try {
+    if (s->precision == 0) return go(drotb::as_session<float>(s->impl));
+    return go(drotb::as_session<double>(s->impl));
+  } catch (const std::exception& e) {
+    return guard_exceptions(e);
+  }
+}
+
+// Download the session's (local) cost matrix, column-major m x n (tests of
+// the on-device generator; the solver never needs it on the host).
+int drotb_session_get_cost(drotb_session* s, void* out) {
+  drotb::clear_error();
+  if (s->precision == 0) {
+    auto* ss = drotb::as_session<float>(s->impl);
+    return ss->download_matrix(static_cast<float*>(out), ss->C);
+  }
+  auto* ss = drotb::as_session<double>(s->impl);
+  return ss->download_matrix(static_cast<double*>(out), ss->C);
 }
 
 int drotb_session_init(drotb_session* s, const void* x0) {

@@ -32,7 +32,7 @@ def shard_rows(m: int, world: int, rank: int):
 
 
 class Session:
-    MARGINALS = {"uniform": 0, "dyadic": 1, "dirichlet": 2}
+    MARGINALS = {"uniform": 0, "dyadic": 1, "dirichlet": 2, "random_simplex": 3}
 
     def __init__(self, m: int, n: int, dtype=np.float32, cfg: Optional[DrotConfig] = None):
         self.m, self.n = int(m), int(n)
@@ -96,6 +96,18 @@ class Session:
     def gen_gaussian(self, sigma_t: float = 5.0, seed: int = 0, marginals: str = "dyadic"):
         _check(_lib.load().drotb_session_gen_gaussian(self._h, sigma_t, seed,
                                                       self.MARGINALS[marginals]))
+
+    def gen_uniform(self, seed: int = 1, lo: float = 0.0, hi: float = 1.0,
+                    marginals: str = "uniform"):
+        """random_matrix(m, n, seed, lo, hi) generated on the device (K7)."""
+        _check(_lib.load().drotb_session_gen_uniform(self._h, int(seed), float(lo), float(hi),
+                                                     self.MARGINALS[marginals]))
+
+    def cost(self) -> np.ndarray:
+        """The session's (local rows of the) cost matrix, copied to the host."""
+        out = np.empty((self.m, self.n), self.dtype, order="F")
+        _check(_lib.load().drotb_session_get_cost(self._h, _p(out)))
+        return out
 
     def init(self, x0: Optional[np.ndarray] = None):
         x = None if x0 is None else _cm(x0, self.dtype)
