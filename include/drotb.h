@@ -286,6 +286,11 @@ int drotb_session_gen_gaussian(drotb_session* s, double sigma_t, uint64_t seed,
  * the device in the global column-major storage order; marginals as above. */
 int drotb_session_gen_uniform(drotb_session* s, uint64_t seed, double lo, double hi,
                               int32_t marginals);
+/* Support of the current plan (materialize_plan values, solver.hpp:204-217):
+ * xmax = max x_ij and nnz = #{x_ij > max(abs_tau, rel_tau * xmax)}, over all
+ * ranks when row-sharded (collective).  SURVEY §8(c) support parity. */
+int drotb_session_support(drotb_session* s, double rel_tau, double abs_tau, int64_t* nnz,
+                          double* xmax);
 /* Copy the session's (local) cost matrix to host, m x n column-major. */
 int drotb_session_get_cost(drotb_session* s, void* out);
 /* init_state (x0 host pointer or NULL); resets the solve bookkeeping. */

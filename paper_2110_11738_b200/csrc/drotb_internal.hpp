@@ -176,6 +176,13 @@ void launch_materialize(const T* xy, const T* cost, T* out, T rho,
                         int folded, int64_t m, int64_t n, int64_t ld,
                         cudaStream_t st);
 
+template <class T>
+void launch_plan_max(const T* xy, const T* cost, T rho, int folded, int64_t m, int64_t n,
+                     int64_t ld, unsigned long long* stats, cudaStream_t st);
+template <class T>
+void launch_plan_count(const T* xy, const T* cost, T rho, int folded, int64_t m, int64_t n,
+                       int64_t ld, double thr, unsigned long long* stats, cudaStream_t st);
+
 // ---- K7 on-device problem generation (probgen.cu) -------------------------
 void launch_gaussian_cmax(const double* xs, const double* xt, int64_t m, int64_t n,
                           unsigned long long* cmax_bits, cudaStream_t st);

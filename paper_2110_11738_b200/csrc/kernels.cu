@@ -1628,6 +1628,66 @@ void launch_materialize(const T* xy, const T* cost, T* out, T rho, int folded,
   count_launch();
 }
 
+// ---------------------------------------------------------------------------
+// Support of the materialized plan (SURVEY §8(c) sparsity-support parity):
+// stats[0] = bits of max_ij x_ij (x >= 0 orders like its bit pattern),
+// then stats[1] = #{x_ij > thr}.  x is the materialize_plan value (unfolded
+// and clamped when the array holds X - rho C, solver.hpp:204-217).
+// ---------------------------------------------------------------------------
+template <class T>
+__device__ __forceinline__ T plan_value(const T* xy, const T* cost, T rho, int folded,
+                                        int64_t off) {
+  const T x = xy[off];
+  if (!folded) return x;
+  const T v = x + rho * cost[off];
+  return v > T(0) ? v : T(0);
+}
+
+template <class T>
+__global__ void __launch_bounds__(256)
+    plan_max_kernel(const T* xy, const T* cost, T rho, int folded, int64_t m, int64_t n,
+                    int64_t ld, unsigned long long* stats) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double mx = 0.0;
+  if (i < m)
+    for (int64_t j = blockIdx.y; j < n; j += gridDim.y)
+      mx = fmax(mx, static_cast<double>(plan_value(xy, cost, rho, folded, j * ld + i)));
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0)
+    atomicMax(stats, static_cast<unsigned long long>(__double_as_longlong(mx)));
+}
+
+template <class T>
+__global__ void __launch_bounds__(256)
+    plan_count_kernel(const T* xy, const T* cost, T rho, int folded, int64_t m, int64_t n,
+                      int64_t ld, double thr, unsigned long long* stats) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  unsigned long long c = 0;
+  if (i < m)
+    for (int64_t j = blockIdx.y; j < n; j += gridDim.y)
+      c += static_cast<double>(plan_value(xy, cost, rho, folded, j * ld + i)) > thr ? 1 : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(stats + 1, c);
+}
+
+template <class T>
+void launch_plan_max(const T* xy, const T* cost, T rho, int folded, int64_t m, int64_t n,
+                     int64_t ld, unsigned long long* stats, cudaStream_t st) {
+  cudaMemsetAsync(stats, 0, 2 * sizeof(unsigned long long), st);
+  dim3 grid(static_cast<unsigned>((m + 255) / 256), static_cast<unsigned>(imin64(n, 1024)));
+  plan_max_kernel<T><<<grid, 256, 0, st>>>(xy, cost, rho, folded, m, n, ld, stats);
+  count_launch();
+}
+
+template <class T>
+void launch_plan_count(const T* xy, const T* cost, T rho, int folded, int64_t m, int64_t n,
+                       int64_t ld, double thr, unsigned long long* stats, cudaStream_t st) {
+  dim3 grid(static_cast<unsigned>((m + 255) / 256), static_cast<unsigned>(imin64(n, 1024)));
+  plan_count_kernel<T><<<grid, 256, 0, st>>>(xy, cost, rho, folded, m, n, ld, thr, stats);
+  count_launch();
+}
+
 // ---- explicit instantiations ----------------------------------------------
 #define DROTB_INST(T)                                                          \
   template void launch_pass<T>(const PassArgs<T>&, int, bool, bool,            \
@@ -1652,7 +1712,13 @@ void launch_materialize(const T* xy, const T* cost, T* out, T rho, int folded,
                                    unsigned long long*, unsigned long long*,   \
                                    cudaStream_t);                              \
   template void launch_materialize<T>(const T*, const T*, T*, T, int, int64_t, \
-                                      int64_t, int64_t, cudaStream_t);
+                                      int64_t, int64_t, cudaStream_t);         \
+  template void launch_plan_max<T>(const T*, const T*, T, int, int64_t,        \
+                                   int64_t, int64_t, unsigned long long*,      \
+                                   cudaStream_t);                              \
+  template void launch_plan_count<T>(const T*, const T*, T, int, int64_t,      \
+                                     int64_t, int64_t, double,                 \
+                                     unsigned long long*, cudaStream_t);
 DROTB_INST(float)
 DROTB_INST(double)
 

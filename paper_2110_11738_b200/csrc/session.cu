@@ -1006,6 +1006,41 @@ struct Session {
     return 0;
   }
 
+  // Support of the current plan: xmax = max x_ij, nnz = #{x_ij > max(abs_tau,
+  // rel_tau * xmax)} (over all ranks when row-sharded).
+  int support(double rel_tau, double abs_tau, int64_t* nnz, double* xmax) {
+    Book<T> hb;
+    RC_TRY(read_book(&hb));
+    unsigned long long stats[2] = {0, 0};
+    launch_plan_max<T>(X, C, rho, hb.folded, m, n, ld, vflags, stream);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(stats, vflags, sizeof(stats), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    double mx;
+    std::memcpy(&mx, &stats[0], sizeof(mx));
+    if (sharded) {
+      CUDA_TRY(cudaMemcpyAsync(dpack + 10, &mx, sizeof(double), cudaMemcpyHostToDevice, stream));
+      RC_TRY(allreduce(dpack + 10, 1, ncclMax));
+      CUDA_TRY(cudaMemcpyAsync(&mx, dpack + 10, sizeof(double), cudaMemcpyDeviceToHost, stream));
+      CUDA_TRY(cudaStreamSynchronize(stream));
+    }
+    const double thr = std::max(abs_tau, rel_tau * mx);
+    launch_plan_count<T>(X, C, rho, hb.folded, m, n, ld, thr, vflags, stream);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(stats, vflags, sizeof(stats), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    double cnt = static_cast<double>(stats[1]);
+    if (sharded) {
+      CUDA_TRY(cudaMemcpyAsync(dpack + 10, &cnt, sizeof(double), cudaMemcpyHostToDevice, stream));
+      RC_TRY(allreduce(dpack + 10, 1, ncclSum));
+      CUDA_TRY(cudaMemcpyAsync(&cnt, dpack + 10, sizeof(double), cudaMemcpyDeviceToHost, stream));
+      CUDA_TRY(cudaStreamSynchronize(stream));
+    }
+    if (nnz) *nnz = static_cast<int64_t>(cnt);
+    if (xmax) *xmax = mx;
+    return 0;
+  }
+
   int get_trace(drotb_trace_row* out, int64_t cap, int64_t* len) {
     Book<T> hb;
     RC_TRY(read_book(&hb));
@@ -1602,6 +1637,16 @@ int drotb_session_gen_uniform(drotb_session* s, uint64_t seed, double lo, double
   try {
     if (s->precision == 0) return go(drotb::as_session<float>(s->impl));
     return go(drotb::as_session<double>(s->impl));
+  } catch (const std::exception& e) {
+    return guard_exceptions(e);
+  }
+}
+
+int drotb_session_support(drotb_session* s, double rel_tau, double abs_tau, int64_t* nnz,
+                          double* xmax) {
+  drotb::clear_error();
+  try {
+    return DROTB_DISPATCH(s, support(rel_tau, abs_tau, nnz, xmax));
   } catch (const std::exception& e) {
     return guard_exceptions(e);
   }

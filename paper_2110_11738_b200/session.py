@@ -109,6 +109,13 @@ class Session:
         _check(_lib.load().drotb_session_get_cost(self._h, _p(out)))
         return out
 
+    def support(self, rel_tau: float = 1e-6, abs_tau: float = 0.0):
+        """(nnz, xmax) of the current plan: nnz = #{x > max(abs_tau, rel_tau * xmax)}."""
+        nnz, xmax = C.c_int64(0), C.c_double(0)
+        _check(_lib.load().drotb_session_support(self._h, float(rel_tau), float(abs_tau),
+                                                 C.byref(nnz), C.byref(xmax)))
+        return int(nnz.value), float(xmax.value)
+
     def init(self, x0: Optional[np.ndarray] = None):
         x = None if x0 is None else _cm(x0, self.dtype)
         _check(_lib.load().drotb_session_init(self._h, _p(x)))

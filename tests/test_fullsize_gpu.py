@@ -1,0 +1,120 @@
+"""Parity at the BASELINE configs' full sizes.
+
+The CPU reference needs ~0.2-0.5 s per iteration at these sizes, so parity
+here is fixed-K trajectory parity: both solvers run K iterations of the
+default solve loop (skip-C, trace on) from the same inputs; in the exact
+reduction order the B200 plan, duals, report and trace must equal the
+reference bit for bit, in the fast order they must agree to the stated
+tolerances.  Size-independent properties (finite, nonnegative plan;
+bitwise agreement of the host and device generators) are checked on the
+same instances.
+
+  C2  m = n = 10 000 fp32, Gaussian squared-Euclidean cost (seed 0),
+      dyadic-uniform marginals
+  C3  m = 40 000, n = 5 000 fp64, random_matrix cost (seed 1),
+      random_simplex marginals
+"""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+K = 6
+
+
+def _oracle():
+    from pyoracle import LIB_PATHS, Oracle
+    return Oracle("ref" if os.path.exists(LIB_PATHS["ref"]) else "orc")
+
+
+def _cfg(**kw):
+    from pyoracle import default_config
+    return default_config(**kw)
+
+
+def _simplex(n, seed):
+    import ctypes as Cc
+    from pyoracle import Oracle
+    f = Oracle("orc").lib.orc_random_simplex
+    f.argtypes = [Cc.c_int64, Cc.c_uint64, Cc.c_void_p]
+    f.restype = None
+    out = np.empty(n)
+    f(n, seed, out.ctypes.data)
+    return out
+
+
+@pytest.fixture(scope="module")
+def c2():
+    from pyoracle import dyadic_marginal
+    m = n = 10000
+    C, _, _ = _oracle().gen_gaussian(m, n, 5.0, 0)
+    return m, n, C.astype(np.float32), dyadic_marginal(m, np.float32), \
+        dyadic_marginal(n, np.float32)
+
+
+@pytest.fixture(scope="module")
+def c3():
+    m, n = 40000, 5000
+    C = _oracle().random_unit(1, m * n)
+    return m, n, C, _simplex(m, 1 ^ 0x1111), _simplex(n, 1 ^ 0x2222)
+
+
+def _run(drot, ref, prob, order):
+    m, n, C, p, q = prob
+    want = ref.solve(C, p, q, m, n, _cfg(max_iters=K))
+    got = drot.solve(drot.TransportProblem(C.reshape((m, n), order="F"), p, q),
+                     drot.DrotConfig(order=drot.Order[order], max_iters=K))
+    return want, got
+
+
+def _props(got, p, q):
+    x = got.plan.x
+    assert np.isfinite(x).all() and (x >= 0).all()  # materialize_plan clamps
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_fullsize_exact_order_bitwise(drot, ref, name, request):
+    prob = request.getfixturevalue(name)
+    want, got = _run(drot, ref, prob, "reference")
+    assert got.trace.iterations == want.iterations == K
+    assert got.status.name == want.status
+    np.testing.assert_array_equal(got.plan.x.ravel(order="F"), want.plan)
+    np.testing.assert_array_equal(got.cert.mu, want.mu)
+    np.testing.assert_array_equal(got.cert.nu, want.nu)
+    for k in ("r_primal", "r_dual", "gap", "objective"):
+        assert getattr(got.report, k) == want.report[k], k
+    for gr, rr in zip(got.trace.rows, want.trace):
+        for k, v in rr.items():
+            a = getattr(gr, k)
+            assert a == v or (np.isnan(a) and np.isnan(v)), (gr.iter, k, a, v)
+    _props(got, prob[3], prob[4])
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_fullsize_fast_order(drot, ref, name, request):
+    prob = request.getfixturevalue(name)
+    want, got = _run(drot, ref, prob, "fast")
+    assert got.trace.iterations == want.iterations == K
+    fp32 = prob[2].dtype == np.float32
+    # X is elementwise-identical in both orders until a reduction's rounding
+    # differs; over K iterations the plans must stay within a few ulps of the
+    # iterate scale
+    x, w = got.plan.x.ravel(order="F"), want.plan
+    scale = float(np.abs(w).max())
+    tol = (1e-5 if fp32 else 1e-12) * scale
+    assert float(np.abs(x - w).max()) <= tol
+    rel = 1e-4 if fp32 else 1e-10
+    assert abs(got.report.objective - want.report["objective"]) <= rel * abs(
+        want.report["objective"])
+    _props(got, prob[3], prob[4])
+
+
+def test_c2_device_generator_matches_reference(drot, c2):
+    m, n, C, p, q = c2
+    s = drot.Session(m, n, np.float32, drot.DrotConfig())
+    s.gen_gaussian(5.0, 0, "dyadic")
+    got = s.cost()
+    s.close()
+    assert np.array_equal(got.ravel(order="F"), C)
