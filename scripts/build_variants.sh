@@ -8,6 +8,6 @@ while [ $# -ge 2 ]; do
   ( nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC -I../include \
       $flags -c csrc/kernels.cu -o _variants/k_$name.o 2>/dev/null && \
     nvcc -gencode arch=compute_100a,code=sm_100a -shared -o _variants/lib_$name.so _variants/k_$name.o \
-      _build/session.cu.o _build/probgen.cpp.o -lpthread ) &
+      _build/session.cu.o _build/probgen.cpp.o _build/probgen.cu.o -lpthread ) &
 done
 wait

@@ -144,7 +144,7 @@ def main():
         if md:
             # algorithmic bytes: fold/plain sweeps 3*s*m*n, skip sweeps 2*s*m*n
             for e in ls:
-                skip = "Li3E" in e["kernel"] or "kSkip" in e["kernel"]
+                skip = re.search(r"<(float|double), 3,", e["kernel"]) is not None
                 e["algorithmic_bytes"] = (2 if skip else 3) * s * args.m * args.n
             md2, _ = full_capture(rpath, args.tag, None)
             lines = [md2]
