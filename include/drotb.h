@@ -240,6 +240,17 @@ int drotb_check_problem_f32(const float* C, int64_t m, int64_t n,
 int drotb_check_problem_f64(const double* C, int64_t m, int64_t n,
                             const double* p, const double* q);
 
+/* residual_report (problem.hpp:174-225) of an arbitrary (plan, cert) pair,
+ * evaluated on the device: plan (m*n), mu (m), nu (n) host arrays.
+ * exact != 0 evaluates every sum in the reference's order (bitwise equal
+ * report, serial chains); exact == 0 uses fixed parallel trees. */
+int drotb_residual_report_f32(const float* C, int64_t m, int64_t n, const float* p,
+                              const float* q, const float* plan, const float* mu,
+                              const float* nu, int32_t exact, drotb_report* out);
+int drotb_residual_report_f64(const double* C, int64_t m, int64_t n, const double* p,
+                              const double* q, const double* plan, const double* mu,
+                              const double* nu, int32_t exact, drotb_report* out);
+
 /* ---- problem generation (probgen.hpp:131-170, host, bit-identical) ------ *
  * Writes C (m*n column-major, normalized to max 1), p (m), q (n) in double.
  * dirichlet != 0 selects Dirichlet(1..1) marginals (probgen.hpp:115-127). */

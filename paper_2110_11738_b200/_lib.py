@@ -86,6 +86,10 @@ SIGNATURES = {
                                         P(drotb_counters)]),
     "drotb_check_problem_f32": (C.c_int, [vp, i64, i64, vp, vp]),
     "drotb_check_problem_f64": (C.c_int, [vp, i64, i64, vp, vp]),
+    "drotb_residual_report_f32": (C.c_int, [vp, i64, i64, vp, vp, vp, vp, vp, i32,
+                                            P(drotb_report)]),
+    "drotb_residual_report_f64": (C.c_int, [vp, i64, i64, vp, vp, vp, vp, vp, i32,
+                                            P(drotb_report)]),
     "drotb_gen_gaussian": (C.c_int, [i64, i64, f64, u64, i32, vp, vp, vp]),
     "drotb_gen_gaussian_f32": (C.c_int, [i64, i64, f64, u64, vp]),
     "drotb_counter_uniform": (C.c_int, [u64, i64, f64, f64, vp]),

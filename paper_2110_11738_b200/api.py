@@ -266,6 +266,34 @@ def check_problem(problem: TransportProblem) -> None:
     _check(getattr(lib, "drotb_check_problem_" + _sfx(dt))(_p(cm), m, n, _p(pv), _p(qv)))
 
 
+def residual_report(problem: TransportProblem, plan: TransportPlan, cert: DualCertificate,
+                    exact: bool = True) -> ResidualReport:
+    """residual_report (problem.hpp:174-225) evaluated on the B200.  exact=True
+    sums in the reference's order (bitwise equal report); exact=False uses
+    parallel trees."""
+    dt = _dtype_of(problem)
+    m, n = problem.m, problem.n
+    x = np.asarray(plan.x)
+    if x.shape != (m, n):
+        raise Error(Errc.shape_mismatch, "shape_mismatch: residual_report: plan vs cost")
+    if len(cert.mu) != m or len(cert.nu) != n:
+        raise Error(Errc.shape_mismatch, "shape_mismatch: residual_report: dual lengths")
+    cm, xm = _cm(problem.cost, dt), _cm(x, dt)
+    pv, qv = _vec(problem.p, dt), _vec(problem.q, dt)
+    mu, nu = _vec(cert.mu, dt), _vec(cert.nu, dt)
+    rep = drotb_report()
+    _check(getattr(_lib.load(), "drotb_residual_report_" + _sfx(dt))(
+        _p(cm), m, n, _p(pv), _p(qv), _p(xm), _p(mu), _p(nu), int(bool(exact)), C.byref(rep)))
+    return ResidualReport(rep.r_primal, rep.r_dual, rep.gap, rep.objective)
+
+
+def objective(problem: TransportProblem, plan: TransportPlan) -> float:
+    """<C, X> in storage order (problem.hpp:158-169), on the B200."""
+    m, n = problem.m, problem.n
+    zeros_m, zeros_n = np.zeros(m), np.zeros(n)
+    return residual_report(problem, plan, DualCertificate(zeros_m, zeros_n)).objective
+
+
 def solve(problem: TransportProblem, cfg: Optional[DrotConfig] = None,
           x0: Optional[np.ndarray] = None,
           plan_out: Optional[np.ndarray] = None) -> SolveResult:

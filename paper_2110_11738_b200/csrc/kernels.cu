@@ -447,12 +447,18 @@ __device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0
                                                 int lane) {
   using V = typename V16<T>::type;
   constexpr int R = 16 / sizeof(T);
-  constexpr int S = kAsyncS, G = kAsyncG, CH = kChunkCols;
+  constexpr bool RC = MODE != kSkip;
+  // a stage holds 2*kAsyncG 16-B slots per lane: G columns of X and C, or --
+  // on skip sweeps, which read no C -- 2G columns of X (same bytes in flight)
+  constexpr int S = kAsyncS, G = RC ? kAsyncG : 2 * kAsyncG, CH = kChunkCols;
   constexpr int NG = CH / G;
   static_assert(NG % S == 0, "stages must divide the groups of a chunk");
-  constexpr bool RC = MODE != kSkip;
   const bool live = !MASK || nvalid > 0;
   T vb[S][G];
+  auto xslot = [&](int st, int k) { return ring + (st * 2 * kAsyncG + k) * 32 + lane; };
+  auto cslot = [&](int st, int k) {
+    return ring + (st * 2 * kAsyncG + kAsyncG + k) * 32 + lane;
+  };
   auto issue = [&](int st, int64_t jg) {
 #pragma unroll
     for (int k = 0; k < G; ++k) {
@@ -461,8 +467,8 @@ __device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0
       if (col < c1) {
         if (live) {
           const int64_t off = col * a.ld + row0;
-          cp_async16(ring + ((st * 2 + 0) * G + k) * 32 + lane, a.xy + off);
-          if (RC) cp_async16(ring + ((st * 2 + 1) * G + k) * 32 + lane, a.cost + off);
+          cp_async16(xslot(st, k), a.xy + off);
+          if (RC) cp_async16(cslot(st, k), a.cost + off);
         }
         vb[st][k] = __ldg(a.varphi + col);
       }
@@ -485,8 +491,8 @@ __device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0
 #pragma unroll
           for (int t = 0; t < R; ++t) x[t] = cc[t] = T(0);
           if (live) {
-            unpack(ring[((st * 2 + 0) * G + k) * 32 + lane], x);
-            if (RC) unpack(ring[((st * 2 + 1) * G + k) * 32 + lane], cc);
+            unpack(*xslot(st, k), x);
+            if (RC) unpack(*cslot(st, k), cc);
           }
           compute_col<T, MODE, DUAL, DX, MASK>(a, x, cc, vb[st][k], col, gg * G + k, row0,
                                                nvalid, ph, u, acc, wbuf, lane);

@@ -1369,6 +1369,48 @@ static int gen_marginals(int64_t mg, int64_t n, uint64_t seed, int32_t kind,
 }
 }  // namespace drotb
 
+// residual_report (problem.hpp:174-225) on the device: transient buffers,
+// host in/out.
+template <class T>
+static int residual_report_t(const T* C, int64_t m, int64_t n, const T* p, const T* q,
+                             const T* plan, const T* mu, const T* nu, int32_t exact,
+                             drotb_report* out) {
+  if (m <= 0 || n <= 0)
+    return drotb::set_error(DROTB_ERRC_EMPTY_DIMENSION, "residual_report: empty dimension");
+  if (!C || !p || !q || !plan || !mu || !nu || !out)
+    return drotb::set_error(DROTB_ERRC_SHAPE_MISMATCH, "residual_report: null argument");
+  const size_t mn = static_cast<size_t>(m) * static_cast<size_t>(n);
+  const size_t tb = sizeof(T) * (2 * mn + 2 * static_cast<size_t>(m + n));
+  const size_t db = sizeof(double) * (2 * static_cast<size_t>(m + n) + 4);
+  char* buf = nullptr;
+  CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&buf), tb + db));
+  std::unique_ptr<char, decltype(&cudaFree)> hold(buf, &cudaFree);
+  T* dX = reinterpret_cast<T*>(buf);
+  T* dC = dX + mn;
+  T* dmu = dC + mn;
+  T* dp = dmu + m;
+  T* dnu = dp + m;
+  T* dq = dnu + n;
+  double* scratch = reinterpret_cast<double*>(buf + tb);
+  double* dout = scratch + 2 * (m + n);
+  CUDA_TRY(cudaMemcpy(dX, plan, sizeof(T) * mn, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(dC, C, sizeof(T) * mn, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(dmu, mu, sizeof(T) * m, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(dp, p, sizeof(T) * m, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(dnu, nu, sizeof(T) * n, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(dq, q, sizeof(T) * n, cudaMemcpyHostToDevice));
+  drotb::launch_residual_report<T>(dX, dC, dmu, dnu, dp, dq, m, n, exact != 0, scratch, dout,
+                                   nullptr);
+  CUDA_TRY(cudaGetLastError());
+  double r[4];
+  CUDA_TRY(cudaMemcpy(r, dout, sizeof(r), cudaMemcpyDeviceToHost));
+  out->r_primal = r[0];
+  out->r_dual = r[1];
+  out->gap = r[2];
+  out->objective = r[3];
+  return 0;
+}
+
 extern "C" {
 
 int32_t drotb_abi_version(void) { return DROTB_ABI_VERSION; }
@@ -1640,6 +1682,19 @@ int drotb_session_gen_uniform(drotb_session* s, uint64_t seed, double lo, double
   } catch (const std::exception& e) {
     return guard_exceptions(e);
   }
+}
+
+int drotb_residual_report_f32(const float* C, int64_t m, int64_t n, const float* p,
+                              const float* q, const float* plan, const float* mu,
+                              const float* nu, int32_t exact, drotb_report* out) {
+  drotb::clear_error();
+  return residual_report_t<float>(C, m, n, p, q, plan, mu, nu, exact, out);
+}
+int drotb_residual_report_f64(const double* C, int64_t m, int64_t n, const double* p,
+                              const double* q, const double* plan, const double* mu,
+                              const double* nu, int32_t exact, drotb_report* out) {
+  drotb::clear_error();
+  return residual_report_t<double>(C, m, n, p, q, plan, mu, nu, exact, out);
 }
 
 int drotb_session_support(drotb_session* s, double rel_tau, double abs_tau, int64_t* nnz,
