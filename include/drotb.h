@@ -302,6 +302,9 @@ int drotb_session_gen_uniform(drotb_session* s, uint64_t seed, double lo, double
  * ranks when row-sharded (collective).  SURVEY §8(c) support parity. */
 int drotb_session_support(drotb_session* s, double rel_tau, double abs_tau, int64_t* nnz,
                           double* xmax);
+/* CTAs of the persistent solver kernel this session runs its iterations
+ * with (fast order, one GPU; 0 = per-launch kernels + CUDA graphs). */
+int32_t drotb_session_persistent_grid(drotb_session* s);
 /* Copy the session's (local) cost matrix to host, m x n column-major. */
 int drotb_session_get_cost(drotb_session* s, void* out);
 /* init_state (x0 host pointer or NULL); resets the solve bookkeeping. */

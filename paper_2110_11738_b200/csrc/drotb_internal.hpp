@@ -136,6 +136,46 @@ struct TailArgs {
   double* dpack; // [dual_i, dphi^2, dphi, cross_i | obj, dual^2]    (sum)
 };
 
+// Persistent solver kernel (persistent.cu): one cooperative launch runs up to
+// `iters` iterations; phases separated by grid barriers.
+template <class T>
+struct PersistArgs {
+  PassArgs<T> pa;           // xy, cost, phi, varphi, rho, m, n, ld
+  T* a;
+  T* b;
+  const T* p;
+  const T* q;
+  T* rb0;
+  T* rb1;
+  T* sb0;
+  T* sb1;
+  int64_t m_global, n_global;
+  int64_t rows_cta;         // rows per CTA row block (4 warps x 32 lanes x R)
+  int64_t n_rb;             // row blocks
+  int64_t max_seg;          // u-partial slots per CTA
+  T* ustrip;                // [grid * max_seg][rows_cta]
+  const int32_t* seg_ptr;   // [n_rb + 1] CSR of the u slots per row block
+  const int32_t* seg_slot;  // slots in column order
+  T* vstrip;                // [n_rb][n]
+  T* cpart;                 // [grid][16] per-CTA T partials
+  double* dpart;            // [grid][16] per-CTA double partials
+  unsigned* bar;            // [2] barrier count, generation
+  Book<T>* book;
+  TraceRowDev* trace;
+  int64_t iters;            // iterations this launch (upper bound)
+  int32_t engine_ref, skip_cost;
+  unsigned long long* sweep_ns;  // accumulated P1 time (CTA 0, %globaltimer)
+};
+
+template <class T>
+size_t persistent_smem_bytes();
+template <class T>
+int persistent_grid(int device);
+template <class T>
+int rows_per_cta();
+template <class T>
+cudaError_t launch_persistent(const PersistArgs<T>& g, int grid, bool dx, cudaStream_t st);
+
 // ---- kernel launchers (kernels.cu) ---------------------------------------
 template <class T>
 void launch_pass(const PassArgs<T>& a, int mode, bool want_dual, bool want_dx,

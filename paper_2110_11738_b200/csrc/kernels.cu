@@ -22,6 +22,7 @@
 #include <cstdlib>
 
 #include "drotb_internal.hpp"
+#include "sweep.cuh"
 
 namespace drotb {
 
@@ -29,301 +30,8 @@ namespace drotb {
 // small helpers
 // ---------------------------------------------------------------------------
 static int64_t g_launches = 0;
-__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) {
-  return a < b ? a : b;
-}
 int64_t kernel_launch_count() { return g_launches; }
 void count_launch(int64_t k) { g_launches += k; }
-
-template <class T>
-struct V16;
-template <>
-struct V16<float> {
-  using type = float4;
-};
-template <>
-struct V16<double> {
-  using type = double2;
-};
-
-__device__ __forceinline__ void unpack(const float4& v, float* o) {
-  o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
-}
-__device__ __forceinline__ void unpack(const double2& v, double* o) {
-  o[0] = v.x; o[1] = v.y;
-}
-__device__ __forceinline__ float4 pack4(const float* o) {
-  return make_float4(o[0], o[1], o[2], o[3]);
-}
-__device__ __forceinline__ double2 pack4(const double* o) {
-  return make_double2(o[0], o[1]);
-}
-template <class T>
-__device__ __forceinline__ typename V16<T>::type vzero() {
-  typename V16<T>::type z;
-  T* p = reinterpret_cast<T*>(&z);
-#pragma unroll
-  for (int t = 0; t < int(16 / sizeof(T)); ++t) p[t] = T(0);
-  return z;
-}
-
-template <class T>
-__device__ __forceinline__ T max_finite();
-template <>
-__device__ __forceinline__ float max_finite<float>() { return FLT_MAX; }
-template <>
-__device__ __forceinline__ double max_finite<double>() { return DBL_MAX; }
-
-template <class T>
-__device__ __forceinline__ T warp_sum(T v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-template <class T>
-__device__ __forceinline__ T warp_max(T v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-
-// Fixed-shape block tree reduction of K values (deterministic: the tree
-// depends only on blockDim).  Result valid in thread 0.
-template <class T, int K>
-__device__ __forceinline__ void block_sum(T (&v)[K], T* sh /* K*32 */) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nw = (blockDim.x + 31) >> 5;
-#pragma unroll
-  for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
-  __syncthreads();
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < K; ++k) sh[k * 32 + warp] = v[k];
-  __syncthreads();
-  if (warp == 0) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      T x = lane < nw ? sh[k * 32 + lane] : T(0);
-      v[k] = warp_sum(x);
-    }
-  }
-  __syncthreads();
-}
-
-// Grid-level "last block done" ticket (threadFenceReduction pattern).
-__device__ __forceinline__ bool last_block(unsigned int* ticket) {
-  __shared__ bool is_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned int t = atomicAdd(ticket, 1u);
-    is_last = (t == gridDim.x * gridDim.y - 1);
-  }
-  __syncthreads();
-  if (is_last) __threadfence();
-  return is_last;
-}
-
-// ---------------------------------------------------------------------------
-// K1: the fused sweep
-// ---------------------------------------------------------------------------
-// Thread mapping: a warp owns 32*R consecutive rows (R = 16 B / sizeof(T)
-// rows per lane, one 128-bit load per column) of one tile column
-// [c0, c0+tc).  Each lane walks the tile's columns in order, so its row
-// partials are exactly the reference's u strips (fused.hpp:267, tile-local
-// running sum from 0).  Column partials must be sequential over each
-// 64-row block (fused.hpp:268): the warp stages x+ of 16 columns in shared
-// memory and one lane per (column, 64-row block) sums the 64 values in row
-// order with 128-bit shared loads.
-//
-// Staging layout (per warp, 16 columns x 32R rows, 16-B chunks): chunk q
-// (rows qR..qR+R-1) of column c lives at chunk slot c*32 + (q ^ (c & 7)).
-// The STS.128 of a column (lane l writes chunk l) and the LDS.128 of the
-// row-order reads (lane = column [+16 * block], same q across lanes) both
-// touch 8 distinct 16-B bank groups per 8-lane phase: conflict free.
-//
-// Memory pipeline: columns are processed in groups of G with register
-// double buffering -- the loads of group g+1 (and of the next chunk's first
-// group, across the v-phase) are in flight while group g is computed.
-template <class T>
-struct PassAcc {
-  T cost, prev, dual, dx, mx;
-  bool bad;
-};
-
-template <class T, int G>
-struct ColGroup {
-  typename V16<T>::type x[G], c[G];
-  T v[G];
-};
-
-template <class T, int MODE, int G>
-__device__ __forceinline__ void load_group(const PassArgs<T>& a, ColGroup<T, G>& g,
-                                           int64_t j, int64_t c1, int64_t row0,
-                                           bool live) {
-  using V = typename V16<T>::type;
-  constexpr bool RC = MODE != kSkip;
-#pragma unroll
-  for (int k = 0; k < G; ++k) {
-    if (j + k < c1) {
-      const int64_t off = (j + k) * a.ld + row0;
-      if (live) {
-        g.x[k] = __ldcs(reinterpret_cast<const V*>(a.xy + off));
-        if (RC) g.c[k] = __ldcs(reinterpret_cast<const V*>(a.cost + off));
-      }
-      g.v[k] = __ldg(a.varphi + j + k);
-    }
-  }
-}
-
-// The elementwise update of one column slice (R rows) and its reductions
-// (fused.hpp:249-284).  c = column index within the 16-column staging chunk.
-template <class T, int MODE, bool DUAL, bool DX, bool MASK>
-__device__ __forceinline__ void compute_col(const PassArgs<T>& a, const T (&x)[16 / sizeof(T)],
-                                            const T (&cc)[16 / sizeof(T)], T vj, int64_t col,
-                                            int c, int64_t row0, int nvalid,
-                                            const T (&ph)[16 / sizeof(T)],
-                                            T (&u)[16 / sizeof(T)], PassAcc<T>& acc, T* wbuf,
-                                            int lane) {
-  using V = typename V16<T>::type;
-  constexpr int R = 16 / sizeof(T);
-  constexpr bool RC = MODE != kSkip;
-  const bool live = !MASK || nvalid > 0;
-  T xp[R], st[R];
-#pragma unroll
-  for (int t = 0; t < R; ++t) {
-    T e = T(0), tv;
-    if (RC) {
-      e = a.rho * cc[t];
-      if (MODE == kPlain1)
-        tv = ((x[t] - e) + ph[t]) + vj;
-      else
-        tv = ((x[t] + ph[t]) + vj) - e;
-    } else {
-      tv = (x[t] + ph[t]) + vj;
-    }
-    T p = tv > T(0) ? tv : T(0);
-    const bool valid = !MASK || t < nvalid;
-    if (MASK && !valid) {
-      p = T(0);
-      tv = T(0);
-    }
-    xp[t] = p;
-    st[t] = (MODE == kFold) ? p - e : p;
-    u[t] += p;
-    if (RC) {
-      acc.cost = fma(cc[t], p, acc.cost);
-      acc.prev = fma(cc[t], x[t], acc.prev);
-      if (DUAL) {
-        T d = (ph[t] + vj) - e;
-        d = d > T(0) ? d : T(0);
-        if (MASK && !valid) d = T(0);
-        acc.dual = fma(d, d, acc.dual);
-      }
-    }
-    if (DX) {
-      const T dd = p - x[t];
-      acc.dx = fma(dd, dd, acc.dx);
-    }
-    const T at = fabs(tv);
-    acc.mx = fmax(acc.mx, at);
-    acc.bad |= !(at <= max_finite<T>());
-  }
-  if (live) __stcs(reinterpret_cast<V*>(a.xy + col * a.ld + row0), pack4(st));
-  *reinterpret_cast<V*>(wbuf + (c * 32 + (lane ^ (c & 7))) * R) = pack4(xp);
-}
-
-template <class T, int MODE, bool DUAL, bool DX, bool MASK, int G>
-__device__ __forceinline__ void compute_group(const PassArgs<T>& a,
-                                              const ColGroup<T, G>& g, int64_t j,
-                                              int cbase, int64_t c1, int64_t row0,
-                                              int nvalid, const T (&ph)[16 / sizeof(T)],
-                                              T (&u)[16 / sizeof(T)], PassAcc<T>& acc,
-                                              T* wbuf, int lane) {
-  constexpr int R = 16 / sizeof(T);
-  constexpr bool RC = MODE != kSkip;
-  const bool live = !MASK || nvalid > 0;
-#pragma unroll
-  for (int k = 0; k < G; ++k) {
-    if (j + k < c1) {
-      T x[R], cc[R];
-#pragma unroll
-      for (int t = 0; t < R; ++t) x[t] = cc[t] = T(0);
-      if (live) {
-        unpack(g.x[k], x);
-        if (RC) unpack(g.c[k], cc);
-      }
-      compute_col<T, MODE, DUAL, DX, MASK>(a, x, cc, g.v[k], j + k, cbase + k, row0, nvalid,
-                                           ph, u, acc, wbuf, lane);
-    }
-  }
-}
-
-// v-phase: lane (c, b) sums the 64 rows of block b of staged column c in
-// row order (fused.hpp:268) and writes the v strip entry.
-template <class T>
-__device__ __forceinline__ void v_phase(const PassArgs<T>& a, const T* wbuf, int64_t j0,
-                                        int cnt, int64_t wrow0, int lane) {
-  using V = typename V16<T>::type;
-  constexpr int R = 16 / sizeof(T);
-  constexpr int NB = 32 * R / kVBlockRows;
-  constexpr int CH = kChunkCols;
-  if (lane < CH * NB) {
-    const int c = lane % CH, b = lane / CH;
-    const int64_t gb = wrow0 / kVBlockRows + b;
-    if (c < cnt && gb * kVBlockRows < a.m) {
-      const V* col = reinterpret_cast<const V*>(wbuf) + c * 32;
-      const int g7 = c & 7;
-      constexpr int QB = kVBlockRows / R;  // chunks per 64-row block
-      T s = T(0);
-#pragma unroll
-      for (int qq = 0; qq < QB; ++qq) {
-        T v4[R];
-        unpack(col[(b * QB + qq) ^ g7], v4);
-#pragma unroll
-        for (int t = 0; t < R; ++t) s += v4[t];
-      }
-      a.vstrip[gb * a.n + j0 + c] = s;
-    }
-  }
-}
-
-template <class T, int MODE, bool DUAL, bool DX, bool MASK, int G>
-__device__ __forceinline__ void pass_tile(const PassArgs<T>& a, int64_t c0, int64_t c1,
-                                          int64_t wrow0, int64_t row0, int nvalid,
-                                          const T (&ph)[16 / sizeof(T)],
-                                          T (&u)[16 / sizeof(T)], PassAcc<T>& acc,
-                                          T* wbuf, int lane) {
-  using V = typename V16<T>::type;
-  constexpr int R = 16 / sizeof(T);
-  constexpr int ROWS_W = 32 * R;
-  constexpr int NB = ROWS_W / kVBlockRows;
-  constexpr int CH = kChunkCols;
-  constexpr int NG = CH / G;
-  static_assert(NG % 2 == 0, "groups per chunk must be even (ping-pong)");
-  const bool live = !MASK || nvalid > 0;
-  ColGroup<T, G> A, B;
-#pragma unroll
-  for (int k = 0; k < G; ++k) {
-    A.x[k] = B.x[k] = A.c[k] = B.c[k] = vzero<T>();
-    A.v[k] = B.v[k] = T(0);
-  }
-  load_group<T, MODE, G>(a, A, c0, c1, row0, live);
-  for (int64_t j0 = c0; j0 < c1; j0 += CH) {
-#pragma unroll
-    for (int gi = 0; gi < NG; gi += 2) {
-      load_group<T, MODE, G>(a, B, j0 + (gi + 1) * G, c1, row0, live);
-      compute_group<T, MODE, DUAL, DX, MASK, G>(a, A, j0 + gi * G, gi * G, c1, row0,
-                                                nvalid, ph, u, acc, wbuf, lane);
-      load_group<T, MODE, G>(a, A, j0 + (gi + 2) * G, c1, row0, live);
-      compute_group<T, MODE, DUAL, DX, MASK, G>(a, B, j0 + (gi + 1) * G, (gi + 1) * G,
-                                                c1, row0, nvalid, ph, u, acc, wbuf, lane);
-    }
-    __syncwarp();
-    v_phase<T>(a, wbuf, j0, static_cast<int>(imin64(CH, c1 - j0)), wrow0, lane);
-    __syncwarp();
-  }
-}
 
 #ifndef DROTB_PASS_G
 #define DROTB_PASS_G 4  // columns per load group (two groups in flight)
@@ -400,110 +108,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_PASS_MINB)
     }
     a.partials[static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x] = out;
   }
-}
-
-// ---------------------------------------------------------------------------
-// K1 (async): the same sweep with a per-lane cp.async ring in shared memory.
-// Each lane copies its own 16-B slices of X and C for kAsyncStages-1 column
-// groups ahead (LDGSTS, no register cost for data in flight) and consumes
-// them in order; completion is per-thread (cp.async.wait_group), so no
-// cross-lane synchronisation is needed for the ring.
-// ---------------------------------------------------------------------------
-#ifndef DROTB_ASYNC_S
-#define DROTB_ASYNC_S 4  // ring stages (S-1 groups in flight)
-#endif
-#ifndef DROTB_ASYNC_G
-#define DROTB_ASYNC_G 2  // columns per stage
-#endif
-constexpr int kAsyncS = DROTB_ASYNC_S;
-constexpr int kAsyncG = DROTB_ASYNC_G;
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-
-template <class T>
-constexpr size_t async_smem_bytes() {
-  // per warp: ring [S][2][G][32 lanes] x 16 B + staging [16 cols][32 R] x sizeof(T)
-  return static_cast<size_t>(kWarpsPerCta) *
-         (static_cast<size_t>(kAsyncS) * 2 * kAsyncG * 32 * 16 +
-          static_cast<size_t>(kChunkCols) * 32 * 16);
-}
-
-template <class T, int MODE, bool DUAL, bool DX, bool MASK>
-__device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0, int64_t c1,
-                                                int64_t wrow0, int64_t row0, int nvalid,
-                                                const T (&ph)[16 / sizeof(T)],
-                                                T (&u)[16 / sizeof(T)], PassAcc<T>& acc,
-                                                T* wbuf, typename V16<T>::type* ring,
-                                                int lane) {
-  using V = typename V16<T>::type;
-  constexpr int R = 16 / sizeof(T);
-  constexpr bool RC = MODE != kSkip;
-  // a stage holds 2*kAsyncG 16-B slots per lane: G columns of X and C, or --
-  // on skip sweeps, which read no C -- 2G columns of X (same bytes in flight)
-  constexpr int S = kAsyncS, G = RC ? kAsyncG : 2 * kAsyncG, CH = kChunkCols;
-  constexpr int NG = CH / G;
-  static_assert(NG % S == 0, "stages must divide the groups of a chunk");
-  const bool live = !MASK || nvalid > 0;
-  T vb[S][G];
-  auto xslot = [&](int st, int k) { return ring + (st * 2 * kAsyncG + k) * 32 + lane; };
-  auto cslot = [&](int st, int k) {
-    return ring + (st * 2 * kAsyncG + kAsyncG + k) * 32 + lane;
-  };
-  auto issue = [&](int st, int64_t jg) {
-#pragma unroll
-    for (int k = 0; k < G; ++k) {
-      const int64_t col = jg + k;
-      vb[st][k] = T(0);
-      if (col < c1) {
-        if (live) {
-          const int64_t off = col * a.ld + row0;
-          cp_async16(xslot(st, k), a.xy + off);
-          if (RC) cp_async16(cslot(st, k), a.cost + off);
-        }
-        vb[st][k] = __ldg(a.varphi + col);
-      }
-    }
-    cp_async_commit();
-  };
-#pragma unroll
-  for (int st = 0; st < S - 1; ++st) issue(st, c0 + st * G);
-  for (int64_t j0 = c0; j0 < c1; j0 += CH) {
-#pragma unroll
-    for (int gg = 0; gg < NG; ++gg) {
-      const int st = gg % S;
-      issue((gg + S - 1) % S, j0 + (gg + S - 1) * G);
-      cp_async_wait<S - 1>();
-#pragma unroll
-      for (int k = 0; k < G; ++k) {
-        const int64_t col = j0 + gg * G + k;
-        if (col < c1) {
-          T x[R], cc[R];
-#pragma unroll
-          for (int t = 0; t < R; ++t) x[t] = cc[t] = T(0);
-          if (live) {
-            unpack(*xslot(st, k), x);
-            if (RC) unpack(*cslot(st, k), cc);
-          }
-          compute_col<T, MODE, DUAL, DX, MASK>(a, x, cc, vb[st][k], col, gg * G + k, row0,
-                                               nvalid, ph, u, acc, wbuf, lane);
-        }
-      }
-    }
-    __syncwarp();
-    v_phase<T>(a, wbuf, j0, static_cast<int>(imin64(CH, c1 - j0)), wrow0, lane);
-    __syncwarp();
-  }
-  cp_async_wait<0>();
 }
 
 template <class T, int MODE, bool DUAL, bool DX>
@@ -824,85 +428,27 @@ __device__ void staged_chains(int64_t len, F term, T* sbuf /* K*kStage */,
   __syncthreads();
 }
 
+// Strip merge: one thread per row / column, sequential over the strips
+// (fused.hpp:314-321; consecutive threads read consecutive entries of each
+// strip, so every load is coalesced).  Both orders sum the strips in strip
+// order; they differ in the scalar totals.  (An earlier fast variant split
+// each index over 8 lanes: 8 strips per warp load = 8x sector
+// amplification, 18 us per merge at 10k^2 -- measured, r1.)
+
 template <class T>
-__device__ __forceinline__ void erg_update(Book<T>* bk, double value) {
-  bk->erg_count += 1;
-  bk->erg_mean += (value - bk->erg_mean) / static_cast<double>(bk->erg_count);
-}
-
-// Strip merge.  Exact order: one thread per row / column, sequential over
-// the strips (fused.hpp:314-321).  Fast order: kMergeLanes threads per row /
-// column sum interleaved strip subsets, combined by a fixed shuffle tree.
-constexpr int kMergeLanes = 8;
-
-template <class T, bool EXACT>
 __device__ __forceinline__ T strip_sum(const T* strips, int64_t count, int64_t stride,
-                                       int64_t idx, int sub) {
+                                       int64_t idx) {
   T acc = T(0);
-  if (EXACT) {
-    int64_t g = 0;
-    for (; g + 8 <= count; g += 8) {
-      T v8[8];
+  int64_t g = 0;
+  for (; g + 8 <= count; g += 8) {
+    T v8[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) v8[q] = strips[(g + q) * stride + idx];
+    for (int q = 0; q < 8; ++q) v8[q] = strips[(g + q) * stride + idx];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) acc += v8[q];
-    }
-    for (; g < count; ++g) acc += strips[g * stride + idx];
-  } else {
-    int64_t g = sub;
-    for (; g + 3 * kMergeLanes < count; g += 4 * kMergeLanes) {
-      T v4[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) v4[q] = strips[(g + q * kMergeLanes) * stride + idx];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc += v4[q];
-    }
-    for (; g < count; g += kMergeLanes) acc += strips[g * stride + idx];
-#pragma unroll
-    for (int o = kMergeLanes / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    for (int q = 0; q < 8; ++q) acc += v8[q];
   }
+  for (; g < count; ++g) acc += strips[g * stride + idx];
   return acc;
-}
-
-// Pass totals -> FusedPassOutput scalars, step_impl recursions and the
-// objective bookkeeping of solve (fused.hpp:346-356; solver.hpp:266,
-// 273-277, 418-437).  tot = {cost, prev, dual, dx, max|t|, sum r, |r|^2, |s|^2}.
-template <class T>
-__device__ void merge_scalars(Book<T>* bk, const TailArgs<T>& t, const T (&tot)[8],
-                              int totbad) {
-  bk->pass_cost = tot[0];
-  bk->pass_prev = tot[1];
-  bk->pass_dual = tot[2];
-  bk->pass_dx = tot[3];
-  bk->pass_max_abs = tot[4];
-  bk->pass_bad = totbad;
-  if (!t.solver) return;
-  const int64_t k = bk->iter;
-  bk->folded = t.folded_after;
-  if (totbad) {  // solver.hpp:266, 418-422
-    bk->failed = 1;
-    bk->iterations = k + 1;
-    bk->stop = 1;
-    return;
-  }
-  const T beta = tot[5] / static_cast<T>(t.m_global + t.n_global);
-  bk->beta = beta;
-  bk->coef = T(2) * beta - bk->alpha;
-  bk->nr2 = tot[6];
-  bk->ns2 = tot[7];
-  bk->iterations = k + 1;
-  const bool cost_valid = t.reads_cost != 0;
-  const bool dual_valid = t.reads_cost && t.want_dual;
-  if (!bk->prev_pass_had_cost && cost_valid)
-    erg_update(bk, static_cast<double>(tot[1]));
-  if (cost_valid) {
-    bk->last_cost = static_cast<double>(tot[0]);
-    erg_update(bk, bk->last_cost);
-  }
-  bk->prev_pass_had_cost = cost_valid ? 1 : 0;
-  if (dual_valid)
-    bk->last_r_dual = sqrt(static_cast<double>(tot[2])) / static_cast<double>(t.rho);
 }
 
 template <class T, bool EXACT>
@@ -910,14 +456,11 @@ __global__ void __launch_bounds__(kTailThreads) merge_kernel(const TailArgs<T> t
   Book<T>* bk = t.book;
   if (t.solver && *reinterpret_cast<volatile int*>(&bk->stop)) return;
   __shared__ T shT[4 * 32];
-  constexpr int L = EXACT ? 1 : kMergeLanes;
-  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t idx = gtid / L;
-  const int sub = static_cast<int>(gtid % L);
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   T part[3] = {T(0), T(0), T(0)};  // sum r, sum r^2, sum s^2
   if (idx < t.m) {
-    const T acc = strip_sum<T, EXACT>(t.ustrip, t.grid_cols, t.ld, idx, sub);
-    if (sub == 0) {
+    const T acc = strip_sum<T>(t.ustrip, t.grid_cols, t.ld, idx);
+    {
       t.u[idx] = acc;
       const T r = acc - t.p[idx];
       t.r_new[idx] = r;
@@ -926,8 +469,8 @@ __global__ void __launch_bounds__(kTailThreads) merge_kernel(const TailArgs<T> t
     }
   } else if (idx < t.m + t.n) {
     const int64_t j = idx - t.m;
-    const T acc = strip_sum<T, EXACT>(t.vstrip, t.grid_rows64, t.n, j, sub);
-    if (sub == 0) {
+    const T acc = strip_sum<T>(t.vstrip, t.grid_rows64, t.n, j);
+    {
       t.v[j] = acc;  // sharded: v points at the allreduce pack
       if (!t.sharded) {
         const T s = acc - t.q[j];
@@ -1081,9 +624,8 @@ __global__ void __launch_bounds__(kTailThreads) merge_kernel(const TailArgs<T> t
 
 template <class T>
 void launch_merge(const TailArgs<T>& t, bool exact, cudaStream_t st) {
-  const int64_t L = exact ? 1 : kMergeLanes;
   const unsigned blocks =
-      static_cast<unsigned>(((t.m + t.n) * L + kTailThreads - 1) / kTailThreads);
+      static_cast<unsigned>((t.m + t.n + kTailThreads - 1) / kTailThreads);
   if (exact)
     merge_kernel<T, true><<<blocks, kTailThreads, 0, st>>>(t);
   else
@@ -1130,59 +672,6 @@ void launch_finish(const TailArgs<T>& t, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 // K3: shift / defect recursions, dual value, trace row, gate
 // ---------------------------------------------------------------------------
-// Gate of solve (solver.hpp:439-504) given the O(m+n) sums of this iteration:
-// dual value sum_i p_i phi_i/rho + sum_j q_j varphi_j/rho and the rank-two
-// fixed-point terms.  Fires the confirm report (graph IF node, or a pause
-// when row-sharded) when the stale-dual gate passes.
-template <class T>
-__device__ void gate_logic(Book<T>* bk, const TailArgs<T>& t, double dual_value, double dphi2,
-                           double dphi, double dvarphi2, double dvarphi, double cross) {
-  const bool fp = bk->record_trace != 0;
-  bk->alpha = bk->alpha - bk->beta;  // solver.hpp:289
-  const int64_t k = bk->iter;
-  bk->iter = k + 1;
-  double fp_residual = __longlong_as_double(0x7ff8000000000000ULL);
-  if (fp) {  // rank-two identity (solver.hpp:443-472)
-    double fp_sq = static_cast<double>(t.n_global) * dphi2 +
-                   static_cast<double>(t.m_global) * dvarphi2 + 2.0 * dphi * dvarphi;
-    if (t.reads_cost && t.want_dx) fp_sq += static_cast<double>(bk->pass_dx) + 2.0 * cross;
-    fp_residual = sqrt(fmax(fp_sq, 0.0));
-  }
-  bk->fp_residual = fp_residual;
-  const double r_primal = sqrt(static_cast<double>(bk->nr2) + static_cast<double>(bk->ns2));
-  const double gap = fabs(bk->last_cost - dual_value);
-  const double gap_scale = bk->relative ? 1.0 / (1.0 + fabs(bk->last_cost)) : 1.0;
-  bk->r_primal = r_primal;
-  bk->dual_value = dual_value;
-  bk->gap = gap;
-  const bool check = ((k + 1) % bk->check_every) == 0;
-  const bool trace_row = bk->record_trace && ((k + 1) % bk->trace_every) == 0;
-  if (trace_row) {
-    if (bk->trace_rows < bk->trace_cap) {
-      TraceRowDev& row = t.trace[bk->trace_rows];
-      row.iter = k + 1;
-      row.r_primal = r_primal;
-      row.r_dual = bk->last_r_dual;
-      row.gap = gap;
-      row.objective = bk->last_cost;
-      row.ergodic_objective = bk->erg_mean;
-      row.fixed_point_residual = fp_residual;
-    }
-    bk->trace_rows += 1;
-  }
-  const bool fire = check && r_primal * bk->primal_scale <= bk->tol_primal &&
-                    bk->last_r_dual <= bk->tol_dual && gap * gap_scale <= bk->tol_gap;
-  if (fire) {
-    bk->confirm = 1;
-    bk->gate_hits += 1;
-    if (t.sharded) bk->stop = 2;  // pause: the host runs the collective confirm
-  } else if (k + 1 >= bk->max_iters) {
-    bk->stop = 1;
-  }
-  // the confirm report runs only when the gate fires (graph IF node)
-  if (t.use_cond) cudaGraphSetConditional(t.cond, fire ? 1u : 0u);
-}
-
 template <class T, bool EXACT>
 __global__ void __launch_bounds__(kTailThreads) update_kernel(const TailArgs<T> t) {
   Book<T>* bk = t.book;
@@ -1342,44 +831,6 @@ void launch_update(const TailArgs<T>& t, bool exact, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 // K5: exact matched-pair report (detail::state_report) + confirm
 // ---------------------------------------------------------------------------
-template <class T>
-__device__ __forceinline__ void report_elem(T xv, T cv, T phi_i, double nu_j,
-                                            double drho, T rho, bool folded,
-                                            double& obj, double& dsq) {
-  const double c = static_cast<double>(cv);
-  double x = static_cast<double>(xv);
-  if (folded) {
-    x += static_cast<double>(rho) * c;
-    if (x < 0) x = 0;
-  }
-  obj += c * x;
-  const double slack = static_cast<double>(phi_i) / drho + nu_j - c;
-  if (slack > 0) dsq += slack * slack;
-}
-
-// Exact report of the matched pair and the confirm decision
-// (solver.hpp:339-353, 508-519).  obj / dual_sq: the streamed sums.
-template <class T>
-__device__ void report_decide(Book<T>* bk, double obj, double dual_sq, int always) {
-  const double r_primal = sqrt(static_cast<double>(bk->nr2) + static_cast<double>(bk->ns2));
-  const double r_dual = sqrt(dual_sq);
-  const double gap = fabs(obj - bk->dual_value);
-  bk->rep_objective = obj;
-  bk->rep_r_primal = r_primal;
-  bk->rep_r_dual = r_dual;
-  bk->rep_gap = gap;
-  if (always) return;
-  const double egs = bk->relative ? 1.0 / (1.0 + fabs(obj)) : 1.0;
-  if (r_primal * bk->primal_scale <= bk->tol_primal && r_dual <= bk->tol_dual &&
-      gap * egs <= bk->tol_gap) {
-    bk->converged = 1;
-    bk->stop = 1;
-  } else {
-    bk->confirm = 0;
-    bk->stop = bk->iter >= bk->max_iters ? 1 : 0;  // also ends a sharded pause
-  }
-}
-
 template <class T, bool EXACT>
 __global__ void __launch_bounds__(kTailThreads)
     report_kernel(const T* __restrict__ xy, const T* __restrict__ cost,

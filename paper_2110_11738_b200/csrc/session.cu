@@ -164,6 +164,18 @@ struct Session {
   double* dpack = nullptr;  // [row-side update sums (4) | report sums (2) | misc]
   int32_t* dint = nullptr;
 
+  // persistent solver kernel (fast order, one GPU; persistent.cu)
+  bool persist = false;
+  int pgrid = 0;
+  int64_t prows = 0, pn_rb = 0, pmax_seg = 0;
+  T *pustrip = nullptr, *pvstrip = nullptr, *pcpart = nullptr;
+  double* pdpart = nullptr;
+  unsigned* pbar = nullptr;
+  int32_t *pseg_ptr = nullptr, *pseg_slot = nullptr;
+  unsigned long long* psweep_ns = nullptr;
+  bool h_stale = false;  // h_iter / h_folded lag the device after persistent launches
+  bool no_persist = false;
+
   std::vector<T> hp, hq;
   T rho = T(0);
   double rho_d = 0;
@@ -184,7 +196,14 @@ struct Session {
   void release() {
     void* bufs[] = {X, C, Xout, phi, varphi, a, b, rb[0], rb[1], sb[0], sb[1],
                     p, q, u, v, ustrip, vstrip, tscr, partials, tiles, dscr,
-                    terms, book, trace, vflags, pack, pmax, dpack, dint};
+                    terms, book, trace, vflags, pack, pmax, dpack, dint,
+                    pustrip, pvstrip, pcpart, pdpart, pbar, pseg_ptr, pseg_slot, psweep_ns};
+    pustrip = pvstrip = pcpart = nullptr;
+    pdpart = nullptr;
+    pbar = nullptr;
+    pseg_ptr = pseg_slot = nullptr;
+    psweep_ns = nullptr;
+    persist = false;
     if (comm) nccl().commDestroy(comm);
     comm = nullptr;
     pack = pmax = nullptr;
@@ -226,7 +245,116 @@ struct Session {
     bs = std::max<int64_t>(1, cfg.block_rows);
     tc = bs * std::max<int64_t>(1, cfg.work_size);
     if (!exact && !engine) tc = fast_tile_cols();
-    return allocate();
+    RC_TRY(allocate());
+    if (!exact && !engine && !no_persist) {
+      const char* e = std::getenv("DROTB_PERSIST");
+      if (!(e && e[0] == '0')) RC_TRY(setup_persistent());
+    }
+    return 0;
+  }
+
+  // Static schedule of the persistent kernel: CTA b sweeps the flat range
+  // [b*W/G, (b+1)*W/G) of the (row block, column) space; its segments get u
+  // slots b*max_seg + s, listed per row block in column order (CSR).
+  int setup_persistent() {
+    pgrid = persistent_grid<T>(device);
+    if (pgrid <= 0) return 0;  // cannot co-reside: stay on the per-launch path
+    prows = rows_per_cta<T>();
+    pn_rb = (m + prows - 1) / prows;
+    const int64_t W = pn_rb * n, G = pgrid;
+    std::vector<std::vector<int32_t>> per(static_cast<size_t>(pn_rb));
+    pmax_seg = 1;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (auto& v : per) v.clear();
+      for (int64_t bi = 0; bi < G; ++bi) {
+        int64_t f0 = bi * W / G;
+        const int64_t f1 = (bi + 1) * W / G;
+        int64_t seg = 0;
+        while (f0 < f1) {
+          const int64_t rbk = f0 / n, c0 = f0 - rbk * n;
+          const int64_t c1 = std::min<int64_t>(n, c0 + (f1 - f0));
+          per[static_cast<size_t>(rbk)].push_back(static_cast<int32_t>(bi * pmax_seg + seg));
+          f0 += c1 - c0;
+          ++seg;
+        }
+        if (pass == 0) pmax_seg = std::max<int64_t>(pmax_seg, seg);
+      }
+    }
+    std::vector<int32_t> ptr(static_cast<size_t>(pn_rb + 1), 0), slots;
+    for (int64_t r = 0; r < pn_rb; ++r) {
+      ptr[static_cast<size_t>(r + 1)] = ptr[static_cast<size_t>(r)] +
+                                        static_cast<int32_t>(per[static_cast<size_t>(r)].size());
+      slots.insert(slots.end(), per[static_cast<size_t>(r)].begin(),
+                   per[static_cast<size_t>(r)].end());
+    }
+    RC_TRY(dev_alloc(&pustrip, static_cast<size_t>(G * pmax_seg * prows)));
+    RC_TRY(dev_alloc(&pvstrip, static_cast<size_t>(pn_rb * n)));
+    RC_TRY(dev_alloc(&pcpart, static_cast<size_t>(G * 16)));
+    RC_TRY(dev_alloc(&pdpart, static_cast<size_t>(G * 16)));
+    RC_TRY(dev_alloc(&pbar, 2));
+    RC_TRY(dev_alloc(&pseg_ptr, ptr.size()));
+    RC_TRY(dev_alloc(&pseg_slot, slots.size()));
+    RC_TRY(dev_alloc(&psweep_ns, 1));
+    CUDA_TRY(cudaMemsetAsync(pbar, 0, 2 * sizeof(unsigned), stream));
+    CUDA_TRY(cudaMemsetAsync(psweep_ns, 0, sizeof(unsigned long long), stream));
+    CUDA_TRY(cudaMemsetAsync(pustrip, 0, sizeof(T) * G * pmax_seg * prows, stream));
+    CUDA_TRY(cudaMemcpyAsync(pseg_ptr, ptr.data(), sizeof(int32_t) * ptr.size(),
+                             cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaMemcpyAsync(pseg_slot, slots.data(), sizeof(int32_t) * slots.size(),
+                             cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    persist = true;
+    return 0;
+  }
+
+  PersistArgs<T> persist_args(int64_t iters) {
+    PersistArgs<T> g;
+    std::memset(&g, 0, sizeof(g));
+    g.pa = pass_args();
+    g.pa.stop = nullptr;
+    g.a = a;
+    g.b = b;
+    g.p = p;
+    g.q = q;
+    g.rb0 = rb[0];
+    g.rb1 = rb[1];
+    g.sb0 = sb[0];
+    g.sb1 = sb[1];
+    g.m_global = m_global;
+    g.n_global = n_global;
+    g.rows_cta = prows;
+    g.n_rb = pn_rb;
+    g.max_seg = pmax_seg;
+    g.ustrip = pustrip;
+    g.seg_ptr = pseg_ptr;
+    g.seg_slot = pseg_slot;
+    g.vstrip = pvstrip;
+    g.cpart = pcpart;
+    g.dpart = pdpart;
+    g.bar = pbar;
+    g.book = book;
+    g.trace = trace;
+    g.iters = iters;
+    g.engine_ref = cfg.engine == DROTB_ENGINE_REFERENCE ? 1 : 0;
+    g.skip_cost = cfg.skip_cost ? 1 : 0;
+    g.sweep_ns = psweep_ns;
+    return g;
+  }
+
+  int launch_persist(int64_t iters) {
+    CUDA_TRY(launch_persistent<T>(persist_args(iters), pgrid, want_dx, stream));
+    h_stale = true;
+    return 0;
+  }
+
+  int resync() {  // host mirrors of the iteration counter and fold state
+    if (!h_stale) return 0;
+    Book<T> hb;
+    RC_TRY(read_book(&hb));
+    h_iter = hb.iter;
+    h_folded = hb.folded != 0;
+    h_stale = false;
+    return 0;
   }
 
   // Row shard [row_begin, row_end) of an m_global x n problem on `world`
@@ -242,6 +370,7 @@ struct Session {
     if (!nccl().ok) return set_error(DROTB_ERRC_BAD_CONFIG, "NCCL unavailable: " + nccl().err);
     drotb_config c2 = c;
     c2.use_graphs = 0;  // sharded iterations are enqueued eagerly (NCCL + pause)
+    no_persist = true;  // the persistent kernel has no collective phase
     RC_TRY(create(r1 - r0, n_, c2));
     m_global = m_glob;
     row_begin = r0;
@@ -556,6 +685,7 @@ struct Session {
     gate = true;
     h_iter = 0;
     h_folded = false;
+    h_stale = false;
     initialized = true;
     return 0;
   }
@@ -796,6 +926,8 @@ struct Session {
 
   int enqueue(int64_t n_iters) {
     if (!initialized) return set_error(DROTB_ERRC_BAD_CONFIG, "session not initialized");
+    if (persist && gate && n_iters > 0) return launch_persist(n_iters);
+    RC_TRY(resync());
     const int64_t bi = batch_iters();
     while (n_iters > 0) {
       if (n_iters >= bi && graph_ok(bi)) {
@@ -831,7 +963,39 @@ struct Session {
                 int64_t* n_pass, double* pass_bytes, int64_t* launches) {
     if (!initialized) return set_error(DROTB_ERRC_BAD_CONFIG, "session not initialized");
     RC_TRY(ensure_events(static_cast<size_t>(2 * n_iters + 2)));
+    RC_TRY(resync());
     const int64_t before = kernel_launch_count();
+    if (persist && gate) {
+      // one persistent launch of n_iters iterations between two events; the
+      // sweep phases are timed inside the kernel (%globaltimer, CTA 0)
+      unsigned long long ns0 = 0, ns1 = 0;
+      CUDA_TRY(cudaMemcpyAsync(&ns0, psweep_ns, sizeof(ns0), cudaMemcpyDeviceToHost, stream));
+      int64_t k = h_iter;
+      bool f = h_folded;
+      double bsum = 0;
+      const double cells = static_cast<double>(m) * static_cast<double>(n);
+      for (int64_t it = 0; it < n_iters; ++it, ++k) {
+        int md;
+        bool fa;
+        RC_TRY(pass_mode(k, f, &md, &fa));
+        f = fa;
+        bsum += (md == kSkip ? 2.0 : 3.0) * sizeof(T) * cells;
+      }
+      CUDA_TRY(cudaEventRecord(tev[0], stream));
+      RC_TRY(launch_persist(n_iters));
+      CUDA_TRY(cudaEventRecord(tev[1], stream));
+      CUDA_TRY(cudaEventSynchronize(tev[1]));
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaMemcpy(&ns1, psweep_ns, sizeof(ns1), cudaMemcpyDeviceToHost));
+      float ms = 0;
+      CUDA_TRY(cudaEventElapsedTime(&ms, tev[0], tev[1]));
+      if (total_ms) *total_ms = ms;
+      if (pass_ms) *pass_ms = static_cast<double>(ns1 - ns0) * 1e-6;
+      if (n_pass) *n_pass = n_iters;
+      if (pass_bytes) *pass_bytes = bsum;
+      if (launches) *launches = kernel_launch_count() - before;
+      return 0;
+    }
     std::vector<int> modes(static_cast<size_t>(n_iters));
     {  // modes of the iterations about to run (host-side symbolic state)
       int64_t k = h_iter;
@@ -878,9 +1042,9 @@ struct Session {
   int64_t batch_iters() const {
     // ~1 ms of pass traffic per batch at ~6 TB/s, at least 8 iterations
     const double bytes = 3.0 * sizeof(T) * static_cast<double>(m) * n;
-    const double t_iter = bytes / 6.0e12 + 20e-6;
+    const double t_iter = bytes / 6.0e12 + (persist ? 6e-6 : 20e-6);
     int64_t bi = static_cast<int64_t>(1e-3 / t_iter) + 1;
-    bi = std::max<int64_t>(8, std::min<int64_t>(bi, 256));
+    bi = std::max<int64_t>(8, std::min<int64_t>(bi, persist ? 1024 : 256));
     return bi + (bi & 1);
   }
 
@@ -927,8 +1091,10 @@ struct Session {
     int slot = 0;
     bool pending = false;
     const int64_t limit = std::max<int64_t>(cfg.max_iters, 0) + 4 * bi + 4;
+    int64_t launched = 0;
     while (true) {
       RC_TRY(enqueue(bi));
+      launched += bi;
       CUDA_TRY(cudaMemcpyAsync(&h_stop[slot], &book->stop, sizeof(int32_t),
                                cudaMemcpyDeviceToHost, stream));
       CUDA_TRY(cudaEventRecord(ev[slot], stream));
@@ -938,7 +1104,7 @@ struct Session {
       }
       pending = true;
       slot ^= 1;
-      if (h_iter > limit) break;  // the device sets stop at max_iters
+      if (launched > limit) break;  // the device sets stop at max_iters
     }
     CUDA_TRY(cudaStreamSynchronize(stream));
     return 0;
@@ -1089,6 +1255,7 @@ struct Session {
     gate = false;
     h_iter = iter;
     h_folded = folded != 0;
+    h_stale = false;
     initialized = true;
     return 0;
   }
@@ -1695,6 +1862,15 @@ int drotb_residual_report_f64(const double* C, int64_t m, int64_t n, const doubl
                               const double* nu, int32_t exact, drotb_report* out) {
   drotb::clear_error();
   return residual_report_t<double>(C, m, n, p, q, plan, mu, nu, exact, out);
+}
+
+int32_t drotb_session_persistent_grid(drotb_session* s) {
+  if (s->precision == 0) {
+    auto* ss = drotb::as_session<float>(s->impl);
+    return ss->persist ? ss->pgrid : 0;
+  }
+  auto* ss = drotb::as_session<double>(s->impl);
+  return ss->persist ? ss->pgrid : 0;
 }
 
 int drotb_session_support(drotb_session* s, double rel_tau, double abs_tau, int64_t* nnz,

@@ -159,5 +159,10 @@ class Session:
         return dict(total_ms=tot.value, pass_ms=pms.value, n_pass=npass.value,
                     pass_bytes=pb.value, launches=launches.value)
 
+    @property
+    def persistent_grid(self) -> int:
+        """CTAs of the persistent solver kernel (0: per-launch kernels + graphs)."""
+        return int(_lib.load().drotb_session_persistent_grid(self._h))
+
     def device_xy(self) -> int:
         return _lib.load().drotb_session_device_xy(self._h)

@@ -11,8 +11,8 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("dt", [np.float64, np.float32])
 def test_sharded_world1_matches_single(drot, dt):
-    m, n = 900, 700
-    cfg = drot.DrotConfig(max_iters=20000)
+    m, n = 400, 300
+    cfg = drot.DrotConfig(max_iters=200000)
     single = drot.Session(m, n, dt, cfg)
     single.gen_gaussian(5.0, 3, "dyadic")
     single.init()
