@@ -167,6 +167,11 @@ int drotb_solve_f64(const double* C, int64_t m, int64_t n, const double* p,
                     int64_t* trace_len, int64_t* iterations, int32_t* status,
                     double* wall_time_s);
 
+/* drotb_solve_* keeps one device context per host thread and precision
+ * (buffers, stream, schedule, graphs) for repeated solves of the same shape
+ * and configuration; this frees it. */
+void drotb_release_cache(void);
+
 /* ---- one iteration on caller-owned state: drot::drot_step<T> ------------ *
  * (solver.hpp:361-370).  The DrotState<T> fields (solver.hpp:98-114) are
  * passed as arrays and updated in place: xy (m*n), *cost_folded, row_shift

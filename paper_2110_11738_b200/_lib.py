@@ -62,6 +62,7 @@ SIGNATURES = {
     "drotb_errc_name": (C.c_char_p, [i32]),
     "drotb_config_default": (None, [P(drotb_config)]),
     "drotb_kernel_launches": (i64, []),
+    "drotb_release_cache": (None, []),
     "drotb_solve_f32": (C.c_int, [vp, i64, i64, vp, vp, P(drotb_config), vp, vp, vp, vp,
                                   P(f32), P(drotb_report), vp, i64, P(i64), P(i64),
                                   P(i32), P(f64)]),

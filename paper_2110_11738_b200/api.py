@@ -649,5 +649,10 @@ def dyadic_marginal(length: int, dtype=np.float64) -> np.ndarray:
     return out
 
 
+def release_device_cache() -> None:
+    """Free the device context solve() keeps for repeated solves of one shape."""
+    _lib.load().drotb_release_cache()
+
+
 def kernel_launches() -> int:
     return int(_lib.load().drotb_kernel_launches())

@@ -165,6 +165,7 @@ struct PersistArgs {
   int64_t iters;            // iterations this launch (upper bound)
   int32_t engine_ref, skip_cost;
   unsigned long long* sweep_ns;  // accumulated P1 time (CTA 0, %globaltimer)
+  double* mud;              // [m] phi_i / rho of the current iterate (confirm report)
 };
 
 template <class T>
@@ -206,7 +207,7 @@ void launch_init_x0(T* xy, const T* p, const T* q, int64_t m, int64_t n,
 template <class T>
 void launch_init_sums(const T* xy, const T* p, const T* q, T* a, T* b,
                       int64_t m, int64_t n, int64_t ld, Book<T>* book,
-                      cudaStream_t st, T* shard_pack = nullptr);
+                      cudaStream_t st, T* shard_pack = nullptr, bool x0_is_pq = false);
 template <class T>
 void launch_validate(const T* buf, int64_t m, int64_t n, int64_t ld,
                      unsigned long long* first_nonfinite,

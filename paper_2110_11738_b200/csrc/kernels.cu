@@ -17,6 +17,7 @@
 // expression below is evaluated exactly as written, in the association order
 // of the reference (no FMA contraction).  The fast-mode scalar reductions of
 // K1 use explicit fma() because their order is ours anyway.
+#include <algorithm>
 #include <cfloat>
 #include <cstdio>
 #include <cstdlib>
@@ -920,16 +921,80 @@ void launch_report_final(const TailArgs<T>& t, bool always, cudaStream_t st) {
   count_launch();
 }
 
+// Fast-order report: 2-D grid of (256*R-row chunk, column stride) blocks;
+// each thread owns R rows (128-bit loads of X and C) with mu_i = phi_i/rho
+// computed once, and walks the block's columns.
+template <class T>
+__global__ void __launch_bounds__(kTailThreads)
+    report_fast_kernel(const T* __restrict__ xy, const T* __restrict__ cost,
+                       const TailArgs<T> t, int always) {
+  using V = typename V16<T>::type;
+  constexpr int R = 16 / sizeof(T);
+  Book<T>* bk = t.book;
+  if (!always) {
+    if (*reinterpret_cast<volatile int*>(&bk->stop) == 1 ||
+        !*reinterpret_cast<volatile int*>(&bk->confirm))
+      return;
+  }
+  __shared__ double shD[2 * 32];
+  const bool folded = bk->folded != 0;
+  const double drho = static_cast<double>(t.rho);
+  const int64_t row0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * R;
+  double mu[R];
+  int nvalid = 0;
+  if (row0 < t.m) {
+    nvalid = static_cast<int>(imin64(R, t.m - row0));
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+      mu[k] = k < nvalid ? static_cast<double>(t.phi[row0 + k]) / drho : 0.0;
+  }
+  double part[2] = {0, 0};
+  if (nvalid > 0) {
+    for (int64_t j = blockIdx.y; j < t.n; j += gridDim.y) {
+      const double nu_j = static_cast<double>(t.varphi[j]) / drho;
+      T xv[R], cv[R];
+      unpack(__ldcs(reinterpret_cast<const V*>(xy + j * t.ld + row0)), xv);
+      unpack(__ldcs(reinterpret_cast<const V*>(cost + j * t.ld + row0)), cv);
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+        if (k < nvalid) report_elem_mu<T>(xv[k], cv[k], mu[k], nu_j, t.rho, folded, part[0], part[1]);
+    }
+  }
+  block_sum<double, 2>(part, shD);
+  const int64_t bid = static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x;
+  if (threadIdx.x == 0) {
+    t.dscratch[bid * 2 + 0] = part[0];
+    t.dscratch[bid * 2 + 1] = part[1];
+  }
+  if (!last_block(&bk->ticket_report)) return;
+  const int64_t nb = static_cast<int64_t>(gridDim.x) * gridDim.y;
+  double s2[2] = {0, 0};
+  for (int64_t k = threadIdx.x; k < nb; k += blockDim.x) {
+    s2[0] += t.dscratch[k * 2 + 0];
+    s2[1] += t.dscratch[k * 2 + 1];
+  }
+  block_sum<double, 2>(s2, shD);
+  if (threadIdx.x != 0) return;
+  bk->ticket_report = 0u;
+  if (t.sharded) {
+    t.dpack[4] = s2[0];
+    t.dpack[5] = s2[1];
+    return;
+  }
+  report_decide<T>(bk, s2[0], s2[1], always);
+}
+
 template <class T>
 void launch_report(const T* xy, const T* cost, const TailArgs<T>& t,
                    bool exact, bool always, cudaStream_t st) {
   if (exact) {
     report_kernel<T, true><<<1, kTailThreads, 0, st>>>(xy, cost, t, always ? 1 : 0);
   } else {
-    const int64_t blocks = imin64(t.n, 148 * 4);
-    report_kernel<T, false>
-        <<<static_cast<unsigned>(blocks), kTailThreads, 0, st>>>(xy, cost, t,
-                                                                 always ? 1 : 0);
+    constexpr int R = 16 / sizeof(T);
+    const int64_t gx = (t.m + int64_t(kTailThreads) * R - 1) / (int64_t(kTailThreads) * R);
+    const int64_t gy = imin64(t.n, std::max<int64_t>(1, (148 * 8 + gx - 1) / gx));
+    report_fast_kernel<T><<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy)),
+                            kTailThreads, 0, st>>>(xy, cost, t, always ? 1 : 0);
   }
   count_launch();
 }
@@ -956,44 +1021,96 @@ void launch_init_x0(T* xy, const T* p, const T* q, int64_t m, int64_t n,
   count_launch();
 }
 
-// a = row_sums(X0) - p (untiled, sequential over columns, matrix.hpp:128-136)
+// a = row_sums(X0) - p (untiled, sequential over columns, matrix.hpp:128-136).
+// With X0 = p q^T (no user x0) the entries are recomputed as p_i * q_j -- the
+// very products init_x0 stored -- from q staged in shared memory, so the
+// sequential chains need no pass over X0 and stay bitwise the reference's.
+constexpr int kInitStage = 2048;
+
 template <class T>
-__global__ void init_rows_kernel(const T* xy, const T* p, T* a, int64_t m,
-                                 int64_t n, int64_t ld) {
+__global__ void __launch_bounds__(128)
+    init_rows_kernel(const T* xy, const T* p, const T* q, T* a, int64_t m, int64_t n,
+                     int64_t ld, int pq) {
+  __shared__ T sq[kInitStage];
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= m) return;
+  const T pi = i < m ? p[i] : T(0);
   T acc = T(0);
-  for (int64_t j = 0; j < n; ++j) acc += xy[j * ld + i];
-  a[i] = acc - p[i];
+  if (pq) {
+    for (int64_t j0 = 0; j0 < n; j0 += kInitStage) {
+      const int cnt = static_cast<int>(imin64(kInitStage, n - j0));
+      __syncthreads();
+      for (int e = threadIdx.x; e < cnt; e += blockDim.x) sq[e] = q[j0 + e];
+      __syncthreads();
+      if (i < m)
+        for (int e = 0; e < cnt; ++e) acc += pi * sq[e];
+    }
+  } else if (i < m) {
+    int64_t j = 0;
+    for (; j + 16 <= n; j += 16) {
+      T v[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) v[t] = xy[(j + t) * ld + i];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) acc += v[t];
+    }
+    for (; j < n; ++j) acc += xy[j * ld + i];
+  }
+  if (i < m) a[i] = acc - pi;
 }
 
 // b = col_sums(X0) - q (sequential over rows, matrix.hpp:139-149); sharded
-// ranks write the local column partial (q subtracted after the allreduce)
+// ranks write the local column partial (q subtracted after the allreduce).
+// Same recomputation for X0 = p q^T; a user x0 is read through a shared-
+// memory transpose (32 columns per block, coalesced loads).
 template <class T>
-__global__ void init_cols_kernel(const T* xy, const T* q, T* b, int64_t m,
-                                 int64_t n, int64_t ld, int subtract) {
+__global__ void __launch_bounds__(128)
+    init_cols_kernel(const T* xy, const T* p, const T* q, T* b, int64_t m, int64_t n,
+                     int64_t ld, int subtract, int pq) {
+  __shared__ T sp[kInitStage];
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  const T* c = xy + j * ld;
+  const T qj = j < n ? q[j] : T(0);
   T acc = T(0);
-  for (int64_t i = 0; i < m; ++i) acc += c[i];
-  b[j] = subtract ? acc - q[j] : acc;
+  if (pq) {
+    for (int64_t i0 = 0; i0 < m; i0 += kInitStage) {
+      const int cnt = static_cast<int>(imin64(kInitStage, m - i0));
+      __syncthreads();
+      for (int e = threadIdx.x; e < cnt; e += blockDim.x) sp[e] = p[i0 + e];
+      __syncthreads();
+      if (j < n)
+        for (int e = 0; e < cnt; ++e) acc += sp[e] * qj;
+    }
+  } else if (j < n) {
+    const T* c = xy + j * ld;
+    for (int64_t i = 0; i < m; ++i) acc += c[i];
+  }
+  if (j < n) b[j] = subtract ? acc - qj : acc;
 }
 
 template <class T>
-__global__ void init_alpha_kernel(const T* a, const T* b, int64_t m, int64_t n,
-                                  int64_t mn_global, Book<T>* bk, T* shard_pack) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__global__ void __launch_bounds__(256)
+    init_alpha_kernel(const T* a, const T* b, int64_t m, int64_t n, int64_t mn_global,
+                      Book<T>* bk, T* shard_pack) {
+  __shared__ double sraw[2 * kStage];
+  __shared__ T ch[2];
+  T* sb = reinterpret_cast<T*>(sraw);
+  // sequential vec_sum(a) and vec_norm_sq(a) (matrix.hpp:99-118), staged
+  staged_chains<T, 2>(m, [&](int k, int64_t e) { const T v = a[e]; return k == 0 ? v : v * v; },
+                      sb, ch);
+  const T sa = ch[0], sa2 = ch[1];
+  __syncthreads();
+  staged_chains<T, 1>(n, [&](int, int64_t e) { const T v = b[e]; return v * v; }, sb, ch);
+  const T sb2 = ch[0];
+  if (threadIdx.x != 0) return;
   if (shard_pack) {  // rank-local sums, finished after the allreduce
-    shard_pack[0] = serial_sum<T, false>(a, m);
-    shard_pack[1] = serial_sum<T, true>(a, m);
+    shard_pack[0] = sa;
+    shard_pack[1] = sa2;
     return;
   }
-  const T alpha = serial_sum<T, false>(a, m) / static_cast<T>(mn_global);
+  const T alpha = sa / static_cast<T>(mn_global);
   bk->alpha = alpha;  // solver.hpp:177-178
   bk->beta = alpha;   // solver.hpp:183
-  bk->nr2 = serial_sum<T, true>(a, m);  // r = a, s = b (solver.hpp:181-182)
-  bk->ns2 = serial_sum<T, true>(b, n);
+  bk->nr2 = sa2;      // r = a, s = b (solver.hpp:181-182)
+  bk->ns2 = sb2;
 }
 
 template <class T>
@@ -1018,12 +1135,12 @@ void launch_init_sharded_finish(T* b, const T* q, int64_t n, const T* pack,
 template <class T>
 void launch_init_sums(const T* xy, const T* p, const T* q, T* a, T* b,
                       int64_t m, int64_t n, int64_t ld, Book<T>* book,
-                      cudaStream_t st, T* shard_pack) {
+                      cudaStream_t st, T* shard_pack, bool x0_is_pq) {
   init_rows_kernel<T><<<static_cast<unsigned>((m + 127) / 128), 128, 0, st>>>(
-      xy, p, a, m, n, ld);
+      xy, p, q, a, m, n, ld, x0_is_pq ? 1 : 0);
   init_cols_kernel<T><<<static_cast<unsigned>((n + 127) / 128), 128, 0, st>>>(
-      xy, q, b, m, n, ld, shard_pack ? 0 : 1);
-  init_alpha_kernel<T><<<1, 32, 0, st>>>(a, b, m, n, m + n, book, shard_pack);
+      xy, p, q, b, m, n, ld, shard_pack ? 0 : 1, x0_is_pq ? 1 : 0);
+  init_alpha_kernel<T><<<1, 256, 0, st>>>(a, b, m, n, m + n, book, shard_pack);
   count_launch(3);
 }
 
@@ -1159,7 +1276,7 @@ void launch_plan_count(const T* xy, const T* cost, T rho, int folded, int64_t m,
                                   int64_t, cudaStream_t);                      \
   template void launch_init_sums<T>(const T*, const T*, const T*, T*, T*,      \
                                     int64_t, int64_t, int64_t, Book<T>*,       \
-                                    cudaStream_t, T*);                         \
+                                    cudaStream_t, T*, bool);                   \
   template void launch_finish<T>(const TailArgs<T>&, cudaStream_t);            \
   template void launch_gate<T>(const TailArgs<T>&, cudaStream_t);              \
   template void launch_report_final<T>(const TailArgs<T>&, bool, cudaStream_t);\

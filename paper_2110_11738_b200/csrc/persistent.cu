@@ -139,9 +139,43 @@ __device__ __forceinline__ void cta_store(U (&v)[K], U* part, int off, U* sh) {
 }
 
 // P1 on one column segment [c0, c1) of row block rbk: the cp.async ring of
-// K1-async, with the v partials summed over the CTA's 4 warps (rows
-// [rbk*rows_cta, +rows_cta)) per 16-column chunk and written to
-// vstrip[rbk][j].
+// K1-async over sub-segments of kSub columns.  Per sub-segment the CTA
+// stages varphi[j] in shared memory once (one coalesced L2 read per column
+// for the 4 warps, instead of a dependent L2 load per warp and column); the
+// per-warp v partials of kVGroup consecutive 16-column chunks go to one half
+// of a double-buffered shared array and are combined over the 4 warps (fixed
+// order) after one __syncthreads per kVGroup chunks, into vstrip[rbk][j].
+constexpr int kVGroup = 4;
+
+template <class T>
+constexpr int sub_cols() {
+  return 4096 / static_cast<int>(sizeof(T));  // 1024 fp32 / 512 fp64 columns
+}
+
+template <class T>
+struct SweepSmem {
+  T vp[sub_cols<T>()];                                      // staged varphi
+  T vacc[2][kVGroup][kWarpsPerCta][kChunkCols];             // v partials
+};
+
+template <class T>
+__device__ __forceinline__ void flush_vgroup(const PersistArgs<T>& g, SweepSmem<T>& sm, int half,
+                                             int64_t rbk, int64_t gcol0, int64_t c1, int n_in,
+                                             int64_t n) {
+  // threads 0 .. kVGroup*16-1: one column of the group each
+  const int t = threadIdx.x;
+  if (t < kVGroup * kChunkCols) {
+    const int ch = t / kChunkCols, c = t % kChunkCols;
+    const int64_t j = gcol0 + static_cast<int64_t>(ch) * kChunkCols + c;
+    if (ch < n_in && j < c1) {
+      T tot = T(0);
+#pragma unroll
+      for (int w = 0; w < kWarpsPerCta; ++w) tot += sm.vacc[half][ch][w][c];
+      g.vstrip[rbk * n + j] = tot;
+    }
+  }
+}
+
 template <class T, int MODE, bool DUAL, bool DX, bool MASK>
 __device__ __forceinline__ void sweep_segment(const PersistArgs<T>& g, const PassArgs<T>& a,
                                               int64_t rbk, int64_t c0, int64_t c1,
@@ -149,102 +183,106 @@ __device__ __forceinline__ void sweep_segment(const PersistArgs<T>& g, const Pas
                                               const T (&ph)[16 / sizeof(T)],
                                               T (&u)[16 / sizeof(T)], PassAcc<T>& acc,
                                               T* wbuf, typename V16<T>::type* ring,
-                                              T (*vacc)[kWarpsPerCta][kChunkCols], int warp,
-                                              int lane) {
+                                              SweepSmem<T>& sm, int warp, int lane) {
   constexpr int R = 16 / sizeof(T);
   constexpr int ROWS_W = 32 * R;
   constexpr int NB = ROWS_W / kVBlockRows;  // 64-row blocks per warp (2 fp32, 1 fp64)
   constexpr bool RC = MODE != kSkip;
   constexpr int S = kAsyncS, G = RC ? kAsyncG : 2 * kAsyncG, CH = kChunkCols;
   constexpr int NG = CH / G;
+  constexpr int SUB = sub_cols<T>();
   static_assert(NG % S == 0, "stages must divide the groups of a chunk");
+  static_assert(SUB % (CH * kVGroup) == 0, "sub-segments hold whole chunk groups");
   const bool live = !MASK || nvalid > 0;
-  T vb[S][G];
   auto xslot = [&](int st, int k) { return ring + (st * 2 * kAsyncG + k) * 32 + lane; };
   auto cslot = [&](int st, int k) {
     return ring + (st * 2 * kAsyncG + kAsyncG + k) * 32 + lane;
   };
-  auto issue = [&](int st, int64_t jg) {
+  int half = 0;
+  for (int64_t s0 = c0; s0 < c1; s0 += SUB) {
+    const int64_t s1 = imin64(c1, s0 + SUB);
+    __syncthreads();  // previous sub-segment's readers of sm.vp are done
+    for (int64_t j = s0 + threadIdx.x; j < s1; j += kPT) sm.vp[j - s0] = __ldcg(a.varphi + j);
+    __syncthreads();
+    auto issue = [&](int st, int64_t jg) {
 #pragma unroll
-    for (int k = 0; k < G; ++k) {
-      const int64_t col = jg + k;
-      vb[st][k] = T(0);
-      if (col < c1) {
-        if (live) {
+      for (int k = 0; k < G; ++k) {
+        const int64_t col = jg + k;
+        if (live && col < s1) {
           const int64_t off = col * a.ld + row0;
           cp_async16(xslot(st, k), a.xy + off);
           if (RC) cp_async16(cslot(st, k), a.cost + off);
         }
-        vb[st][k] = __ldcg(a.varphi + col);
       }
-    }
-    cp_async_commit();
-  };
+      cp_async_commit();
+    };
 #pragma unroll
-  for (int st = 0; st < S - 1; ++st) issue(st, c0 + st * G);
-  int buf = 0;
-  for (int64_t j0 = c0; j0 < c1; j0 += CH) {
+    for (int st = 0; st < S - 1; ++st) issue(st, s0 + st * G);
+    int ch_in = 0;  // chunk index within the current v group
+    int64_t gcol0 = s0;
+    for (int64_t j0 = s0; j0 < s1; j0 += CH) {
 #pragma unroll
-    for (int gg = 0; gg < NG; ++gg) {
-      const int st = gg % S;
-      issue((gg + S - 1) % S, j0 + (gg + S - 1) * G);
-      cp_async_wait<S - 1>();
+      for (int gg = 0; gg < NG; ++gg) {
+        const int st = gg % S;
+        issue((gg + S - 1) % S, j0 + (gg + S - 1) * G);
+        cp_async_wait<S - 1>();
 #pragma unroll
-      for (int k = 0; k < G; ++k) {
-        const int64_t col = j0 + gg * G + k;
-        if (col < c1) {
-          T x[R], cc[R];
+        for (int k = 0; k < G; ++k) {
+          const int64_t col = j0 + gg * G + k;
+          if (col < s1) {
+            T x[R], cc[R];
 #pragma unroll
-          for (int t = 0; t < R; ++t) x[t] = cc[t] = T(0);
-          if (live) {
-            unpack(*xslot(st, k), x);
-            if (RC) unpack(*cslot(st, k), cc);
+            for (int t = 0; t < R; ++t) x[t] = cc[t] = T(0);
+            if (live) {
+              unpack(*xslot(st, k), x);
+              if (RC) unpack(*cslot(st, k), cc);
+            }
+            compute_col<T, MODE, DUAL, DX, MASK>(a, x, cc, sm.vp[col - s0], col, gg * G + k,
+                                                 row0, nvalid, ph, u, acc, wbuf, lane);
           }
-          compute_col<T, MODE, DUAL, DX, MASK>(a, x, cc, vb[st][k], col, gg * G + k, row0,
-                                               nvalid, ph, u, acc, wbuf, lane);
         }
       }
-    }
-    const int cnt = static_cast<int>(imin64(CH, c1 - j0));
-    __syncwarp();
-    // per-warp column partials: lane (c, b) sums 64-row block b of staged
-    // column c in row order, then the warp's blocks are added
-    T s = T(0);
-    if (lane < CH * NB) {
-      const int c = lane % CH, bb = lane / CH;
-      if (c < cnt) {
-        using V = typename V16<T>::type;
-        const V* col = reinterpret_cast<const V*>(wbuf) + c * 32;
-        const int g7 = c & 7;
-        constexpr int QB = kVBlockRows / R;
+      const int cnt = static_cast<int>(imin64(CH, s1 - j0));
+      __syncwarp();
+      // per-warp column partials: lane (c, b) sums 64-row block b of staged
+      // column c in row order, then the warp's blocks are added
+      T sv = T(0);
+      if (lane < CH * NB) {
+        const int c = lane % CH, bb = lane / CH;
+        if (c < cnt) {
+          using V = typename V16<T>::type;
+          const V* col = reinterpret_cast<const V*>(wbuf) + c * 32;
+          const int g7 = c & 7;
+          constexpr int QB = kVBlockRows / R;
 #pragma unroll
-        for (int qq = 0; qq < QB; ++qq) {
-          T v4[R];
-          unpack(col[(bb * QB + qq) ^ g7], v4);
+          for (int qq = 0; qq < QB; ++qq) {
+            T v4[R];
+            unpack(col[(bb * QB + qq) ^ g7], v4);
 #pragma unroll
-          for (int t = 0; t < R; ++t) s += v4[t];
+            for (int t = 0; t < R; ++t) sv += v4[t];
+          }
         }
       }
+      if (NB == 2) sv += __shfl_down_sync(0xffffffffu, sv, 16);
+      if (lane < CH) sm.vacc[half][ch_in][warp][lane] = sv;
+      __syncwarp();  // the staging buffer is rewritten by the next chunk
+      if (++ch_in == kVGroup || j0 + CH >= s1) {
+        __syncthreads();
+        flush_vgroup(g, sm, half, rbk, gcol0, s1, ch_in, a.n);
+        half ^= 1;
+        ch_in = 0;
+        gcol0 = j0 + CH;
+      }
     }
-    if (NB == 2) s += __shfl_down_sync(0xffffffffu, s, 16);
-    if (lane < CH) vacc[buf][warp][lane] = s;
-    __syncthreads();
-    if (warp == 0 && lane < cnt) {
-      T tot = T(0);
-#pragma unroll
-      for (int w = 0; w < kWarpsPerCta; ++w) tot += vacc[buf][w][lane];
-      g.vstrip[rbk * a.n + j0 + lane] = tot;
-    }
-    buf ^= 1;
+    cp_async_wait<0>();
   }
-  cp_async_wait<0>();
 }
 
 template <class T, int MODE, bool DUAL, bool DX>
 __device__ void sweep_phase(const PersistArgs<T>& g, const PassArgs<T>& a, int64_t f0,
                             int64_t f1, PassAcc<T>& acc, T* wbuf,
-                            typename V16<T>::type* ring, T (*vacc)[kWarpsPerCta][kChunkCols],
-                            int warp, int lane) {
+                            typename V16<T>::type* ring, SweepSmem<T>& sm, int warp,
+                            int lane) {
   using V = typename V16<T>::type;
   constexpr int R = 16 / sizeof(T);
   constexpr int ROWS_W = 32 * R;
@@ -269,10 +307,10 @@ __device__ void sweep_phase(const PersistArgs<T>& g, const PassArgs<T>& a, int64
     for (int t = 0; t < R; ++t) u[t] = T(0);
     if (__syncthreads_and(nvalid == R))
       sweep_segment<T, MODE, DUAL, DX, false>(g, a, rbk, c0, c1, row0, nvalid, ph, u, acc,
-                                              wbuf, ring, vacc, warp, lane);
+                                              wbuf, ring, sm, warp, lane);
     else
       sweep_segment<T, MODE, DUAL, DX, true>(g, a, rbk, c0, c1, row0, nvalid, ph, u, acc,
-                                             wbuf, ring, vacc, warp, lane);
+                                             wbuf, ring, sm, warp, lane);
     if (nvalid > 0) {
       const int64_t slot = static_cast<int64_t>(blockIdx.x) * g.max_seg + seg;
       *reinterpret_cast<V*>(g.ustrip + slot * g.rows_cta + (row0 - rbk * g.rows_cta)) =
@@ -307,7 +345,7 @@ __global__ void __launch_bounds__(kPT, 3) solve_kernel(const PersistArgs<T> g) {
   constexpr int ROWS_W = 32 * R;
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   __shared__ Book<T> S;
-  __shared__ T vacc[2][kWarpsPerCta][kChunkCols];
+  __shared__ SweepSmem<T> sm;
   __shared__ PassAcc<T> wacc[kWarpsPerCta];
   __shared__ T shT[16 * kWarpsPerCta];
   __shared__ double shD[16 * kWarpsPerCta];
@@ -357,16 +395,16 @@ __global__ void __launch_bounds__(kPT, 3) solve_kernel(const PersistArgs<T> g) {
     PassAcc<T> acc{T(0), T(0), T(0), T(0), T(0), false};
     switch (mode) {
       case kPlain0:
-        sweep_phase<T, kPlain0, true, DX>(g, a, f0, f1, acc, wbuf, ring, vacc, warp, lane);
+        sweep_phase<T, kPlain0, true, DX>(g, a, f0, f1, acc, wbuf, ring, sm, warp, lane);
         break;
       case kPlain1:
-        sweep_phase<T, kPlain1, true, DX>(g, a, f0, f1, acc, wbuf, ring, vacc, warp, lane);
+        sweep_phase<T, kPlain1, true, DX>(g, a, f0, f1, acc, wbuf, ring, sm, warp, lane);
         break;
       case kFold:
-        sweep_phase<T, kFold, true, DX>(g, a, f0, f1, acc, wbuf, ring, vacc, warp, lane);
+        sweep_phase<T, kFold, true, DX>(g, a, f0, f1, acc, wbuf, ring, sm, warp, lane);
         break;
       default:
-        sweep_phase<T, kSkip, false, false>(g, a, f0, f1, acc, wbuf, ring, vacc, warp, lane);
+        sweep_phase<T, kSkip, false, false>(g, a, f0, f1, acc, wbuf, ring, sm, warp, lane);
     }
     acc.cost = warp_sum(acc.cost);
     acc.prev = warp_sum(acc.prev);
@@ -483,6 +521,7 @@ __global__ void __launch_bounds__(kPT, 3) solve_kernel(const PersistArgs<T> g) {
           const_cast<T*>(a.phi)[idx] = ph;
           g.a[idx] = ai - r;  // solver.hpp:287
           part[0] = part[0] + static_cast<double>(g.p[idx]) * static_cast<double>(ph) / drho;
+          g.mud[idx] = static_cast<double>(ph) / drho;  // mu_i of the confirm report
           if (fp) {
             const double d = static_cast<double>(ph) - static_cast<double>(ph_old);
             part[1] += d * d;
@@ -530,8 +569,8 @@ __global__ void __launch_bounds__(kPT, 3) solve_kernel(const PersistArgs<T> g) {
         const T* xc = a.xy + j * a.ld;
         const T* cc = a.cost + j * a.ld;
         for (int64_t i = tid; i < m; i += kPT)
-          report_elem<T>(__ldcg(xc + i), __ldcg(cc + i), __ldcg(a.phi + i), nu_j, drho, a.rho,
-                         fo, part[0], part[1]);
+          report_elem_mu<T>(__ldcg(xc + i), __ldcg(cc + i), __ldcg(g.mud + i), nu_j, a.rho, fo,
+                            part[0], part[1]);
       }
       cta_store<double, 2>(part, g.dpart, 8, shD);
       grid_barrier(g.bar, G);

@@ -173,6 +173,7 @@ struct Session {
   unsigned* pbar = nullptr;
   int32_t *pseg_ptr = nullptr, *pseg_slot = nullptr;
   unsigned long long* psweep_ns = nullptr;
+  double* pmud = nullptr;
   bool h_stale = false;  // h_iter / h_folded lag the device after persistent launches
   bool no_persist = false;
 
@@ -197,12 +198,13 @@ struct Session {
     void* bufs[] = {X, C, Xout, phi, varphi, a, b, rb[0], rb[1], sb[0], sb[1],
                     p, q, u, v, ustrip, vstrip, tscr, partials, tiles, dscr,
                     terms, book, trace, vflags, pack, pmax, dpack, dint,
-                    pustrip, pvstrip, pcpart, pdpart, pbar, pseg_ptr, pseg_slot, psweep_ns};
+                    pustrip, pvstrip, pcpart, pdpart, pbar, pseg_ptr, pseg_slot, psweep_ns, pmud};
     pustrip = pvstrip = pcpart = nullptr;
     pdpart = nullptr;
     pbar = nullptr;
     pseg_ptr = pseg_slot = nullptr;
     psweep_ns = nullptr;
+    pmud = nullptr;
     persist = false;
     if (comm) nccl().commDestroy(comm);
     comm = nullptr;
@@ -295,6 +297,7 @@ struct Session {
     RC_TRY(dev_alloc(&pseg_ptr, ptr.size()));
     RC_TRY(dev_alloc(&pseg_slot, slots.size()));
     RC_TRY(dev_alloc(&psweep_ns, 1));
+    RC_TRY(dev_alloc(&pmud, static_cast<size_t>(ld)));
     CUDA_TRY(cudaMemsetAsync(pbar, 0, 2 * sizeof(unsigned), stream));
     CUDA_TRY(cudaMemsetAsync(psweep_ns, 0, sizeof(unsigned long long), stream));
     CUDA_TRY(cudaMemsetAsync(pustrip, 0, sizeof(T) * G * pmax_seg * prows, stream));
@@ -338,6 +341,7 @@ struct Session {
     g.engine_ref = cfg.engine == DROTB_ENGINE_REFERENCE ? 1 : 0;
     g.skip_cost = cfg.skip_cost ? 1 : 0;
     g.sweep_ns = psweep_ns;
+    g.mud = pmud;
     return g;
   }
 
@@ -434,7 +438,7 @@ struct Session {
     tile_grid_rows = (m + bs - 1) / bs;
     n_tiles = tile_grid_rows * grid_cols;
     tail_blocks = (m + n + 255) / 256;
-    report_blocks = std::min<int64_t>(n, 148 * 4);
+    report_blocks = 148 * 8 + (m + 256 * R - 1) / (256 * R) + 1;  // report_fast_kernel grid bound
     const size_t mat = static_cast<size_t>(ld) * static_cast<size_t>(n);
     RC_TRY(dev_alloc(&X, mat));
     RC_TRY(dev_alloc(&C, mat));
@@ -670,12 +674,12 @@ struct Session {
     if (cfg.max_iters <= 0) hb.stop = 1;
     CUDA_TRY(cudaMemcpyAsync(book, &hb, sizeof(hb), cudaMemcpyHostToDevice, stream));
     if (sharded) {  // column sums and sum(a) span all ranks
-      launch_init_sums<T>(X, p, q, a, b, m, n, ld, book, stream, pack);
+      launch_init_sums<T>(X, p, q, a, b, m, n, ld, book, stream, pack, x0 == nullptr);
       RC_TRY(allreduce(b, static_cast<size_t>(n), ncclSum));
       RC_TRY(allreduce(pack, 2, ncclSum));
       launch_init_sharded_finish<T>(b, q, n, pack, m_global + n_global, book, stream);
     } else {
-      launch_init_sums<T>(X, p, q, a, b, m, n, ld, book, stream);
+      launch_init_sums<T>(X, p, q, a, b, m, n, ld, book, stream, nullptr, x0 == nullptr);
     }
     CUDA_TRY(cudaMemcpyAsync(rb[0], a, sizeof(T) * ld, cudaMemcpyDeviceToDevice, stream));
     CUDA_TRY(cudaMemcpyAsync(sb[0], b, sizeof(T) * n, cudaMemcpyDeviceToDevice, stream));
@@ -1359,6 +1363,35 @@ drotb_config effective(const drotb_config* cfg) {
   return c;
 }
 
+// One cached session per host thread and precision: a repeated solve of the
+// same shape and configuration reuses its device buffers, stream, schedule
+// and captured graphs instead of reallocating ~2*m*n*sizeof(T) per call
+// (drotb_release_cache() frees it).
+template <class T>
+struct SolveCache {
+  std::unique_ptr<Session<T>> s;
+  int64_t m = 0, n = 0;
+  drotb_config cfg{};
+  Session<T>* get(int64_t m_, int64_t n_, const drotb_config& c, int* rc) {
+    *rc = 0;
+    if (s && m == m_ && n == n_ && std::memcmp(&cfg, &c, sizeof(c)) == 0) return s.get();
+    s.reset();  // free the old buffers before allocating new ones
+    std::unique_ptr<Session<T>> fresh(new Session<T>());
+    *rc = fresh->create(m_, n_, c);
+    if (*rc) return nullptr;
+    s = std::move(fresh);
+    m = m_;
+    n = n_;
+    cfg = c;
+    return s.get();
+  }
+};
+template <class T>
+static SolveCache<T>& solve_cache() {
+  static thread_local SolveCache<T> c;
+  return c;
+}
+
 template <class T>
 int solve_t(const T* C, int64_t m, int64_t n, const T* p, const T* q,
             const drotb_config* cfgp, const T* x0, T* plan, T* mu, T* nu,
@@ -1370,8 +1403,11 @@ int solve_t(const T* C, int64_t m, int64_t n, const T* p, const T* q,
   drotb::clear_error();
   const drotb_config cfg = effective(cfgp);
   try {
-    std::unique_ptr<Session<T>> s(new Session<T>());
-    RC_TRY(s->create(m, n, cfg));
+    if (m <= 0 || n <= 0)
+      return drotb::set_error(DROTB_ERRC_EMPTY_DIMENSION, "cost matrix has an empty dimension");
+    int crc = 0;
+    Session<T>* s = solve_cache<T>().get(m, n, cfg, &crc);
+    if (!s) return crc;
     RC_TRY(s->set_problem(C, p, q, false, true));
     RC_TRY(s->init(x0));
     RC_TRY(s->run());
@@ -1862,6 +1898,11 @@ int drotb_residual_report_f64(const double* C, int64_t m, int64_t n, const doubl
                               const double* nu, int32_t exact, drotb_report* out) {
   drotb::clear_error();
   return residual_report_t<double>(C, m, n, p, q, plan, mu, nu, exact, out);
+}
+
+void drotb_release_cache(void) {
+  solve_cache<float>().s.reset();
+  solve_cache<double>().s.reset();
 }
 
 int32_t drotb_session_persistent_grid(drotb_session* s) {

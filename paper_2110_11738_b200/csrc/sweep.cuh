@@ -512,6 +512,22 @@ __device__ void gate_logic(Book<T>* bk, const TailArgs<T>& t, double dual_value,
   if (t.use_cond) cudaGraphSetConditional(t.cond, fire ? 1u : 0u);
 }
 
+// report_elem with mu_i = double(phi_i) / rho precomputed once per row
+// (the same division, so the slack is bitwise identical)
+template <class T>
+__device__ __forceinline__ void report_elem_mu(T xv, T cv, double mu_i, double nu_j, T rho,
+                                               bool folded, double& obj, double& dsq) {
+  const double c = static_cast<double>(cv);
+  double x = static_cast<double>(xv);
+  if (folded) {
+    x += static_cast<double>(rho) * c;
+    if (x < 0) x = 0;
+  }
+  obj += c * x;
+  const double slack = mu_i + nu_j - c;
+  if (slack > 0) dsq += slack * slack;
+}
+
 template <class T>
 __device__ __forceinline__ void report_elem(T xv, T cv, T phi_i, double nu_j,
                                             double drho, T rho, bool folded,
