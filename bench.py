@@ -114,14 +114,17 @@ def measured_hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(m, n, dtype):
-    """DRAM bytes per sweep launch from the committed ncu capture, if any."""
+def ncu_traffic(m, n, dtype, iters=None):
+    """DRAM bytes per launch from the committed ncu capture (profiles/), if
+    any: per K1 sweep launch, or -- persistent kernel, `iters` iterations per
+    launch -- the captured bytes per iteration times `iters`."""
     path = os.path.join(ROOT, "profiles", "ncu_pass_summary.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        key = f"{m}x{n}_{dtype}"
-        return d[key]["dram_bytes_per_launch_avg"]
+        if iters:
+            return d[f"solve_{m}x{n}_{dtype}"]["dram_bytes_per_iteration"] * iters
+        return d[f"pass_{m}x{n}_{dtype}"]["dram_bytes_per_launch_avg"]
     except Exception:
         return None
 
@@ -268,7 +271,7 @@ def run_b200(args, rank, world, local_rank):
                             "share_of_step": r["pass_ms"] / r["total_ms"],
                             "how": "%globaltimer in CTA 0 from iteration start to the barrier "
                                    "after the sweep (includes barrier skew)"},
-            "traffic": ncu_traffic(m, n, "f32"),
+            "traffic": ncu_traffic(m, n, "f32", args.steps),
         }
     else:
         achieved = bytes_avg / (sweep_ms_avg / 1e3) / 1e9

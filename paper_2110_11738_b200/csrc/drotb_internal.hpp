@@ -153,6 +153,7 @@ struct PersistArgs {
   int64_t rows_cta;         // rows per CTA row block (4 warps x 32 lanes x R)
   int64_t n_rb;             // row blocks
   int64_t max_seg;          // u-partial slots per CTA
+  int64_t ileave;           // > 0: interleaved schedule with ileave CTAs per row block
   T* ustrip;                // [grid * max_seg][rows_cta]
   const int32_t* seg_ptr;   // [n_rb + 1] CSR of the u slots per row block
   const int32_t* seg_slot;  // slots in column order

@@ -167,7 +167,7 @@ struct Session {
   // persistent solver kernel (fast order, one GPU; persistent.cu)
   bool persist = false;
   int pgrid = 0;
-  int64_t prows = 0, pn_rb = 0, pmax_seg = 0;
+  int64_t prows = 0, pn_rb = 0, pmax_seg = 0, pileave = 0;
   T *pustrip = nullptr, *pvstrip = nullptr, *pcpart = nullptr;
   double* pdpart = nullptr;
   unsigned* pbar = nullptr;
@@ -182,7 +182,7 @@ struct Session {
   double rho_d = 0;
   int64_t bs = 64, tc = 256, grid_cols = 0, grid_rows64 = 0, n_partials = 0;
   int64_t tile_grid_rows = 0, n_tiles = 0, tail_blocks = 0, report_blocks = 0;
-  int64_t trace_cap = 0;
+  int64_t trace_cap = 0, trace_alloc = 0;
   bool exact = false, have_problem = false, initialized = false;
   bool want_dual = true, want_dx = true, gate = true;
   int64_t h_iter = 0;
@@ -266,7 +266,21 @@ struct Session {
     const int64_t W = pn_rb * n, G = pgrid;
     std::vector<std::vector<int32_t>> per(static_cast<size_t>(pn_rb));
     pmax_seg = 1;
-    for (int pass = 0; pass < 2; ++pass) {
+    // interleaved schedule (co-running CTAs stream contiguous column bands)
+    // when whole row blocks fill >= 90 % of the grid, else flat slices
+    const int64_t k = G / pn_rb;
+    pileave = 0;
+    if (k >= 1 && pn_rb * k * 10 >= G * 9) pileave = k;
+    if (const char* e = std::getenv("DROTB_PSK_SCHED")) {
+      if (e[0] == 'f') pileave = 0;
+      if (e[0] == 'i' && k >= 1) pileave = k;
+    }
+    if (pileave > 0) {
+      for (int64_t r = 0; r < pn_rb; ++r)
+        for (int64_t cg = 0; cg < pileave; ++cg)
+          per[static_cast<size_t>(r)].push_back(static_cast<int32_t>(r + cg * pn_rb));
+    }
+    for (int pass = 0; pass < (pileave > 0 ? 0 : 2); ++pass) {
       for (auto& v : per) v.clear();
       for (int64_t bi = 0; bi < G; ++bi) {
         int64_t f0 = bi * W / G;
@@ -328,6 +342,7 @@ struct Session {
     g.rows_cta = prows;
     g.n_rb = pn_rb;
     g.max_seg = pmax_seg;
+    g.ileave = pileave;
     g.ustrip = pustrip;
     g.seg_ptr = pseg_ptr;
     g.seg_slot = pseg_slot;
@@ -640,9 +655,17 @@ struct Session {
     // bookkeeping
     if (cfg.record_trace) {
       const int64_t te = std::max<int64_t>(1, cfg.trace_every);
-      trace_cap = std::min<int64_t>(std::max<int64_t>(cfg.max_iters, 0) / te + 1, int64_t(1) << 23);
-      if (trace) cudaFree(trace);
-      RC_TRY(dev_alloc(&trace, static_cast<size_t>(trace_cap)));
+      const int64_t cap = std::min<int64_t>(std::max<int64_t>(cfg.max_iters, 0) / te + 1,
+                                            int64_t(1) << 23);
+      if (!trace || cap != trace_alloc) {
+        // captured graphs hold the trace pointer: drop them with the buffer
+        drop_graphs();
+        if (trace) cudaFree(trace);
+        trace = nullptr;
+        RC_TRY(dev_alloc(&trace, static_cast<size_t>(cap)));
+        trace_alloc = cap;
+      }
+      trace_cap = cap;
     } else {
       trace_cap = 0;
     }

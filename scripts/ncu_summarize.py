@@ -128,6 +128,9 @@ def main():
     ap.add_argument("--m", type=int, default=10000)
     ap.add_argument("--n", type=int, default=10000)
     ap.add_argument("--dtype", default="f32")
+    ap.add_argument("--iters-per-launch", type=int, default=0,
+                    help="persistent solve_kernel capture: iterations per launch "
+                         "(alternating fold / skip sweeps)")
     args = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     go = os.path.join(ROOT, "gpurun_out")
@@ -144,6 +147,10 @@ def main():
         if md:
             # algorithmic bytes: fold/plain sweeps 3*s*m*n, skip sweeps 2*s*m*n
             for e in ls:
+                if args.iters_per_launch:
+                    k = args.iters_per_launch
+                    e["algorithmic_bytes"] = (3 * ((k + 1) // 2) + 2 * (k // 2)) * s * args.m * args.n
+                    continue
                 skip = re.search(r"<(float|double), 3,", e["kernel"]) is not None
                 e["algorithmic_bytes"] = (2 if skip else 3) * s * args.m * args.n
             md2, _ = full_capture(rpath, args.tag, None)
@@ -163,9 +170,13 @@ def main():
                     summ = json.load(f)
             dram = [e["dram_bytes"] for e in ls if "dram_bytes" in e]
             if dram:
-                summ[f"{args.m}x{args.n}_{args.dtype}"] = {
+                key = ("solve_" if args.iters_per_launch else "pass_") + f"{args.m}x{args.n}_{args.dtype}"
+                summ[key] = {
                     "tag": args.tag,
                     "dram_bytes_per_launch_avg": sum(dram) / len(dram),
+                    "iters_per_launch": args.iters_per_launch or None,
+                    "dram_bytes_per_iteration": (sum(dram) / len(dram) / args.iters_per_launch)
+                    if args.iters_per_launch else None,
                     "launches": [{"kernel": e["kernel"], "dram_bytes": e.get("dram_bytes"),
                                   "algorithmic_bytes": e["algorithmic_bytes"]} for e in ls],
                 }
