@@ -134,6 +134,9 @@ struct TailArgs {
   T* pack;       // [v (n) | sum r, sum r^2, cost, prev, dual, dx]  (sum)
   T* pmax;       // [max|t| or +inf if non-finite]                   (max)
   double* dpack; // [dual_i, dphi^2, dphi, cross_i | obj, dual^2]    (sum)
+  // cooperative tail (tail.cu): the arrays the confirm report streams
+  const T* report_x;
+  const T* report_c;
 };
 
 // Persistent solver kernel (persistent.cu): one cooperative launch runs up to
@@ -177,6 +180,14 @@ template <class T>
 int rows_per_cta();
 template <class T>
 cudaError_t launch_persistent(const PersistArgs<T>& g, int grid, bool dx, cudaStream_t st);
+
+// Cooperative per-iteration tail (tail.cu): merge + recursions + update +
+// gate (+ confirm report) in one launch after K1 (fast order, one GPU).
+template <class T>
+int tail_grid(int device);
+template <class T>
+cudaError_t launch_tail(const TailArgs<T>& t, T* cpart, double* dpart, unsigned* bar, int grid,
+                        cudaStream_t st);
 
 // ---- kernel launchers (kernels.cu) ---------------------------------------
 template <class T>

@@ -175,6 +175,12 @@ struct Session {
   unsigned long long* psweep_ns = nullptr;
   double* pmud = nullptr;
   bool h_stale = false;  // h_iter / h_folded lag the device after persistent launches
+  // cooperative tail kernel (fast order, one GPU; tail.cu)
+  bool coop = false, coop_graphs = false;
+  int tgrid = 0;
+  T* tcpart = nullptr;
+  double* tdpart = nullptr;
+  unsigned* tbar = nullptr;
   bool no_persist = false;
 
   std::vector<T> hp, hq;
@@ -198,7 +204,11 @@ struct Session {
     void* bufs[] = {X, C, Xout, phi, varphi, a, b, rb[0], rb[1], sb[0], sb[1],
                     p, q, u, v, ustrip, vstrip, tscr, partials, tiles, dscr,
                     terms, book, trace, vflags, pack, pmax, dpack, dint,
-                    pustrip, pvstrip, pcpart, pdpart, pbar, pseg_ptr, pseg_slot, psweep_ns, pmud};
+                    pustrip, pvstrip, pcpart, pdpart, pbar, pseg_ptr, pseg_slot, psweep_ns, pmud, tcpart, tdpart, tbar};
+    tcpart = nullptr;
+    tdpart = nullptr;
+    tbar = nullptr;
+    coop = false;
     pustrip = pvstrip = pcpart = nullptr;
     pdpart = nullptr;
     pbar = nullptr;
@@ -249,9 +259,48 @@ struct Session {
     if (!exact && !engine) tc = fast_tile_cols();
     RC_TRY(allocate());
     if (!exact && !engine && !no_persist) {
+      // default: K1 + the cooperative tail kernel; DROTB_PERSIST=1 selects the
+      // persistent solver kernel, DROTB_TAIL=legacy the three tail kernels
       const char* e = std::getenv("DROTB_PERSIST");
-      if (!(e && e[0] == '0')) RC_TRY(setup_persistent());
+      if (e && e[0] == '1') RC_TRY(setup_persistent());
+      const char* tl = std::getenv("DROTB_TAIL");
+      if (!persist && !(tl && tl[0] == 'l')) RC_TRY(setup_coop_tail());
     }
+    return 0;
+  }
+
+  int setup_coop_tail() {
+    tgrid = tail_grid<T>(device);
+    if (tgrid <= 0) return 0;
+    RC_TRY(dev_alloc(&tcpart, static_cast<size_t>(tgrid) * 16));
+    RC_TRY(dev_alloc(&tdpart, static_cast<size_t>(tgrid) * 16));
+    RC_TRY(dev_alloc(&tbar, 2));
+    CUDA_TRY(cudaMemsetAsync(tbar, 0, 2 * sizeof(unsigned), stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    coop = true;
+    // can a cooperative launch be captured into a graph here?  (probe on a
+    // private stream; the captured launch is never executed)
+    coop_graphs = false;
+    cudaStream_t ps = nullptr;
+    if (cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking) == cudaSuccess) {
+      cudaGraph_t gph = nullptr;
+      if (cudaStreamBeginCapture(ps, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+        TailArgs<T> ta = tail_args(0, kFold, true, true);
+        const cudaError_t le = launch_tail<T>(ta, tcpart, tdpart, tbar, tgrid, ps);
+        count_launch(-1);
+        const cudaError_t ce = cudaStreamEndCapture(ps, &gph);
+        if (le == cudaSuccess && ce == cudaSuccess && gph) {
+          cudaGraphExec_t ex = nullptr;
+          if (cudaGraphInstantiate(&ex, gph, 0) == cudaSuccess) {
+            coop_graphs = true;
+            cudaGraphExecDestroy(ex);
+          }
+        }
+        if (gph) cudaGraphDestroy(gph);
+      }
+      cudaStreamDestroy(ps);
+    }
+    (void)cudaGetLastError();  // a failed probe leaves no sticky error
     return 0;
   }
 
@@ -795,6 +844,8 @@ struct Session {
     t.pmax = pmax;
     t.dpack = dpack;
     if (sharded) t.v = pack;  // the merge writes the local v partial into the pack
+    t.report_x = X;
+    t.report_c = C;
     return t;
   }
 
@@ -831,6 +882,12 @@ struct Session {
       h_folded = folded_after;
       return 0;
     }
+    if (coop && !exact) {  // K1 + one cooperative tail kernel (tail.cu)
+      CUDA_TRY(launch_tail<T>(ta, tcpart, tdpart, tbar, tgrid, stream));
+      h_iter = k + 1;
+      h_folded = folded_after;
+      return 0;
+    }
     if (cond_out) {  // graph build: the report goes into an IF node body
       ta.cond = *cond_out;
       ta.use_cond = 1;
@@ -861,9 +918,10 @@ struct Session {
     std::vector<cudaGraphNode_t> deps;
     const cudaStreamCaptureMode cm = cudaStreamCaptureModeThreadLocal;
     int rc = 0;
+    const bool ifnode = gate && !coop;  // the cooperative tail runs its own report
     for (int64_t it = 0; it < n_iters && rc == 0; ++it) {
       cudaGraphConditionalHandle h = 0;
-      if (gate) CUDA_TRY(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+      if (ifnode) CUDA_TRY(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
       CUDA_TRY(cudaStreamBeginCaptureToGraph(stream, g, deps.empty() ? nullptr : deps.data(),
                                              nullptr, deps.size(), cm));
       if (timed && it == 0)
@@ -872,8 +930,8 @@ struct Session {
       unsigned long long hv = static_cast<unsigned long long>(h);
       rc = enqueue_iteration(timed ? tev[2 + 2 * it] : nullptr,
                              timed ? tev[3 + 2 * it] : nullptr, nullptr,
-                             gate ? &hv : nullptr, &ra);
-      if (timed && it + 1 == n_iters && !gate)
+                             ifnode ? &hv : nullptr, &ra);
+      if (timed && it + 1 == n_iters && !ifnode)
         CUDA_TRY(cudaEventRecordWithFlags(tev[1], stream, cudaEventRecordExternal));
       cudaStreamCaptureStatus cs;
       const cudaGraphNode_t* d = nullptr;
@@ -882,7 +940,7 @@ struct Session {
       deps.assign(d, d + nd);
       cudaGraph_t tmp;
       CUDA_TRY(cudaStreamEndCapture(stream, &tmp));
-      if (rc || !gate) continue;
+      if (rc || !ifnode) continue;
       cudaGraphNodeParams cp = {};
       cp.type = cudaGraphNodeTypeConditional;
       cp.conditional.handle = h;
@@ -948,7 +1006,8 @@ struct Session {
   }
 
   bool graph_ok(int64_t len) const {
-    return !sharded && cfg.use_graphs && len >= 2 && (len & 1) == 0 && (h_iter & 1) == 0 && !h_folded;
+    return !sharded && cfg.use_graphs && (!coop || coop_graphs) && len >= 2 && (len & 1) == 0 &&
+           (h_iter & 1) == 0 && !h_folded;
   }
 
   int enqueue(int64_t n_iters) {

@@ -1,0 +1,358 @@
+// tail.cu -- KT: the per-iteration tail of the solve loop (fast reduction
+// order, one GPU) as ONE cooperative kernel after the fused sweep K1.
+//
+//   A  merge      u_i = sum of the K1 row strips, v_j = sum of the 64-row
+//                 column strips (fused.hpp:312-321), r = u - p, s = v - q
+//                 (solver.hpp:269-272); per-CTA partials of sum r, |r|^2,
+//                 |s|^2 and of a fixed slice of the K1 CTA scalars
+//   -- reduce-barrier: the last CTA to arrive reduces the per-CTA partials in
+//      CTA order and runs the scalar recursions (solver.hpp:273-277,
+//      418-437) on the device Book, then releases the others --
+//   B  update     phi, varphi, a, b (solver.hpp:279-289) + dual-value and
+//                 fixed-point partials
+//   -- reduce-barrier: last CTA -> gate (solver.hpp:443-504) --
+//   C  report     only when the gate fired: the exact matched-pair report
+//                 of (X_{k+1}, phi/rho, varphi/rho) (solver.hpp:312-354)
+//   -- reduce-barrier: last CTA -> confirm decision (solver.hpp:508-519) --
+//
+// It replaces three kernels and a graph IF node of the per-launch tail
+// (merge_kernel, update_kernel, report_kernel) whose launch gaps and
+// single-block "last block" reductions cost ~32 us per iteration at 10k^2
+// (r1 measurement).  The reduce-barrier makes the grid-wide reduction part of
+// the barrier itself: no CTA re-reads all partials (a G^2 L2 hot spot) and no
+// second barrier is needed to broadcast the totals.  Deterministic: every
+// reduction runs in a fixed order independent of which CTA arrives last.
+#include <cstdint>
+
+#include "drotb_internal.hpp"
+#include "sweep.cuh"
+
+namespace drotb {
+
+namespace {
+
+constexpr int kTT = 256;            // threads per CTA
+constexpr int kTW = kTT / 32;       // warps per CTA = strip partitions in A
+constexpr int kTSlots = 16;         // per-CTA partial slots
+
+// Every CTA has published its partials; the last CTA to arrive runs fn()
+// (whole CTA) and then releases the others.  bar = {count, generation}.
+template <class F>
+__device__ __forceinline__ void reduce_barrier(unsigned* bar, F&& fn) {
+  __shared__ int s_last;
+  __shared__ unsigned s_gen;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    s_gen = *gen;
+    __threadfence();
+    s_last = atomicAdd(bar, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    fn();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bar[0] = 0u;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    }
+  } else if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    while (*gen == s_gen) __nanosleep(32);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Fixed-order sum over the G per-CTA slots [off, off+K): thread t takes
+// CTAs t, t+kTT, ...; then a fixed warp tree and the warps in order.
+// Result valid in thread 0.
+template <class U, int K>
+__device__ __forceinline__ void totals(const U* part, int nb, int off, U (&out)[K], U* sh) {
+  U acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = U(0);
+  for (int b = threadIdx.x; b < nb; b += kTT)
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] += __ldcg(part + b * kTSlots + off + k);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = warp_sum(acc[k]);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < K; ++k) sh[k * kTW + warp] = acc[k];
+  __syncthreads();
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      U s = U(0);
+#pragma unroll
+      for (int w = 0; w < kTW; ++w) s += sh[k * kTW + w];
+      out[k] = s;
+    }
+  __syncthreads();
+}
+
+template <class U, int K>
+__device__ __forceinline__ void store_partials(U (&v)[K], U* part, int off, U* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < K; ++k) sh[k * kTW + warp] = v[k];
+  __syncthreads();
+  if (threadIdx.x < K) {
+    U s = U(0);
+#pragma unroll
+    for (int w = 0; w < kTW; ++w) s += sh[threadIdx.x * kTW + w];
+    part[blockIdx.x * kTSlots + off + threadIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+template <class T>
+__global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart,
+                                                   double* dpart, unsigned* bar) {
+  using V = typename V16<T>::type;
+  constexpr int R = 16 / sizeof(T);
+  Book<T>* bk = t.book;
+  if (*reinterpret_cast<volatile int*>(&bk->stop)) return;
+  __shared__ T red[kTW][32];
+  __shared__ T shT[16 * kTW];
+  __shared__ double shD[16 * kTW];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x;
+  const int64_t m = t.m, n = t.n;
+
+  // ---- A: merge -----------------------------------------------------------
+  {
+    T pr[3] = {T(0), T(0), T(0)};
+    const int64_t ngr = (m + 31) / 32, ngc = (n + 31) / 32;
+    for (int64_t grp = blockIdx.x; grp < ngr + ngc; grp += G) {
+      T acc = T(0);
+      if (grp < ngr) {
+        const int64_t idx = grp * 32 + lane;
+        if (idx < m) {
+          int64_t g = warp;
+          for (; g + 3 * kTW < t.grid_cols; g += 4 * kTW) {
+            T v4[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) v4[q] = t.ustrip[(g + q * kTW) * t.ld + idx];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc += v4[q];
+          }
+          for (; g < t.grid_cols; g += kTW) acc += t.ustrip[g * t.ld + idx];
+        }
+      } else {
+        const int64_t j = (grp - ngr) * 32 + lane;
+        if (j < n) {
+          int64_t g = warp;
+          for (; g + 3 * kTW < t.grid_rows64; g += 4 * kTW) {
+            T v4[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) v4[q] = t.vstrip[(g + q * kTW) * n + j];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc += v4[q];
+          }
+          for (; g < t.grid_rows64; g += kTW) acc += t.vstrip[g * n + j];
+        }
+      }
+      red[warp][lane] = acc;
+      __syncthreads();
+      if (warp == 0) {
+        T tot = T(0);
+#pragma unroll
+        for (int w = 0; w < kTW; ++w) tot += red[w][lane];
+        if (grp < ngr) {
+          const int64_t idx = grp * 32 + lane;
+          if (idx < m) {
+            const T r = tot - t.p[idx];
+            t.r_new[idx] = r;
+            pr[0] += r;
+            pr[1] += r * r;
+          }
+        } else {
+          const int64_t j = (grp - ngr) * 32 + lane;
+          if (j < n) {
+            const T s = tot - t.q[j];
+            t.s_new[j] = s;
+            pr[2] += s * s;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // this CTA's fixed slice of the K1 CTA scalars
+    const int64_t np = t.n_pass_partials;
+    const int64_t k0 = static_cast<int64_t>(blockIdx.x) * np / G;
+    const int64_t k1 = static_cast<int64_t>(blockIdx.x + 1) * np / G;
+    T ps[4] = {T(0), T(0), T(0), T(0)};
+    T mx = T(0), bad = T(0);
+    for (int64_t k = k0 + tid; k < k1; k += kTT) {
+      const PassPartial<T> sc = t.pass_partials[k];
+      ps[0] += sc.cost;
+      ps[1] += sc.prev;
+      ps[2] += sc.dual;
+      ps[3] += sc.dx;
+      mx = fmax(mx, sc.max_abs);
+      bad += sc.bad ? T(1) : T(0);
+    }
+    // max through a warp/CTA max (fixed order), the rest through the sum tree
+    mx = warp_max(mx);
+    if (lane == 0) shT[warp] = mx;
+    __syncthreads();
+    T cmx = T(0);
+#pragma unroll
+    for (int w = 0; w < kTW; ++w) cmx = fmax(cmx, shT[w]);
+    __syncthreads();
+    T v8[8] = {ps[0], ps[1], ps[2], ps[3], bad, pr[0], pr[1], pr[2]};
+    store_partials<T, 8>(v8, cpart, 0, shT);
+    if (tid == 0) cpart[blockIdx.x * kTSlots + 8] = cmx;
+  }
+  reduce_barrier(bar, [&] {
+    T s8[8];
+    totals<T, 8>(cpart, G, 0, s8, shT);
+    T m1 = T(0);
+    for (int b = tid; b < G; b += kTT) m1 = fmax(m1, __ldcg(cpart + b * kTSlots + 8));
+    m1 = warp_max(m1);
+    if (lane == 0) shT[warp] = m1;
+    __syncthreads();
+    if (tid == 0) {
+      T mxt = T(0);
+#pragma unroll
+      for (int w = 0; w < kTW; ++w) mxt = fmax(mxt, shT[w]);
+      // {cost, prev, dual, dx, max|t|, sum r, |r|^2, |s|^2} (merge_kernel order)
+      const T tot[8] = {s8[0], s8[1], s8[2], s8[3], mxt, s8[5], s8[6], s8[7]};
+      merge_scalars<T>(bk, t, tot, s8[4] > T(0) ? 1 : 0);
+    }
+  });
+  if (*reinterpret_cast<volatile int*>(&bk->stop)) return;  // non-finite pass
+
+  // ---- B: phi / varphi / a / b + dual-value and fixed-point partials --------
+  {
+    const T coef = *reinterpret_cast<volatile T*>(&bk->coef);
+    const T inv_n = T(1) / static_cast<T>(t.n_global);
+    const T inv_m = T(1) / static_cast<T>(t.m_global);
+    const double drho = static_cast<double>(t.rho);
+    const bool fp = bk->record_trace != 0;
+    double part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const int64_t TT = static_cast<int64_t>(G) * kTT;
+    for (int64_t idx = static_cast<int64_t>(blockIdx.x) * kTT + tid; idx < m + n; idx += TT) {
+      if (idx < m) {
+        const T r = __ldcg(t.r_new + idx);
+        const T ph_old = t.phi[idx];
+        const T ai = t.a[idx];
+        const T ph = (ai - T(2) * r + coef) * inv_n;  // solver.hpp:280-282
+        t.phi[idx] = ph;
+        t.a[idx] = ai - r;  // solver.hpp:287
+        part[0] += static_cast<double>(t.p[idx]) * static_cast<double>(ph) / drho;
+        if (fp) {
+          const double d = static_cast<double>(ph) - static_cast<double>(ph_old);
+          part[1] += d * d;
+          part[2] += d;
+          part[3] += d * (static_cast<double>(r) - static_cast<double>(t.r_old[idx]));
+        }
+      } else {
+        const int64_t j = idx - m;
+        const T s = __ldcg(t.s_new + j);
+        const T vp_old = t.varphi[j];
+        const T bj = t.b[j];
+        const T vp = (bj - T(2) * s + coef) * inv_m;  // solver.hpp:283-285
+        t.varphi[j] = vp;
+        t.b[j] = bj - s;  // solver.hpp:288
+        part[4] += static_cast<double>(t.q[j]) * static_cast<double>(vp) / drho;
+        if (fp) {
+          const double d = static_cast<double>(vp) - static_cast<double>(vp_old);
+          part[5] += d * d;
+          part[6] += d;
+          part[7] += d * (static_cast<double>(s) - static_cast<double>(t.s_old[j]));
+        }
+      }
+    }
+    store_partials<double, 8>(part, dpart, 0, shD);
+  }
+  reduce_barrier(bar, [&] {
+    double d8[8];
+    totals<double, 8>(dpart, G, 0, d8, shD);
+    if (tid == 0)
+      gate_logic<T>(bk, t, d8[0] + d8[4], d8[1], d8[2], d8[5], d8[6], d8[3] + d8[7]);
+  });
+  if (!*reinterpret_cast<volatile int*>(&bk->confirm) ||
+      *reinterpret_cast<volatile int*>(&bk->stop) == 1)
+    return;
+
+  // ---- C: exact confirm report (only when the gate fired) ------------------
+  {
+    const bool folded = *reinterpret_cast<volatile int*>(&bk->folded) != 0;
+    const double drho = static_cast<double>(t.rho);
+    const int64_t ngx = (m + int64_t(kTT) * R - 1) / (int64_t(kTT) * R);
+    const int64_t ncs = imin64(n, (2 * static_cast<int64_t>(G) + ngx - 1) / ngx);
+    double part[2] = {0, 0};
+    for (int64_t unit = blockIdx.x; unit < ngx * ncs; unit += G) {
+      const int64_t rx = unit % ngx, cs = unit / ngx;
+      const int64_t row0 = (rx * kTT + tid) * R;
+      if (row0 >= m) continue;
+      const int nvalid = static_cast<int>(imin64(R, m - row0));
+      double mu[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+        mu[k] = k < nvalid ? static_cast<double>(__ldcg(t.phi + row0 + k)) / drho : 0.0;
+      for (int64_t j = cs; j < n; j += ncs) {
+        const double nu_j = static_cast<double>(__ldcg(t.varphi + j)) / drho;
+        T xv[R], cv[R];
+        unpack(__ldcs(reinterpret_cast<const V*>(t.report_x + j * t.ld + row0)), xv);
+        unpack(__ldcs(reinterpret_cast<const V*>(t.report_c + j * t.ld + row0)), cv);
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+          if (k < nvalid)
+            report_elem_mu<T>(xv[k], cv[k], mu[k], nu_j, t.rho, folded, part[0], part[1]);
+      }
+    }
+    store_partials<double, 2>(part, dpart, 8, shD);
+  }
+  reduce_barrier(bar, [&] {
+    double d2[2];
+    totals<double, 2>(dpart, G, 8, d2, shD);
+    if (tid == 0) report_decide<T>(bk, d2[0], d2[1], 0);
+  });
+}
+
+}  // namespace
+
+template <class T>
+int tail_grid(int device) {
+  int sms = 0, per = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tail_kernel<T>, kTT, 0);
+  return sms * (per < 2 ? per : 2);
+}
+
+template <class T>
+cudaError_t launch_tail(const TailArgs<T>& t, T* cpart, double* dpart, unsigned* bar, int grid,
+                        cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kTT);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  count_launch();
+  return cudaLaunchKernelEx(&cfg, tail_kernel<T>, t, cpart, dpart, bar);
+}
+
+template int tail_grid<float>(int);
+template int tail_grid<double>(int);
+template cudaError_t launch_tail<float>(const TailArgs<float>&, float*, double*, unsigned*, int,
+                                        cudaStream_t);
+template cudaError_t launch_tail<double>(const TailArgs<double>&, double*, double*, unsigned*,
+                                         int, cudaStream_t);
+
+}  // namespace drotb

@@ -1,0 +1,90 @@
+"""The cooperative per-iteration tail (csrc/tail.cu, the default fast-order
+path on one GPU) against the per-launch tail kernels (DROTB_TAIL=legacy) and
+against itself:
+
+* captured CUDA graphs and eager launches run the same kernels: bitwise
+  identical iterates, duals and reports;
+* solves to tolerance agree with the legacy tail and the reference to the
+  fast-order tolerances; the confirm report inside the tail decides
+  convergence exactly like the graph IF-node path (same status);
+* a non-finite sweep stops the loop with numerical_failure.
+"""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+class _env:
+    def __init__(self, **kv):
+        self.kv = kv
+
+    def __enter__(self):
+        self.old = {k: os.environ.get(k) for k in self.kv}
+        os.environ.update(self.kv)
+
+    def __exit__(self, *a):
+        for k, v in self.old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def _run(drot, m, n, dt, iters=None, legacy=False, **kw):
+    with _env(DROTB_TAIL="legacy" if legacy else "coop", DROTB_PERSIST="0"):
+        s = drot.Session(m, n, dt, drot.DrotConfig(**kw))
+    s.gen_gaussian(5.0, 4, "dyadic")
+    s.init()
+    if iters is None:
+        s.run()
+    else:
+        s.enqueue(iters)
+        s.synchronize()
+    st = s.status()
+    plan, mu, nu = s.plan()
+    s.close()
+    return st, plan, mu, nu
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_graphs_equal_eager(drot, dt):
+    a = _run(drot, 700, 500, dt, iters=40, tol_primal=-1.0, max_iters=10 ** 9)
+    b = _run(drot, 700, 500, dt, iters=40, tol_primal=-1.0, max_iters=10 ** 9, use_graphs=False)
+    assert a[0][1] == b[0][1] == 40
+    for x, y in zip(a[1:], b[1:]):
+        np.testing.assert_array_equal(x, y)
+    assert a[0][2].objective == b[0][2].objective
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_converges_like_legacy_tail(drot, dt):
+    (s1, i1, r1), *_ = _run(drot, 500, 400, dt, max_iters=80000)
+    (s2, i2, r2), *_ = _run(drot, 500, 400, dt, max_iters=80000, legacy=True)
+    assert s1 == s2 == drot.SolveStatus.converged
+    assert abs(i1 - i2) <= max(5, int(0.005 * i2))
+    rel = 1e-5 if dt == np.float64 else 1e-3
+    assert abs(r1.objective - r2.objective) <= rel * abs(r2.objective)
+    for v in (r1.r_primal, r1.r_dual, r1.gap):
+        assert v <= 1e-4
+
+
+def test_max_iters_status_and_report(drot):
+    (st, it, rep), *_ = _run(drot, 300, 300, np.float64, max_iters=777)
+    assert st == drot.SolveStatus.max_iters and it == 777
+    (st2, it2, rep2), *_ = _run(drot, 300, 300, np.float64, max_iters=777, legacy=True)
+    assert it2 == 777
+    assert abs(rep.objective - rep2.objective) <= 1e-9 * abs(rep2.objective)
+
+
+def test_numerical_failure(drot):
+    m, n = 64, 48
+    C = np.full((m, n), 1e300)
+    prob = drot.TransportProblem(np.asfortranarray(C), np.full(m, 1.0 / m), np.full(n, 1.0 / n))
+    with _env(DROTB_TAIL="coop", DROTB_PERSIST="0"):
+        drot.release_device_cache()
+        r = drot.solve(prob, drot.DrotConfig(rho_override=1e10))
+        drot.release_device_cache()
+    assert r.status == drot.SolveStatus.numerical_failure
