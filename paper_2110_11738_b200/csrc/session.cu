@@ -870,6 +870,12 @@ struct Session {
     launch_pass<T>(pa, mode, want_dual, want_dx, stream);
     if (pass_end) CUDA_TRY(cudaEventRecordWithFlags(pass_end, stream, evf));
     TailArgs<T> ta = tail_args(k, mode, folded_after, true);
+    if (coop && !exact && !sharded) {  // K1 + one cooperative tail kernel (tail.cu)
+      CUDA_TRY(launch_tail<T>(ta, tcpart, tdpart, tbar, tgrid, stream));
+      h_iter = k + 1;
+      h_folded = folded_after;
+      return 0;
+    }
     launch_merge<T>(ta, exact, stream);
     if (sharded) {  // one exchange per phase; gate pauses for confirm
       RC_TRY(allreduce(pack, static_cast<size_t>(n + 6), ncclSum));
@@ -878,12 +884,6 @@ struct Session {
       launch_update<T>(ta, false, stream);
       RC_TRY(allreduce(dpack, 4, ncclSum));
       launch_gate<T>(ta, stream);
-      h_iter = k + 1;
-      h_folded = folded_after;
-      return 0;
-    }
-    if (coop && !exact) {  // K1 + one cooperative tail kernel (tail.cu)
-      CUDA_TRY(launch_tail<T>(ta, tcpart, tdpart, tbar, tgrid, stream));
       h_iter = k + 1;
       h_folded = folded_after;
       return 0;
