@@ -483,6 +483,10 @@ struct Session {
   // ~6 waves of 4 CTAs on each of the 148 SMs (wave-quantization and
   // latency), in multiples of the 16-column staging chunk, at most 256.
   int64_t fast_tile_cols() const {
+    if (const char* e = std::getenv("DROTB_TC")) {  // tuning aid
+      const int64_t v = std::atoll(e);
+      if (v >= kChunkCols) return round_up(v, kChunkCols);
+    }
     constexpr int R = 16 / sizeof(T);
     const int64_t rows_cta = int64_t(kWarpsPerCta) * 32 * R;
     const int64_t row_ctas = (m + rows_cta - 1) / rows_cta;

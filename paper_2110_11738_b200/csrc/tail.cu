@@ -23,6 +23,7 @@
 // second barrier is needed to broadcast the totals.  Deterministic: every
 // reduction runs in a fixed order independent of which CTA arrives last.
 #include <cstdint>
+#include <cstdlib>
 
 #include "drotb_internal.hpp"
 #include "sweep.cuh"
@@ -138,12 +139,12 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
         const int64_t idx = grp * 32 + lane;
         if (idx < m) {
           int64_t g = warp;
-          for (; g + 3 * kTW < t.grid_cols; g += 4 * kTW) {
-            T v4[4];
+          for (; g + 7 * kTW < t.grid_cols; g += 8 * kTW) {
+            T v8[8];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) v4[q] = t.ustrip[(g + q * kTW) * t.ld + idx];
+            for (int q = 0; q < 8; ++q) v8[q] = t.ustrip[(g + q * kTW) * t.ld + idx];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) acc += v4[q];
+            for (int q = 0; q < 8; ++q) acc += v8[q];
           }
           for (; g < t.grid_cols; g += kTW) acc += t.ustrip[g * t.ld + idx];
         }
@@ -151,12 +152,12 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
         const int64_t j = (grp - ngr) * 32 + lane;
         if (j < n) {
           int64_t g = warp;
-          for (; g + 3 * kTW < t.grid_rows64; g += 4 * kTW) {
-            T v4[4];
+          for (; g + 7 * kTW < t.grid_rows64; g += 8 * kTW) {
+            T v8[8];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) v4[q] = t.vstrip[(g + q * kTW) * n + j];
+            for (int q = 0; q < 8; ++q) v8[q] = t.vstrip[(g + q * kTW) * n + j];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) acc += v4[q];
+            for (int q = 0; q < 8; ++q) acc += v8[q];
           }
           for (; g < t.grid_rows64; g += kTW) acc += t.vstrip[g * n + j];
         }
@@ -328,7 +329,10 @@ int tail_grid(int device) {
   int sms = 0, per = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tail_kernel<T>, kTT, 0);
-  return sms * (per < 2 ? per : 2);
+  int want = 2;
+  if (const char* e = std::getenv("DROTB_TAIL_CTAS")) want = std::atoi(e);  // tuning aid
+  if (want < 1) want = 1;
+  return sms * (per < want ? per : want);
 }
 
 template <class T>
