@@ -310,6 +310,12 @@ int drotb_session_support(drotb_session* s, double rel_tau, double abs_tau, int6
 /* CTAs of the persistent solver kernel this session runs its iterations
  * with (fast order, one GPU; 0 = per-launch kernels + CUDA graphs). */
 int32_t drotb_session_persistent_grid(drotb_session* s);
+/* Profiling aid (sessions created with DROTB_TAIL_STAMPS=1): copy and reset
+ * 8 %globaltimer stamps (ns) of the cooperative tail: [0] first CTA entry
+ * (min), [1] last arrival at the merge barrier, [2] merge totals done,
+ * [3] last CTA past it, [4] last arrival at the update barrier, [5] gate
+ * done, [6] last CTA past it (max over the launches since the last reset). */
+int drotb_session_tail_stamps(drotb_session* s, uint64_t* out8);
 /* Copy the session's (local) cost matrix to host, m x n column-major. */
 int drotb_session_get_cost(drotb_session* s, void* out);
 /* init_state (x0 host pointer or NULL); resets the solve bookkeeping. */

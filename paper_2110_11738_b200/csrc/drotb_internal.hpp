@@ -137,6 +137,7 @@ struct TailArgs {
   // cooperative tail (tail.cu): the arrays the confirm report streams
   const T* report_x;
   const T* report_c;
+  unsigned long long* stamps;  // profiling aid: tail phase timestamps (or null)
 };
 
 // Persistent solver kernel (persistent.cu): one cooperative launch runs up to

@@ -181,6 +181,7 @@ struct Session {
   T* tcpart = nullptr;
   double* tdpart = nullptr;
   unsigned* tbar = nullptr;
+  unsigned long long* tstamps = nullptr;  // DROTB_TAIL_STAMPS profiling aid
   bool no_persist = false;
 
   std::vector<T> hp, hq;
@@ -204,7 +205,8 @@ struct Session {
     void* bufs[] = {X, C, Xout, phi, varphi, a, b, rb[0], rb[1], sb[0], sb[1],
                     p, q, u, v, ustrip, vstrip, tscr, partials, tiles, dscr,
                     terms, book, trace, vflags, pack, pmax, dpack, dint,
-                    pustrip, pvstrip, pcpart, pdpart, pbar, pseg_ptr, pseg_slot, psweep_ns, pmud, tcpart, tdpart, tbar};
+                    pustrip, pvstrip, pcpart, pdpart, pbar, pseg_ptr, pseg_slot, psweep_ns, pmud, tcpart, tdpart, tbar, tstamps};
+    tstamps = nullptr;
     tcpart = nullptr;
     tdpart = nullptr;
     tbar = nullptr;
@@ -276,6 +278,12 @@ struct Session {
     RC_TRY(dev_alloc(&tdpart, static_cast<size_t>(tgrid) * 16));
     RC_TRY(dev_alloc(&tbar, 2));
     CUDA_TRY(cudaMemsetAsync(tbar, 0, 2 * sizeof(unsigned), stream));
+    if (const char* e = std::getenv("DROTB_TAIL_STAMPS"))
+      if (e[0] == '1') {
+        RC_TRY(dev_alloc(&tstamps, 8));
+        const unsigned long long init[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
+        CUDA_TRY(cudaMemcpy(tstamps, init, sizeof(init), cudaMemcpyHostToDevice));
+      }
     CUDA_TRY(cudaStreamSynchronize(stream));
     coop = true;
     // can a cooperative launch be captured into a graph here?  (probe on a
@@ -850,6 +858,7 @@ struct Session {
     if (sharded) t.v = pack;  // the merge writes the local v partial into the pack
     t.report_x = X;
     t.report_c = C;
+    t.stamps = tstamps;
     return t;
   }
 
@@ -1989,6 +1998,20 @@ int drotb_residual_report_f64(const double* C, int64_t m, int64_t n, const doubl
 void drotb_release_cache(void) {
   solve_cache<float>().s.reset();
   solve_cache<double>().s.reset();
+}
+
+// Profiling aid: copy (and reset) the 8 tail-phase timestamps (ns).
+int drotb_session_tail_stamps(drotb_session* s, uint64_t* out8) {
+  auto go = [&](auto* ss) -> int {
+    if (!ss->tstamps) return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "DROTB_TAIL_STAMPS not set");
+    CUDA_TRY(cudaStreamSynchronize(ss->stream));
+    CUDA_TRY(cudaMemcpy(out8, ss->tstamps, 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    uint64_t init[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
+    CUDA_TRY(cudaMemcpy(ss->tstamps, init, sizeof(init), cudaMemcpyHostToDevice));
+    return 0;
+  };
+  if (s->precision == 0) return go(drotb::as_session<float>(s->impl));
+  return go(drotb::as_session<double>(s->impl));
 }
 
 int32_t drotb_session_persistent_grid(drotb_session* s) {

@@ -36,6 +36,17 @@ constexpr int kTT = 256;            // threads per CTA
 constexpr int kTW = kTT / 32;       // warps per CTA = strip partitions in A
 constexpr int kTSlots = 16;         // per-CTA partial slots
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// profiling aid (DROTB_TAIL_STAMPS): per-phase min / max timestamps
+#define TAIL_STAMP(slot, op)                                            \
+  do {                                                                  \
+    if (t.stamps && threadIdx.x == 0) op(t.stamps + (slot), gtimer());  \
+  } while (0)
+
 // Every CTA has published its partials; the last CTA to arrive runs fn()
 // (whole CTA) and then releases the others.  bar = {count, generation}.
 template <class F>
@@ -121,6 +132,7 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
   using V = typename V16<T>::type;
   constexpr int R = 16 / sizeof(T);
   Book<T>* bk = t.book;
+  TAIL_STAMP(0, atomicMin);
   if (*reinterpret_cast<volatile int*>(&bk->stop)) return;
   __shared__ T red[kTW][32];
   __shared__ T shT[16 * kTW];
@@ -214,6 +226,7 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
     store_partials<T, 8>(v8, cpart, 0, shT);
     if (tid == 0) cpart[blockIdx.x * kTSlots + 8] = cmx;
   }
+  TAIL_STAMP(1, atomicMax);
   reduce_barrier(bar, [&] {
     T s8[8];
     totals<T, 8>(cpart, G, 0, s8, shT);
@@ -230,7 +243,9 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
       const T tot[8] = {s8[0], s8[1], s8[2], s8[3], mxt, s8[5], s8[6], s8[7]};
       merge_scalars<T>(bk, t, tot, s8[4] > T(0) ? 1 : 0);
     }
+    TAIL_STAMP(2, atomicMax);
   });
+  TAIL_STAMP(3, atomicMax);
   if (*reinterpret_cast<volatile int*>(&bk->stop)) return;  // non-finite pass
 
   // ---- B: phi / varphi / a / b + dual-value and fixed-point partials --------
@@ -276,12 +291,15 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
     }
     store_partials<double, 8>(part, dpart, 0, shD);
   }
+  TAIL_STAMP(4, atomicMax);
   reduce_barrier(bar, [&] {
     double d8[8];
     totals<double, 8>(dpart, G, 0, d8, shD);
     if (tid == 0)
       gate_logic<T>(bk, t, d8[0] + d8[4], d8[1], d8[2], d8[5], d8[6], d8[3] + d8[7]);
+    TAIL_STAMP(5, atomicMax);
   });
+  TAIL_STAMP(6, atomicMax);
   if (!*reinterpret_cast<volatile int*>(&bk->confirm) ||
       *reinterpret_cast<volatile int*>(&bk->stop) == 1)
     return;
