@@ -49,31 +49,45 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 // Every CTA has published its partials; the last CTA to arrive runs fn()
 // (whole CTA) and then releases the others.  bar = {count, generation}.
+// The arrival is one acq_rel atomic (releases this CTA's partials, acquires
+// everyone's for the last CTA), the release a red.release on the
+// generation, the wait an ld.acquire spin -- no full membar.gl on the path.
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 template <class F>
 __device__ __forceinline__ void reduce_barrier(unsigned* bar, F&& fn) {
   __shared__ int s_last;
   __shared__ unsigned s_gen;
-  __syncthreads();
+  __syncthreads();  // this CTA's partials are written (CTA scope)
   if (threadIdx.x == 0) {
-    volatile unsigned* gen = bar + 1;
-    s_gen = *gen;
-    __threadfence();
-    s_last = atomicAdd(bar, 1u) == gridDim.x - 1;
+    const unsigned g = ld_acquire(bar + 1);
+    s_gen = g;
+    __threadfence_block();
+    s_last = atom_add_acq_rel(bar, 1u) == gridDim.x - 1;
   }
   __syncthreads();
   if (s_last) {
-    __threadfence();
     fn();
     __syncthreads();
     if (threadIdx.x == 0) {
       bar[0] = 0u;
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
+      red_release_add(bar + 1, 1u);
     }
   } else if (threadIdx.x == 0) {
-    volatile unsigned* gen = bar + 1;
-    while (*gen == s_gen) __nanosleep(32);
-    __threadfence();
+    while (ld_acquire(bar + 1) == s_gen) {
+    }
   }
   __syncthreads();
 }
@@ -252,18 +266,41 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
   }
   TAIL_STAMP(1, atomicMax);
   reduce_barrier(bar, [&] {
-    book_load(&sbk, bk);
-    T s8[8];
-    totals<T, 8>(cpart, G, 0, s8, shT);
+    // one round of loads: the Book words, the 8 sums and the max of every CTA
+    constexpr int BW = static_cast<int>(sizeof(Book<T>) / 8);
+    unsigned long long bw = tid < BW ? __ldcg(reinterpret_cast<const unsigned long long*>(bk) + tid)
+                                     : 0ull;
+    T acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = T(0);
     T m1 = T(0);
-    for (int b = tid; b < G; b += kTT) m1 = fmax(m1, __ldcg(cpart + b * kTSlots + 8));
+    for (int b = tid; b < G; b += kTT) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] += __ldcg(cpart + b * kTSlots + k);
+      m1 = fmax(m1, __ldcg(cpart + b * kTSlots + 8));
+    }
+    if (tid < BW) reinterpret_cast<unsigned long long*>(&sbk)[tid] = bw;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = warp_sum(acc[k]);
     m1 = warp_max(m1);
-    if (lane == 0) shT[warp] = m1;
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) shT[k * kTW + warp] = acc[k];
+      shT[8 * kTW + warp] = m1;
+    }
     __syncthreads();
     if (tid == 0) {
+      T s8[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        T sum = T(0);
+#pragma unroll
+        for (int w = 0; w < kTW; ++w) sum += shT[k * kTW + w];
+        s8[k] = sum;
+      }
       T mxt = T(0);
 #pragma unroll
-      for (int w = 0; w < kTW; ++w) mxt = fmax(mxt, shT[w]);
+      for (int w = 0; w < kTW; ++w) mxt = fmax(mxt, shT[8 * kTW + w]);
       // {cost, prev, dual, dx, max|t|, sum r, |r|^2, |s|^2} (merge_kernel order)
       const T tot[8] = {s8[0], s8[1], s8[2], s8[3], mxt, s8[5], s8[6], s8[7]};
       merge_scalars<T>(&sbk, t, tot, s8[4] > T(0) ? 1 : 0);
@@ -319,9 +356,13 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
   }
   TAIL_STAMP(4, atomicMax);
   reduce_barrier(bar, [&] {
-    book_load(&sbk, bk);
+    constexpr int BW = static_cast<int>(sizeof(Book<T>) / 8);
+    unsigned long long bw = tid < BW ? __ldcg(reinterpret_cast<const unsigned long long*>(bk) + tid)
+                                     : 0ull;
     double d8[8];
-    totals<double, 8>(dpart, G, 0, d8, shD);
+    totals<double, 8>(dpart, G, 0, d8, shD);  // (its __syncthreads also publish sbk)
+    if (tid < BW) reinterpret_cast<unsigned long long*>(&sbk)[tid] = bw;
+    __syncthreads();
     if (tid == 0)
       gate_logic<T>(&sbk, t, d8[0] + d8[4], d8[1], d8[2], d8[5], d8[6], d8[3] + d8[7]);
     book_store(bk, &sbk);
