@@ -315,6 +315,9 @@ def run_b200(args, rank, world, local_rank):
         ttt = time_to_tol_c2(args, drot, torch, dist, m, n, m_global, rank, world, local_rank)
         if out is not None:
             out["time_to_tol_c2"] = ttt
+    # ---- config C5 at N = 1: m = n = 100 000 fp32 (X + C = 80 GB) ----------
+    if world == 1 and rank == 0 and not args.no_c5:
+        out["c5_single_gpu"] = c5_single(args, drot, torch)
     # ---- e2e through the public API with host buffers -----------------------
     if not args.no_e2e:
         e2e = run_e2e(args, drot, torch, m, n, local_rank)
@@ -368,6 +371,40 @@ def run_e2e(args, drot, torch, m, n, local_rank):
             "step": f"one drot.solve() call of {S} iterations from pinned host buffers "
                     f"(validation, init, {S} gated iterations, final report, plan/duals/trace "
                     f"download); median of 2 after 1 warm call, {t*1e3:.1f} ms/call"}
+
+
+def c5_single(args, drot, torch, size=100000, iters=20):
+    """Config C5 on one GPU: the 10^5 x 10^5 fp32 Gaussian
+    instance generated on the device (K7; 40 GB per matrix -- no host copy
+    exists), `iters` timed iterations after 4 warm-up ones, CUDA events on
+    the session stream."""
+    free, _ = torch.cuda.mem_get_info()
+    need = 2 * 4 * size * size * 1.05
+    if free < need:
+        return {"skipped": f"needs {need / 1e9:.0f} GB, {free / 1e9:.0f} GB free"}
+    t0 = time.perf_counter()
+    s = drot.Session(size, size, np.float32, drot.DrotConfig(tol_primal=-1.0, max_iters=10 ** 12))
+    stream = torch.cuda.current_stream()
+    s.set_stream(stream.cuda_stream)
+    s.gen_gaussian(5.0, 0, "dyadic")
+    s.init()
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t0
+    s.enqueue(4)
+    r = s.run_timed(iters)
+    s.close()
+    torch.cuda.empty_cache()
+    ms = r["total_ms"] / iters
+    bytes_it = r["pass_bytes"] / iters
+    peak, _ = measured_hbm_peak()
+    return {"config": f"C5 {size}x{size} fp32 Gaussian seed 0 (generated on the device), "
+                      "dyadic-uniform marginals, 1 GPU",
+            "iterations_per_s": 1e3 / ms, "ms_per_iteration": ms,
+            "sweep_ms_avg": r["pass_ms"] / iters,
+            "hbm_gbs_step": bytes_it / (ms / 1e3) / 1e9,
+            "sweep_gbs": bytes_it / (r["pass_ms"] / iters / 1e3) / 1e9,
+            "frac_of_peak_step": bytes_it / (ms / 1e3) / 1e9 / peak,
+            "setup_s_generation_validation_init": setup, "timed_iterations": iters}
 
 
 def time_to_tol_c2(args, drot, torch, dist, m, n, m_global, rank, world, local_rank):
@@ -455,6 +492,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ttt", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--ttt-max-iters", type=int, default=400000)
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))

@@ -131,8 +131,8 @@ struct TailArgs {
   // row-sharded multi-GPU (0: single device): merge/update/report write
   // their rank-local partials to these buffers for the NCCL allreduces
   int32_t sharded;
-  T* pack;       // [v (n) | sum r, sum r^2, cost, prev, dual, dx]  (sum)
-  T* pmax;       // [max|t| or +inf if non-finite]                   (max)
+  T* pack;       // [v (n) | sum r, sum r^2, cost, prev, dual, dx, #bad]  (sum)
+  T* pmax;       // [rank-local max|t|] (diagnostic, not reduced)
   double* dpack; // [dual_i, dphi^2, dphi, cross_i | obj, dual^2]    (sum)
   // cooperative tail (tail.cu): the arrays the confirm report streams
   const T* report_x;

@@ -617,10 +617,15 @@ __global__ void __launch_bounds__(kTailThreads) merge_kernel(const TailArgs<T> t
     for (int k = 0; k < 4; ++k) t.pack[t.n + 2 + k] = tot[k];
     t.pack[t.n + 0] = tot[5];
     t.pack[t.n + 1] = tot[6];
-    t.pmax[0] = totbad ? __int_as_float(0x7f800000) : tot[4];
+    t.pack[t.n + 6] = totbad ? T(1) : T(0);  // non-finite count rides in the sum
+    t.pmax[0] = tot[4];                        // rank-local max|t| (diagnostic only)
     return;
   }
-  merge_scalars<T>(bk, t, tot, totbad);
+  {  // one bulk round trip for the Book instead of one per field
+    Book<T> lb = *bk;
+    merge_scalars<T>(&lb, t, tot, totbad);
+    *bk = lb;
+  }
 }
 
 template <class T>
@@ -657,10 +662,14 @@ __global__ void __launch_bounds__(kTailThreads) finish_kernel(const TailArgs<T> 
   if (threadIdx.x != 0) return;
   bk->ticket_merge = 0u;
   const T mx = t.pmax[0];
-  const int bad = !(mx <= max_finite<T>());
+  const int bad = t.pack[t.n + 6] > T(0) ? 1 : 0;
   const T tot[8] = {t.pack[t.n + 2], t.pack[t.n + 3], t.pack[t.n + 4], t.pack[t.n + 5],
                     mx,              t.pack[t.n + 0], t.pack[t.n + 1], s1[0]};
-  merge_scalars<T>(bk, t, tot, bad);
+  {
+    Book<T> lb = *bk;
+    merge_scalars<T>(&lb, t, tot, bad);
+    *bk = lb;
+  }
 }
 
 template <class T>
@@ -798,7 +807,11 @@ __global__ void __launch_bounds__(kTailThreads) update_kernel(const TailArgs<T> 
     }
     return;
   }
-  gate_logic<T>(bk, t, tot[0] + tot[4], tot[1], tot[2], tot[5], tot[6], tot[3] + tot[7]);
+  {
+    Book<T> lb = *bk;
+    gate_logic<T>(&lb, t, tot[0] + tot[4], tot[1], tot[2], tot[5], tot[6], tot[3] + tot[7]);
+    *bk = lb;
+  }
 }
 
 // Sharded continuation of K3 after the allreduce of the row-side sums.
@@ -906,7 +919,11 @@ __global__ void __launch_bounds__(kTailThreads)
     t.dpack[5] = s2[1];
     return;
   }
-  report_decide<T>(bk, s2[0], s2[1], always);
+  {
+    Book<T> lb = *bk;
+    report_decide<T>(&lb, s2[0], s2[1], always);
+    *bk = lb;
+  }
 }
 
 template <class T>
@@ -981,7 +998,11 @@ __global__ void __launch_bounds__(kTailThreads)
     t.dpack[5] = s2[1];
     return;
   }
-  report_decide<T>(bk, s2[0], s2[1], always);
+  {
+    Book<T> lb = *bk;
+    report_decide<T>(&lb, s2[0], s2[1], always);
+    *bk = lb;
+  }
 }
 
 template <class T>

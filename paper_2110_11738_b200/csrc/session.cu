@@ -159,7 +159,7 @@ struct Session {
   int rank = 0, world = 1;
   bool sharded = false;
   ncclComm_t comm = nullptr;
-  T* pack = nullptr;      // [v (n) | sum r, |r|^2, cost, prev, dual, dx]
+  T* pack = nullptr;      // [v (n) | sum r, |r|^2, cost, prev, dual, dx, non-finite count]
   T* pmax = nullptr;      // [max|t|]
   double* dpack = nullptr;  // [row-side update sums (4) | report sums (2) | misc]
   int32_t* dint = nullptr;
@@ -891,8 +891,7 @@ struct Session {
     }
     launch_merge<T>(ta, exact, stream);
     if (sharded) {  // one exchange per phase; gate pauses for confirm
-      RC_TRY(allreduce(pack, static_cast<size_t>(n + 6), ncclSum));
-      RC_TRY(allreduce(pmax, 1, ncclMax));
+      RC_TRY(allreduce(pack, static_cast<size_t>(n + 7), ncclSum));
       launch_finish<T>(ta, stream);
       launch_update<T>(ta, false, stream);
       RC_TRY(allreduce(dpack, 4, ncclSum));
