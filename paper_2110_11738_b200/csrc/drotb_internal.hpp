@@ -80,6 +80,14 @@ struct Book {
   int32_t record_trace, relative;
   unsigned int ticket_merge, ticket_update, ticket_report, pad1;
   double jpart[4];  // sharded: replicated column-side partials of the update
+  // fused-gate tail (tail.cu): the exact dual value and fixed-point terms of
+  // an iteration are reduced one iteration later (or at finish) and patched
+  int64_t pend_row;       // trace row awaiting its gap / fixed-point residual (-1: none)
+  int32_t pend_valid;     // the tail's update partials of the last iteration are pending
+  int32_t pend_use_dx;    // that iteration read C and wanted dx
+  double pend_last_cost;  // last_cost seen by its gate
+  double pend_dx;         // its pass dx^2
+  double sum_p, sum_q;    // sum p_i, sum q_j (double, sequential; set at init)
 };
 
 struct TraceRowDev {
@@ -138,6 +146,8 @@ struct TailArgs {
   const T* report_x;
   const T* report_c;
   unsigned long long* stamps;  // profiling aid: tail phase timestamps (or null)
+  int32_t fused_gate;          // tail: gate on the algebraic dual value (one barrier less)
+  int32_t pad_fg;
 };
 
 // Persistent solver kernel (persistent.cu): one cooperative launch runs up to
@@ -189,6 +199,9 @@ int tail_grid(int device);
 template <class T>
 cudaError_t launch_tail(const TailArgs<T>& t, T* cpart, double* dpart, unsigned* bar, int grid,
                         cudaStream_t st);
+// patch the pending exact dual value / fixed-point residual (end of a run)
+template <class T>
+void launch_tail_finalize(const TailArgs<T>& t, const double* dpart, int grid, cudaStream_t st);
 
 // ---- kernel launchers (kernels.cu) ---------------------------------------
 template <class T>

@@ -176,7 +176,7 @@ struct Session {
   double* pmud = nullptr;
   bool h_stale = false;  // h_iter / h_folded lag the device after persistent launches
   // cooperative tail kernel (fast order, one GPU; tail.cu)
-  bool coop = false, coop_graphs = false;
+  bool coop = false, coop_graphs = false, fused_gate = true;
   int tgrid = 0;
   T* tcpart = nullptr;
   double* tdpart = nullptr;
@@ -272,6 +272,7 @@ struct Session {
   }
 
   int setup_coop_tail() {
+    if (const char* e = std::getenv("DROTB_TAIL_GATE")) fused_gate = e[0] != 'e';
     tgrid = tail_grid<T>(device);
     if (tgrid <= 0) return 0;
     RC_TRY(dev_alloc(&tcpart, static_cast<size_t>(tgrid) * 16));
@@ -755,6 +756,15 @@ struct Session {
     hb.primal_scale = cfg.relative_tolerances ? 1.0 / (1.0 + p_norm + q_norm) : 1.0;
     hb.record_trace = cfg.record_trace ? 1 : 0;
     hb.relative = cfg.relative_tolerances ? 1 : 0;
+    hb.pend_row = -1;
+    hb.pend_valid = 0;
+    {
+      double sp = 0, sq = 0;
+      for (T e : hp) sp += static_cast<double>(e);
+      for (T e : hq) sq += static_cast<double>(e);
+      hb.sum_p = sp;
+      hb.sum_q = sq;
+    }
     if (cfg.max_iters <= 0) hb.stop = 1;
     CUDA_TRY(cudaMemcpyAsync(book, &hb, sizeof(hb), cudaMemcpyHostToDevice, stream));
     if (sharded) {  // column sums and sum(a) span all ranks
@@ -859,6 +869,7 @@ struct Session {
     t.report_x = X;
     t.report_c = C;
     t.stamps = tstamps;
+    t.fused_gate = fused_gate ? 1 : 0;
     return t;
   }
 
@@ -1215,7 +1226,16 @@ struct Session {
   }
 
   // Final status and report (solver.hpp:527-538).
+  int finalize_pending() {  // coop tail: patch the last iteration's exact dual / trace terms
+    if (!coop || !tdpart) return 0;
+    TailArgs<T> ta = tail_args(h_iter, kFold, h_folded, true);
+    launch_tail_finalize<T>(ta, tdpart, tgrid, stream);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
+
   int finish(int32_t* status, int64_t* iterations, drotb_report* rep) {
+    RC_TRY(finalize_pending());
     Book<T> hb;
     RC_TRY(read_book(&hb));
     int32_t st = DROTB_MAX_ITERS;
@@ -1306,6 +1326,7 @@ struct Session {
   }
 
   int get_trace(drotb_trace_row* out, int64_t cap, int64_t* len) {
+    RC_TRY(finalize_pending());
     Book<T> hb;
     RC_TRY(read_book(&hb));
     if (len) *len = hb.trace_rows;

@@ -163,6 +163,83 @@ __device__ __forceinline__ void book_store(Book<T>* dst, const Book<T>* src) {
   __syncthreads();
 }
 
+// Fused gate (t.fused_gate): the gate of iteration k runs right after the
+// merge totals, on the dual value in closed form,
+//   sum_i p_i phi_i^{k+1} = (sum p_i a_i - 2 sum p_i r_i + coef sum p_i) / n
+// (and likewise for the columns), so the update phase needs no barrier
+// behind it.  It is only the pre-filter of solver.hpp:474-504: the confirm
+// report recomputes the exact dual value (sum of p_i * phi_i / rho, as the
+// reference) and decides convergence.  The exact dual value and the
+// fixed-point residual of an iteration (trace columns gap and
+// fixed_point_residual) are reduced one iteration later -- or by the
+// finalize kernel at the end of a run -- and patched into its trace row.
+template <class T>
+__device__ void patch_pending(Book<T>* bk, const TailArgs<T>& t, const double (&d8)[8]) {
+  if (!bk->pend_valid) return;
+  const double dual = d8[0] + d8[4];
+  double fpr = __longlong_as_double(0x7ff8000000000000ULL);
+  if (bk->record_trace) {  // rank-two identity (solver.hpp:443-472)
+    double fp_sq = static_cast<double>(t.n_global) * d8[1] +
+                   static_cast<double>(t.m_global) * d8[5] + 2.0 * d8[2] * d8[6];
+    if (bk->pend_use_dx) fp_sq += bk->pend_dx + 2.0 * (d8[3] + d8[7]);
+    fpr = sqrt(fmax(fp_sq, 0.0));
+  }
+  bk->dual_value = dual;
+  bk->gap = fabs(bk->pend_last_cost - dual);
+  bk->fp_residual = fpr;
+  if (t.trace && bk->pend_row >= 0 && bk->pend_row < bk->trace_cap) {
+    TraceRowDev& row = t.trace[bk->pend_row];
+    row.gap = bk->gap;
+    row.fixed_point_residual = fpr;
+  }
+  bk->pend_valid = 0;
+  bk->pend_row = -1;
+}
+
+template <class T>
+__device__ void gate_fused(Book<T>* bk, const TailArgs<T>& t, double dual_alg) {
+  bk->alpha = bk->alpha - bk->beta;  // solver.hpp:289
+  const int64_t k = bk->iter;
+  bk->iter = k + 1;
+  const double nan = __longlong_as_double(0x7ff8000000000000ULL);
+  const double r_primal = sqrt(static_cast<double>(bk->nr2) + static_cast<double>(bk->ns2));
+  const double gap = fabs(bk->last_cost - dual_alg);
+  const double gap_scale = bk->relative ? 1.0 / (1.0 + fabs(bk->last_cost)) : 1.0;
+  bk->r_primal = r_primal;
+  bk->dual_value = dual_alg;
+  bk->gap = gap;
+  bk->fp_residual = nan;
+  const bool check = ((k + 1) % bk->check_every) == 0;
+  const bool trace_row = bk->record_trace && ((k + 1) % bk->trace_every) == 0;
+  bk->pend_row = -1;
+  if (trace_row) {
+    if (t.trace && bk->trace_rows < bk->trace_cap) {
+      TraceRowDev& row = t.trace[bk->trace_rows];
+      row.iter = k + 1;
+      row.r_primal = r_primal;
+      row.r_dual = bk->last_r_dual;
+      row.gap = gap;  // patched with the exact dual value later
+      row.objective = bk->last_cost;
+      row.ergodic_objective = bk->erg_mean;
+      row.fixed_point_residual = nan;  // patched later
+      bk->pend_row = bk->trace_rows;
+    }
+    bk->trace_rows += 1;
+  }
+  bk->pend_valid = 1;
+  bk->pend_last_cost = bk->last_cost;
+  bk->pend_use_dx = (t.reads_cost && t.want_dx) ? 1 : 0;
+  bk->pend_dx = static_cast<double>(bk->pass_dx);
+  const bool fire = check && r_primal * bk->primal_scale <= bk->tol_primal &&
+                    bk->last_r_dual <= bk->tol_dual && gap * gap_scale <= bk->tol_gap;
+  if (fire) {
+    bk->confirm = 1;
+    bk->gate_hits += 1;
+  } else if (k + 1 >= bk->max_iters) {
+    bk->stop = 1;
+  }
+}
+
 template <class T>
 __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart,
                                                    double* dpart, unsigned* bar) {
@@ -182,6 +259,7 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
   // ---- A: merge -----------------------------------------------------------
   {
     T pr[3] = {T(0), T(0), T(0)};
+    double pd[4] = {0, 0, 0, 0};  // sum p a, sum p r, sum q b, sum q s (fused gate)
     const int64_t ngr = (m + 31) / 32, ngc = (n + 31) / 32;
     for (int64_t grp = blockIdx.x; grp < ngr + ngc; grp += G) {
       T acc = T(0);
@@ -221,17 +299,23 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
         if (grp < ngr) {
           const int64_t idx = grp * 32 + lane;
           if (idx < m) {
-            const T r = tot - t.p[idx];
+            const T pi = t.p[idx];
+            const T r = tot - pi;
             t.r_new[idx] = r;
             pr[0] += r;
             pr[1] += r * r;
+            pd[0] += static_cast<double>(pi) * static_cast<double>(t.a[idx]);
+            pd[1] += static_cast<double>(pi) * static_cast<double>(r);
           }
         } else {
           const int64_t j = (grp - ngr) * 32 + lane;
           if (j < n) {
-            const T s = tot - t.q[j];
+            const T qj = t.q[j];
+            const T s = tot - qj;
             t.s_new[j] = s;
             pr[2] += s * s;
+            pd[2] += static_cast<double>(qj) * static_cast<double>(t.b[j]);
+            pd[3] += static_cast<double>(qj) * static_cast<double>(s);
           }
         }
       }
@@ -262,6 +346,7 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
     __syncthreads();
     T v8[8] = {ps[0], ps[1], ps[2], ps[3], bad, pr[0], pr[1], pr[2]};
     store_partials<T, 8>(v8, cpart, 0, shT);
+    if (t.fused_gate) store_partials<double, 4>(pd, dpart, 10, shD);
     if (tid == 0) cpart[blockIdx.x * kTSlots + 8] = cmx;
   }
   TAIL_STAMP(1, atomicMax);
@@ -305,11 +390,30 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
       const T tot[8] = {s8[0], s8[1], s8[2], s8[3], mxt, s8[5], s8[6], s8[7]};
       merge_scalars<T>(&sbk, t, tot, s8[4] > T(0) ? 1 : 0);
     }
+    if (t.fused_gate) {
+      __syncthreads();
+      double dp8[8], d4[4];
+      totals<double, 8>(dpart, G, 0, dp8, shD);  // previous iteration's update partials
+      totals<double, 4>(dpart, G, 10, d4, shD);  // this iteration's p.a, p.r, q.b, q.s
+      if (tid == 0) {
+        patch_pending<T>(&sbk, t, dp8);
+        if (!sbk.stop) {
+          const double coef = static_cast<double>(sbk.coef);
+          const double inv_n = 1.0 / static_cast<double>(t.n_global);
+          const double inv_m = 1.0 / static_cast<double>(t.m_global);
+          const double dual_alg = ((d4[0] - 2.0 * d4[1] + coef * sbk.sum_p) * inv_n +
+                                   (d4[2] - 2.0 * d4[3] + coef * sbk.sum_q) * inv_m) /
+                                  static_cast<double>(t.rho);
+          gate_fused<T>(&sbk, t, dual_alg);
+        }
+      }
+    }
     book_store(bk, &sbk);
     TAIL_STAMP(2, atomicMax);
   });
   TAIL_STAMP(3, atomicMax);
-  if (*reinterpret_cast<volatile int*>(&bk->stop)) return;  // non-finite pass
+  if (*reinterpret_cast<volatile int*>(&bk->failed)) return;  // non-finite pass
+  if (!t.fused_gate && *reinterpret_cast<volatile int*>(&bk->stop)) return;
 
   // ---- B: phi / varphi / a / b + dual-value and fixed-point partials --------
   {
@@ -355,6 +459,24 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
     store_partials<double, 8>(part, dpart, 0, shD);
   }
   TAIL_STAMP(4, atomicMax);
+  if (t.fused_gate) {
+    // gate already decided after the merge; the confirm report needs the
+    // updated phi / varphi everywhere and the exact dual value
+    if (!*reinterpret_cast<volatile int*>(&bk->confirm) ||
+        *reinterpret_cast<volatile int*>(&bk->stop) == 1)
+      return;
+    reduce_barrier(bar, [&] {
+      constexpr int BW = static_cast<int>(sizeof(Book<T>) / 8);
+      unsigned long long bw = tid < BW ? __ldcg(reinterpret_cast<const unsigned long long*>(bk) + tid)
+                                       : 0ull;
+      double d8[8];
+      totals<double, 8>(dpart, G, 0, d8, shD);
+      if (tid < BW) reinterpret_cast<unsigned long long*>(&sbk)[tid] = bw;
+      __syncthreads();
+      if (tid == 0) patch_pending<T>(&sbk, t, d8);
+      book_store(bk, &sbk);
+    });
+  } else {
   reduce_barrier(bar, [&] {
     constexpr int BW = static_cast<int>(sizeof(Book<T>) / 8);
     unsigned long long bw = tid < BW ? __ldcg(reinterpret_cast<const unsigned long long*>(bk) + tid)
@@ -368,6 +490,7 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
     book_store(bk, &sbk);
     TAIL_STAMP(5, atomicMax);
   });
+  }
   TAIL_STAMP(6, atomicMax);
   if (!*reinterpret_cast<volatile int*>(&bk->confirm) ||
       *reinterpret_cast<volatile int*>(&bk->stop) == 1)
@@ -414,6 +537,21 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
 }  // namespace
 
 template <class T>
+__global__ void __launch_bounds__(kTT) tail_finalize_kernel(const TailArgs<T> t,
+                                                            const double* dpart, int G) {
+  __shared__ double shD[16 * kTW];
+  Book<T>* bk = t.book;
+  if (!*reinterpret_cast<volatile int*>(&bk->pend_valid)) return;
+  double d8[8];
+  totals<double, 8>(dpart, G, 0, d8, shD);
+  if (threadIdx.x == 0) {
+    Book<T> lb = *bk;
+    patch_pending<T>(&lb, t, d8);
+    *bk = lb;
+  }
+}
+
+template <class T>
 int tail_grid(int device) {
   int sms = 0, per = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -441,6 +579,16 @@ cudaError_t launch_tail(const TailArgs<T>& t, T* cpart, double* dpart, unsigned*
   return cudaLaunchKernelEx(&cfg, tail_kernel<T>, t, cpart, dpart, bar);
 }
 
+template <class T>
+void launch_tail_finalize(const TailArgs<T>& t, const double* dpart, int grid, cudaStream_t st) {
+  tail_finalize_kernel<T><<<1, kTT, 0, st>>>(t, dpart, grid);
+  count_launch();
+}
+
+template void launch_tail_finalize<float>(const TailArgs<float>&, const double*, int,
+                                          cudaStream_t);
+template void launch_tail_finalize<double>(const TailArgs<double>&, const double*, int,
+                                           cudaStream_t);
 template int tail_grid<float>(int);
 template int tail_grid<double>(int);
 template cudaError_t launch_tail<float>(const TailArgs<float>&, float*, double*, unsigned*, int,

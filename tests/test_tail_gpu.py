@@ -88,3 +88,32 @@ def test_numerical_failure(drot):
         r = drot.solve(prob, drot.DrotConfig(rho_override=1e10))
         drot.release_device_cache()
     assert r.status == drot.SolveStatus.numerical_failure
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_fused_gate_matches_exact_gate(drot, dt):
+    """The fused gate (closed-form dual value as the pre-filter, exact values
+    patched into the trace one iteration later) against the two-barrier tail
+    that gates on the summed dual value: same status, iterations within
+    max(2, 0.1 %), trace rows equal to rounding."""
+    m, n = 300, 260
+    C = np.asfortranarray(drot.random_matrix(m, n, 9).astype(dt))
+    p = drot.dyadic_marginal(m, dt)
+    q = drot.dyadic_marginal(n, dt)
+    res = []
+    for gate in ("fused", "exact"):
+        with _env(DROTB_TAIL="coop", DROTB_PERSIST="0", DROTB_TAIL_GATE=gate):
+            drot.release_device_cache()
+            res.append(drot.solve(drot.TransportProblem(C, p, q), drot.DrotConfig(max_iters=60000)))
+            drot.release_device_cache()
+    a, b = res
+    assert a.status == b.status == drot.SolveStatus.converged
+    assert abs(a.trace.iterations - b.trace.iterations) <= max(2, b.trace.iterations // 1000)
+    rel = 1e-9 if dt == np.float64 else 1e-4
+    assert abs(a.report.objective - b.report.objective) <= rel * abs(b.report.objective)
+    k = min(len(a.trace.rows), len(b.trace.rows))
+    for ra, rb in zip(a.trace.rows[:k], b.trace.rows[:k]):
+        assert ra.iter == rb.iter
+        for f in ("gap", "fixed_point_residual", "objective", "r_primal"):
+            x, y = getattr(ra, f), getattr(rb, f)
+            assert x == y or (np.isnan(x) and np.isnan(y)) or abs(x - y) <= 1e-6 * max(abs(y), 1e-12), (ra.iter, f, x, y)
