@@ -351,27 +351,43 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
   }
   TAIL_STAMP(1, atomicMax);
   reduce_barrier(bar, [&] {
-    // one round of loads: the Book words, the 8 sums and the max of every CTA
+    // ONE round of loads: the Book words and, per CTA, the 8 T sums, the max,
+    // the previous update's 8 double partials and this merge's 4 (fused gate)
     constexpr int BW = static_cast<int>(sizeof(Book<T>) / 8);
+    const bool fg = t.fused_gate != 0;
     unsigned long long bw = tid < BW ? __ldcg(reinterpret_cast<const unsigned long long*>(bk) + tid)
                                      : 0ull;
     T acc[8];
+    double dd[12];
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc[k] = T(0);
+#pragma unroll
+    for (int k = 0; k < 12; ++k) dd[k] = 0.0;
     T m1 = T(0);
     for (int b = tid; b < G; b += kTT) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) acc[k] += __ldcg(cpart + b * kTSlots + k);
       m1 = fmax(m1, __ldcg(cpart + b * kTSlots + 8));
+      if (fg) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) dd[k] += __ldcg(dpart + b * kTSlots + k);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) dd[8 + k] += __ldcg(dpart + b * kTSlots + 10 + k);
+      }
     }
     if (tid < BW) reinterpret_cast<unsigned long long*>(&sbk)[tid] = bw;
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc[k] = warp_sum(acc[k]);
     m1 = warp_max(m1);
+    if (fg)
+#pragma unroll
+      for (int k = 0; k < 12; ++k) dd[k] = warp_sum(dd[k]);
     if (lane == 0) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) shT[k * kTW + warp] = acc[k];
       shT[8 * kTW + warp] = m1;
+#pragma unroll
+      for (int k = 0; k < 12; ++k) shD[k * kTW + warp] = dd[k];
     }
     __syncthreads();
     if (tid == 0) {
@@ -389,20 +405,23 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
       // {cost, prev, dual, dx, max|t|, sum r, |r|^2, |s|^2} (merge_kernel order)
       const T tot[8] = {s8[0], s8[1], s8[2], s8[3], mxt, s8[5], s8[6], s8[7]};
       merge_scalars<T>(&sbk, t, tot, s8[4] > T(0) ? 1 : 0);
-    }
-    if (t.fused_gate) {
-      __syncthreads();
-      double dp8[8], d4[4];
-      totals<double, 8>(dpart, G, 0, dp8, shD);  // previous iteration's update partials
-      totals<double, 4>(dpart, G, 10, d4, shD);  // this iteration's p.a, p.r, q.b, q.s
-      if (tid == 0) {
-        patch_pending<T>(&sbk, t, dp8);
+      if (fg) {
+        double d12[12];
+#pragma unroll
+        for (int k = 0; k < 12; ++k) {
+          double sum = 0.0;
+#pragma unroll
+          for (int w = 0; w < kTW; ++w) sum += shD[k * kTW + w];
+          d12[k] = sum;
+        }
+        const double dp8[8] = {d12[0], d12[1], d12[2], d12[3], d12[4], d12[5], d12[6], d12[7]};
+        patch_pending<T>(&sbk, t, dp8);  // the previous iteration's exact dual / trace terms
         if (!sbk.stop) {
           const double coef = static_cast<double>(sbk.coef);
           const double inv_n = 1.0 / static_cast<double>(t.n_global);
           const double inv_m = 1.0 / static_cast<double>(t.m_global);
-          const double dual_alg = ((d4[0] - 2.0 * d4[1] + coef * sbk.sum_p) * inv_n +
-                                   (d4[2] - 2.0 * d4[3] + coef * sbk.sum_q) * inv_m) /
+          const double dual_alg = ((d12[8] - 2.0 * d12[9] + coef * sbk.sum_p) * inv_n +
+                                   (d12[10] - 2.0 * d12[11] + coef * sbk.sum_q) * inv_m) /
                                   static_cast<double>(t.rho);
           gate_fused<T>(&sbk, t, dual_alg);
         }
