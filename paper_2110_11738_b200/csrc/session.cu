@@ -277,8 +277,8 @@ struct Session {
     if (tgrid <= 0) return 0;
     RC_TRY(dev_alloc(&tcpart, static_cast<size_t>(tgrid) * 16));
     RC_TRY(dev_alloc(&tdpart, static_cast<size_t>(tgrid) * 16));
-    RC_TRY(dev_alloc(&tbar, 2));
-    CUDA_TRY(cudaMemsetAsync(tbar, 0, 2 * sizeof(unsigned), stream));
+    RC_TRY(dev_alloc(&tbar, 1024));  // top count, generation, 16 group counters (tail.cu)
+    CUDA_TRY(cudaMemsetAsync(tbar, 0, 1024 * sizeof(unsigned), stream));
     if (const char* e = std::getenv("DROTB_TAIL_STAMPS"))
       if (e[0] == '1') {
         RC_TRY(dev_alloc(&tstamps, 8));

@@ -66,29 +66,42 @@ __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// bar layout (unsigned words): [0] top count, [1] generation, and
+// kBarSub group counters at [kBarStride * (1 + g)] (one 128-B line each).
+// Arrival is hierarchical -- CTA b increments group counter b % kBarSub;
+// the last of its group increments the top counter -- so no address sees
+// more than ~G/kBarSub serialized atomics.  The generation a CTA waits on
+// is tracked in shared memory from one read at kernel start.
+constexpr int kBarSub = 16;
+constexpr int kBarStride = 32;
+
 template <class F>
-__device__ __forceinline__ void reduce_barrier(unsigned* bar, F&& fn) {
+__device__ __forceinline__ void reduce_barrier(unsigned* bar, unsigned& my_gen, F&& fn) {
   __shared__ int s_last;
-  __shared__ unsigned s_gen;
   __syncthreads();  // this CTA's partials are written (CTA scope)
   if (threadIdx.x == 0) {
-    const unsigned g = ld_acquire(bar + 1);
-    s_gen = g;
-    __threadfence_block();
-    s_last = atom_add_acq_rel(bar, 1u) == gridDim.x - 1;
+    const unsigned G = gridDim.x;
+    const unsigned grp = blockIdx.x % kBarSub;
+    const unsigned ngrp = G < kBarSub ? G : kBarSub;
+    const unsigned members = G / kBarSub + (grp < G % kBarSub ? 1u : 0u);
+    int last = 0;
+    if (atom_add_acq_rel(bar + kBarStride * (1 + grp), 1u) == members - 1)
+      last = atom_add_acq_rel(bar, 1u) == ngrp - 1;
+    s_last = last;
   }
   __syncthreads();
   if (s_last) {
     fn();
     __syncthreads();
-    if (threadIdx.x == 0) {
-      bar[0] = 0u;
-      red_release_add(bar + 1, 1u);
-    }
+    if (threadIdx.x < kBarSub) bar[kBarStride * (1 + threadIdx.x)] = 0u;
+    if (threadIdx.x == 0) bar[0] = 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) red_release_add(bar + 1, 1u);
   } else if (threadIdx.x == 0) {
-    while (ld_acquire(bar + 1) == s_gen) {
+    while (ld_acquire(bar + 1) == my_gen) {
     }
   }
+  ++my_gen;
   __syncthreads();
 }
 
@@ -255,6 +268,10 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x;
   const int64_t m = t.m, n = t.n;
+  __shared__ unsigned s_gen0;
+  if (tid == 0) s_gen0 = ld_acquire(bar + 1);  // no barrier is in flight at launch
+  __syncthreads();
+  unsigned my_gen = s_gen0;
 
   // ---- A: merge -----------------------------------------------------------
   {
@@ -350,7 +367,7 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
     if (tid == 0) cpart[blockIdx.x * kTSlots + 8] = cmx;
   }
   TAIL_STAMP(1, atomicMax);
-  reduce_barrier(bar, [&] {
+  reduce_barrier(bar, my_gen, [&] {
     // ONE round of loads: the Book words and, per CTA, the 8 T sums, the max,
     // the previous update's 8 double partials and this merge's 4 (fused gate)
     constexpr int BW = static_cast<int>(sizeof(Book<T>) / 8);
@@ -484,7 +501,7 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
     if (!*reinterpret_cast<volatile int*>(&bk->confirm) ||
         *reinterpret_cast<volatile int*>(&bk->stop) == 1)
       return;
-    reduce_barrier(bar, [&] {
+    reduce_barrier(bar, my_gen, [&] {
       constexpr int BW = static_cast<int>(sizeof(Book<T>) / 8);
       unsigned long long bw = tid < BW ? __ldcg(reinterpret_cast<const unsigned long long*>(bk) + tid)
                                        : 0ull;
@@ -496,7 +513,7 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
       book_store(bk, &sbk);
     });
   } else {
-  reduce_barrier(bar, [&] {
+  reduce_barrier(bar, my_gen, [&] {
     constexpr int BW = static_cast<int>(sizeof(Book<T>) / 8);
     unsigned long long bw = tid < BW ? __ldcg(reinterpret_cast<const unsigned long long*>(bk) + tid)
                                      : 0ull;
@@ -544,7 +561,7 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
     }
     store_partials<double, 2>(part, dpart, 8, shD);
   }
-  reduce_barrier(bar, [&] {
+  reduce_barrier(bar, my_gen, [&] {
     book_load(&sbk, bk);
     double d2[2];
     totals<double, 2>(dpart, G, 8, d2, shD);
