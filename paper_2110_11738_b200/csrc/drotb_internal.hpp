@@ -49,6 +49,8 @@ struct PassArgs {
   T* __restrict__ vstrip;
   PassPartial<T>* __restrict__ partials;
   const int* stop;      // device stop flag (nullptr: never)
+  int32_t pdl;          // launch as a programmatic dependent (after the coop tail)
+  int32_t pad_pdl;
 };
 
 // Device-resident solver bookkeeping: every scalar of the solve loop

@@ -119,6 +119,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
   constexpr int ROWS_W = 32 * R;
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   __shared__ PassAcc<T> wacc[kWarpsPerCta];
+  // programmatic dependent launch: the CTAs may be scheduled while the
+  // preceding tail kernel still runs; wait for its completion and memory
+  // before touching any data (no-op for an ordinary launch)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (a.stop != nullptr && *reinterpret_cast<const volatile int*>(a.stop)) return;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -203,7 +207,21 @@ static void launch_pass_t(const PassArgs<T>& a, cudaStream_t st) {
       return true;
     }();
     (void)attr;
-    pass_kernel_async<T, MODE, DUAL, DX><<<grid, kWarpsPerCta * 32, smem, st>>>(a);
+    if (a.pdl) {  // launched as a programmatic dependent of the cooperative tail
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = grid;
+      cfg.blockDim = dim3(kWarpsPerCta * 32);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, pass_kernel_async<T, MODE, DUAL, DX>, a);
+    } else {
+      pass_kernel_async<T, MODE, DUAL, DX><<<grid, kWarpsPerCta * 32, smem, st>>>(a);
+    }
   } else {
     pass_kernel<T, MODE, DUAL, DX><<<grid, kWarpsPerCta * 32, 0, st>>>(a);
   }

@@ -259,6 +259,9 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
   using V = typename V16<T>::type;
   constexpr int R = 16 / sizeof(T);
   Book<T>* bk = t.book;
+  // the next sweep (a programmatic dependent) may be scheduled now; it waits
+  // in griddepcontrol.wait for this grid's completion
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   TAIL_STAMP(0, atomicMin);
   if (*reinterpret_cast<volatile int*>(&bk->stop)) return;
   __shared__ T red[kTW][32];
