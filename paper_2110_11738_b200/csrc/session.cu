@@ -176,7 +176,7 @@ struct Session {
   double* pmud = nullptr;
   bool h_stale = false;  // h_iter / h_folded lag the device after persistent launches
   // cooperative tail kernel (fast order, one GPU; tail.cu)
-  bool coop = false, coop_graphs = false, fused_gate = true, pdl_ok = true;
+  bool coop = false, coop_graphs = false, fused_gate = true, pdl_ok = false;
   int tgrid = 0;
   T* tcpart = nullptr;
   double* tdpart = nullptr;
@@ -273,7 +273,9 @@ struct Session {
 
   int setup_coop_tail() {
     if (const char* e = std::getenv("DROTB_TAIL_GATE")) fused_gate = e[0] != 'e';
-    if (const char* e = std::getenv("DROTB_PDL")) pdl_ok = e[0] != '0';
+    // PDL for K1 after the tail: no gain in graphs (186 vs 186 us/iteration
+    // at 10k^2) and it inflates the event-timed sweep, so opt-in
+    if (const char* e = std::getenv("DROTB_PDL")) pdl_ok = e[0] == '1';
     tgrid = tail_grid<T>(device);
     if (tgrid <= 0) return 0;
     RC_TRY(dev_alloc(&tcpart, static_cast<size_t>(tgrid) * 16));
