@@ -256,6 +256,24 @@ int drotb_residual_report_f64(const double* C, int64_t m, int64_t n, const doubl
                               const double* q, const double* plan, const double* mu,
                               const double* nu, int32_t exact, drotb_report* out);
 
+/* ---- Sinkhorn baseline: drot::sinkhorn_solve<T> (reference.hpp:165-288) --
+ * The paper's comparison method on the B200 (plain Sinkhorn on
+ * K = exp(-C/eta)); errors: bad_config (eta <= 0), zero_marginal (p or q has
+ * a non-positive entry).  Divergence is a status (numerical_failure, zero
+ * plan/duals, NaN report).  trace rows: one per check (r_primal = the
+ * marginal error, r_dual = -1 = kResidualNotApplicable).  exact_report
+ * selects the reference-order residual_report. */
+int drotb_sinkhorn_f32(const float* C, int64_t m, int64_t n, const float* p, const float* q,
+                       float eta, double tol, int64_t max_iters, int64_t check_every,
+                       int32_t exact_report, float* plan, float* mu, float* nu,
+                       drotb_report* report, drotb_trace_row* trace, int64_t trace_cap,
+                       int64_t* trace_len, int64_t* iterations, int32_t* status, double* wall);
+int drotb_sinkhorn_f64(const double* C, int64_t m, int64_t n, const double* p, const double* q,
+                       double eta, double tol, int64_t max_iters, int64_t check_every,
+                       int32_t exact_report, double* plan, double* mu, double* nu,
+                       drotb_report* report, drotb_trace_row* trace, int64_t trace_cap,
+                       int64_t* trace_len, int64_t* iterations, int32_t* status, double* wall);
+
 /* ---- problem generation (probgen.hpp:131-170, host, bit-identical) ------ *
  * Writes C (m*n column-major, normalized to max 1), p (m), q (n) in double.
  * dirichlet != 0 selects Dirichlet(1..1) marginals (probgen.hpp:115-127). */

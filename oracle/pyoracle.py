@@ -297,6 +297,37 @@ class Oracle:
                       C.byref(spi), C.byref(tot)))
         return spi.value, tot.value
 
+    def sinkhorn(self, cost, p, q, m, n, eta, tol, max_iters, check_every=10):
+        """drot::sinkhorn_solve<T> (reference only)."""
+        assert self.kind == "ref"
+        dt = np.asarray(p).dtype
+        sfx = self._sfx(dt)
+        tc = C.c_float if dt == np.float32 else C.c_double
+        plan = np.empty(m * n, dt)
+        mu = np.empty(m, dt)
+        nu = np.empty(n, dt)
+        rep = OrcReport()
+        cap = max(int(max_iters) // max(int(check_every), 1) + 2, 1)
+        trace = (OrcTraceRow * cap)()
+        tlen, iters = C.c_int64(0), C.c_int64(0)
+        status, wall = C.c_int32(0), C.c_double(0)
+        f = self._fn("sinkhorn_" + sfx)
+        f.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, tc, C.c_double,
+                      C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                      C.POINTER(OrcReport), C.c_void_p, C.c_int64, C.POINTER(C.c_int64),
+                      C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_double)]
+        self._check(f(_ptr(np.ascontiguousarray(cost, dt)), m, n,
+                      _ptr(np.ascontiguousarray(p, dt)), _ptr(np.ascontiguousarray(q, dt)),
+                      eta, tol, max_iters, check_every, _ptr(plan), _ptr(mu), _ptr(nu),
+                      C.byref(rep), C.cast(trace, C.c_void_p), cap, C.byref(tlen),
+                      C.byref(iters), C.byref(status), C.byref(wall)))
+        rows = [{k: getattr(trace[i], k) for k, _ in OrcTraceRow._fields_}
+                for i in range(min(tlen.value, cap))]
+        return SolveOut(plan=plan, mu=mu, nu=nu,
+                        report={k: getattr(rep, k) for k, _ in OrcReport._fields_},
+                        iterations=iters.value, status=STATUS_NAMES[status.value],
+                        trace=rows, wall_time_s=wall.value)
+
     def lp_exact(self, cost, p, q, m, n):
         assert self.kind == "ref"
         f = self._fn("lp_exact")

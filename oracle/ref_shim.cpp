@@ -17,6 +17,7 @@
 //   drot::gen_gaussian_problem probgen.hpp:131-170
 //   drot::CounterRng           rng.hpp:30-106
 //   drot::lp_exact             reference.hpp:537-552
+//   drot::sinkhorn_solve       reference.hpp:165-288
 #include <chrono>
 #include <cstring>
 #include <string>
@@ -80,6 +81,39 @@ void put_report(orc_report* out, const drot::ResidualReport& r) {
   out->r_dual = r.r_dual;
   out->gap = r.gap;
   out->objective = r.objective;
+}
+
+template <class T>
+int sinkhorn_impl(const T* C, int64_t m, int64_t n, const T* p, const T* q, T eta, double tol,
+                  int64_t max_iters, int64_t check_every, T* plan, T* mu, T* nu,
+                  orc_report* rep, orc_trace_row* trace, int64_t trace_cap,
+                  int64_t* trace_len, int64_t* iters, int32_t* status, double* wall) {
+  try {
+    auto pr = to_problem(C, m, n, p, q);
+    auto res = drot::sinkhorn_solve<T>(pr, eta, tol, max_iters, check_every);
+    if (plan) std::memcpy(plan, res.plan.x.data(), sizeof(T) * m * n);
+    if (mu) std::memcpy(mu, res.cert.mu.data(), sizeof(T) * m);
+    if (nu) std::memcpy(nu, res.cert.nu.data(), sizeof(T) * n);
+    put_report(rep, res.report);
+    if (trace_len) *trace_len = static_cast<int64_t>(res.trace.rows.size());
+    if (trace) {
+      const int64_t cnt =
+          std::min<int64_t>(trace_cap, static_cast<int64_t>(res.trace.rows.size()));
+      for (int64_t k = 0; k < cnt; ++k) {
+        const auto& r = res.trace.rows[k];
+        trace[k] = orc_trace_row{r.iter,      r.r_primal,
+                                 r.r_dual,    r.gap,
+                                 r.objective, r.ergodic_objective,
+                                 r.fixed_point_residual};
+      }
+    }
+    if (iters) *iters = res.trace.iterations;
+    if (status) *status = static_cast<int32_t>(res.status);
+    if (wall) *wall = res.trace.wall_time_s;
+    return 0;
+  } catch (const drot::Error& e) {
+    return errc_ret(e);
+  }
 }
 
 template <class T>
@@ -358,6 +392,16 @@ void ref_default_config(orc_config* c) {
     } catch (const drot::Error& e) {                                          \
       return errc_ret(e);                                                     \
     }                                                                         \
+  }                                                                           \
+  int ref_sinkhorn_##SFX(const T* C, int64_t m, int64_t n, const T* p,        \
+                         const T* q, T eta, double tol, int64_t max_iters,    \
+                         int64_t check_every, T* plan, T* mu, T* nu,          \
+                         orc_report* rep, orc_trace_row* trace,               \
+                         int64_t trace_cap, int64_t* trace_len,               \
+                         int64_t* iters, int32_t* status, double* wall) {     \
+    return sinkhorn_impl<T>(C, m, n, p, q, eta, tol, max_iters, check_every,  \
+                            plan, mu, nu, rep, trace, trace_cap, trace_len,   \
+                            iters, status, wall);                             \
   }                                                                           \
   int ref_residual_report_##SFX(const T* C, int64_t m, int64_t n,             \
                                 const T* p, const T* q, const T* plan,        \

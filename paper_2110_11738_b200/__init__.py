@@ -13,7 +13,8 @@ from .api import (DeviceError, DrotConfig, DrotState, DualCertificate, EngineKin
                   SolveResult, SolveStatus, SolveTrace, TilePlan, TraceRow, TransportPlan,
                   TransportProblem, check_problem, drot_step, dyadic_marginal,
                   gen_gaussian_problem, gen_gaussian_problem_as, init_state,
-                  kernel_launches, objective, release_device_cache, plan_tiles, residual_report, counter_uniform, random_matrix, recover_duals, rho0_warmup_preset, solve)
+                  kernel_launches, objective, release_device_cache, plan_tiles, residual_report,
+                  sinkhorn_solve, counter_uniform, random_matrix, recover_duals, rho0_warmup_preset, solve)
 from .session import Session, nccl_unique_id, shard_rows
 
 LIB_PATH = _lib.LIB_PATH
@@ -26,5 +27,5 @@ __all__ = [
     "SolveStatus", "SolveTrace", "TilePlan", "TraceRow", "TransportPlan",
     "TransportProblem", "check_problem", "drot_step", "dyadic_marginal",
     "gen_gaussian_problem", "gen_gaussian_problem_as", "init_state", "kernel_launches",
-    "objective", "release_device_cache", "residual_report", "plan_tiles", "counter_uniform", "random_matrix", "recover_duals", "rho0_warmup_preset", "solve", "Session", "nccl_unique_id", "shard_rows", "LIB_PATH",
+    "objective", "release_device_cache", "residual_report", "sinkhorn_solve", "plan_tiles", "counter_uniform", "random_matrix", "recover_duals", "rho0_warmup_preset", "solve", "Session", "nccl_unique_id", "shard_rows", "LIB_PATH",
 ]

@@ -349,6 +349,46 @@ def solve(problem: TransportProblem, cfg: Optional[DrotConfig] = None,
         status=st)
 
 
+def sinkhorn_solve(problem: TransportProblem, eta: float, tol: float, max_iters: int,
+                   check_every: int = 10, exact_report: bool = False) -> SolveResult:
+    """drot::sinkhorn_solve<T> (reference.hpp:165-288) on the B200: the
+    paper's comparison baseline.  exact_report evaluates the final
+    residual_report in the reference's summation order."""
+    dt = _dtype_of(problem)
+    m, n = problem.m, problem.n
+    if m == 0 or n == 0:
+        raise Error(Errc.empty_dimension, "empty_dimension: cost matrix has an empty dimension")
+    if len(problem.p) != m or len(problem.q) != n:
+        raise Error(Errc.shape_mismatch,
+                    "shape_mismatch: marginal lengths do not match the cost matrix")
+    cm = _cm(problem.cost, dt)
+    pv, qv = _vec(problem.p, dt), _vec(problem.q, dt)
+    plan = np.empty((m, n), dtype=dt, order="F")
+    mu = np.empty(m, dtype=dt)
+    nu = np.empty(n, dtype=dt)
+    rep = drotb_report()
+    ce = max(int(check_every), 1)
+    cap = int(max(int(max_iters), 0) // ce + 2)
+    trace = (drotb_trace_row * cap)()
+    tlen, iters = C.c_int64(0), C.c_int64(0)
+    status, wall = C.c_int32(0), C.c_double(0)
+    _check(getattr(_lib.load(), "drotb_sinkhorn_" + _sfx(dt))(
+        _p(cm), m, n, _p(pv), _p(qv), _ctype(dt)(eta), float(tol), int(max_iters), ce,
+        int(bool(exact_report)), _p(plan), _p(mu), _p(nu), C.byref(rep),
+        C.cast(trace, C.c_void_p), cap, C.byref(tlen), C.byref(iters), C.byref(status),
+        C.byref(wall)))
+    rows = [TraceRow(trace[k].iter, trace[k].r_primal, trace[k].r_dual, trace[k].gap,
+                     trace[k].objective, trace[k].ergodic_objective,
+                     trace[k].fixed_point_residual) for k in range(min(tlen.value, cap))]
+    st = SolveStatus(status.value)
+    return SolveResult(
+        plan=TransportPlan(plan),
+        cert=DualCertificate(mu, nu, float(eta)),
+        report=ResidualReport(rep.r_primal, rep.r_dual, rep.gap, rep.objective),
+        trace=SolveTrace(rows, st, int(iters.value), float(wall.value)),
+        status=st)
+
+
 @dataclass
 class FusedArray:
     """fused.hpp:64-68."""

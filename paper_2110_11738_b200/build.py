@@ -25,7 +25,7 @@ NVCC_FLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
     "-Xcompiler", "-O3", "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include"),
 ]
-SOURCES = ["kernels.cu", "session.cu", "probgen.cpp", "probgen.cu", "report.cu", "persistent.cu", "tail.cu"]
+SOURCES = ["kernels.cu", "session.cu", "probgen.cpp", "probgen.cu", "report.cu", "persistent.cu", "tail.cu", "sinkhorn.cu"]
 HEADERS = ["drotb_internal.hpp", "drotb_host.hpp", "sweep.cuh"]
 
 

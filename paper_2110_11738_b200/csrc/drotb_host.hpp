@@ -4,6 +4,8 @@
 #pragma once
 
 #include <cstdint>
+
+#include <cuda_runtime.h>
 #include <string>
 #include <vector>
 
@@ -37,3 +39,20 @@ template <class T>
 int dyadic_marginal(int64_t len, T* out);
 
 }  // namespace drotb
+
+// Error propagation helpers of the host code (C ABI return codes).
+#define CUDA_TRY(expr)                                                       \
+  do {                                                                       \
+    cudaError_t e_ = (expr);                                                 \
+    if (e_ != cudaSuccess)                                                   \
+      return ::drotb::set_cuda_error(DROTB_ERR_CUDA + static_cast<int>(e_),  \
+                            std::string("cuda: ") + #expr + ": " +           \
+                                cudaGetErrorString(e_));                     \
+  } while (0)
+
+#define RC_TRY(expr)          \
+  do {                        \
+    int rc_ = (expr);         \
+    if (rc_) return rc_;      \
+  } while (0)
+

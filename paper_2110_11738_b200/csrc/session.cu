@@ -93,21 +93,6 @@ int set_cuda_error(int code, const std::string& what) {
 void clear_error() { g_err.clear(); }
 const char* last_error_cstr() { return g_err.c_str(); }
 
-#define CUDA_TRY(expr)                                                       \
-  do {                                                                       \
-    cudaError_t e_ = (expr);                                                 \
-    if (e_ != cudaSuccess)                                                   \
-      return ::drotb::set_cuda_error(DROTB_ERR_CUDA + static_cast<int>(e_),  \
-                            std::string("cuda: ") + #expr + ": " +           \
-                                cudaGetErrorString(e_));                     \
-  } while (0)
-
-#define RC_TRY(expr)          \
-  do {                        \
-    int rc_ = (expr);         \
-    if (rc_) return rc_;      \
-  } while (0)
-
 #define NCCL_TRY(expr)                                                        \
   do {                                                                        \
     ncclResult_t r_ = (expr);                                                 \
