@@ -96,5 +96,8 @@ def test_matches_reference_sinkhorn(drot, ref, dt, shape, eta, tol):
                                    rtol=1e-6 if dt == np.float64 else 1e-2, atol=1e-30)
         for a, b in zip(got.trace.rows, want.trace):
             assert a.iter == b["iter"]
-            assert abs(a.r_primal - b["r_primal"]) <= (1e-6 if dt == np.float64 else 1e-2) * max(
-                b["r_primal"], 1e-300)
+            # fp32: the marginal error bottoms out at the rounding floor of
+            # u * (K v) - p (~1e-9 here), so an absolute term is needed
+            atol = 1e-14 if dt == np.float64 else 1e-8
+            assert abs(a.r_primal - b["r_primal"]) <= (1e-6 if dt == np.float64 else 1e-2) * \
+                b["r_primal"] + atol
