@@ -315,6 +315,9 @@ def run_b200(args, rank, world, local_rank):
         ttt = time_to_tol_c2(args, drot, torch, dist, m, n, m_global, rank, world, local_rank)
         if out is not None:
             out["time_to_tol_c2"] = ttt
+    # ---- the paper's comparison: Sinkhorn per-iteration cost at C2 ----------
+    if world == 1 and rank == 0 and not args.no_sinkhorn:
+        out["sinkhorn_c2"] = sinkhorn_c2(drot, m, n, out["ms_per_step"])
     # ---- config C5 at N = 1: m = n = 100 000 fp32 (X + C = 80 GB) ----------
     if world == 1 and rank == 0 and not args.no_c5:
         out["c5_single_gpu"] = c5_single(args, drot, torch)
@@ -371,6 +374,28 @@ def run_e2e(args, drot, torch, m, n, local_rank):
             "step": f"one drot.solve() call of {S} iterations from pinned host buffers "
                     f"(validation, init, {S} gated iterations, final report, plan/duals/trace "
                     f"download); median of 2 after 1 warm call, {t*1e3:.1f} ms/call"}
+
+
+def sinkhorn_c2(drot, m, n, drot_ms, eta=0.05):
+    """PAPER.md:392-394 compares DROT's and Sinkhorn's per-iteration runtime:
+    drot.sinkhorn_solve (GPU, csrc/sinkhorn.cu) on the C2 instance with an
+    unreachable tolerance, timed as the difference of a 110- and a
+    10-iteration call (uploads and the kernel build cancel out)."""
+    prob = drot.gen_gaussian_problem_as(drot.GaussianSpec(m, n, 5.0, 0), np.float32)
+    prob.p = drot.dyadic_marginal(m, np.float32)
+    prob.q = drot.dyadic_marginal(n, np.float32)
+    walls = {}
+    for k in (10, 110):
+        t0 = time.perf_counter()
+        r = drot.sinkhorn_solve(prob, eta, -1.0, k)
+        walls[k] = time.perf_counter() - t0
+        assert r.trace.iterations == k, r.status
+    ms = (walls[110] - walls[10]) / 100 * 1e3
+    bytes_it = (2 + 1 / 10) * 4 * m * n  # two sweeps per iteration + a check sweep every 10
+    return {"config": f"C2 {m}x{n} fp32, eta={eta}, check_every=10", "ms_per_iteration": ms,
+            "iterations_per_s": 1e3 / ms, "hbm_gbs": bytes_it / (ms / 1e3) / 1e9,
+            "drot_ms_per_iteration": drot_ms, "drot_over_sinkhorn_time": drot_ms / ms,
+            "how": "host wall clock: (110-iteration call - 10-iteration call) / 100"}
 
 
 def c5_single(args, drot, torch, size=100000, iters=20):
@@ -493,6 +518,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ttt", action="store_true")
     ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--no-sinkhorn", action="store_true")
     ap.add_argument("--ttt-max-iters", type=int, default=400000)
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
