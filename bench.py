@@ -318,6 +318,9 @@ def run_b200(args, rank, world, local_rank):
     # ---- the paper's comparison: Sinkhorn per-iteration cost at C2 ----------
     if world == 1 and rank == 0 and not args.no_sinkhorn:
         out["sinkhorn_c2"] = sinkhorn_c2(drot, m, n, out["ms_per_step"])
+    # ---- config C2 in fp64 (the north_star keeps fp32 and fp64) -------------
+    if world == 1 and rank == 0 and not args.no_f64:
+        out["c2_f64"] = c2_f64(drot, torch, m, n)
     # ---- config C5 at N = 1: m = n = 100 000 fp32 (X + C = 80 GB) ----------
     if world == 1 and rank == 0 and not args.no_c5:
         out["c5_single_gpu"] = c5_single(args, drot, torch)
@@ -374,6 +377,25 @@ def run_e2e(args, drot, torch, m, n, local_rank):
             "step": f"one drot.solve() call of {S} iterations from pinned host buffers "
                     f"(validation, init, {S} gated iterations, final report, plan/duals/trace "
                     f"download); median of 2 after 1 warm call, {t*1e3:.1f} ms/call"}
+
+
+def c2_f64(drot, torch, m, n, iters=100):
+    """C2 in fp64: same loop, 24 / 16 bytes per entry on fold / skip sweeps."""
+    s = drot.Session(m, n, np.float64, drot.DrotConfig(tol_primal=-1.0, max_iters=10 ** 12))
+    stream = torch.cuda.current_stream()
+    s.set_stream(stream.cuda_stream)
+    s.gen_gaussian(5.0, 0, "dyadic")
+    s.init()
+    s.enqueue(10)
+    r = s.run_timed(iters)
+    s.close()
+    peak, _ = measured_hbm_peak()
+    sweep = r["pass_ms"] / r["n_pass"]
+    gbs = r["pass_bytes"] / r["n_pass"] / (sweep / 1e3) / 1e9
+    return {"config": f"C2 {m}x{n} fp64 Gaussian seed 0, dyadic-uniform marginals, fast order",
+            "iterations_per_s": iters / (r["total_ms"] / 1e3),
+            "ms_per_iteration": r["total_ms"] / iters, "sweep_ms_avg": sweep,
+            "sweep_gbs": gbs, "sweep_frac_of_peak": gbs / peak}
 
 
 def sinkhorn_c2(drot, m, n, drot_ms, eta=0.05):
@@ -519,6 +541,7 @@ def main():
     ap.add_argument("--no-ttt", action="store_true")
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--no-sinkhorn", action="store_true")
+    ap.add_argument("--no-f64", action="store_true")
     ap.add_argument("--ttt-max-iters", type=int, default=400000)
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
