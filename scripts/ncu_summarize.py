@@ -128,6 +128,7 @@ def main():
     ap.add_argument("--m", type=int, default=10000)
     ap.add_argument("--n", type=int, default=10000)
     ap.add_argument("--dtype", default="f32")
+    ap.add_argument("--key", default=None, help="summary key prefix (default pass / solve)")
     ap.add_argument("--iters-per-launch", type=int, default=0,
                     help="persistent solve_kernel capture: iterations per launch "
                          "(alternating fold / skip sweeps)")
@@ -170,7 +171,8 @@ def main():
                     summ = json.load(f)
             dram = [e["dram_bytes"] for e in ls if "dram_bytes" in e]
             if dram:
-                key = ("solve_" if args.iters_per_launch else "pass_") + f"{args.m}x{args.n}_{args.dtype}"
+                key = (args.key or ("solve" if args.iters_per_launch else "pass")) + \
+                    f"_{args.m}x{args.n}_{args.dtype}"
                 summ[key] = {
                     "tag": args.tag,
                     "dram_bytes_per_launch_avg": sum(dram) / len(dram),
