@@ -111,8 +111,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_PASS_MINB)
   }
 }
 
+#ifndef DROTB_ASYNC_MINB
+#define DROTB_ASYNC_MINB 1  // tuning aid: minimum resident CTAs for the register budget
+#endif
 template <class T, int MODE, bool DUAL, bool DX>
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
+__global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_ASYNC_MINB)
     pass_kernel_async(const PassArgs<T> a) {
   using V = typename V16<T>::type;
   constexpr int R = 16 / sizeof(T);
