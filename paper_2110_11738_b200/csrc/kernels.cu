@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_PASS_MINB)
 }
 
 #ifndef DROTB_ASYNC_MINB
-#define DROTB_ASYNC_MINB 1  // tuning aid: minimum resident CTAs for the register budget
+#define DROTB_ASYNC_MINB 3  // 3 CTAs (12 warps) per SM: caps registers at 170 (r1 tuning)
 #endif
 template <class T, int MODE, bool DUAL, bool DX>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_ASYNC_MINB)
