@@ -388,6 +388,24 @@ int drotb_session_create_sharded(drotb_session** s, int64_t m_global, int64_t n,
                                  const char* nccl_id128, int64_t row_begin,
                                  int64_t row_end);
 
+/* The same row shard with the per-iteration exchange fused into the
+ * cooperative tail kernel over NVLink peer memory (no NCCL): each rank
+ * writes its column partials and scalars straight into every peer's
+ * exchange buffer, raises a generation flag there, and reduces the world
+ * payloads in rank order (bit-identical on every rank).  Setup collectives
+ * (validation, init, confirm report) use the same buffers.  After creation,
+ * exchange the buffers -- drotb_session_exchange_buffer gives this rank's
+ * device pointer (peers in the same process) and CUDA IPC handle (64 bytes,
+ * one process per GPU) -- then call drotb_session_attach_peers on every rank
+ * with all ranks' pointers or handles (rank order; this rank's entry is
+ * ignored) before set_problem / gen_*.  Every later call is collective. */
+int drotb_session_create_sharded_p2p(drotb_session** s, int64_t m_global, int64_t n,
+                                     int32_t precision, const drotb_config* cfg, int32_t rank,
+                                     int32_t world_size, int64_t row_begin, int64_t row_end);
+int drotb_session_exchange_buffer(drotb_session* s, uint64_t* dev_ptr, char* ipc_handle64);
+int drotb_session_attach_peers(drotb_session* s, const uint64_t* dev_ptrs,
+                               const char* ipc_handles);
+
 #ifdef __cplusplus
 }
 #endif

@@ -124,6 +124,10 @@ SIGNATURES = {
     "drotb_session_run_timed": (C.c_int, [vp, i64, P(f64), P(f64), P(i64), P(f64), P(i64)]),
     "drotb_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "drotb_shard_rows": (C.c_int, [i64, i32, i32, P(i64), P(i64)]),
+    "drotb_session_create_sharded_p2p": (C.c_int, [P(vp), i64, i64, i32, P(drotb_config), i32,
+                                                   i32, i64, i64]),
+    "drotb_session_exchange_buffer": (C.c_int, [vp, P(u64), C.c_char_p]),
+    "drotb_session_attach_peers": (C.c_int, [vp, vp, C.c_char_p]),
     "drotb_session_create_sharded": (C.c_int, [P(vp), i64, i64, i32, P(drotb_config), i32, i32,
                                                C.c_char_p, i64, i64]),
 }

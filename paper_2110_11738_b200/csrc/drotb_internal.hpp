@@ -201,6 +201,45 @@ int tail_grid(int device);
 template <class T>
 cudaError_t launch_tail(const TailArgs<T>& t, T* cpart, double* dpart, unsigned* bar, int grid,
                         cudaStream_t st);
+// Row-shard exchange over NVLink peer memory (tail.cu): every rank owns one
+// exchange buffer, mapped by every peer (CUDA IPC across processes, plain
+// device pointers within one):
+//   [0, 256)          iteration flags: uint64 generation per sending rank
+//   [256, 512)        setup-collective flags
+//   [512, ...)        2 parity buffers x world slots of slot_bytes: slot s
+//                     holds rank s's payload [v partial: n T, 16-B aligned |
+//                     16 doubles of scalars]
+//   [setup_off, ...)  2 parity buffers x world slots of setup_bytes
+// peers[r] = rank r's buffer as mapped here (peers[rank] = own buffer).
+struct XArgs {
+  char* const* peers;   // device array [world]
+  int32_t world, rank;
+  int64_t vec_bytes;    // round_up(n * sizeof(T), 16)
+  int64_t slot_bytes;   // vec_bytes + 16 * 8
+  int64_t buf_bytes;    // world * slot_bytes
+};
+constexpr int64_t kXIterOff = 512;
+constexpr int64_t kXSetupFlagOff = 256;
+
+// setup collective over the same buffers: out[i] = op_r in[r][i] in rank
+// order (op 0 = sum, 1 = max); U in {float, double, int32}; one CTA
+template <class U>
+void launch_xallreduce(const U* in, U* out, int64_t count, int op, char* const* peers,
+                       int world, int rank, int64_t setup_off, int64_t setup_bytes,
+                       unsigned long long gen, cudaStream_t st);
+
+template <class T>
+cudaError_t launch_shard_tail(const TailArgs<T>& t, T* cpart, double* dpart, unsigned* bar,
+                              const XArgs& x, int grid, cudaStream_t st);
+// pause / finish: local row-side pending sums -> out4 (for an allreduce), then
+// patch with the global row part and the local (replicated) column part
+template <class T>
+void launch_shard_pending_local(const TailArgs<T>& t, const double* dpart, int grid,
+                                double* out4, cudaStream_t st);
+template <class T>
+void launch_shard_pending_patch(const TailArgs<T>& t, const double* dpart, int grid,
+                                const double* glob4, cudaStream_t st);
+
 // patch the pending exact dual value / fixed-point residual (end of a run)
 template <class T>
 void launch_tail_finalize(const TailArgs<T>& t, const double* dpart, int grid, cudaStream_t st);

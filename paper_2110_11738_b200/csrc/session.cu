@@ -141,6 +141,16 @@ struct Session {
   cudaEvent_t ev[2] = {nullptr, nullptr};
 
   // row sharding (multi-GPU): this rank holds rows [row_begin, row_begin+m)
+  // exchange: 0 = NCCL allreduces (per-launch kernels), 1 = NVLink peer
+  // memory fused into the cooperative tail (tail.cu shard_tail_kernel)
+  int xmode = 0;
+  char* xbuf = nullptr;            // this rank's exchange buffer (see XArgs)
+  int64_t xbytes = 0, xsetup_off = 0, xsetup_bytes = 0;
+  char** d_xpeers = nullptr;       // device array of the peers' buffers
+  std::vector<void*> xopened;      // IPC mappings to close
+  XArgs xa{};
+  bool x_attached = false;
+  unsigned long long xsetup_gen = 0;
   int rank = 0, world = 1;
   bool sharded = false;
   ncclComm_t comm = nullptr;
@@ -205,6 +215,13 @@ struct Session {
     persist = false;
     if (comm) nccl().commDestroy(comm);
     comm = nullptr;
+    for (void* ptr : xopened) cudaIpcCloseMemHandle(ptr);
+    xopened.clear();
+    if (xbuf) cudaFree(xbuf);
+    if (d_xpeers) cudaFree(d_xpeers);
+    xbuf = nullptr;
+    d_xpeers = nullptr;
+    x_attached = false;
     pack = pmax = nullptr;
     dpack = nullptr;
     dint = nullptr;
@@ -425,16 +442,19 @@ struct Session {
   // Row shard [row_begin, row_end) of an m_global x n problem on `world`
   // ranks (one process per GPU); collectives over NCCL.
   int create_sharded(int64_t m_glob, int64_t n_, const drotb_config& c, int rk, int ws,
-                     const char* id128, int64_t r0, int64_t r1) {
+                     const char* id128, int64_t r0, int64_t r1, int exchange = 0) {
     if (ws < 1 || rk < 0 || rk >= ws || r0 < 0 || r1 <= r0 || r1 > m_glob)
       return set_error(DROTB_ERRC_BAD_CONFIG, "invalid shard");
     if (c.order == DROTB_ORDER_REFERENCE)
       return set_error(DROTB_ERRC_BAD_CONFIG,
                        "order=reference reproduces the single-threaded CPU tree; "
                        "row sharding needs order=fast");
-    if (!nccl().ok) return set_error(DROTB_ERRC_BAD_CONFIG, "NCCL unavailable: " + nccl().err);
+    if (exchange == 1 && ws > 32)
+      return set_error(DROTB_ERRC_BAD_CONFIG, "peer-memory exchange supports <= 32 ranks");
+    if (exchange == 0 && !nccl().ok)
+      return set_error(DROTB_ERRC_BAD_CONFIG, "NCCL unavailable: " + nccl().err);
     drotb_config c2 = c;
-    c2.use_graphs = 0;  // sharded iterations are enqueued eagerly (NCCL + pause)
+    if (exchange == 0) c2.use_graphs = 0;  // NCCL iterations are enqueued eagerly (+ pause)
     no_persist = true;  // the persistent kernel has no collective phase
     RC_TRY(create(r1 - r0, n_, c2));
     m_global = m_glob;
@@ -446,14 +466,69 @@ struct Session {
     RC_TRY(dev_alloc(&pmax, 2));
     RC_TRY(dev_alloc(&dpack, 16));
     RC_TRY(dev_alloc(&dint, 2));
+    if (exchange == 1) {
+      xmode = 1;
+      RC_TRY(setup_coop_tail());
+      if (!coop) return set_error(DROTB_ERRC_BAD_CONFIG, "cooperative tail unavailable");
+      fused_gate = true;
+      const int64_t vec = round_up(static_cast<int64_t>(sizeof(T)) * n, 16);
+      xa.vec_bytes = vec;
+      xa.slot_bytes = vec + 16 * 8;
+      xa.buf_bytes = world * xa.slot_bytes;
+      xa.world = world;
+      xa.rank = rank;
+      xsetup_bytes = round_up(std::max<int64_t>(n, 32) * 8, 16);
+      xsetup_off = kXIterOff + 2 * xa.buf_bytes;
+      xbytes = xsetup_off + 2 * world * xsetup_bytes;
+      CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&xbuf), static_cast<size_t>(xbytes)));
+      CUDA_TRY(cudaMemset(xbuf, 0, static_cast<size_t>(xbytes)));
+      return 0;
+    }
     ncclUniqueId id;
     std::memcpy(&id, id128, sizeof(id));
     NCCL_TRY(nccl().commInitRank(&comm, world, id, rank));
     return 0;
   }
 
+  // peers: device pointers of the peers' exchange buffers in this process
+  // (ptrs, e.g. sessions of one process on one or several GPUs) or CUDA IPC
+  // handles (handles, world x 64 bytes; one process per GPU)
+  int attach_peers(const uint64_t* ptrs, const char* handles) {
+    if (xmode != 1) return set_error(DROTB_ERRC_BAD_CONFIG, "session has no peer exchange");
+    std::vector<char*> pv(static_cast<size_t>(world), nullptr);
+    for (int r = 0; r < world; ++r) {
+      if (r == rank) {
+        pv[r] = xbuf;
+      } else if (ptrs) {
+        pv[r] = reinterpret_cast<char*>(ptrs[r]);
+      } else {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handles + 64 * r, sizeof(h));
+        void* ptr = nullptr;
+        CUDA_TRY(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+        xopened.push_back(ptr);
+        pv[r] = static_cast<char*>(ptr);
+      }
+    }
+    if (!d_xpeers) RC_TRY(dev_alloc(&d_xpeers, static_cast<size_t>(world)));
+    CUDA_TRY(cudaMemcpy(d_xpeers, pv.data(), sizeof(char*) * world, cudaMemcpyHostToDevice));
+    xa.peers = d_xpeers;
+    x_attached = true;
+    return 0;
+  }
+
   template <class U>
   int allreduce(U* buf, size_t count, ncclRedOp_t op) {
+    if (xmode == 1) {  // setup collective over the peer buffers (no NCCL)
+      if (!x_attached) return set_error(DROTB_ERRC_BAD_CONFIG, "peers not attached");
+      if (static_cast<int64_t>(count * sizeof(U)) > xsetup_bytes)
+        return set_error(DROTB_ERRC_BAD_CONFIG, "setup collective too large");
+      launch_xallreduce<U>(buf, buf, static_cast<int64_t>(count), op == ncclMax ? 1 : 0,
+                           d_xpeers, world, rank, xsetup_off, xsetup_bytes, ++xsetup_gen,
+                           stream);
+      CUDA_TRY(cudaGetLastError());
+      return 0;
+    }
     ncclDataType_t dt = std::is_same<U, double>::value  ? ncclFloat64
                         : std::is_same<U, float>::value ? ncclFloat32
                                                         : ncclInt32;
@@ -683,6 +758,10 @@ struct Session {
   int init(const T* x0, bool x0_is_device = false) {
     if (!have_problem) return set_error(DROTB_ERRC_BAD_CONFIG, "no problem set");
     RC_TRY(resolve_rho());
+    if (xmode == 1) {  // iteration generations restart at 1 (before any collective)
+      if (!x_attached) return set_error(DROTB_ERRC_BAD_CONFIG, "peers not attached");
+      CUDA_TRY(cudaMemsetAsync(xbuf, 0, kXSetupFlagOff, stream));
+    }
     if (x0) {
       RC_TRY(upload_matrix(X, x0, x0_is_device));
       unsigned long long nf, ng;
@@ -750,6 +829,12 @@ struct Session {
       double sp = 0, sq = 0;
       for (T e : hp) sp += static_cast<double>(e);
       for (T e : hq) sq += static_cast<double>(e);
+      if (sharded) {  // global sum p (rank-local rows)
+        CUDA_TRY(cudaMemcpyAsync(dpack + 11, &sp, sizeof(double), cudaMemcpyHostToDevice, stream));
+        RC_TRY(allreduce(dpack + 11, 1, ncclSum));
+        CUDA_TRY(cudaMemcpyAsync(&sp, dpack + 11, sizeof(double), cudaMemcpyDeviceToHost, stream));
+        CUDA_TRY(cudaStreamSynchronize(stream));
+      }
       hb.sum_p = sp;
       hb.sum_q = sq;
     }
@@ -883,6 +968,12 @@ struct Session {
     launch_pass<T>(pa, mode, want_dual, want_dx, stream);
     if (pass_end) CUDA_TRY(cudaEventRecordWithFlags(pass_end, stream, evf));
     TailArgs<T> ta = tail_args(k, mode, folded_after, true);
+    if (sharded && xmode == 1) {  // K1 + the tail with the fused peer exchange
+      CUDA_TRY(launch_shard_tail<T>(ta, tcpart, tdpart, tbar, xa, tgrid, stream));
+      h_iter = k + 1;
+      h_folded = folded_after;
+      return 0;
+    }
     if (coop && !exact && !sharded) {  // K1 + one cooperative tail kernel (tail.cu)
       CUDA_TRY(launch_tail<T>(ta, tcpart, tdpart, tbar, tgrid, stream));
       h_iter = k + 1;
@@ -1018,8 +1109,8 @@ struct Session {
   }
 
   bool graph_ok(int64_t len) const {
-    return !sharded && cfg.use_graphs && (!coop || coop_graphs) && len >= 2 && (len & 1) == 0 &&
-           (h_iter & 1) == 0 && !h_folded;
+    return (!sharded || xmode == 1) && cfg.use_graphs && (!coop || coop_graphs) && len >= 2 &&
+           (len & 1) == 0 && (h_iter & 1) == 0 && !h_folded;
   }
 
   int enqueue(int64_t n_iters) {
@@ -1151,7 +1242,19 @@ struct Session {
   // GPU queue never drains.
   // Sharded confirm after a gate pause (stop == 2): the exact report's sums
   // over all ranks, then the replicated decision (stop -> 1 or back to 0).
+  // p2p shards: the last iteration's exact dual value / trace terms (the
+  // row part is summed over the ranks, the column part is replicated)
+  int shard_patch_pending() {
+    TailArgs<T> ta = tail_args(h_iter, kFold, h_folded, true);
+    launch_shard_pending_local<T>(ta, tdpart, tgrid, dpack, stream);
+    RC_TRY(allreduce(dpack, 4, ncclSum));
+    launch_shard_pending_patch<T>(ta, tdpart, tgrid, dpack, stream);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
+
   int sharded_report(bool always) {
+    if (xmode == 1) RC_TRY(shard_patch_pending());
     Book<T> hb;
     RC_TRY(read_book(&hb));
     TailArgs<T> ta = tail_args(hb.iter, kPlain0, hb.folded != 0, true);
@@ -1217,6 +1320,7 @@ struct Session {
   // Final status and report (solver.hpp:527-538).
   int finalize_pending() {  // coop tail: patch the last iteration's exact dual / trace terms
     if (!coop || !tdpart) return 0;
+    if (sharded) return xmode == 1 ? shard_patch_pending() : 0;
     TailArgs<T> ta = tail_args(h_iter, kFold, h_folded, true);
     launch_tail_finalize<T>(ta, tdpart, tgrid, stream);
     CUDA_TRY(cudaGetLastError());
@@ -2159,6 +2263,57 @@ int drotb_session_create_sharded(drotb_session** s, int64_t m_global, int64_t n,
   } catch (const std::exception& e) {
     return guard_exceptions(e);
   }
+}
+
+int drotb_session_create_sharded_p2p(drotb_session** s, int64_t m_global, int64_t n,
+                                     int32_t precision, const drotb_config* cfgp, int32_t rank,
+                                     int32_t world_size, int64_t row_begin, int64_t row_end) {
+  drotb::clear_error();
+  *s = nullptr;
+  const drotb_config cfg = effective(cfgp);
+  try {
+    std::unique_ptr<drotb_session> h(new drotb_session{precision, nullptr});
+    if (precision == 0) {
+      std::unique_ptr<Session<float>> ss(new Session<float>());
+      RC_TRY(ss->create_sharded(m_global, n, cfg, rank, world_size, nullptr, row_begin, row_end,
+                                1));
+      h->impl = ss.release();
+    } else {
+      std::unique_ptr<Session<double>> ss(new Session<double>());
+      RC_TRY(ss->create_sharded(m_global, n, cfg, rank, world_size, nullptr, row_begin, row_end,
+                                1));
+      h->impl = ss.release();
+    }
+    *s = h.release();
+    return 0;
+  } catch (const std::exception& e) {
+    return guard_exceptions(e);
+  }
+}
+
+int drotb_session_exchange_buffer(drotb_session* s, uint64_t* dev_ptr, char* ipc_handle64) {
+  drotb::clear_error();
+  auto go = [&](auto* ss) -> int {
+    if (ss->xmode != 1 || !ss->xbuf)
+      return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "session has no peer exchange");
+    if (dev_ptr) *dev_ptr = reinterpret_cast<uint64_t>(ss->xbuf);
+    if (ipc_handle64) {
+      cudaIpcMemHandle_t h;
+      CUDA_TRY(cudaIpcGetMemHandle(&h, ss->xbuf));
+      std::memcpy(ipc_handle64, &h, 64);
+    }
+    return 0;
+  };
+  if (s->precision == 0) return go(drotb::as_session<float>(s->impl));
+  return go(drotb::as_session<double>(s->impl));
+}
+
+int drotb_session_attach_peers(drotb_session* s, const uint64_t* dev_ptrs,
+                               const char* ipc_handles) {
+  drotb::clear_error();
+  if (!dev_ptrs && !ipc_handles)
+    return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "attach_peers: no pointers or handles");
+  return DROTB_DISPATCH(s, attach_peers(dev_ptrs, ipc_handles));
 }
 
 int drotb_shard_rows(int64_t m, int32_t world_size, int32_t rank, int64_t* row_begin,

@@ -575,6 +575,436 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// Row shards: the per-iteration exchange fused into the tail over NVLink
+// peer memory (no NCCL in the iteration loop).
+//
+//   A  local merge: r (local rows), the local column partial of v -- written
+//      straight into slot `rank` of EVERY peer's receive buffer (NVLink
+//      stores) -- and the local scalar partials
+//   -- reduce-barrier; its last CTA writes the 16 scalar payload doubles to
+//      every peer, fences at system scope, raises its generation flag on
+//      every peer (st.release.sys) and waits until all `world` flags of its
+//      own buffer reach this iteration (ld.acquire.sys) --
+//   B  v_j = sum over ranks r = 0..world-1 of slot r (a FIXED order: every
+//      rank computes bit-identical column sums, independent of timing),
+//      s = v - q (replicated), closed-form dual column terms
+//   -- reduce-barrier: global scalars (payloads summed in rank order),
+//      recursions, patch of the previous trace row, fused gate (a fire
+//      pauses the loop for the collective confirm report, stop = 2) --
+//   C  phi (local rows), varphi (all columns, replicated), a, b, pending
+//      update partials (row part travels in the next payload)
+//
+// Receive buffers alternate with the iteration parity: a rank can run at
+// most one exchange ahead of any peer (it cannot pass the next flag wait
+// before that peer has consumed the previous buffer), so two suffice.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ char* xslot(const XArgs& x, int peer, int buf, int slot) {
+  return x.peers[peer] + kXIterOff + buf * x.buf_bytes + slot * x.slot_bytes;
+}
+
+// Setup collectives (init sums, error agreement, confirm report): one CTA
+// writes this rank's vector into slot `rank` of every peer, raises its
+// setup flag there and reduces the world slots of its own buffer in rank
+// order once every flag reached `gen`.  Parity buffers as for the iteration
+// exchange.
+template <class U>
+__global__ void __launch_bounds__(1024) xallreduce_kernel(const U* in, U* out, int64_t count,
+                                                          int op, char* const* peers, int world,
+                                                          int rank, int64_t setup_off,
+                                                          int64_t setup_bytes,
+                                                          unsigned long long gen) {
+  const int pb = static_cast<int>(gen & 1);
+  for (int64_t i = threadIdx.x; i < count; i += blockDim.x) {
+    const U v = in[i];
+    for (int r = 0; r < world; ++r)
+      reinterpret_cast<U*>(peers[r] + setup_off + (pb * world + rank) * setup_bytes)[i] = v;
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < world; ++r)
+      st_release_sys_u64(reinterpret_cast<unsigned long long*>(peers[r] + kXSetupFlagOff) + rank,
+                         gen);
+    const unsigned long long* mine =
+        reinterpret_cast<const unsigned long long*>(peers[rank] + kXSetupFlagOff);
+    for (int r = 0; r < world; ++r)
+      while (ld_acquire_sys_u64(mine + r) < gen) {
+      }
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < count; i += blockDim.x) {
+    U acc = U(0);
+    for (int r = 0; r < world; ++r) {
+      const U v = *reinterpret_cast<volatile const U*>(
+          reinterpret_cast<const U*>(peers[rank] + setup_off + (pb * world + r) * setup_bytes) + i);
+      acc = (r == 0) ? v : (op == 0 ? acc + v : (v > acc ? v : acc));
+    }
+    out[i] = acc;
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kTT) shard_tail_kernel(const TailArgs<T> t, T* cpart,
+                                                         double* dpart, unsigned* bar,
+                                                         const XArgs x) {
+  Book<T>* bk = t.book;
+  if (*reinterpret_cast<volatile int*>(&bk->stop)) return;
+  __shared__ T red[kTW][32];
+  __shared__ Book<T> sbk;
+  __shared__ T shT[16 * kTW];
+  __shared__ double shD[16 * kTW];
+  __shared__ unsigned s_gen0;
+  __shared__ long long s_k;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x;
+  const int64_t m = t.m, n = t.n;
+  if (tid == 0) {
+    s_gen0 = ld_acquire(bar + 1);
+    s_k = *reinterpret_cast<volatile long long*>(&bk->iter);
+  }
+  __syncthreads();
+  unsigned my_gen = s_gen0;
+  const int64_t k = s_k;
+  const int pb = static_cast<int>(k & 1);
+  const unsigned long long gen = static_cast<unsigned long long>(k + 1);
+
+  // ---- A: local merge; v partials go straight to every peer ---------------
+  {
+    T pr[3] = {T(0), T(0), T(0)};
+    double pd[2] = {0, 0};
+    const int64_t ngr = (m + 31) / 32, ngc = (n + 31) / 32;
+    for (int64_t grp = blockIdx.x; grp < ngr + ngc; grp += G) {
+      T acc = T(0);
+      if (grp < ngr) {
+        const int64_t idx = grp * 32 + lane;
+        if (idx < m) {
+          int64_t g = warp;
+          for (; g + 7 * kTW < t.grid_cols; g += 8 * kTW) {
+            T v8[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v8[q] = t.ustrip[(g + q * kTW) * t.ld + idx];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc += v8[q];
+          }
+          for (; g < t.grid_cols; g += kTW) acc += t.ustrip[g * t.ld + idx];
+        }
+      } else {
+        const int64_t j = (grp - ngr) * 32 + lane;
+        if (j < n) {
+          int64_t g = warp;
+          for (; g + 7 * kTW < t.grid_rows64; g += 8 * kTW) {
+            T v8[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v8[q] = t.vstrip[(g + q * kTW) * n + j];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc += v8[q];
+          }
+          for (; g < t.grid_rows64; g += kTW) acc += t.vstrip[g * n + j];
+        }
+      }
+      red[warp][lane] = acc;
+      __syncthreads();
+      if (warp == 0) {
+        T tot = T(0);
+#pragma unroll
+        for (int w = 0; w < kTW; ++w) tot += red[w][lane];
+        if (grp < ngr) {
+          const int64_t idx = grp * 32 + lane;
+          if (idx < m) {
+            const T pi = t.p[idx];
+            const T r = tot - pi;
+            t.r_new[idx] = r;
+            pr[0] += r;
+            pr[1] += r * r;
+            pd[0] += static_cast<double>(pi) * static_cast<double>(t.a[idx]);
+            pd[1] += static_cast<double>(pi) * static_cast<double>(r);
+          }
+        } else {
+          const int64_t j = (grp - ngr) * 32 + lane;
+          if (j < n)
+            for (int r = 0; r < x.world; ++r)
+              reinterpret_cast<T*>(xslot(x, r, pb, x.rank))[j] = tot;
+        }
+      }
+      __syncthreads();
+    }
+    __threadfence_system();  // this CTA's peer stores before its arrival
+    const int64_t np = t.n_pass_partials;
+    const int64_t k0 = static_cast<int64_t>(blockIdx.x) * np / G;
+    const int64_t k1 = static_cast<int64_t>(blockIdx.x + 1) * np / G;
+    T ps[4] = {T(0), T(0), T(0), T(0)};
+    T mx = T(0), bad = T(0);
+    for (int64_t q = k0 + tid; q < k1; q += kTT) {
+      const PassPartial<T> sc = t.pass_partials[q];
+      ps[0] += sc.cost;
+      ps[1] += sc.prev;
+      ps[2] += sc.dual;
+      ps[3] += sc.dx;
+      mx = fmax(mx, sc.max_abs);
+      bad += sc.bad ? T(1) : T(0);
+    }
+    mx = warp_max(mx);
+    if (lane == 0) shT[warp] = mx;
+    __syncthreads();
+    T cmx = T(0);
+#pragma unroll
+    for (int w = 0; w < kTW; ++w) cmx = fmax(cmx, shT[w]);
+    __syncthreads();
+    T v8[8] = {ps[0], ps[1], ps[2], ps[3], bad, pr[0], pr[1], pr[2]};
+    store_partials<T, 8>(v8, cpart, 0, shT);
+    if (tid == 0) cpart[blockIdx.x * kTSlots + 8] = cmx;
+    store_partials<double, 2>(pd, dpart, 10, shD);
+  }
+  reduce_barrier(bar, my_gen, [&] {
+    // local totals -> the 16-double scalar payload of this rank
+    const bool pend = *reinterpret_cast<volatile int*>(&bk->pend_valid) != 0;
+    T acc[8];
+    double dd[6];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = T(0);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) dd[q] = 0.0;
+    T m1 = T(0);
+    for (int b = tid; b < G; b += kTT) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] += __ldcg(cpart + b * kTSlots + q);
+      m1 = fmax(m1, __ldcg(cpart + b * kTSlots + 8));
+#pragma unroll
+      for (int q = 0; q < 2; ++q) dd[q] += __ldcg(dpart + b * kTSlots + 10 + q);
+      if (pend)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dd[2 + q] += __ldcg(dpart + b * kTSlots + q);  // row part
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = warp_sum(acc[q]);
+    m1 = warp_max(m1);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) dd[q] = warp_sum(dd[q]);
+    if (lane == 0) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) shT[q * kTW + warp] = acc[q];
+      shT[8 * kTW + warp] = m1;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) shD[q * kTW + warp] = dd[q];
+    }
+    __syncthreads();
+    __shared__ double payload[16];
+    if (tid < 16) {
+      double v = 0.0;
+      if (tid < 8) {
+        T sum = T(0);
+#pragma unroll
+        for (int w = 0; w < kTW; ++w) sum += shT[tid * kTW + w];
+        v = static_cast<double>(sum);  // cost prev dual dx bad sum_r |r|^2 |s|^2(unused)
+      } else if (tid == 8) {
+        T mm = T(0);
+#pragma unroll
+        for (int w = 0; w < kTW; ++w) mm = fmax(mm, shT[8 * kTW + w]);
+        v = static_cast<double>(mm);
+      } else if (tid < 15) {
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < kTW; ++w) sum += shD[(tid - 9) * kTW + w];
+        v = sum;  // 9: sum p a, 10: sum p r, 11..14: pending row part
+      }
+      payload[tid] = v;
+    }
+    __syncthreads();
+    if (tid < 16)
+      for (int r = 0; r < x.world; ++r)
+        reinterpret_cast<double*>(xslot(x, r, pb, x.rank) + x.vec_bytes)[tid] = payload[tid];
+    __threadfence_system();
+    __syncthreads();
+    if (tid == 0) {
+      for (int r = 0; r < x.world; ++r)
+        st_release_sys_u64(reinterpret_cast<unsigned long long*>(x.peers[r]) + x.rank, gen);
+      const unsigned long long* mine = reinterpret_cast<const unsigned long long*>(x.peers[x.rank]);
+      for (int r = 0; r < x.world; ++r)
+        while (ld_acquire_sys_u64(mine + r) < gen) {
+        }
+    }
+    __syncthreads();
+  });
+
+  // ---- B: global column sums in rank order; s = v - q (replicated) --------
+  {
+    T ps2 = T(0);
+    double pq[2] = {0, 0};
+    for (int64_t j = static_cast<int64_t>(blockIdx.x) * kTT + tid; j < n;
+         j += static_cast<int64_t>(G) * kTT) {
+      T v = T(0);
+      for (int r = 0; r < x.world; ++r)
+        v += __ldcg(reinterpret_cast<const T*>(xslot(x, x.rank, pb, r)) + j);
+      const T qj = t.q[j];
+      const T sv = v - qj;
+      t.s_new[j] = sv;
+      ps2 += sv * sv;
+      pq[0] += static_cast<double>(qj) * static_cast<double>(t.b[j]);
+      pq[1] += static_cast<double>(qj) * static_cast<double>(sv);
+    }
+    T one[1] = {ps2};
+    store_partials<T, 1>(one, cpart, 9, shT);
+    store_partials<double, 2>(pq, dpart, 14, shD);
+  }
+  reduce_barrier(bar, my_gen, [&] {
+    constexpr int BW = static_cast<int>(sizeof(Book<T>) / 8);
+    unsigned long long bw = tid < BW ? __ldcg(reinterpret_cast<const unsigned long long*>(bk) + tid)
+                                     : 0ull;
+    T s2 = T(0);
+    double dc[6] = {0, 0, 0, 0, 0, 0};  // q.b, q.s, pending column part (4)
+    for (int b = tid; b < G; b += kTT) {
+      s2 += __ldcg(cpart + b * kTSlots + 9);
+      dc[0] += __ldcg(dpart + b * kTSlots + 14);
+      dc[1] += __ldcg(dpart + b * kTSlots + 15);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dc[2 + q] += __ldcg(dpart + b * kTSlots + 4 + q);
+    }
+    if (tid < BW) reinterpret_cast<unsigned long long*>(&sbk)[tid] = bw;
+    s2 = warp_sum(s2);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) dc[q] = warp_sum(dc[q]);
+    if (lane == 0) {
+      shT[warp] = s2;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) shD[q * kTW + warp] = dc[q];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      T ss = T(0);
+#pragma unroll
+      for (int w = 0; w < kTW; ++w) ss += shT[w];
+      double c6[6];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < kTW; ++w) sum += shD[q * kTW + w];
+        c6[q] = sum;
+      }
+      // global scalars: the ranks' payloads summed in rank order
+      double g16[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) g16[q] = 0.0;
+      double gmax = 0.0;
+      for (int r = 0; r < x.world; ++r) {
+        const double* pl =
+            reinterpret_cast<const double*>(xslot(x, x.rank, pb, r) + x.vec_bytes);
+        for (int q = 0; q < 16; ++q) {
+          const double v = __ldcg(pl + q);
+          if (q == 8)
+            gmax = fmax(gmax, v);
+          else
+            g16[q] += v;
+        }
+      }
+      // the previous iteration's exact dual value / fixed-point terms
+      const double d8[8] = {g16[11], g16[12], g16[13], g16[14], c6[2], c6[3], c6[4], c6[5]};
+      patch_pending<T>(&sbk, t, d8);
+      const T tot[8] = {static_cast<T>(g16[0]), static_cast<T>(g16[1]), static_cast<T>(g16[2]),
+                        static_cast<T>(g16[3]), static_cast<T>(gmax),   static_cast<T>(g16[5]),
+                        static_cast<T>(g16[6]), ss};
+      merge_scalars<T>(&sbk, t, tot, g16[4] > 0.0 ? 1 : 0);
+      if (!sbk.stop) {
+        const double coef = static_cast<double>(sbk.coef);
+        const double inv_n = 1.0 / static_cast<double>(t.n_global);
+        const double inv_m = 1.0 / static_cast<double>(t.m_global);
+        const double dual_alg = ((g16[9] - 2.0 * g16[10] + coef * sbk.sum_p) * inv_n +
+                                 (c6[0] - 2.0 * c6[1] + coef * sbk.sum_q) * inv_m) /
+                                static_cast<double>(t.rho);
+        gate_fused<T>(&sbk, t, dual_alg);
+        if (sbk.confirm && !sbk.stop) sbk.stop = 2;  // pause: collective confirm on the host
+      }
+    }
+    book_store(bk, &sbk);
+  });
+  if (*reinterpret_cast<volatile int*>(&bk->failed)) return;
+
+  // ---- C: phi (local rows), varphi (all columns), a, b + pending partials ---
+  {
+    const T coef = *reinterpret_cast<volatile T*>(&bk->coef);
+    const T inv_n = T(1) / static_cast<T>(t.n_global);
+    const T inv_m = T(1) / static_cast<T>(t.m_global);
+    const double drho = static_cast<double>(t.rho);
+    const bool fp = bk->record_trace != 0;
+    double part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const int64_t TT = static_cast<int64_t>(G) * kTT;
+    for (int64_t idx = static_cast<int64_t>(blockIdx.x) * kTT + tid; idx < m + n; idx += TT) {
+      if (idx < m) {
+        const T r = __ldcg(t.r_new + idx);
+        const T ph_old = t.phi[idx];
+        const T ai = t.a[idx];
+        const T ph = (ai - T(2) * r + coef) * inv_n;  // solver.hpp:280-282
+        t.phi[idx] = ph;
+        t.a[idx] = ai - r;  // solver.hpp:287
+        part[0] += static_cast<double>(t.p[idx]) * static_cast<double>(ph) / drho;
+        if (fp) {
+          const double d = static_cast<double>(ph) - static_cast<double>(ph_old);
+          part[1] += d * d;
+          part[2] += d;
+          part[3] += d * (static_cast<double>(r) - static_cast<double>(t.r_old[idx]));
+        }
+      } else {
+        const int64_t j = idx - m;
+        const T sv = __ldcg(t.s_new + j);
+        const T vp_old = t.varphi[j];
+        const T bj = t.b[j];
+        const T vp = (bj - T(2) * sv + coef) * inv_m;  // solver.hpp:283-285
+        t.varphi[j] = vp;
+        t.b[j] = bj - sv;  // solver.hpp:288
+        part[4] += static_cast<double>(t.q[j]) * static_cast<double>(vp) / drho;
+        if (fp) {
+          const double d = static_cast<double>(vp) - static_cast<double>(vp_old);
+          part[5] += d * d;
+          part[6] += d;
+          part[7] += d * (static_cast<double>(sv) - static_cast<double>(t.s_old[j]));
+        }
+      }
+    }
+    store_partials<double, 8>(part, dpart, 0, shD);
+  }
+}
+
+// pause / finish helpers: the pending update partials of the last iteration
+template <class T>
+__global__ void __launch_bounds__(kTT) shard_pending_local_kernel(const TailArgs<T> t,
+                                                                  const double* dpart, int G,
+                                                                  double* out4) {
+  __shared__ double shD[16 * kTW];
+  Book<T>* bk = t.book;
+  const bool pend = *reinterpret_cast<volatile int*>(&bk->pend_valid) != 0;
+  double d4[4];
+  totals<double, 4>(dpart, G, 0, d4, shD);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < 4; ++q) out4[q] = pend ? d4[q] : 0.0;
+}
+
+template <class T>
+__global__ void __launch_bounds__(kTT) shard_pending_patch_kernel(const TailArgs<T> t,
+                                                                  const double* dpart, int G,
+                                                                  const double* glob4) {
+  __shared__ double shD[16 * kTW];
+  Book<T>* bk = t.book;
+  if (!*reinterpret_cast<volatile int*>(&bk->pend_valid)) return;
+  double c4[4];
+  totals<double, 4>(dpart, G, 4, c4, shD);
+  if (threadIdx.x == 0) {
+    Book<T> lb = *bk;
+    const double d8[8] = {glob4[0], glob4[1], glob4[2], glob4[3], c4[0], c4[1], c4[2], c4[3]};
+    patch_pending<T>(&lb, t, d8);
+    *bk = lb;
+  }
+}
+
 template <class T>
 __global__ void __launch_bounds__(kTT) tail_finalize_kernel(const TailArgs<T> t,
                                                             const double* dpart, int G) {
@@ -617,6 +1047,65 @@ cudaError_t launch_tail(const TailArgs<T>& t, T* cpart, double* dpart, unsigned*
   count_launch();
   return cudaLaunchKernelEx(&cfg, tail_kernel<T>, t, cpart, dpart, bar);
 }
+
+template <class U>
+void launch_xallreduce(const U* in, U* out, int64_t count, int op, char* const* peers,
+                       int world, int rank, int64_t setup_off, int64_t setup_bytes,
+                       unsigned long long gen, cudaStream_t st) {
+  xallreduce_kernel<U><<<1, 1024, 0, st>>>(in, out, count, op, peers, world, rank, setup_off,
+                                           setup_bytes, gen);
+  count_launch();
+}
+template void launch_xallreduce<float>(const float*, float*, int64_t, int, char* const*, int,
+                                       int, int64_t, int64_t, unsigned long long, cudaStream_t);
+template void launch_xallreduce<double>(const double*, double*, int64_t, int, char* const*, int,
+                                        int, int64_t, int64_t, unsigned long long, cudaStream_t);
+template void launch_xallreduce<int32_t>(const int32_t*, int32_t*, int64_t, int, char* const*,
+                                         int, int, int64_t, int64_t, unsigned long long,
+                                         cudaStream_t);
+
+template <class T>
+cudaError_t launch_shard_tail(const TailArgs<T>& t, T* cpart, double* dpart, unsigned* bar,
+                              const XArgs& x, int grid, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kTT);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  count_launch();
+  return cudaLaunchKernelEx(&cfg, shard_tail_kernel<T>, t, cpart, dpart, bar, x);
+}
+
+template <class T>
+void launch_shard_pending_local(const TailArgs<T>& t, const double* dpart, int grid,
+                                double* out4, cudaStream_t st) {
+  shard_pending_local_kernel<T><<<1, kTT, 0, st>>>(t, dpart, grid, out4);
+  count_launch();
+}
+
+template <class T>
+void launch_shard_pending_patch(const TailArgs<T>& t, const double* dpart, int grid,
+                                const double* glob4, cudaStream_t st) {
+  shard_pending_patch_kernel<T><<<1, kTT, 0, st>>>(t, dpart, grid, glob4);
+  count_launch();
+}
+
+template cudaError_t launch_shard_tail<float>(const TailArgs<float>&, float*, double*,
+                                              unsigned*, const XArgs&, int, cudaStream_t);
+template cudaError_t launch_shard_tail<double>(const TailArgs<double>&, double*, double*,
+                                               unsigned*, const XArgs&, int, cudaStream_t);
+template void launch_shard_pending_local<float>(const TailArgs<float>&, const double*, int,
+                                                double*, cudaStream_t);
+template void launch_shard_pending_local<double>(const TailArgs<double>&, const double*, int,
+                                                 double*, cudaStream_t);
+template void launch_shard_pending_patch<float>(const TailArgs<float>&, const double*, int,
+                                                const double*, cudaStream_t);
+template void launch_shard_pending_patch<double>(const TailArgs<double>&, const double*, int,
+                                                 const double*, cudaStream_t);
 
 template <class T>
 void launch_tail_finalize(const TailArgs<T>& t, const double* dpart, int grid, cudaStream_t st) {

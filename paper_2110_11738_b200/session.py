@@ -63,6 +63,44 @@ class Session:
         self._h = h
         return self
 
+    @classmethod
+    def sharded_p2p(cls, m_global: int, n: int, dtype, cfg: Optional[DrotConfig], rank: int,
+                    world: int, row_begin: int, row_end: int) -> "Session":
+        """Row shard whose per-iteration exchange is fused into the cooperative
+        tail over NVLink peer memory (no NCCL).  Call attach_peers() with every
+        rank's exchange_pointer() (same process) or exchange_handle() (one
+        process per GPU) before set_problem / gen_*."""
+        self = cls.__new__(cls)
+        self.m, self.n = int(row_end - row_begin), int(n)
+        self.m_global, self.row_begin = int(m_global), int(row_begin)
+        self.dtype = np.dtype(dtype)
+        self.cfg = cfg or DrotConfig()
+        h = C.c_void_p()
+        ccfg = self.cfg.to_c()
+        _check(_lib.load().drotb_session_create_sharded_p2p(
+            C.byref(h), int(m_global), int(n), 0 if self.dtype == np.float32 else 1,
+            C.byref(ccfg), int(rank), int(world), int(row_begin), int(row_end)))
+        self._h = h
+        return self
+
+    def exchange_pointer(self) -> int:
+        ptr = C.c_uint64(0)
+        _check(_lib.load().drotb_session_exchange_buffer(self._h, C.byref(ptr), None))
+        return int(ptr.value)
+
+    def exchange_handle(self) -> bytes:
+        buf = C.create_string_buffer(64)
+        _check(_lib.load().drotb_session_exchange_buffer(self._h, None, buf))
+        return buf.raw
+
+    def attach_peers(self, pointers=None, handles=None):
+        if pointers is not None:
+            arr = (C.c_uint64 * len(pointers))(*[int(x) for x in pointers])
+            _check(_lib.load().drotb_session_attach_peers(self._h, C.cast(arr, C.c_void_p), None))
+        else:
+            blob = b"".join(bytes(h).ljust(64, b"\0")[:64] for h in handles)
+            _check(_lib.load().drotb_session_attach_peers(self._h, None, blob))
+
     def close(self):
         if getattr(self, "_h", None):
             _lib.load().drotb_session_destroy(self._h)
