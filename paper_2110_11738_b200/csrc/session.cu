@@ -262,6 +262,11 @@ struct Session {
     tc = bs * std::max<int64_t>(1, cfg.work_size);
     if (!exact && !engine) tc = fast_tile_cols();
     RC_TRY(allocate());
+    if (cfg.record_trace) {  // sized here so that init() (collective when sharded) never allocates
+      const int64_t te = std::max<int64_t>(1, cfg.trace_every);
+      trace_alloc = std::min<int64_t>(std::max<int64_t>(cfg.max_iters, 0) / te + 1, int64_t(1) << 23);
+      RC_TRY(dev_alloc(&trace, static_cast<size_t>(trace_alloc)));
+    }
     if (!exact && !engine && !no_persist) {
       // default: K1 + the cooperative tail kernel; DROTB_PERSIST=1 selects the
       // persistent solver kernel, DROTB_TAIL=legacy the three tail kernels
@@ -2041,8 +2046,13 @@ int drotb_session_gen_gaussian(drotb_session* s, double sigma_t, uint64_t seed,
     RC_TRY(drotb::gaussian_points(mg, n, sigma_t, seed, xs, xt));
     double* dpts = nullptr;
     unsigned long long* dmax = nullptr;
-    CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&dpts), sizeof(double) * 2 * (mg + n) + 16));
-    std::unique_ptr<double, decltype(&cudaFree)> hold(dpts, &cudaFree);
+    // stream-ordered allocation: no device-wide synchronization (shards of one
+    // process may be spinning in a collective on the same device)
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&dpts), sizeof(double) * 2 * (mg + n) + 16,
+                             ss->stream));
+    cudaStream_t hs = ss->stream;
+    auto freer = [hs](double* ptr) { cudaFreeAsync(ptr, hs); };
+    std::unique_ptr<double, decltype(freer)> hold(dpts, freer);
     dmax = reinterpret_cast<unsigned long long*>(dpts + 2 * (mg + n));
     double* dxs = dpts;
     double* dxt = dpts + 2 * mg;
