@@ -138,6 +138,7 @@ struct Session {
   TraceRowDev* trace = nullptr;
   unsigned long long* vflags = nullptr;
   int32_t* h_stop = nullptr;  // pinned, 2 slots
+  char* hpin = nullptr;       // pinned staging for small host <-> device transfers
   cudaEvent_t ev[2] = {nullptr, nullptr};
 
   // row sharding (multi-GPU): this rank holds rows [row_begin, row_begin+m)
@@ -237,6 +238,8 @@ struct Session {
     vflags = nullptr;
     if (h_stop) cudaFreeHost(h_stop);
     h_stop = nullptr;
+    if (hpin) cudaFreeHost(hpin);
+    hpin = nullptr;
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     ev[0] = ev[1] = nullptr;
@@ -545,10 +548,9 @@ struct Session {
   int agree(int local_rc, const std::string& local_msg) {
     if (!sharded) return local_rc;
     int32_t v = local_rc;
-    CUDA_TRY(cudaMemcpyAsync(dint, &v, sizeof(v), cudaMemcpyHostToDevice, stream));
+    RC_TRY(h2d_small(dint, &v, sizeof(v)));
     RC_TRY(allreduce(dint, 1, ncclMax));
-    CUDA_TRY(cudaMemcpyAsync(&v, dint, sizeof(v), cudaMemcpyDeviceToHost, stream));
-    CUDA_TRY(cudaStreamSynchronize(stream));
+    RC_TRY(d2h_small(&v, dint, sizeof(v)));
     if (v == 0) return 0;
     if (v != local_rc) g_err = "rank " + std::to_string(rank) + ": another rank failed: " +
                                std::string(v < DROTB_ERR_CUDA ? errc_name(v - 1) : "device error");
@@ -615,6 +617,7 @@ struct Session {
     CUDA_TRY(cudaMemsetAsync(p, 0, sizeof(T) * ld, stream));
     CUDA_TRY(cudaMemsetAsync(u, 0, sizeof(T) * ld, stream));
     CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&h_stop), 2 * sizeof(int32_t)));
+    CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&hpin), kPinBytes));
     CUDA_TRY(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
     return 0;
@@ -732,10 +735,9 @@ struct Session {
     }
     const std::string msg = g_err;
     RC_TRY(agree(rc, msg));
-    CUDA_TRY(cudaMemcpyAsync(dpack + 8, &psum, sizeof(double), cudaMemcpyHostToDevice, stream));
+    RC_TRY(h2d_small(dpack + 8, &psum, sizeof(double)));
     RC_TRY(allreduce(dpack + 8, 1, ncclSum));
-    CUDA_TRY(cudaMemcpyAsync(&psum, dpack + 8, sizeof(double), cudaMemcpyDeviceToHost, stream));
-    CUDA_TRY(cudaStreamSynchronize(stream));
+    RC_TRY(d2h_small(&psum, dpack + 8, sizeof(double)));
     if (std::abs(psum - 1.0) > 1e-12)
       return set_error(DROTB_ERRC_MARGINAL_NOT_SIMPLEX, "p sums to " + std::to_string(psum));
     return check_marginal(hq, "q");
@@ -818,10 +820,9 @@ struct Session {
     hb.tol_gap = cfg.tol_gap;
     double p_norm2 = static_cast<double>(host_norm_sq(hp));
     if (sharded) {  // global |p|^2 (allreduce of the rank-local T sums)
-      CUDA_TRY(cudaMemcpyAsync(dpack + 9, &p_norm2, sizeof(double), cudaMemcpyHostToDevice, stream));
+      RC_TRY(h2d_small(dpack + 9, &p_norm2, sizeof(double)));
       RC_TRY(allreduce(dpack + 9, 1, ncclSum));
-      CUDA_TRY(cudaMemcpyAsync(&p_norm2, dpack + 9, sizeof(double), cudaMemcpyDeviceToHost, stream));
-      CUDA_TRY(cudaStreamSynchronize(stream));
+      RC_TRY(d2h_small(&p_norm2, dpack + 9, sizeof(double)));
     }
     const double p_norm = std::sqrt(p_norm2);
     const double q_norm = std::sqrt(static_cast<double>(host_norm_sq(hq)));
@@ -835,10 +836,9 @@ struct Session {
       for (T e : hp) sp += static_cast<double>(e);
       for (T e : hq) sq += static_cast<double>(e);
       if (sharded) {  // global sum p (rank-local rows)
-        CUDA_TRY(cudaMemcpyAsync(dpack + 11, &sp, sizeof(double), cudaMemcpyHostToDevice, stream));
+        RC_TRY(h2d_small(dpack + 11, &sp, sizeof(double)));
         RC_TRY(allreduce(dpack + 11, 1, ncclSum));
-        CUDA_TRY(cudaMemcpyAsync(&sp, dpack + 11, sizeof(double), cudaMemcpyDeviceToHost, stream));
-        CUDA_TRY(cudaStreamSynchronize(stream));
+        RC_TRY(d2h_small(&sp, dpack + 11, sizeof(double)));
       }
       hb.sum_p = sp;
       hb.sum_q = sq;
@@ -1316,10 +1316,26 @@ struct Session {
     return 0;
   }
 
-  int read_book(Book<T>* hb) {
-    CUDA_TRY(cudaMemcpyAsync(hb, book, sizeof(Book<T>), cudaMemcpyDeviceToHost, stream));
+  // Small transfers through pinned staging: a pageable copy blocks inside the
+  // CUDA call until the stream drains, which must not happen while another
+  // shard of this process needs the driver to reach the same exchange.
+  static constexpr size_t kPinBytes = 4096;
+  int d2h_small(void* dst, const void* src, size_t bytes) {
+    CUDA_TRY(cudaMemcpyAsync(hpin, src, bytes, cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    std::memcpy(dst, hpin, bytes);
+    return 0;
+  }
+  int h2d_small(void* dst, const void* src, size_t bytes) {
+    std::memcpy(hpin, src, bytes);
+    CUDA_TRY(cudaMemcpyAsync(dst, hpin, bytes, cudaMemcpyHostToDevice, stream));
     CUDA_TRY(cudaStreamSynchronize(stream));
     return 0;
+  }
+
+  int read_book(Book<T>* hb) {
+    static_assert(sizeof(Book<T>) <= kPinBytes, "Book fits the pinned staging");
+    return d2h_small(hb, book, sizeof(Book<T>));
   }
 
   // Final status and report (solver.hpp:527-538).
@@ -1401,10 +1417,9 @@ struct Session {
     double mx;
     std::memcpy(&mx, &stats[0], sizeof(mx));
     if (sharded) {
-      CUDA_TRY(cudaMemcpyAsync(dpack + 10, &mx, sizeof(double), cudaMemcpyHostToDevice, stream));
+      RC_TRY(h2d_small(dpack + 10, &mx, sizeof(double)));
       RC_TRY(allreduce(dpack + 10, 1, ncclMax));
-      CUDA_TRY(cudaMemcpyAsync(&mx, dpack + 10, sizeof(double), cudaMemcpyDeviceToHost, stream));
-      CUDA_TRY(cudaStreamSynchronize(stream));
+      RC_TRY(d2h_small(&mx, dpack + 10, sizeof(double)));
     }
     const double thr = std::max(abs_tau, rel_tau * mx);
     launch_plan_count<T>(X, C, rho, hb.folded, m, n, ld, thr, vflags, stream);
@@ -1413,10 +1428,9 @@ struct Session {
     CUDA_TRY(cudaStreamSynchronize(stream));
     double cnt = static_cast<double>(stats[1]);
     if (sharded) {
-      CUDA_TRY(cudaMemcpyAsync(dpack + 10, &cnt, sizeof(double), cudaMemcpyHostToDevice, stream));
+      RC_TRY(h2d_small(dpack + 10, &cnt, sizeof(double)));
       RC_TRY(allreduce(dpack + 10, 1, ncclSum));
-      CUDA_TRY(cudaMemcpyAsync(&cnt, dpack + 10, sizeof(double), cudaMemcpyDeviceToHost, stream));
-      CUDA_TRY(cudaStreamSynchronize(stream));
+      RC_TRY(d2h_small(&cnt, dpack + 10, sizeof(double)));
     }
     if (nnz) *nnz = static_cast<int64_t>(cnt);
     if (xmax) *xmax = mx;
