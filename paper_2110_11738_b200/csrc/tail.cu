@@ -1076,6 +1076,12 @@ cudaError_t launch_shard_tail(const TailArgs<T>& t, T* cpart, double* dpart, uns
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // test aid: several shards of ONE process on ONE device run their tails
+  // concurrently; the driver does not overlap two cooperative grids, so the
+  // in-process test launches ordinary grids small enough to be co-resident
+  const char* nc = std::getenv("DROTB_TAIL_NONCOOP");
+  const bool noncoop = nc && nc[0] == '1';
+  if (noncoop) cfg.numAttrs = 0;
   count_launch();
   return cudaLaunchKernelEx(&cfg, shard_tail_kernel<T>, t, cpart, dpart, bar, x);
 }

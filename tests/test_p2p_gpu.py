@@ -10,8 +10,10 @@ over peer memory (tail.cu shard_tail_kernel; no NCCL).
   collective confirm all run for real.  Both ranks must agree bit for bit
   on every replicated quantity (status, iterations, report, nu), and the
   joined solution must match the one-rank solve.
-Two cooperative tails must be co-resident for the in-process world = 2
-run, so the tail grid is reduced to one CTA per SM there (DROTB_TAIL_CTAS).
+Two tails must be co-resident for the in-process world = 2 run: the tail
+grid is reduced to one CTA per SM and launched as an ordinary grid there
+(DROTB_TAIL_CTAS, DROTB_TAIL_NONCOOP -- the driver does not overlap two
+cooperative grids on one device; one process per GPU never needs this).
 """
 import os
 import threading
@@ -91,8 +93,14 @@ def test_world1_matches_single_gpu(drot, dt):
         assert v <= 1e-4
 
 
+@pytest.fixture()
+def noncoop_tail():
+    with _env(DROTB_TAIL_NONCOOP="1"):
+        yield
+
+
 @pytest.mark.parametrize("dt", [np.float64, np.float32])
-def test_world2_in_process(drot, dt):
+def test_world2_in_process(drot, dt, noncoop_tail):
     m, n = 700, 500
     # eager launches: graph instantiation must not wait on the peer session's
     # spinning exchange kernel on the same device (in-process test only)
