@@ -1,0 +1,71 @@
+"""Dev aid: world = 2 shards in one process, one iteration at a time, with a
+watchdog that dumps both exchange buffers' flags through a side stream."""
+import ctypes as C
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+os.environ["DROTB_TAIL_CTAS"] = "1"
+os.environ["DROTB_TAIL_NONCOOP"] = "1"
+sys.path.insert(0, ".")
+import torch  # noqa: E402
+import paper_2110_11738_b200 as drot  # noqa: E402
+
+cudart = C.CDLL("libcudart.so.12")
+m, n = 700, 500
+cfg = drot.DrotConfig(max_iters=100000, use_graphs=False)
+ranges = [drot.shard_rows(m, 2, r) for r in range(2)]
+ss = [drot.Session.sharded_p2p(m, n, np.float64, cfg, r, 2, *ranges[r]) for r in range(2)]
+streams = [torch.cuda.Stream() for _ in range(2)]
+for s, stm in zip(ss, streams):
+    s.set_stream(stm.cuda_stream)
+ptrs = [s.exchange_pointer() for s in ss]
+for s in ss:
+    s.attach_peers(pointers=ptrs)
+progress = [0, 0]
+stage = ["", ""]
+
+
+def par(fs):
+    th = [threading.Thread(target=f) for f in fs]
+    [t.start() for t in th]
+    return th
+
+
+def work(r, nit):
+    s = ss[r]
+    stage[r] = "gen"
+    s.gen_gaussian(5.0, 5, "dyadic")
+    stage[r] = "init"
+    s.init()
+    for k in range(nit):
+        stage[r] = f"enqueue {k}"
+        s.enqueue(1)
+        stage[r] = f"sync {k}"
+        s.synchronize()
+        progress[r] = k + 1
+    stage[r] = "done"
+
+
+th = par([lambda r=r: work(r, 12) for r in range(2)])
+side = C.c_void_p()
+cudart.cudaStreamCreateWithFlags(C.byref(side), 1)
+t0 = time.time()
+while any(t.is_alive() for t in th) and time.time() - t0 < 40:
+    time.sleep(5)
+    flags = []
+    for p in ptrs:
+        buf = (C.c_uint64 * 4)()
+        cudart.cudaMemcpyAsync(buf, C.c_void_p(p), 32, 2, side)
+        cudart.cudaStreamSynchronize(side)
+        buf2 = (C.c_uint64 * 4)()
+        cudart.cudaMemcpyAsync(buf2, C.c_void_p(p + 256), 32, 2, side)
+        cudart.cudaStreamSynchronize(side)
+        flags.append((list(buf)[:2], list(buf2)[:2]))
+    print(f"t={time.time()-t0:.0f}s progress={progress} stage={stage} iter/setup flags={flags}",
+          flush=True)
+print("alive:", [t.is_alive() for t in th], flush=True)
+os._exit(0)
