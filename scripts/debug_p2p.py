@@ -41,30 +41,33 @@ def work(r, nit):
     s.gen_gaussian(5.0, 5, "dyadic")
     stage[r] = "init"
     s.init()
+    print(f"rank {r} init done", flush=True)
     for k in range(nit):
         stage[r] = f"enqueue {k}"
         s.enqueue(1)
         stage[r] = f"sync {k}"
         s.synchronize()
         progress[r] = k + 1
+        print(f"rank {r} iteration {k + 1}", flush=True)
     stage[r] = "done"
 
 
+print("start", flush=True)
 th = par([lambda r=r: work(r, 12) for r in range(2)])
 side = C.c_void_p()
 cudart.cudaStreamCreateWithFlags(C.byref(side), 1)
+pin = C.c_void_p()
+cudart.cudaMallocHost(C.byref(pin), 1024)
 t0 = time.time()
 while any(t.is_alive() for t in th) and time.time() - t0 < 40:
     time.sleep(5)
     flags = []
     for p in ptrs:
-        buf = (C.c_uint64 * 4)()
-        cudart.cudaMemcpyAsync(buf, C.c_void_p(p), 32, 2, side)
+        cudart.cudaMemcpyAsync(pin, C.c_void_p(p), 16, 2, side)
+        cudart.cudaMemcpyAsync(C.c_void_p(pin.value + 16), C.c_void_p(p + 256), 16, 2, side)
         cudart.cudaStreamSynchronize(side)
-        buf2 = (C.c_uint64 * 4)()
-        cudart.cudaMemcpyAsync(buf2, C.c_void_p(p + 256), 32, 2, side)
-        cudart.cudaStreamSynchronize(side)
-        flags.append((list(buf)[:2], list(buf2)[:2]))
+        buf = (C.c_uint64 * 4).from_address(pin.value)
+        flags.append((list(buf)[:2], list(buf)[2:4]))
     print(f"t={time.time()-t0:.0f}s progress={progress} stage={stage} iter/setup flags={flags}",
           flush=True)
 print("alive:", [t.is_alive() for t in th], flush=True)
