@@ -334,6 +334,9 @@ int32_t drotb_session_persistent_grid(drotb_session* s);
  * [3] last CTA past it, [4] last arrival at the update barrier, [5] gate
  * done, [6] last CTA past it (max over the launches since the last reset). */
 int drotb_session_tail_stamps(drotb_session* s, uint64_t* out8);
+/* Debug aid: device addresses of the book, the tail barrier words and the
+ * exchange buffer, and the tail grid size. */
+int drotb_session_debug_ptrs(drotb_session* s, uint64_t* out4);
 /* Copy the session's (local) cost matrix to host, m x n column-major. */
 int drotb_session_get_cost(drotb_session* s, void* out);
 /* init_state (x0 host pointer or NULL); resets the solve bookkeeping. */

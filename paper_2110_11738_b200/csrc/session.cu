@@ -2151,6 +2151,20 @@ int drotb_session_tail_stamps(drotb_session* s, uint64_t* out8) {
   return go(drotb::as_session<double>(s->impl));
 }
 
+// Debug aid: device addresses of the book, the tail barrier words and the
+// exchange buffer (for side-stream inspection of a stuck exchange).
+int drotb_session_debug_ptrs(drotb_session* s, uint64_t* out4) {
+  auto go = [&](auto* ss) -> int {
+    out4[0] = reinterpret_cast<uint64_t>(ss->book);
+    out4[1] = reinterpret_cast<uint64_t>(ss->tbar);
+    out4[2] = reinterpret_cast<uint64_t>(ss->xbuf);
+    out4[3] = static_cast<uint64_t>(ss->tgrid);
+    return 0;
+  };
+  if (s->precision == 0) return go(drotb::as_session<float>(s->impl));
+  return go(drotb::as_session<double>(s->impl));
+}
+
 int32_t drotb_session_persistent_grid(drotb_session* s) {
   if (s->precision == 0) {
     auto* ss = drotb::as_session<float>(s->impl);

@@ -8,6 +8,7 @@ import time
 
 import numpy as np
 
+os.environ["CUDA_MODULE_LOADING"] = "EAGER"  # see tests/test_p2p_gpu.py
 os.environ["DROTB_TAIL_CTAS"] = "1"
 os.environ["DROTB_TAIL_NONCOOP"] = "1"
 sys.path.insert(0, ".")
@@ -25,6 +26,13 @@ for s, stm in zip(ss, streams):
 ptrs = [s.exchange_pointer() for s in ss]
 for s in ss:
     s.attach_peers(pointers=ptrs)
+from paper_2110_11738_b200 import _lib  # noqa: E402
+dbg = []
+for s in ss:
+    a = (C.c_uint64 * 4)()
+    _lib.load().drotb_session_debug_ptrs(s.handle, a)
+    dbg.append(list(a))
+print("debug ptrs", dbg, flush=True)
 progress = [0, 0]
 stage = ["", ""]
 
@@ -68,6 +76,17 @@ while any(t.is_alive() for t in th) and time.time() - t0 < 40:
         cudart.cudaStreamSynchronize(side)
         buf = (C.c_uint64 * 4).from_address(pin.value)
         flags.append((list(buf)[:2], list(buf)[2:4]))
+    bars = []
+    for d in dbg:
+        cudart.cudaMemcpyAsync(pin, C.c_void_p(d[1]), 8, 2, side)
+        for g in range(16):
+            cudart.cudaMemcpyAsync(C.c_void_p(pin.value + 8 + 4 * g), C.c_void_p(d[1] + 4 * 32 * (1 + g)), 4, 2, side)
+        cudart.cudaMemcpyAsync(C.c_void_p(pin.value + 128), C.c_void_p(d[0] + 40), 8, 2, side)
+        cudart.cudaStreamSynchronize(side)
+        w = (C.c_uint32 * 18).from_address(pin.value)
+        it = C.c_int64.from_address(pin.value + 128).value
+        bars.append((list(w)[:2], list(w)[2:18], it))
+    print("   bars (top count, gen | group counts | book.iter?)", bars, flush=True)
     print(f"t={time.time()-t0:.0f}s progress={progress} stage={stage} iter/setup flags={flags}",
           flush=True)
 print("alive:", [t.is_alive() for t in th], flush=True)
