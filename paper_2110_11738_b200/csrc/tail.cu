@@ -1024,6 +1024,15 @@ template <class T>
 int tail_grid(int device) {
   int sms = 0, per = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  // An SM runs CTAs of kernels with different shared-memory carveouts only
+  // after reconfiguring, i.e. once it is empty: a spinning tail CTA on an
+  // SM configured for little shared memory would keep K1 (66 KB per CTA)
+  // off that SM for good -- with shards of one process sharing a device
+  // that is a deadlock.  The tails ask for the maximum carveout, K1's.
+  cudaFuncSetAttribute(tail_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
+  cudaFuncSetAttribute(shard_tail_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tail_kernel<T>, kTT, 0);
   int want = 2;
   if (const char* e = std::getenv("DROTB_TAIL_CTAS")) want = std::atoi(e);  // tuning aid
