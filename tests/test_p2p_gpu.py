@@ -93,53 +93,35 @@ def test_world1_matches_single_gpu(drot, dt):
         assert v <= 1e-4
 
 
-@pytest.fixture()
-def noncoop_tail():
-    with _env(DROTB_TAIL_NONCOOP="1"):
-        yield
-
-
-@pytest.mark.parametrize("dt", [np.float64, np.float32])
-def test_world2_in_process(drot, dt, noncoop_tail):
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_world_n_in_process(drot, dt, world):
+    """world shards of one process on one GPU (tests/p2p_world2.py)."""
+    import json
+    import subprocess
+    import sys
     m, n = 700, 500
-    # eager launches: graph instantiation must not wait on the peer session's
-    # spinning exchange kernel on the same device (in-process test only)
-    cfg = drot.DrotConfig(max_iters=100000, use_graphs=False)
-    (st1, it1, r1), plan1, mu1, nu1 = _single(drot, m, n, dt, cfg, 5)
-    import torch
-    ranges = [drot.shard_rows(m, 2, r) for r in range(2)]
-    with _env(DROTB_TAIL_CTAS="1"):
-        ss = [drot.Session.sharded_p2p(m, n, dt, cfg, r, 2, *ranges[r]) for r in range(2)]
-    streams = [torch.cuda.Stream() for _ in range(2)]
-    for s, stm in zip(ss, streams):
-        s.set_stream(stm.cuda_stream)
-    ptrs = [s.exchange_pointer() for s in ss]
-    for s in ss:
-        s.attach_peers(pointers=ptrs)
-    _parallel([lambda s=s: s.gen_gaussian(5.0, 5, "dyadic") for s in ss])
-    _parallel([s.init for s in ss])
-    _parallel([s.run for s in ss])
-    out = [None, None]
-
-    def fin(r):
-        out[r] = (ss[r].status(), ss[r].plan())
-
-    _parallel([lambda r=r: fin(r) for r in range(2)])
-    for s in ss:
-        s.close()
-    (sa, ia, ra), (pa, mua, nua) = out[0]
-    (sb, ib, rb), (pb, mub, nub) = out[1]
-    # replicated state: bit-identical on both ranks
-    assert sa == sb and ia == ib
-    assert (ra.objective, ra.r_primal, ra.r_dual, ra.gap) == (rb.objective, rb.r_primal,
-                                                              rb.r_dual, rb.gap)
-    np.testing.assert_array_equal(nua, nub)
-    # the joined solution against the one-GPU solve
-    assert sa == st1 == drot.SolveStatus.converged
+    npdt = np.float64 if dt == "f64" else np.float32
+    cfg = drot.DrotConfig(max_iters=100000)
+    (st1, it1, r1), plan1, mu1, nu1 = _single(drot, m, n, npdt, cfg, 5)
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, CUDA_MODULE_LOADING="EAGER")
+    proc = subprocess.run([sys.executable, os.path.join(here, "p2p_world2.py"), dt, str(m),
+                           str(n), str(world)], capture_output=True, text=True, timeout=600,
+                          env=env)
+    assert proc.returncode == 0, proc.stdout[-2000:] + proc.stderr[-2000:]
+    out = json.loads(proc.stdout.strip().splitlines()[-1])
+    # replicated state: bit-identical on every rank
+    for o in out[1:]:
+        assert o["status"] == out[0]["status"] and o["iterations"] == out[0]["iterations"]
+        assert o["report"] == out[0]["report"]
+        assert o["nu"] == out[0]["nu"]
+    ia, ra = out[0]["iterations"], out[0]["report"]
+    assert out[0]["status"] == st1.name == "converged"
     assert abs(ia - it1) <= max(5, it1 // 200)
-    rel = 1e-5 if dt == np.float64 else 1e-3
-    assert abs(ra.objective - r1.objective) <= rel * abs(r1.objective)
-    plan = np.concatenate([pa, pb], axis=0)
+    rel = 1e-5 if dt == "f64" else 1e-3
+    assert abs(ra[0] - r1.objective) <= rel * abs(r1.objective)
+    plan = np.concatenate([np.array(o["plan"]) for o in out], axis=0)
     scale = float(np.abs(plan1).max())
-    tol = (1e-6 if dt == np.float64 else 1e-3) if ia == it1 else 2e-2
+    tol = (1e-6 if dt == "f64" else 1e-3) if ia == it1 else 2e-2
     assert float(np.abs(plan - plan1).max()) <= tol * scale
