@@ -938,8 +938,12 @@ __global__ void __launch_bounds__(kTT) shard_tail_kernel(const TailArgs<T> t, T*
     const bool fp = bk->record_trace != 0;
     double part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const int64_t TT = static_cast<int64_t>(G) * kTT;
-    for (int64_t idx = static_cast<int64_t>(blockIdx.x) * kTT + tid; idx < m + n; idx += TT) {
-      if (idx < m) {
+    // rows and columns in separate loops: the column mapping (and so the
+    // rounding of the replicated column sums) must not depend on the
+    // rank's row count
+    const int64_t g0 = static_cast<int64_t>(blockIdx.x) * kTT + tid;
+    for (int64_t idx = g0; idx < m; idx += TT) {
+      {
         const T r = __ldcg(t.r_new + idx);
         const T ph_old = t.phi[idx];
         const T ai = t.a[idx];
@@ -953,8 +957,10 @@ __global__ void __launch_bounds__(kTT) shard_tail_kernel(const TailArgs<T> t, T*
           part[2] += d;
           part[3] += d * (static_cast<double>(r) - static_cast<double>(t.r_old[idx]));
         }
-      } else {
-        const int64_t j = idx - m;
+      }
+    }
+    for (int64_t j = g0; j < n; j += TT) {
+      {
         const T sv = __ldcg(t.s_new + j);
         const T vp_old = t.varphi[j];
         const T bj = t.b[j];
@@ -1037,6 +1043,10 @@ int tail_grid(int device) {
   int want = 2;
   if (const char* e = std::getenv("DROTB_TAIL_CTAS")) want = std::atoi(e);  // tuning aid
   if (want < 1) want = 1;
+  if (const char* e = std::getenv("DROTB_TAIL_GRID")) {  // test aid: absolute grid size
+    const int g = std::atoi(e);
+    if (g >= 1 && g <= sms * per) return g;
+  }
   return sms * (per < want ? per : want);
 }
 

@@ -10,6 +10,8 @@ import threading
 
 os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 os.environ["DROTB_TAIL_CTAS"] = "1"
+# several spinning tails + the next K1 must fit on one device at once
+os.environ["DROTB_TAIL_GRID"] = str(148 // max(1, int(sys.argv[4]) - 1) // 2 * 2)
 os.environ["DROTB_TAIL_NONCOOP"] = "1"
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
