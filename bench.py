@@ -185,6 +185,23 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def make_shard(drot, dist, args, m_global, n, dt, cfg, rank, world):
+    """One row shard per rank.  exchange 'p2p' (default): the per-iteration
+    exchange runs inside the cooperative tail over NVLink peer memory (CUDA
+    IPC handles all-gathered over torch.distributed); 'nccl': NCCL
+    allreduces between per-launch kernels."""
+    r0, r1 = drot.shard_rows(m_global, world, rank)
+    if args.exchange == "p2p":
+        sess = drot.Session.sharded_p2p(m_global, n, dt, cfg, rank, world, r0, r1)
+        handles = [None] * world
+        dist.all_gather_object(handles, sess.exchange_handle())
+        sess.attach_peers(handles=handles)
+        return sess
+    obj = [drot.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return drot.Session.sharded(m_global, n, dt, cfg, rank, world, obj[0], r0, r1)
+
+
 # ---------------------------------------------------------------------------
 # B200 arm
 # ---------------------------------------------------------------------------
@@ -211,14 +228,11 @@ def run_b200(args, rank, world, local_rank):
     if world > 1:
         # weak scaling over row shards: ONE m_global x n problem,
         # m_global = world * size, each rank holding `size` rows; the column
-        # sums and scalars are allreduced over NCCL every iteration.
+        # sums and scalars are exchanged every iteration (--exchange).
         order = "fast"
         cfg.order = drot.Order.fast
         m_global = world * m
-        obj = [drot.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        r0, r1 = drot.shard_rows(m_global, world, rank)
-        sess = drot.Session.sharded(m_global, n, dt, cfg, rank, world, obj[0], r0, r1)
+        sess = make_shard(drot, dist, args, m_global, n, dt, cfg, rank, world)
     else:
         m_global = m
         sess = drot.Session(m, n, dt, cfg)
@@ -301,9 +315,10 @@ def run_b200(args, rank, world, local_rank):
                     "to the reference generator; inputs resident in HBM)",
             "config": workload_config(m, n, order, {
                 "parallelism": (f"row-sharded over {world} GPUs: one {m_global}x{n} problem, "
-                                f"{m} rows per GPU, NCCL allreduce of the n column sums + "
-                                "scalars per iteration; value counts 10k x 10k "
-                                "iteration-equivalents (world x iterations/s)")
+                                f"{m} rows per GPU, per-iteration exchange of the n column "
+                                f"sums + scalars: {args.exchange} ('p2p' = fused into the "
+                                "cooperative tail over NVLink peer memory); value counts "
+                                "10k x 10k iteration-equivalents (world x iterations/s)")
                 if world > 1 else "1 GPU"}),
             "hbm_gbs_step": step_bytes_gbs,
             "roofline": roof,
@@ -466,10 +481,7 @@ def time_to_tol_c2(args, drot, torch, dist, m, n, m_global, rank, world, local_r
     on the session stream around run(), max over ranks."""
     cfg = drot.DrotConfig(max_iters=args.ttt_max_iters, record_trace=False, device=local_rank)
     if world > 1:
-        obj = [drot.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        r0, r1 = drot.shard_rows(m_global, world, rank)
-        sess = drot.Session.sharded(m_global, n, np.float32, cfg, rank, world, obj[0], r0, r1)
+        sess = make_shard(drot, dist, args, m_global, n, np.float32, cfg, rank, world)
     else:
         sess = drot.Session(m, n, np.float32, cfg)
     stream = torch.cuda.current_stream()
@@ -545,6 +557,7 @@ def main():
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--no-sinkhorn", action="store_true")
     ap.add_argument("--no-f64", action="store_true")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"])
     ap.add_argument("--ttt-max-iters", type=int, default=400000)
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))

@@ -125,3 +125,42 @@ def test_world_n_in_process(drot, dt, world):
     scale = float(np.abs(plan1).max())
     tol = (1e-6 if dt == "f64" else 1e-3) if ia == it1 else 2e-2
     assert float(np.abs(plan - plan1).max()) <= tol * scale
+
+
+def test_ipc_two_processes(drot, tmp_path):
+    """Two processes, one shard each, peers attached through CUDA IPC handles
+    (tests/p2p_ipc_worker.py) -- against the one-GPU solve of the same 40
+    iterations."""
+    import json
+    import socket
+    import subprocess
+    import sys
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, CUDA_MODULE_LOADING="EAGER", MASTER_ADDR="127.0.0.1",
+               MASTER_PORT=str(port))
+    outs = [str(tmp_path / f"r{r}.json") for r in range(2)]
+    procs = [subprocess.Popen([sys.executable, os.path.join(here, "p2p_ipc_worker.py"), str(r),
+                               "2", outs[r]], env=env, stdout=subprocess.PIPE,
+                              stderr=subprocess.STDOUT, text=True) for r in range(2)]
+    logs = []
+    for pr in procs:
+        try:
+            logs.append(pr.communicate(timeout=400)[0])
+        except subprocess.TimeoutExpired:
+            for q in procs:
+                q.kill()
+            raise AssertionError("IPC exchange did not finish")
+    assert all(pr.returncode == 0 for pr in procs), "\n".join(l[-1500:] for l in logs)
+    res = [json.load(open(o)) for o in outs]
+    assert res[0]["iterations"] == res[1]["iterations"] == 40
+    assert res[0]["report"] == res[1]["report"] and res[0]["nu"] == res[1]["nu"]
+    cfg = drot.DrotConfig(tol_primal=-1.0, max_iters=40)
+    (st1, it1, r1), plan1, mu1, nu1 = _single(drot, 640, 480, np.float64, cfg, 7)
+    assert it1 == 40
+    assert abs(res[0]["report"][0] - r1.objective) <= 1e-9 * abs(r1.objective)
+    plan = np.concatenate([np.array(r["plan"]) for r in res], axis=0)
+    assert float(np.abs(plan - plan1).max()) <= 1e-9 * float(np.abs(plan1).max())
