@@ -209,12 +209,22 @@ def run_b200(args, rank, world, local_rank):
     import torch
     import paper_2110_11738_b200 as drot
 
+    # DROTB_BENCH_SHARE_GPU=1 (test aid): every rank on cuda:0 with a gloo
+    # process group -- exercises the N > 1 path on one GPU (time-sliced, so
+    # its numbers mean nothing)
+    share = os.environ.get("DROTB_BENCH_SHARE_GPU") == "1"
+    if share:
+        os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
         if dist is not None:
@@ -257,7 +267,7 @@ def run_b200(args, rank, world, local_rank):
 
     ms = r["total_ms"]
     if dist is not None:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms], device="cpu" if share else dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = world * args.steps / (ms / 1e3)
@@ -500,7 +510,8 @@ def time_to_tol_c2(args, drot, torch, dist, m, n, m_global, rank, world, local_r
     wall = time.perf_counter() - t0
     sec = e0.elapsed_time(e1) / 1e3
     if dist is not None:
-        t = torch.tensor([sec], device="cuda", dtype=torch.float64)
+        share = os.environ.get("DROTB_BENCH_SHARE_GPU") == "1"
+        t = torch.tensor([sec], device="cpu" if share else "cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         sec = float(t.item())
     st, iters, rep = sess.status()
