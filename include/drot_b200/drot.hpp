@@ -297,6 +297,75 @@ void check_problem(const TransportProblem<T>& pr) {
     detail::check(drotb_check_problem_f64(pr.cost.data(), m, n, pr.p.data(), pr.q.data()));
 }
 
+// ---- problem.hpp:155-225 (evaluated on the B200) --------------------------------
+template <class T>
+ResidualReport residual_report(const TransportProblem<T>& pr, const TransportPlan<T>& plan,
+                               const DualCertificate<T>& cert) {
+  if (plan.x.rows() != pr.m() || plan.x.cols() != pr.n())
+    fail(Errc::shape_mismatch, "residual_report: plan vs cost");
+  if (cert.mu.size() != pr.m() || cert.nu.size() != pr.n())
+    fail(Errc::shape_mismatch, "residual_report: dual lengths");
+  const auto m = static_cast<int64_t>(pr.m()), n = static_cast<int64_t>(pr.n());
+  drotb_report r{};
+  // exact = 1: the reference's summation order, bitwise equal report
+  if constexpr (detail::is_f32<T>)
+    detail::check(drotb_residual_report_f32(pr.cost.data(), m, n, pr.p.data(), pr.q.data(),
+                                            plan.x.data(), cert.mu.data(), cert.nu.data(), 1, &r));
+  else
+    detail::check(drotb_residual_report_f64(pr.cost.data(), m, n, pr.p.data(), pr.q.data(),
+                                            plan.x.data(), cert.mu.data(), cert.nu.data(), 1, &r));
+  return ResidualReport{r.r_primal, r.r_dual, r.gap, r.objective};
+}
+
+template <class T>
+double objective(const TransportProblem<T>& pr, const TransportPlan<T>& plan) {
+  DualCertificate<T> zero;
+  zero.mu.assign(pr.m(), T(0));
+  zero.nu.assign(pr.n(), T(0));
+  return residual_report(pr, plan, zero).objective;
+}
+
+// ---- reference.hpp:165-288: the Sinkhorn baseline on the B200 -----------------------
+template <class T>
+SolveResult<T> sinkhorn_solve(const TransportProblem<T>& pr, T eta, double tol,
+                              std::int64_t max_iters, std::int64_t check_every = 10) {
+  const std::size_t m = pr.m(), n = pr.n();
+  if (m == 0 || n == 0) fail(Errc::empty_dimension, "cost matrix has an empty dimension");
+  SolveResult<T> res;
+  res.plan.x = Matrix<T>(m, n);
+  res.cert.mu.assign(m, T(0));
+  res.cert.nu.assign(n, T(0));
+  res.cert.rho = eta;
+  const std::int64_t ce = check_every < 1 ? 1 : check_every;
+  const std::int64_t cap = (max_iters > 0 ? max_iters : 0) / ce + 2;
+  std::vector<drotb_trace_row> tr(static_cast<std::size_t>(cap));
+  drotb_report r{};
+  int64_t tlen = 0, iters = 0;
+  int32_t status = 0;
+  double wall = 0;
+  const auto mi = static_cast<int64_t>(m), ni = static_cast<int64_t>(n);
+  if constexpr (detail::is_f32<T>)
+    detail::check(drotb_sinkhorn_f32(pr.cost.data(), mi, ni, pr.p.data(), pr.q.data(), eta, tol,
+                                     max_iters, ce, 0, res.plan.x.data(), res.cert.mu.data(),
+                                     res.cert.nu.data(), &r, tr.data(), cap, &tlen, &iters,
+                                     &status, &wall));
+  else
+    detail::check(drotb_sinkhorn_f64(pr.cost.data(), mi, ni, pr.p.data(), pr.q.data(), eta, tol,
+                                     max_iters, ce, 0, res.plan.x.data(), res.cert.mu.data(),
+                                     res.cert.nu.data(), &r, tr.data(), cap, &tlen, &iters,
+                                     &status, &wall));
+  res.report = ResidualReport{r.r_primal, r.r_dual, r.gap, r.objective};
+  res.status = static_cast<SolveStatus>(status);
+  res.trace.termination = res.status;
+  res.trace.iterations = iters;
+  res.trace.wall_time_s = wall;
+  for (int64_t k = 0; k < tlen && k < cap; ++k)
+    res.trace.rows.push_back(TraceRow{tr[k].iter, tr[k].r_primal, tr[k].r_dual, tr[k].gap,
+                                      tr[k].objective, tr[k].ergodic_objective,
+                                      tr[k].fixed_point_residual});
+  return res;
+}
+
 // ---- solver.hpp:143-186 / 361-370 / 372-540 -------------------------------------
 template <class T>
 DrotState<T> init_state(const TransportProblem<T>& pr, const DrotConfig& cfg,

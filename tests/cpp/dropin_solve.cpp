@@ -23,6 +23,13 @@ int main() {
               drot::to_string(res.status), static_cast<long long>(res.trace.iterations),
               res.report.objective, res.plan.x(0, 0), res.plan.x(0, 1), res.plan.x(1, 0),
               res.plan.x(1, 1), res.trace.rows.size());
+  // residual_report of the returned pair, and the Sinkhorn baseline
+  // (problem.hpp:174-225, reference.hpp:165-288) through the same header
+  auto rep = drot::residual_report(pr, res.plan, res.cert);
+  auto sk = drot::sinkhorn_solve(pr, 0.1, 1e-6, 20000);
+  std::printf("{\"report_objective\": %.17g, \"sinkhorn_status\": \"%s\", "
+              "\"sinkhorn_objective\": %.17g}\n",
+              rep.objective, drot::to_string(sk.status), sk.report.objective);
   // errors surface as drot::Error with the reference's codes
   pr.p = {0.5, 0.6};
   try {

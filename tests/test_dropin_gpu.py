@@ -31,4 +31,8 @@ def test_cpp_dropin_runs(tmp_path, ref):
     assert out["iterations"] == want.iterations
     assert out["objective"] == want.report["objective"]
     assert out["x00"] == want.plan[0] and out["x11"] == want.plan[3]
-    assert lines[1]["error"].startswith("marginal_not_simplex: ")
+    # residual_report of (plan, cert) through the header: exact order = the report
+    assert lines[1]["report_objective"] == out["objective"]
+    assert lines[1]["sinkhorn_status"] == "converged"
+    assert abs(lines[1]["sinkhorn_objective"] - 0.3) < 0.07  # test_reference.cpp:231-232
+    assert lines[2]["error"].startswith("marginal_not_simplex: ")
