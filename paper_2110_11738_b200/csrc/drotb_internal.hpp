@@ -292,7 +292,7 @@ void launch_plan_count(const T* xy, const T* cost, T rho, int folded, int64_t m,
                        int64_t ld, double thr, unsigned long long* stats, cudaStream_t st);
 
 // residual_report / objective of an arbitrary (plan, cert) pair (report.cu);
-// scratch: 2*(m+n) doubles; out: r_primal, r_dual, gap, objective
+// scratch: m + 3n doubles; out: r_primal, r_dual, gap, objective
 template <class T>
 void launch_residual_report(const T* x, const T* c, const T* mu, const T* nu, const T* p,
                             const T* q, int64_t m, int64_t n, bool exact, double* scratch,

@@ -1810,8 +1810,10 @@ static int residual_report_t(const T* C, int64_t m, int64_t n, const T* p, const
   if (!C || !p || !q || !plan || !mu || !nu || !out)
     return drotb::set_error(DROTB_ERRC_SHAPE_MISMATCH, "residual_report: null argument");
   const size_t mn = static_cast<size_t>(m) * static_cast<size_t>(n);
-  const size_t tb = sizeof(T) * (2 * mn + 2 * static_cast<size_t>(m + n));
-  const size_t db = sizeof(double) * (2 * static_cast<size_t>(m + n) + 4);
+  // scratch: rowdev[m], coldev[n], colobj[n], coldsq[n] (report.cu), then out[4]
+  const size_t ns = static_cast<size_t>(m) + 3 * static_cast<size_t>(n);
+  const size_t tb = (sizeof(T) * (2 * mn + 2 * static_cast<size_t>(m + n)) + 15) & ~size_t{15};
+  const size_t db = sizeof(double) * (ns + 4);
   char* buf = nullptr;
   CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&buf), tb + db));
   std::unique_ptr<char, decltype(&cudaFree)> hold(buf, &cudaFree);
@@ -1822,7 +1824,7 @@ static int residual_report_t(const T* C, int64_t m, int64_t n, const T* p, const
   T* dnu = dp + m;
   T* dq = dnu + n;
   double* scratch = reinterpret_cast<double*>(buf + tb);
-  double* dout = scratch + 2 * (m + n);
+  double* dout = scratch + ns;
   CUDA_TRY(cudaMemcpy(dX, plan, sizeof(T) * mn, cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(dC, C, sizeof(T) * mn, cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(dmu, mu, sizeof(T) * m, cudaMemcpyHostToDevice));
