@@ -25,8 +25,8 @@ NVCC_FLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
     "-Xcompiler", "-O3", "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include"),
 ]
-SOURCES = ["kernels.cu", "session.cu", "probgen.cpp", "probgen.cu", "report.cu", "persistent.cu", "tail.cu", "sinkhorn.cu"]
-HEADERS = ["drotb_internal.hpp", "drotb_host.hpp", "sweep.cuh"]
+SOURCES = ["kernels.cu", "session.cu", "probgen.cpp", "probgen.cu", "report.cu", "persistent.cu", "tail.cu", "iter.cu", "sinkhorn.cu"]
+HEADERS = ["drotb_internal.hpp", "drotb_host.hpp", "sweep.cuh", "gate.cuh"]
 
 
 def _nvcc() -> str:

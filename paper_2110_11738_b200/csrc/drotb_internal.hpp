@@ -50,7 +50,7 @@ struct PassArgs {
   PassPartial<T>* __restrict__ partials;
   const int* stop;      // device stop flag (nullptr: never)
   int32_t pdl;          // launch as a programmatic dependent (after the coop tail)
-  int32_t pad_pdl;
+  int32_t l2hint;       // 1: stream X / C with an L2 evict_first policy (sweep.cuh)
 };
 
 // Device-resident solver bookkeeping: every scalar of the solve loop
@@ -90,6 +90,11 @@ struct Book {
   double pend_last_cost;  // last_cost seen by its gate
   double pend_dx;         // its pass dx^2
   double sum_p, sum_q;    // sum p_i, sum q_j (double, sequential; set at init)
+  // single-launch iteration (iter.cu): 1 = phi / varphi arrays hold the
+  // current duals; 0 = they are pending as phi_i = (ta_i + coef) / n and
+  // varphi_j = (tb_j + coef) / m (materialized by the next sweep's prologue,
+  // the confirm report on the fly, or the finalize kernel)
+  int32_t phi_mat, pad_pm;
 };
 
 struct TraceRowDev {
@@ -151,6 +156,64 @@ struct TailArgs {
   int32_t fused_gate;          // tail: gate on the algebraic dual value (one barrier less)
   int32_t pad_fg;
 };
+
+// Single-launch iteration (iter.cu): the sweep K1 with the whole per-iteration
+// tail fused into its epilogue ("last arriving CTA" merges, no grid barrier):
+//   - the last of the rbn CTAs of column tile gc sums their CTA-level column
+//     partials (vcta) -> s, tb = b - 2s, b -= s, column-tile record;
+//   - the last of the CTAs of row block rb in u group grp sums that group's
+//     row strips (ugrp); the last group of rb sums the groups -> r,
+//     ta = a - 2r, a -= r, row-block record;
+//   - the last of all those merges reduces the records in fixed order and
+//     runs the scalar recursions and the fused gate on the Book.
+// The next launch's prologue forms phi / varphi from ta / tb and the new coef.
+template <class T>
+struct IterColRec {  // per column tile
+  T cost, prev, dual, dx, mx, s2;
+  int32_t bad, pad;
+  double qb, qs;  // sum q_j b_j (pre-update), sum q_j s_j
+};
+template <class T>
+struct IterRowRec {  // per row block
+  T sr, sr2;
+  double pa, pr;  // sum p_i a_i (pre-update), sum p_i r_i
+};
+template <class T>
+struct IterArgs {
+  PassArgs<T> pa;
+  TailArgs<T> t;
+  T* ta;  // a - 2r (ld)
+  T* tb;  // b - 2s (n)
+  T* a_prev;
+  T* b_prev;
+  T* ugrp;  // [ngrp][ld] grouped row strips
+  T* vcta;  // [rbn][n] CTA-level column partials
+  IterRowRec<T>* rowrec;
+  IterColRec<T>* colrec;
+  double* urow;  // [rbn][4] update partials (prologue, gc == 0 CTAs)
+  double* ucol;  // [gcn][4] (rb == 0 CTAs)
+  unsigned* cnt;  // counters, see iter.cu
+  double* dpart;  // confirm kernel per-CTA partials [grid][16]
+  const T* rbuf0;  // r / s parity buffers (finalize picks by Book.iter)
+  const T* rbuf1;
+  const T* sbuf0;
+  const T* sbuf1;
+  int32_t rbn, gcn, gu, ngrp;
+  int64_t off_col, off_row, off_ug;
+};
+
+template <class T>
+void iter_layout(int64_t m, int64_t n, int64_t tc, int32_t* rbn, int32_t* gcn, int32_t* gu,
+                 int32_t* ngrp, int64_t* cnt_words);
+template <class T>
+size_t iter_smem_bytes(int64_t tc);
+template <class T>
+void launch_iter(const IterArgs<T>& g, int mode, bool want_dual, bool want_dx, cudaStream_t st);
+template <class T>
+void launch_iter_confirm(const IterArgs<T>& g, cudaStream_t st);
+template <class T>
+void launch_iter_finalize(const IterArgs<T>& g, cudaStream_t st);
+constexpr int kIterConfirmGrid = 148 * 4;
 
 // Persistent solver kernel (persistent.cu): one cooperative launch runs up to
 // `iters` iterations; phases separated by grid barriers.

@@ -173,6 +173,19 @@ struct Session {
   bool h_stale = false;  // h_iter / h_folded lag the device after persistent launches
   // cooperative tail kernel (fast order, one GPU; tail.cu)
   bool coop = false, coop_graphs = false, fused_gate = true, pdl_ok = false;
+  // single-launch iteration (iter.cu; the default for order=fast on one GPU)
+  bool fiter = false;
+  bool l2hint = [] {  // evict_first on the streamed reads: opt-in (no net gain measured)
+    const char* e = std::getenv("DROTB_L2HINT");
+    return e && e[0] == '1';
+  }();
+  T *ita = nullptr, *itb = nullptr, *iaprev = nullptr, *ibprev = nullptr;
+  T *iugrp = nullptr, *ivcta = nullptr;
+  IterRowRec<T>* irow = nullptr;
+  IterColRec<T>* icol = nullptr;
+  double *iurow = nullptr, *iucol = nullptr, *idpart = nullptr;
+  unsigned* icnt = nullptr;
+  int32_t irbn = 0, igcn = 0, igu = 1, ingrp = 1;
   int tgrid = 0;
   T* tcpart = nullptr;
   double* tdpart = nullptr;
@@ -201,7 +214,14 @@ struct Session {
     void* bufs[] = {X, C, Xout, phi, varphi, a, b, rb[0], rb[1], sb[0], sb[1],
                     p, q, u, v, ustrip, vstrip, tscr, partials, tiles, dscr,
                     terms, book, trace, vflags, pack, pmax, dpack, dint,
-                    pustrip, pvstrip, pcpart, pdpart, pbar, pseg_ptr, pseg_slot, psweep_ns, pmud, tcpart, tdpart, tbar, tstamps};
+                    pustrip, pvstrip, pcpart, pdpart, pbar, pseg_ptr, pseg_slot, psweep_ns, pmud, tcpart, tdpart, tbar, tstamps,
+                    ita, itb, iaprev, ibprev, iugrp, ivcta, irow, icol, iurow, iucol, idpart, icnt};
+    ita = itb = iaprev = ibprev = iugrp = ivcta = nullptr;
+    irow = nullptr;
+    icol = nullptr;
+    iurow = iucol = idpart = nullptr;
+    icnt = nullptr;
+    fiter = false;
     tstamps = nullptr;
     tcpart = nullptr;
     tdpart = nullptr;
@@ -275,10 +295,74 @@ struct Session {
       // persistent solver kernel, DROTB_TAIL=legacy the three tail kernels
       const char* e = std::getenv("DROTB_PERSIST");
       if (e && e[0] == '1') RC_TRY(setup_persistent());
+      // DROTB_TAIL: unset / 'c' the cooperative tail kernel (tail.cu), 'f'
+      // the single-launch iteration (iter.cu; measured slower at 10k^2, see
+      // DESIGN.md), 'l' the three tail kernels
       const char* tl = std::getenv("DROTB_TAIL");
-      if (!persist && !(tl && tl[0] == 'l')) RC_TRY(setup_coop_tail());
+      if (!persist && tl && tl[0] == 'f') RC_TRY(setup_fused_iter());
+      if (!persist && !(tl && (tl[0] == 'f' || tl[0] == 'l'))) RC_TRY(setup_coop_tail());
     }
     return 0;
+  }
+
+  int setup_fused_iter() {
+    int64_t words = 0;
+    iter_layout<T>(m, n, tc, &irbn, &igcn, &igu, &ingrp, &words);
+    RC_TRY(dev_alloc(&ita, static_cast<size_t>(ld)));
+    RC_TRY(dev_alloc(&itb, static_cast<size_t>(n)));
+    RC_TRY(dev_alloc(&iaprev, static_cast<size_t>(ld)));
+    RC_TRY(dev_alloc(&ibprev, static_cast<size_t>(n)));
+    RC_TRY(dev_alloc(&iugrp, static_cast<size_t>(ingrp) * static_cast<size_t>(ld)));
+    RC_TRY(dev_alloc(&ivcta, static_cast<size_t>(irbn) * static_cast<size_t>(n)));
+    RC_TRY(dev_alloc(&irow, static_cast<size_t>(irbn)));
+    RC_TRY(dev_alloc(&icol, static_cast<size_t>(igcn)));
+    RC_TRY(dev_alloc(&iurow, static_cast<size_t>(irbn) * 4));
+    RC_TRY(dev_alloc(&iucol, static_cast<size_t>(igcn) * 4));
+    RC_TRY(dev_alloc(&idpart, static_cast<size_t>(kIterConfirmGrid) * 16));
+    RC_TRY(dev_alloc(&icnt, static_cast<size_t>(words)));
+    CUDA_TRY(cudaMemsetAsync(ita, 0, sizeof(T) * ld, stream));
+    CUDA_TRY(cudaMemsetAsync(itb, 0, sizeof(T) * n, stream));
+    CUDA_TRY(cudaMemsetAsync(icnt, 0, sizeof(unsigned) * words, stream));
+    if (const char* e = std::getenv("DROTB_TAIL_STAMPS"))
+      if (e[0] == '1') {
+        RC_TRY(dev_alloc(&tstamps, 8));
+        const unsigned long long init[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
+        CUDA_TRY(cudaMemcpy(tstamps, init, sizeof(init), cudaMemcpyHostToDevice));
+      }
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    fiter = true;
+    return 0;
+  }
+
+  IterArgs<T> iter_args(int64_t k, int mode, bool folded_after) {
+    IterArgs<T> g;
+    std::memset(&g, 0, sizeof(g));
+    g.pa = pass_args();
+    g.t = tail_args(k, mode, folded_after, true);
+    g.ta = ita;
+    g.tb = itb;
+    g.a_prev = iaprev;
+    g.b_prev = ibprev;
+    g.ugrp = iugrp;
+    g.vcta = ivcta;
+    g.rowrec = irow;
+    g.colrec = icol;
+    g.urow = iurow;
+    g.ucol = iucol;
+    g.cnt = icnt;
+    g.dpart = idpart;
+    g.rbuf0 = rb[0];
+    g.rbuf1 = rb[1];
+    g.sbuf0 = sb[0];
+    g.sbuf1 = sb[1];
+    g.rbn = irbn;
+    g.gcn = igcn;
+    g.gu = igu;
+    g.ngrp = ingrp;
+    g.off_col = 32;
+    g.off_row = 32 + igcn;
+    g.off_ug = 32 + igcn + irbn;
+    return g;
   }
 
   int setup_coop_tail() {
@@ -831,6 +915,7 @@ struct Session {
     hb.relative = cfg.relative_tolerances ? 1 : 0;
     hb.pend_row = -1;
     hb.pend_valid = 0;
+    hb.phi_mat = 1;
     {
       double sp = 0, sq = 0;
       for (T e : hp) sp += static_cast<double>(e);
@@ -898,6 +983,7 @@ struct Session {
     pa.partials = partials;
     pa.stop = &book->stop;
     pa.pdl = (coop && pdl_ok) ? 1 : 0;
+    pa.l2hint = l2hint ? 1 : 0;
     return pa;
   }
 
@@ -969,6 +1055,16 @@ struct Session {
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (pass_begin || pass_end) CUDA_TRY(cudaStreamIsCapturing(stream, &cap));
     const unsigned evf = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
+    if (fiter) {  // one launch: sweep + merges + recursions + gate (iter.cu)
+      const IterArgs<T> g = iter_args(k, mode, folded_after);
+      if (pass_begin) CUDA_TRY(cudaEventRecordWithFlags(pass_begin, stream, evf));
+      launch_iter<T>(g, mode, want_dual, want_dx, stream);
+      if (pass_end) CUDA_TRY(cudaEventRecordWithFlags(pass_end, stream, evf));
+      launch_iter_confirm<T>(g, stream);  // exits at once unless the gate fired
+      h_iter = k + 1;
+      h_folded = folded_after;
+      return 0;
+    }
     if (pass_begin) CUDA_TRY(cudaEventRecordWithFlags(pass_begin, stream, evf));
     launch_pass<T>(pa, mode, want_dual, want_dx, stream);
     if (pass_end) CUDA_TRY(cudaEventRecordWithFlags(pass_end, stream, evf));
@@ -1026,7 +1122,7 @@ struct Session {
     std::vector<cudaGraphNode_t> deps;
     const cudaStreamCaptureMode cm = cudaStreamCaptureModeThreadLocal;
     int rc = 0;
-    const bool ifnode = gate && !coop;  // the cooperative tail runs its own report
+    const bool ifnode = gate && !coop && !fiter;  // the fused tails run their own report
     for (int64_t it = 0; it < n_iters && rc == 0; ++it) {
       cudaGraphConditionalHandle h = 0;
       if (ifnode) CUDA_TRY(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
@@ -1340,6 +1436,11 @@ struct Session {
 
   // Final status and report (solver.hpp:527-538).
   int finalize_pending() {  // coop tail: patch the last iteration's exact dual / trace terms
+    if (fiter) {  // single-launch iteration: materialize pending duals + patch
+      launch_iter_finalize<T>(iter_args(h_iter, kFold, h_folded), stream);
+      CUDA_TRY(cudaGetLastError());
+      return 0;
+    }
     if (!coop || !tdpart) return 0;
     if (sharded) return xmode == 1 ? shard_patch_pending() : 0;
     TailArgs<T> ta = tail_args(h_iter, kFold, h_folded, true);
@@ -1383,6 +1484,7 @@ struct Session {
 
   // materialize_plan + recover_duals (solver.hpp:188-217)
   int get_plan(T* plan, T* mu, T* nu) {
+    RC_TRY(finalize_pending());
     Book<T> hb;
     RC_TRY(read_book(&hb));
     if (plan) {
@@ -1479,6 +1581,8 @@ struct Session {
     hb.check_every = 1;
     hb.trace_every = 1;
     hb.tol_primal = hb.tol_dual = hb.tol_gap = -1.0;
+    hb.pend_row = -1;
+    hb.phi_mat = 1;
     CUDA_TRY(cudaMemcpyAsync(book, &hb, sizeof(hb), cudaMemcpyHostToDevice, stream));
     CUDA_TRY(cudaStreamSynchronize(stream));
     want_dual = false;  // default PassOptions (solver.hpp:367)
@@ -1493,6 +1597,7 @@ struct Session {
 
   int store_state(T* xy, int32_t* folded, T* rs, T* cs, T* ya, T* yb, T* alpha,
                   T* r, T* s, T* beta, int64_t* iter, bool full) {
+    RC_TRY(finalize_pending());
     Book<T> hb;
     RC_TRY(read_book(&hb));
     RC_TRY(download_matrix(xy, X));

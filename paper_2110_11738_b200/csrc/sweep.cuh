@@ -311,6 +311,9 @@ __device__ __forceinline__ void pass_tile(const PassArgs<T>& a, int64_t c0, int6
 // them in order; completion is per-thread (cp.async.wait_group), so no
 // cross-lane synchronisation is needed for the ring.
 // ---------------------------------------------------------------------------
+#ifndef DROTB_ASYNC_MINB
+#define DROTB_ASYNC_MINB 3  // 3 CTAs (12 warps) per SM: caps registers at 170 (r1 tuning)
+#endif
 #ifndef DROTB_ASYNC_S
 #define DROTB_ASYNC_S 4  // ring stages (S-1 groups in flight)
 #endif
@@ -320,6 +323,23 @@ __device__ __forceinline__ void pass_tile(const PassArgs<T>& a, int64_t c0, int6
 constexpr int kAsyncS = DROTB_ASYNC_S;
 constexpr int kAsyncG = DROTB_ASYNC_G;
 
+// L2 eviction policy of the streamed X / C reads: evict_first keeps the
+// small per-iteration data (strips, records, the Book, kernel code) resident
+// in L2 across the 0.4-80 GB sweep (PassArgs::l2hint; evict_normal otherwise)
+__device__ __forceinline__ uint64_t stream_policy(int evict_first) {
+  uint64_t pol;
+  if (evict_first)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, uint64_t pol) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(sa),
+               "l"(gmem), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
@@ -340,13 +360,71 @@ constexpr size_t async_smem_bytes() {
           static_cast<size_t>(kChunkCols) * 32 * 16);
 }
 
-template <class T, int MODE, bool DUAL, bool DX, bool MASK>
+// v sums of a staged chunk into the CTA's shared-memory column partials
+// (single-launch iteration, iter.cu): slot [warp * NB + b][column - ctile0]
+template <class T>
+__device__ __forceinline__ void v_phase_cta(const T* wbuf, int64_t j0, int cnt, int lane,
+                                            T* svs, int64_t ctile0, int64_t tcs, int warp) {
+  using V = typename V16<T>::type;
+  constexpr int R = 16 / sizeof(T);
+  constexpr int NB = 32 * R / kVBlockRows;
+  constexpr int CH = kChunkCols;
+  if (lane < CH * NB) {
+    const int c = lane % CH, b = lane / CH;
+    if (c < cnt) {
+      const V* col = reinterpret_cast<const V*>(wbuf) + c * 32;
+      const int g7 = c & 7;
+      constexpr int QB = kVBlockRows / R;
+      T s = T(0);
+#pragma unroll
+      for (int qq = 0; qq < QB; ++qq) {
+        T v4[R];
+        unpack(col[(b * QB + qq) ^ g7], v4);
+#pragma unroll
+        for (int t = 0; t < R; ++t) s += v4[t];
+      }
+      svs[(warp * NB + b) * tcs + (j0 + c - ctile0)] = s;
+    }
+  }
+}
+
+// The first S-1 ring stages of pass_tile_async (same slots and addresses),
+// issued by the single-launch iteration before its prologue so that the
+// prologue's dependent loads overlap the first column groups in flight
+template <class T, int MODE>
+__device__ __forceinline__ void ring_prime(const PassArgs<T>& a, int64_t c0, int64_t c1,
+                                           int64_t row0, bool live,
+                                           typename V16<T>::type* ring, int lane) {
+  constexpr bool RC = MODE != kSkip;
+  constexpr int S = kAsyncS, G = RC ? kAsyncG : 2 * kAsyncG;
+  const uint64_t pol = stream_policy(a.l2hint);
+#pragma unroll
+  for (int st = 0; st < S - 1; ++st) {
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      const int64_t col = c0 + st * G + k;
+      if (col < c1 && live) {
+        const int64_t off = col * a.ld + row0;
+        cp_async16_hint(ring + (st * 2 * kAsyncG + k) * 32 + lane, a.xy + off, pol);
+        if (RC) cp_async16_hint(ring + (st * 2 * kAsyncG + kAsyncG + k) * 32 + lane,
+                                a.cost + off, pol);
+      }
+    }
+    cp_async_commit();
+  }
+}
+
+// FUSE (iter.cu): varphi_j comes from the CTA's shared-memory copy svphi
+// (computed in the kernel prologue) and the v sums go to svs
+template <class T, int MODE, bool DUAL, bool DX, bool MASK, bool FUSE = false>
 __device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0, int64_t c1,
                                                 int64_t wrow0, int64_t row0, int nvalid,
                                                 const T (&ph)[16 / sizeof(T)],
                                                 T (&u)[16 / sizeof(T)], PassAcc<T>& acc,
                                                 T* wbuf, typename V16<T>::type* ring,
-                                                int lane) {
+                                                int lane, const T* svphi = nullptr,
+                                                T* svs = nullptr, int64_t tcs = 0,
+                                                int warp = 0) {
   using V = typename V16<T>::type;
   constexpr int R = 16 / sizeof(T);
   constexpr bool RC = MODE != kSkip;
@@ -357,6 +435,7 @@ __device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0
   static_assert(NG % S == 0, "stages must divide the groups of a chunk");
   const bool live = !MASK || nvalid > 0;
   T vb[S][G];
+  const uint64_t pol = stream_policy(a.l2hint);
   auto xslot = [&](int st, int k) { return ring + (st * 2 * kAsyncG + k) * 32 + lane; };
   auto cslot = [&](int st, int k) {
     return ring + (st * 2 * kAsyncG + kAsyncG + k) * 32 + lane;
@@ -369,16 +448,18 @@ __device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0
       if (col < c1) {
         if (live) {
           const int64_t off = col * a.ld + row0;
-          cp_async16(xslot(st, k), a.xy + off);
-          if (RC) cp_async16(cslot(st, k), a.cost + off);
+          cp_async16_hint(xslot(st, k), a.xy + off, pol);
+          if (RC) cp_async16_hint(cslot(st, k), a.cost + off, pol);
         }
-        vb[st][k] = __ldg(a.varphi + col);
+        if (!FUSE) vb[st][k] = __ldg(a.varphi + col);
       }
     }
     cp_async_commit();
   };
+  // FUSE: the caller primed the ring (ring_prime) before its prologue
+  if (!FUSE)
 #pragma unroll
-  for (int st = 0; st < S - 1; ++st) issue(st, c0 + st * G);
+    for (int st = 0; st < S - 1; ++st) issue(st, c0 + st * G);
   for (int64_t j0 = c0; j0 < c1; j0 += CH) {
 #pragma unroll
     for (int gg = 0; gg < NG; ++gg) {
@@ -396,13 +477,17 @@ __device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0
             unpack(*xslot(st, k), x);
             if (RC) unpack(*cslot(st, k), cc);
           }
-          compute_col<T, MODE, DUAL, DX, MASK>(a, x, cc, vb[st][k], col, gg * G + k, row0,
-                                               nvalid, ph, u, acc, wbuf, lane);
+          compute_col<T, MODE, DUAL, DX, MASK>(a, x, cc, FUSE ? svphi[col - c0] : vb[st][k],
+                                               col, gg * G + k, row0, nvalid, ph, u, acc, wbuf,
+                                               lane);
         }
       }
     }
     __syncwarp();
-    v_phase<T>(a, wbuf, j0, static_cast<int>(imin64(CH, c1 - j0)), wrow0, lane);
+    if (FUSE)
+      v_phase_cta<T>(wbuf, j0, static_cast<int>(imin64(CH, c1 - j0)), lane, svs, c0, tcs, warp);
+    else
+      v_phase<T>(a, wbuf, j0, static_cast<int>(imin64(CH, c1 - j0)), wrow0, lane);
     __syncwarp();
   }
   cp_async_wait<0>();
