@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_PASS_MINB)
     pass_tile<T, MODE, DUAL, DX, true, G>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc,
                                           wbuf, lane);
   if (nvalid > 0)
-    *reinterpret_cast<V*>(a.ustrip + gc * a.ld + row0) = pack4(u);
+    st_keep(reinterpret_cast<V*>(a.ustrip + gc * a.ld + row0), pack4(u), a.l2hint);
 
   // deterministic CTA partials: warp tree, then warps in order
   acc.cost = warp_sum(acc.cost);
@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_ASYNC_MINB)
     pass_tile_async<T, MODE, DUAL, DX, true>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc, wbuf,
                                              ring, lane);
   if (nvalid > 0)
-    *reinterpret_cast<V*>(a.ustrip + gc * a.ld + row0) = pack4(u);
+    st_keep(reinterpret_cast<V*>(a.ustrip + gc * a.ld + row0), pack4(u), a.l2hint);
 
   acc.cost = warp_sum(acc.cost);
   acc.prev = warp_sum(acc.prev);

@@ -175,9 +175,12 @@ struct Session {
   bool coop = false, coop_graphs = false, fused_gate = true, pdl_ok = false;
   // single-launch iteration (iter.cu; the default for order=fast on one GPU)
   bool fiter = false;
-  bool l2hint = [] {  // evict_first on the streamed reads: opt-in (no net gain measured)
+  // L2 policies (sweep.cuh): bit 0 evict_first on the streamed X / C reads
+  // (measured slower: off), bit 1 evict_last on the row / column strips K1
+  // leaves for the tail (default: +2 % per iteration at 10k^2, r1n)
+  int l2hint = [] {
     const char* e = std::getenv("DROTB_L2HINT");
-    return e && e[0] == '1';
+    return e ? std::atoi(e) : 2;
   }();
   T *ita = nullptr, *itb = nullptr, *iaprev = nullptr, *ibprev = nullptr;
   T *iugrp = nullptr, *ivcta = nullptr;
@@ -983,7 +986,7 @@ struct Session {
     pa.partials = partials;
     pa.stop = &book->stop;
     pa.pdl = (coop && pdl_ok) ? 1 : 0;
-    pa.l2hint = l2hint ? 1 : 0;
+    pa.l2hint = l2hint;
     return pa;
   }
 

@@ -46,6 +46,43 @@ __device__ __forceinline__ typename V16<T>::type vzero() {
   return z;
 }
 
+// the per-iteration strips / partials K1 writes for the tail: evict_last
+// keeps them in L2 while the sweep streams (PassArgs::l2hint bit 1)
+__device__ __forceinline__ uint64_t keep_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void st_keep(float* p, float v, int hint) {
+  if (hint & 2)
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(keep_policy())
+                 : "memory");
+  else
+    *p = v;
+}
+__device__ __forceinline__ void st_keep(double* p, double v, int hint) {
+  if (hint & 2)
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(keep_policy())
+                 : "memory");
+  else
+    *p = v;
+}
+__device__ __forceinline__ void st_keep(float4* p, float4 v, int hint) {
+  if (hint & 2)
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p),
+                 "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(keep_policy())
+                 : "memory");
+  else
+    *p = v;
+}
+__device__ __forceinline__ void st_keep(double2* p, double2 v, int hint) {
+  if (hint & 2)
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x),
+                 "d"(v.y), "l"(keep_policy())
+                 : "memory");
+  else
+    *p = v;
+}
 template <class T>
 __device__ __forceinline__ T max_finite();
 template <>
@@ -262,7 +299,7 @@ __device__ __forceinline__ void v_phase(const PassArgs<T>& a, const T* wbuf, int
 #pragma unroll
         for (int t = 0; t < R; ++t) s += v4[t];
       }
-      a.vstrip[gb * a.n + j0 + c] = s;
+      st_keep(a.vstrip + gb * a.n + j0 + c, s, a.l2hint);
     }
   }
 }
@@ -328,7 +365,7 @@ constexpr int kAsyncG = DROTB_ASYNC_G;
 // in L2 across the 0.4-80 GB sweep (PassArgs::l2hint; evict_normal otherwise)
 __device__ __forceinline__ uint64_t stream_policy(int evict_first) {
   uint64_t pol;
-  if (evict_first)
+  if (evict_first & 1)
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   else
     asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
