@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_PASS_MINB)
 
   T ph[R], u[R];
   if (nvalid > 0) {
-    unpack(*reinterpret_cast<const V*>(a.phi + row0), ph);
+    unpack(ld_keep(reinterpret_cast<const V*>(a.phi + row0)), ph);
   } else {
 #pragma unroll
     for (int t = 0; t < R; ++t) ph[t] = T(0);
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_PASS_MINB)
       out.max_abs = fmax(out.max_abs, wacc[w].mx);
       out.bad |= wacc[w].bad ? 1 : 0;
     }
-    a.partials[static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x] = out;
+    st_partial_keep(a.partials + static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x, out);
   }
 }
 
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_ASYNC_MINB)
 
   T ph[R], u[R];
   if (nvalid > 0) {
-    unpack(*reinterpret_cast<const V*>(a.phi + row0), ph);
+    unpack(ld_keep(reinterpret_cast<const V*>(a.phi + row0)), ph);
   } else {
 #pragma unroll
     for (int t = 0; t < R; ++t) ph[t] = T(0);
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_ASYNC_MINB)
       out.max_abs = fmax(out.max_abs, wacc[w].mx);
       out.bad |= wacc[w].bad ? 1 : 0;
     }
-    a.partials[static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x] = out;
+    st_partial_keep(a.partials + static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x, out);
   }
 }
 

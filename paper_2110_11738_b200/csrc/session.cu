@@ -178,10 +178,7 @@ struct Session {
   // L2 policies (sweep.cuh): bit 0 evict_first on the streamed X / C reads
   // (measured slower: off), bit 1 evict_last on the row / column strips K1
   // leaves for the tail (default: +2 % per iteration at 10k^2, r1n)
-  int l2hint = [] {
-    const char* e = std::getenv("DROTB_L2HINT");
-    return e ? std::atoi(e) : 2;
-  }();
+  int l2hint = -1;  // resolved in allocate(): 2 while the strips fit a third of L2
   T *ita = nullptr, *itb = nullptr, *iaprev = nullptr, *ibprev = nullptr;
   T *iugrp = nullptr, *ivcta = nullptr;
   IterRowRec<T>* irow = nullptr;
@@ -668,6 +665,13 @@ struct Session {
     const int64_t rows_cta = int64_t(kWarpsPerCta) * 32 * R;
     grid_cols = (n + tc - 1) / tc;
     grid_rows64 = (m + kVBlockRows - 1) / kVBlockRows;
+    {
+      const double strip_bytes =
+          static_cast<double>(sizeof(T)) * (static_cast<double>(grid_cols) * round_up(m, 32) +
+                                            static_cast<double>(grid_rows64) * n);
+      const char* e = std::getenv("DROTB_L2HINT");
+      l2hint = e ? std::atoi(e) : (strip_bytes <= 40e6 ? 2 : 0);
+    }
     n_partials = ((m + rows_cta - 1) / rows_cta) * grid_cols;
     tile_grid_rows = (m + bs - 1) / bs;
     n_tiles = tile_grid_rows * grid_cols;

@@ -83,6 +83,66 @@ __device__ __forceinline__ void st_keep(double2* p, double2 v, int hint) {
   else
     *p = v;
 }
+// loads of the small per-iteration vectors with the same evict_last policy
+// (cg: data written by other CTAs of the same kernel)
+__device__ __forceinline__ float ld_keep(const float* p) {
+  float v;
+  asm volatile("ld.global.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(keep_policy()));
+  return v;
+}
+__device__ __forceinline__ double ld_keep(const double* p) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(keep_policy()));
+  return v;
+}
+__device__ __forceinline__ float ld_keep_cg(const float* p) {
+  float v;
+  asm volatile("ld.global.cg.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(keep_policy()));
+  return v;
+}
+__device__ __forceinline__ double ld_keep_cg(const double* p) {
+  double v;
+  asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(keep_policy()));
+  return v;
+}
+
+__device__ __forceinline__ float ld_keep_nc(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(keep_policy()));
+  return v;
+}
+__device__ __forceinline__ double ld_keep_nc(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(keep_policy()));
+  return v;
+}
+__device__ __forceinline__ float4 ld_keep(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(keep_policy()));
+  return v;
+}
+__device__ __forceinline__ double2 ld_keep(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p), "l"(keep_policy()));
+  return v;
+}
+template <class T>
+struct PassPartial;
+// per-CTA K1 scalars, kept in L2 for the tail
+template <class T>
+__device__ __forceinline__ void st_partial_keep(PassPartial<T>* d, const PassPartial<T>& v) {
+  st_keep(&d->cost, v.cost, 2);
+  st_keep(&d->prev, v.prev, 2);
+  st_keep(&d->dual, v.dual, 2);
+  st_keep(&d->dx, v.dx, 2);
+  st_keep(&d->max_abs, v.max_abs, 2);
+  d->bad = v.bad;
+}
+
 template <class T>
 __device__ __forceinline__ T max_finite();
 template <>
@@ -485,8 +545,13 @@ __device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0
       if (col < c1) {
         if (live) {
           const int64_t off = col * a.ld + row0;
-          cp_async16_hint(xslot(st, k), a.xy + off, pol);
-          if (RC) cp_async16_hint(cslot(st, k), a.cost + off, pol);
+          if (a.l2hint & 1) {
+            cp_async16_hint(xslot(st, k), a.xy + off, pol);
+            if (RC) cp_async16_hint(cslot(st, k), a.cost + off, pol);
+          } else {
+            cp_async16(xslot(st, k), a.xy + off);
+            if (RC) cp_async16(cslot(st, k), a.cost + off);
+          }
         }
         if (!FUSE) vb[st][k] = __ldg(a.varphi + col);
       }

@@ -222,22 +222,22 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
         if (grp < ngr) {
           const int64_t idx = grp * 32 + lane;
           if (idx < m) {
-            const T pi = t.p[idx];
+            const T pi = ld_keep(t.p + idx);
             const T r = tot - pi;
-            t.r_new[idx] = r;
+            st_keep(t.r_new + idx, r, 2);
             pr[0] += r;
             pr[1] += r * r;
-            pd[0] += static_cast<double>(pi) * static_cast<double>(t.a[idx]);
+            pd[0] += static_cast<double>(pi) * static_cast<double>(ld_keep(t.a + idx));
             pd[1] += static_cast<double>(pi) * static_cast<double>(r);
           }
         } else {
           const int64_t j = (grp - ngr) * 32 + lane;
           if (j < n) {
-            const T qj = t.q[j];
+            const T qj = ld_keep(t.q + j);
             const T s = tot - qj;
-            t.s_new[j] = s;
+            st_keep(t.s_new + j, s, 2);
             pr[2] += s * s;
-            pd[2] += static_cast<double>(qj) * static_cast<double>(t.b[j]);
+            pd[2] += static_cast<double>(qj) * static_cast<double>(ld_keep(t.b + j));
             pd[3] += static_cast<double>(qj) * static_cast<double>(s);
           }
         }
@@ -368,33 +368,33 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
     const int64_t TT = static_cast<int64_t>(G) * kTT;
     for (int64_t idx = static_cast<int64_t>(blockIdx.x) * kTT + tid; idx < m + n; idx += TT) {
       if (idx < m) {
-        const T r = __ldcg(t.r_new + idx);
-        const T ph_old = t.phi[idx];
-        const T ai = t.a[idx];
+        const T r = ld_keep_cg(t.r_new + idx);
+        const T ph_old = ld_keep(t.phi + idx);
+        const T ai = ld_keep(t.a + idx);
         const T ph = (ai - T(2) * r + coef) * inv_n;  // solver.hpp:280-282
-        t.phi[idx] = ph;
-        t.a[idx] = ai - r;  // solver.hpp:287
-        part[0] += static_cast<double>(t.p[idx]) * static_cast<double>(ph) / drho;
+        st_keep(t.phi + idx, ph, 2);
+        st_keep(t.a + idx, ai - r, 2);  // solver.hpp:287
+        part[0] += static_cast<double>(ld_keep(t.p + idx)) * static_cast<double>(ph) / drho;
         if (fp) {
           const double d = static_cast<double>(ph) - static_cast<double>(ph_old);
           part[1] += d * d;
           part[2] += d;
-          part[3] += d * (static_cast<double>(r) - static_cast<double>(t.r_old[idx]));
+          part[3] += d * (static_cast<double>(r) - static_cast<double>(ld_keep(t.r_old + idx)));
         }
       } else {
         const int64_t j = idx - m;
-        const T s = __ldcg(t.s_new + j);
-        const T vp_old = t.varphi[j];
-        const T bj = t.b[j];
+        const T s = ld_keep_cg(t.s_new + j);
+        const T vp_old = ld_keep(t.varphi + j);
+        const T bj = ld_keep(t.b + j);
         const T vp = (bj - T(2) * s + coef) * inv_m;  // solver.hpp:283-285
-        t.varphi[j] = vp;
-        t.b[j] = bj - s;  // solver.hpp:288
-        part[4] += static_cast<double>(t.q[j]) * static_cast<double>(vp) / drho;
+        st_keep(t.varphi + j, vp, 2);
+        st_keep(t.b + j, bj - s, 2);  // solver.hpp:288
+        part[4] += static_cast<double>(ld_keep(t.q + j)) * static_cast<double>(vp) / drho;
         if (fp) {
           const double d = static_cast<double>(vp) - static_cast<double>(vp_old);
           part[5] += d * d;
           part[6] += d;
-          part[7] += d * (static_cast<double>(s) - static_cast<double>(t.s_old[j]));
+          part[7] += d * (static_cast<double>(s) - static_cast<double>(ld_keep(t.s_old + j)));
         }
       }
     }

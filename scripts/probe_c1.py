@@ -1,0 +1,17 @@
+"""Dev aid: C1 drot.solve() wall time, first and repeated calls."""
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2110_11738_b200 as drot  # noqa: E402
+
+m = n = 1000
+C = drot.counter_uniform(1, m * n)
+prob = drot.TransportProblem(C.reshape((m, n), order="F"), np.full(m, 1.0 / m), np.full(n, 1.0 / n))
+for k in range(3):
+    t0 = time.perf_counter()
+    res = drot.solve(prob, drot.DrotConfig())
+    print(f"call {k}: {time.perf_counter() - t0:.3f} s, {res.trace.iterations} iterations", flush=True)
