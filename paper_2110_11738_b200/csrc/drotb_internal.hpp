@@ -51,6 +51,10 @@ struct PassArgs {
   const int* stop;      // device stop flag (nullptr: never)
   int32_t pdl;          // launch as a programmatic dependent (after the coop tail)
   int32_t l2hint;       // 1: stream X / C with an L2 evict_first policy (sweep.cuh)
+  int32_t pad_l2;
+  T* __restrict__ vcta;  // non-null (fast order, one GPU): one column-sum row per CTA
+                         // ([row block][n], the 64-row sums combined in shared memory)
+                         // instead of the 64-row vstrip
 };
 
 // Device-resident solver bookkeeping: every scalar of the solve loop

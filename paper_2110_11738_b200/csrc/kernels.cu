@@ -152,12 +152,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_ASYNC_MINB)
 #pragma unroll
   for (int t = 0; t < R; ++t) u[t] = T(0);
   PassAcc<T> acc{T(0), T(0), T(0), T(0), T(0), false};
+  // a.vcta: the 64-row column sums go to shared memory and are combined per CTA
+  T* svs = a.vcta ? reinterpret_cast<T*>(dyn_smem + async_smem_bytes<T>()) : nullptr;
   if (__all_sync(0xffffffffu, nvalid == R))
     pass_tile_async<T, MODE, DUAL, DX, false>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc, wbuf,
-                                              ring, lane);
+                                              ring, lane, nullptr, svs, a.tc, warp);
   else
     pass_tile_async<T, MODE, DUAL, DX, true>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc, wbuf,
-                                             ring, lane);
+                                             ring, lane, nullptr, svs, a.tc, warp);
   if (nvalid > 0)
     st_keep(reinterpret_cast<V*>(a.ustrip + gc * a.ld + row0), pack4(u), a.l2hint);
 
@@ -185,6 +187,22 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_ASYNC_MINB)
     }
     st_partial_keep(a.partials + static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x, out);
   }
+  if (svs) {  // one column-sum row per CTA: 64-row blocks in ascending order
+    constexpr int NB = ROWS_W / kVBlockRows;
+    const int ncol = static_cast<int>(c1 - c0);
+    for (int cc = threadIdx.x; cc < ncol; cc += kWarpsPerCta * 32) {
+      T s = T(0);
+#pragma unroll
+      for (int w = 0; w < kWarpsPerCta * NB; ++w) s += svs[w * a.tc + cc];
+      st_keep(a.vcta + static_cast<int64_t>(blockIdx.x) * a.n + c0 + cc, s, 2);
+    }
+  }
+}
+
+template <class T>
+constexpr size_t vcta_smem_bytes(int64_t tc) {
+  return static_cast<size_t>(kWarpsPerCta) * (32 * (16 / sizeof(T)) / kVBlockRows) *
+         static_cast<size_t>(tc) * sizeof(T);
 }
 
 static int k1_impl() {  // 0 = register double buffer, 1 = cp.async ring
@@ -203,10 +221,11 @@ static void launch_pass_t(const PassArgs<T>& a, cudaStream_t st) {
   dim3 grid(static_cast<unsigned>((a.m + rows_cta - 1) / rows_cta),
             static_cast<unsigned>((a.n + a.tc - 1) / a.tc));
   if (k1_impl() == 1) {
-    constexpr size_t smem = async_smem_bytes<T>();
+    const size_t smem = async_smem_bytes<T>() + (a.vcta ? vcta_smem_bytes<T>(a.tc) : 0);
     static bool attr = [] {
       cudaFuncSetAttribute(pass_kernel_async<T, MODE, DUAL, DX>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(async_smem_bytes<T>() + vcta_smem_bytes<T>(256)));
       return true;
     }();
     (void)attr;

@@ -175,6 +175,8 @@ struct Session {
   bool coop = false, coop_graphs = false, fused_gate = true, pdl_ok = false;
   // single-launch iteration (iter.cu; the default for order=fast on one GPU)
   bool fiter = false;
+  T* vcta_buf = nullptr;  // [row block][n] per-CTA column sums (coop tail, one GPU)
+  int64_t vcta_rows = 0;
   // L2 policies (sweep.cuh): bit 0 evict_first on the streamed X / C reads
   // (measured slower: off), bit 1 evict_last on the row / column strips K1
   // leaves for the tail (default: +2 % per iteration at 10k^2, r1n)
@@ -215,7 +217,10 @@ struct Session {
                     p, q, u, v, ustrip, vstrip, tscr, partials, tiles, dscr,
                     terms, book, trace, vflags, pack, pmax, dpack, dint,
                     pustrip, pvstrip, pcpart, pdpart, pbar, pseg_ptr, pseg_slot, psweep_ns, pmud, tcpart, tdpart, tbar, tstamps,
-                    ita, itb, iaprev, ibprev, iugrp, ivcta, irow, icol, iurow, iucol, idpart, icnt};
+                    ita, itb, iaprev, ibprev, iugrp, ivcta, irow, icol, iurow, iucol, idpart, icnt,
+                    vcta_buf};
+    vcta_buf = nullptr;
+    vcta_rows = 0;
     ita = itb = iaprev = ibprev = iugrp = ivcta = nullptr;
     irow = nullptr;
     icol = nullptr;
@@ -384,6 +389,17 @@ struct Session {
       }
     CUDA_TRY(cudaStreamSynchronize(stream));
     coop = true;
+    if (!sharded && !no_persist) {  // K1 leaves one column-sum row per CTA for the tail
+      const char* k1 = std::getenv("DROTB_K1");
+      const char* vc = std::getenv("DROTB_VCTA");
+      // opt-in: measured ~1 us per iteration slower at 10k^2 (the in-CTA
+      // combine costs the sweep more than the shorter merge saves)
+      if (!(k1 && k1[0] == 'r') && vc && vc[0] == '1') {
+        constexpr int R = 16 / sizeof(T);
+        vcta_rows = (m + int64_t(kWarpsPerCta) * 32 * R - 1) / (int64_t(kWarpsPerCta) * 32 * R);
+        RC_TRY(dev_alloc(&vcta_buf, static_cast<size_t>(vcta_rows) * static_cast<size_t>(n)));
+      }
+    }
     // can a cooperative launch be captured into a graph here?  (probe on a
     // private stream; the captured launch is never executed)
     coop_graphs = false;
@@ -991,6 +1007,8 @@ struct Session {
     pa.stop = &book->stop;
     pa.pdl = (coop && pdl_ok) ? 1 : 0;
     pa.l2hint = l2hint;
+    pa.pad_l2 = 0;
+    pa.vcta = (coop && !exact && !sharded) ? vcta_buf : nullptr;
     return pa;
   }
 
@@ -1038,6 +1056,10 @@ struct Session {
     t.pmax = pmax;
     t.dpack = dpack;
     if (sharded) t.v = pack;  // the merge writes the local v partial into the pack
+    if (coop && !exact && !sharded && vcta_buf) {  // the strips K1 wrote
+      t.vstrip = vcta_buf;
+      t.grid_rows64 = vcta_rows;
+    }
     t.report_x = X;
     t.report_c = C;
     t.stamps = tstamps;

@@ -586,7 +586,7 @@ __device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0
       }
     }
     __syncwarp();
-    if (FUSE)
+    if (FUSE || svs)
       v_phase_cta<T>(wbuf, j0, static_cast<int>(imin64(CH, c1 - j0)), lane, svs, c0, tcs, warp);
     else
       v_phase<T>(a, wbuf, j0, static_cast<int>(imin64(CH, c1 - j0)), wrow0, lane);
