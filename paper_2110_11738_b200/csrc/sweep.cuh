@@ -425,7 +425,7 @@ constexpr int kAsyncG = DROTB_ASYNC_G;
 // in L2 across the 0.4-80 GB sweep (PassArgs::l2hint; evict_normal otherwise)
 __device__ __forceinline__ uint64_t stream_policy(int evict_first) {
   uint64_t pol;
-  if (evict_first & 1)
+  if (evict_first & 5)
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   else
     asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
@@ -545,12 +545,16 @@ __device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0
       if (col < c1) {
         if (live) {
           const int64_t off = col * a.ld + row0;
-          if (a.l2hint & 1) {
+          // bit 0: evict_first on X and C; bit 2: on C only (read-only here)
+          if (a.l2hint & 1)
             cp_async16_hint(xslot(st, k), a.xy + off, pol);
-            if (RC) cp_async16_hint(cslot(st, k), a.cost + off, pol);
-          } else {
+          else
             cp_async16(xslot(st, k), a.xy + off);
-            if (RC) cp_async16(cslot(st, k), a.cost + off);
+          if (RC) {
+            if (a.l2hint & 5)
+              cp_async16_hint(cslot(st, k), a.cost + off, pol);
+            else
+              cp_async16(cslot(st, k), a.cost + off);
           }
         }
         if (!FUSE) vb[st][k] = __ldg(a.varphi + col);

@@ -117,3 +117,27 @@ def test_fused_gate_matches_exact_gate(drot, dt):
         for f in ("gap", "fixed_point_residual", "objective", "r_primal"):
             x, y = getattr(ra, f), getattr(rb, f)
             assert x == y or (np.isnan(x) and np.isnan(y)) or abs(x - y) <= 1e-6 * max(abs(y), 1e-12), (ra.iter, f, x, y)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_l2_policies_do_not_change_results(drot, dt):
+    """DROTB_L2HINT only changes L2 eviction priorities (sweep.cuh): the
+    iterates must be bitwise identical with and without them."""
+    runs = []
+    for hint in ("0", "3"):
+        with _env(DROTB_L2HINT=hint):
+            runs.append(_run(drot, 700, 500, dt, iters=40, tol_primal=-1.0, max_iters=10 ** 9))
+    a, b = runs
+    assert a[0][1] == b[0][1] == 40
+    for x, y in zip(a[1:], b[1:]):
+        np.testing.assert_array_equal(x, y)
+
+
+def test_vcta_rows_close_to_strips(drot):
+    """DROTB_VCTA=1 (per-CTA column-sum rows) changes only the association of
+    the column sums: fixed-iteration fp64 iterates agree to rounding."""
+    with _env(DROTB_VCTA="1"):
+        a = _run(drot, 700, 500, np.float64, iters=40, tol_primal=-1.0, max_iters=10 ** 9)
+    b = _run(drot, 700, 500, np.float64, iters=40, tol_primal=-1.0, max_iters=10 ** 9)
+    for x, y in zip(a[1:], b[1:]):
+        assert float(np.abs(x - y).max()) <= 1e-12 * max(1.0, float(np.abs(y).max()))
