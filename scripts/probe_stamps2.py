@@ -20,7 +20,7 @@ for (m, n, dt) in [(10000, 10000, np.float32), (1000, 1000, np.float64)]:
         v = np.array(list(buf), dtype=np.float64)
         acc += (v[1:8] - v[0]) / 1e3
     acc /= K
-    names = ["A done", "RB1 done", "all past RB1", "B done", "last CTA enters", "sums done", "thread0 done"]
+    names = ["A done", "RB1 done", "all past RB1", "B done", "loads issued", "warp sums done", "thread0 sums done"]
     print(f"{m}x{n} {np.dtype(dt).name}: " + ", ".join(f"{nm} {x:.1f}" for nm, x in zip(names, acc)) + " us after first CTA entry")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st); s.enqueue(50); e1.record(st); torch.cuda.synchronize()
