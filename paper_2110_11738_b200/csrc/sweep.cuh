@@ -419,6 +419,14 @@ __device__ __forceinline__ void pass_tile(const PassArgs<T>& a, int64_t c0, int6
 #endif
 constexpr int kAsyncS = DROTB_ASYNC_S;
 constexpr int kAsyncG = DROTB_ASYNC_G;
+// skip sweeps (no C): the same ring as kAsyncS stages of 2*kAsyncG columns
+// of X; DROTB_SKIP_FINE builds 2*kAsyncS stages of kAsyncG columns (more
+// columns in flight -- measured equal at 10k^2, r1o)
+#ifdef DROTB_SKIP_FINE
+constexpr int kSkipS = 2 * kAsyncS, kSkipG = kAsyncG;
+#else
+constexpr int kSkipS = kAsyncS, kSkipG = 2 * kAsyncG;
+#endif
 
 // L2 eviction policy of the streamed X / C reads: evict_first keeps the
 // small per-iteration data (strips, records, the Book, kernel code) resident
@@ -493,7 +501,8 @@ __device__ __forceinline__ void ring_prime(const PassArgs<T>& a, int64_t c0, int
                                            int64_t row0, bool live,
                                            typename V16<T>::type* ring, int lane) {
   constexpr bool RC = MODE != kSkip;
-  constexpr int S = kAsyncS, G = RC ? kAsyncG : 2 * kAsyncG;
+  constexpr int S = RC ? kAsyncS : kSkipS, G = RC ? kAsyncG : kSkipG;
+  constexpr int SLOTS = 2 * kAsyncG * kAsyncS / S;  // 16-B slots per lane and stage
   const uint64_t pol = stream_policy(a.l2hint);
 #pragma unroll
   for (int st = 0; st < S - 1; ++st) {
@@ -502,9 +511,9 @@ __device__ __forceinline__ void ring_prime(const PassArgs<T>& a, int64_t c0, int
       const int64_t col = c0 + st * G + k;
       if (col < c1 && live) {
         const int64_t off = col * a.ld + row0;
-        cp_async16_hint(ring + (st * 2 * kAsyncG + k) * 32 + lane, a.xy + off, pol);
-        if (RC) cp_async16_hint(ring + (st * 2 * kAsyncG + kAsyncG + k) * 32 + lane,
-                                a.cost + off, pol);
+        cp_async16_hint(ring + (st * SLOTS + k) * 32 + lane, a.xy + off, pol);
+        if (RC) cp_async16_hint(ring + (st * SLOTS + kAsyncG + k) * 32 + lane, a.cost + off,
+                                pol);
       }
     }
     cp_async_commit();
@@ -527,16 +536,16 @@ __device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0
   constexpr bool RC = MODE != kSkip;
   // a stage holds 2*kAsyncG 16-B slots per lane: G columns of X and C, or --
   // on skip sweeps, which read no C -- 2G columns of X (same bytes in flight)
-  constexpr int S = kAsyncS, G = RC ? kAsyncG : 2 * kAsyncG, CH = kChunkCols;
+  constexpr int S = RC ? kAsyncS : kSkipS, G = RC ? kAsyncG : kSkipG, CH = kChunkCols;
+  constexpr int SLOTS = 2 * kAsyncG * kAsyncS / S;  // 16-B slots per lane and stage
   constexpr int NG = CH / G;
   static_assert(NG % S == 0, "stages must divide the groups of a chunk");
+  static_assert(SLOTS >= G * (RC ? 2 : 1), "ring slots per stage");
   const bool live = !MASK || nvalid > 0;
   T vb[S][G];
   const uint64_t pol = stream_policy(a.l2hint);
-  auto xslot = [&](int st, int k) { return ring + (st * 2 * kAsyncG + k) * 32 + lane; };
-  auto cslot = [&](int st, int k) {
-    return ring + (st * 2 * kAsyncG + kAsyncG + k) * 32 + lane;
-  };
+  auto xslot = [&](int st, int k) { return ring + (st * SLOTS + k) * 32 + lane; };
+  auto cslot = [&](int st, int k) { return ring + (st * SLOTS + kAsyncG + k) * 32 + lane; };
   auto issue = [&](int st, int64_t jg) {
 #pragma unroll
     for (int k = 0; k < G; ++k) {
