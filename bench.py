@@ -169,7 +169,9 @@ def run_reference_arm(args, rank, world):
         return
     m = n = args.size
     est = 0.3  # s/iter, conservative for 10k^2 fp32 on a multi-core host
-    k = max(1, min(args.steps, int(150 / est)))
+    # >= 30 iterations: the difference of two solve() calls must dominate
+    # their fixed costs (init / validation / report sweeps)
+    k = max(30, min(args.steps, int(150 / est)))
     ips, cores, kind, k_run, total = reference_iters_per_s(m, n, k, 1)
     line = {
         "impl": "reference", "metric": METRIC, "value": ips, "unit": UNIT,
@@ -179,7 +181,8 @@ def run_reference_arm(args, rank, world):
         "config": workload_config(m, n, "reference CPU deterministic tile order"),
         "cpu_baseline": {"value": ips, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": f"{k_run} solve-loop iterations (difference of solve(max_iters=1) "
-                                   f"and solve(max_iters={1 + k_run})), {total:.1f} s wall"},
+                                   f"and solve(max_iters={1 + k_run}) after a warm "
+                                   f"solve(max_iters=1)), {total:.1f} s wall"},
         "e2e": {"value": ips, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -361,7 +364,8 @@ def run_b200(args, rank, world, local_rank):
             "value": ips, "unit": UNIT, "cores": cores, "kind": kind,
             "sample": f"{k_run} iterations of reference solve<float> on the same 10k x 10k fp32 "
                       f"instance (difference of solve(max_iters=1) and solve(max_iters="
-                      f"{1 + k_run})), {total:.1f} s wall, {cores} host threads"}
+                      f"{1 + k_run}) after a warm solve(max_iters=1)), {total:.1f} s wall, "
+                      f"{cores} host threads"}
     # ---- time to tolerance (C1: 1000x1000 fp64, the results-oracle config) --
     if rank == 0 and not args.no_ttt:
         out["time_to_tol"] = time_to_tol(drot)
