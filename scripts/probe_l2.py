@@ -8,7 +8,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2110_11738_b200 as drot  # noqa: E402
 
 for dt in (np.float32, np.float64):
-    for hint in ("2", "2"):
+    for hint in ("2",):
         os.environ["DROTB_L2HINT"] = hint
         m = n = 10000
         s = drot.Session(m, n, dt, drot.DrotConfig(tol_primal=-1.0, max_iters=10 ** 9))
