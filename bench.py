@@ -249,7 +249,9 @@ def run_b200(args, rank, world, local_rank):
     else:
         m_global = m
         sess = drot.Session(m, n, dt, cfg)
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated stream: the session would ignore the legacy default stream
+    # (handle 0) and keep its own, and the timing events must be on its stream
+    stream = torch.cuda.Stream(dev)
     sess.set_stream(stream.cuda_stream)
     sess.gen_gaussian(5.0, 0, "dyadic")  # K7: generated on the device
     sess.init()
@@ -261,6 +263,26 @@ def run_b200(args, rank, world, local_rank):
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.3)
+    pgrid = sess.persistent_grid
+    plain_ms = None
+    if not pgrid:
+        # the timed region: K steps (CUDA graphs of the solve loop) between two
+        # CUDA events on the session stream -- no per-launch event nodes,
+        # which cost ~10 us per step (scripts/probe_events.py)
+        barrier()
+        torch.cuda.synchronize()
+        l0 = drot.kernel_launches()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        sess.enqueue(args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        plain_ms = ev0.elapsed_time(ev1)
+        plain_launches = drot.kernel_launches() - l0
+    # per-launch timing pass (roofline): the same K steps again with an event
+    # pair around every K1 launch (the whole step for the persistent kernel)
     barrier()
     torch.cuda.synchronize()
     r = sess.run_timed(args.steps)
@@ -268,13 +290,12 @@ def run_b200(args, rank, world, local_rank):
     barrier()
     clk = clocks.stop()
 
-    ms = r["total_ms"]
+    ms = r["total_ms"] if plain_ms is None else plain_ms
     if dist is not None:
         t = torch.tensor([ms], device="cpu" if share else dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = world * args.steps / (ms / 1e3)
-    pgrid = sess.persistent_grid
     peak, peak_src = measured_hbm_peak()
     step_bytes_gbs = r["pass_bytes"] / (r["total_ms"] / 1e3) / 1e9
     sweep_ms_avg = r["pass_ms"] / r["n_pass"]
@@ -310,7 +331,11 @@ def run_b200(args, rank, world, local_rank):
             "bytes_model": "3*4*m*n on C-reading (fold) sweeps, 2*4*m*n on skip sweeps "
                            "(SURVEY §8(d)); averaged over the timed launches",
             "kernel_ms_avg": sweep_ms_avg,
-            "kernel_share_of_step": r["pass_ms"] / r["total_ms"],
+            "kernel_share_of_step": sweep_ms_avg * args.steps / ms,
+            "timing": "K1 launch durations from CUDA event pairs around every K1 launch in a "
+                      "second pass of the same K steps on the session stream (the headline "
+                      "value is timed without those event nodes, ~10 us per step); share = "
+                      "K1 time / timed-region step",
             "traffic": ncu_traffic(m, n, "f32"),
         }
     st, it_done, _ = sess.status()
@@ -336,7 +361,7 @@ def run_b200(args, rank, world, local_rank):
             "hbm_gbs_step": step_bytes_gbs,
             "roofline": roof,
             "clocks": clk,
-            "gpu_launches": r["launches"],
+            "gpu_launches": r["launches"] if plain_ms is None else plain_launches,
         }
     # ---- time to 1e-4 on the headline instance (every rank) -----------------
     if not args.no_ttt:
@@ -411,7 +436,7 @@ def run_e2e(args, drot, torch, m, n, local_rank):
 def c2_f64(drot, torch, m, n, iters=100):
     """C2 in fp64: same loop, 24 / 16 bytes per entry on fold / skip sweeps."""
     s = drot.Session(m, n, np.float64, drot.DrotConfig(tol_primal=-1.0, max_iters=10 ** 12))
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()
     s.set_stream(stream.cuda_stream)
     s.gen_gaussian(5.0, 0, "dyadic")
     s.init()
@@ -464,7 +489,7 @@ def c5_single(args, drot, torch, size=100000, iters=20):
         return {"skipped": f"needs {need / 1e9:.0f} GB, {free / 1e9:.0f} GB free"}
     t0 = time.perf_counter()
     s = drot.Session(size, size, np.float32, drot.DrotConfig(tol_primal=-1.0, max_iters=10 ** 12))
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()
     s.set_stream(stream.cuda_stream)
     s.gen_gaussian(5.0, 0, "dyadic")
     s.init()
@@ -499,7 +524,7 @@ def time_to_tol_c2(args, drot, torch, dist, m, n, m_global, rank, world, local_r
         sess = make_shard(drot, dist, args, m_global, n, np.float32, cfg, rank, world)
     else:
         sess = drot.Session(m, n, np.float32, cfg)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()
     sess.set_stream(stream.cuda_stream)
     sess.gen_gaussian(5.0, 0, "dyadic")
     sess.init()
