@@ -37,17 +37,18 @@ METRIC = "DROT iterations/s (m=n=10000 fp32, Gaussian squared-Euclidean cost)"
 UNIT = "iter/s"
 
 
-def workload_config(m, n, order, extra=None):
-    cfg = {
+def workload_config(m, n, world=1):
+    """The workload keys both arms share (identical at the same N)."""
+    return {
         "workload": f"C2: m=n={m} fp32 DROT solve loop on gen_gaussian_problem(seed=0, "
                     "sigma_t=5) cost, dyadic-uniform marginals, rho0=2, tol 1e-4, "
                     "skip_cost=true, record_trace=true (reference defaults)",
-        "m": m, "n": n, "reduction_order": order,
+        "m": m, "n": n,
         "l2_policy": "inputs larger than L2 (X + C = %.0f MB vs 126 MB L2)" % (8.0 * m * n / 1e6),
+        "parallelism": "1 GPU" if world == 1 else
+                       f"row-sharded over {world} GPUs (weak scaling: {world * m}x{n}, {m} "
+                       "rows per GPU)",
     }
-    if extra:
-        cfg.update(extra)
-    return cfg
 
 
 # ---------------------------------------------------------------------------
@@ -114,16 +115,13 @@ def measured_hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(m, n, dtype, iters=None):
-    """DRAM bytes per launch from the committed ncu capture (profiles/), if
-    any: per K1 sweep launch, or -- persistent kernel, `iters` iterations per
-    launch -- the captured bytes per iteration times `iters`."""
+def ncu_traffic(m, n, dtype):
+    """DRAM bytes per K1 launch (fold / skip average) from the committed ncu
+    capture (profiles/ncu_pass_summary.json), if any."""
     path = os.path.join(ROOT, "profiles", "ncu_pass_summary.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        if iters:
-            return d[f"solve_{m}x{n}_{dtype}"]["dram_bytes_per_iteration"] * iters
         return d[f"pass_{m}x{n}_{dtype}"]["dram_bytes_per_launch_avg"]
     except Exception:
         return None
@@ -147,42 +145,44 @@ def reference_problem(m, n):
 def reference_iters_per_s(m, n, iters, warm):
     """Per-iteration wall time of the reference solve<float> loop on all host
     threads: solve(max_iters=warm) and solve(max_iters=warm+iters) with
-    unreachable tolerances; the difference isolates `iters` iterations."""
+    unreachable tolerances (reference defaults otherwise, record_trace on);
+    the difference isolates `iters` iterations."""
     orc, kind, C, p, q, default_config = reference_problem(m, n)
     cores = orc.hardware_workers() if kind == "reference" else 1
     cfg = default_config(tol_primal=-1.0, tol_dual=-1.0, tol_gap=-1.0, record_trace=1)
     if kind == "reference":
-        spi, tot = orc.time_iters(C, p, q, m, n, iters, cfg)
+        spi, tot = orc.time_iters(C, p, q, m, n, iters, cfg, warm=warm)
         return 1.0 / spi, cores, kind, iters, tot
     t0 = time.perf_counter()
     cfg.max_iters = warm
-    orc.solve(C, p, q, m, n, cfg, trace_cap=0)
+    orc.solve(C, p, q, m, n, cfg)
     t1 = time.perf_counter()
     cfg.max_iters = warm + iters
-    orc.solve(C, p, q, m, n, cfg, trace_cap=0)
+    orc.solve(C, p, q, m, n, cfg)
     t2 = time.perf_counter()
     return iters / ((t2 - t1) - (t1 - t0)), cores, kind, iters, t2 - t0
 
 
 def run_reference_arm(args, rank, world):
+    """The reference's own CPU solve loop (oracle/_ref = the unmodified
+    reference compiled here) on all host threads, on the B200 arm's workload:
+    exactly --steps timed iterations after --warmup ones."""
     if rank != 0:
         return
     m = n = args.size
-    est = 0.3  # s/iter, conservative for 10k^2 fp32 on a multi-core host
-    # >= 30 iterations: the difference of two solve() calls must dominate
-    # their fixed costs (init / validation / report sweeps)
-    k = max(30, min(args.steps, int(150 / est)))
-    ips, cores, kind, k_run, total = reference_iters_per_s(m, n, k, 1)
+    w = max(args.warmup, 1)
+    ips, cores, kind, k_run, total = reference_iters_per_s(m, n, args.steps, w)
     line = {
         "impl": "reference", "metric": METRIC, "value": ips, "unit": UNIT,
-        "n_gpus": world, "steps": k_run, "warmup": 1, "ms_per_step": 1e3 / ips,
+        "n_gpus": world, "steps": k_run, "warmup": w, "ms_per_step": 1e3 / ips,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (reference gen_gaussian_problem, seed 0)",
-        "config": workload_config(m, n, "reference CPU deterministic tile order"),
+        "config": workload_config(m, n, 1),
+        "reduction_order": "reference CPU deterministic tile order",
         "cpu_baseline": {"value": ips, "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": f"{k_run} solve-loop iterations (difference of solve(max_iters=1) "
-                                   f"and solve(max_iters={1 + k_run}) after a warm "
-                                   f"solve(max_iters=1)), {total:.1f} s wall"},
+                         "sample": f"{k_run} solve-loop iterations with record_trace on "
+                                   f"(solve(max_iters={w + k_run}) - solve(max_iters={w}), best of 2 calls each), "
+                                   f"{total:.1f} s wall, {cores} host threads"},
         "e2e": {"value": ips, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -256,33 +256,40 @@ def run_b200(args, rank, world, local_rank):
     sess.gen_gaussian(5.0, 0, "dyadic")  # K7: generated on the device
     sess.init()
     # warmup: W iterations (graphs captured, clocks up)
+    # warm-up: W iterations (>= 3), rounded up to an even count so that the
+    # timed steps start from an even, unfolded state (every CUDA graph of the
+    # solve loop covers an even/odd iteration pair); then every graph the
+    # timed enqueue(K) launches is captured up front (prepare), so the timed
+    # region launches graphs and captures nothing
     w = max(args.warmup, 3)
-    sess.run_timed(w)
+    w += w & 1
+    sess.enqueue(w)
+    sess.prepare(args.steps)
     torch.cuda.synchronize()
+    builds0 = sess.graph_builds
 
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.3)
-    pgrid = sess.persistent_grid
-    plain_ms = None
-    if not pgrid:
-        # the timed region: K steps (CUDA graphs of the solve loop) between two
-        # CUDA events on the session stream -- no per-launch event nodes,
-        # which cost ~10 us per step (scripts/probe_events.py)
-        barrier()
-        torch.cuda.synchronize()
-        l0 = drot.kernel_launches()
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        sess.enqueue(args.steps)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        barrier()
-        plain_ms = ev0.elapsed_time(ev1)
-        plain_launches = drot.kernel_launches() - l0
+    # the timed region: K steps (CUDA graphs of the solve loop) between two
+    # CUDA events on the session stream -- no per-launch event nodes, which
+    # cost ~10 us per step (scripts/probe_events.py)
+    barrier()
+    torch.cuda.synchronize()
+    l0 = drot.kernel_launches()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    sess.enqueue(args.steps)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = drot.kernel_launches() - l0
+    captures = sess.graph_builds - builds0
+    assert captures == 0, f"{captures} graph captures inside the timed region"
     # per-launch timing pass (roofline): the same K steps again with an event
-    # pair around every K1 launch (the whole step for the persistent kernel)
+    # pair around every K1 launch
     barrier()
     torch.cuda.synchronize()
     r = sess.run_timed(args.steps)
@@ -290,54 +297,32 @@ def run_b200(args, rank, world, local_rank):
     barrier()
     clk = clocks.stop()
 
-    ms = r["total_ms"] if plain_ms is None else plain_ms
     if dist is not None:
         t = torch.tensor([ms], device="cpu" if share else dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = world * args.steps / (ms / 1e3)
     peak, peak_src = measured_hbm_peak()
-    step_bytes_gbs = r["pass_bytes"] / (r["total_ms"] / 1e3) / 1e9
     sweep_ms_avg = r["pass_ms"] / r["n_pass"]
     bytes_avg = r["pass_bytes"] / r["n_pass"]
-    if pgrid:
-        # the persistent solver kernel IS the step: one launch of K iterations
-        # between two CUDA events; its sweep phases are timed inside the kernel
-        roof = {
-            "bound": "hbm",
-            "kernel": f"solve_kernel (persistent, {pgrid} CTAs: sweep + merge + update + "
-                      "gate phases of every iteration, grid barriers between phases)",
-            "achieved": step_bytes_gbs, "peak": peak, "unit": "GB/s",
-            "frac": step_bytes_gbs / peak, "peak_source": peak_src,
-            "algorithmic_bytes_per_launch": r["pass_bytes"],
-            "bytes_model": "per iteration 3*4*m*n on C-reading (fold) sweeps, 2*4*m*n on skip "
-                           "sweeps (SURVEY §8(d)); summed over the K iterations of the launch",
-            "kernel_ms_avg": r["total_ms"],
-            "kernel_share_of_step": 1.0,
-            "sweep_phase": {"ms_avg": sweep_ms_avg,
-                            "gbs": bytes_avg / (sweep_ms_avg / 1e3) / 1e9,
-                            "share_of_step": r["pass_ms"] / r["total_ms"],
-                            "how": "%globaltimer in CTA 0 from iteration start to the barrier "
-                                   "after the sweep (includes barrier skew)"},
-            "traffic": ncu_traffic(m, n, "f32", args.steps),
-        }
-    else:
-        achieved = bytes_avg / (sweep_ms_avg / 1e3) / 1e9
-        roof = {
-            "bound": "hbm", "kernel": "pass_kernel (fused DROT sweep, K1)",
-            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "peak_source": peak_src,
-            "algorithmic_bytes_per_launch": bytes_avg,
-            "bytes_model": "3*4*m*n on C-reading (fold) sweeps, 2*4*m*n on skip sweeps "
-                           "(SURVEY §8(d)); averaged over the timed launches",
-            "kernel_ms_avg": sweep_ms_avg,
-            "kernel_share_of_step": sweep_ms_avg * args.steps / ms,
-            "timing": "K1 launch durations from CUDA event pairs around every K1 launch in a "
-                      "second pass of the same K steps on the session stream (the headline "
-                      "value is timed without those event nodes, ~10 us per step); share = "
-                      "K1 time / timed-region step",
-            "traffic": ncu_traffic(m, n, "f32"),
-        }
+    step_bytes_gbs = bytes_avg * args.steps / (ms / 1e3) / 1e9
+    achieved = bytes_avg / (sweep_ms_avg / 1e3) / 1e9
+    roof = {
+        "bound": "hbm", "kernel": "pass_kernel_async (fused DROT sweep, K1)",
+        "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+        "peak_source": peak_src,
+        "algorithmic_bytes_per_launch": bytes_avg,
+        "bytes_model": "3*4*m*n on C-reading (fold) sweeps, 2*4*m*n on skip sweeps "
+                       "(SURVEY §8(d)); averaged over the timed launches",
+        "kernel_ms_avg": sweep_ms_avg,
+        "kernel_share_of_step": sweep_ms_avg * args.steps / ms,
+        "step_frac_of_peak": step_bytes_gbs / peak,
+        "timing": "K1 launch durations from CUDA event pairs around every K1 launch in a "
+                  "second pass of the same K steps on the session stream (the headline "
+                  "value is timed without those event nodes, ~10 us per step); share = "
+                  "K1 time / timed-region step",
+        "traffic": ncu_traffic(m, n, "f32"),
+    }
     st, it_done, _ = sess.status()
     sess.close()
     del sess
@@ -351,17 +336,14 @@ def run_b200(args, rank, world, local_rank):
             "dtype": "f32",
             "data": "synthetic (gen_gaussian_problem seed 0 generated on the device, bit-identical "
                     "to the reference generator; inputs resident in HBM)",
-            "config": workload_config(m, n, order, {
-                "parallelism": (f"row-sharded over {world} GPUs: one {m_global}x{n} problem, "
-                                f"{m} rows per GPU, per-iteration exchange of the n column "
-                                f"sums + scalars: {args.exchange} ('p2p' = fused into the "
-                                "cooperative tail over NVLink peer memory); value counts "
-                                "10k x 10k iteration-equivalents (world x iterations/s)")
-                if world > 1 else "1 GPU"}),
+            "config": workload_config(m, n, world),
+            "reduction_order": order,
+            "exchange": args.exchange if world > 1 else None,
             "hbm_gbs_step": step_bytes_gbs,
             "roofline": roof,
             "clocks": clk,
-            "gpu_launches": r["launches"] if plain_ms is None else plain_launches,
+            "gpu_launches": launches,
+            "graph_captures_in_timed_region": captures,
         }
     # ---- time to 1e-4 on the headline instance (every rank) -----------------
     if not args.no_ttt:
@@ -388,9 +370,8 @@ def run_b200(args, rank, world, local_rank):
         out["cpu_baseline"] = {
             "value": ips, "unit": UNIT, "cores": cores, "kind": kind,
             "sample": f"{k_run} iterations of reference solve<float> on the same 10k x 10k fp32 "
-                      f"instance (difference of solve(max_iters=1) and solve(max_iters="
-                      f"{1 + k_run}) after a warm solve(max_iters=1)), {total:.1f} s wall, "
-                      f"{cores} host threads"}
+                      f"instance, record_trace on (solve(max_iters={1 + k_run}) - "
+                      f"solve(max_iters=1)), {total:.1f} s wall, {cores} host threads"}
     # ---- time to tolerance (C1: 1000x1000 fp64, the results-oracle config) --
     if rank == 0 and not args.no_ttt:
         out["time_to_tol"] = time_to_tol(drot)

@@ -325,9 +325,6 @@ int drotb_session_gen_uniform(drotb_session* s, uint64_t seed, double lo, double
  * ranks when row-sharded (collective).  SURVEY §8(c) support parity. */
 int drotb_session_support(drotb_session* s, double rel_tau, double abs_tau, int64_t* nnz,
                           double* xmax);
-/* CTAs of the persistent solver kernel this session runs its iterations
- * with (fast order, one GPU; 0 = per-launch kernels + CUDA graphs). */
-int32_t drotb_session_persistent_grid(drotb_session* s);
 /* Profiling aid (sessions created with DROTB_TAIL_STAMPS=1): copy and reset
  * 8 %globaltimer stamps (ns) of the cooperative tail: [0] first CTA entry
  * (min), [1] last arrival at the merge barrier, [2] merge totals done,
@@ -344,6 +341,12 @@ int drotb_session_init(drotb_session* s, const void* x0);
 /* Enqueue up to n_iters iterations of the solve loop (gating included) on
  * the session stream; returns without synchronizing. */
 int drotb_session_enqueue(drotb_session* s, int64_t n_iters);
+/* Capture and instantiate (without launching) every CUDA graph that
+ * drotb_session_enqueue(s, n_iters) would launch from the current state, so
+ * that a timed enqueue of the same length captures nothing. */
+int drotb_session_prepare(drotb_session* s, int64_t n_iters);
+/* Number of CUDA graphs this session has captured and instantiated. */
+int64_t drotb_session_graph_builds(drotb_session* s);
 /* Run the loop to termination (converged / max_iters / failure). */
 int drotb_session_run(drotb_session* s);
 int drotb_session_synchronize(drotb_session* s);

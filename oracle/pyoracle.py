@@ -282,18 +282,21 @@ class Oracle:
         return {k: getattr(rep, k) for k, _ in OrcReport._fields_}
 
     # -- reference-only helpers ---------------------------------------------
-    def time_iters(self, cost, p, q, m, n, k, cfg: OrcConfig | None = None):
+    def time_iters(self, cost, p, q, m, n, k, cfg: OrcConfig | None = None, warm: int = 1):
+        """Seconds per solve-loop iteration: (solve(max_iters=warm+k) -
+        solve(max_iters=warm)) / k, cfg as given otherwise (tolerances made
+        unreachable).  Returns (s/iter, total seconds of the two calls)."""
         assert self.kind == "ref"
         dt = np.asarray(p).dtype
         f = self._fn("time_iters_" + self._sfx(dt))
         f.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
-                      C.POINTER(OrcConfig), C.c_int64, C.POINTER(C.c_double),
+                      C.POINTER(OrcConfig), C.c_int64, C.c_int64, C.POINTER(C.c_double),
                       C.POINTER(C.c_double)]
         spi, tot = C.c_double(0), C.c_double(0)
         cfg = cfg or default_config()
         self._check(f(_ptr(np.ascontiguousarray(cost, dt)), m, n,
                       _ptr(np.ascontiguousarray(p, dt)),
-                      _ptr(np.ascontiguousarray(q, dt)), C.byref(cfg), k,
+                      _ptr(np.ascontiguousarray(q, dt)), C.byref(cfg), k, max(1, warm),
                       C.byref(spi), C.byref(tot)))
         return spi.value, tot.value
 

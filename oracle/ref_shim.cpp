@@ -18,6 +18,7 @@
 //   drot::CounterRng           rng.hpp:30-106
 //   drot::lp_exact             reference.hpp:537-552
 //   drot::sinkhorn_solve       reference.hpp:165-288
+#include <algorithm>
 #include <chrono>
 #include <cstring>
 #include <string>
@@ -250,31 +251,35 @@ int steps_impl(const T* C, int64_t m, int64_t n, const T* p, const T* q,
   }
 }
 
-// Per-iteration wall time of the reference solve loop: solve(max_iters=1)
-// and solve(max_iters=1+k) with unreachable tolerances; the difference / k
-// removes validation, init and the final report from the figure.
+// Per-iteration wall time of the reference solve loop: solve(max_iters=w)
+// and solve(max_iters=w+k) (best of two calls each) with unreachable tolerances (every other field of
+// cfg, record_trace included, as given); the difference / k removes
+// validation, init, the w warm-up iterations and the final report.
 template <class T>
 int time_iters_impl(const T* C, int64_t m, int64_t n, const T* p, const T* q,
-                    const orc_config* c, int64_t k, double* sec_per_iter,
+                    const orc_config* c, int64_t k, int64_t w, double* sec_per_iter,
                     double* sec_total) {
   try {
     auto pr = to_problem(C, m, n, p, q);
     auto cfg = to_cfg(c);
     cfg.tol_primal = cfg.tol_dual = cfg.tol_gap = -1.0;
-    cfg.record_trace = false;
     using clk = std::chrono::steady_clock;
-    cfg.max_iters = 1;
+    auto timed = [&](int64_t iters) {  // best of two calls
+      cfg.max_iters = static_cast<decltype(cfg.max_iters)>(iters);
+      double best = 1e300;
+      for (int rep = 0; rep < 2; ++rep) {
+        const auto t0 = clk::now();
+        (void)drot::solve<T>(pr, cfg);
+        best = std::min(best, std::chrono::duration<double>(clk::now() - t0).count());
+      }
+      return best;
+    };
+    cfg.max_iters = static_cast<decltype(cfg.max_iters)>(w);
     (void)drot::solve<T>(pr, cfg);  // warm: first-touch of the solver's buffers
-    auto t0 = clk::now();
-    (void)drot::solve<T>(pr, cfg);
-    auto t1 = clk::now();
-    cfg.max_iters = 1 + k;
-    (void)drot::solve<T>(pr, cfg);
-    auto t2 = clk::now();
-    const double a = std::chrono::duration<double>(t1 - t0).count();
-    const double b = std::chrono::duration<double>(t2 - t1).count();
+    const double a = timed(w);
+    const double b = timed(w + k);
     if (sec_per_iter) *sec_per_iter = (b - a) / static_cast<double>(k);
-    if (sec_total) *sec_total = a + b;
+    if (sec_total) *sec_total = 2.0 * (a + b);
     return 0;
   } catch (const drot::Error& e) {
     return errc_ret(e);
@@ -375,8 +380,9 @@ void ref_default_config(orc_config* c) {
   }                                                                           \
   int ref_time_iters_##SFX(const T* C, int64_t m, int64_t n, const T* p,      \
                            const T* q, const orc_config* c, int64_t k,        \
-                           double* sec_per_iter, double* sec_total) {         \
-    return time_iters_impl<T>(C, m, n, p, q, c, k, sec_per_iter, sec_total);  \
+                           int64_t w, double* sec_per_iter,                   \
+                           double* sec_total) {                               \
+    return time_iters_impl<T>(C, m, n, p, q, c, k, w, sec_per_iter, sec_total); \
   }                                                                           \
   int ref_time_pass_##SFX(T* xy, const T* C, int64_t m, int64_t n,            \
                           const T* phi, const T* varphi, T rho,               \

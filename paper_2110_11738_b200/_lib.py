@@ -109,12 +109,13 @@ SIGNATURES = {
     "drotb_session_gen_gaussian": (C.c_int, [vp, f64, u64, i32]),
     "drotb_session_gen_uniform": (C.c_int, [vp, u64, f64, f64, i32]),
     "drotb_session_get_cost": (C.c_int, [vp, vp]),
-    "drotb_session_persistent_grid": (i32, [vp]),
     "drotb_session_debug_ptrs": (C.c_int, [vp, vp]),
     "drotb_session_tail_stamps": (C.c_int, [vp, vp]),
     "drotb_session_support": (C.c_int, [vp, f64, f64, P(i64), P(f64)]),
     "drotb_session_init": (C.c_int, [vp, vp]),
     "drotb_session_enqueue": (C.c_int, [vp, i64]),
+    "drotb_session_prepare": (C.c_int, [vp, i64]),
+    "drotb_session_graph_builds": (i64, [vp]),
     "drotb_session_run": (C.c_int, [vp]),
     "drotb_session_synchronize": (C.c_int, [vp]),
     "drotb_session_status": (C.c_int, [vp, P(i32), P(i64), P(drotb_report)]),

@@ -1,8 +1,8 @@
 """Builds libdrotb200.so in-tree for sm_100a (nvcc; no GPU needed).
 
-The library is the whole product: CUDA kernels (csrc/kernels.cu), the host
-driver and C ABI (csrc/session.cu) and the host problem generator
-(csrc/probgen.cpp).  It is compiled with -fmad=false so that every device
+The library is the whole product: CUDA kernels (csrc/kernels.cu, tail.cu,
+report.cu, sinkhorn.cu, probgen.cu), the host driver (csrc/session*.cu), the
+C ABI (csrc/abi.cu) and the host problem generator (csrc/probgen.cpp).  It is compiled with -fmad=false so that every device
 expression is evaluated in the reference's association order without FMA
 contraction (the reference is built without FMA).
 """
@@ -25,8 +25,9 @@ NVCC_FLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
     "-Xcompiler", "-O3", "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include"),
 ]
-SOURCES = ["kernels.cu", "session.cu", "probgen.cpp", "probgen.cu", "report.cu", "persistent.cu", "tail.cu", "iter.cu", "sinkhorn.cu"]
-HEADERS = ["drotb_internal.hpp", "drotb_host.hpp", "sweep.cuh", "gate.cuh"]
+SOURCES = ["kernels.cu", "tail.cu", "report.cu", "sinkhorn.cu", "probgen.cu", "probgen.cpp",
+           "session.cu", "session_shard.cu", "session_state.cu", "abi.cu"]
+HEADERS = ["drotb_internal.hpp", "drotb_host.hpp", "session.hpp", "sweep.cuh", "gate.cuh"]
 
 
 def _nvcc() -> str:

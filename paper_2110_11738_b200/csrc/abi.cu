@@ -1,0 +1,827 @@
+// abi.cu -- the C ABI of libdrotb200.so (include/drotb.h): return code =
+// 1 + drot::Errc ordinal (or a CUDA / NCCL code >= DROTB_ERR_CUDA), message
+// "<errc_name>: <what>" as drot::fail formats it (errors.hpp:86-88).  Every
+// entry point that touches a session runs on the session's device and
+// restores the caller's current device on return.
+#include <chrono>
+
+#include "session.hpp"
+
+namespace drotb {
+
+// ---------------------------------------------------------------------------
+// errors (errors.hpp:48-88)
+// ---------------------------------------------------------------------------
+namespace {
+thread_local std::string g_err;
+const char* const kErrcNames[] = {
+    "negative_cost",  "marginal_not_simplex", "empty_dimension",
+    "non_finite_entry", "shape_mismatch",     "non_positive_rho",
+    "invalid_initial_plan", "non_finite_iterate", "zero_marginal",
+    "too_large",      "degenerate_cost",      "dimension_mismatch",
+    "fold_state_mismatch", "bad_magic",       "version_unsupported",
+    "size_mismatch",  "ragged_csv",           "empty_image",
+    "k_too_large",    "io_error",             "bad_config"};
+}  // namespace
+
+const char* errc_name(int errc) {
+  if (errc < 0 || errc >= static_cast<int>(sizeof(kErrcNames) / sizeof(kErrcNames[0])))
+    return "unknown";
+  return kErrcNames[errc];
+}
+int set_error(int errc, const std::string& what) {
+  g_err = std::string(errc_name(errc)) + ": " + what;
+  return 1 + errc;
+}
+int set_cuda_error(int code, const std::string& what) {
+  g_err = what;
+  return code;
+}
+void clear_error() { g_err.clear(); }
+void set_error_text(const std::string& what) { g_err = what; }
+const char* last_error_cstr() { return g_err.c_str(); }
+
+}  // namespace drotb
+
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+using drotb::Session;
+
+struct drotb_session {
+  int32_t precision;
+  void* impl;
+};
+struct drotb_engine {
+  int32_t precision;
+  void* impl;
+};
+
+namespace {
+
+int guard_exceptions(const std::exception& e) {
+  return drotb::set_cuda_error(DROTB_ERR_CUDA, std::string("exception: ") + e.what());
+}
+
+drotb_config effective(const drotb_config* cfg) {
+  drotb_config c;
+  drotb_config_default(&c);
+  if (cfg) c = *cfg;
+  return c;
+}
+
+// One cached session per host thread and precision: a repeated solve of the
+// same shape and configuration reuses its device buffers, stream, schedule
+// and captured graphs instead of reallocating ~2*m*n*sizeof(T) per call
+// (drotb_release_cache() frees it).
+template <class T>
+struct SolveCache {
+  std::unique_ptr<Session<T>> s;
+  int64_t m = 0, n = 0;
+  drotb_config cfg{};
+  Session<T>* get(int64_t m_, int64_t n_, const drotb_config& c, int* rc) {
+    *rc = 0;
+    if (s && m == m_ && n == n_ && std::memcmp(&cfg, &c, sizeof(c)) == 0) return s.get();
+    s.reset();  // free the old buffers before allocating new ones
+    std::unique_ptr<Session<T>> fresh(new Session<T>());
+    *rc = fresh->create(m_, n_, c);
+    if (*rc) return nullptr;
+    s = std::move(fresh);
+    m = m_;
+    n = n_;
+    cfg = c;
+    return s.get();
+  }
+};
+template <class T>
+static SolveCache<T>& solve_cache() {
+  static thread_local SolveCache<T> c;
+  return c;
+}
+
+template <class T>
+int solve_t(const T* C, int64_t m, int64_t n, const T* p, const T* q,
+            const drotb_config* cfgp, const T* x0, T* plan, T* mu, T* nu,
+            T* rho_out, drotb_report* rep, drotb_trace_row* trace,
+            int64_t trace_cap, int64_t* trace_len, int64_t* iters,
+            int32_t* status, double* wall) {
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
+  drotb::clear_error();
+  const drotb_config cfg = effective(cfgp);
+  try {
+    if (m <= 0 || n <= 0)
+      return drotb::set_error(DROTB_ERRC_EMPTY_DIMENSION, "cost matrix has an empty dimension");
+    int crc = 0;
+    Session<T>* s = solve_cache<T>().get(m, n, cfg, &crc);
+    if (!s) return crc;
+    drotb::DeviceGuard g(s->device);
+    RC_TRY(s->set_problem(C, p, q, false, true));
+    RC_TRY(s->init(x0));
+    RC_TRY(s->run());
+    const auto t1 = clk::now();
+    RC_TRY(s->finish(status, iters, rep));
+    RC_TRY(s->get_plan(plan, mu, nu));
+    RC_TRY(s->get_trace(trace, trace_cap, trace_len));
+    if (rho_out) *rho_out = s->rho;
+    if (wall) *wall = std::chrono::duration<double>(t1 - t0).count();
+    return 0;
+  } catch (const std::exception& e) {
+    return guard_exceptions(e);
+  }
+}
+
+template <class T>
+int step_t(T* xy, int32_t* folded, T* rs, T* cs, T* ya, T* yb, T* alpha, T* r,
+           T* s, T* beta, int64_t* iter, const T* C, int64_t m, int64_t n,
+           const T* p, const T* q, const drotb_config* cfgp) {
+  drotb::clear_error();
+  const drotb_config cfg = effective(cfgp);
+  try {
+    std::unique_ptr<Session<T>> ss(new Session<T>());
+    RC_TRY(ss->create(m, n, cfg));
+    drotb::DeviceGuard g(ss->device);
+    RC_TRY(ss->set_problem(C, p, q, false, false));
+    RC_TRY(ss->load_state(xy, *folded, rs, cs, ya, yb, *alpha, r, s, *beta, *iter));
+    RC_TRY(ss->enqueue_iteration());
+    CUDA_TRY(cudaGetLastError());
+    drotb::Book<T> hb;
+    RC_TRY(ss->read_book(&hb));
+    if (hb.pass_bad) {
+      RC_TRY(ss->store_state(xy, folded, rs, cs, ya, yb, alpha, r, s, beta, iter, false));
+      return drotb::set_error(DROTB_ERRC_NON_FINITE_ITERATE,
+                              "non-finite value in iterate update");
+    }
+    return ss->store_state(xy, folded, rs, cs, ya, yb, alpha, r, s, beta, iter, true);
+  } catch (const std::exception& e) {
+    return guard_exceptions(e);
+  }
+}
+
+template <class T>
+int init_state_t(T* xy, int32_t* folded, T* rs, T* cs, T* ya, T* yb, T* alpha,
+                 T* r, T* s, T* beta, int64_t* iter, const T* C, int64_t m,
+                 int64_t n, const T* p, const T* q, const T* x0,
+                 const drotb_config* cfgp) {
+  drotb::clear_error();
+  drotb_config cfg = effective(cfgp);
+  try {
+    std::unique_ptr<Session<T>> ss(new Session<T>());
+    RC_TRY(ss->create(m, n, cfg));
+    drotb::DeviceGuard g(ss->device);
+    RC_TRY(ss->set_problem(C, p, q, false, false));
+    RC_TRY(ss->init(x0));
+    return ss->store_state(xy, folded, rs, cs, ya, yb, alpha, r, s, beta, iter, true);
+  } catch (const std::exception& e) {
+    return guard_exceptions(e);
+  }
+}
+
+template <class T>
+int engine_pass_t(drotb_engine* eng, T* xy, const T* C, const T* rs,
+                  const T* cs, T rho, int32_t kind, int32_t fold,
+                  int32_t* cost_folded, int32_t parity, int32_t want_dual,
+                  int32_t want_dx, int32_t deterministic, T* row_sums,
+                  T* col_sums, drotb_pass_out* out, drotb_counters* counters) {
+  drotb::clear_error();
+  if (!eng) return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "null engine");
+  if ((eng->precision == 0) != (sizeof(T) == 4))
+    return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "engine precision mismatch");
+  auto* s = static_cast<Session<T>*>(eng->impl);
+  int mode;
+  bool fold_write = false;
+  if (kind == DROTB_PASS_SKIP_COST) {
+    if (!cost_folded) return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "cost_folded required");
+    if ((fold != 0) == (*cost_folded != 0))
+      return drotb::set_error(DROTB_ERRC_FOLD_STATE_MISMATCH,
+                              fold ? "array already stores X - rho C"
+                                   : "array does not store X - rho C");
+    mode = fold ? drotb::kFold : drotb::kSkip;
+    fold_write = fold != 0;
+  } else {
+    mode = parity ? drotb::kPlain1 : drotb::kPlain0;
+  }
+  try {
+    drotb::DeviceGuard g(s->device);
+    const bool dual = want_dual != 0;
+    const bool dx = want_dx != 0;
+    RC_TRY(s->engine_pass(xy, C, rs, cs, rho, mode, dual, dx, deterministic != 0,
+                          row_sums, col_sums, out));
+  } catch (const std::exception& e) {
+    return guard_exceptions(e);
+  }
+  if (kind == DROTB_PASS_SKIP_COST) *cost_folded = fold_write ? 1 : 0;
+  if (kind == DROTB_PASS_UNFUSED && out) {
+    out->dual_valid = want_dual != 0;
+    out->dx_valid = want_dx != 0;
+  }
+  if (counters) {  // MemoryCounters (fused.hpp:305-310, 423-519)
+    const uint64_t cells = static_cast<uint64_t>(s->m) * static_cast<uint64_t>(s->n);
+    counters->passes += 1;
+    if (kind == DROTB_PASS_UNFUSED) {
+      counters->xy_elems_read += 4 * cells;
+      counters->xy_elems_written += cells;
+      counters->cost_elems_read += 2 * cells;
+    } else {
+      counters->xy_elems_read += cells;
+      counters->xy_elems_written += cells;
+      if (mode != drotb::kSkip) counters->cost_elems_read += cells;
+    }
+  }
+  return 0;
+}
+
+template <class T>
+int check_problem_t(const T* C, int64_t m, int64_t n, const T* p, const T* q) {
+  drotb::clear_error();
+  drotb_config cfg;
+  drotb_config_default(&cfg);
+  try {
+    std::unique_ptr<Session<T>> s(new Session<T>());
+    RC_TRY(s->create(m, n, cfg));
+    drotb::DeviceGuard g(s->device);
+    return s->set_problem(C, p, q, false, true);
+  } catch (const std::exception& e) {
+    return guard_exceptions(e);
+  }
+}
+
+}  // namespace
+
+// Marginals of the generated instances (rank-local slice of p, all of q).
+//   0 uniform 1/m (gen_gaussian_problem, probgen.hpp:163-164)
+//   1 dyadic-exact uniform (passes the 1e-12 check in fp32)
+//   2 Dirichlet(1..1) (probgen.hpp:115-127, substreams 4 and 5)
+//   3 random_simplex(seed ^ 0x1111), random_simplex(seed ^ 0x2222)
+//     (oracles.hpp:137-147, the pattern of test_reference.cpp:22-29)
+namespace drotb {
+template <class T>
+static int gen_marginals(int64_t mg, int64_t n, uint64_t seed, int32_t kind,
+                         std::vector<T>& pg, std::vector<T>& q) {
+  pg.assign(static_cast<size_t>(mg), T(0));
+  q.assign(static_cast<size_t>(n), T(0));
+  if (kind == 1) {
+    RC_TRY(dyadic_marginal<T>(mg, pg.data()));
+    RC_TRY(dyadic_marginal<T>(n, q.data()));
+  } else if (kind == 2 || kind == 3) {
+    std::vector<double> pd(static_cast<size_t>(mg)), qd(static_cast<size_t>(n));
+    if (kind == 2) {
+      dirichlet_marginal(seed, 4, mg, pd.data());
+      dirichlet_marginal(seed, 5, n, qd.data());
+    } else {
+      random_simplex(mg, seed ^ 0x1111u, pd.data());
+      random_simplex(n, seed ^ 0x2222u, qd.data());
+    }
+    for (int64_t i = 0; i < mg; ++i) pg[i] = static_cast<T>(pd[i]);
+    for (int64_t j = 0; j < n; ++j) q[j] = static_cast<T>(qd[j]);
+  } else if (kind == 0) {
+    for (int64_t i = 0; i < mg; ++i) pg[i] = static_cast<T>(1.0 / static_cast<double>(mg));
+    for (int64_t j = 0; j < n; ++j) q[j] = static_cast<T>(1.0 / static_cast<double>(n));
+  } else {
+    return set_error(DROTB_ERRC_BAD_CONFIG, "unknown marginal kind");
+  }
+  return 0;
+}
+}  // namespace drotb
+
+// residual_report (problem.hpp:174-225) on the device: transient buffers,
+// host in/out.
+template <class T>
+static int residual_report_t(const T* C, int64_t m, int64_t n, const T* p, const T* q,
+                             const T* plan, const T* mu, const T* nu, int32_t exact,
+                             drotb_report* out) {
+  if (m <= 0 || n <= 0)
+    return drotb::set_error(DROTB_ERRC_EMPTY_DIMENSION, "residual_report: empty dimension");
+  if (!C || !p || !q || !plan || !mu || !nu || !out)
+    return drotb::set_error(DROTB_ERRC_SHAPE_MISMATCH, "residual_report: null argument");
+  const size_t mn = static_cast<size_t>(m) * static_cast<size_t>(n);
+  // scratch: rowdev[m], coldev[n], colobj[n], coldsq[n] (report.cu), then out[4]
+  const size_t ns = static_cast<size_t>(m) + 3 * static_cast<size_t>(n);
+  const size_t tb = (sizeof(T) * (2 * mn + 2 * static_cast<size_t>(m + n)) + 15) & ~size_t{15};
+  const size_t db = sizeof(double) * (ns + 4);
+  char* buf = nullptr;
+  CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&buf), tb + db));
+  std::unique_ptr<char, decltype(&cudaFree)> hold(buf, &cudaFree);
+  T* dX = reinterpret_cast<T*>(buf);
+  T* dC = dX + mn;
+  T* dmu = dC + mn;
+  T* dp = dmu + m;
+  T* dnu = dp + m;
+  T* dq = dnu + n;
+  double* scratch = reinterpret_cast<double*>(buf + tb);
+  double* dout = scratch + ns;
+  CUDA_TRY(cudaMemcpy(dX, plan, sizeof(T) * mn, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(dC, C, sizeof(T) * mn, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(dmu, mu, sizeof(T) * m, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(dp, p, sizeof(T) * m, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(dnu, nu, sizeof(T) * n, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(dq, q, sizeof(T) * n, cudaMemcpyHostToDevice));
+  drotb::launch_residual_report<T>(dX, dC, dmu, dnu, dp, dq, m, n, exact != 0, scratch, dout,
+                                   nullptr);
+  CUDA_TRY(cudaGetLastError());
+  double r[4];
+  CUDA_TRY(cudaMemcpy(r, dout, sizeof(r), cudaMemcpyDeviceToHost));
+  out->r_primal = r[0];
+  out->r_dual = r[1];
+  out->gap = r[2];
+  out->objective = r[3];
+  return 0;
+}
+
+extern "C" {
+
+int32_t drotb_abi_version(void) { return DROTB_ABI_VERSION; }
+const char* drotb_last_error(void) { return drotb::last_error_cstr(); }
+const char* drotb_errc_name(int32_t errc) { return drotb::errc_name(errc); }
+int64_t drotb_kernel_launches(void) { return drotb::kernel_launch_count(); }
+
+void drotb_config_default(drotb_config* c) {  // DrotConfig{} (solver.hpp:51-88)
+  std::memset(c, 0, sizeof(*c));
+  c->rho0 = 2.0;
+  c->has_rho_override = 0;
+  c->relative_tolerances = 0;
+  c->rho_override = 0.0;
+  c->tol_primal = c->tol_dual = c->tol_gap = 1e-4;
+  c->max_iters = 100000;
+  c->check_every = 1;
+  c->engine = DROTB_ENGINE_FUSED;
+  c->skip_cost = 1;
+  c->deterministic = 1;
+  c->record_trace = 1;
+  c->workers = 0;
+  c->block_rows = 64;
+  c->work_size = 4;
+  c->trace_every = 1;
+  c->precision = 1;
+  c->device = -1;
+  c->order = DROTB_ORDER_FAST;
+  c->use_graphs = 1;
+}
+
+int drotb_solve_f32(const float* C, int64_t m, int64_t n, const float* p,
+                    const float* q, const drotb_config* cfg, const float* x0,
+                    float* plan, float* mu, float* nu, float* rho_out,
+                    drotb_report* rep, drotb_trace_row* trace,
+                    int64_t trace_cap, int64_t* trace_len, int64_t* iters,
+                    int32_t* status, double* wall) {
+  return solve_t<float>(C, m, n, p, q, cfg, x0, plan, mu, nu, rho_out, rep,
+                        trace, trace_cap, trace_len, iters, status, wall);
+}
+int drotb_solve_f64(const double* C, int64_t m, int64_t n, const double* p,
+                    const double* q, const drotb_config* cfg, const double* x0,
+                    double* plan, double* mu, double* nu, double* rho_out,
+                    drotb_report* rep, drotb_trace_row* trace,
+                    int64_t trace_cap, int64_t* trace_len, int64_t* iters,
+                    int32_t* status, double* wall) {
+  return solve_t<double>(C, m, n, p, q, cfg, x0, plan, mu, nu, rho_out, rep,
+                         trace, trace_cap, trace_len, iters, status, wall);
+}
+
+int drotb_step_f32(float* xy, int32_t* folded, float* rs, float* cs, float* ya,
+                   float* yb, float* alpha, float* r, float* s, float* beta,
+                   int64_t* iter, const float* C, int64_t m, int64_t n,
+                   const float* p, const float* q, const drotb_config* cfg) {
+  return step_t<float>(xy, folded, rs, cs, ya, yb, alpha, r, s, beta, iter, C,
+                       m, n, p, q, cfg);
+}
+int drotb_step_f64(double* xy, int32_t* folded, double* rs, double* cs,
+                   double* ya, double* yb, double* alpha, double* r, double* s,
+                   double* beta, int64_t* iter, const double* C, int64_t m,
+                   int64_t n, const double* p, const double* q,
+                   const drotb_config* cfg) {
+  return step_t<double>(xy, folded, rs, cs, ya, yb, alpha, r, s, beta, iter, C,
+                        m, n, p, q, cfg);
+}
+int drotb_init_state_f32(float* xy, int32_t* folded, float* rs, float* cs,
+                         float* ya, float* yb, float* alpha, float* r, float* s,
+                         float* beta, int64_t* iter, const float* C, int64_t m,
+                         int64_t n, const float* p, const float* q,
+                         const float* x0, const drotb_config* cfg) {
+  return init_state_t<float>(xy, folded, rs, cs, ya, yb, alpha, r, s, beta,
+                             iter, C, m, n, p, q, x0, cfg);
+}
+int drotb_init_state_f64(double* xy, int32_t* folded, double* rs, double* cs,
+                         double* ya, double* yb, double* alpha, double* r,
+                         double* s, double* beta, int64_t* iter,
+                         const double* C, int64_t m, int64_t n, const double* p,
+                         const double* q, const double* x0,
+                         const drotb_config* cfg) {
+  return init_state_t<double>(xy, folded, rs, cs, ya, yb, alpha, r, s, beta,
+                              iter, C, m, n, p, q, x0, cfg);
+}
+
+int drotb_engine_create(drotb_engine** eng, int64_t m, int64_t n,
+                        int64_t block_rows, int64_t work_size,
+                        int32_t precision, int32_t device) {
+  drotb::clear_error();
+  *eng = nullptr;
+  drotb_config cfg;
+  drotb_config_default(&cfg);
+  cfg.block_rows = block_rows;
+  cfg.work_size = work_size;
+  cfg.device = device;
+  cfg.order = DROTB_ORDER_FAST;
+  try {
+    std::unique_ptr<drotb_engine> e(new drotb_engine{precision, nullptr});
+    if (precision == 0) {
+      std::unique_ptr<Session<float>> s(new Session<float>());
+      RC_TRY(s->create(m, n, cfg, true));
+      e->impl = s.release();
+    } else {
+      std::unique_ptr<Session<double>> s(new Session<double>());
+      RC_TRY(s->create(m, n, cfg, true));
+      e->impl = s.release();
+    }
+    *eng = e.release();
+    return 0;
+  } catch (const std::exception& ex) {
+    return guard_exceptions(ex);
+  }
+}
+
+void drotb_engine_destroy(drotb_engine* eng) {
+  if (!eng) return;
+  if (eng->precision == 0)
+    delete static_cast<Session<float>*>(eng->impl);
+  else
+    delete static_cast<Session<double>*>(eng->impl);
+  delete eng;
+}
+
+int drotb_engine_pass_f32(drotb_engine* eng, float* xy, const float* C,
+                          const float* rs, const float* cs, float rho,
+                          int32_t kind, int32_t fold, int32_t* cost_folded,
+                          int32_t parity, int32_t want_dual, int32_t want_dx,
+                          int32_t deterministic, float* row_sums,
+                          float* col_sums, drotb_pass_out* out,
+                          drotb_counters* counters) {
+  return engine_pass_t<float>(eng, xy, C, rs, cs, rho, kind, fold, cost_folded,
+                              parity, want_dual, want_dx, deterministic,
+                              row_sums, col_sums, out, counters);
+}
+int drotb_engine_pass_f64(drotb_engine* eng, double* xy, const double* C,
+                          const double* rs, const double* cs, double rho,
+                          int32_t kind, int32_t fold, int32_t* cost_folded,
+                          int32_t parity, int32_t want_dual, int32_t want_dx,
+                          int32_t deterministic, double* row_sums,
+                          double* col_sums, drotb_pass_out* out,
+                          drotb_counters* counters) {
+  return engine_pass_t<double>(eng, xy, C, rs, cs, rho, kind, fold,
+                               cost_folded, parity, want_dual, want_dx,
+                               deterministic, row_sums, col_sums, out,
+                               counters);
+}
+
+int drotb_check_problem_f32(const float* C, int64_t m, int64_t n,
+                            const float* p, const float* q) {
+  return check_problem_t<float>(C, m, n, p, q);
+}
+int drotb_check_problem_f64(const double* C, int64_t m, int64_t n,
+                            const double* p, const double* q) {
+  return check_problem_t<double>(C, m, n, p, q);
+}
+
+// ---- sessions ----------------------------------------------------------------
+// ---- sessions ----------------------------------------------------------------
+}  // extern "C"
+
+namespace {
+
+// Runs f(Session<T>*) on the session's device (the caller's current device
+// is restored on return), with the thread's error state cleared first.
+template <class F>
+int with_session(drotb_session* s, F&& f) {
+  drotb::clear_error();
+  if (!s || !s->impl) return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "null session");
+  try {
+    if (s->precision == 0) {
+      auto* ss = drotb::as_session<float>(s->impl);
+      drotb::DeviceGuard g(ss->device);
+      return f(ss);
+    }
+    auto* ss = drotb::as_session<double>(s->impl);
+    drotb::DeviceGuard g(ss->device);
+    return f(ss);
+  } catch (const std::exception& e) {
+    return guard_exceptions(e);
+  }
+}
+
+template <class S>
+using elem_t = typename std::remove_pointer<decltype(std::declval<S*>()->X)>::type;
+
+template <class Make>
+int create_session(drotb_session** s, int32_t precision, Make&& make) {
+  drotb::clear_error();
+  if (!s) return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "null session pointer");
+  *s = nullptr;
+  try {
+    std::unique_ptr<drotb_session> h(new drotb_session{precision, nullptr});
+    if (precision == 0) {
+      std::unique_ptr<Session<float>> ss(new Session<float>());
+      RC_TRY(make(ss.get()));
+      h->impl = ss.release();
+    } else {
+      std::unique_ptr<Session<double>> ss(new Session<double>());
+      RC_TRY(make(ss.get()));
+      h->impl = ss.release();
+    }
+    *s = h.release();
+    return 0;
+  } catch (const std::exception& e) {
+    return guard_exceptions(e);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int drotb_session_create(drotb_session** s, int64_t m, int64_t n,
+                         int32_t precision, const drotb_config* cfgp) {
+  const drotb_config cfg = effective(cfgp);
+  return create_session(s, precision, [&](auto* ss) { return ss->create(m, n, cfg); });
+}
+
+void drotb_session_destroy(drotb_session* s) {
+  if (!s) return;
+  if (s->impl) {
+    if (s->precision == 0) {
+      auto* ss = drotb::as_session<float>(s->impl);
+      drotb::DeviceGuard g(ss->device);
+      delete ss;
+    } else {
+      auto* ss = drotb::as_session<double>(s->impl);
+      drotb::DeviceGuard g(ss->device);
+      delete ss;
+    }
+  }
+  delete s;
+}
+
+int drotb_session_set_stream(drotb_session* s, void* stream) {
+  return with_session(s, [&](auto* ss) { return ss->set_stream(stream); });
+}
+
+int drotb_session_set_problem(drotb_session* s, const void* C, const void* p,
+                              const void* q, int32_t is_device) {
+  return with_session(s, [&](auto* ss) {
+    using T = elem_t<std::remove_pointer_t<decltype(ss)>>;
+    return ss->set_problem(static_cast<const T*>(C), static_cast<const T*>(p),
+                           static_cast<const T*>(q), is_device != 0, true);
+  });
+}
+
+// K7: the Gaussian instance generated on the device (probgen.cu); only the
+// O(m+n) points and marginals are drawn on the host.
+int drotb_session_gen_gaussian(drotb_session* s, double sigma_t, uint64_t seed,
+                               int32_t marginals) {
+  return with_session(s, [&](auto* ss) -> int {
+    using T = elem_t<std::remove_pointer_t<decltype(ss)>>;
+    const int64_t m = ss->m, n = ss->n, mg = ss->m_global, r0 = ss->row_begin;
+    std::vector<double> xs, xt;
+    RC_TRY(drotb::gaussian_points(mg, n, sigma_t, seed, xs, xt));
+    double* dpts = nullptr;
+    // stream-ordered allocation: no device-wide synchronization (shards of one
+    // process may be spinning in a collective on the same device)
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&dpts), sizeof(double) * 2 * (mg + n) + 16,
+                             ss->stream));
+    cudaStream_t hs = ss->stream;
+    auto freer = [hs](double* ptr) { cudaFreeAsync(ptr, hs); };
+    std::unique_ptr<double, decltype(freer)> hold(dpts, freer);
+    auto* dmax = reinterpret_cast<unsigned long long*>(dpts + 2 * (mg + n));
+    double* dxs = dpts;
+    double* dxt = dpts + 2 * mg;
+    CUDA_TRY(cudaMemcpyAsync(dxs, xs.data(), sizeof(double) * 2 * mg, cudaMemcpyHostToDevice,
+                             ss->stream));
+    CUDA_TRY(cudaMemcpyAsync(dxt, xt.data(), sizeof(double) * 2 * n, cudaMemcpyHostToDevice,
+                             ss->stream));
+    drotb::launch_gaussian_cmax(dxs, dxt, mg, n, dmax, ss->stream);
+    unsigned long long bits = 0;
+    CUDA_TRY(cudaMemcpyAsync(&bits, dmax, sizeof(bits), cudaMemcpyDeviceToHost, ss->stream));
+    CUDA_TRY(cudaStreamSynchronize(ss->stream));
+    double cmax;
+    std::memcpy(&cmax, &bits, sizeof(cmax));
+    if (!(cmax > 0)) return drotb::set_error(DROTB_ERRC_DEGENERATE_COST, "all samples coincide");
+    drotb::launch_gaussian_cost<T>(dxs + 2 * r0, dxt, m, n, ss->ld, dmax, ss->C, ss->stream);
+    CUDA_TRY(cudaGetLastError());
+    std::vector<T> pg, q;
+    RC_TRY(drotb::gen_marginals<T>(mg, n, seed, marginals, pg, q));
+    return ss->set_problem(nullptr, pg.data() + r0, q.data(), false, true);
+  });
+}
+
+// K7: random_matrix(m, n, seed, lo, hi) (oracles.hpp:128-135) generated on
+// the device, in the global storage order (shards generate their rows).
+int drotb_session_gen_uniform(drotb_session* s, uint64_t seed, double lo, double hi,
+                              int32_t marginals) {
+  return with_session(s, [&](auto* ss) -> int {
+    using T = elem_t<std::remove_pointer_t<decltype(ss)>>;
+    const int64_t m = ss->m, n = ss->n, mg = ss->m_global, r0 = ss->row_begin;
+    drotb::launch_uniform_cost<T>(seed, lo, hi, m, mg, r0, n, ss->ld, ss->C, ss->stream);
+    CUDA_TRY(cudaGetLastError());
+    std::vector<T> pg, q;
+    RC_TRY(drotb::gen_marginals<T>(mg, n, seed, marginals, pg, q));
+    return ss->set_problem(nullptr, pg.data() + r0, q.data(), false, true);
+  });
+}
+
+int drotb_residual_report_f32(const float* C, int64_t m, int64_t n, const float* p,
+                              const float* q, const float* plan, const float* mu,
+                              const float* nu, int32_t exact, drotb_report* out) {
+  drotb::clear_error();
+  return residual_report_t<float>(C, m, n, p, q, plan, mu, nu, exact, out);
+}
+int drotb_residual_report_f64(const double* C, int64_t m, int64_t n, const double* p,
+                              const double* q, const double* plan, const double* mu,
+                              const double* nu, int32_t exact, drotb_report* out) {
+  drotb::clear_error();
+  return residual_report_t<double>(C, m, n, p, q, plan, mu, nu, exact, out);
+}
+
+void drotb_release_cache(void) {
+  solve_cache<float>().s.reset();
+  solve_cache<double>().s.reset();
+}
+
+// Profiling aid: copy (and reset) the 8 tail-phase timestamps (ns).
+int drotb_session_tail_stamps(drotb_session* s, uint64_t* out8) {
+  return with_session(s, [&](auto* ss) -> int {
+    if (!ss->tstamps) return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "DROTB_TAIL_STAMPS not set");
+    CUDA_TRY(cudaStreamSynchronize(ss->stream));
+    CUDA_TRY(cudaMemcpy(out8, ss->tstamps, 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    uint64_t init[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
+    CUDA_TRY(cudaMemcpy(ss->tstamps, init, sizeof(init), cudaMemcpyHostToDevice));
+    return 0;
+  });
+}
+
+// Debug aid: device addresses of the book, the tail barrier words and the
+// exchange buffer (for side-stream inspection of a stuck exchange).
+int drotb_session_debug_ptrs(drotb_session* s, uint64_t* out4) {
+  return with_session(s, [&](auto* ss) -> int {
+    out4[0] = reinterpret_cast<uint64_t>(ss->book);
+    out4[1] = reinterpret_cast<uint64_t>(ss->tbar);
+    out4[2] = reinterpret_cast<uint64_t>(ss->xbuf);
+    out4[3] = static_cast<uint64_t>(ss->tgrid);
+    return 0;
+  });
+}
+
+int drotb_session_support(drotb_session* s, double rel_tau, double abs_tau, int64_t* nnz,
+                          double* xmax) {
+  return with_session(s, [&](auto* ss) { return ss->support(rel_tau, abs_tau, nnz, xmax); });
+}
+
+// Download the session's (local) cost matrix, column-major m x n (tests of
+// the on-device generator; the solver never needs it on the host).
+int drotb_session_get_cost(drotb_session* s, void* out) {
+  return with_session(s, [&](auto* ss) {
+    using T = elem_t<std::remove_pointer_t<decltype(ss)>>;
+    return ss->download_matrix(static_cast<T*>(out), ss->C);
+  });
+}
+
+int drotb_session_init(drotb_session* s, const void* x0) {
+  return with_session(s, [&](auto* ss) {
+    using T = elem_t<std::remove_pointer_t<decltype(ss)>>;
+    return ss->init(static_cast<const T*>(x0));
+  });
+}
+
+int drotb_session_enqueue(drotb_session* s, int64_t n_iters) {
+  return with_session(s, [&](auto* ss) { return ss->enqueue(n_iters); });
+}
+
+int drotb_session_prepare(drotb_session* s, int64_t n_iters) {
+  return with_session(s, [&](auto* ss) { return ss->prepare(n_iters); });
+}
+
+int64_t drotb_session_graph_builds(drotb_session* s) {
+  if (!s || !s->impl) return -1;
+  return s->precision == 0 ? drotb::as_session<float>(s->impl)->graph_builds
+                           : drotb::as_session<double>(s->impl)->graph_builds;
+}
+
+int drotb_session_run(drotb_session* s) {
+  return with_session(s, [&](auto* ss) { return ss->run(); });
+}
+
+int drotb_session_synchronize(drotb_session* s) {
+  return with_session(s, [&](auto* ss) -> int {
+    CUDA_TRY(cudaStreamSynchronize(ss->stream));
+    return 0;
+  });
+}
+
+int drotb_session_status(drotb_session* s, int32_t* status, int64_t* iterations,
+                         drotb_report* report) {
+  return with_session(s, [&](auto* ss) { return ss->finish(status, iterations, report); });
+}
+
+int drotb_session_get_plan(drotb_session* s, void* plan, void* mu, void* nu) {
+  return with_session(s, [&](auto* ss) {
+    using T = elem_t<std::remove_pointer_t<decltype(ss)>>;
+    return ss->get_plan(static_cast<T*>(plan), static_cast<T*>(mu), static_cast<T*>(nu));
+  });
+}
+
+void* drotb_session_device_xy(drotb_session* s) {
+  return s->precision == 0 ? static_cast<void*>(drotb::as_session<float>(s->impl)->X)
+                           : static_cast<void*>(drotb::as_session<double>(s->impl)->X);
+}
+
+void* drotb_session_stream(drotb_session* s) {
+  return s->precision == 0 ? static_cast<void*>(drotb::as_session<float>(s->impl)->stream)
+                           : static_cast<void*>(drotb::as_session<double>(s->impl)->stream);
+}
+
+int drotb_session_pass_bytes(drotb_session* s, double* bytes_fold,
+                             double* bytes_skip) {
+  return with_session(s, [&](auto* ss) -> int {
+    using T = elem_t<std::remove_pointer_t<decltype(ss)>>;
+    const double cells = static_cast<double>(ss->m) * static_cast<double>(ss->n);
+    if (bytes_fold) *bytes_fold = 3.0 * sizeof(T) * cells;  // read X, C; write X
+    if (bytes_skip) *bytes_skip = 2.0 * sizeof(T) * cells;  // read X; write X
+    return 0;
+  });
+}
+
+int drotb_session_run_timed(drotb_session* s, int64_t n_iters, double* total_ms,
+                            double* pass_ms, int64_t* n_pass, double* pass_bytes,
+                            int64_t* launches) {
+  return with_session(s, [&](auto* ss) {
+    return ss->run_timed(n_iters, total_ms, pass_ms, n_pass, pass_bytes, launches);
+  });
+}
+
+int drotb_nccl_unique_id(char* out128) {
+  drotb::clear_error();
+  if (!drotb::nccl().ok)
+    return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "NCCL unavailable: " + drotb::nccl().err);
+  ncclUniqueId id;
+  NCCL_TRY(drotb::nccl().getUniqueId(&id));
+  static_assert(sizeof(id) == DROTB_NCCL_ID_BYTES, "ncclUniqueId size");
+  std::memcpy(out128, &id, sizeof(id));
+  return 0;
+}
+
+int drotb_session_create_sharded(drotb_session** s, int64_t m_global, int64_t n,
+                                 int32_t precision, const drotb_config* cfgp, int32_t rank,
+                                 int32_t world_size, const char* nccl_id128,
+                                 int64_t row_begin, int64_t row_end) {
+  const drotb_config cfg = effective(cfgp);
+  return create_session(s, precision, [&](auto* ss) {
+    return ss->create_sharded(m_global, n, cfg, rank, world_size, nccl_id128, row_begin,
+                              row_end);
+  });
+}
+
+int drotb_session_create_sharded_p2p(drotb_session** s, int64_t m_global, int64_t n,
+                                     int32_t precision, const drotb_config* cfgp, int32_t rank,
+                                     int32_t world_size, int64_t row_begin, int64_t row_end) {
+  const drotb_config cfg = effective(cfgp);
+  return create_session(s, precision, [&](auto* ss) {
+    return ss->create_sharded(m_global, n, cfg, rank, world_size, nullptr, row_begin, row_end,
+                              1);
+  });
+}
+
+int drotb_session_exchange_buffer(drotb_session* s, uint64_t* dev_ptr, char* ipc_handle64) {
+  return with_session(s, [&](auto* ss) -> int {
+    if (ss->xmode != 1 || !ss->xbuf)
+      return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "session has no peer exchange");
+    if (dev_ptr) *dev_ptr = reinterpret_cast<uint64_t>(ss->xbuf);
+    if (ipc_handle64) {
+      cudaIpcMemHandle_t h;
+      CUDA_TRY(cudaIpcGetMemHandle(&h, ss->xbuf));
+      std::memcpy(ipc_handle64, &h, 64);
+    }
+    return 0;
+  });
+}
+
+int drotb_session_attach_peers(drotb_session* s, const uint64_t* dev_ptrs,
+                               const char* ipc_handles) {
+  if (!dev_ptrs && !ipc_handles) {
+    drotb::clear_error();
+    return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "attach_peers: no pointers or handles");
+  }
+  return with_session(s, [&](auto* ss) { return ss->attach_peers(dev_ptrs, ipc_handles); });
+}
+
+int drotb_shard_rows(int64_t m, int32_t world_size, int32_t rank, int64_t* row_begin,
+                     int64_t* row_end) {
+  // contiguous row blocks aligned to the 64-row v blocks, as even as possible
+  drotb::clear_error();
+  if (world_size < 1 || rank < 0 || rank >= world_size || m < 1)
+    return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "invalid shard request");
+  const int64_t blocks = (m + 63) / 64;
+  const int64_t b0 = blocks * rank / world_size, b1 = blocks * (rank + 1) / world_size;
+  *row_begin = std::min<int64_t>(m, b0 * 64);
+  *row_end = std::min<int64_t>(m, b1 * 64);
+  return 0;
+}
+
+}  // extern "C"

@@ -52,9 +52,6 @@ struct PassArgs {
   int32_t pdl;          // launch as a programmatic dependent (after the coop tail)
   int32_t l2hint;       // 1: stream X / C with an L2 evict_first policy (sweep.cuh)
   int32_t pad_l2;
-  T* __restrict__ vcta;  // non-null (fast order, one GPU): one column-sum row per CTA
-                         // ([row block][n], the 64-row sums combined in shared memory)
-                         // instead of the 64-row vstrip
 };
 
 // Device-resident solver bookkeeping: every scalar of the solve loop
@@ -160,106 +157,6 @@ struct TailArgs {
   int32_t fused_gate;          // tail: gate on the algebraic dual value (one barrier less)
   int32_t pad_fg;
 };
-
-// Single-launch iteration (iter.cu): the sweep K1 with the whole per-iteration
-// tail fused into its epilogue ("last arriving CTA" merges, no grid barrier):
-//   - the last of the rbn CTAs of column tile gc sums their CTA-level column
-//     partials (vcta) -> s, tb = b - 2s, b -= s, column-tile record;
-//   - the last of the CTAs of row block rb in u group grp sums that group's
-//     row strips (ugrp); the last group of rb sums the groups -> r,
-//     ta = a - 2r, a -= r, row-block record;
-//   - the last of all those merges reduces the records in fixed order and
-//     runs the scalar recursions and the fused gate on the Book.
-// The next launch's prologue forms phi / varphi from ta / tb and the new coef.
-template <class T>
-struct IterColRec {  // per column tile
-  T cost, prev, dual, dx, mx, s2;
-  int32_t bad, pad;
-  double qb, qs;  // sum q_j b_j (pre-update), sum q_j s_j
-};
-template <class T>
-struct IterRowRec {  // per row block
-  T sr, sr2;
-  double pa, pr;  // sum p_i a_i (pre-update), sum p_i r_i
-};
-template <class T>
-struct IterArgs {
-  PassArgs<T> pa;
-  TailArgs<T> t;
-  T* ta;  // a - 2r (ld)
-  T* tb;  // b - 2s (n)
-  T* a_prev;
-  T* b_prev;
-  T* ugrp;  // [ngrp][ld] grouped row strips
-  T* vcta;  // [rbn][n] CTA-level column partials
-  IterRowRec<T>* rowrec;
-  IterColRec<T>* colrec;
-  double* urow;  // [rbn][4] update partials (prologue, gc == 0 CTAs)
-  double* ucol;  // [gcn][4] (rb == 0 CTAs)
-  unsigned* cnt;  // counters, see iter.cu
-  double* dpart;  // confirm kernel per-CTA partials [grid][16]
-  const T* rbuf0;  // r / s parity buffers (finalize picks by Book.iter)
-  const T* rbuf1;
-  const T* sbuf0;
-  const T* sbuf1;
-  int32_t rbn, gcn, gu, ngrp;
-  int64_t off_col, off_row, off_ug;
-};
-
-template <class T>
-void iter_layout(int64_t m, int64_t n, int64_t tc, int32_t* rbn, int32_t* gcn, int32_t* gu,
-                 int32_t* ngrp, int64_t* cnt_words);
-template <class T>
-size_t iter_smem_bytes(int64_t tc);
-template <class T>
-void launch_iter(const IterArgs<T>& g, int mode, bool want_dual, bool want_dx, cudaStream_t st);
-template <class T>
-void launch_iter_confirm(const IterArgs<T>& g, cudaStream_t st);
-template <class T>
-void launch_iter_finalize(const IterArgs<T>& g, cudaStream_t st);
-constexpr int kIterConfirmGrid = 148 * 4;
-
-// Persistent solver kernel (persistent.cu): one cooperative launch runs up to
-// `iters` iterations; phases separated by grid barriers.
-template <class T>
-struct PersistArgs {
-  PassArgs<T> pa;           // xy, cost, phi, varphi, rho, m, n, ld
-  T* a;
-  T* b;
-  const T* p;
-  const T* q;
-  T* rb0;
-  T* rb1;
-  T* sb0;
-  T* sb1;
-  int64_t m_global, n_global;
-  int64_t rows_cta;         // rows per CTA row block (4 warps x 32 lanes x R)
-  int64_t n_rb;             // row blocks
-  int64_t max_seg;          // u-partial slots per CTA
-  int64_t ileave;           // > 0: interleaved schedule with ileave CTAs per row block
-  T* ustrip;                // [grid * max_seg][rows_cta]
-  const int32_t* seg_ptr;   // [n_rb + 1] CSR of the u slots per row block
-  const int32_t* seg_slot;  // slots in column order
-  T* vstrip;                // [n_rb][n]
-  T* cpart;                 // [grid][16] per-CTA T partials
-  double* dpart;            // [grid][16] per-CTA double partials
-  unsigned* bar;            // [2] barrier count, generation
-  Book<T>* book;
-  TraceRowDev* trace;
-  int64_t iters;            // iterations this launch (upper bound)
-  int32_t engine_ref, skip_cost;
-  unsigned long long* sweep_ns;  // accumulated P1 time (CTA 0, %globaltimer)
-  double* mud;              // [m] phi_i / rho of the current iterate (confirm report)
-};
-
-template <class T>
-size_t persistent_smem_bytes();
-template <class T>
-int persistent_grid(int device);
-template <class T>
-int rows_per_cta();
-template <class T>
-cudaError_t launch_persistent(const PersistArgs<T>& g, int grid, bool dx, cudaStream_t st);
 
 // Cooperative per-iteration tail (tail.cu): merge + recursions + update +
 // gate (+ confirm report) in one launch after K1 (fast order, one GPU).

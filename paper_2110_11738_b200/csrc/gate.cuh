@@ -1,6 +1,6 @@
-// gate.cuh -- solve-loop scalar logic shared by the cooperative tail (tail.cu)
-// and the single-launch iteration (iter.cu): Book copies through shared
-// memory, the fused gate and the deferred exact dual / fixed-point patch.
+// gate.cuh -- solve-loop scalar logic of the cooperative tails (tail.cu):
+// Book copies through shared memory, the fused gate and the deferred exact
+// dual / fixed-point patch.
 #pragma once
 
 #include "drotb_internal.hpp"

@@ -18,6 +18,7 @@
 // of the reference (no FMA contraction).  The fast-mode scalar reductions of
 // K1 use explicit fma() because their order is ours anyway.
 #include <algorithm>
+#include <atomic>
 #include <cfloat>
 #include <cstdio>
 #include <cstdlib>
@@ -33,83 +34,6 @@ namespace drotb {
 static int64_t g_launches = 0;
 int64_t kernel_launch_count() { return g_launches; }
 void count_launch(int64_t k) { g_launches += k; }
-
-#ifndef DROTB_PASS_G
-#define DROTB_PASS_G 4  // columns per load group (two groups in flight)
-#endif
-#ifndef DROTB_PASS_MINB
-#define DROTB_PASS_MINB 4  // resident CTAs per SM the register budget targets
-#endif
-
-template <class T, int MODE, bool DUAL, bool DX>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_PASS_MINB)
-    pass_kernel(const PassArgs<T> a) {
-  using V = typename V16<T>::type;
-  constexpr int R = 16 / sizeof(T);
-  constexpr int ROWS_W = 32 * R;
-  constexpr int CH = kChunkCols;
-  constexpr int G = DROTB_PASS_G;
-  __shared__ __align__(16) T sbuf[kWarpsPerCta][CH * ROWS_W];
-  __shared__ PassAcc<T> wacc[kWarpsPerCta];
-  if (a.stop != nullptr && *reinterpret_cast<const volatile int*>(a.stop)) return;
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t wrow0 =
-      (static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + warp) * ROWS_W;
-  const int64_t row0 = wrow0 + static_cast<int64_t>(lane) * R;
-  const int64_t gc = blockIdx.y;
-  const int64_t c0 = gc * a.tc;
-  const int64_t c1 = imin64(a.n, c0 + a.tc);
-  const int64_t nv = a.m - row0;
-  const int nvalid = nv <= 0 ? 0 : (nv >= R ? R : static_cast<int>(nv));
-  T* wbuf = sbuf[warp];
-
-  T ph[R], u[R];
-  if (nvalid > 0) {
-    unpack(ld_keep(reinterpret_cast<const V*>(a.phi + row0)), ph);
-  } else {
-#pragma unroll
-    for (int t = 0; t < R; ++t) ph[t] = T(0);
-  }
-#pragma unroll
-  for (int t = 0; t < R; ++t) u[t] = T(0);
-  PassAcc<T> acc{T(0), T(0), T(0), T(0), T(0), false};
-
-  if (__all_sync(0xffffffffu, nvalid == R))
-    pass_tile<T, MODE, DUAL, DX, false, G>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc,
-                                           wbuf, lane);
-  else
-    pass_tile<T, MODE, DUAL, DX, true, G>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc,
-                                          wbuf, lane);
-  if (nvalid > 0)
-    st_keep(reinterpret_cast<V*>(a.ustrip + gc * a.ld + row0), pack4(u), a.l2hint);
-
-  // deterministic CTA partials: warp tree, then warps in order
-  acc.cost = warp_sum(acc.cost);
-  acc.prev = warp_sum(acc.prev);
-  acc.dual = warp_sum(acc.dual);
-  acc.dx = warp_sum(acc.dx);
-  acc.mx = warp_max(acc.mx);
-  const bool wbad = __any_sync(0xffffffffu, acc.bad);
-  if (lane == 0) {
-    acc.bad = wbad;
-    wacc[warp] = acc;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    PassPartial<T> out{T(0), T(0), T(0), T(0), T(0), 0, 0};
-#pragma unroll
-    for (int w = 0; w < kWarpsPerCta; ++w) {
-      out.cost += wacc[w].cost;
-      out.prev += wacc[w].prev;
-      out.dual += wacc[w].dual;
-      out.dx += wacc[w].dx;
-      out.max_abs = fmax(out.max_abs, wacc[w].mx);
-      out.bad |= wacc[w].bad ? 1 : 0;
-    }
-    st_partial_keep(a.partials + static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x, out);
-  }
-}
 
 #ifndef DROTB_ASYNC_MINB
 #define DROTB_ASYNC_MINB 3  // 3 CTAs (12 warps) per SM: caps registers at 170 (r1 tuning)
@@ -152,14 +76,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_ASYNC_MINB)
 #pragma unroll
   for (int t = 0; t < R; ++t) u[t] = T(0);
   PassAcc<T> acc{T(0), T(0), T(0), T(0), T(0), false};
-  // a.vcta: the 64-row column sums go to shared memory and are combined per CTA
-  T* svs = a.vcta ? reinterpret_cast<T*>(dyn_smem + async_smem_bytes<T>()) : nullptr;
   if (__all_sync(0xffffffffu, nvalid == R))
     pass_tile_async<T, MODE, DUAL, DX, false>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc, wbuf,
-                                              ring, lane, nullptr, svs, a.tc, warp);
+                                              ring, lane);
   else
     pass_tile_async<T, MODE, DUAL, DX, true>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc, wbuf,
-                                             ring, lane, nullptr, svs, a.tc, warp);
+                                             ring, lane);
   if (nvalid > 0)
     st_keep(reinterpret_cast<V*>(a.ustrip + gc * a.ld + row0), pack4(u), a.l2hint);
 
@@ -187,31 +109,19 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_ASYNC_MINB)
     }
     st_partial_keep(a.partials + static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x, out);
   }
-  if (svs) {  // one column-sum row per CTA: 64-row blocks in ascending order
-    constexpr int NB = ROWS_W / kVBlockRows;
-    const int ncol = static_cast<int>(c1 - c0);
-    for (int cc = threadIdx.x; cc < ncol; cc += kWarpsPerCta * 32) {
-      T s = T(0);
-#pragma unroll
-      for (int w = 0; w < kWarpsPerCta * NB; ++w) s += svs[w * a.tc + cc];
-      st_keep(a.vcta + static_cast<int64_t>(blockIdx.x) * a.n + c0 + cc, s, 2);
-    }
-  }
 }
 
-template <class T>
-constexpr size_t vcta_smem_bytes(int64_t tc) {
-  return static_cast<size_t>(kWarpsPerCta) * (32 * (16 / sizeof(T)) / kVBlockRows) *
-         static_cast<size_t>(tc) * sizeof(T);
-}
-
-static int k1_impl() {  // 0 = register double buffer, 1 = cp.async ring
-  static int impl = [] {
-    const char* e = std::getenv("DROTB_K1");
-    if (e && e[0] == 'r') return 0;
-    return 1;
-  }();
-  return impl;
+// The shared-memory opt-in is a per-device function attribute: set it once
+// per (kernel, device), not once per process.
+template <class K>
+static void opt_in_smem(K kernel, int bytes) {
+  static std::atomic<unsigned long long> done{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  done.fetch_or(bit, std::memory_order_acq_rel);
 }
 
 template <class T, int MODE, bool DUAL, bool DX>
@@ -220,32 +130,22 @@ static void launch_pass_t(const PassArgs<T>& a, cudaStream_t st) {
   const int64_t rows_cta = int64_t(kWarpsPerCta) * 32 * R;
   dim3 grid(static_cast<unsigned>((a.m + rows_cta - 1) / rows_cta),
             static_cast<unsigned>((a.n + a.tc - 1) / a.tc));
-  if (k1_impl() == 1) {
-    const size_t smem = async_smem_bytes<T>() + (a.vcta ? vcta_smem_bytes<T>(a.tc) : 0);
-    static bool attr = [] {
-      cudaFuncSetAttribute(pass_kernel_async<T, MODE, DUAL, DX>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(async_smem_bytes<T>() + vcta_smem_bytes<T>(256)));
-      return true;
-    }();
-    (void)attr;
-    if (a.pdl) {  // launched as a programmatic dependent of the cooperative tail
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = grid;
-      cfg.blockDim = dim3(kWarpsPerCta * 32);
-      cfg.dynamicSmemBytes = smem;
-      cfg.stream = st;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      at[0].val.programmaticStreamSerializationAllowed = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      cudaLaunchKernelEx(&cfg, pass_kernel_async<T, MODE, DUAL, DX>, a);
-    } else {
-      pass_kernel_async<T, MODE, DUAL, DX><<<grid, kWarpsPerCta * 32, smem, st>>>(a);
-    }
+  const size_t smem = async_smem_bytes<T>();
+  opt_in_smem(pass_kernel_async<T, MODE, DUAL, DX>, static_cast<int>(smem));
+  if (a.pdl) {  // launched as a programmatic dependent of the cooperative tail
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kWarpsPerCta * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, pass_kernel_async<T, MODE, DUAL, DX>, a);
   } else {
-    pass_kernel<T, MODE, DUAL, DX><<<grid, kWarpsPerCta * 32, 0, st>>>(a);
+    pass_kernel_async<T, MODE, DUAL, DX><<<grid, kWarpsPerCta * 32, smem, st>>>(a);
   }
   count_launch();
 }

@@ -227,31 +227,6 @@ struct PassAcc {
   bool bad;
 };
 
-template <class T, int G>
-struct ColGroup {
-  typename V16<T>::type x[G], c[G];
-  T v[G];
-};
-
-template <class T, int MODE, int G>
-__device__ __forceinline__ void load_group(const PassArgs<T>& a, ColGroup<T, G>& g,
-                                           int64_t j, int64_t c1, int64_t row0,
-                                           bool live) {
-  using V = typename V16<T>::type;
-  constexpr bool RC = MODE != kSkip;
-#pragma unroll
-  for (int k = 0; k < G; ++k) {
-    if (j + k < c1) {
-      const int64_t off = (j + k) * a.ld + row0;
-      if (live) {
-        g.x[k] = __ldcs(reinterpret_cast<const V*>(a.xy + off));
-        if (RC) g.c[k] = __ldcs(reinterpret_cast<const V*>(a.cost + off));
-      }
-      g.v[k] = __ldg(a.varphi + j + k);
-    }
-  }
-}
-
 // The elementwise update of one column slice (R rows) and its reductions
 // (fused.hpp:249-284).  c = column index within the 16-column staging chunk.
 template <class T, int MODE, bool DUAL, bool DX, bool MASK>
@@ -309,32 +284,6 @@ __device__ __forceinline__ void compute_col(const PassArgs<T>& a, const T (&x)[1
   *reinterpret_cast<V*>(wbuf + (c * 32 + (lane ^ (c & 7))) * R) = pack4(xp);
 }
 
-template <class T, int MODE, bool DUAL, bool DX, bool MASK, int G>
-__device__ __forceinline__ void compute_group(const PassArgs<T>& a,
-                                              const ColGroup<T, G>& g, int64_t j,
-                                              int cbase, int64_t c1, int64_t row0,
-                                              int nvalid, const T (&ph)[16 / sizeof(T)],
-                                              T (&u)[16 / sizeof(T)], PassAcc<T>& acc,
-                                              T* wbuf, int lane) {
-  constexpr int R = 16 / sizeof(T);
-  constexpr bool RC = MODE != kSkip;
-  const bool live = !MASK || nvalid > 0;
-#pragma unroll
-  for (int k = 0; k < G; ++k) {
-    if (j + k < c1) {
-      T x[R], cc[R];
-#pragma unroll
-      for (int t = 0; t < R; ++t) x[t] = cc[t] = T(0);
-      if (live) {
-        unpack(g.x[k], x);
-        if (RC) unpack(g.c[k], cc);
-      }
-      compute_col<T, MODE, DUAL, DX, MASK>(a, x, cc, g.v[k], j + k, cbase + k, row0, nvalid,
-                                           ph, u, acc, wbuf, lane);
-    }
-  }
-}
-
 // v-phase: lane (c, b) sums the 64 rows of block b of staged column c in
 // row order (fused.hpp:268) and writes the v strip entry.
 template <class T>
@@ -361,43 +310,6 @@ __device__ __forceinline__ void v_phase(const PassArgs<T>& a, const T* wbuf, int
       }
       st_keep(a.vstrip + gb * a.n + j0 + c, s, a.l2hint);
     }
-  }
-}
-
-template <class T, int MODE, bool DUAL, bool DX, bool MASK, int G>
-__device__ __forceinline__ void pass_tile(const PassArgs<T>& a, int64_t c0, int64_t c1,
-                                          int64_t wrow0, int64_t row0, int nvalid,
-                                          const T (&ph)[16 / sizeof(T)],
-                                          T (&u)[16 / sizeof(T)], PassAcc<T>& acc,
-                                          T* wbuf, int lane) {
-  using V = typename V16<T>::type;
-  constexpr int R = 16 / sizeof(T);
-  constexpr int ROWS_W = 32 * R;
-  constexpr int NB = ROWS_W / kVBlockRows;
-  constexpr int CH = kChunkCols;
-  constexpr int NG = CH / G;
-  static_assert(NG % 2 == 0, "groups per chunk must be even (ping-pong)");
-  const bool live = !MASK || nvalid > 0;
-  ColGroup<T, G> A, B;
-#pragma unroll
-  for (int k = 0; k < G; ++k) {
-    A.x[k] = B.x[k] = A.c[k] = B.c[k] = vzero<T>();
-    A.v[k] = B.v[k] = T(0);
-  }
-  load_group<T, MODE, G>(a, A, c0, c1, row0, live);
-  for (int64_t j0 = c0; j0 < c1; j0 += CH) {
-#pragma unroll
-    for (int gi = 0; gi < NG; gi += 2) {
-      load_group<T, MODE, G>(a, B, j0 + (gi + 1) * G, c1, row0, live);
-      compute_group<T, MODE, DUAL, DX, MASK, G>(a, A, j0 + gi * G, gi * G, c1, row0,
-                                                nvalid, ph, u, acc, wbuf, lane);
-      load_group<T, MODE, G>(a, A, j0 + (gi + 2) * G, c1, row0, live);
-      compute_group<T, MODE, DUAL, DX, MASK, G>(a, B, j0 + (gi + 1) * G, (gi + 1) * G,
-                                                c1, row0, nvalid, ph, u, acc, wbuf, lane);
-    }
-    __syncwarp();
-    v_phase<T>(a, wbuf, j0, static_cast<int>(imin64(CH, c1 - j0)), wrow0, lane);
-    __syncwarp();
   }
 }
 
@@ -465,37 +377,9 @@ constexpr size_t async_smem_bytes() {
           static_cast<size_t>(kChunkCols) * 32 * 16);
 }
 
-// v sums of a staged chunk into the CTA's shared-memory column partials
-// (single-launch iteration, iter.cu): slot [warp * NB + b][column - ctile0]
-template <class T>
-__device__ __forceinline__ void v_phase_cta(const T* wbuf, int64_t j0, int cnt, int lane,
-                                            T* svs, int64_t ctile0, int64_t tcs, int warp) {
-  using V = typename V16<T>::type;
-  constexpr int R = 16 / sizeof(T);
-  constexpr int NB = 32 * R / kVBlockRows;
-  constexpr int CH = kChunkCols;
-  if (lane < CH * NB) {
-    const int c = lane % CH, b = lane / CH;
-    if (c < cnt) {
-      const V* col = reinterpret_cast<const V*>(wbuf) + c * 32;
-      const int g7 = c & 7;
-      constexpr int QB = kVBlockRows / R;
-      T s = T(0);
-#pragma unroll
-      for (int qq = 0; qq < QB; ++qq) {
-        T v4[R];
-        unpack(col[(b * QB + qq) ^ g7], v4);
-#pragma unroll
-        for (int t = 0; t < R; ++t) s += v4[t];
-      }
-      svs[(warp * NB + b) * tcs + (j0 + c - ctile0)] = s;
-    }
-  }
-}
-
-// The first S-1 ring stages of pass_tile_async (same slots and addresses),
-// issued by the single-launch iteration before its prologue so that the
-// prologue's dependent loads overlap the first column groups in flight
+// The first S-1 ring stages of pass_tile_async (same slots and addresses):
+// they depend on X and C only, so K1 can issue them before it waits for the
+// tail that produces phi / varphi (programmatic dependent launch)
 template <class T, int MODE>
 __device__ __forceinline__ void ring_prime(const PassArgs<T>& a, int64_t c0, int64_t c1,
                                            int64_t row0, bool live,
@@ -520,17 +404,14 @@ __device__ __forceinline__ void ring_prime(const PassArgs<T>& a, int64_t c0, int
   }
 }
 
-// FUSE (iter.cu): varphi_j comes from the CTA's shared-memory copy svphi
-// (computed in the kernel prologue) and the v sums go to svs
-template <class T, int MODE, bool DUAL, bool DX, bool MASK, bool FUSE = false>
+// PRIMED: the caller issued the first S-1 stages (ring_prime)
+template <class T, int MODE, bool DUAL, bool DX, bool MASK, bool PRIMED = false>
 __device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0, int64_t c1,
                                                 int64_t wrow0, int64_t row0, int nvalid,
                                                 const T (&ph)[16 / sizeof(T)],
                                                 T (&u)[16 / sizeof(T)], PassAcc<T>& acc,
                                                 T* wbuf, typename V16<T>::type* ring,
-                                                int lane, const T* svphi = nullptr,
-                                                T* svs = nullptr, int64_t tcs = 0,
-                                                int warp = 0) {
+                                                int lane) {
   using V = typename V16<T>::type;
   constexpr int R = 16 / sizeof(T);
   constexpr bool RC = MODE != kSkip;
@@ -566,15 +447,23 @@ __device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0
               cp_async16(cslot(st, k), a.cost + off);
           }
         }
-        if (!FUSE) vb[st][k] = __ldg(a.varphi + col);
+        vb[st][k] = __ldg(a.varphi + col);
       }
     }
     cp_async_commit();
   };
-  // FUSE: the caller primed the ring (ring_prime) before its prologue
-  if (!FUSE)
+  if (!PRIMED) {
 #pragma unroll
     for (int st = 0; st < S - 1; ++st) issue(st, c0 + st * G);
+  } else {  // X / C of the first stages are in flight; varphi only exists now
+#pragma unroll
+    for (int st = 0; st < S - 1; ++st)
+#pragma unroll
+      for (int k = 0; k < G; ++k) {
+        const int64_t col = c0 + st * G + k;
+        vb[st][k] = col < c1 ? __ldg(a.varphi + col) : T(0);
+      }
+  }
   for (int64_t j0 = c0; j0 < c1; j0 += CH) {
 #pragma unroll
     for (int gg = 0; gg < NG; ++gg) {
@@ -592,17 +481,14 @@ __device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0
             unpack(*xslot(st, k), x);
             if (RC) unpack(*cslot(st, k), cc);
           }
-          compute_col<T, MODE, DUAL, DX, MASK>(a, x, cc, FUSE ? svphi[col - c0] : vb[st][k],
+          compute_col<T, MODE, DUAL, DX, MASK>(a, x, cc, vb[st][k],
                                                col, gg * G + k, row0, nvalid, ph, u, acc, wbuf,
                                                lane);
         }
       }
     }
     __syncwarp();
-    if (FUSE || svs)
-      v_phase_cta<T>(wbuf, j0, static_cast<int>(imin64(CH, c1 - j0)), lane, svs, c0, tcs, warp);
-    else
-      v_phase<T>(a, wbuf, j0, static_cast<int>(imin64(CH, c1 - j0)), wrow0, lane);
+    v_phase<T>(a, wbuf, j0, static_cast<int>(imin64(CH, c1 - j0)), wrow0, lane);
     __syncwarp();
   }
   cp_async_wait<0>();

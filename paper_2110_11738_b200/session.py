@@ -161,6 +161,14 @@ class Session:
     def enqueue(self, iters: int):
         _check(_lib.load().drotb_session_enqueue(self._h, int(iters)))
 
+    def prepare(self, iters: int):
+        """Capture every CUDA graph enqueue(iters) would launch (no launch)."""
+        _check(_lib.load().drotb_session_prepare(self._h, int(iters)))
+
+    @property
+    def graph_builds(self) -> int:
+        return int(_lib.load().drotb_session_graph_builds(self._h))
+
     def run(self):
         _check(_lib.load().drotb_session_run(self._h))
 
@@ -196,11 +204,6 @@ class Session:
             C.byref(launches)))
         return dict(total_ms=tot.value, pass_ms=pms.value, n_pass=npass.value,
                     pass_bytes=pb.value, launches=launches.value)
-
-    @property
-    def persistent_grid(self) -> int:
-        """CTAs of the persistent solver kernel (0: per-launch kernels + graphs)."""
-        return int(_lib.load().drotb_session_persistent_grid(self._h))
 
     def device_xy(self) -> int:
         return _lib.load().drotb_session_device_xy(self._h)

@@ -42,7 +42,8 @@ def problem(R: Oracle, spec: dict):
     if kind == "uniform_random":
         C = R.random_unit(spec["seed"], m * n)
     elif kind == "gaussian":
-        C, _, _ = R.gen_gaussian(m, n, seed=spec["seed"])
+        C, pd, qd = R.gen_gaussian(m, n, seed=spec["seed"],
+                                   dirichlet=spec["marginals"] == "dirichlet")
     else:
         raise ValueError(kind)
     marg = spec["marginals"]
@@ -52,6 +53,8 @@ def problem(R: Oracle, spec: dict):
     elif marg == "dyadic":
         p = dyadic_marginal(m, dt).astype(np.float64)
         q = dyadic_marginal(n, dt).astype(np.float64)
+    elif marg == "dirichlet":  # probgen.hpp:115-127 (Dirichlet(1..1), substreams 4/5)
+        p, q = pd, qd
     elif marg == "random_simplex":  # test_reference.cpp:22-29 pattern
         from pyoracle import Oracle as _O  # noqa
         orc = Oracle("orc")
@@ -66,6 +69,16 @@ def problem(R: Oracle, spec: dict):
     else:
         raise ValueError(marg)
     return C.astype(dt), p.astype(dt), q.astype(dt)
+
+
+def warm_start(R: Oracle, spec: dict):
+    """Optional x0 (solver.hpp:143-159): a nonnegative m x n matrix in
+    column-major order, CounterRng(seed) uniforms scaled by 1/(m*n)."""
+    x0 = spec.get("x0")
+    if x0 is None:
+        return None
+    m, n = spec["m"], spec["n"]
+    return (R.random_unit(x0["seed"], m * n) * (x0["scale"] / (m * n))).astype(spec["dtype"])
 
 
 CASES = {
@@ -88,7 +101,30 @@ CASES = {
     "rect4000x500_f32_k200": dict(m=4000, n=500, dtype="float32", cost="uniform_random",
                                   seed=5, marginals="dyadic",
                                   cfg=dict(max_iters=200, tol_primal=-1.0)),
+    # round 2: converged runs SURVEY §6 measured but round 1 never pinned
+    "dirichlet1000_f64": dict(m=1000, n=1000, dtype="float64", cost="gaussian", seed=0,
+                              marginals="dirichlet", cfg={}),
+    "gauss2000_f64": dict(m=2000, n=2000, dtype="float64", cost="gaussian", seed=0,
+                          marginals="uniform", cfg={}),
+    # valid warm start x0 (solver.hpp:143-159)
+    "warm_x0_f64": dict(m=300, n=300, dtype="float64", cost="uniform_random", seed=3,
+                        marginals="uniform", x0=dict(seed=11, scale=2.0), cfg={}),
+    "warm_x0_f32": dict(m=256, n=200, dtype="float32", cost="gaussian", seed=2,
+                        marginals="dyadic", x0=dict(seed=12, scale=1.0), cfg={}),
 }
+
+# C4 grid (BASELINE configs[3]) at 256^2 fp32: rho0 x tol, including the
+# warm-up preset 1/ln m (solver.hpp:47-49) and tol 1e-6, where the reference
+# stalls until max_iters; max_iters = the reference default 1e5.
+C4_RHO = {"0.5": 0.5, "1": 1.0, "2": 2.0, "4": 4.0, "invlnm": None}
+C4_TOL = ["1e-3", "1e-4", "1e-5", "1e-6"]
+for _rk, _rv in C4_RHO.items():
+    for _tk in C4_TOL:
+        _t = float(_tk)
+        _rho = _rv if _rv is not None else 1.0 / __import__("math").log(256)
+        CASES[f"c4grid_f32_rho{_rk}_tol{_tk}"] = dict(
+            m=256, n=256, dtype="float32", cost="gaussian", seed=0, marginals="dyadic",
+            cfg=dict(rho0=_rho, tol_primal=_t, tol_dual=_t, tol_gap=_t))
 
 
 def run_case(R: Oracle, name: str, spec: dict) -> dict:
@@ -96,7 +132,7 @@ def run_case(R: Oracle, name: str, spec: dict) -> dict:
     m, n = spec["m"], spec["n"]
     cfg = default_config(**spec["cfg"])
     t0 = time.time()
-    out = R.solve(C, p, q, m, n, cfg)
+    out = R.solve(C, p, q, m, n, cfg, x0=warm_start(R, spec))
     wall = time.time() - t0
     tr = np.array([[r[k] for k in ("iter", "r_primal", "r_dual", "gap", "objective",
                                    "ergodic_objective", "fixed_point_residual")]

@@ -16,7 +16,7 @@ def test_reference_arm_json_line():
     if not (os.path.exists(ref) or os.path.exists(orc)):
         pytest.skip("oracle not built")
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
-                          "--steps", "3", "--warmup", "3", "--size", "1500"],
+                          "--steps", "20", "--warmup", "3", "--size", "1500"],
                          capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
@@ -24,6 +24,6 @@ def test_reference_arm_json_line():
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
               "higher_is_better", "cpu_baseline", "e2e", "config"):
         assert k in line, k
-    assert line["value"] > 0 and line["steps"] >= 30
+    assert line["value"] > 0 and line["steps"] == 20 and line["warmup"] == 3
     assert line["cpu_baseline"]["value"] == line["value"]
     assert line["e2e"]["h2d_bytes_per_step"] == 0

@@ -14,8 +14,11 @@ same instances.
   C3  m = 40 000, n = 5 000 fp64, random_matrix cost (seed 1),
       random_simplex marginals
   C4  m = n = 30 000 fp32, Gaussian cost (seed 0), dyadic-uniform marginals,
-      rho0 = 0.5 (the sweep's smallest rho; K = 3 iterations: 3.6 GB per
-      matrix on the host)
+      rho0 = 0.5 (the sweep's smallest rho)
+
+K = 200 iterations at C2 / C3 and 50 at C4 (3.6 GB per matrix; ~2 s per
+reference iteration on the host); the reference run of each instance is
+shared by the exact- and fast-order tests.
 """
 import os
 
@@ -24,7 +27,8 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-K = 6
+K = {"c2": 200, "c3": 200, "c4": 50}
+_WANT = {}
 
 
 def _oracle():
@@ -73,10 +77,13 @@ def c4():
         dyadic_marginal(n, np.float32)
 
 
-def _run(drot, ref, prob, order):
+def _run(drot, ref, name, prob, order):
     m, n, C, p, q = prob
-    k, rho0 = (3, 0.5) if m == 30000 else (K, 2.0)
-    want = ref.solve(C, p, q, m, n, _cfg(max_iters=k, rho0=rho0))
+    k = K[name]
+    rho0 = 0.5 if name == "c4" else 2.0
+    if name not in _WANT:
+        _WANT[name] = ref.solve(C, p, q, m, n, _cfg(max_iters=k, rho0=rho0))
+    want = _WANT[name]
     got = drot.solve(drot.TransportProblem(C.reshape((m, n), order="F"), p, q),
                      drot.DrotConfig(order=drot.Order[order], max_iters=k, rho0=rho0))
     drot.release_device_cache()
@@ -91,7 +98,7 @@ def _props(got, p, q):
 @pytest.mark.parametrize("name", ["c2", "c3", "c4"])
 def test_fullsize_exact_order_bitwise(drot, ref, name, request):
     prob = request.getfixturevalue(name)
-    want, got = _run(drot, ref, prob, "reference")
+    want, got = _run(drot, ref, name, prob, "reference")
     assert got.trace.iterations == want.iterations
     assert got.status.name == want.status
     np.testing.assert_array_equal(got.plan.x.ravel(order="F"), want.plan)
@@ -109,19 +116,22 @@ def test_fullsize_exact_order_bitwise(drot, ref, name, request):
 @pytest.mark.parametrize("name", ["c2", "c3", "c4"])
 def test_fullsize_fast_order(drot, ref, name, request):
     prob = request.getfixturevalue(name)
-    want, got = _run(drot, ref, prob, "fast")
+    want, got = _run(drot, ref, name, prob, "fast")
     assert got.trace.iterations == want.iterations
     fp32 = prob[2].dtype == np.float32
     # X is elementwise-identical in both orders until a reduction's rounding
-    # differs; over K iterations the plans must stay within a few ulps of the
-    # iterate scale
+    # differs; over K iterations the plans stay within a few ulps of the
+    # iterate scale (the DR map is nonexpansive: rounding does not grow)
     x, w = got.plan.x.ravel(order="F"), want.plan
     scale = float(np.abs(w).max())
-    tol = (1e-5 if fp32 else 1e-12) * scale
-    assert float(np.abs(x - w).max()) <= tol
-    rel = 1e-4 if fp32 else 1e-10
-    assert abs(got.report.objective - want.report["objective"]) <= rel * abs(
-        want.report["objective"])
+    diff = float(np.abs(x.astype(np.float64) - w).max())
+    rel_obj = abs(got.report.objective - want.report["objective"]) / abs(want.report["objective"])
+    print(f"{name}: K={K[name]} max|dX|/max|X| = {diff / scale:.3e}, objective rel {rel_obj:.3e}")
+    assert diff <= (1e-4 if fp32 else 1e-10) * scale
+    assert rel_obj <= (1e-4 if fp32 else 1e-10)
+    for gr, rr in zip(got.trace.rows, want.trace):
+        assert abs(gr.objective - rr["objective"]) <= (1e-4 if fp32 else 1e-10) * abs(
+            rr["objective"]) + 1e-30, gr.iter
     _props(got, prob[3], prob[4])
 
 

@@ -41,7 +41,7 @@ class _env:
 
 
 def _single(drot, m, n, dt, cfg, seed):
-    with _env(DROTB_TAIL="coop", DROTB_PERSIST="0"):
+    with _env(DROTB_TAIL="coop"):
         s = drot.Session(m, n, dt, cfg)
     s.gen_gaussian(5.0, seed, "dyadic")
     s.init()

@@ -34,7 +34,7 @@ class _env:
 
 
 def _run(drot, m, n, dt, iters=None, legacy=False, **kw):
-    with _env(DROTB_TAIL="legacy" if legacy else "coop", DROTB_PERSIST="0"):
+    with _env(DROTB_TAIL="legacy" if legacy else "coop"):
         s = drot.Session(m, n, dt, drot.DrotConfig(**kw))
     s.gen_gaussian(5.0, 4, "dyadic")
     s.init()
@@ -83,7 +83,7 @@ def test_numerical_failure(drot):
     m, n = 64, 48
     C = np.full((m, n), 1e300)
     prob = drot.TransportProblem(np.asfortranarray(C), np.full(m, 1.0 / m), np.full(n, 1.0 / n))
-    with _env(DROTB_TAIL="coop", DROTB_PERSIST="0"):
+    with _env(DROTB_TAIL="coop"):
         drot.release_device_cache()
         r = drot.solve(prob, drot.DrotConfig(rho_override=1e10))
         drot.release_device_cache()
@@ -102,7 +102,7 @@ def test_fused_gate_matches_exact_gate(drot, dt):
     q = drot.dyadic_marginal(n, dt)
     res = []
     for gate in ("fused", "exact"):
-        with _env(DROTB_TAIL="coop", DROTB_PERSIST="0", DROTB_TAIL_GATE=gate):
+        with _env(DROTB_TAIL="coop", DROTB_TAIL_GATE=gate):
             drot.release_device_cache()
             res.append(drot.solve(drot.TransportProblem(C, p, q), drot.DrotConfig(max_iters=60000)))
             drot.release_device_cache()
@@ -131,13 +131,3 @@ def test_l2_policies_do_not_change_results(drot, dt):
     assert a[0][1] == b[0][1] == 40
     for x, y in zip(a[1:], b[1:]):
         np.testing.assert_array_equal(x, y)
-
-
-def test_vcta_rows_close_to_strips(drot):
-    """DROTB_VCTA=1 (per-CTA column-sum rows) changes only the association of
-    the column sums: fixed-iteration fp64 iterates agree to rounding."""
-    with _env(DROTB_VCTA="1"):
-        a = _run(drot, 700, 500, np.float64, iters=40, tol_primal=-1.0, max_iters=10 ** 9)
-    b = _run(drot, 700, 500, np.float64, iters=40, tol_primal=-1.0, max_iters=10 ** 9)
-    for x, y in zip(a[1:], b[1:]):
-        assert float(np.abs(x - y).max()) <= 1e-12 * max(1.0, float(np.abs(y).max()))
