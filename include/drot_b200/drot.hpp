@@ -4,21 +4,34 @@
 //   drot::solve<T>, drot::drot_step<T>, drot::init_state<T>,
 //   drot::FusedEngine<T>, drot::check_problem, drot::DrotConfig, ...
 // compiles unchanged against this header (swap the include path, link
-// libdrotb200.so) and runs on a B200.  Every call goes through the C ABI of
-// include/drotb.h; the types below mirror the reference's field for field
-// (cited per type).  Header-only; C++17.
+// libdrotb200.so) and runs on a B200.  Every array-sized computation goes
+// through the C ABI of include/drotb.h; the types below mirror the
+// reference's field for field (cited per type).  The small host helpers
+// (Matrix, vec_*, row_sums / col_sums, ErgodicMean, ThreadPool) are the
+// reference's value-type utilities, kept so that client code written against
+// them compiles; the solver never calls them.  Header-only; C++20 (std::span,
+// as the reference).
 #ifndef DROT_B200_DROT_HPP_
 #define DROT_B200_DROT_HPP_
 
+#if __cplusplus < 202002L
+#error "drot_b200/drot.hpp mirrors the reference's C++20 API (std::span): build with -std=c++20"
+#endif
+
+#include <algorithm>
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
+#include <functional>
 #include <initializer_list>
 #include <memory>
 #include <optional>
+#include <span>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "../drotb.h"
@@ -94,11 +107,139 @@ class Matrix {
   const T* data() const { return data_.data(); }
   T* col(std::size_t j) { return data_.data() + j * rows_; }
   const T* col(std::size_t j) const { return data_.data() + j * rows_; }
+  std::span<T> flat() { return std::span<T>(data_); }
+  std::span<const T> flat() const { return std::span<const T>(data_); }
   bool same_shape(const Matrix& o) const { return rows_ == o.rows_ && cols_ == o.cols_; }
+  template <class U>
+  Matrix<U> cast() const {  // element-wise static_cast, storage order
+    Matrix<U> out(rows_, cols_);
+    std::transform(data_.begin(), data_.end(), out.data(),
+                   [](T v) { return static_cast<U>(v); });
+    return out;
+  }
 
  private:
   std::size_t rows_ = 0, cols_ = 0;
   std::vector<T> data_;
+};
+
+template <class T>
+void require_same_shape(const Matrix<T>& a, const Matrix<T>& b, const char* where) {
+  if (!a.same_shape(b)) fail(Errc::shape_mismatch, where);
+}
+
+// ---- matrix.hpp:93-158: host vector helpers, ascending-index order ---------
+template <class T>
+T vec_sum(std::span<const T> x) {
+  T s = T(0);
+  for (std::size_t k = 0; k < x.size(); ++k) s += x[k];
+  return s;
+}
+template <class T>
+T vec_dot(std::span<const T> x, std::span<const T> y) {
+  T s = T(0);
+  for (std::size_t k = 0; k < x.size(); ++k) s += x[k] * y[k];
+  return s;
+}
+template <class T>
+T vec_norm_sq(std::span<const T> x) {
+  T s = T(0);
+  for (std::size_t k = 0; k < x.size(); ++k) s += x[k] * x[k];
+  return s;
+}
+template <class T>
+bool all_finite(std::span<const T> x) {
+  return std::all_of(x.begin(), x.end(),
+                     [](T v) { return std::isfinite(static_cast<double>(v)); });
+}
+template <class T>
+std::vector<T> row_sums(const Matrix<T>& x) {  // X e, column by column
+  std::vector<T> u(x.rows(), T(0));
+  for (std::size_t j = 0; j < x.cols(); ++j)
+    for (std::size_t i = 0; i < x.rows(); ++i) u[i] += x(i, j);
+  return u;
+}
+template <class T>
+std::vector<T> col_sums(const Matrix<T>& x) {  // X' f, one chain per column
+  std::vector<T> v(x.cols(), T(0));
+  for (std::size_t j = 0; j < x.cols(); ++j) {
+    T s = T(0);
+    for (std::size_t i = 0; i < x.rows(); ++i) s += x(i, j);
+    v[j] = s;
+  }
+  return v;
+}
+template <class T>
+T frobenius_dot(const Matrix<T>& a, const Matrix<T>& b) {
+  return vec_dot(std::span<const T>(a.flat()), std::span<const T>(b.flat()));
+}
+template <class T>
+T frobenius_norm_sq(const Matrix<T>& a) {
+  return vec_norm_sq(std::span<const T>(a.flat()));
+}
+template <class T>
+double frobenius_distance(const Matrix<T>& a, const Matrix<T>& b) {
+  double s = 0;
+  for (std::size_t k = 0; k < a.size(); ++k) {
+    const double d = static_cast<double>(a.data()[k]) - static_cast<double>(b.data()[k]);
+    s += d * d;
+  }
+  return std::sqrt(s);
+}
+
+// ---- rng.hpp:30-106: the counter-based generator behind every synthetic
+// input (SplitMix64 finalizer over key + k * golden gamma).  The host and
+// device generators (csrc/probgen.cpp / probgen.cu) restate the same stream.
+class CounterRng {
+ public:
+  explicit CounterRng(std::uint64_t key) : key_(key) {}
+  static std::uint64_t mix(std::uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }
+  static std::uint64_t derive_key(std::uint64_t key, std::uint64_t stream) {
+    return mix(key ^ mix(stream + kGamma));
+  }
+  CounterRng substream(std::uint64_t stream) const { return CounterRng(derive_key(key_, stream)); }
+  std::uint64_t next_u64() { return mix(key_ + (ctr_ += kGamma)); }
+  double next_unit() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
+  double next_unit_open() { return (static_cast<double>(next_u64() >> 11) + 0.5) * 0x1.0p-53; }
+  void next_gaussian_pair(double& z0, double& z1) {  // Marsaglia polar
+    while (true) {
+      const double a = 2.0 * next_unit() - 1.0;
+      const double b = 2.0 * next_unit() - 1.0;
+      const double s = a * a + b * b;
+      if (!(s > 0.0 && s < 1.0)) continue;
+      const double r = std::sqrt(-2.0 * std::log(s) / s);
+      z0 = a * r;
+      z1 = b * r;
+      return;
+    }
+  }
+  double next_gaussian() {
+    if (spare_ok_) {
+      spare_ok_ = false;
+      return spare_;
+    }
+    double z0 = 0;
+    next_gaussian_pair(z0, spare_);
+    spare_ok_ = true;
+    return z0;
+  }
+  std::uint64_t next_below(std::uint64_t bound) {  // rejection, bias-free
+    const std::uint64_t floor_ = (0 - bound) % bound;
+    std::uint64_t r = next_u64();
+    while (r < floor_) r = next_u64();
+    return r % bound;
+  }
+
+ private:
+  static constexpr std::uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+  std::uint64_t key_;
+  std::uint64_t ctr_ = 0;
+  double spare_ = 0;
+  bool spare_ok_ = false;
 };
 
 // ---- problem.hpp:31-92 ------------------------------------------------------
@@ -143,6 +284,29 @@ struct SolveTrace {
   double wall_time_s = 0;
 };
 
+// ---- threadpool.hpp:19-52 ---------------------------------------------------
+// The reference's CPU worker pool.  On the B200 the CUDA grid does this
+// work, so the pool only keeps the API: run() executes the tasks in order on
+// the calling thread (worker index 0); FusedEngine accepts a pool and ignores
+// it.
+class ThreadPool {
+ public:
+  explicit ThreadPool(std::size_t workers) : workers_(workers ? workers : 1) {}
+  ThreadPool(const ThreadPool&) = delete;
+  ThreadPool& operator=(const ThreadPool&) = delete;
+  std::size_t workers() const { return workers_; }
+  void run(std::size_t n_tasks, const std::function<void(std::size_t, std::size_t)>& fn) {
+    for (std::size_t t = 0; t < n_tasks; ++t) fn(t, 0);
+  }
+  static std::size_t hardware_workers() {
+    const unsigned hc = std::thread::hardware_concurrency();
+    return hc ? static_cast<std::size_t>(hc) : 1;
+  }
+
+ private:
+  std::size_t workers_;
+};
+
 // ---- solver.hpp:37-123 ------------------------------------------------------
 enum class EngineKind { reference, fused };
 enum class Precision { f32, f64 };
@@ -179,6 +343,9 @@ struct DrotConfig {
     if (!(rho > 0) || !std::isfinite(rho))
       fail(Errc::non_positive_rho, "resolved rho must be positive");
     return rho;
+  }
+  std::size_t resolved_workers() const {
+    return workers == 0 ? ThreadPool::hardware_workers() : workers;
   }
 
   drotb_config to_c() const {
@@ -265,10 +432,37 @@ struct SolveResult {
   SolveStatus status = SolveStatus::max_iters;
 };
 
-// ---- tiles.hpp:22-49 ----------------------------------------------------------
+// solver.hpp:127-139: running mean of the per-iterate objectives (the solve
+// keeps its own copy of this recursion on the device, csrc/gate.cuh)
+class ErgodicMean {
+ public:
+  void update(double value) {
+    count_ += 1;
+    mean_ += (value - mean_) / static_cast<double>(count_);
+  }
+  double mean() const { return mean_; }
+  std::int64_t count() const { return count_; }
+
+ private:
+  double mean_ = 0;
+  std::int64_t count_ = 0;
+};
+
+// ---- tiles.hpp:22-49, tiles.cpp:20-47 -----------------------------------------
+// The tile list is the reference's reduction order (tile-column-major); the
+// device kernels reproduce it from (block_rows, work_size) in order=reference.
+struct TileRange {
+  std::size_t r0 = 0, r1 = 0;
+  std::size_t c0 = 0, c1 = 0;
+  std::size_t grid_r = 0, grid_c = 0;
+  std::size_t rows() const { return r1 - r0; }
+  std::size_t cols() const { return c1 - c0; }
+  std::size_t size() const { return rows() * cols(); }
+};
 struct TilePlan {
   std::size_t rows = 0, cols = 0, block_rows = 64, work_size = 4, workers = 1;
   std::size_t grid_rows = 0, grid_cols = 0;
+  std::vector<TileRange> tiles;
   std::size_t tile_cols() const { return work_size * block_rows; }
 };
 inline TilePlan plan_tiles(std::size_t m, std::size_t n, std::size_t bs, std::size_t ws,
@@ -276,25 +470,63 @@ inline TilePlan plan_tiles(std::size_t m, std::size_t n, std::size_t bs, std::si
   TilePlan p;
   p.rows = m;
   p.cols = n;
-  p.block_rows = bs ? bs : 1;
-  p.work_size = ws ? ws : 1;
-  p.workers = workers ? workers : 1;
+  p.block_rows = std::max<std::size_t>(bs, 1);
+  p.work_size = std::max<std::size_t>(ws, 1);
+  p.workers = std::max<std::size_t>(workers, 1);
+  const std::size_t tc = p.tile_cols();
   p.grid_rows = (m + p.block_rows - 1) / p.block_rows;
-  p.grid_cols = (n + p.tile_cols() - 1) / p.tile_cols();
+  p.grid_cols = (n + tc - 1) / tc;
+  p.tiles.resize(p.grid_rows * p.grid_cols);
+  std::size_t k = 0;
+  for (std::size_t gc = 0; gc < p.grid_cols; ++gc)
+    for (std::size_t gr = 0; gr < p.grid_rows; ++gr, ++k) {
+      TileRange& t = p.tiles[k];
+      t.grid_r = gr;
+      t.grid_c = gc;
+      t.r0 = gr * p.block_rows;
+      t.r1 = std::min(m, t.r0 + p.block_rows);
+      t.c0 = gc * tc;
+      t.c1 = std::min(n, t.c0 + tc);
+    }
   return p;
 }
 
-// ---- problem.hpp:122-136 --------------------------------------------------------
+// ---- problem.hpp:96-154 ---------------------------------------------------------
+struct ValidateOptions {
+  bool renormalize = false;    // rescale marginals to sum exactly to one
+  double simplex_tol = 1e-12;  // allowed |sum - 1|
+};
+
+// The matrix scan runs on the device (K0, first offending entry in flat
+// order); the marginals are checked with the reference's sequential double sum.
 template <class T>
-void check_problem(const TransportProblem<T>& pr) {
+void check_problem(const TransportProblem<T>& pr, double simplex_tol = 1e-12) {
   if (pr.m() == 0 || pr.n() == 0) fail(Errc::empty_dimension, "cost matrix has an empty dimension");
   if (pr.p.size() != pr.m() || pr.q.size() != pr.n())
     fail(Errc::shape_mismatch, "marginal lengths do not match the cost matrix");
   const auto m = static_cast<int64_t>(pr.m()), n = static_cast<int64_t>(pr.n());
   if constexpr (detail::is_f32<T>)
-    detail::check(drotb_check_problem_f32(pr.cost.data(), m, n, pr.p.data(), pr.q.data()));
+    detail::check(drotb_check_problem_tol_f32(pr.cost.data(), m, n, pr.p.data(), pr.q.data(),
+                                              simplex_tol));
   else
-    detail::check(drotb_check_problem_f64(pr.cost.data(), m, n, pr.p.data(), pr.q.data()));
+    detail::check(drotb_check_problem_tol_f64(pr.cost.data(), m, n, pr.p.data(), pr.q.data(),
+                                              simplex_tol));
+}
+
+// Marginals are divided by their double sum (then cast back to T) only under
+// renormalize; the result is then checked like check_problem.
+template <class T>
+TransportProblem<T> validate_problem(TransportProblem<T> pr, const ValidateOptions& opts = {}) {
+  if (opts.renormalize) {
+    for (std::vector<T>* marg : {&pr.p, &pr.q}) {
+      double total = 0;
+      for (T e : *marg) total += static_cast<double>(e);
+      if (!(total > 0)) continue;
+      for (T& e : *marg) e = static_cast<T>(static_cast<double>(e) / total);
+    }
+  }
+  check_problem(pr, opts.simplex_tol);
+  return pr;
 }
 
 // ---- problem.hpp:155-225 (evaluated on the B200) --------------------------------
@@ -364,6 +596,40 @@ SolveResult<T> sinkhorn_solve(const TransportProblem<T>& pr, T eta, double tol,
                                       tr[k].objective, tr[k].ergodic_objective,
                                       tr[k].fixed_point_residual});
   return res;
+}
+
+// ---- probgen.hpp:40-51, 131-180: the synthetic Gaussian instance ------------------
+// Bit-identical to the reference generator (same CounterRng substreams);
+// on_degenerate = resample is not supported (a degenerate draw fails).
+struct GaussianSpec {
+  std::size_t m = 0, n = 0;
+  double sigma_t = 5.0;
+  std::uint64_t seed = 0;
+  enum class OnDegenerate { error, resample };
+  OnDegenerate on_degenerate = OnDegenerate::error;
+  bool dirichlet_marginals = false;
+};
+
+inline TransportProblem<double> gen_gaussian_problem(const GaussianSpec& spec) {
+  if (spec.m == 0 || spec.n == 0) fail(Errc::empty_dimension, "gen_gaussian_problem");
+  TransportProblem<double> pr;
+  pr.cost = Matrix<double>(spec.m, spec.n);
+  pr.p.assign(spec.m, 0.0);
+  pr.q.assign(spec.n, 0.0);
+  detail::check(drotb_gen_gaussian(static_cast<int64_t>(spec.m), static_cast<int64_t>(spec.n),
+                                   spec.sigma_t, spec.seed, spec.dirichlet_marginals ? 1 : 0,
+                                   pr.cost.data(), pr.p.data(), pr.q.data()));
+  return pr;
+}
+
+template <class T>
+TransportProblem<T> gen_gaussian_problem_as(const GaussianSpec& spec) {
+  TransportProblem<double> d = gen_gaussian_problem(spec);
+  TransportProblem<T> out;
+  out.cost = d.cost.template cast<T>();
+  out.p.assign(d.p.begin(), d.p.end());
+  out.q.assign(d.q.begin(), d.q.end());
+  return out;
 }
 
 // ---- solver.hpp:143-186 / 361-370 / 372-540 -------------------------------------
@@ -477,31 +743,78 @@ DualCertificate<T> recover_duals(const DrotState<T>& st, T rho) {
   return cert;
 }
 
+// solver.hpp:204-217: the plan iterate of a state, unfolded (and clamped)
+// when the array holds X - rho C; evaluated on the device (K6).
+template <class T>
+TransportPlan<T> materialize_plan(const DrotState<T>& st, const Matrix<T>& cost, T rho) {
+  const Matrix<T>& xy = st.xy.values;
+  if (st.xy.cost_folded) require_same_shape(xy, cost, "materialize_plan: array vs cost");
+  TransportPlan<T> plan{Matrix<T>(xy.rows(), xy.cols())};
+  if (xy.size() == 0) return plan;
+  const auto m = static_cast<int64_t>(xy.rows()), n = static_cast<int64_t>(xy.cols());
+  const int32_t f = st.xy.cost_folded ? 1 : 0;
+  if constexpr (detail::is_f32<T>)
+    detail::check(drotb_materialize_plan_f32(xy.data(), f, cost.data(), m, n, rho, plan.x.data()));
+  else
+    detail::check(drotb_materialize_plan_f64(xy.data(), f, cost.data(), m, n, rho, plan.x.data()));
+  return plan;
+}
+
+// solver.hpp:219-230: Y_k = X_k + phi e' + f varphi' (tests / diagnostics).
+template <class T>
+Matrix<T> materialize_y(const DrotState<T>& st, const Matrix<T>& cost, T rho) {
+  const Matrix<T>& xy = st.xy.values;
+  if (st.xy.cost_folded) require_same_shape(xy, cost, "materialize_y: array vs cost");
+  if (st.row_shift.size() != xy.rows() || st.col_shift.size() != xy.cols())
+    fail(Errc::shape_mismatch, "materialize_y: shift lengths");
+  Matrix<T> y(xy.rows(), xy.cols());
+  if (xy.size() == 0) return y;
+  const auto m = static_cast<int64_t>(xy.rows()), n = static_cast<int64_t>(xy.cols());
+  const int32_t f = st.xy.cost_folded ? 1 : 0;
+  if constexpr (detail::is_f32<T>)
+    detail::check(drotb_materialize_y_f32(xy.data(), f, cost.data(), st.row_shift.data(),
+                                          st.col_shift.data(), m, n, rho, y.data()));
+  else
+    detail::check(drotb_materialize_y_f64(xy.data(), f, cost.data(), st.row_shift.data(),
+                                          st.col_shift.data(), m, n, rho, y.data()));
+  return y;
+}
+
 // ---- fused.hpp:107-202: the engine on the device ----------------------------------
 template <class T>
 class FusedEngine {
  public:
-  explicit FusedEngine(TilePlan plan, int device = -1) : plan_(plan) {
+  // The pool is accepted for source compatibility (fused.hpp:110-113) and
+  // kept for pool(); the passes run on `device` (-1: the current device).
+  explicit FusedEngine(TilePlan plan, std::shared_ptr<ThreadPool> pool = nullptr,
+                       int device = -1)
+      : plan_(std::move(plan)),
+        pool_(pool ? std::move(pool) : std::make_shared<ThreadPool>(plan_.workers)) {
     drotb_engine* e = nullptr;
-    detail::check(drotb_engine_create(&e, static_cast<int64_t>(plan.rows),
-                                      static_cast<int64_t>(plan.cols),
-                                      static_cast<int64_t>(plan.block_rows),
-                                      static_cast<int64_t>(plan.work_size),
+    detail::check(drotb_engine_create(&e, static_cast<int64_t>(plan_.rows),
+                                      static_cast<int64_t>(plan_.cols),
+                                      static_cast<int64_t>(plan_.block_rows),
+                                      static_cast<int64_t>(plan_.work_size),
                                       detail::is_f32<T> ? 0 : 1, device));
     eng_.reset(e);
   }
   const TilePlan& plan() const { return plan_; }
+  ThreadPool& pool() { return *pool_; }
 
   FusedPassOutput<T> fused_pass(Matrix<T>& xy, const Matrix<T>& cost,
-                                const std::vector<T>& row_shift,
-                                const std::vector<T>& col_shift, T rho,
+                                std::span<const T> row_shift,
+                                std::span<const T> col_shift, T rho,
                                 const PassOptions& opts = {}) {
     return run(xy, cost, row_shift, col_shift, rho, DROTB_PASS_FUSED, 0, nullptr, opts);
   }
   FusedPassOutput<T> fused_pass_skip_cost(FusedArray<T>& xy, const Matrix<T>& cost,
-                                          const std::vector<T>& row_shift,
-                                          const std::vector<T>& col_shift, T rho, bool fold,
+                                          std::span<const T> row_shift,
+                                          std::span<const T> col_shift, T rho, bool fold,
                                           PassOptions opts = {}) {
+    if (fold == xy.cost_folded)
+      fail(Errc::fold_state_mismatch,
+           fold ? "array already stores X - rho C" : "array does not store X - rho C");
+    opts.parity = fold ? 0 : 1;
     int32_t folded = xy.cost_folded ? 1 : 0;
     auto out = run(xy.values, cost, row_shift, col_shift, rho, DROTB_PASS_SKIP_COST,
                    fold ? 1 : 0, &folded, opts);
@@ -509,8 +822,8 @@ class FusedEngine {
     return out;
   }
   FusedPassOutput<T> unfused_pass(Matrix<T>& xy, const Matrix<T>& cost,
-                                  const std::vector<T>& row_shift,
-                                  const std::vector<T>& col_shift, T rho,
+                                  std::span<const T> row_shift,
+                                  std::span<const T> col_shift, T rho,
                                   const PassOptions& opts = {}) {
     return run(xy, cost, row_shift, col_shift, rho, DROTB_PASS_UNFUSED, 0, nullptr, opts);
   }
@@ -519,8 +832,8 @@ class FusedEngine {
   struct Del {
     void operator()(drotb_engine* e) const { drotb_engine_destroy(e); }
   };
-  FusedPassOutput<T> run(Matrix<T>& xy, const Matrix<T>& cost, const std::vector<T>& rs,
-                         const std::vector<T>& cs, T rho, int32_t kind, int32_t fold,
+  FusedPassOutput<T> run(Matrix<T>& xy, const Matrix<T>& cost, std::span<const T> rs,
+                         std::span<const T> cs, T rho, int32_t kind, int32_t fold,
                          int32_t* folded, const PassOptions& opts) {
     if (xy.rows() != plan_.rows || xy.cols() != plan_.cols)
       fail(Errc::shape_mismatch, "fused pass: array vs tile plan");
@@ -570,6 +883,7 @@ class FusedEngine {
     return o;
   }
   TilePlan plan_;
+  std::shared_ptr<ThreadPool> pool_;
   std::unique_ptr<drotb_engine, Del> eng_;
 };
 

@@ -11,6 +11,9 @@
  *     drotb_engine_pass_f32/_f64   fused_pass :127-134 / fused_pass_skip_cost
  *                                  :140-155 / unfused_pass :359-531
  *   drotb_check_problem_f32/_f64 drot::check_problem      problem.hpp:122-136
+ *   drotb_check_problem_tol_*   check_problem(pr, simplex_tol) problem.hpp:122-124
+ *   drotb_materialize_plan_*    drot::materialize_plan<T> solver.hpp:204-217
+ *   drotb_materialize_y_*       drot::materialize_y<T>    solver.hpp:221-230
  *   drotb_gen_gaussian          drot::gen_gaussian_problem probgen.hpp:131-170
  *   drotb_config_default        drot::DrotConfig{}        solver.hpp:51-88
  *   drotb_errc_name             drot::errc_name           errors.hpp:48-73
@@ -244,6 +247,30 @@ int drotb_check_problem_f32(const float* C, int64_t m, int64_t n,
                             const float* p, const float* q);
 int drotb_check_problem_f64(const double* C, int64_t m, int64_t n,
                             const double* p, const double* q);
+/* check_problem(problem, simplex_tol) (problem.hpp:122-124): the same scan
+ * with the caller's |sum - 1| tolerance (the two functions above use the
+ * reference default 1e-12).  validate_problem's renormalize option
+ * (problem.hpp:141-154) is O(m+n) host work in the front ends, followed by
+ * this check. */
+int drotb_check_problem_tol_f32(const float* C, int64_t m, int64_t n,
+                                const float* p, const float* q, double simplex_tol);
+int drotb_check_problem_tol_f64(const double* C, int64_t m, int64_t n,
+                                const double* p, const double* q, double simplex_tol);
+
+/* materialize_plan (solver.hpp:204-217) / materialize_y (:221-230) of a
+ * caller-owned DrotState array xy (m*n; holds X - rho C when cost_folded):
+ * plan = max(xy + rho*C, 0) when folded, else xy; y = plan + (phi_i +
+ * varphi_j).  C may be NULL when cost_folded == 0.  Evaluated on the device. */
+int drotb_materialize_plan_f32(const float* xy, int32_t cost_folded, const float* C,
+                               int64_t m, int64_t n, float rho, float* plan);
+int drotb_materialize_plan_f64(const double* xy, int32_t cost_folded, const double* C,
+                               int64_t m, int64_t n, double rho, double* plan);
+int drotb_materialize_y_f32(const float* xy, int32_t cost_folded, const float* C,
+                            const float* row_shift, const float* col_shift, int64_t m,
+                            int64_t n, float rho, float* y);
+int drotb_materialize_y_f64(const double* xy, int32_t cost_folded, const double* C,
+                            const double* row_shift, const double* col_shift, int64_t m,
+                            int64_t n, double rho, double* y);
 
 /* residual_report (problem.hpp:174-225) of an arbitrary (plan, cert) pair,
  * evaluated on the device: plan (m*n), mu (m), nu (n) host arrays.

@@ -8,6 +8,8 @@ been built -- there is no CPU fallback.
 """
 from . import _lib
 from .api import (DeviceError, DrotConfig, DrotState, DualCertificate, EngineKind, Errc,
+                  ErgodicMean, TileRange, ValidateOptions, materialize_plan, materialize_y,
+                  validate_problem,
                   Error, FusedArray, FusedEngine, FusedPassOutput, GaussianSpec,
                   MemoryCounters, Order, PassOptions, Precision, ResidualReport,
                   SolveResult, SolveStatus, SolveTrace, TilePlan, TraceRow, TransportPlan,
@@ -21,7 +23,8 @@ LIB_PATH = _lib.LIB_PATH
 _lib.load()
 
 __all__ = [
-    "DeviceError", "DrotConfig", "DrotState", "DualCertificate", "EngineKind", "Errc",
+    "ErgodicMean", "TileRange", "ValidateOptions", "materialize_plan", "materialize_y",
+    "validate_problem", "DeviceError", "DrotConfig", "DrotState", "DualCertificate", "EngineKind", "Errc",
     "Error", "FusedArray", "FusedEngine", "FusedPassOutput", "GaussianSpec",
     "MemoryCounters", "Order", "PassOptions", "Precision", "ResidualReport", "SolveResult",
     "SolveStatus", "SolveTrace", "TilePlan", "TraceRow", "TransportPlan",

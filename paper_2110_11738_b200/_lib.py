@@ -87,6 +87,12 @@ SIGNATURES = {
                                         P(drotb_counters)]),
     "drotb_check_problem_f32": (C.c_int, [vp, i64, i64, vp, vp]),
     "drotb_check_problem_f64": (C.c_int, [vp, i64, i64, vp, vp]),
+    "drotb_check_problem_tol_f32": (C.c_int, [vp, i64, i64, vp, vp, f64]),
+    "drotb_check_problem_tol_f64": (C.c_int, [vp, i64, i64, vp, vp, f64]),
+    "drotb_materialize_plan_f32": (C.c_int, [vp, i32, vp, i64, i64, f32, vp]),
+    "drotb_materialize_plan_f64": (C.c_int, [vp, i32, vp, i64, i64, f64, vp]),
+    "drotb_materialize_y_f32": (C.c_int, [vp, i32, vp, vp, vp, i64, i64, f32, vp]),
+    "drotb_materialize_y_f64": (C.c_int, [vp, i32, vp, vp, vp, i64, i64, f64, vp]),
     "drotb_residual_report_f32": (C.c_int, [vp, i64, i64, vp, vp, vp, vp, vp, i32,
                                             P(drotb_report)]),
     "drotb_residual_report_f64": (C.c_int, [vp, i64, i64, vp, vp, vp, vp, vp, i32,

@@ -253,17 +253,48 @@ def _p(a: Optional[np.ndarray]):
 
 
 # ---- solver --------------------------------------------------------------------
-def check_problem(problem: TransportProblem) -> None:
-    """problem.hpp:122-136 (matrix scan on the GPU)."""
+def check_problem(problem: TransportProblem, simplex_tol: float = 1e-12) -> None:
+    """problem.hpp:122-136 (matrix scan on the GPU; marginals by the
+    reference's sequential double sum against simplex_tol)."""
     dt = _dtype_of(problem)
     m, n = problem.m, problem.n
+    if m == 0 or n == 0:
+        raise Error(Errc.empty_dimension, "empty_dimension: cost matrix has an empty dimension")
     if len(problem.p) != m or len(problem.q) != n:
         raise Error(Errc.shape_mismatch,
                     "shape_mismatch: marginal lengths do not match the cost matrix")
     lib = _lib.load()
     cm = _cm(problem.cost, dt)
     pv, qv = _vec(problem.p, dt), _vec(problem.q, dt)  # keep alive across the call
-    _check(getattr(lib, "drotb_check_problem_" + _sfx(dt))(_p(cm), m, n, _p(pv), _p(qv)))
+    _check(getattr(lib, "drotb_check_problem_tol_" + _sfx(dt))(_p(cm), m, n, _p(pv), _p(qv),
+                                                               float(simplex_tol)))
+
+
+@dataclass
+class ValidateOptions:
+    """problem.hpp:96-99."""
+    renormalize: bool = False
+    simplex_tol: float = 1e-12
+
+
+def validate_problem(problem: TransportProblem,
+                     opts: Optional[ValidateOptions] = None) -> TransportProblem:
+    """problem.hpp:141-154: returns a checked copy; under renormalize each
+    marginal is divided by its sequential double sum (then cast back to T)."""
+    opts = opts or ValidateOptions()
+    dt = _dtype_of(problem)
+    p = np.array(problem.p, dtype=dt, copy=True)
+    q = np.array(problem.q, dtype=dt, copy=True)
+    if opts.renormalize:
+        for v in (p, q):
+            total = 0.0
+            for e in v.tolist():  # ascending-index double sum, as the reference
+                total += float(e)
+            if total > 0:
+                v[:] = (v.astype(np.float64) / total).astype(dt)
+    out = TransportProblem(np.array(problem.cost, dtype=dt, order="F", copy=True), p, q)
+    check_problem(out, opts.simplex_tol)
+    return out
 
 
 def residual_report(problem: TransportProblem, plan: TransportPlan, cert: DualCertificate,
@@ -467,6 +498,59 @@ def drot_step(st: DrotState, problem: TransportProblem,
     _state_call("drotb_step", problem, cfg, st)
 
 
+def _materialize(st: DrotState, cost, rho: float, want_y: bool) -> np.ndarray:
+    xy = st.xy.values
+    dt = xy.dtype
+    m, n = xy.shape
+    out = np.empty((m, n), dt, order="F")
+    if m == 0 or n == 0:
+        return out
+    if st.xy.cost_folded and tuple(np.shape(cost)) != (m, n):
+        raise Error(Errc.shape_mismatch, "shape_mismatch: materialize: array vs cost")
+    xm = _cm(xy, dt)
+    cm = _cm(cost, dt) if st.xy.cost_folded else None
+    lib = _lib.load()
+    if want_y:
+        rs, cs = _vec(st.row_shift, dt), _vec(st.col_shift, dt)
+        if len(rs) != m or len(cs) != n:
+            raise Error(Errc.shape_mismatch, "shape_mismatch: materialize_y: shift lengths")
+        _check(getattr(lib, "drotb_materialize_y_" + _sfx(dt))(
+            _p(xm), int(st.xy.cost_folded), _p(cm), _p(rs), _p(cs), m, n, rho, _p(out)))
+    else:
+        _check(getattr(lib, "drotb_materialize_plan_" + _sfx(dt))(
+            _p(xm), int(st.xy.cost_folded), _p(cm), m, n, rho, _p(out)))
+    return out
+
+
+def materialize_plan(st: DrotState, cost, rho: float) -> TransportPlan:
+    """solver.hpp:204-217 on the device: the plan iterate, unfolded and
+    clamped when the array holds X - rho C."""
+    return TransportPlan(_materialize(st, cost, rho, False))
+
+
+def materialize_y(st: DrotState, cost, rho: float) -> np.ndarray:
+    """solver.hpp:219-230 on the device: Y = X + phi e' + f varphi'."""
+    return _materialize(st, cost, rho, True)
+
+
+class ErgodicMean:
+    """solver.hpp:127-139: running mean of the per-iterate objectives."""
+
+    def __init__(self):
+        self._mean = 0.0
+        self._count = 0
+
+    def update(self, value: float) -> None:
+        self._count += 1
+        self._mean += (float(value) - self._mean) / float(self._count)
+
+    def mean(self) -> float:
+        return self._mean
+
+    def count(self) -> int:
+        return self._count
+
+
 def recover_duals(st: DrotState, rho: float) -> DualCertificate:
     """solver.hpp:188-199 (mu = phi / rho in T)."""
     dt = st.row_shift.dtype
@@ -518,6 +602,26 @@ class FusedPassOutput:
 
 
 @dataclass
+class TileRange:
+    """tiles.hpp:22-33."""
+    r0: int
+    r1: int
+    c0: int
+    c1: int
+    grid_r: int
+    grid_c: int
+
+    def rows(self):
+        return self.r1 - self.r0
+
+    def cols(self):
+        return self.c1 - self.c0
+
+    def size(self):
+        return self.rows() * self.cols()
+
+
+@dataclass
 class TilePlan:
     """tiles.hpp:37-46 (the reduction tree the GPU reproduces)."""
     rows: int
@@ -533,6 +637,18 @@ class TilePlan:
     @property
     def grid_cols(self):
         return -(-self.cols // (self.block_rows * self.work_size))
+
+    def tile_cols(self):
+        return self.work_size * self.block_rows
+
+    @property
+    def tiles(self):
+        """Tile-column-major list = the reference's reduction order
+        (tiles.cpp:33-44)."""
+        tc = self.tile_cols()
+        return [TileRange(gr * self.block_rows, min(self.rows, (gr + 1) * self.block_rows),
+                          gc * tc, min(self.cols, (gc + 1) * tc), gr, gc)
+                for gc in range(self.grid_cols) for gr in range(self.grid_rows)]
 
 
 def plan_tiles(m: int, n: int, bs: int = 64, ws: int = 4, workers: int = 1) -> TilePlan:

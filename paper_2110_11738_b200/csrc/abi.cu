@@ -233,7 +233,8 @@ int engine_pass_t(drotb_engine* eng, T* xy, const T* C, const T* rs,
 }
 
 template <class T>
-int check_problem_t(const T* C, int64_t m, int64_t n, const T* p, const T* q) {
+int check_problem_t(const T* C, int64_t m, int64_t n, const T* p, const T* q,
+                    double simplex_tol) {
   drotb::clear_error();
   drotb_config cfg;
   drotb_config_default(&cfg);
@@ -241,7 +242,49 @@ int check_problem_t(const T* C, int64_t m, int64_t n, const T* p, const T* q) {
     std::unique_ptr<Session<T>> s(new Session<T>());
     RC_TRY(s->create(m, n, cfg));
     drotb::DeviceGuard g(s->device);
+    s->simplex_tol = simplex_tol;
     return s->set_problem(C, p, q, false, true);
+  } catch (const std::exception& e) {
+    return guard_exceptions(e);
+  }
+}
+
+// materialize_plan / materialize_y (solver.hpp:204-230) of a caller-owned
+// DrotState array: transient device copies, K6 (or its Y form), host out.
+template <class T>
+int materialize_t(const T* xy, int32_t folded, const T* C, const T* phi, const T* varphi,
+                  int64_t m, int64_t n, T rho, T* out) {
+  drotb::clear_error();
+  if (m <= 0 || n <= 0)
+    return drotb::set_error(DROTB_ERRC_EMPTY_DIMENSION, "materialize: empty dimension");
+  const bool want_y = phi != nullptr;
+  if (!xy || !out || (folded && !C) || (want_y && !varphi))
+    return drotb::set_error(DROTB_ERRC_SHAPE_MISMATCH, "materialize: null argument");
+  try {
+    const size_t mn = static_cast<size_t>(m) * static_cast<size_t>(n);
+    const size_t cnt = (folded ? 3 : 2) * mn + (want_y ? static_cast<size_t>(m + n) : 0);
+    T* buf = nullptr;
+    CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&buf), cnt * sizeof(T)));
+    std::unique_ptr<T, decltype(&cudaFree)> hold(buf, &cudaFree);
+    T* dx = buf;
+    T* dout = buf + mn;
+    T* dc = folded ? buf + 2 * mn : nullptr;
+    T* dphi = want_y ? buf + (folded ? 3 : 2) * mn : nullptr;
+    T* dvphi = want_y ? dphi + m : nullptr;
+    cudaStream_t st = nullptr;
+    CUDA_TRY(cudaMemcpyAsync(dx, xy, mn * sizeof(T), cudaMemcpyHostToDevice, st));
+    if (dc) CUDA_TRY(cudaMemcpyAsync(dc, C, mn * sizeof(T), cudaMemcpyHostToDevice, st));
+    if (want_y) {
+      CUDA_TRY(cudaMemcpyAsync(dphi, phi, m * sizeof(T), cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaMemcpyAsync(dvphi, varphi, n * sizeof(T), cudaMemcpyHostToDevice, st));
+      drotb::launch_materialize_y<T>(dx, dc, dphi, dvphi, dout, rho, folded ? 1 : 0, m, n, m, st);
+    } else {
+      drotb::launch_materialize<T>(dx, dc, dout, rho, folded ? 1 : 0, m, n, m, st);
+    }
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(out, dout, mn * sizeof(T), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return 0;
   } catch (const std::exception& e) {
     return guard_exceptions(e);
   }
@@ -475,11 +518,37 @@ int drotb_engine_pass_f64(drotb_engine* eng, double* xy, const double* C,
 
 int drotb_check_problem_f32(const float* C, int64_t m, int64_t n,
                             const float* p, const float* q) {
-  return check_problem_t<float>(C, m, n, p, q);
+  return check_problem_t<float>(C, m, n, p, q, 1e-12);
 }
 int drotb_check_problem_f64(const double* C, int64_t m, int64_t n,
                             const double* p, const double* q) {
-  return check_problem_t<double>(C, m, n, p, q);
+  return check_problem_t<double>(C, m, n, p, q, 1e-12);
+}
+int drotb_check_problem_tol_f32(const float* C, int64_t m, int64_t n,
+                                const float* p, const float* q, double simplex_tol) {
+  return check_problem_t<float>(C, m, n, p, q, simplex_tol);
+}
+int drotb_check_problem_tol_f64(const double* C, int64_t m, int64_t n,
+                                const double* p, const double* q, double simplex_tol) {
+  return check_problem_t<double>(C, m, n, p, q, simplex_tol);
+}
+int drotb_materialize_plan_f32(const float* xy, int32_t cost_folded, const float* C,
+                               int64_t m, int64_t n, float rho, float* plan) {
+  return materialize_t<float>(xy, cost_folded, C, nullptr, nullptr, m, n, rho, plan);
+}
+int drotb_materialize_plan_f64(const double* xy, int32_t cost_folded, const double* C,
+                               int64_t m, int64_t n, double rho, double* plan) {
+  return materialize_t<double>(xy, cost_folded, C, nullptr, nullptr, m, n, rho, plan);
+}
+int drotb_materialize_y_f32(const float* xy, int32_t cost_folded, const float* C,
+                            const float* row_shift, const float* col_shift, int64_t m,
+                            int64_t n, float rho, float* y) {
+  return materialize_t<float>(xy, cost_folded, C, row_shift, col_shift, m, n, rho, y);
+}
+int drotb_materialize_y_f64(const double* xy, int32_t cost_folded, const double* C,
+                            const double* row_shift, const double* col_shift, int64_t m,
+                            int64_t n, double rho, double* y) {
+  return materialize_t<double>(xy, cost_folded, C, row_shift, col_shift, m, n, rho, y);
 }
 
 // ---- sessions ----------------------------------------------------------------

@@ -247,6 +247,10 @@ template <class T>
 void launch_materialize(const T* xy, const T* cost, T* out, T rho,
                         int folded, int64_t m, int64_t n, int64_t ld,
                         cudaStream_t st);
+template <class T>
+void launch_materialize_y(const T* xy, const T* cost, const T* phi, const T* varphi,
+                          T* out, T rho, int folded, int64_t m, int64_t n, int64_t ld,
+                          cudaStream_t st);
 
 template <class T>
 void launch_plan_max(const T* xy, const T* cost, T rho, int folded, int64_t m, int64_t n,

@@ -112,15 +112,18 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_ASYNC_MINB)
 }
 
 // The shared-memory opt-in is a per-device function attribute: set it once
-// per (kernel, device), not once per process.
-template <class K>
-static void opt_in_smem(K kernel, int bytes) {
+// per (kernel, device), not once per process.  Every instantiation has its
+// own flag word (a static keyed by the function-pointer TYPE alone would be
+// shared by all K1 variants of one T -- the first launch would mark them all).
+template <class T, int MODE, bool DUAL, bool DX>
+static void opt_in_pass_smem(int bytes) {
   static std::atomic<unsigned long long> done{0};
   int dev = 0;
   cudaGetDevice(&dev);
   const unsigned long long bit = 1ull << (dev & 63);
   if (done.load(std::memory_order_acquire) & bit) return;
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(pass_kernel_async<T, MODE, DUAL, DX>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   done.fetch_or(bit, std::memory_order_acq_rel);
 }
 
@@ -131,7 +134,7 @@ static void launch_pass_t(const PassArgs<T>& a, cudaStream_t st) {
   dim3 grid(static_cast<unsigned>((a.m + rows_cta - 1) / rows_cta),
             static_cast<unsigned>((a.n + a.tc - 1) / a.tc));
   const size_t smem = async_smem_bytes<T>();
-  opt_in_smem(pass_kernel_async<T, MODE, DUAL, DX>, static_cast<int>(smem));
+  opt_in_pass_smem<T, MODE, DUAL, DX>(static_cast<int>(smem));
   if (a.pdl) {  // launched as a programmatic dependent of the cooperative tail
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
@@ -1163,6 +1166,36 @@ void launch_materialize(const T* xy, const T* cost, T* out, T rho, int folded,
   count_launch();
 }
 
+// materialize_y (solver.hpp:221-230): Y = materialize_plan(...) + phi e' +
+// f varphi', accumulated as the reference does: y_ij = x_ij + (phi_i + varphi_j)
+template <class T>
+__global__ void materialize_y_kernel(const T* xy, const T* cost, const T* phi,
+                                     const T* varphi, T* out, T rho, int folded,
+                                     int64_t m, int64_t n, int64_t ld) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const T ph = phi[i];
+  for (int64_t j = blockIdx.y; j < n; j += gridDim.y) {
+    T x = xy[j * ld + i];
+    if (folded) {
+      const T v = x + rho * cost[j * ld + i];
+      x = v > T(0) ? v : T(0);
+    }
+    out[j * ld + i] = x + (ph + varphi[j]);
+  }
+}
+
+template <class T>
+void launch_materialize_y(const T* xy, const T* cost, const T* phi, const T* varphi,
+                          T* out, T rho, int folded, int64_t m, int64_t n, int64_t ld,
+                          cudaStream_t st) {
+  dim3 grid(static_cast<unsigned>((m + 255) / 256),
+            static_cast<unsigned>(imin64(n, 2048)));
+  materialize_y_kernel<T><<<grid, 256, 0, st>>>(xy, cost, phi, varphi, out, rho, folded,
+                                                m, n, ld);
+  count_launch();
+}
+
 // ---------------------------------------------------------------------------
 // Support of the materialized plan (SURVEY §8(c) sparsity-support parity):
 // stats[0] = bits of max_ij x_ij (x >= 0 orders like its bit pattern),
@@ -1248,6 +1281,9 @@ void launch_plan_count(const T* xy, const T* cost, T rho, int folded, int64_t m,
                                    cudaStream_t);                              \
   template void launch_materialize<T>(const T*, const T*, T*, T, int, int64_t, \
                                       int64_t, int64_t, cudaStream_t);         \
+  template void launch_materialize_y<T>(const T*, const T*, const T*,          \
+                                        const T*, T*, T, int, int64_t,         \
+                                        int64_t, int64_t, cudaStream_t);       \
   template void launch_plan_max<T>(const T*, const T*, T, int, int64_t,        \
                                    int64_t, int64_t, unsigned long long*,      \
                                    cudaStream_t);                              \

@@ -267,7 +267,7 @@ int Session<T>::scan_matrix(const T* buf, unsigned long long* nf, unsigned long 
 
 // check_marginal (problem.hpp:103-117), host: sequential double sum
 template <class T>
-int Session<T>::check_marginal(const std::vector<T>& vv, const char* name) {
+int Session<T>::check_marginal(const std::vector<T>& vv, const char* name, double tol) {
   if (vv.empty()) return set_error(DROTB_ERRC_EMPTY_DIMENSION, std::string(name) + " is empty");
   double sum = 0;
   for (T e : vv) {
@@ -277,7 +277,7 @@ int Session<T>::check_marginal(const std::vector<T>& vv, const char* name) {
       return set_error(DROTB_ERRC_MARGINAL_NOT_SIMPLEX, std::string(name) + " has a negative entry");
     sum += static_cast<double>(e);
   }
-  if (std::abs(sum - 1.0) > 1e-12)
+  if (std::abs(sum - 1.0) > tol)
     return set_error(DROTB_ERRC_MARGINAL_NOT_SIMPLEX,
                      std::string(name) + " sums to " + std::to_string(sum));
   return 0;
@@ -307,8 +307,8 @@ int Session<T>::set_problem(const T* C_, const T* p_, const T* q_, bool is_devic
         return set_error(DROTB_ERRC_NON_FINITE_ENTRY, "cost matrix has a non-finite entry");
       return set_error(DROTB_ERRC_NEGATIVE_COST, "cost matrix has a negative entry");
     }
-    RC_TRY(check_marginal(hp, "p"));
-    RC_TRY(check_marginal(hq, "q"));
+    RC_TRY(check_marginal(hp, "p", simplex_tol));
+    RC_TRY(check_marginal(hq, "q", simplex_tol));
     return 0;
   }
   // sharded: local scans, then a collective verdict (every rank agrees);
@@ -333,9 +333,9 @@ int Session<T>::set_problem(const T* C_, const T* p_, const T* q_, bool is_devic
   RC_TRY(h2d_small(dpack + 8, &psum, sizeof(double)));
   RC_TRY(allreduce(dpack + 8, 1, ncclSum));
   RC_TRY(d2h_small(&psum, dpack + 8, sizeof(double)));
-  if (std::abs(psum - 1.0) > 1e-12)
+  if (std::abs(psum - 1.0) > simplex_tol)
     return set_error(DROTB_ERRC_MARGINAL_NOT_SIMPLEX, "p sums to " + std::to_string(psum));
-  return check_marginal(hq, "q");
+  return check_marginal(hq, "q", simplex_tol);
 }
 
 
@@ -974,8 +974,8 @@ template int Session<float>::download_matrix(float* dst, const float* src);
 template int Session<double>::download_matrix(double* dst, const double* src);
 template int Session<float>::scan_matrix(const float* buf, unsigned long long* nf, unsigned long long* ng);
 template int Session<double>::scan_matrix(const double* buf, unsigned long long* nf, unsigned long long* ng);
-template int Session<float>::check_marginal(const std::vector<float>& vv, const char* name);
-template int Session<double>::check_marginal(const std::vector<double>& vv, const char* name);
+template int Session<float>::check_marginal(const std::vector<float>& vv, const char* name, double tol);
+template int Session<double>::check_marginal(const std::vector<double>& vv, const char* name, double tol);
 template int Session<float>::set_problem(const float* C_, const float* p_, const float* q_, bool is_device, bool validate);
 template int Session<double>::set_problem(const double* C_, const double* p_, const double* q_, bool is_device, bool validate);
 template int Session<float>::resolve_rho();

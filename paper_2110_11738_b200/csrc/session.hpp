@@ -204,7 +204,9 @@ struct Session {
   int scan_matrix(const T* buf, unsigned long long* nf, unsigned long long* ng);
 
   // check_marginal (problem.hpp:103-117), host: sequential double sum
-  static int check_marginal(const std::vector<T>& vv, const char* name);
+  static int check_marginal(const std::vector<T>& vv, const char* name, double tol);
+  // check_problem's simplex_tol (problem.hpp:122-124); solve uses the default
+  double simplex_tol = 1e-12;
 
   // set_problem + check_problem (problem.hpp:122-136)
   int set_problem(const T* C_, const T* p_, const T* q_, bool is_device,

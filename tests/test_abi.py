@@ -42,7 +42,7 @@ def test_no_cuda_needed_for_host_entry_points():
 def test_cpp_dropin_compiles(tmp_path):
     exe = tmp_path / "dropin"
     lib_dir = os.path.join(ROOT, "paper_2110_11738_b200")
-    r = subprocess.run(["g++", "-std=c++17", "-O1", "-Wall", "-I", os.path.join(ROOT, "include"),
+    r = subprocess.run(["g++", "-std=c++20", "-O1", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"),
                         os.path.join(ROOT, "tests", "cpp", "dropin_solve.cpp"), "-o", str(exe),
                         "-L", lib_dir, "-ldrotb200", f"-Wl,-rpath,{lib_dir}"],
                        capture_output=True, text=True)
