@@ -698,9 +698,10 @@ SolveResult<T> solve(const TransportProblem<T>& pr, const DrotConfig& cfg,
   res.cert.mu.assign(m, T(0));
   res.cert.nu.assign(n, T(0));
   std::int64_t cap = 0;
-  if (cfg.record_trace) {
+  if (cfg.record_trace) {  // the device trace holds at most 2^23 rows (as the other front ends)
     const std::int64_t te = cfg.trace_every > 0 ? cfg.trace_every : 1;
-    cap = (cfg.max_iters > 0 ? cfg.max_iters : 0) / te + 1;
+    cap = std::min<std::int64_t>((cfg.max_iters > 0 ? cfg.max_iters : 0) / te + 1,
+                                 std::int64_t(1) << 23);
   }
   std::vector<drotb_trace_row> rows(static_cast<std::size_t>(cap ? cap : 1));
   drotb_report rep{};

@@ -714,14 +714,18 @@ void drotb_release_cache(void) {
   solve_cache<double>().s.reset();
 }
 
-// Profiling aid: copy (and reset) the 8 tail-phase timestamps (ns).
-int drotb_session_tail_stamps(drotb_session* s, uint64_t* out8) {
+// Profiling aid: copy (and reset) the device timeline (drotb_internal.hpp
+// kStampWords words: slot-major, (min, max) ns per point).
+int drotb_session_tail_stamps(drotb_session* s, uint64_t* out) {
   return with_session(s, [&](auto* ss) -> int {
     if (!ss->tstamps) return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "DROTB_TAIL_STAMPS not set");
     CUDA_TRY(cudaStreamSynchronize(ss->stream));
-    CUDA_TRY(cudaMemcpy(out8, ss->tstamps, 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
-    uint64_t init[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
-    CUDA_TRY(cudaMemcpy(ss->tstamps, init, sizeof(init), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(out, ss->tstamps, drotb::kStampWords * sizeof(uint64_t),
+                        cudaMemcpyDeviceToHost));
+    std::vector<uint64_t> init(drotb::kStampWords);
+    for (int k = 0; k < drotb::kStampWords; ++k) init[k] = (k & 1) ? 0ull : ~0ull;
+    CUDA_TRY(cudaMemcpy(ss->tstamps, init.data(), init.size() * sizeof(uint64_t),
+                        cudaMemcpyHostToDevice));
     return 0;
   });
 }

@@ -28,6 +28,15 @@ constexpr int kWarpsPerCta = 4;
 constexpr int kChunkCols = 16;   // columns staged per warp for the v sums
 constexpr int kVBlockRows = 64;  // reference block_rows of the v strips
 
+// Profiling aid (DROTB_TAIL_STAMPS=1): a %globaltimer timeline of the solve
+// loop, kStampSlots iterations deep (slot = iteration & (kStampSlots - 1)),
+// kStampPts points per iteration, each as a (min, max) pair over CTAs:
+//   0 K1 entry, 1 K1 exit, 2 tail entry, 3 tail merge done, 4 tail release
+//   (scalar section done), 5 tail update done, 6 tail exit
+constexpr int kStampSlots = 64;
+constexpr int kStampPts = 8;
+constexpr int kStampWords = kStampSlots * kStampPts * 2;
+
 template <class T>
 struct PassPartial {  // per-CTA partial reductions (fused.hpp:85-93)
   T cost, prev, dual, dx, max_abs;
@@ -49,6 +58,8 @@ struct PassArgs {
   T* __restrict__ vstrip;
   PassPartial<T>* __restrict__ partials;
   const int* stop;      // device stop flag (nullptr: never)
+  unsigned long long* stamps;  // profiling aid (DROTB_TAIL_STAMPS): device timeline, or null
+  const int64_t* iter;         // Book::iter (timeline slot of this sweep)
   int32_t pdl;          // launch as a programmatic dependent (after the coop tail)
   int32_t l2hint;       // 1: stream X / C with an L2 evict_first policy (sweep.cuh)
   int32_t pad_l2;

@@ -98,14 +98,33 @@ __device__ void gate_fused(Book<T>* bk, const TailArgs<T>& t, double dual_alg) {
   bk->pend_last_cost = bk->last_cost;
   bk->pend_use_dx = (t.reads_cost && t.want_dx) ? 1 : 0;
   bk->pend_dx = static_cast<double>(bk->pass_dx);
+  // pre-filter: the closed-form dual value differs from the reference's sum
+  // by rounding only, so the gap test gets a slack far above that rounding
+  // (and far below tol_gap); gate_recheck then applies the reference's exact
+  // test (solver.hpp:498-504) before any confirm report runs
+  const double slack = 1e-6 * bk->tol_gap + 1e-12 * fabs(bk->last_cost);
   const bool fire = check && r_primal * bk->primal_scale <= bk->tol_primal &&
-                    bk->last_r_dual <= bk->tol_dual && gap * gap_scale <= bk->tol_gap;
+                    bk->last_r_dual <= bk->tol_dual && gap * gap_scale <= bk->tol_gap + slack;
   if (fire) {
     bk->confirm = 1;
     bk->gate_hits += 1;
   } else if (k + 1 >= bk->max_iters) {
     bk->stop = 1;
   }
+}
+
+// After patch_pending has put the EXACT dual value of the gated iteration in
+// the Book: the reference's gap test on it (solver.hpp:498-504).  A pre-filter
+// fire the exact gap rejects is withdrawn (no confirm report, the loop goes
+// on -- or stops at max_iters, as the reference would).
+template <class T>
+__device__ void gate_recheck(Book<T>* bk) {
+  if (!bk->confirm) return;
+  const double gap_scale = bk->relative ? 1.0 / (1.0 + fabs(bk->pend_last_cost)) : 1.0;
+  if (bk->gap * gap_scale <= bk->tol_gap) return;
+  bk->confirm = 0;
+  bk->gate_hits -= 1;
+  bk->stop = bk->iter >= bk->max_iters ? 1 : 0;
 }
 
 }  // namespace drotb

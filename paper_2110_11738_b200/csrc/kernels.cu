@@ -49,8 +49,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_ASYNC_MINB)
   // programmatic dependent launch: the CTAs may be scheduled while the
   // preceding tail kernel still runs; wait for its completion and memory
   // before touching any data (no-op for an ordinary launch)
+  const unsigned long long t_entry = a.stamps ? global_ns() : 0ull;
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (a.stop != nullptr && *reinterpret_cast<const volatile int*>(a.stop)) return;
+  const int64_t it_stamp = a.stamps ? *reinterpret_cast<const volatile int64_t*>(a.iter) : 0;
+  if (a.stamps && threadIdx.x == 0) timeline_point(a.stamps, it_stamp, 0, t_entry);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr size_t ring_v = static_cast<size_t>(kAsyncS) * 2 * kAsyncG * 32;  // V per warp
@@ -108,6 +111,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_ASYNC_MINB)
       out.bad |= wacc[w].bad ? 1 : 0;
     }
     st_partial_keep(a.partials + static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x, out);
+    if (a.stamps) timeline_point(a.stamps, it_stamp, 1, global_ns());
   }
 }
 

@@ -99,9 +99,11 @@ int Session<T>::setup_coop_tail() {
   CUDA_TRY(cudaMemsetAsync(tbar, 0, 1024 * sizeof(unsigned), stream));
   if (const char* e = std::getenv("DROTB_TAIL_STAMPS"))
     if (e[0] == '1') {
-      RC_TRY(dev_alloc(&tstamps, 8));
-      const unsigned long long init[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
-      CUDA_TRY(cudaMemcpy(tstamps, init, sizeof(init), cudaMemcpyHostToDevice));
+      RC_TRY(dev_alloc(&tstamps, kStampWords));
+      std::vector<unsigned long long> init(kStampWords);
+      for (int k = 0; k < kStampWords; ++k) init[k] = (k & 1) ? 0ull : ~0ull;
+      CUDA_TRY(cudaMemcpy(tstamps, init.data(), sizeof(unsigned long long) * kStampWords,
+                          cudaMemcpyHostToDevice));
     }
   CUDA_TRY(cudaStreamSynchronize(stream));
   coop = true;
@@ -477,6 +479,8 @@ PassArgs<T> Session<T>::pass_args() {
   pa.vstrip = vstrip;
   pa.partials = partials;
   pa.stop = &book->stop;
+  pa.stamps = tstamps;
+  pa.iter = &book->iter;
   pa.pdl = (coop && pdl_ok) ? 1 : 0;
   pa.l2hint = l2hint;
   pa.pad_l2 = 0;

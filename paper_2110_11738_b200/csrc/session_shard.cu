@@ -175,6 +175,8 @@ int Session<T>::sharded_report(bool always) {
   if (xmode == 1) RC_TRY(shard_patch_pending());
   Book<T> hb;
   RC_TRY(read_book(&hb));
+  // the exact gap withdrew the gate (gate_recheck; same verdict on every rank)
+  if (!always && xmode == 1 && !hb.confirm) return 0;
   TailArgs<T> ta = tail_args(hb.iter, kPlain0, hb.folded != 0, true);
   launch_report<T>(X, C, ta, false, always, stream);
   RC_TRY(allreduce(dpack + 4, 2, ncclSum));

@@ -402,8 +402,9 @@ int sinkhorn_t(const T* C, int64_t m, int64_t n, const T* p, const T* q, T eta, 
         r.iter = it;
         r.r_primal = errs[c];
         r.r_dual = -1.0;  // kResidualNotApplicable (problem.hpp:64)
-        const double nan = std::numeric_limits<double>::quiet_NaN();
-        r.gap = r.objective = r.ergodic_objective = r.fixed_point_residual = nan;
+        // the reference leaves the other TraceRow fields at their defaults
+        // (problem.hpp:77-85; reference.hpp:279-283)
+        r.gap = r.objective = r.ergodic_objective = r.fixed_point_residual = 0.0;
       }
       ++rows;
     }

@@ -130,6 +130,19 @@ __device__ __forceinline__ double2 ld_keep(const double2* p) {
                : "l"(p), "l"(keep_policy()));
   return v;
 }
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// one timeline point (min and max over the CTAs that record it)
+__device__ __forceinline__ void timeline_point(unsigned long long* st, int64_t iter, int pt,
+                                               unsigned long long t) {
+  unsigned long long* w = st + ((iter & (kStampSlots - 1)) * kStampPts + pt) * 2;
+  atomicMin(w, t);
+  atomicMax(w + 1, t);
+}
+
 template <class T>
 struct PassPartial;
 // per-CTA K1 scalars, kept in L2 for the tail

@@ -37,15 +37,10 @@ constexpr int kTT = 256;            // threads per CTA
 constexpr int kTW = kTT / 32;       // warps per CTA = strip partitions in A
 constexpr int kTSlots = 16;         // per-CTA partial slots
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-// profiling aid (DROTB_TAIL_STAMPS): per-phase min / max timestamps
-#define TAIL_STAMP(slot, op)                                            \
-  do {                                                                  \
-    if (t.stamps && threadIdx.x == 0) op(t.stamps + (slot), gtimer());  \
+// profiling aid (DROTB_TAIL_STAMPS): timeline points (drotb_internal.hpp)
+#define TAIL_STAMP(pt)                                                          \
+  do {                                                                          \
+    if (t.stamps && threadIdx.x == 0) timeline_point(t.stamps, it_stamp, pt, global_ns()); \
   } while (0)
 
 // Every CTA has published its partials; the last CTA to arrive runs fn()
@@ -169,9 +164,10 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
   // the next sweep (a programmatic dependent) may be scheduled now; it waits
   // in griddepcontrol.wait for this grid's completion
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  TAIL_STAMP(0, atomicMin);
+  const int64_t it_stamp = t.stamps ? *reinterpret_cast<volatile int64_t*>(&bk->iter) : 0;
+  TAIL_STAMP(2);
   if (*reinterpret_cast<volatile int*>(&bk->stop)) return;
-  __shared__ T red[kTW][32];
+  __shared__ __align__(16) T red[kTT * R];  // merge partition sums [P][CV][R]
   __shared__ Book<T> sbk;
   __shared__ T shT[16 * kTW];
   __shared__ double shD[16 * kTW];
@@ -184,69 +180,108 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
   unsigned my_gen = s_gen0;
 
   // ---- A: merge -----------------------------------------------------------
+  // The (m + n) merged sums as RV-wide vectors (16-B loads): u vectors
+  // [0, nvu), v vectors [nvu, nvu + nvv).  CTA b owns the balanced range
+  // [b*NV/G, (b+1)*NV/G); thread t of a chunk of CV vectors handles vector
+  // t % CV over the strip rows g = t / CV (mod P), 8 loads in flight, and
+  // the P partition sums are combined in a fixed order in shared memory.
   {
     T pr[3] = {T(0), T(0), T(0)};
     double pd[4] = {0, 0, 0, 0};  // sum p a, sum p r, sum q b, sum q s (fused gate)
-    const int64_t ngr = (m + 31) / 32, ngc = (n + 31) / 32;
-    for (int64_t grp = blockIdx.x; grp < ngr + ngc; grp += G) {
-      T acc = T(0);
-      if (grp < ngr) {
-        const int64_t idx = grp * 32 + lane;
-        if (idx < m) {
-          int64_t g = warp;
-          for (; g + 7 * kTW < t.grid_cols; g += 8 * kTW) {
-            T v8[8];
+    const int64_t nvu = (m + R - 1) / R, nvv = (n + R - 1) / R, NV = nvu + nvv;
+    const bool vvec = (n % R) == 0;  // v strip rows 16-B aligned
+    const int64_t v0 = static_cast<int64_t>(blockIdx.x) * NV / G;
+    const int64_t v1 = static_cast<int64_t>(blockIdx.x + 1) * NV / G;
+    const int64_t cnt = v1 - v0;
+    int P = cnt > 0 ? static_cast<int>(kTT / cnt) : 8;
+    P = P < 1 ? 1 : (P > 8 ? 8 : P);
+    const int CV = kTT / P;
+    T* redv = red;
+    for (int64_t c0 = v0; c0 < v1; c0 += CV) {
+      const int64_t vec = c0 + tid % CV;
+      const int part = tid / CV;
+      T acc[R];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) v8[q] = t.ustrip[(g + q * kTW) * t.ld + idx];
+      for (int k = 0; k < R; ++k) acc[k] = T(0);
+      if (part < P && vec < v1) {
+        const bool isu = vec < nvu;
+        const int64_t rows = isu ? t.grid_cols : t.grid_rows64;
+        const int64_t stride = isu ? t.ld : n;
+        const T* base = isu ? t.ustrip + vec * R : t.vstrip + (vec - nvu) * R;
+        if (isu || vvec) {
+          const V* bv = reinterpret_cast<const V*>(base);
+          const int64_t sv = stride / R;
+          int64_t g = part;
+          for (; g + 7 * P < rows; g += 8 * P) {
+            V x8[8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) acc += v8[q];
+            for (int q = 0; q < 8; ++q) x8[q] = bv[(g + q * P) * sv];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              T e[R];
+              unpack(x8[q], e);
+#pragma unroll
+              for (int k = 0; k < R; ++k) acc[k] += e[k];
+            }
           }
-          for (; g < t.grid_cols; g += kTW) acc += t.ustrip[g * t.ld + idx];
-        }
-      } else {
-        const int64_t j = (grp - ngr) * 32 + lane;
-        if (j < n) {
-          int64_t g = warp;
-          for (; g + 7 * kTW < t.grid_rows64; g += 8 * kTW) {
-            T v8[8];
+          for (; g < rows; g += P) {
+            T e[R];
+            unpack(bv[g * sv], e);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) v8[q] = t.vstrip[(g + q * kTW) * n + j];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) acc += v8[q];
+            for (int k = 0; k < R; ++k) acc[k] += e[k];
           }
-          for (; g < t.grid_rows64; g += kTW) acc += t.vstrip[g * n + j];
+        } else {  // v strips of a row length that is not a multiple of R
+          const int64_t j0 = (vec - nvu) * R;
+          for (int64_t g = part; g < rows; g += P)
+#pragma unroll
+            for (int k = 0; k < R; ++k)
+              if (j0 + k < n) acc[k] += base[g * stride + k];
         }
       }
-      red[warp][lane] = acc;
       __syncthreads();
-      if (warp == 0) {
-        T tot = T(0);
+      if (part < P)
 #pragma unroll
-        for (int w = 0; w < kTW; ++w) tot += red[w][lane];
-        if (grp < ngr) {
-          const int64_t idx = grp * 32 + lane;
-          if (idx < m) {
-            const T pi = ld_keep(t.p + idx);
-            const T r = tot - pi;
-            st_keep(t.r_new + idx, r, 2);
-            pr[0] += r;
-            pr[1] += r * r;
-            pd[0] += static_cast<double>(pi) * static_cast<double>(ld_keep(t.a + idx));
-            pd[1] += static_cast<double>(pi) * static_cast<double>(r);
+        for (int k = 0; k < R; ++k) redv[(part * CV + tid % CV) * R + k] = acc[k];
+      __syncthreads();
+      if (tid < CV && vec < v1) {
+        T tot[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          T sum = T(0);
+          for (int q = 0; q < P; ++q) sum += redv[(q * CV + tid) * R + k];
+          tot[k] = sum;
+        }
+        if (vec < nvu) {
+          const int64_t i0 = vec * R;
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            const int64_t idx = i0 + k;
+            if (idx < m) {
+              const T pi = ld_keep(t.p + idx);
+              const T r = tot[k] - pi;
+              st_keep(t.r_new + idx, r, 2);
+              pr[0] += r;
+              pr[1] += r * r;
+              pd[0] += static_cast<double>(pi) * static_cast<double>(ld_keep(t.a + idx));
+              pd[1] += static_cast<double>(pi) * static_cast<double>(r);
+            }
           }
         } else {
-          const int64_t j = (grp - ngr) * 32 + lane;
-          if (j < n) {
-            const T qj = ld_keep(t.q + j);
-            const T s = tot - qj;
-            st_keep(t.s_new + j, s, 2);
-            pr[2] += s * s;
-            pd[2] += static_cast<double>(qj) * static_cast<double>(ld_keep(t.b + j));
-            pd[3] += static_cast<double>(qj) * static_cast<double>(s);
+          const int64_t j0 = (vec - nvu) * R;
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            const int64_t j = j0 + k;
+            if (j < n) {
+              const T qj = ld_keep(t.q + j);
+              const T sv = tot[k] - qj;
+              st_keep(t.s_new + j, sv, 2);
+              pr[2] += sv * sv;
+              pd[2] += static_cast<double>(qj) * static_cast<double>(ld_keep(t.b + j));
+              pd[3] += static_cast<double>(qj) * static_cast<double>(sv);
+            }
           }
         }
       }
-      __syncthreads();
     }
     // this CTA's fixed slice of the K1 CTA scalars
     const int64_t np = t.n_pass_partials;
@@ -276,7 +311,7 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
     if (t.fused_gate) store_partials<double, 4>(pd, dpart, 10, shD);
     if (tid == 0) cpart[blockIdx.x * kTSlots + 8] = cmx;
   }
-  TAIL_STAMP(1, atomicMax);
+  TAIL_STAMP(3);
   reduce_barrier(bar, my_gen, [&] {
     // ONE round of loads: the Book words and, per CTA, the 8 T sums, the max,
     // the previous update's 8 double partials and this merge's 4 (fused gate)
@@ -355,9 +390,8 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
       }
     }
     book_store(bk, &sbk);
-    TAIL_STAMP(2, atomicMax);
+    TAIL_STAMP(4);
   });
-  TAIL_STAMP(3, atomicMax);
   if (*reinterpret_cast<volatile int*>(&bk->failed)) return;  // non-finite pass
   if (!t.fused_gate && *reinterpret_cast<volatile int*>(&bk->stop)) return;
 
@@ -404,13 +438,15 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
     }
     store_partials<double, 8>(part, dpart, 0, shD);
   }
-  TAIL_STAMP(4, atomicMax);
+  TAIL_STAMP(5);
   if (t.fused_gate) {
     // gate already decided after the merge; the confirm report needs the
     // updated phi / varphi everywhere and the exact dual value
     if (!*reinterpret_cast<volatile int*>(&bk->confirm) ||
-        *reinterpret_cast<volatile int*>(&bk->stop) == 1)
+        *reinterpret_cast<volatile int*>(&bk->stop) == 1) {
+      TAIL_STAMP(6);
       return;
+    }
     reduce_barrier(bar, my_gen, [&] {
       constexpr int BW = static_cast<int>(sizeof(Book<T>) / 8);
       unsigned long long bw = tid < BW ? __ldcg(reinterpret_cast<const unsigned long long*>(bk) + tid)
@@ -419,7 +455,10 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
       totals<double, 8>(dpart, G, 0, d8, shD);
       if (tid < BW) reinterpret_cast<unsigned long long*>(&sbk)[tid] = bw;
       __syncthreads();
-      if (tid == 0) patch_pending<T>(&sbk, t, d8);
+      if (tid == 0) {
+        patch_pending<T>(&sbk, t, d8);
+        gate_recheck<T>(&sbk);  // exact gap before the report
+      }
       book_store(bk, &sbk);
     });
   } else {
@@ -434,10 +473,8 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
     if (tid == 0)
       gate_logic<T>(&sbk, t, d8[0] + d8[4], d8[1], d8[2], d8[5], d8[6], d8[3] + d8[7]);
     book_store(bk, &sbk);
-    TAIL_STAMP(5, atomicMax);
   });
   }
-  TAIL_STAMP(6, atomicMax);
   if (!*reinterpret_cast<volatile int*>(&bk->confirm) ||
       *reinterpret_cast<volatile int*>(&bk->stop) == 1)
     return;
@@ -913,7 +950,9 @@ __global__ void __launch_bounds__(kTT) shard_pending_patch_kernel(const TailArgs
   if (threadIdx.x == 0) {
     Book<T> lb = *bk;
     const double d8[8] = {glob4[0], glob4[1], glob4[2], glob4[3], c4[0], c4[1], c4[2], c4[3]};
+    const bool paused = lb.confirm && lb.stop == 2;
     patch_pending<T>(&lb, t, d8);
+    if (paused) gate_recheck<T>(&lb);  // exact gap (replicated on every rank)
     *bk = lb;
   }
 }

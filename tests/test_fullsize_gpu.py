@@ -125,13 +125,17 @@ def test_fullsize_fast_order(drot, ref, name, request):
     x, w = got.plan.x.ravel(order="F"), want.plan
     scale = float(np.abs(w).max())
     diff = float(np.abs(x.astype(np.float64) - w).max())
-    rel_obj = abs(got.report.objective - want.report["objective"]) / abs(want.report["objective"])
-    print(f"{name}: K={K[name]} max|dX|/max|X| = {diff / scale:.3e}, objective rel {rel_obj:.3e}")
+    # the objective is exactly 0 while the iterate sits in the all-zero
+    # warm-up phase of the product-coupling start (solver.hpp:44-49), hence
+    # the absolute floor next to the relative tolerance
+    rtol, atol = (1e-4, 1e-9) if fp32 else (1e-10, 1e-18)
+    d_obj = abs(got.report.objective - want.report["objective"])
+    print(f"{name}: K={K[name]} max|dX|/max|X| = {diff / max(scale, 1e-300):.3e}, "
+          f"objective {want.report['objective']:.6e} diff {d_obj:.3e}")
     assert diff <= (1e-4 if fp32 else 1e-10) * scale
-    assert rel_obj <= (1e-4 if fp32 else 1e-10)
+    assert d_obj <= rtol * abs(want.report["objective"]) + atol
     for gr, rr in zip(got.trace.rows, want.trace):
-        assert abs(gr.objective - rr["objective"]) <= (1e-4 if fp32 else 1e-10) * abs(
-            rr["objective"]) + 1e-30, gr.iter
+        assert abs(gr.objective - rr["objective"]) <= rtol * abs(rr["objective"]) + atol, gr.iter
     _props(got, prob[3], prob[4])
 
 

@@ -88,6 +88,11 @@ def test_matches_reference_sinkhorn(drot, ref, dt, shape, eta, tol):
                               20000, exact_report=True)
     assert got.status.name == want.status
     assert abs(got.trace.iterations - want.iterations) <= 10  # one check interval
+    # every row: r_dual = kResidualNotApplicable, the other fields left at the
+    # TraceRow defaults (0) as the reference pushes them (reference.hpp:279-283)
+    for a in got.trace.rows:
+        assert a.r_dual == -1.0
+        assert (a.gap, a.objective, a.ergodic_objective, a.fixed_point_residual) == (0, 0, 0, 0)
     rel = 1e-7 if dt == np.float64 else 1e-3
     assert abs(got.report.objective - want.report["objective"]) <= rel * abs(
         want.report["objective"])
