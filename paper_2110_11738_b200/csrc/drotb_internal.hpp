@@ -32,9 +32,18 @@ constexpr int kVBlockRows = 64;  // reference block_rows of the v strips
 // loop, kStampSlots iterations deep (slot = iteration & (kStampSlots - 1)),
 // kStampPts points per iteration, each as a (min, max) pair over CTAs:
 //   0 K1 entry, 1 K1 exit, 2 tail entry, 3 tail merge done, 4 tail release
-//   (scalar section done), 5 tail update done, 6 tail exit
+//   (scalar section done), 5 tail update done, 6 tail exit, 7 merge strips
+//   loaded, 8 merge r/s stored, 9 K1 partial slice loaded, 10 last CTA
+//   knows it is last, 11 last CTA partial loads + sums done, 12 last CTA
+//   scalar logic done, 13 release observed (waiting CTAs)
+// fixed-point row / column sums (PassArgs::fx): value = integer * 2^-46,
+// |sum| < 2^17; resolution 1.4e-14 per partial (fp32 sums of O(1e-5..1)
+// entries need ~1e-12 absolute)
+constexpr double kFxScale = 70368744177664.0;       // 2^46
+constexpr double kFxInv = 1.4210854715202004e-14;   // 2^-46
+
 constexpr int kStampSlots = 64;
-constexpr int kStampPts = 8;
+constexpr int kStampPts = 16;
 constexpr int kStampWords = kStampSlots * kStampPts * 2;
 
 template <class T>
@@ -60,6 +69,13 @@ struct PassArgs {
   const int* stop;      // device stop flag (nullptr: never)
   unsigned long long* stamps;  // profiling aid (DROTB_TAIL_STAMPS): device timeline, or null
   const int64_t* iter;         // Book::iter (timeline slot of this sweep)
+  // fx = 1 (fp32 fast order, one GPU): the row / column sums are accumulated
+  // as 64-bit fixed point (kFxScale) with integer atomics -- exact, hence
+  // order-independent and deterministic -- instead of strips
+  long long* ufx;
+  long long* vfx;
+  int32_t fx;
+  int32_t pad_fx;
   int32_t pdl;          // launch as a programmatic dependent (after the coop tail)
   int32_t l2hint;       // 1: stream X / C with an L2 evict_first policy (sweep.cuh)
   int32_t pad_l2;
@@ -102,11 +118,9 @@ struct Book {
   double pend_last_cost;  // last_cost seen by its gate
   double pend_dx;         // its pass dx^2
   double sum_p, sum_q;    // sum p_i, sum q_j (double, sequential; set at init)
-  // single-launch iteration (iter.cu): 1 = phi / varphi arrays hold the
-  // current duals; 0 = they are pending as phi_i = (ta_i + coef) / n and
-  // varphi_j = (tb_j + coef) / m (materialized by the next sweep's prologue,
-  // the confirm report on the fly, or the finalize kernel)
-  int32_t phi_mat, pad_pm;
+  // cooperative tail: which of its two pending-partial buffers holds the
+  // partials of pend_valid (tail.cu)
+  int32_t pend_buf, pad_pm;
 };
 
 struct TraceRowDev {
@@ -166,11 +180,18 @@ struct TailArgs {
   const T* report_c;
   unsigned long long* stamps;  // profiling aid: tail phase timestamps (or null)
   int32_t fused_gate;          // tail: gate on the algebraic dual value (one barrier less)
-  int32_t pad_fg;
+  int32_t tpar;                // tail: iteration parity (counter / pending-partial buffers)
+  long long* ufx;              // fx: the sweep's fixed-point row / column sums (read + zeroed)
+  long long* vfx;
+  int32_t fx;
+  int32_t pad_fx;
+  double inv_n_d, inv_m_d;     // 1 / double(n_global), 1 / double(m_global)
 };
 
 // Cooperative per-iteration tail (tail.cu): merge + recursions + update +
 // gate (+ confirm report) in one launch after K1 (fast order, one GPU).
+// Its double partials use kTailDSlots words per CTA (tail.cu layout).
+constexpr int kTailDSlots = 32;
 template <class T>
 int tail_grid(int device);
 template <class T>
@@ -220,6 +241,7 @@ template <class T>
 void launch_tail_finalize(const TailArgs<T>& t, const double* dpart, int grid, cudaStream_t st);
 
 // ---- kernel launchers (kernels.cu) ---------------------------------------
+void launch_spin(unsigned long long ns, cudaStream_t st);
 template <class T>
 void launch_pass(const PassArgs<T>& a, int mode, bool want_dual, bool want_dx,
                  cudaStream_t st);

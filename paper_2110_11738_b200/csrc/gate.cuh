@@ -42,7 +42,8 @@ __device__ __forceinline__ void book_store(Book<T>* dst, const Book<T>* src) {
 // fixed_point_residual) are reduced one iteration later -- or by the
 // finalize kernel at the end of a run -- and patched into its trace row.
 template <class T>
-__device__ void patch_pending(Book<T>* bk, const TailArgs<T>& t, const double (&d8)[8]) {
+__device__ void patch_pending(Book<T>* bk, const TailArgs<T>& t, const double (&d8)[8],
+                              bool write_trace = true) {
   if (!bk->pend_valid) return;
   const double dual = d8[0] + d8[4];
   double fpr = __longlong_as_double(0x7ff8000000000000ULL);
@@ -55,7 +56,7 @@ __device__ void patch_pending(Book<T>* bk, const TailArgs<T>& t, const double (&
   bk->dual_value = dual;
   bk->gap = fabs(bk->pend_last_cost - dual);
   bk->fp_residual = fpr;
-  if (t.trace && bk->pend_row >= 0 && bk->pend_row < bk->trace_cap) {
+  if (write_trace && t.trace && bk->pend_row >= 0 && bk->pend_row < bk->trace_cap) {
     TraceRowDev& row = t.trace[bk->pend_row];
     row.gap = bk->gap;
     row.fixed_point_residual = fpr;
@@ -65,7 +66,8 @@ __device__ void patch_pending(Book<T>* bk, const TailArgs<T>& t, const double (&
 }
 
 template <class T>
-__device__ void gate_fused(Book<T>* bk, const TailArgs<T>& t, double dual_alg) {
+__device__ void gate_fused(Book<T>* bk, const TailArgs<T>& t, double dual_alg,
+                           bool write_trace = true) {
   bk->alpha = bk->alpha - bk->beta;  // solver.hpp:289
   const int64_t k = bk->iter;
   bk->iter = k + 1;
@@ -77,19 +79,21 @@ __device__ void gate_fused(Book<T>* bk, const TailArgs<T>& t, double dual_alg) {
   bk->dual_value = dual_alg;
   bk->gap = gap;
   bk->fp_residual = nan;
-  const bool check = ((k + 1) % bk->check_every) == 0;
-  const bool trace_row = bk->record_trace && ((k + 1) % bk->trace_every) == 0;
+  const bool check = every(k + 1, bk->check_every);
+  const bool trace_row = bk->record_trace && every(k + 1, bk->trace_every);
   bk->pend_row = -1;
   if (trace_row) {
     if (t.trace && bk->trace_rows < bk->trace_cap) {
-      TraceRowDev& row = t.trace[bk->trace_rows];
-      row.iter = k + 1;
-      row.r_primal = r_primal;
-      row.r_dual = bk->last_r_dual;
-      row.gap = gap;  // patched with the exact dual value later
-      row.objective = bk->last_cost;
-      row.ergodic_objective = bk->erg_mean;
-      row.fixed_point_residual = nan;  // patched later
+      if (write_trace) {
+        TraceRowDev& row = t.trace[bk->trace_rows];
+        row.iter = k + 1;
+        row.r_primal = r_primal;
+        row.r_dual = bk->last_r_dual;
+        row.gap = gap;  // patched with the exact dual value later
+        row.objective = bk->last_cost;
+        row.ergodic_objective = bk->erg_mean;
+        row.fixed_point_residual = nan;  // patched later
+      }
       bk->pend_row = bk->trace_rows;
     }
     bk->trace_rows += 1;

@@ -85,8 +85,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_ASYNC_MINB)
   else
     pass_tile_async<T, MODE, DUAL, DX, true>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc, wbuf,
                                              ring, lane);
-  if (nvalid > 0)
+  if (a.fx) {
+#pragma unroll
+    for (int t = 0; t < R; ++t)
+      if (t < nvalid) red_add_fx(a.ufx + row0 + t, static_cast<double>(u[t]));
+  } else if (nvalid > 0) {
     st_keep(reinterpret_cast<V*>(a.ustrip + gc * a.ld + row0), pack4(u), a.l2hint);
+  }
 
   acc.cost = warp_sum(acc.cost);
   acc.prev = warp_sum(acc.prev);
@@ -1139,6 +1144,18 @@ void launch_validate(const T* buf, int64_t m, int64_t n, int64_t ld,
   validate_kernel<T><<<grid, 256, 0, st>>>(buf, m, n, ld, first_nonfinite,
                                            first_negative);
   count_launch();
+}
+
+// Profiling aid (DROTB_TAIL_DELAY_US): one CTA that spins for `ns`, placed
+// between K1 and the tail to separate the tail's own latency from the L2
+// state the sweep leaves behind.
+__global__ void spin_kernel(unsigned long long ns) {
+  const unsigned long long t0 = global_ns();
+  while (global_ns() - t0 < ns) {
+  }
+}
+void launch_spin(unsigned long long ns, cudaStream_t st) {
+  spin_kernel<<<1, 32, 0, st>>>(ns);
 }
 
 // ---------------------------------------------------------------------------

@@ -11,8 +11,10 @@ void Session<T>::release() {
   void* bufs[] = {X, C, Xout, phi, varphi, a, b, rb[0], rb[1], sb[0], sb[1],
                   p, q, u, v, ustrip, vstrip, tscr, partials, tiles, dscr,
                   terms, book, trace, vflags, pack, pmax, dpack, dint,
-                  tcpart, tdpart, tbar, tstamps};
+                  tcpart, tdpart, tbar, tstamps, ufx, vfx};
   tstamps = nullptr;
+  ufx = vfx = nullptr;
+  fx_ok = fx = false;
   tcpart = nullptr;
   tdpart = nullptr;
   tbar = nullptr;
@@ -93,8 +95,9 @@ int Session<T>::setup_coop_tail() {
   if (const char* e = std::getenv("DROTB_PDL")) pdl_ok = e[0] == '1';
   tgrid = tail_grid<T>(device);
   if (tgrid <= 0) return 0;
-  RC_TRY(dev_alloc(&tcpart, static_cast<size_t>(tgrid) * 16));
-  RC_TRY(dev_alloc(&tdpart, static_cast<size_t>(tgrid) * 16));
+  const size_t gp = static_cast<size_t>((tgrid + 31) / 32 * 32);  // value-major partials (tail.cu)
+  RC_TRY(dev_alloc(&tcpart, gp * 16));
+  RC_TRY(dev_alloc(&tdpart, gp * kTailDSlots));
   RC_TRY(dev_alloc(&tbar, 1024));  // top count, generation, 16 group counters (tail.cu)
   CUDA_TRY(cudaMemsetAsync(tbar, 0, 1024 * sizeof(unsigned), stream));
   if (const char* e = std::getenv("DROTB_TAIL_STAMPS"))
@@ -105,6 +108,18 @@ int Session<T>::setup_coop_tail() {
       CUDA_TRY(cudaMemcpy(tstamps, init.data(), sizeof(unsigned long long) * kStampWords,
                           cudaMemcpyHostToDevice));
     }
+  // fixed-point sums: fp32, one GPU (the shard tail merges strips and
+  // exchanges them); DROTB_FX=0 disables
+  if (std::is_same<T, float>::value && !sharded) {
+    const char* e = std::getenv("DROTB_FX");
+    if (!(e && e[0] == '0')) {
+      RC_TRY(dev_alloc(&ufx, static_cast<size_t>(ld)));
+      RC_TRY(dev_alloc(&vfx, static_cast<size_t>(n)));
+      CUDA_TRY(cudaMemsetAsync(ufx, 0, sizeof(long long) * ld, stream));
+      CUDA_TRY(cudaMemsetAsync(vfx, 0, sizeof(long long) * n, stream));
+      fx_ok = true;
+    }
+  }
   CUDA_TRY(cudaStreamSynchronize(stream));
   coop = true;
   // can a cooperative launch be captured into a graph here?  (probe on a
@@ -364,6 +379,14 @@ int Session<T>::init(const T* x0, bool x0_is_device) {
     if (!x_attached) return set_error(DROTB_ERRC_BAD_CONFIG, "peers not attached");
     CUDA_TRY(cudaMemsetAsync(xbuf, 0, kXSetupFlagOff, stream));
   }
+  if (tbar) CUDA_TRY(cudaMemsetAsync(tbar, 0, 1024 * sizeof(unsigned), stream));  // tail counters
+  if (fx_ok) {  // X0 = p q' bounds every row / column sum by 1; a warm start has no bound
+    CUDA_TRY(cudaMemsetAsync(ufx, 0, sizeof(long long) * ld, stream));
+    CUDA_TRY(cudaMemsetAsync(vfx, 0, sizeof(long long) * n, stream));
+    const bool want = x0 == nullptr;
+    if (want != fx) drop_graphs();
+    fx = want;
+  }
   if (x0) {
     RC_TRY(upload_matrix(X, x0, x0_is_device));
     unsigned long long nf, ng;
@@ -426,7 +449,7 @@ int Session<T>::init(const T* x0, bool x0_is_device) {
   hb.relative = cfg.relative_tolerances ? 1 : 0;
   hb.pend_row = -1;
   hb.pend_valid = 0;
-  hb.phi_mat = 1;
+  hb.pend_buf = 0;
   {
     double sp = 0, sq = 0;
     for (T e : hp) sp += static_cast<double>(e);
@@ -481,6 +504,10 @@ PassArgs<T> Session<T>::pass_args() {
   pa.stop = &book->stop;
   pa.stamps = tstamps;
   pa.iter = &book->iter;
+  pa.ufx = ufx;
+  pa.vfx = vfx;
+  pa.fx = fx ? 1 : 0;
+  pa.pad_fx = 0;
   pa.pdl = (coop && pdl_ok) ? 1 : 0;
   pa.l2hint = l2hint;
   pa.pad_l2 = 0;
@@ -537,6 +564,12 @@ TailArgs<T> Session<T>::tail_args(int64_t k, int mode, bool folded_after, bool s
   t.report_c = C;
   t.stamps = tstamps;
   t.fused_gate = fused_gate ? 1 : 0;
+  t.tpar = static_cast<int32_t>(k & 1);
+  t.ufx = ufx;
+  t.vfx = vfx;
+  t.fx = fx ? 1 : 0;
+  t.inv_n_d = 1.0 / static_cast<double>(n_global);
+  t.inv_m_d = 1.0 / static_cast<double>(m_global);
   return t;
 }
 
@@ -567,6 +600,13 @@ int Session<T>::enqueue_iteration(cudaEvent_t pass_begin, cudaEvent_t pass_end, 
     return 0;
   }
   if (coop && !exact && !sharded) {  // K1 + one cooperative tail kernel (tail.cu)
+    if (tstamps) {
+      static const long long delay_us = [] {
+        const char* e = std::getenv("DROTB_TAIL_DELAY_US");
+        return e ? std::atoll(e) : 0ll;
+      }();
+      if (delay_us > 0) launch_spin(static_cast<unsigned long long>(delay_us) * 1000ull, stream);
+    }
     CUDA_TRY(launch_tail<T>(ta, tcpart, tdpart, tbar, tgrid, stream));
     h_iter = k + 1;
     h_folded = folded_after;

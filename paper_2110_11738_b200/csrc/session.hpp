@@ -143,6 +143,11 @@ struct Session {
   double* tdpart = nullptr;
   unsigned* tbar = nullptr;
   unsigned long long* tstamps = nullptr;  // DROTB_TAIL_STAMPS profiling aid
+  // fixed-point row / column sums (fp32 fast order with the cooperative tail;
+  // PassArgs::fx): fx_ok = available, fx = used by the current solve (off
+  // for warm starts, whose row sums have no a-priori bound)
+  long long *ufx = nullptr, *vfx = nullptr;
+  bool fx_ok = false, fx = false;
 
   std::vector<T> hp, hq;
   T rho = T(0);

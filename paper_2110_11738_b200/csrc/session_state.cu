@@ -10,6 +10,11 @@ namespace drotb {
 template <class T>
 int Session<T>::load_state(const T* xy, int32_t folded, const T* rs, const T* cs, const T* ya, const T* yb, T alpha, const T* r, const T* s, T beta, int64_t iter) {
   RC_TRY(resolve_rho());
+  if (tbar) CUDA_TRY(cudaMemsetAsync(tbar, 0, 1024 * sizeof(unsigned), stream));  // tail counters
+  if (fx) {  // an external state carries no bound on its row sums: strips
+    drop_graphs();
+    fx = false;
+  }
   RC_TRY(upload_matrix(X, xy, false));
   CUDA_TRY(cudaMemcpyAsync(phi, rs, sizeof(T) * m, cudaMemcpyHostToDevice, stream));
   CUDA_TRY(cudaMemcpyAsync(varphi, cs, sizeof(T) * n, cudaMemcpyHostToDevice, stream));
@@ -31,7 +36,7 @@ int Session<T>::load_state(const T* xy, int32_t folded, const T* rs, const T* cs
   hb.trace_every = 1;
   hb.tol_primal = hb.tol_dual = hb.tol_gap = -1.0;
   hb.pend_row = -1;
-  hb.phi_mat = 1;
+  hb.pend_buf = 0;
   CUDA_TRY(cudaMemcpyAsync(book, &hb, sizeof(hb), cudaMemcpyHostToDevice, stream));
   CUDA_TRY(cudaStreamSynchronize(stream));
   want_dual = false;  // default PassOptions (solver.hpp:367)

@@ -297,8 +297,14 @@ __device__ __forceinline__ void compute_col(const PassArgs<T>& a, const T (&x)[1
   *reinterpret_cast<V*>(wbuf + (c * 32 + (lane ^ (c & 7))) * R) = pack4(xp);
 }
 
+__device__ __forceinline__ void red_add_fx(long long* p, double v) {
+  const long long q = __double2ll_rn(v * kFxScale);
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(q) : "memory");
+}
+
 // v-phase: lane (c, b) sums the 64 rows of block b of staged column c in
-// row order (fused.hpp:268) and writes the v strip entry.
+// row order (fused.hpp:268) and writes the v strip entry -- or, in fixed
+// point mode, the warp's column sum joins the column's integer accumulator.
 template <class T>
 __device__ __forceinline__ void v_phase(const PassArgs<T>& a, const T* wbuf, int64_t j0,
                                         int cnt, int64_t wrow0, int lane) {
@@ -306,6 +312,29 @@ __device__ __forceinline__ void v_phase(const PassArgs<T>& a, const T* wbuf, int
   constexpr int R = 16 / sizeof(T);
   constexpr int NB = 32 * R / kVBlockRows;
   constexpr int CH = kChunkCols;
+  if (a.fx) {  // one fixed-point red per (column, warp): sum the NB blocks first
+    T s = T(0);
+    if (lane < CH * NB) {
+      const int c = lane % CH, b = lane / CH;
+      const int64_t gb = wrow0 / kVBlockRows + b;
+      if (c < cnt && gb * kVBlockRows < a.m) {
+        const V* col = reinterpret_cast<const V*>(wbuf) + c * 32;
+        const int g7 = c & 7;
+        constexpr int QB = kVBlockRows / R;
+#pragma unroll
+        for (int qq = 0; qq < QB; ++qq) {
+          T v4[R];
+          unpack(col[(b * QB + qq) ^ g7], v4);
+#pragma unroll
+          for (int t = 0; t < R; ++t) s += v4[t];
+        }
+      }
+    }
+#pragma unroll
+    for (int o = CH; o < 32; o <<= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane < CH && lane < cnt && wrow0 < a.m) red_add_fx(a.vfx + j0 + lane, static_cast<double>(s));
+    return;
+  }
   if (lane < CH * NB) {
     const int c = lane % CH, b = lane / CH;
     const int64_t gb = wrow0 / kVBlockRows + b;
@@ -512,6 +541,12 @@ __device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0
 // Solve-loop scalar logic shared by the tail kernels and the persistent
 // solver kernel (operates on a Book<T>, in global or shared memory)
 // ---------------------------------------------------------------------------
+// (i % period) == 0 without a 64-bit division in the common period == 1
+// (the default check_every / trace_every)
+__device__ __forceinline__ bool every(int64_t i, int64_t period) {
+  return period == 1 || (i % period) == 0;
+}
+
 template <class T>
 __device__ __forceinline__ void erg_update(Book<T>* bk, double value) {
   bk->erg_count += 1;
@@ -564,7 +599,8 @@ __device__ void merge_scalars(Book<T>* bk, const TailArgs<T>& t, const T (&tot)[
 // when row-sharded) when the stale-dual gate passes.
 template <class T>
 __device__ void gate_logic(Book<T>* bk, const TailArgs<T>& t, double dual_value, double dphi2,
-                           double dphi, double dvarphi2, double dvarphi, double cross) {
+                           double dphi, double dvarphi2, double dvarphi, double cross,
+                           bool write_trace = true) {
   const bool fp = bk->record_trace != 0;
   bk->alpha = bk->alpha - bk->beta;  // solver.hpp:289
   const int64_t k = bk->iter;
@@ -583,10 +619,10 @@ __device__ void gate_logic(Book<T>* bk, const TailArgs<T>& t, double dual_value,
   bk->r_primal = r_primal;
   bk->dual_value = dual_value;
   bk->gap = gap;
-  const bool check = ((k + 1) % bk->check_every) == 0;
-  const bool trace_row = bk->record_trace && ((k + 1) % bk->trace_every) == 0;
+  const bool check = every(k + 1, bk->check_every);
+  const bool trace_row = bk->record_trace && every(k + 1, bk->trace_every);
   if (trace_row) {
-    if (t.trace && bk->trace_rows < bk->trace_cap) {
+    if (write_trace && t.trace && bk->trace_rows < bk->trace_cap) {
       TraceRowDev& row = t.trace[bk->trace_rows];
       row.iter = k + 1;
       row.r_primal = r_primal;
@@ -608,7 +644,7 @@ __device__ void gate_logic(Book<T>* bk, const TailArgs<T>& t, double dual_value,
     bk->stop = 1;
   }
   // the confirm report runs only when the gate fires (graph IF node)
-  if (t.use_cond) cudaGraphSetConditional(t.cond, fire ? 1u : 0u);
+  if (t.use_cond && write_trace) cudaGraphSetConditional(t.cond, fire ? 1u : 0u);
 }
 
 // report_elem with mu_i = double(phi_i) / rho precomputed once per row

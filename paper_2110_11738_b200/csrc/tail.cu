@@ -74,7 +74,9 @@ constexpr int kBarStride = 32;
 __constant__ int c_bar_flat = 1;  // 1: one arrival counter (DROTB_BAR_FLAT)
 
 template <class F>
-__device__ __forceinline__ void reduce_barrier(unsigned* bar, unsigned& my_gen, F&& fn) {
+__device__ __forceinline__ void reduce_barrier(unsigned* bar, unsigned& my_gen, F&& fn,
+                                               unsigned long long* stamps = nullptr,
+                                               int64_t it_stamp = 0) {
   __shared__ int s_last;
   __syncthreads();  // this CTA's partials are written (CTA scope)
   if (threadIdx.x == 0) {
@@ -91,6 +93,7 @@ __device__ __forceinline__ void reduce_barrier(unsigned* bar, unsigned& my_gen, 
   }
   __syncthreads();
   if (s_last) {
+    if (stamps && threadIdx.x == 0) timeline_point(stamps, it_stamp, 10, global_ns());
     fn();
     __syncthreads();
     if (threadIdx.x < kBarSub) bar[kBarStride * (1 + threadIdx.x)] = 0u;
@@ -100,6 +103,7 @@ __device__ __forceinline__ void reduce_barrier(unsigned* bar, unsigned& my_gen, 
   } else if (threadIdx.x == 0) {
     while (ld_acquire(bar + 1) == my_gen) {
     }
+    if (stamps) timeline_point(stamps, it_stamp, 13, global_ns());
   }
   ++my_gen;
   __syncthreads();
@@ -155,39 +159,256 @@ __device__ __forceinline__ void store_partials(U (&v)[K], U* part, int off, U* s
 
 // book_load / book_store / patch_pending / gate_fused: gate.cuh
 
+// Counter barrier of the cooperative tail: every CTA arrives with one
+// release-add on the counter of this launch and spins (relaxed loads, no
+// cache invalidation per poll) until all G arrivals are visible, then
+// acquires.  No CTA waits for another to compute anything: after the
+// barrier every CTA reduces the per-CTA partials itself, in the same fixed
+// order, and runs the scalar logic on its own shared-memory copy of the Book
+// (bit-identical everywhere); CTA 0 alone writes the Book and the trace.
+// Counters: bar[kCtr0] / bar[kCtr1] by iteration parity; a launch resets the
+// other parity's counter for the next launch (consecutive tails alternate).
+constexpr int kCtr0 = 768, kCtr1 = 896;
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void count_barrier(unsigned* ctr, unsigned target,
+                                              unsigned long long* stamps, int64_t it_stamp) {
+  __syncthreads();  // this CTA's partials are written (CTA scope)
+  if (threadIdx.x == 0) {
+    red_release_add(ctr, 1u);
+    while (static_cast<int>(ld_relaxed(ctr) - target) < 0) {
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    if (stamps) timeline_point(stamps, it_stamp, 10, global_ns());
+  }
+  __syncthreads();
+}
+
+// Partials are stored value-major -- part[k * Gp + b] for value k of CTA b,
+// Gp = G rounded up to 32 -- so that reading all of them is a few coalesced
+// 128-B requests per value instead of one request per (CTA, value): every
+// CTA reads every partial after a counter barrier (the L2 would otherwise
+// serve ~G^2 * K small requests).
+__device__ __forceinline__ int padded_grid(int G) { return (G + 31) & ~31; }
+
+template <class U, int K>
+__device__ __forceinline__ void store_partials_vm(U (&v)[K], U* part, int Gp, int off, U* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < K; ++k) sh[k * kTW + warp] = v[k];
+  __syncthreads();
+  if (threadIdx.x < K) {
+    U s = U(0);
+#pragma unroll
+    for (int w = 0; w < kTW; ++w) s += sh[threadIdx.x * kTW + w];
+    part[(off + threadIdx.x) * Gp + blockIdx.x] = s;
+  }
+}
+
+// Fixed-order totals of K value-major partials: warp w sums values
+// w, w + kTW, ...: lane l adds CTAs l, l + 32, ... in order, then the warp
+// tree.  out[k] valid in every thread after the call (through sh).
+template <class U, int K>
+__device__ __forceinline__ void all_totals_vm(const U* part, int G, int Gp, int off,
+                                              U (&out)[K], U* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = warp; k < K; k += kTW) {
+    U acc = U(0);
+    for (int b = lane; b < G; b += 32) acc += __ldcg(part + (off + k) * Gp + b);
+    acc = warp_sum(acc);
+    if (lane == 0) sh[k] = acc;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) out[k] = sh[k];
+  __syncthreads();
+}
+
+// dpart values: [0, 8) pending update partials of parity 0, [8, 10) confirm
+// report, [10, 14) fused-gate merge sums, [16, 24) pending partials of parity 1
+constexpr int kDS = kTailDSlots;
+__device__ __forceinline__ int pend_off(int par) { return par ? 16 : 0; }
+
+template <class T>
+__device__ __forceinline__ void book_store_cta0(Book<T>* dst, const Book<T>* src) {
+  constexpr int W = static_cast<int>(sizeof(Book<T>) / 8);
+  __syncthreads();
+  if (blockIdx.x == 0)
+    for (int k = threadIdx.x; k < W; k += blockDim.x)
+      reinterpret_cast<unsigned long long*>(dst)[k] =
+          reinterpret_cast<const unsigned long long*>(src)[k];
+}
+
+// The pending exact dual value / fixed-point residual of the previous
+// iteration (gate.cuh patch_pending), split so that it can run beside the
+// current iteration's gate: snapshot the pending fields, compute, apply.
+struct PendSnap {
+  int valid, use_dx, record;
+  int64_t row, cap;
+  double last_cost, dx;
+};
+template <class T>
+__device__ __forceinline__ PendSnap pend_snap(const Book<T>& b) {
+  return PendSnap{b.pend_valid, b.pend_use_dx, b.record_trace, b.pend_row, b.trace_cap,
+                  b.pend_last_cost, b.pend_dx};
+}
+template <class T>
+__device__ __forceinline__ void pend_compute(const PendSnap& ps, const TailArgs<T>& t,
+                                             const double (&d8)[8], bool write_trace,
+                                             double* out3) {
+  const double dual = d8[0] + d8[4];
+  double fpr = __longlong_as_double(0x7ff8000000000000ULL);
+  if (ps.record) {  // rank-two identity (solver.hpp:443-472)
+    double fp_sq = static_cast<double>(t.n_global) * d8[1] +
+                   static_cast<double>(t.m_global) * d8[5] + 2.0 * d8[2] * d8[6];
+    if (ps.use_dx) fp_sq += ps.dx + 2.0 * (d8[3] + d8[7]);
+    fpr = sqrt(fmax(fp_sq, 0.0));
+  }
+  const double gap = fabs(ps.last_cost - dual);
+  if (write_trace && t.trace && ps.row >= 0 && ps.row < ps.cap) {
+    TraceRowDev& row = t.trace[ps.row];
+    row.gap = gap;
+    row.fixed_point_residual = fpr;
+  }
+  out3[0] = dual;
+  out3[1] = gap;
+  out3[2] = fpr;
+}
+
+constexpr int kLoadsPerLane = 6;  // totals: 6 x 32 = 192 CTAs per load round
+
+// update-phase threads: warps kUW.. (warps 0 and 1 run the scalar logic of
+// barrier 1 meanwhile)
+constexpr int kUW = 2;
+constexpr int kUT = kTT - 32 * kUW;
+
 template <class T>
 __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart,
                                                    double* dpart, unsigned* bar) {
   using V = typename V16<T>::type;
   constexpr int R = 16 / sizeof(T);
+  constexpr int BW = static_cast<int>(sizeof(Book<T>) / 8);
   Book<T>* bk = t.book;
   // the next sweep (a programmatic dependent) may be scheduled now; it waits
   // in griddepcontrol.wait for this grid's completion
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x, Gp = padded_grid(G);
+  const int par = t.tpar & 1;
+  unsigned* ctr = bar + (par ? kCtr1 : kCtr0);
+  if (blockIdx.x == 0 && tid == 0) bar[par ? kCtr0 : kCtr1] = 0u;  // for the next tail
   const int64_t it_stamp = t.stamps ? *reinterpret_cast<volatile int64_t*>(&bk->iter) : 0;
   TAIL_STAMP(2);
   if (*reinterpret_cast<volatile int*>(&bk->stop)) return;
-  __shared__ __align__(16) T red[kTT * R];  // merge partition sums [P][CV][R]
+  __shared__ __align__(16) T red[kTT * R];  // strip merge partition sums [P][CV][R]
   __shared__ Book<T> sbk;
   __shared__ T shT[16 * kTW];
   __shared__ double shD[16 * kTW];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int G = gridDim.x;
+  __shared__ T s_tt[16];
+  __shared__ double s_td[16];
+  __shared__ double s_patch[3];
+  __shared__ int s_gate_ran;
   const int64_t m = t.m, n = t.n;
-  __shared__ unsigned s_gen0;
-  if (tid == 0) s_gen0 = ld_acquire(bar + 1);  // no barrier is in flight at launch
-  __syncthreads();
-  unsigned my_gen = s_gen0;
+  // the Book as this launch found it (CTA 0 of the previous tail or the host
+  // wrote it; nobody writes it before barrier 1)
+  if (tid < BW)
+    reinterpret_cast<unsigned long long*>(&sbk)[tid] =
+        __ldcg(reinterpret_cast<const unsigned long long*>(bk) + tid);
+  const bool fp = bk->record_trace != 0;  // configuration: constant over the solve
+
+  // this CTA's balanced range of [0, m + n): the update of both modes and
+  // the fixed-point merge; update thread ut takes e0 + ut, e0 + ut + kUT, ...
+  const int64_t E = m + n;
+  const int64_t e0 = static_cast<int64_t>(blockIdx.x) * E / G;
+  const int64_t e1 = static_cast<int64_t>(blockIdx.x + 1) * E / G;
+  const int ut = tid - 32 * kUW;
+  const int64_t ef = e0 + ut;
+  const bool has_first = ut >= 0 && ef < e1;
+  // first element: its update inputs are independent of the merge -- load
+  // them now (a / b, p / q, old phi / varphi, old r / s)
+  T f_ab = T(0), f_pq = T(0), f_old = T(0), f_rso = T(0), f_rs = T(0);
+  if (has_first) {
+    if (ef < m) {
+      f_ab = ld_keep(t.a + ef);
+      f_pq = ld_keep(t.p + ef);
+      f_old = ld_keep(t.phi + ef);
+      if (fp) f_rso = ld_keep(t.r_old + ef);
+    } else {
+      const int64_t j = ef - m;
+      f_ab = ld_keep(t.b + j);
+      f_pq = ld_keep(t.q + j);
+      f_old = ld_keep(t.varphi + j);
+      if (fp) f_rso = ld_keep(t.s_old + j);
+    }
+  }
+  // this CTA's fixed slice of the K1 CTA scalars (independent of the merge)
+  T ps[4] = {T(0), T(0), T(0), T(0)};
+  T mx = T(0), bad = T(0);
+  {
+    const int64_t np = t.n_pass_partials;
+    const int64_t k0 = static_cast<int64_t>(blockIdx.x) * np / G;
+    const int64_t k1 = static_cast<int64_t>(blockIdx.x + 1) * np / G;
+    for (int64_t k = k0 + tid; k < k1; k += kTT) {
+      const PassPartial<T> sc = t.pass_partials[k];
+      ps[0] += sc.cost;
+      ps[1] += sc.prev;
+      ps[2] += sc.dual;
+      ps[3] += sc.dx;
+      mx = fmax(mx, sc.max_abs);
+      bad += sc.bad ? T(1) : T(0);
+    }
+  }
 
   // ---- A: merge -----------------------------------------------------------
-  // The (m + n) merged sums as RV-wide vectors (16-B loads): u vectors
-  // [0, nvu), v vectors [nvu, nvu + nvv).  CTA b owns the balanced range
-  // [b*NV/G, (b+1)*NV/G); thread t of a chunk of CV vectors handles vector
-  // t % CV over the strip rows g = t / CV (mod P), 8 loads in flight, and
-  // the P partition sums are combined in a fixed order in shared memory.
-  {
-    T pr[3] = {T(0), T(0), T(0)};
-    double pd[4] = {0, 0, 0, 0};  // sum p a, sum p r, sum q b, sum q s (fused gate)
+  T pr[3] = {T(0), T(0), T(0)};
+  double pd[4] = {0, 0, 0, 0};  // sum p a, sum p r, sum q b, sum q s (fused gate)
+  if (t.fx) {
+    // fixed-point sums (PassArgs::fx): complete after the sweep; one read
+    // (and reset) per index, by the update thread that owns it
+    if (ut >= 0) {
+      for (int64_t e = ef; e < e1; e += kUT) {
+        const bool first = e == ef;
+        if (e < m) {
+          const T pi = first ? f_pq : ld_keep(t.p + e);
+          const T ai = first ? f_ab : ld_keep(t.a + e);
+          const long long qf = __ldcg(t.ufx + e);
+          t.ufx[e] = 0;
+          const T r = static_cast<T>(static_cast<double>(qf) * kFxInv) - pi;
+          st_keep(t.r_new + e, r, 2);
+          if (first) f_rs = r;
+          pr[0] += r;
+          pr[1] += r * r;
+          pd[0] += static_cast<double>(pi) * static_cast<double>(ai);
+          pd[1] += static_cast<double>(pi) * static_cast<double>(r);
+        } else {
+          const int64_t jj = e - m;
+          const T qj = first ? f_pq : ld_keep(t.q + jj);
+          const T bj = first ? f_ab : ld_keep(t.b + jj);
+          const long long qf = __ldcg(t.vfx + jj);
+          t.vfx[jj] = 0;
+          const T sv = static_cast<T>(static_cast<double>(qf) * kFxInv) - qj;
+          st_keep(t.s_new + jj, sv, 2);
+          if (first) f_rs = sv;
+          pr[2] += sv * sv;
+          pd[2] += static_cast<double>(qj) * static_cast<double>(bj);
+          pd[3] += static_cast<double>(qj) * static_cast<double>(sv);
+        }
+      }
+    }
+    TAIL_STAMP(8);
+  } else {
+    // strips: (m + n) merged sums as RV-wide vectors (16-B loads), u vectors
+    // [0, nvu), v vectors [nvu, nvu + nvv); CTA b owns the balanced range
+    // [b*NV/G, (b+1)*NV/G); thread t of a chunk of CV vectors handles vector
+    // t % CV over the strip rows g = t / CV (mod P), 8 loads in flight, and
+    // the P partition sums are combined in a fixed order in shared memory
     const int64_t nvu = (m + R - 1) / R, nvv = (n + R - 1) / R, NV = nvu + nvv;
     const bool vvec = (n % R) == 0;  // v strip rows 16-B aligned
     const int64_t v0 = static_cast<int64_t>(blockIdx.x) * NV / G;
@@ -238,6 +459,7 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
               if (j0 + k < n) acc[k] += base[g * stride + k];
         }
       }
+      if (c0 == v0) TAIL_STAMP(7);
       __syncthreads();
       if (part < P)
 #pragma unroll
@@ -283,22 +505,10 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
         }
       }
     }
-    // this CTA's fixed slice of the K1 CTA scalars
-    const int64_t np = t.n_pass_partials;
-    const int64_t k0 = static_cast<int64_t>(blockIdx.x) * np / G;
-    const int64_t k1 = static_cast<int64_t>(blockIdx.x + 1) * np / G;
-    T ps[4] = {T(0), T(0), T(0), T(0)};
-    T mx = T(0), bad = T(0);
-    for (int64_t k = k0 + tid; k < k1; k += kTT) {
-      const PassPartial<T> sc = t.pass_partials[k];
-      ps[0] += sc.cost;
-      ps[1] += sc.prev;
-      ps[2] += sc.dual;
-      ps[3] += sc.dx;
-      mx = fmax(mx, sc.max_abs);
-      bad += sc.bad ? T(1) : T(0);
-    }
-    // max through a warp/CTA max (fixed order), the rest through the sum tree
+    TAIL_STAMP(8);
+  }
+  TAIL_STAMP(9);
+  {
     mx = warp_max(mx);
     if (lane == 0) shT[warp] = mx;
     __syncthreads();
@@ -307,181 +517,201 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
     for (int w = 0; w < kTW; ++w) cmx = fmax(cmx, shT[w]);
     __syncthreads();
     T v8[8] = {ps[0], ps[1], ps[2], ps[3], bad, pr[0], pr[1], pr[2]};
-    store_partials<T, 8>(v8, cpart, 0, shT);
-    if (t.fused_gate) store_partials<double, 4>(pd, dpart, 10, shD);
-    if (tid == 0) cpart[blockIdx.x * kTSlots + 8] = cmx;
+    store_partials_vm<T, 8>(v8, cpart, Gp, 0, shT);
+    if (t.fused_gate) store_partials_vm<double, 4>(pd, dpart, Gp, 10, shD);
+    if (tid == 0) cpart[8 * Gp + blockIdx.x] = cmx;
   }
   TAIL_STAMP(3);
-  reduce_barrier(bar, my_gen, [&] {
-    // ONE round of loads: the Book words and, per CTA, the 8 T sums, the max,
-    // the previous update's 8 double partials and this merge's 4 (fused gate)
-    constexpr int BW = static_cast<int>(sizeof(Book<T>) / 8);
-    const bool fg = t.fused_gate != 0;
-    unsigned long long bw = tid < BW ? __ldcg(reinterpret_cast<const unsigned long long*>(bk) + tid)
-                                     : 0ull;
-    T acc[8];
-    double dd[12];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) acc[k] = T(0);
-#pragma unroll
-    for (int k = 0; k < 12; ++k) dd[k] = 0.0;
-    T m1 = T(0);
-    for (int b = tid; b < G; b += kTT) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) acc[k] += __ldcg(cpart + b * kTSlots + k);
-      m1 = fmax(m1, __ldcg(cpart + b * kTSlots + 8));
-      if (fg) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) dd[k] += __ldcg(dpart + b * kTSlots + k);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) dd[8 + k] += __ldcg(dpart + b * kTSlots + 10 + k);
-      }
-    }
-    if (tid < BW) reinterpret_cast<unsigned long long*>(&sbk)[tid] = bw;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) acc[k] = warp_sum(acc[k]);
-    m1 = warp_max(m1);
-    if (fg)
-#pragma unroll
-      for (int k = 0; k < 12; ++k) dd[k] = warp_sum(dd[k]);
-    if (lane == 0) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) shT[k * kTW + warp] = acc[k];
-      shT[8 * kTW + warp] = m1;
-#pragma unroll
-      for (int k = 0; k < 12; ++k) shD[k * kTW + warp] = dd[k];
-    }
-    __syncthreads();
-    if (tid == 0) {
-      T s8[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        T sum = T(0);
-#pragma unroll
-        for (int w = 0; w < kTW; ++w) sum += shT[k * kTW + w];
-        s8[k] = sum;
-      }
-      T mxt = T(0);
-#pragma unroll
-      for (int w = 0; w < kTW; ++w) mxt = fmax(mxt, shT[8 * kTW + w]);
-      // {cost, prev, dual, dx, max|t|, sum r, |r|^2, |s|^2} (merge_kernel order)
-      const T tot[8] = {s8[0], s8[1], s8[2], s8[3], mxt, s8[5], s8[6], s8[7]};
-      merge_scalars<T>(&sbk, t, tot, s8[4] > T(0) ? 1 : 0);
-      if (fg) {
-        double d12[12];
-#pragma unroll
-        for (int k = 0; k < 12; ++k) {
-          double sum = 0.0;
-#pragma unroll
-          for (int w = 0; w < kTW; ++w) sum += shD[k * kTW + w];
-          d12[k] = sum;
-        }
-        const double dp8[8] = {d12[0], d12[1], d12[2], d12[3], d12[4], d12[5], d12[6], d12[7]};
-        patch_pending<T>(&sbk, t, dp8);  // the previous iteration's exact dual / trace terms
-        if (!sbk.stop) {
-          const double coef = static_cast<double>(sbk.coef);
-          const double inv_n = 1.0 / static_cast<double>(t.n_global);
-          const double inv_m = 1.0 / static_cast<double>(t.m_global);
-          const double dual_alg = ((d12[8] - 2.0 * d12[9] + coef * sbk.sum_p) * inv_n +
-                                   (d12[10] - 2.0 * d12[11] + coef * sbk.sum_q) * inv_m) /
-                                  static_cast<double>(t.rho);
-          gate_fused<T>(&sbk, t, dual_alg);
-        }
-      }
-    }
-    book_store(bk, &sbk);
-    TAIL_STAMP(4);
-  });
-  if (*reinterpret_cast<volatile int*>(&bk->failed)) return;  // non-finite pass
-  if (!t.fused_gate && *reinterpret_cast<volatile int*>(&bk->stop)) return;
-
-  // ---- B: phi / varphi / a / b + dual-value and fixed-point partials --------
+  // ---- barrier 1: every CTA reduces the merge totals itself ----------------
+  count_barrier(ctr, static_cast<unsigned>(G), t.stamps, it_stamp);
+  const bool fg = t.fused_gate != 0;
   {
-    const T coef = *reinterpret_cast<volatile T*>(&bk->coef);
+    const int po = pend_off(par ^ 1);  // the previous tail's update partials
+    // warp w: values w, w + 8, w + 16 of {9 T: cpart 0..8} and {12 double:
+    // pending 0..7, fused-gate sums 10..13}
+    // all of a warp's loads are issued before any is consumed (a rolled
+    // load-add loop would serialize one L2 round trip per 32 CTAs)
+    for (int b0 = 0; b0 < G; b0 += 32 * kLoadsPerLane) {
+      T tv[3][kLoadsPerLane];
+      double dv[3][kLoadsPerLane];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int k = warp + i * kTW;
+#pragma unroll
+        for (int q = 0; q < kLoadsPerLane; ++q) {
+          const int b = b0 + lane + 32 * q;
+          tv[i][q] = T(0);
+          dv[i][q] = 0.0;
+          if (b < G) {
+            if (k < 9) {
+              tv[i][q] = __ldcg(cpart + k * Gp + b);
+            } else if (k < 21 && fg) {
+              const int kd = k - 9;
+              dv[i][q] = __ldcg(dpart + (kd < 8 ? po + kd : 10 + (kd - 8)) * Gp + b);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int k = warp + i * kTW;
+        if (k < 9) {
+          T acc = T(0);
+#pragma unroll
+          for (int q = 0; q < kLoadsPerLane; ++q)
+            acc = k == 8 ? fmax(acc, tv[i][q]) : acc + tv[i][q];
+          acc = k == 8 ? warp_max(acc) : warp_sum(acc);
+          if (b0 > 0) acc = k == 8 ? fmax(acc, s_tt[k]) : acc + s_tt[k];
+          __syncwarp();
+          if (lane == 0) s_tt[k] = acc;
+        } else if (k < 21 && fg) {
+          double acc = 0.0;
+#pragma unroll
+          for (int q = 0; q < kLoadsPerLane; ++q) acc += dv[i][q];
+          acc = warp_sum(acc);
+          if (b0 > 0) acc += s_td[k - 9];
+          __syncwarp();
+          if (lane == 0) s_td[k - 9] = acc;
+        }
+      }
+    }
+  }
+  TAIL_STAMP(11);
+  __syncthreads();
+  // coef exactly as merge_scalars forms it (solver.hpp:273-277), from the
+  // Book before this iteration's scalar logic touches it
+  const T beta_all = s_tt[5] / static_cast<T>(t.m_global + t.n_global);
+  const T coef = T(2) * beta_all - sbk.alpha;
+  const bool pass_bad = s_tt[4] > T(0);
+  PendSnap snap{};
+  __shared__ int s_pvalid;
+  if (tid == 32) {
+    snap = pend_snap(sbk);
+    s_pvalid = snap.valid;
+  }
+  __syncthreads();
+  // warp 0: recursions + gate; warp 1: the previous iteration's exact dual /
+  // fixed-point patch; warps 2..7: the update (solver.hpp:279-289)
+  if (warp == 0) {
+    if (lane == 0) {
+      // {cost, prev, dual, dx, max|t|, sum r, |r|^2, |s|^2} (merge_kernel order)
+      const T tot[8] = {s_tt[0], s_tt[1], s_tt[2], s_tt[3], s_tt[8], s_tt[5], s_tt[6], s_tt[7]};
+      merge_scalars<T>(&sbk, t, tot, pass_bad ? 1 : 0);
+      int ran = 0;
+      if (fg && !sbk.stop) {
+        const double dcoef = static_cast<double>(sbk.coef);
+        const double dual_alg = ((s_td[8] - 2.0 * s_td[9] + dcoef * sbk.sum_p) * t.inv_n_d +
+                                 (s_td[10] - 2.0 * s_td[11] + dcoef * sbk.sum_q) * t.inv_m_d) /
+                                static_cast<double>(t.rho);
+        gate_fused<T>(&sbk, t, dual_alg, blockIdx.x == 0);
+        sbk.pend_buf = par;
+        ran = 1;
+      }
+      s_gate_ran = ran;
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && fg && snap.valid) {
+      const double d8[8] = {s_td[0], s_td[1], s_td[2], s_td[3], s_td[4], s_td[5], s_td[6], s_td[7]};
+      pend_compute<T>(snap, t, d8, blockIdx.x == 0, s_patch);
+    }
+  } else if (!pass_bad) {
+    // ---- B: phi / varphi / a / b + dual-value and fixed-point partials ----
     const T inv_n = T(1) / static_cast<T>(t.n_global);
     const T inv_m = T(1) / static_cast<T>(t.m_global);
     const double drho = static_cast<double>(t.rho);
-    const bool fp = bk->record_trace != 0;
     double part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const int64_t TT = static_cast<int64_t>(G) * kTT;
-    for (int64_t idx = static_cast<int64_t>(blockIdx.x) * kTT + tid; idx < m + n; idx += TT) {
-      if (idx < m) {
-        const T r = ld_keep_cg(t.r_new + idx);
-        const T ph_old = ld_keep(t.phi + idx);
-        const T ai = ld_keep(t.a + idx);
+    for (int64_t e = ef; e < e1; e += kUT) {
+      const bool first = e == ef && t.fx;
+      if (e < m) {
+        const T r = first ? f_rs : ld_keep_cg(t.r_new + e);
+        const T ph_old = e == ef ? f_old : ld_keep(t.phi + e);
+        const T ai = e == ef ? f_ab : ld_keep(t.a + e);
+        const T pi = e == ef ? f_pq : ld_keep(t.p + e);
         const T ph = (ai - T(2) * r + coef) * inv_n;  // solver.hpp:280-282
-        st_keep(t.phi + idx, ph, 2);
-        st_keep(t.a + idx, ai - r, 2);  // solver.hpp:287
-        part[0] += static_cast<double>(ld_keep(t.p + idx)) * static_cast<double>(ph) / drho;
+        st_keep(t.phi + e, ph, 2);
+        st_keep(t.a + e, ai - r, 2);  // solver.hpp:287
+        part[0] += static_cast<double>(pi) * static_cast<double>(ph) / drho;
         if (fp) {
+          const T ro = e == ef ? f_rso : ld_keep(t.r_old + e);
           const double d = static_cast<double>(ph) - static_cast<double>(ph_old);
           part[1] += d * d;
           part[2] += d;
-          part[3] += d * (static_cast<double>(r) - static_cast<double>(ld_keep(t.r_old + idx)));
+          part[3] += d * (static_cast<double>(r) - static_cast<double>(ro));
         }
       } else {
-        const int64_t j = idx - m;
-        const T s = ld_keep_cg(t.s_new + j);
-        const T vp_old = ld_keep(t.varphi + j);
-        const T bj = ld_keep(t.b + j);
-        const T vp = (bj - T(2) * s + coef) * inv_m;  // solver.hpp:283-285
+        const int64_t j = e - m;
+        const T sv = first ? f_rs : ld_keep_cg(t.s_new + j);
+        const T vp_old = e == ef ? f_old : ld_keep(t.varphi + j);
+        const T bj = e == ef ? f_ab : ld_keep(t.b + j);
+        const T qj = e == ef ? f_pq : ld_keep(t.q + j);
+        const T vp = (bj - T(2) * sv + coef) * inv_m;  // solver.hpp:283-285
         st_keep(t.varphi + j, vp, 2);
-        st_keep(t.b + j, bj - s, 2);  // solver.hpp:288
-        part[4] += static_cast<double>(ld_keep(t.q + j)) * static_cast<double>(vp) / drho;
+        st_keep(t.b + j, bj - sv, 2);  // solver.hpp:288
+        part[4] += static_cast<double>(qj) * static_cast<double>(vp) / drho;
         if (fp) {
+          const T so = e == ef ? f_rso : ld_keep(t.s_old + j);
           const double d = static_cast<double>(vp) - static_cast<double>(vp_old);
           part[5] += d * d;
           part[6] += d;
-          part[7] += d * (static_cast<double>(s) - static_cast<double>(ld_keep(t.s_old + j)));
+          part[7] += d * (static_cast<double>(sv) - static_cast<double>(so));
         }
       }
     }
-    store_partials<double, 8>(part, dpart, 0, shD);
+    // update-warp partial sums of this CTA (fixed order), stored below
+#pragma unroll
+    for (int k = 0; k < 8; ++k) part[k] = warp_sum(part[k]);
+    if (lane == 0)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) shD[k * kTW + warp] = part[k];
   }
-  TAIL_STAMP(5);
-  if (t.fused_gate) {
-    // gate already decided after the merge; the confirm report needs the
-    // updated phi / varphi everywhere and the exact dual value
-    if (!*reinterpret_cast<volatile int*>(&bk->confirm) ||
-        *reinterpret_cast<volatile int*>(&bk->stop) == 1) {
-      TAIL_STAMP(6);
-      return;
+  __syncthreads();
+  if (tid == 0) {
+    if (fg && s_pvalid && !s_gate_ran) {  // gate did not run: the patch stands
+      sbk.dual_value = s_patch[0];
+      sbk.gap = s_patch[1];
+      sbk.fp_residual = s_patch[2];
+      sbk.pend_valid = 0;
+      sbk.pend_row = -1;
     }
-    reduce_barrier(bar, my_gen, [&] {
-      constexpr int BW = static_cast<int>(sizeof(Book<T>) / 8);
-      unsigned long long bw = tid < BW ? __ldcg(reinterpret_cast<const unsigned long long*>(bk) + tid)
-                                       : 0ull;
-      double d8[8];
-      totals<double, 8>(dpart, G, 0, d8, shD);
-      if (tid < BW) reinterpret_cast<unsigned long long*>(&sbk)[tid] = bw;
-      __syncthreads();
-      if (tid == 0) {
-        patch_pending<T>(&sbk, t, d8);
-        gate_recheck<T>(&sbk);  // exact gap before the report
-      }
-      book_store(bk, &sbk);
-    });
-  } else {
-  reduce_barrier(bar, my_gen, [&] {
-    constexpr int BW = static_cast<int>(sizeof(Book<T>) / 8);
-    unsigned long long bw = tid < BW ? __ldcg(reinterpret_cast<const unsigned long long*>(bk) + tid)
-                                     : 0ull;
-    double d8[8];
-    totals<double, 8>(dpart, G, 0, d8, shD);  // (its __syncthreads also publish sbk)
-    if (tid < BW) reinterpret_cast<unsigned long long*>(&sbk)[tid] = bw;
-    __syncthreads();
-    if (tid == 0)
-      gate_logic<T>(&sbk, t, d8[0] + d8[4], d8[1], d8[2], d8[5], d8[6], d8[3] + d8[7]);
-    book_store(bk, &sbk);
-  });
   }
-  if (!*reinterpret_cast<volatile int*>(&bk->confirm) ||
-      *reinterpret_cast<volatile int*>(&bk->stop) == 1)
+  TAIL_STAMP(12);
+  book_store_cta0(bk, &sbk);
+  TAIL_STAMP(4);
+  if (!pass_bad && tid < 8) {  // the update partials of this CTA: warps kUW.. in order
+    double s = 0.0;
+#pragma unroll
+    for (int w = kUW; w < kTW; ++w) s += shD[tid * kTW + w];
+    dpart[(pend_off(par) + tid) * Gp + blockIdx.x] = s;
+  }
+  __syncthreads();
+  TAIL_STAMP(5);
+  if (sbk.failed) return;  // non-finite pass
+  if (fg && (!sbk.confirm || sbk.stop == 1)) {
+    TAIL_STAMP(6);
     return;
+  }
+  // ---- barrier 2 (only when needed): exact dual value / exact gate ----------
+  count_barrier(ctr, 2u * static_cast<unsigned>(G), nullptr, 0);
+  {
+    double d8[8];
+    all_totals_vm<double, 8>(dpart, G, Gp, pend_off(par), d8, shD);
+    if (tid == 0) {
+      if (fg) {
+        patch_pending<T>(&sbk, t, d8, blockIdx.x == 0);
+        gate_recheck<T>(&sbk);  // exact gap before the report
+      } else {
+        gate_logic<T>(&sbk, t, d8[0] + d8[4], d8[1], d8[2], d8[5], d8[6], d8[3] + d8[7],
+                      blockIdx.x == 0);
+      }
+    }
+    book_store_cta0(bk, &sbk);
+  }
+  __syncthreads();
+  if (!sbk.confirm || sbk.stop == 1) return;
 
   // ---- C: exact confirm report (only when the gate fired) ------------------
   {
-    const bool folded = *reinterpret_cast<volatile int*>(&bk->folded) != 0;
+    const bool folded = sbk.folded != 0;
     const double drho = static_cast<double>(t.rho);
     const int64_t ngx = (m + int64_t(kTT) * R - 1) / (int64_t(kTT) * R);
     const int64_t ncs = imin64(n, (2 * static_cast<int64_t>(G) + ngx - 1) / ngx);
@@ -506,15 +736,13 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
             report_elem_mu<T>(xv[k], cv[k], mu[k], nu_j, t.rho, folded, part[0], part[1]);
       }
     }
-    store_partials<double, 2>(part, dpart, 8, shD);
+    store_partials_vm<double, 2>(part, dpart, Gp, 8, shD);
   }
-  reduce_barrier(bar, my_gen, [&] {
-    book_load(&sbk, bk);
-    double d2[2];
-    totals<double, 2>(dpart, G, 8, d2, shD);
-    if (tid == 0) report_decide<T>(&sbk, d2[0], d2[1], 0);
-    book_store(bk, &sbk);
-  });
+  count_barrier(ctr, 3u * static_cast<unsigned>(G), nullptr, 0);
+  double d2[2];
+  all_totals_vm<double, 2>(dpart, G, Gp, 8, d2, shD);
+  if (tid == 0) report_decide<T>(&sbk, d2[0], d2[1], 0);
+  book_store_cta0(bk, &sbk);
 }
 
 }  // namespace
@@ -963,8 +1191,9 @@ __global__ void __launch_bounds__(kTT) tail_finalize_kernel(const TailArgs<T> t,
   __shared__ double shD[16 * kTW];
   Book<T>* bk = t.book;
   if (!*reinterpret_cast<volatile int*>(&bk->pend_valid)) return;
+  const int buf = *reinterpret_cast<volatile int*>(&bk->pend_buf);
   double d8[8];
-  totals<double, 8>(dpart, G, 0, d8, shD);
+  all_totals_vm<double, 8>(dpart, G, padded_grid(G), pend_off(buf), d8, shD);
   if (threadIdx.x == 0) {
     Book<T> lb = *bk;
     patch_pending<T>(&lb, t, d8);

@@ -27,7 +27,7 @@ s.init()
 s.enqueue(8)
 s.prepare(K)
 s.synchronize()
-buf = (C.c_uint64 * 1024)()
+buf = (C.c_uint64 * 2048)()
 _lib.load().drotb_session_tail_stamps(s.handle, buf)  # reset
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(st)
@@ -35,9 +35,12 @@ s.enqueue(K)
 e1.record(st)
 torch.cuda.synchronize()
 _lib.load().drotb_session_tail_stamps(s.handle, buf)
-a = np.array(list(buf), dtype=np.float64).reshape(64, 8, 2)
+a = np.array(list(buf), dtype=np.float64).reshape(64, 16, 2)
 it0 = 8
-names = ["K1 entry", "K1 exit", "tail entry", "merge done", "release", "update done", "tail exit"]
+names = ["K1 entry", "K1 exit", "tail entry", "merge done", "book stored", "update done", "tail exit",
+         "strips loaded", "r/s stored", "K1 slice ld", "barrier passed", "totals loaded",
+         "scalars done", "(unused)"]
+NP = len(names)
 rows = []
 for k in range(it0 + 2, it0 + K - 1):
     sl = a[k & 63]
@@ -45,20 +48,24 @@ for k in range(it0 + 2, it0 + K - 1):
     nxt = a[(k + 1) & 63][0, 0]
     if base == 2 ** 64 - 1 or nxt == 2 ** 64 - 1:
         continue
-    rows.append([(sl[p, 0] - base) / 1e3 for p in range(7)] +
-                [(sl[p, 1] - base) / 1e3 for p in range(7)] + [(nxt - base) / 1e3])
+    rows.append([(sl[p, 0] - base) / 1e3 for p in range(NP)] +
+                [(sl[p, 1] - base) / 1e3 for p in range(NP)] + [(nxt - base) / 1e3])
 r = np.array(rows)
 mean = r.mean(axis=0)
 print(f"{m}x{m} {np.dtype(dt).name}: {len(r)} iterations, graph-timed "
       f"{e0.elapsed_time(e1) * 1e3 / K:.1f} us/iter; mean us after the first K1 CTA entry:")
-for p, nm in enumerate(names):
-    print(f"  {nm:12s} min {mean[p]:8.1f}  max {mean[7 + p]:8.1f}")
-print(f"  next K1 entry    {mean[14]:8.1f}")
-print(f"  gaps: K1 last exit -> tail first entry {mean[2] - mean[8]:.1f} us; "
-      f"tail last exit -> next K1 entry {mean[14] - mean[13]:.1f} us; "
-      f"tail span {mean[13] - mean[2]:.1f} us; K1 span {mean[8] - mean[0]:.1f} us")
+order = [0, 1, 2, 7, 8, 9, 3, 10, 11, 12, 4, 5, 6]
+for p in order:
+    if mean[p] > 1e9:  # point not recorded
+        continue
+    print(f"  {names[p]:14s} min {mean[p]:8.1f}  max {mean[NP + p]:8.1f}")
+nx = mean[2 * NP]
+print(f"  next K1 entry      {nx:8.1f}")
+print(f"  gaps: K1 last exit -> tail first entry {mean[2] - mean[NP + 1]:.1f} us; "
+      f"tail last exit -> next K1 entry {nx - mean[NP + 6]:.1f} us; "
+      f"tail span {mean[NP + 6] - mean[2]:.1f} us; K1 span {mean[NP + 1] - mean[0]:.1f} us")
 for k in (0, 1):  # fold / skip iterations separately
     sub = r[k::2]
-    print(f"  parity {k}: K1 span {np.mean(sub[:, 8] - sub[:, 0]):.1f} us, "
-          f"iteration {np.mean(sub[:, 14]):.1f} us")
+    print(f"  parity {k}: K1 span {np.mean(sub[:, NP + 1] - sub[:, 0]):.1f} us, "
+          f"iteration {np.mean(sub[:, 2 * NP]):.1f} us")
 s.close()
