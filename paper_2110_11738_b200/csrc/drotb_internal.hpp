@@ -77,6 +77,7 @@ struct PassArgs {
   int32_t fx;
   int32_t pad_fx;
   int32_t pdl;          // launch as a programmatic dependent (after the coop tail)
+  int32_t trigger;      // a programmatic dependent (the coop tail) follows: trigger early
   int32_t l2hint;       // 1: stream X / C with an L2 evict_first policy (sweep.cuh)
   int32_t pad_l2;
 };
@@ -186,6 +187,8 @@ struct TailArgs {
   int32_t fx;
   int32_t pad_fx;
   double inv_n_d, inv_m_d;     // 1 / double(n_global), 1 / double(m_global)
+  int32_t pdl;                 // tail launched as a programmatic dependent of the sweep
+  int32_t pad_pdl;
 };
 
 // Cooperative per-iteration tail (tail.cu): merge + recursions + update +

@@ -46,15 +46,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_ASYNC_MINB)
   constexpr int ROWS_W = 32 * R;
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   __shared__ PassAcc<T> wacc[kWarpsPerCta];
-  // programmatic dependent launch: the CTAs may be scheduled while the
-  // preceding tail kernel still runs; wait for its completion and memory
-  // before touching any data (no-op for an ordinary launch)
   const unsigned long long t_entry = a.stamps ? global_ns() : 0ull;
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (a.stop != nullptr && *reinterpret_cast<const volatile int*>(a.stop)) return;
-  const int64_t it_stamp = a.stamps ? *reinterpret_cast<const volatile int64_t*>(a.iter) : 0;
-  if (a.stamps && threadIdx.x == 0) timeline_point(a.stamps, it_stamp, 0, t_entry);
-
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr size_t ring_v = static_cast<size_t>(kAsyncS) * 2 * kAsyncG * 32;  // V per warp
   V* ring = reinterpret_cast<V*>(dyn_smem) + warp * ring_v;
@@ -68,6 +60,22 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_ASYNC_MINB)
   const int64_t c1 = imin64(a.n, c0 + a.tc);
   const int64_t nv = a.m - row0;
   const int nvalid = nv <= 0 ? 0 : (nv >= R ? R : static_cast<int>(nv));
+  // programmatic dependent launch (a.pdl): the CTAs may be scheduled while
+  // the preceding tail still runs.  X and C do not depend on it, so the
+  // first ring stages are issued first; phi / varphi / the stop flag are
+  // read only after griddepcontrol.wait (the tail's completion and memory)
+  if (a.pdl) ring_prime<T, MODE>(a, c0, c1, row0, nvalid > 0, ring, lane);
+  // the tail (a programmatic dependent of this sweep, a.trigger) may be
+  // scheduled once every CTA of this grid has started: it fits beside three
+  // sweep CTAs per SM and waits in its own griddepcontrol.wait
+  if (a.trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (a.stop != nullptr && *reinterpret_cast<const volatile int*>(a.stop)) {
+    cp_async_wait<0>();
+    return;
+  }
+  const int64_t it_stamp = a.stamps ? *reinterpret_cast<const volatile int64_t*>(a.iter) : 0;
+  if (a.stamps && threadIdx.x == 0) timeline_point(a.stamps, it_stamp, 0, t_entry);
 
   T ph[R], u[R];
   if (nvalid > 0) {
@@ -79,12 +87,22 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_ASYNC_MINB)
 #pragma unroll
   for (int t = 0; t < R; ++t) u[t] = T(0);
   PassAcc<T> acc{T(0), T(0), T(0), T(0), T(0), false};
-  if (__all_sync(0xffffffffu, nvalid == R))
-    pass_tile_async<T, MODE, DUAL, DX, false>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc, wbuf,
-                                              ring, lane);
-  else
-    pass_tile_async<T, MODE, DUAL, DX, true>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc, wbuf,
-                                             ring, lane);
+  const bool full = __all_sync(0xffffffffu, nvalid == R);
+  if (a.pdl) {
+    if (full)
+      pass_tile_async<T, MODE, DUAL, DX, false, true>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc,
+                                                      wbuf, ring, lane);
+    else
+      pass_tile_async<T, MODE, DUAL, DX, true, true>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc,
+                                                     wbuf, ring, lane);
+  } else {
+    if (full)
+      pass_tile_async<T, MODE, DUAL, DX, false>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc, wbuf,
+                                                ring, lane);
+    else
+      pass_tile_async<T, MODE, DUAL, DX, true>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc, wbuf,
+                                               ring, lane);
+  }
   if (a.fx) {
 #pragma unroll
     for (int t = 0; t < R; ++t)

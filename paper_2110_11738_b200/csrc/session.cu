@@ -90,9 +90,16 @@ int Session<T>::create(int64_t m_, int64_t n_, const drotb_config& c, bool engin
 template <class T>
 int Session<T>::setup_coop_tail() {
   if (const char* e = std::getenv("DROTB_TAIL_GATE")) fused_gate = e[0] != 'e';
-  // PDL for K1 after the tail: no gain in graphs (186 vs 186 us/iteration
-  // at 10k^2) and it inflates the event-timed sweep, so opt-in
+  // K1 as a programmatic dependent of the tail: its CTAs issue their first
+  // X / C ring stages while the tail finishes (DROTB_PDL=0 disables)
+  pdl_ok = true;
   if (const char* e = std::getenv("DROTB_PDL")) pdl_ok = e[0] == '1';
+  // the tail as a programmatic dependent of the sweep (opt-in, DROTB_TAIL_PDL=1;
+  // probed below: a cooperative launch must accept the attribute).  Measured
+  // slower: 180.1 vs 177.0 us per iteration at 10k^2 fp32, 24.3 vs 23.0 at
+  // 1000^2 fp64 (r2 timeline) -- tail CTAs parked beside the last sweep wave
+  tail_pdl = false;
+  if (const char* e = std::getenv("DROTB_TAIL_PDL")) tail_pdl = e[0] == '1';
   tgrid = tail_grid<T>(device);
   if (tgrid <= 0) return 0;
   const size_t gp = static_cast<size_t>((tgrid + 31) / 32 * 32);  // value-major partials (tail.cu)
@@ -124,23 +131,31 @@ int Session<T>::setup_coop_tail() {
   coop = true;
   // can a cooperative launch be captured into a graph here?  (probe on a
   // private stream; the captured launch is never executed)
+  // (with the programmatic attribute first; without it if that fails)
   coop_graphs = false;
   cudaStream_t ps = nullptr;
   if (cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking) == cudaSuccess) {
-    cudaGraph_t gph = nullptr;
-    if (cudaStreamBeginCapture(ps, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
-      TailArgs<T> ta = tail_args(0, kFold, true, true);
-      const cudaError_t le = launch_tail<T>(ta, tcpart, tdpart, tbar, tgrid, ps);
-      count_launch(-1);
-      const cudaError_t ce = cudaStreamEndCapture(ps, &gph);
-      if (le == cudaSuccess && ce == cudaSuccess && gph) {
-        cudaGraphExec_t ex = nullptr;
-        if (cudaGraphInstantiate(&ex, gph, 0) == cudaSuccess) {
-          coop_graphs = true;
-          cudaGraphExecDestroy(ex);
-        }
+    for (int attempt = 0; attempt < 2 && !coop_graphs; ++attempt) {
+      if (attempt == 1) {
+        if (!tail_pdl) break;
+        tail_pdl = false;
       }
-      if (gph) cudaGraphDestroy(gph);
+      cudaGraph_t gph = nullptr;
+      if (cudaStreamBeginCapture(ps, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+        TailArgs<T> ta = tail_args(0, kFold, true, true);
+        const cudaError_t le = launch_tail<T>(ta, tcpart, tdpart, tbar, tgrid, ps);
+        count_launch(-1);
+        const cudaError_t ce = cudaStreamEndCapture(ps, &gph);
+        if (le == cudaSuccess && ce == cudaSuccess && gph) {
+          cudaGraphExec_t ex = nullptr;
+          if (cudaGraphInstantiate(&ex, gph, 0) == cudaSuccess) {
+            coop_graphs = true;
+            cudaGraphExecDestroy(ex);
+          }
+        }
+        if (gph) cudaGraphDestroy(gph);
+      }
+      (void)cudaGetLastError();
     }
     cudaStreamDestroy(ps);
   }
@@ -509,6 +524,7 @@ PassArgs<T> Session<T>::pass_args() {
   pa.fx = fx ? 1 : 0;
   pa.pad_fx = 0;
   pa.pdl = (coop && pdl_ok) ? 1 : 0;
+  pa.trigger = (coop && tail_pdl && !exact && !sharded) ? 1 : 0;
   pa.l2hint = l2hint;
   pa.pad_l2 = 0;
   return pa;
@@ -568,6 +584,7 @@ TailArgs<T> Session<T>::tail_args(int64_t k, int mode, bool folded_after, bool s
   t.ufx = ufx;
   t.vfx = vfx;
   t.fx = fx ? 1 : 0;
+  t.pdl = (coop && tail_pdl && !exact && !sharded) ? 1 : 0;
   t.inv_n_d = 1.0 / static_cast<double>(n_global);
   t.inv_m_d = 1.0 / static_cast<double>(m_global);
   return t;
@@ -607,7 +624,14 @@ int Session<T>::enqueue_iteration(cudaEvent_t pass_begin, cudaEvent_t pass_end, 
       }();
       if (delay_us > 0) launch_spin(static_cast<unsigned long long>(delay_us) * 1000ull, stream);
     }
-    CUDA_TRY(launch_tail<T>(ta, tcpart, tdpart, tbar, tgrid, stream));
+    cudaError_t le = launch_tail<T>(ta, tcpart, tdpart, tbar, tgrid, stream);
+    if (le != cudaSuccess && ta.pdl) {  // no programmatic cooperative launch here
+      (void)cudaGetLastError();
+      tail_pdl = false;
+      ta.pdl = 0;
+      le = launch_tail<T>(ta, tcpart, tdpart, tbar, tgrid, stream);
+    }
+    CUDA_TRY(le);
     h_iter = k + 1;
     h_folded = folded_after;
     return 0;

@@ -133,7 +133,7 @@ struct Session {
   int32_t* dint = nullptr;
 
   // cooperative tail kernel (fast order, one GPU; tail.cu)
-  bool coop = false, coop_graphs = false, fused_gate = true, pdl_ok = false;
+  bool coop = false, coop_graphs = false, fused_gate = true, pdl_ok = false, tail_pdl = false;
   // L2 policies (sweep.cuh): bit 0 evict_first on the streamed X / C reads
   // (measured slower: off), bit 1 evict_last on the row / column strips K1
   // leaves for the tail (default: +2 % per iteration at 10k^2, r1n)

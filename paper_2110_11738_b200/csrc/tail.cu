@@ -299,6 +299,9 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
   // the next sweep (a programmatic dependent) may be scheduled now; it waits
   // in griddepcontrol.wait for this grid's completion
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // launched as a programmatic dependent of the sweep (t.pdl): wait for its
+  // completion and memory before touching anything (no-op otherwise)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x, Gp = padded_grid(G);
   const int par = t.tpar & 1;
@@ -1243,11 +1246,13 @@ cudaError_t launch_tail(const TailArgs<T>& t, T* cpart, double* dpart, unsigned*
   cfg.blockDim = dim3(kTT);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = t.pdl ? 2 : 1;  // t.pdl: a programmatic dependent of the sweep
   count_launch();
   return cudaLaunchKernelEx(&cfg, tail_kernel<T>, t, cpart, dpart, bar);
 }
