@@ -300,6 +300,10 @@ int drotb_sinkhorn_f64(const double* C, int64_t m, int64_t n, const double* p, c
                        int32_t exact_report, double* plan, double* mu, double* nu,
                        drotb_report* report, drotb_trace_row* trace, int64_t trace_cap,
                        int64_t* trace_len, int64_t* iterations, int32_t* status, double* wall);
+/* Device time (ms, CUDA events) of the iteration loop of this host thread's
+ * last drotb_sinkhorn_* call -- the batches of sweeps, updates and checks,
+ * without the uploads, the kernel build and the final plan (B200 extension). */
+double drotb_sinkhorn_last_loop_ms(void);
 
 /* ---- problem generation (probgen.hpp:131-170, host, bit-identical) ------ *
  * Writes C (m*n column-major, normalized to max 1), p (m), q (n) in double.

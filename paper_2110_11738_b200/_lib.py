@@ -103,6 +103,7 @@ SIGNATURES = {
     "drotb_sinkhorn_f64": (C.c_int, [vp, i64, i64, vp, vp, f64, f64, i64, i64, i32, vp, vp, vp,
                                      P(drotb_report), vp, i64, P(i64), P(i64), P(i32),
                                      P(f64)]),
+    "drotb_sinkhorn_last_loop_ms": (f64, []),
     "drotb_gen_gaussian": (C.c_int, [i64, i64, f64, u64, i32, vp, vp, vp]),
     "drotb_gen_gaussian_f32": (C.c_int, [i64, i64, f64, u64, vp]),
     "drotb_counter_uniform": (C.c_int, [u64, i64, f64, f64, vp]),

@@ -39,8 +39,31 @@ constexpr int kVBlockRows = 64;  // reference block_rows of the v strips
 // fixed-point row / column sums (PassArgs::fx): value = integer * 2^-46,
 // |sum| < 2^17; resolution 1.4e-14 per partial (fp32 sums of O(1e-5..1)
 // entries need ~1e-12 absolute)
-constexpr double kFxScale = 70368744177664.0;       // 2^46
-constexpr double kFxInv = 1.4210854715202004e-14;   // 2^-46
+constexpr double kFxScale = 0x1p46;
+constexpr double kFxInv = 0x1p-46;
+constexpr double kFxLoScale = 0x1p86;  // fp64 remainder word
+constexpr double kFxLoInv = 0x1p-86;
+
+// Exact accumulators (one-GPU cooperative tail): every scalar sum of an
+// iteration is accumulated as a pair of 64-bit integers -- hi =
+// round(x * 2^42), lo = round((x - hi * 2^-42) * 2^82) -- with integer
+// atomics, so the totals are exact sums of the rounded terms: independent of
+// the order, the grid and the number of GPUs.  Valid for |sum| < 2^20 (every
+// per-iteration sum of a solve from X0 = p q': mass, costs and residuals are
+// O(1)); resolution 2^-82.
+constexpr double kHiScale = 0x1p42;
+constexpr double kHiInv = 0x1p-42;
+constexpr double kLoScale = 0x1p82;
+constexpr double kLoInv = 0x1p-82;
+// accumulator words per parity: [0, 22) A: 11 sums of the sweep + merge
+// {cost, prev, dual, dx, sum r, |r|^2, |s|^2, sum p a, sum p r, sum q b,
+// sum q s}, [22] max |t| bits, [23] non-finite count; [24, 40) P: the 8
+// update sums; [40, 44) R: the 2 confirm-report sums
+enum XAcc : int {
+  kXaCost = 0, kXaPrev = 1, kXaDual = 2, kXaDx = 3, kXaSumR = 4, kXaR2 = 5, kXaS2 = 6,
+  kXaPA = 7, kXaPR = 8, kXaQB = 9, kXaQS = 10, kXaMax = 22, kXaBad = 23, kXaP = 24, kXaR = 40,
+  kXaWords = 64
+};
 
 constexpr int kStampSlots = 64;
 constexpr int kStampPts = 16;
@@ -76,6 +99,7 @@ struct PassArgs {
   long long* vfx;
   int32_t fx;
   int32_t pad_fx;
+  long long* xacc;      // exact accumulators of this iteration (kXaWords), or null: partials
   int32_t pdl;          // launch as a programmatic dependent (after the coop tail)
   int32_t trigger;      // a programmatic dependent (the coop tail) follows: trigger early
   int32_t l2hint;       // 1: stream X / C with an L2 evict_first policy (sweep.cuh)
@@ -187,6 +211,7 @@ struct TailArgs {
   int32_t fx;
   int32_t pad_fx;
   double inv_n_d, inv_m_d;     // 1 / double(n_global), 1 / double(m_global)
+  long long* xacc;             // exact accumulators, 2 parities x kXaWords
   int32_t pdl;                 // tail launched as a programmatic dependent of the sweep
   int32_t pad_pdl;
 };

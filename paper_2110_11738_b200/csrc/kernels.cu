@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_ASYNC_MINB)
   if (a.fx) {
 #pragma unroll
     for (int t = 0; t < R; ++t)
-      if (t < nvalid) red_add_fx(a.ufx + row0 + t, static_cast<double>(u[t]));
+      if (t < nvalid) red_fx<T>(a.ufx, row0 + t, a.ld, u[t]);
   } else if (nvalid > 0) {
     st_keep(reinterpret_cast<V*>(a.ustrip + gc * a.ld + row0), pack4(u), a.l2hint);
   }
@@ -133,7 +133,19 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_ASYNC_MINB)
       out.max_abs = fmax(out.max_abs, wacc[w].mx);
       out.bad |= wacc[w].bad ? 1 : 0;
     }
-    st_partial_keep(a.partials + static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x, out);
+    if (a.xacc) {  // exact accumulators (the per-CTA sums rounded, then summed exactly)
+      red_hilo(a.xacc + 2 * kXaCost, to_hilo(static_cast<double>(out.cost)));
+      red_hilo(a.xacc + 2 * kXaPrev, to_hilo(static_cast<double>(out.prev)));
+      red_hilo(a.xacc + 2 * kXaDual, to_hilo(static_cast<double>(out.dual)));
+      red_hilo(a.xacc + 2 * kXaDx, to_hilo(static_cast<double>(out.dx)));
+      atomicMax(reinterpret_cast<unsigned long long*>(a.xacc + kXaMax),
+                static_cast<unsigned long long>(
+                    __double_as_longlong(static_cast<double>(out.max_abs))));
+      if (out.bad) red_add_u64(a.xacc + kXaBad, 1);
+    } else {
+      st_partial_keep(a.partials + static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x,
+                      out);
+    }
     if (a.stamps) timeline_point(a.stamps, it_stamp, 1, global_ns());
   }
 }

@@ -11,9 +11,10 @@ void Session<T>::release() {
   void* bufs[] = {X, C, Xout, phi, varphi, a, b, rb[0], rb[1], sb[0], sb[1],
                   p, q, u, v, ustrip, vstrip, tscr, partials, tiles, dscr,
                   terms, book, trace, vflags, pack, pmax, dpack, dint,
-                  tcpart, tdpart, tbar, tstamps, ufx, vfx};
+                  tcpart, tdpart, tbar, tstamps, ufx, vfx, xacc};
   tstamps = nullptr;
   ufx = vfx = nullptr;
+  xacc = nullptr;
   fx_ok = fx = false;
   tcpart = nullptr;
   tdpart = nullptr;
@@ -115,15 +116,19 @@ int Session<T>::setup_coop_tail() {
       CUDA_TRY(cudaMemcpy(tstamps, init.data(), sizeof(unsigned long long) * kStampWords,
                           cudaMemcpyHostToDevice));
     }
-  // fixed-point sums: fp32, one GPU (the shard tail merges strips and
-  // exchanges them); DROTB_FX=0 disables
-  if (std::is_same<T, float>::value && !sharded) {
+  if (!sharded) {
+    // exact accumulators of the one-GPU tail (every scalar sum)
+    RC_TRY(dev_alloc(&xacc, 2 * static_cast<size_t>(kXaWords)));
+    CUDA_TRY(cudaMemsetAsync(xacc, 0, sizeof(long long) * 2 * kXaWords, stream));
+    // fixed-point row / column sums (one word per sum in fp32, a hi / lo
+    // pair in fp64); the shard tail merges strips.  DROTB_FX=0 disables
     const char* e = std::getenv("DROTB_FX");
     if (!(e && e[0] == '0')) {
-      RC_TRY(dev_alloc(&ufx, static_cast<size_t>(ld)));
-      RC_TRY(dev_alloc(&vfx, static_cast<size_t>(n)));
-      CUDA_TRY(cudaMemsetAsync(ufx, 0, sizeof(long long) * ld, stream));
-      CUDA_TRY(cudaMemsetAsync(vfx, 0, sizeof(long long) * n, stream));
+      const size_t w = sizeof(T) == 4 ? 1 : 2;
+      RC_TRY(dev_alloc(&ufx, w * static_cast<size_t>(ld)));
+      RC_TRY(dev_alloc(&vfx, w * static_cast<size_t>(n)));
+      CUDA_TRY(cudaMemsetAsync(ufx, 0, sizeof(long long) * w * ld, stream));
+      CUDA_TRY(cudaMemsetAsync(vfx, 0, sizeof(long long) * w * n, stream));
       fx_ok = true;
     }
   }
@@ -395,9 +400,11 @@ int Session<T>::init(const T* x0, bool x0_is_device) {
     CUDA_TRY(cudaMemsetAsync(xbuf, 0, kXSetupFlagOff, stream));
   }
   if (tbar) CUDA_TRY(cudaMemsetAsync(tbar, 0, 1024 * sizeof(unsigned), stream));  // tail counters
+  if (xacc) CUDA_TRY(cudaMemsetAsync(xacc, 0, sizeof(long long) * 2 * kXaWords, stream));
   if (fx_ok) {  // X0 = p q' bounds every row / column sum by 1; a warm start has no bound
-    CUDA_TRY(cudaMemsetAsync(ufx, 0, sizeof(long long) * ld, stream));
-    CUDA_TRY(cudaMemsetAsync(vfx, 0, sizeof(long long) * n, stream));
+    const size_t w = sizeof(T) == 4 ? 1 : 2;
+    CUDA_TRY(cudaMemsetAsync(ufx, 0, sizeof(long long) * w * ld, stream));
+    CUDA_TRY(cudaMemsetAsync(vfx, 0, sizeof(long long) * w * n, stream));
     const bool want = x0 == nullptr;
     if (want != fx) drop_graphs();
     fx = want;
@@ -501,7 +508,7 @@ int Session<T>::init(const T* x0, bool x0_is_device) {
 
 
 template <class T>
-PassArgs<T> Session<T>::pass_args() {
+PassArgs<T> Session<T>::pass_args(int64_t k) {
   PassArgs<T> pa;
   pa.xy = X;
   pa.cost = C;
@@ -523,6 +530,8 @@ PassArgs<T> Session<T>::pass_args() {
   pa.vfx = vfx;
   pa.fx = fx ? 1 : 0;
   pa.pad_fx = 0;
+  // the one-GPU cooperative tail takes the sweep's scalars as exact sums
+  pa.xacc = (k >= 0 && coop && !exact && !sharded && xacc) ? xacc + (k & 1) * kXaWords : nullptr;
   pa.pdl = (coop && pdl_ok) ? 1 : 0;
   pa.trigger = (coop && tail_pdl && !exact && !sharded) ? 1 : 0;
   pa.l2hint = l2hint;
@@ -585,6 +594,7 @@ TailArgs<T> Session<T>::tail_args(int64_t k, int mode, bool folded_after, bool s
   t.vfx = vfx;
   t.fx = fx ? 1 : 0;
   t.pdl = (coop && tail_pdl && !exact && !sharded) ? 1 : 0;
+  t.xacc = xacc;
   t.inv_n_d = 1.0 / static_cast<double>(n_global);
   t.inv_m_d = 1.0 / static_cast<double>(m_global);
   return t;
@@ -600,7 +610,7 @@ int Session<T>::enqueue_iteration(cudaEvent_t pass_begin, cudaEvent_t pass_end, 
   bool folded_after;
   RC_TRY(pass_mode(k, h_folded, &mode, &folded_after));
   if (mode_out) *mode_out = mode;
-  PassArgs<T> pa = pass_args();
+  PassArgs<T> pa = pass_args(k);
   if (exact) launch_tile_chains<T>(pa, mode, want_dual, want_dx, bs, tiles, stream);
   // while capturing, external records become event nodes of the graph
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
@@ -1050,8 +1060,8 @@ template int Session<float>::resolve_rho();
 template int Session<double>::resolve_rho();
 template int Session<float>::init(const float* x0, bool x0_is_device);
 template int Session<double>::init(const double* x0, bool x0_is_device);
-template PassArgs<float> Session<float>::pass_args();
-template PassArgs<double> Session<double>::pass_args();
+template PassArgs<float> Session<float>::pass_args(int64_t);
+template PassArgs<double> Session<double>::pass_args(int64_t);
 template TailArgs<float> Session<float>::tail_args(int64_t k, int mode, bool folded_after, bool solver);
 template TailArgs<double> Session<double>::tail_args(int64_t k, int mode, bool folded_after, bool solver);
 template int Session<float>::enqueue_iteration(cudaEvent_t pass_begin, cudaEvent_t pass_end, int* mode_out, unsigned long long* cond_out, TailArgs<float>* report_args);

@@ -148,6 +148,7 @@ struct Session {
   // for warm starts, whose row sums have no a-priori bound)
   long long *ufx = nullptr, *vfx = nullptr;
   bool fx_ok = false, fx = false;
+  long long* xacc = nullptr;  // exact accumulators of the one-GPU tail (2 x kXaWords)
 
   std::vector<T> hp, hq;
   T rho = T(0);
@@ -244,7 +245,7 @@ struct Session {
     return 0;
   }
 
-  PassArgs<T> pass_args();
+  PassArgs<T> pass_args(int64_t k = -1);
 
   TailArgs<T> tail_args(int64_t k, int mode, bool folded_after, bool solver);
 

@@ -15,6 +15,7 @@ int Session<T>::load_state(const T* xy, int32_t folded, const T* rs, const T* cs
     drop_graphs();
     fx = false;
   }
+  if (xacc) CUDA_TRY(cudaMemsetAsync(xacc, 0, sizeof(long long) * 2 * kXaWords, stream));
   RC_TRY(upload_matrix(X, xy, false));
   CUDA_TRY(cudaMemcpyAsync(phi, rs, sizeof(T) * m, cudaMemcpyHostToDevice, stream));
   CUDA_TRY(cudaMemcpyAsync(varphi, cs, sizeof(T) * n, cudaMemcpyHostToDevice, stream));

@@ -39,6 +39,14 @@
 
 namespace drotb {
 
+// device time of the last Sinkhorn iteration loop on this host thread
+// (CUDA events around the batches; drotb_sinkhorn_last_loop_ms)
+double& sinkhorn_loop_ms() {
+  static thread_local double ms = 0.0;
+  return ms;
+}
+
+
 namespace {
 
 constexpr int kSkW = 8;              // warps per CTA
@@ -360,8 +368,25 @@ int sinkhorn_t(const T* C, int64_t m, int64_t n, const T* p, const T* q, T eta, 
   int64_t launches = 1;
   int64_t checks = 0;
   int32_t hflags[4] = {0, 0, 0, 0};
-  // batches of check_every iterations; the stop flag is read once per batch
-  int64_t k = 0;
+  // batches of check_every iterations; the host reads a batch's stop flags
+  // one batch behind (the next batch is already queued: every kernel returns
+  // at once after a stop), so the device never idles on the poll
+  int32_t* hpin = nullptr;
+  CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&hpin), 8 * sizeof(int32_t)));
+  std::unique_ptr<int32_t, decltype(&cudaFreeHost)> hold_pin(hpin, &cudaFreeHost);
+  cudaEvent_t evb[2] = {nullptr, nullptr}, lt[2] = {nullptr, nullptr};
+  for (auto* e : {&evb[0], &evb[1]}) CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  for (auto* e : {&lt[0], &lt[1]}) CUDA_TRY(cudaEventCreate(e));
+  struct EvHold {
+    cudaEvent_t* e;
+    int k;
+    ~EvHold() {
+      for (int i = 0; i < k; ++i)
+        if (e[i]) cudaEventDestroy(e[i]);
+    }
+  } hold_evb{evb, 2}, hold_lt{lt, 2};
+  CUDA_TRY(cudaEventRecord(lt[0], st));
+  int64_t k = 0, batch = 0;
   for (; k < max_iters;) {
     const int64_t kb = std::min(max_iters, (k / check_every + 1) * check_every);
     for (; k < kb; ++k) {
@@ -376,11 +401,26 @@ int sinkhorn_t(const T* C, int64_t m, int64_t n, const T* p, const T* q, T eta, 
     sk_check<T><<<static_cast<unsigned>(check_blocks), 256, 0, st>>>(s, k - 1, checks, tol, ticket);
     launches += 2;
     ++checks;
-    CUDA_TRY(cudaMemcpyAsync(hflags, s.flags, sizeof(hflags), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    if (hflags[0] || hflags[1]) break;
+    const int slot = static_cast<int>(batch & 1);
+    CUDA_TRY(cudaMemcpyAsync(hpin + 4 * slot, s.flags, 4 * sizeof(int32_t),
+                             cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaEventRecord(evb[slot], st));
+    if (batch >= 1) {
+      CUDA_TRY(cudaEventSynchronize(evb[slot ^ 1]));
+      const int32_t* f = hpin + 4 * (slot ^ 1);
+      if (f[0] || f[1]) break;
+    }
+    ++batch;
   }
+  CUDA_TRY(cudaEventRecord(lt[1], st));
+  CUDA_TRY(cudaStreamSynchronize(st));
   CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpy(hflags, s.flags, sizeof(hflags), cudaMemcpyDeviceToHost));
+  {
+    float lms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&lms, lt[0], lt[1]));
+    sinkhorn_loop_ms() = static_cast<double>(lms);
+  }
   int64_t fail_iter = 0;
   CUDA_TRY(cudaMemcpy(&fail_iter, s.fail_iter, sizeof(fail_iter), cudaMemcpyDeviceToHost));
   const bool failed = hflags[1] != 0, converged = hflags[2] != 0;
@@ -393,7 +433,8 @@ int sinkhorn_t(const T* C, int64_t m, int64_t n, const T* p, const T* q, T eta, 
   {
     // a failed run records the checks before the failing iteration (a
     // non-finite err returns before its row is pushed, reference.hpp:274-276)
-    const int64_t lim = failed ? iters : big;
+    // (batches queued behind a stop ran no check: rows end at the stop)
+    const int64_t lim = failed || converged ? iters : big;
     for (int64_t c = 0; c < checks; ++c) {
       const int64_t it = std::min(max_iters, (c + 1) * check_every);
       if (failed ? it >= lim : it > lim) break;
@@ -508,5 +549,7 @@ int drotb_sinkhorn_f64(const double* C, int64_t m, int64_t n, const double* p, c
                                    plan, mu, nu, report, trace, trace_cap, trace_len, iterations,
                                    status, wall);
 }
+
+double drotb_sinkhorn_last_loop_ms(void) { return drotb::sinkhorn_loop_ms(); }
 
 }  // extern "C"

@@ -297,9 +297,50 @@ __device__ __forceinline__ void compute_col(const PassArgs<T>& a, const T (&x)[1
   *reinterpret_cast<V*>(wbuf + (c * 32 + (lane ^ (c & 7))) * R) = pack4(xp);
 }
 
+// exact accumulation (drotb_internal.hpp kHiScale): split, add, combine
+struct HiLo {
+  long long hi, lo;
+};
+__device__ __forceinline__ HiLo to_hilo(double x) {
+  const long long hi = __double2ll_rn(x * kHiScale);
+  const double rem = x - static_cast<double>(hi) * kHiInv;  // exact
+  return HiLo{hi, __double2ll_rn(rem * kLoScale)};
+}
+__device__ __forceinline__ void hilo_add(HiLo& a, double x) {
+  const HiLo h = to_hilo(x);
+  a.hi += h.hi;
+  a.lo += h.lo;
+}
+__device__ __forceinline__ double hilo_value(long long hi, long long lo) {
+  return static_cast<double>(hi) * kHiInv + static_cast<double>(lo) * kLoInv;
+}
+__device__ __forceinline__ void red_add_u64(long long* p, long long v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_hilo(long long* p, const HiLo& h) {
+  red_add_u64(p, h.hi);
+  red_add_u64(p + 1, h.lo);
+}
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 __device__ __forceinline__ void red_add_fx(long long* p, double v) {
   const long long q = __double2ll_rn(v * kFxScale);
   asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(q) : "memory");
+}
+// element i of a fixed-point sum array of length len: fp32 one word at 2^46;
+// fp64 a hi word at 2^46 and a lo word (at [len + i]) of the remainder at 2^86
+template <class T>
+__device__ __forceinline__ void red_fx(long long* base, int64_t i, int64_t len, T v) {
+  const double d = static_cast<double>(v);
+  const long long hi = __double2ll_rn(d * kFxScale);
+  red_add_u64(base + i, hi);
+  if (sizeof(T) == 8)
+    red_add_u64(base + len + i,
+                __double2ll_rn((d - static_cast<double>(hi) * kFxInv) * kFxLoScale));
 }
 
 // v-phase: lane (c, b) sums the 64 rows of block b of staged column c in
@@ -332,7 +373,7 @@ __device__ __forceinline__ void v_phase(const PassArgs<T>& a, const T* wbuf, int
     }
 #pragma unroll
     for (int o = CH; o < 32; o <<= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-    if (lane < CH && lane < cnt && wrow0 < a.m) red_add_fx(a.vfx + j0 + lane, static_cast<double>(s));
+    if (lane < CH && lane < cnt && wrow0 < a.m) red_fx<T>(a.vfx, j0 + lane, a.n, s);
     return;
   }
   if (lane < CH * NB) {
@@ -661,6 +702,22 @@ __device__ __forceinline__ void report_elem_mu(T xv, T cv, double mu_i, double n
   obj += c * x;
   const double slack = mu_i + nu_j - c;
   if (slack > 0) dsq += slack * slack;
+}
+
+// report_elem_mu with the two terms accumulated exactly (HiLo): the report
+// sums are then independent of the element-to-thread mapping
+template <class T>
+__device__ __forceinline__ void report_elem_exact(T xv, T cv, double mu_i, double nu_j, T rho,
+                                                  bool folded, HiLo (&acc)[2]) {
+  const double c = static_cast<double>(cv);
+  double x = static_cast<double>(xv);
+  if (folded) {
+    x += static_cast<double>(rho) * c;
+    if (x < 0) x = 0;
+  }
+  if (x != 0.0) hilo_add(acc[0], c * x);
+  const double slack = mu_i + nu_j - c;
+  if (slack > 0) hilo_add(acc[1], slack * slack);
 }
 
 template <class T>

@@ -282,16 +282,77 @@ __device__ __forceinline__ void pend_compute(const PendSnap& ps, const TailArgs<
   out3[2] = fpr;
 }
 
-constexpr int kLoadsPerLane = 6;  // totals: 6 x 32 = 192 CTAs per load round
-
 // update-phase threads: warps kUW.. (warps 0 and 1 run the scalar logic of
 // barrier 1 meanwhile)
 constexpr int kUW = 2;
 constexpr int kUT = kTT - 32 * kUW;
 
+// K exact sums (HiLo pairs) of one CTA: fixed-order int64 trees (exact, so
+// the order does not matter anyway), then one red per word into acc[0, 2K)
+template <int K>
+__device__ __forceinline__ void red_cta_hilo(HiLo (&v)[K], long long* acc, long long* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    v[k].hi = warp_sum_ll(v[k].hi);
+    v[k].lo = warp_sum_ll(v[k].lo);
+  }
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      sh[(2 * k) * kTW + warp] = v[k].hi;
+      sh[(2 * k + 1) * kTW + warp] = v[k].lo;
+    }
+  __syncthreads();
+  if (threadIdx.x < 2 * K) {
+    long long s = 0;
+#pragma unroll
+    for (int w = 0; w < kTW; ++w) s += sh[threadIdx.x * kTW + w];
+    red_add_u64(acc + threadIdx.x, s);
+  }
+}
+
+// red_cta_hilo over the update warps only (warps kUW..): named barrier 1,
+// so the sums leave while warp 0 still runs the scalar logic
+template <int K>
+__device__ __forceinline__ void red_upd_hilo(HiLo (&v)[K], long long* acc, long long* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    v[k].hi = warp_sum_ll(v[k].hi);
+    v[k].lo = warp_sum_ll(v[k].lo);
+  }
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      sh[(2 * k) * kTW + warp] = v[k].hi;
+      sh[(2 * k + 1) * kTW + warp] = v[k].lo;
+    }
+  asm volatile("bar.sync 1, %0;" ::"n"(kUT) : "memory");
+  const int t = threadIdx.x - 32 * kUW;
+  if (t < 2 * K) {
+    long long s = 0;
+#pragma unroll
+    for (int w = kUW; w < kTW; ++w) s += sh[t * kTW + w];
+    red_add_u64(acc + t, s);
+  }
+}
+
+// the fixed-point row / column sums of the sweep (PassArgs::fx): fp32 one
+// word at 2^46, fp64 a hi / lo pair (second half of the array)
 template <class T>
-__global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart,
-                                                   double* dpart, unsigned* bar) {
+__device__ __forceinline__ T fx_take(long long* fxa, int64_t i, int64_t len) {
+  const long long hi = __ldcg(fxa + i);
+  fxa[i] = 0;
+  if (sizeof(T) == 4) return static_cast<T>(static_cast<double>(hi) * kFxInv);
+  const long long lo = __ldcg(fxa + len + i);
+  fxa[len + i] = 0;
+  return static_cast<T>(static_cast<double>(hi) * kFxInv + static_cast<double>(lo) * kFxLoInv);
+}
+
+template <class T>
+__global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned* bar) {
   using V = typename V16<T>::type;
   constexpr int R = 16 / sizeof(T);
   constexpr int BW = static_cast<int>(sizeof(Book<T>) / 8);
@@ -299,25 +360,31 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
   // the next sweep (a programmatic dependent) may be scheduled now; it waits
   // in griddepcontrol.wait for this grid's completion
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  // launched as a programmatic dependent of the sweep (t.pdl): wait for its
-  // completion and memory before touching anything (no-op otherwise)
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (t.pdl: after the sweep)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int G = gridDim.x, Gp = padded_grid(G);
+  const int G = gridDim.x;
   const int par = t.tpar & 1;
   unsigned* ctr = bar + (par ? kCtr1 : kCtr0);
-  if (blockIdx.x == 0 && tid == 0) bar[par ? kCtr0 : kCtr1] = 0u;  // for the next tail
+  long long* xa = t.xacc + par * kXaWords;          // this iteration's accumulators
+  long long* xn = t.xacc + (par ^ 1) * kXaWords;    // the previous / next iteration's
+  // CTA 0 prepares what others only touch after barrier 1 or in the next
+  // launch: the next tail's counter and sweep / merge sums (A of the other
+  // parity), this iteration's update and report sums (P, R of this parity)
+  if (blockIdx.x == 0) {
+    if (tid == 0) bar[par ? kCtr0 : kCtr1] = 0u;
+    if (tid < kXaP) xn[tid] = 0;
+    else if (tid < kXaWords) xa[tid] = 0;
+  }
   const int64_t it_stamp = t.stamps ? *reinterpret_cast<volatile int64_t*>(&bk->iter) : 0;
   TAIL_STAMP(2);
   if (*reinterpret_cast<volatile int*>(&bk->stop)) return;
   __shared__ __align__(16) T red[kTT * R];  // strip merge partition sums [P][CV][R]
   __shared__ Book<T> sbk;
-  __shared__ T shT[16 * kTW];
-  __shared__ double shD[16 * kTW];
-  __shared__ T s_tt[16];
-  __shared__ double s_td[16];
+  __shared__ long long shL[2 * 8 * kTW];
+  __shared__ long long shP[2 * 8 * kTW];  // update sums (named-barrier reduction)
+  __shared__ double s_tot[24];
   __shared__ double s_patch[3];
-  __shared__ int s_gate_ran;
+  __shared__ int s_gate_ran, s_pvalid;
   const int64_t m = t.m, n = t.n;
   // the Book as this launch found it (CTA 0 of the previous tail or the host
   // wrote it; nobody writes it before barrier 1)
@@ -326,8 +393,8 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
         __ldcg(reinterpret_cast<const unsigned long long*>(bk) + tid);
   const bool fp = bk->record_trace != 0;  // configuration: constant over the solve
 
-  // this CTA's balanced range of [0, m + n): the update of both modes and
-  // the fixed-point merge; update thread ut takes e0 + ut, e0 + ut + kUT, ...
+  // this CTA's balanced range of [0, m + n): the update, and the merge in
+  // fixed-point mode; update thread ut takes e0 + ut, e0 + ut + kUT, ...
   const int64_t E = m + n;
   const int64_t e0 = static_cast<int64_t>(blockIdx.x) * E / G;
   const int64_t e1 = static_cast<int64_t>(blockIdx.x + 1) * E / G;
@@ -351,67 +418,56 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
       if (fp) f_rso = ld_keep(t.s_old + j);
     }
   }
-  // this CTA's fixed slice of the K1 CTA scalars (independent of the merge)
-  T ps[4] = {T(0), T(0), T(0), T(0)};
-  T mx = T(0), bad = T(0);
-  {
-    const int64_t np = t.n_pass_partials;
-    const int64_t k0 = static_cast<int64_t>(blockIdx.x) * np / G;
-    const int64_t k1 = static_cast<int64_t>(blockIdx.x + 1) * np / G;
-    for (int64_t k = k0 + tid; k < k1; k += kTT) {
-      const PassPartial<T> sc = t.pass_partials[k];
-      ps[0] += sc.cost;
-      ps[1] += sc.prev;
-      ps[2] += sc.dual;
-      ps[3] += sc.dx;
-      mx = fmax(mx, sc.max_abs);
-      bad += sc.bad ? T(1) : T(0);
-    }
-  }
 
-  // ---- A: merge -----------------------------------------------------------
-  T pr[3] = {T(0), T(0), T(0)};
-  double pd[4] = {0, 0, 0, 0};  // sum p a, sum p r, sum q b, sum q s (fused gate)
+  // ---- A: merge: r = u - p, s = v - q and their exact sums ------------------
+  // {sum r, |r|^2, |s|^2, sum p a, sum p r, sum q b, sum q s}
+  HiLo hm[7];
+#pragma unroll
+  for (int k = 0; k < 7; ++k) hm[k] = HiLo{0, 0};
+  auto row_terms = [&](int64_t i, T ui, T pi, T ai) -> T {
+    const T r = ui - pi;
+    st_keep(t.r_new + i, r, 2);
+    hilo_add(hm[0], static_cast<double>(r));
+    hilo_add(hm[1], static_cast<double>(r * r));
+    hilo_add(hm[3], static_cast<double>(pi) * static_cast<double>(ai));
+    hilo_add(hm[4], static_cast<double>(pi) * static_cast<double>(r));
+    return r;
+  };
+  auto col_terms = [&](int64_t j, T vj, T qj, T bj) -> T {
+    const T sv = vj - qj;
+    st_keep(t.s_new + j, sv, 2);
+    hilo_add(hm[2], static_cast<double>(sv * sv));
+    hilo_add(hm[5], static_cast<double>(qj) * static_cast<double>(bj));
+    hilo_add(hm[6], static_cast<double>(qj) * static_cast<double>(sv));
+    return sv;
+  };
   if (t.fx) {
-    // fixed-point sums (PassArgs::fx): complete after the sweep; one read
-    // (and reset) per index, by the update thread that owns it
+    // complete after the sweep: one read (and reset) per index, by the
+    // update thread that owns it
     if (ut >= 0) {
       for (int64_t e = ef; e < e1; e += kUT) {
         const bool first = e == ef;
         if (e < m) {
           const T pi = first ? f_pq : ld_keep(t.p + e);
           const T ai = first ? f_ab : ld_keep(t.a + e);
-          const long long qf = __ldcg(t.ufx + e);
-          t.ufx[e] = 0;
-          const T r = static_cast<T>(static_cast<double>(qf) * kFxInv) - pi;
-          st_keep(t.r_new + e, r, 2);
+          const T r = row_terms(e, fx_take<T>(t.ufx, e, t.ld), pi, ai);
           if (first) f_rs = r;
-          pr[0] += r;
-          pr[1] += r * r;
-          pd[0] += static_cast<double>(pi) * static_cast<double>(ai);
-          pd[1] += static_cast<double>(pi) * static_cast<double>(r);
         } else {
           const int64_t jj = e - m;
           const T qj = first ? f_pq : ld_keep(t.q + jj);
           const T bj = first ? f_ab : ld_keep(t.b + jj);
-          const long long qf = __ldcg(t.vfx + jj);
-          t.vfx[jj] = 0;
-          const T sv = static_cast<T>(static_cast<double>(qf) * kFxInv) - qj;
-          st_keep(t.s_new + jj, sv, 2);
+          const T sv = col_terms(jj, fx_take<T>(t.vfx, jj, n), qj, bj);
           if (first) f_rs = sv;
-          pr[2] += sv * sv;
-          pd[2] += static_cast<double>(qj) * static_cast<double>(bj);
-          pd[3] += static_cast<double>(qj) * static_cast<double>(sv);
         }
       }
     }
-    TAIL_STAMP(8);
   } else {
-    // strips: (m + n) merged sums as RV-wide vectors (16-B loads), u vectors
-    // [0, nvu), v vectors [nvu, nvu + nvv); CTA b owns the balanced range
-    // [b*NV/G, (b+1)*NV/G); thread t of a chunk of CV vectors handles vector
-    // t % CV over the strip rows g = t / CV (mod P), 8 loads in flight, and
-    // the P partition sums are combined in a fixed order in shared memory
+    // strips (a warm start): (m + n) merged sums as RV-wide vectors (16-B
+    // loads), u vectors [0, nvu), v vectors [nvu, nvu + nvv); CTA b owns the
+    // balanced range [b*NV/G, (b+1)*NV/G); thread t of a chunk of CV vectors
+    // handles vector t % CV over the strip rows g = t / CV (mod P), 8 loads in
+    // flight; the P partition sums are combined in a fixed order in shared
+    // memory, then the chunk's owner thread forms r / s per element
     const int64_t nvu = (m + R - 1) / R, nvv = (n + R - 1) / R, NV = nvu + nvv;
     const bool vvec = (n % R) == 0;  // v strip rows 16-B aligned
     const int64_t v0 = static_cast<int64_t>(blockIdx.x) * NV / G;
@@ -469,125 +525,52 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
         for (int k = 0; k < R; ++k) redv[(part * CV + tid % CV) * R + k] = acc[k];
       __syncthreads();
       if (tid < CV && vec < v1) {
-        T tot[R];
 #pragma unroll
         for (int k = 0; k < R; ++k) {
-          T sum = T(0);
-          for (int q = 0; q < P; ++q) sum += redv[(q * CV + tid) * R + k];
-          tot[k] = sum;
-        }
-        if (vec < nvu) {
-          const int64_t i0 = vec * R;
-#pragma unroll
-          for (int k = 0; k < R; ++k) {
-            const int64_t idx = i0 + k;
-            if (idx < m) {
-              const T pi = ld_keep(t.p + idx);
-              const T r = tot[k] - pi;
-              st_keep(t.r_new + idx, r, 2);
-              pr[0] += r;
-              pr[1] += r * r;
-              pd[0] += static_cast<double>(pi) * static_cast<double>(ld_keep(t.a + idx));
-              pd[1] += static_cast<double>(pi) * static_cast<double>(r);
-            }
-          }
-        } else {
-          const int64_t j0 = (vec - nvu) * R;
-#pragma unroll
-          for (int k = 0; k < R; ++k) {
-            const int64_t j = j0 + k;
-            if (j < n) {
-              const T qj = ld_keep(t.q + j);
-              const T sv = tot[k] - qj;
-              st_keep(t.s_new + j, sv, 2);
-              pr[2] += sv * sv;
-              pd[2] += static_cast<double>(qj) * static_cast<double>(ld_keep(t.b + j));
-              pd[3] += static_cast<double>(qj) * static_cast<double>(sv);
-            }
+          T tot = T(0);
+          for (int q = 0; q < P; ++q) tot += redv[(q * CV + tid) * R + k];
+          if (vec < nvu) {
+            const int64_t i = vec * R + k;
+            if (i < m) row_terms(i, tot, ld_keep(t.p + i), ld_keep(t.a + i));
+          } else {
+            const int64_t j = (vec - nvu) * R + k;
+            if (j < n) col_terms(j, tot, ld_keep(t.q + j), ld_keep(t.b + j));
           }
         }
       }
     }
-    TAIL_STAMP(8);
   }
-  TAIL_STAMP(9);
-  {
-    mx = warp_max(mx);
-    if (lane == 0) shT[warp] = mx;
-    __syncthreads();
-    T cmx = T(0);
-#pragma unroll
-    for (int w = 0; w < kTW; ++w) cmx = fmax(cmx, shT[w]);
-    __syncthreads();
-    T v8[8] = {ps[0], ps[1], ps[2], ps[3], bad, pr[0], pr[1], pr[2]};
-    store_partials_vm<T, 8>(v8, cpart, Gp, 0, shT);
-    if (t.fused_gate) store_partials_vm<double, 4>(pd, dpart, Gp, 10, shD);
-    if (tid == 0) cpart[8 * Gp + blockIdx.x] = cmx;
-  }
+  TAIL_STAMP(8);
+  red_cta_hilo<7>(hm, xa + 2 * kXaSumR, shL);
   TAIL_STAMP(3);
-  // ---- barrier 1: every CTA reduces the merge totals itself ----------------
+  // ---- barrier 1: every CTA reads the exact totals -------------------------
   count_barrier(ctr, static_cast<unsigned>(G), t.stamps, it_stamp);
   const bool fg = t.fused_gate != 0;
-  {
-    const int po = pend_off(par ^ 1);  // the previous tail's update partials
-    // warp w: values w, w + 8, w + 16 of {9 T: cpart 0..8} and {12 double:
-    // pending 0..7, fused-gate sums 10..13}
-    // all of a warp's loads are issued before any is consumed (a rolled
-    // load-add loop would serialize one L2 round trip per 32 CTAs)
-    for (int b0 = 0; b0 < G; b0 += 32 * kLoadsPerLane) {
-      T tv[3][kLoadsPerLane];
-      double dv[3][kLoadsPerLane];
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const int k = warp + i * kTW;
-#pragma unroll
-        for (int q = 0; q < kLoadsPerLane; ++q) {
-          const int b = b0 + lane + 32 * q;
-          tv[i][q] = T(0);
-          dv[i][q] = 0.0;
-          if (b < G) {
-            if (k < 9) {
-              tv[i][q] = __ldcg(cpart + k * Gp + b);
-            } else if (k < 21 && fg) {
-              const int kd = k - 9;
-              dv[i][q] = __ldcg(dpart + (kd < 8 ? po + kd : 10 + (kd - 8)) * Gp + b);
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const int k = warp + i * kTW;
-        if (k < 9) {
-          T acc = T(0);
-#pragma unroll
-          for (int q = 0; q < kLoadsPerLane; ++q)
-            acc = k == 8 ? fmax(acc, tv[i][q]) : acc + tv[i][q];
-          acc = k == 8 ? warp_max(acc) : warp_sum(acc);
-          if (b0 > 0) acc = k == 8 ? fmax(acc, s_tt[k]) : acc + s_tt[k];
-          __syncwarp();
-          if (lane == 0) s_tt[k] = acc;
-        } else if (k < 21 && fg) {
-          double acc = 0.0;
-#pragma unroll
-          for (int q = 0; q < kLoadsPerLane; ++q) acc += dv[i][q];
-          acc = warp_sum(acc);
-          if (b0 > 0) acc += s_td[k - 9];
-          __syncwarp();
-          if (lane == 0) s_td[k - 9] = acc;
-        }
-      }
-    }
+  // s_tot: [0, 11) the A sums, [11] max|t|, [12] non-finite count,
+  // [13, 21) the previous iteration's P sums
+  if (tid < 11) {
+    s_tot[tid] = hilo_value(__ldcg(xa + 2 * tid), __ldcg(xa + 2 * tid + 1));
+  } else if (tid == 11) {
+    s_tot[11] = __longlong_as_double(__ldcg(xa + kXaMax));
+  } else if (tid == 12) {
+    s_tot[12] = static_cast<double>(__ldcg(xa + kXaBad));
+  } else if (tid >= 32 && tid < 40 && fg) {
+    const int k = tid - 32;
+    s_tot[13 + k] = hilo_value(__ldcg(xn + kXaP + 2 * k), __ldcg(xn + kXaP + 2 * k + 1));
   }
   TAIL_STAMP(11);
   __syncthreads();
+  // the pass totals in T, as the per-CTA sums of the sweep are
+  const T tot8[8] = {static_cast<T>(s_tot[kXaCost]), static_cast<T>(s_tot[kXaPrev]),
+                     static_cast<T>(s_tot[kXaDual]), static_cast<T>(s_tot[kXaDx]),
+                     static_cast<T>(s_tot[11]),      static_cast<T>(s_tot[kXaSumR]),
+                     static_cast<T>(s_tot[kXaR2]),   static_cast<T>(s_tot[kXaS2])};
   // coef exactly as merge_scalars forms it (solver.hpp:273-277), from the
   // Book before this iteration's scalar logic touches it
-  const T beta_all = s_tt[5] / static_cast<T>(t.m_global + t.n_global);
+  const T beta_all = tot8[5] / static_cast<T>(t.m_global + t.n_global);
   const T coef = T(2) * beta_all - sbk.alpha;
-  const bool pass_bad = s_tt[4] > T(0);
+  const bool pass_bad = s_tot[12] > 0.0;
   PendSnap snap{};
-  __shared__ int s_pvalid;
   if (tid == 32) {
     snap = pend_snap(sbk);
     s_pvalid = snap.valid;
@@ -597,15 +580,14 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
   // fixed-point patch; warps 2..7: the update (solver.hpp:279-289)
   if (warp == 0) {
     if (lane == 0) {
-      // {cost, prev, dual, dx, max|t|, sum r, |r|^2, |s|^2} (merge_kernel order)
-      const T tot[8] = {s_tt[0], s_tt[1], s_tt[2], s_tt[3], s_tt[8], s_tt[5], s_tt[6], s_tt[7]};
-      merge_scalars<T>(&sbk, t, tot, pass_bad ? 1 : 0);
+      merge_scalars<T>(&sbk, t, tot8, pass_bad ? 1 : 0);
       int ran = 0;
       if (fg && !sbk.stop) {
         const double dcoef = static_cast<double>(sbk.coef);
-        const double dual_alg = ((s_td[8] - 2.0 * s_td[9] + dcoef * sbk.sum_p) * t.inv_n_d +
-                                 (s_td[10] - 2.0 * s_td[11] + dcoef * sbk.sum_q) * t.inv_m_d) /
-                                static_cast<double>(t.rho);
+        const double dual_alg =
+            ((s_tot[kXaPA] - 2.0 * s_tot[kXaPR] + dcoef * sbk.sum_p) * t.inv_n_d +
+             (s_tot[kXaQB] - 2.0 * s_tot[kXaQS] + dcoef * sbk.sum_q) * t.inv_m_d) /
+            static_cast<double>(t.rho);
         gate_fused<T>(&sbk, t, dual_alg, blockIdx.x == 0);
         sbk.pend_buf = par;
         ran = 1;
@@ -614,15 +596,19 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
     }
   } else if (warp == 1) {
     if (lane == 0 && fg && snap.valid) {
-      const double d8[8] = {s_td[0], s_td[1], s_td[2], s_td[3], s_td[4], s_td[5], s_td[6], s_td[7]};
+      const double d8[8] = {s_tot[13], s_tot[14], s_tot[15], s_tot[16],
+                            s_tot[17], s_tot[18], s_tot[19], s_tot[20]};
       pend_compute<T>(snap, t, d8, blockIdx.x == 0, s_patch);
     }
-  } else if (!pass_bad) {
-    // ---- B: phi / varphi / a / b + dual-value and fixed-point partials ----
+  }
+  // ---- B: phi / varphi / a / b + exact dual-value and fixed-point sums ------
+  HiLo hp[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) hp[k] = HiLo{0, 0};
+  if (warp >= kUW && !pass_bad) {
     const T inv_n = T(1) / static_cast<T>(t.n_global);
     const T inv_m = T(1) / static_cast<T>(t.m_global);
     const double drho = static_cast<double>(t.rho);
-    double part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int64_t e = ef; e < e1; e += kUT) {
       const bool first = e == ef && t.fx;
       if (e < m) {
@@ -633,13 +619,13 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
         const T ph = (ai - T(2) * r + coef) * inv_n;  // solver.hpp:280-282
         st_keep(t.phi + e, ph, 2);
         st_keep(t.a + e, ai - r, 2);  // solver.hpp:287
-        part[0] += static_cast<double>(pi) * static_cast<double>(ph) / drho;
+        hilo_add(hp[0], static_cast<double>(pi) * static_cast<double>(ph) / drho);
         if (fp) {
           const T ro = e == ef ? f_rso : ld_keep(t.r_old + e);
           const double d = static_cast<double>(ph) - static_cast<double>(ph_old);
-          part[1] += d * d;
-          part[2] += d;
-          part[3] += d * (static_cast<double>(r) - static_cast<double>(ro));
+          hilo_add(hp[1], d * d);
+          hilo_add(hp[2], d);
+          hilo_add(hp[3], d * (static_cast<double>(r) - static_cast<double>(ro)));
         }
       } else {
         const int64_t j = e - m;
@@ -650,23 +636,18 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
         const T vp = (bj - T(2) * sv + coef) * inv_m;  // solver.hpp:283-285
         st_keep(t.varphi + j, vp, 2);
         st_keep(t.b + j, bj - sv, 2);  // solver.hpp:288
-        part[4] += static_cast<double>(qj) * static_cast<double>(vp) / drho;
+        hilo_add(hp[4], static_cast<double>(qj) * static_cast<double>(vp) / drho);
         if (fp) {
           const T so = e == ef ? f_rso : ld_keep(t.s_old + j);
           const double d = static_cast<double>(vp) - static_cast<double>(vp_old);
-          part[5] += d * d;
-          part[6] += d;
-          part[7] += d * (static_cast<double>(sv) - static_cast<double>(so));
+          hilo_add(hp[5], d * d);
+          hilo_add(hp[6], d);
+          hilo_add(hp[7], d * (static_cast<double>(sv) - static_cast<double>(so)));
         }
       }
     }
-    // update-warp partial sums of this CTA (fixed order), stored below
-#pragma unroll
-    for (int k = 0; k < 8; ++k) part[k] = warp_sum(part[k]);
-    if (lane == 0)
-#pragma unroll
-      for (int k = 0; k < 8; ++k) shD[k * kTW + warp] = part[k];
   }
+  if (warp >= kUW && !pass_bad) red_upd_hilo<8>(hp, xa + kXaP, shP);
   __syncthreads();
   if (tid == 0) {
     if (fg && s_pvalid && !s_gate_ran) {  // gate did not run: the patch stands
@@ -680,12 +661,6 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
   TAIL_STAMP(12);
   book_store_cta0(bk, &sbk);
   TAIL_STAMP(4);
-  if (!pass_bad && tid < 8) {  // the update partials of this CTA: warps kUW.. in order
-    double s = 0.0;
-#pragma unroll
-    for (int w = kUW; w < kTW; ++w) s += shD[tid * kTW + w];
-    dpart[(pend_off(par) + tid) * Gp + blockIdx.x] = s;
-  }
   __syncthreads();
   TAIL_STAMP(5);
   if (sbk.failed) return;  // non-finite pass
@@ -695,20 +670,20 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
   }
   // ---- barrier 2 (only when needed): exact dual value / exact gate ----------
   count_barrier(ctr, 2u * static_cast<unsigned>(G), nullptr, 0);
-  {
-    double d8[8];
-    all_totals_vm<double, 8>(dpart, G, Gp, pend_off(par), d8, shD);
-    if (tid == 0) {
-      if (fg) {
-        patch_pending<T>(&sbk, t, d8, blockIdx.x == 0);
-        gate_recheck<T>(&sbk);  // exact gap before the report
-      } else {
-        gate_logic<T>(&sbk, t, d8[0] + d8[4], d8[1], d8[2], d8[5], d8[6], d8[3] + d8[7],
-                      blockIdx.x == 0);
-      }
+  if (tid < 8) s_tot[13 + tid] = hilo_value(__ldcg(xa + kXaP + 2 * tid), __ldcg(xa + kXaP + 2 * tid + 1));
+  __syncthreads();
+  if (tid == 0) {
+    const double d8[8] = {s_tot[13], s_tot[14], s_tot[15], s_tot[16],
+                          s_tot[17], s_tot[18], s_tot[19], s_tot[20]};
+    if (fg) {
+      patch_pending<T>(&sbk, t, d8, blockIdx.x == 0);
+      gate_recheck<T>(&sbk);  // exact gap before the report
+    } else {
+      gate_logic<T>(&sbk, t, d8[0] + d8[4], d8[1], d8[2], d8[5], d8[6], d8[3] + d8[7],
+                    blockIdx.x == 0);
     }
-    book_store_cta0(bk, &sbk);
   }
+  book_store_cta0(bk, &sbk);
   __syncthreads();
   if (!sbk.confirm || sbk.stop == 1) return;
 
@@ -718,7 +693,7 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
     const double drho = static_cast<double>(t.rho);
     const int64_t ngx = (m + int64_t(kTT) * R - 1) / (int64_t(kTT) * R);
     const int64_t ncs = imin64(n, (2 * static_cast<int64_t>(G) + ngx - 1) / ngx);
-    double part[2] = {0, 0};
+    HiLo hr[2] = {HiLo{0, 0}, HiLo{0, 0}};
     for (int64_t unit = blockIdx.x; unit < ngx * ncs; unit += G) {
       const int64_t rx = unit % ngx, cs = unit / ngx;
       const int64_t row0 = (rx * kTT + tid) * R;
@@ -736,15 +711,15 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, T* cpart
 #pragma unroll
         for (int k = 0; k < R; ++k)
           if (k < nvalid)
-            report_elem_mu<T>(xv[k], cv[k], mu[k], nu_j, t.rho, folded, part[0], part[1]);
+            report_elem_exact<T>(xv[k], cv[k], mu[k], nu_j, t.rho, folded, hr);
       }
     }
-    store_partials_vm<double, 2>(part, dpart, Gp, 8, shD);
+    red_cta_hilo<2>(hr, xa + kXaR, shL);
   }
   count_barrier(ctr, 3u * static_cast<unsigned>(G), nullptr, 0);
-  double d2[2];
-  all_totals_vm<double, 2>(dpart, G, Gp, 8, d2, shD);
-  if (tid == 0) report_decide<T>(&sbk, d2[0], d2[1], 0);
+  if (tid < 2) s_tot[tid] = hilo_value(__ldcg(xa + kXaR + 2 * tid), __ldcg(xa + kXaR + 2 * tid + 1));
+  __syncthreads();
+  if (tid == 0) report_decide<T>(&sbk, s_tot[0], s_tot[1], 0);
   book_store_cta0(bk, &sbk);
 }
 
@@ -1189,19 +1164,17 @@ __global__ void __launch_bounds__(kTT) shard_pending_patch_kernel(const TailArgs
 }
 
 template <class T>
-__global__ void __launch_bounds__(kTT) tail_finalize_kernel(const TailArgs<T> t,
-                                                            const double* dpart, int G) {
-  __shared__ double shD[16 * kTW];
+__global__ void __launch_bounds__(kTT) tail_finalize_kernel(const TailArgs<T> t) {
   Book<T>* bk = t.book;
-  if (!*reinterpret_cast<volatile int*>(&bk->pend_valid)) return;
+  if (threadIdx.x != 0 || !*reinterpret_cast<volatile int*>(&bk->pend_valid)) return;
   const int buf = *reinterpret_cast<volatile int*>(&bk->pend_buf);
+  const long long* xp = t.xacc + buf * kXaWords + kXaP;
   double d8[8];
-  all_totals_vm<double, 8>(dpart, G, padded_grid(G), pend_off(buf), d8, shD);
-  if (threadIdx.x == 0) {
-    Book<T> lb = *bk;
-    patch_pending<T>(&lb, t, d8);
-    *bk = lb;
-  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) d8[k] = hilo_value(xp[2 * k], xp[2 * k + 1]);
+  Book<T> lb = *bk;
+  patch_pending<T>(&lb, t, d8);
+  *bk = lb;
 }
 
 template <class T>
@@ -1254,7 +1227,9 @@ cudaError_t launch_tail(const TailArgs<T>& t, T* cpart, double* dpart, unsigned*
   cfg.attrs = attr;
   cfg.numAttrs = t.pdl ? 2 : 1;  // t.pdl: a programmatic dependent of the sweep
   count_launch();
-  return cudaLaunchKernelEx(&cfg, tail_kernel<T>, t, cpart, dpart, bar);
+  (void)cpart;
+  (void)dpart;
+  return cudaLaunchKernelEx(&cfg, tail_kernel<T>, t, bar);
 }
 
 template <class U>
@@ -1324,7 +1299,9 @@ template void launch_shard_pending_patch<double>(const TailArgs<double>&, const 
 
 template <class T>
 void launch_tail_finalize(const TailArgs<T>& t, const double* dpart, int grid, cudaStream_t st) {
-  tail_finalize_kernel<T><<<1, kTT, 0, st>>>(t, dpart, grid);
+  (void)dpart;
+  (void)grid;
+  tail_finalize_kernel<T><<<1, 32, 0, st>>>(t);
   count_launch();
 }
 

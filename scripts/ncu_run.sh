@@ -10,4 +10,4 @@ ncu --set full --clock-control none --import-source on -k regex:pass_kernel_asyn
     -o gpurun_out/pass_${TAG} python scripts/ncu_probe.py $SZ $DT 6 > gpurun_out/pp_${TAG}.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:tail_kernel -s 2 -c 1 \
     -o gpurun_out/tail_${TAG} python scripts/ncu_probe.py $SZ $DT 6 > gpurun_out/pt_${TAG}.log 2>&1
-tail -2 gpurun_out/l_${TAG}.log gpurun_out/pp_${TAG}.log gpurun_out/pt_${TAG}.log
+for f in l pp pt; do tail -n 2 gpurun_out/${f}_${TAG}.log; done
