@@ -407,8 +407,10 @@ int drotb_session_run_timed(drotb_session* s, int64_t n_iters, double* total_ms,
 #define DROTB_NCCL_ID_BYTES 128
 /* ncclGetUniqueId for rank 0 to broadcast (e.g. over torch.distributed). */
 int drotb_nccl_unique_id(char* out128);
-/* Row range of `rank` in a world_size-way split of m rows: contiguous,
- * aligned to the 64-row v blocks, as even as possible. */
+/* Row range of `rank` in a world_size-way split of m rows: contiguous, as
+ * even as possible, aligned to the sweep's 512-row CTA blocks (64 rows when
+ * m < 512 * world_size).  With 512-aligned shards the peer-memory exchange
+ * reproduces the one-GPU solve bit for bit. */
 int drotb_shard_rows(int64_t m, int32_t world_size, int32_t rank,
                      int64_t* row_begin, int64_t* row_end);
 /* A session holding rows [row_begin, row_end) of an m_global x n problem,

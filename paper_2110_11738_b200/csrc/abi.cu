@@ -677,6 +677,7 @@ int drotb_session_gen_gaussian(drotb_session* s, double sigma_t, uint64_t seed,
     CUDA_TRY(cudaGetLastError());
     std::vector<T> pg, q;
     RC_TRY(drotb::gen_marginals<T>(mg, n, seed, marginals, pg, q));
+    if (ss->sharded) ss->hp_global = pg;  // for a rank-count-independent init
     return ss->set_problem(nullptr, pg.data() + r0, q.data(), false, true);
   });
 }
@@ -692,6 +693,7 @@ int drotb_session_gen_uniform(drotb_session* s, uint64_t seed, double lo, double
     CUDA_TRY(cudaGetLastError());
     std::vector<T> pg, q;
     RC_TRY(drotb::gen_marginals<T>(mg, n, seed, marginals, pg, q));
+    if (ss->sharded) ss->hp_global = pg;  // for a rank-count-independent init
     return ss->set_problem(nullptr, pg.data() + r0, q.data(), false, true);
   });
 }
@@ -886,14 +888,18 @@ int drotb_session_attach_peers(drotb_session* s, const uint64_t* dev_ptrs,
 
 int drotb_shard_rows(int64_t m, int32_t world_size, int32_t rank, int64_t* row_begin,
                      int64_t* row_end) {
-  // contiguous row blocks aligned to the 64-row v blocks, as even as possible
+  // contiguous row blocks, as even as possible, aligned to the sweep's
+  // 512-row CTA blocks (then every per-CTA sum of a shard is the one-GPU
+  // sweep's, and the trajectory is independent of the rank count); 64-row
+  // alignment when m is too small for every rank to own a 512-row block
   drotb::clear_error();
   if (world_size < 1 || rank < 0 || rank >= world_size || m < 1)
     return drotb::set_error(DROTB_ERRC_BAD_CONFIG, "invalid shard request");
-  const int64_t blocks = (m + 63) / 64;
+  const int64_t unit = m >= 512 * static_cast<int64_t>(world_size) ? 512 : 64;
+  const int64_t blocks = (m + unit - 1) / unit;
   const int64_t b0 = blocks * rank / world_size, b1 = blocks * (rank + 1) / world_size;
-  *row_begin = std::min<int64_t>(m, b0 * 64);
-  *row_end = std::min<int64_t>(m, b1 * 64);
+  *row_begin = std::min<int64_t>(m, b0 * unit);
+  *row_end = std::min<int64_t>(m, b1 * unit);
   return 0;
 }
 

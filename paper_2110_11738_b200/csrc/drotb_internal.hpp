@@ -154,6 +154,36 @@ struct TraceRowDev {
       fixed_point_residual;
 };
 
+// Row-shard exchange over NVLink peer memory (tail.cu): every rank owns one
+// exchange buffer, mapped by every peer (CUDA IPC across processes, plain
+// device pointers within one):
+//   [0, 256)          iteration flags: uint64 generation per sending rank
+//   [256, 512)        setup-collective flags
+//   [512, ...)        2 parity buffers x world slots of slot_bytes: slot s
+//                     holds rank s's payload [v partial: n T, 16-B aligned |
+//                     16 doubles of scalars]
+//   [setup_off, ...)  2 parity buffers x world slots of setup_bytes
+//   [off_ctr, ...)    the iteration tail's cross-rank counters: 2 parities x
+//                     4 barriers, one 128-B line each (unsigned)
+//   [off_acc, ...)    the exact accumulators (2 parities x kXaWords int64):
+//                     every rank adds its row-side sums into every rank's
+//   [off_vsum, ...)   the column sums, 2 parities x vwords x n int64: every
+//                     rank adds its fixed-point column partials into every
+//                     rank's (exact, so independent of the rank order)
+// peers[r] = rank r's buffer as mapped here (peers[rank] = own buffer).
+struct XArgs {
+  char* const* peers;   // device array [world]
+  int32_t world, rank;
+  int64_t vec_bytes;    // round_up(n * sizeof(T), 16)
+  int64_t slot_bytes;   // vec_bytes + 16 * 8
+  int64_t buf_bytes;    // world * slot_bytes
+  int64_t off_ctr, off_acc, off_vsum;
+  int32_t vwords;       // int64 words per fixed-point column sum (1 fp32, 2 fp64)
+  int32_t pad;
+};
+constexpr int64_t kXIterOff = 512;
+constexpr int64_t kXSetupFlagOff = 256;
+
 template <class T>
 struct TailArgs {
   int64_t m, n, ld;
@@ -212,6 +242,10 @@ struct TailArgs {
   int32_t pad_fx;
   double inv_n_d, inv_m_d;     // 1 / double(n_global), 1 / double(m_global)
   long long* xacc;             // exact accumulators, 2 parities x kXaWords
+  // row shards (x.world > 1): the peers' buffers; the sweep's scalars land in
+  // xloc (2 parities x kXaWords, this rank only) and are forwarded by the tail
+  XArgs x;
+  long long* xloc;
   int32_t pdl;                 // tail launched as a programmatic dependent of the sweep
   int32_t pad_pdl;
 };
@@ -225,25 +259,6 @@ int tail_grid(int device);
 template <class T>
 cudaError_t launch_tail(const TailArgs<T>& t, T* cpart, double* dpart, unsigned* bar, int grid,
                         cudaStream_t st);
-// Row-shard exchange over NVLink peer memory (tail.cu): every rank owns one
-// exchange buffer, mapped by every peer (CUDA IPC across processes, plain
-// device pointers within one):
-//   [0, 256)          iteration flags: uint64 generation per sending rank
-//   [256, 512)        setup-collective flags
-//   [512, ...)        2 parity buffers x world slots of slot_bytes: slot s
-//                     holds rank s's payload [v partial: n T, 16-B aligned |
-//                     16 doubles of scalars]
-//   [setup_off, ...)  2 parity buffers x world slots of setup_bytes
-// peers[r] = rank r's buffer as mapped here (peers[rank] = own buffer).
-struct XArgs {
-  char* const* peers;   // device array [world]
-  int32_t world, rank;
-  int64_t vec_bytes;    // round_up(n * sizeof(T), 16)
-  int64_t slot_bytes;   // vec_bytes + 16 * 8
-  int64_t buf_bytes;    // world * slot_bytes
-};
-constexpr int64_t kXIterOff = 512;
-constexpr int64_t kXSetupFlagOff = 256;
 
 // setup collective over the same buffers: out[i] = op_r in[r][i] in rank
 // order (op 0 = sum, 1 = max); U in {float, double, int32}; one CTA
@@ -251,18 +266,6 @@ template <class U>
 void launch_xallreduce(const U* in, U* out, int64_t count, int op, char* const* peers,
                        int world, int rank, int64_t setup_off, int64_t setup_bytes,
                        unsigned long long gen, cudaStream_t st);
-
-template <class T>
-cudaError_t launch_shard_tail(const TailArgs<T>& t, T* cpart, double* dpart, unsigned* bar,
-                              const XArgs& x, int grid, cudaStream_t st);
-// pause / finish: local row-side pending sums -> out4 (for an allreduce), then
-// patch with the global row part and the local (replicated) column part
-template <class T>
-void launch_shard_pending_local(const TailArgs<T>& t, const double* dpart, int grid,
-                                double* out4, cudaStream_t st);
-template <class T>
-void launch_shard_pending_patch(const TailArgs<T>& t, const double* dpart, int grid,
-                                const double* glob4, cudaStream_t st);
 
 // patch the pending exact dual value / fixed-point residual (end of a run)
 template <class T>

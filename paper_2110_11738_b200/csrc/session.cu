@@ -11,10 +11,13 @@ void Session<T>::release() {
   void* bufs[] = {X, C, Xout, phi, varphi, a, b, rb[0], rb[1], sb[0], sb[1],
                   p, q, u, v, ustrip, vstrip, tscr, partials, tiles, dscr,
                   terms, book, trace, vflags, pack, pmax, dpack, dint,
-                  tcpart, tdpart, tbar, tstamps, ufx, vfx, xacc};
+                  tcpart, tdpart, tbar, tstamps, ufx, vfx, xacc_owned ? xacc : nullptr,
+                  xloc};
   tstamps = nullptr;
   ufx = vfx = nullptr;
   xacc = nullptr;
+  xloc = nullptr;
+  xacc_owned = true;
   fx_ok = fx = false;
   tcpart = nullptr;
   tdpart = nullptr;
@@ -116,8 +119,9 @@ int Session<T>::setup_coop_tail() {
       CUDA_TRY(cudaMemcpy(tstamps, init.data(), sizeof(unsigned long long) * kStampWords,
                           cudaMemcpyHostToDevice));
     }
-  if (!sharded) {
-    // exact accumulators of the one-GPU tail (every scalar sum)
+  if (!sharded || xmode == 1) {
+    // exact accumulators of the tail (every scalar sum; for row shards they
+    // move into the peer-visible exchange buffer, create_sharded)
     RC_TRY(dev_alloc(&xacc, 2 * static_cast<size_t>(kXaWords)));
     CUDA_TRY(cudaMemsetAsync(xacc, 0, sizeof(long long) * 2 * kXaWords, stream));
     // fixed-point row / column sums (one word per sum in fp32, a hi / lo
@@ -180,7 +184,11 @@ int64_t Session<T>::fast_tile_cols() const {
   }
   constexpr int R = 16 / sizeof(T);
   const int64_t rows_cta = int64_t(kWarpsPerCta) * 32 * R;
-  const int64_t row_ctas = (m + rows_cta - 1) / rows_cta;
+  // row shards: from the global row count, so that every rank (and the one
+  // GPU solve) uses the same sweep tiles -- the per-CTA sums, and so the
+  // trajectory, are then independent of the GPU count
+  const int64_t rows = tc_rows > 0 ? tc_rows : m;
+  const int64_t row_ctas = (rows + rows_cta - 1) / rows_cta;
   const int64_t target = 148 * 4 * 6;
   const int64_t col_tiles = std::max<int64_t>(1, (target + row_ctas - 1) / row_ctas);
   const int64_t w = round_up((n + col_tiles - 1) / col_tiles, kChunkCols);
@@ -401,11 +409,15 @@ int Session<T>::init(const T* x0, bool x0_is_device) {
   }
   if (tbar) CUDA_TRY(cudaMemsetAsync(tbar, 0, 1024 * sizeof(unsigned), stream));  // tail counters
   if (xacc) CUDA_TRY(cudaMemsetAsync(xacc, 0, sizeof(long long) * 2 * kXaWords, stream));
+  if (xloc) CUDA_TRY(cudaMemsetAsync(xloc, 0, sizeof(long long) * 2 * kXaWords, stream));
+  if (xmode == 1 && xa.off_ctr > 0)  // cross-rank counters, sums (before any collective)
+    CUDA_TRY(cudaMemsetAsync(xbuf + xa.off_ctr, 0, static_cast<size_t>(xbytes - xa.off_ctr), stream));
   if (fx_ok) {  // X0 = p q' bounds every row / column sum by 1; a warm start has no bound
     const size_t w = sizeof(T) == 4 ? 1 : 2;
     CUDA_TRY(cudaMemsetAsync(ufx, 0, sizeof(long long) * w * ld, stream));
     CUDA_TRY(cudaMemsetAsync(vfx, 0, sizeof(long long) * w * n, stream));
-    const bool want = x0 == nullptr;
+    // (row shards always: their tail exchanges the fixed-point column sums)
+    const bool want = x0 == nullptr || (sharded && xmode == 1);
     if (want != fx) drop_graphs();
     fx = want;
   }
@@ -486,7 +498,23 @@ int Session<T>::init(const T* x0, bool x0_is_device) {
   }
   if (cfg.max_iters <= 0) hb.stop = 1;
   CUDA_TRY(cudaMemcpyAsync(book, &hb, sizeof(hb), cudaMemcpyHostToDevice, stream));
-  if (sharded) {  // column sums and sum(a) span all ranks
+  if (sharded && xmode == 1 && x0 == nullptr &&
+      static_cast<int64_t>(hp_global.size()) == m_global) {
+    // X0 = p q' with the whole p known: every rank forms b, sum(a) and the
+    // norms over ALL rows in the one-GPU order (the rows' a are recomputed
+    // in sequence), so the start -- and with the exact tail sums the whole
+    // trajectory -- is bitwise the one-GPU solve's for any rank count
+    T* pgd = nullptr;
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&pgd), sizeof(T) * 2 * m_global, stream));
+    auto freer = [this](T* ptr) { cudaFreeAsync(ptr, stream); };
+    std::unique_ptr<T, decltype(freer)> hold(pgd, freer);
+    CUDA_TRY(cudaMemcpyAsync(pgd, hp_global.data(), sizeof(T) * m_global,
+                             cudaMemcpyHostToDevice, stream));
+    T* ag = pgd + m_global;
+    launch_init_sums<T>(nullptr, pgd, q, ag, b, m_global, n, 0, book, stream, nullptr, true);
+    CUDA_TRY(cudaMemcpyAsync(a, ag + row_begin, sizeof(T) * m, cudaMemcpyDeviceToDevice,
+                             stream));
+  } else if (sharded) {  // column sums and sum(a) span all ranks
     launch_init_sums<T>(X, p, q, a, b, m, n, ld, book, stream, pack, x0 == nullptr);
     RC_TRY(allreduce(b, static_cast<size_t>(n), ncclSum));
     RC_TRY(allreduce(pack, 2, ncclSum));
@@ -506,6 +534,11 @@ int Session<T>::init(const T* x0, bool x0_is_device) {
   return 0;
 }
 
+
+static bool noncoop_env() {
+  const char* e = std::getenv("DROTB_TAIL_NONCOOP");
+  return e && e[0] == '1';
+}
 
 template <class T>
 PassArgs<T> Session<T>::pass_args(int64_t k) {
@@ -530,9 +563,15 @@ PassArgs<T> Session<T>::pass_args(int64_t k) {
   pa.vfx = vfx;
   pa.fx = fx ? 1 : 0;
   pa.pad_fx = 0;
-  // the one-GPU cooperative tail takes the sweep's scalars as exact sums
-  pa.xacc = (k >= 0 && coop && !exact && !sharded && xacc) ? xacc + (k & 1) * kXaWords : nullptr;
-  pa.pdl = (coop && pdl_ok) ? 1 : 0;
+  // the cooperative tail takes the sweep's scalars as exact sums (row
+  // shards: into this rank's xloc; the tail forwards them to every rank)
+  pa.xacc = nullptr;
+  if (k >= 0 && coop && !exact && xacc && (!sharded || xmode == 1))
+    pa.xacc = (sharded && world > 1 ? xloc : xacc) + (k & 1) * kXaWords;
+  // (not for shards of one process sharing a device -- the DROTB_TAIL_NONCOOP
+  // test setup: sweep CTAs parked in griddepcontrol.wait could starve a peer
+  // shard's sweep that a spinning tail waits for)
+  pa.pdl = (coop && pdl_ok && !(sharded && noncoop_env())) ? 1 : 0;
   pa.trigger = (coop && tail_pdl && !exact && !sharded) ? 1 : 0;
   pa.l2hint = l2hint;
   pa.pad_l2 = 0;
@@ -595,6 +634,10 @@ TailArgs<T> Session<T>::tail_args(int64_t k, int mode, bool folded_after, bool s
   t.fx = fx ? 1 : 0;
   t.pdl = (coop && tail_pdl && !exact && !sharded) ? 1 : 0;
   t.xacc = xacc;
+  std::memset(&t.x, 0, sizeof(t.x));
+  t.x.world = 1;
+  if (sharded && xmode == 1) t.x = xa;
+  t.xloc = xloc;
   t.inv_n_d = 1.0 / static_cast<double>(n_global);
   t.inv_m_d = 1.0 / static_cast<double>(m_global);
   return t;
@@ -620,8 +663,8 @@ int Session<T>::enqueue_iteration(cudaEvent_t pass_begin, cudaEvent_t pass_end, 
   launch_pass<T>(pa, mode, want_dual, want_dx, stream);
   if (pass_end) CUDA_TRY(cudaEventRecordWithFlags(pass_end, stream, evf));
   TailArgs<T> ta = tail_args(k, mode, folded_after, true);
-  if (sharded && xmode == 1) {  // K1 + the tail with the fused peer exchange
-    CUDA_TRY(launch_shard_tail<T>(ta, tcpart, tdpart, tbar, xa, tgrid, stream));
+  if (sharded && xmode == 1) {  // K1 + the tail with the exchange over peer memory
+    CUDA_TRY(launch_tail<T>(ta, tcpart, tdpart, tbar, tgrid, stream));
     h_iter = k + 1;
     h_folded = folded_after;
     return 0;
@@ -882,7 +925,7 @@ int Session<T>::run_timed(int64_t n_iters, double* total_ms, double* pass_ms, in
 template <class T>
 int Session<T>::run() {
   if (!initialized) return set_error(DROTB_ERRC_BAD_CONFIG, "session not initialized");
-  if (sharded) return run_sharded();
+  if (sharded && xmode != 1) return run_sharded();  // NCCL: host-driven confirm pauses
   const int64_t bi = batch_iters();
   int slot = 0;
   bool pending = false;
@@ -911,7 +954,7 @@ int Session<T>::run() {
 template <class T>
 int Session<T>::finalize_pending() {  // coop tail: patch the last iteration's exact dual / trace terms
   if (!coop || !tdpart) return 0;
-  if (sharded) return xmode == 1 ? shard_patch_pending() : 0;
+  if (sharded && xmode != 1) return 0;
   TailArgs<T> ta = tail_args(h_iter, kFold, h_folded, true);
   launch_tail_finalize<T>(ta, tdpart, tgrid, stream);
   CUDA_TRY(cudaGetLastError());

@@ -148,9 +148,13 @@ struct Session {
   // for warm starts, whose row sums have no a-priori bound)
   long long *ufx = nullptr, *vfx = nullptr;
   bool fx_ok = false, fx = false;
-  long long* xacc = nullptr;  // exact accumulators of the one-GPU tail (2 x kXaWords)
+  long long* xacc = nullptr;  // exact accumulators of the tail (2 x kXaWords)
+  bool xacc_owned = true;     // false: xacc lives in the exchange buffer (row shards)
+  long long* xloc = nullptr;  // row shards: this rank's sweep scalars (2 x kXaWords)
+  int64_t tc_rows = 0;        // rows the sweep tiles are sized for (0: m)
 
   std::vector<T> hp, hq;
+  std::vector<T> hp_global;  // row shards: the whole p when known (generated problems)
   T rho = T(0);
   double rho_d = 0;
   int64_t bs = 64, tc = 256, grid_cols = 0, grid_rows64 = 0, n_partials = 0;
@@ -312,9 +316,6 @@ struct Session {
   // GPU queue never drains.
   // Sharded confirm after a gate pause (stop == 2): the exact report's sums
   // over all ranks, then the replicated decision (stop -> 1 or back to 0).
-  // p2p shards: the last iteration's exact dual value / trace terms (the
-  // row part is summed over the ranks, the column part is replicated)
-  int shard_patch_pending();
 
   int sharded_report(bool always);
 

@@ -1,7 +1,9 @@
 // session_shard.cu -- row-sharded sessions: rank r owns rows
 // [row_begin, row_end) of X and C; the per-iteration exchange of the column
 // sums and scalars runs either inside the cooperative tail over NVLink peer
-// memory (xmode 1, tail.cu shard_tail_kernel) or as NCCL allreduces between
+// memory (xmode 1: the one tail kernel of tail.cu with world > 1 -- integer
+// atomics into every rank's sums, bit-identical for any rank count) or as
+// NCCL allreduces between
 // per-launch kernels (xmode 0).
 #include <dlfcn.h>
 
@@ -49,6 +51,7 @@ int Session<T>::create_sharded(int64_t m_glob, int64_t n_, const drotb_config& c
   drotb_config c2 = c;
   if (exchange == 0) c2.use_graphs = 0;  // NCCL iterations are enqueued eagerly (+ pause)
   sharded_create = true;  // the sharded tails are set up below
+  tc_rows = m_glob;       // the one-GPU sweep tiles (rank-count-independent sums)
   RC_TRY(create(r1 - r0, n_, c2));
   m_global = m_glob;
   row_begin = r0;
@@ -72,9 +75,20 @@ int Session<T>::create_sharded(int64_t m_glob, int64_t n_, const drotb_config& c
     xa.rank = rank;
     xsetup_bytes = round_up(std::max<int64_t>(n, 32) * 8, 16);
     xsetup_off = kXIterOff + 2 * xa.buf_bytes;
-    xbytes = xsetup_off + 2 * world * xsetup_bytes;
+    // the iteration tail's cross-rank counters, exact sums and column sums
+    xa.off_ctr = xsetup_off + 2 * world * xsetup_bytes;
+    xa.off_acc = xa.off_ctr + 2 * 4 * 128;
+    xa.off_vsum = xa.off_acc + 2 * kXaWords * 8;
+    xa.vwords = sizeof(T) == 4 ? 1 : 2;
+    xbytes = xa.off_vsum + 2 * static_cast<int64_t>(xa.vwords) * n * 8;
     CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&xbuf), static_cast<size_t>(xbytes)));
     CUDA_TRY(cudaMemset(xbuf, 0, static_cast<size_t>(xbytes)));
+    if (!xacc || !fx_ok) return set_error(DROTB_ERRC_BAD_CONFIG, "exact sums unavailable");
+    if (xacc_owned) cudaFree(xacc);
+    xacc = reinterpret_cast<long long*>(xbuf + xa.off_acc);
+    xacc_owned = false;
+    RC_TRY(dev_alloc(&xloc, 2 * static_cast<size_t>(kXaWords)));
+    CUDA_TRY(cudaMemset(xloc, 0, sizeof(long long) * 2 * kXaWords));
     return 0;
   }
   ncclUniqueId id;
@@ -152,31 +166,13 @@ int Session<T>::agree(int local_rc, const std::string& local_msg) {
 }
 
 
-// Runs the loop until the device raises its stop flag (converged,
-// max_iters, numerical failure).  The host polls one batch behind so the
-// GPU queue never drains.
-// Sharded confirm after a gate pause (stop == 2): the exact report's sums
-// over all ranks, then the replicated decision (stop -> 1 or back to 0).
-// p2p shards: the last iteration's exact dual value / trace terms (the
-// row part is summed over the ranks, the column part is replicated)
-template <class T>
-int Session<T>::shard_patch_pending() {
-  TailArgs<T> ta = tail_args(h_iter, kFold, h_folded, true);
-  launch_shard_pending_local<T>(ta, tdpart, tgrid, dpack, stream);
-  RC_TRY(allreduce(dpack, 4, ncclSum));
-  launch_shard_pending_patch<T>(ta, tdpart, tgrid, dpack, stream);
-  CUDA_TRY(cudaGetLastError());
-  return 0;
-}
-
-
+// Sharded confirm after a gate pause (stop == 2, the NCCL exchange): the
+// exact report's sums over all ranks, then the replicated decision (stop ->
+// 1 or back to 0); also the final report of a max_iters run.
 template <class T>
 int Session<T>::sharded_report(bool always) {
-  if (xmode == 1) RC_TRY(shard_patch_pending());
   Book<T> hb;
   RC_TRY(read_book(&hb));
-  // the exact gap withdrew the gate (gate_recheck; same verdict on every rank)
-  if (!always && xmode == 1 && !hb.confirm) return 0;
   TailArgs<T> ta = tail_args(hb.iter, kPlain0, hb.folded != 0, true);
   launch_report<T>(X, C, ta, false, always, stream);
   RC_TRY(allreduce(dpack + 4, 2, ncclSum));
@@ -214,8 +210,6 @@ template int Session<float>::attach_peers(const uint64_t* ptrs, const char* hand
 template int Session<double>::attach_peers(const uint64_t* ptrs, const char* handles);
 template int Session<float>::agree(int local_rc, const std::string& local_msg);
 template int Session<double>::agree(int local_rc, const std::string& local_msg);
-template int Session<float>::shard_patch_pending();
-template int Session<double>::shard_patch_pending();
 template int Session<float>::sharded_report(bool always);
 template int Session<double>::sharded_report(bool always);
 template int Session<float>::run_sharded();

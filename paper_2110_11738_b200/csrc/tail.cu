@@ -313,10 +313,88 @@ __device__ __forceinline__ void red_cta_hilo(HiLo (&v)[K], long long* acc, long 
   }
 }
 
+// ---- row shards (TailArgs::x, world > 1) ----------------------------------
+__device__ __forceinline__ void red_sys_u64(long long* p, long long v) {
+  asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_sys_max_u64(long long* p, long long v) {
+  asm volatile("red.relaxed.sys.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_release_sys_u32(unsigned* p, unsigned v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_relaxed_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// this iteration's accumulators / counters / column sums of rank r
+__device__ __forceinline__ long long* x_acc(const XArgs& x, int r, int par) {
+  return reinterpret_cast<long long*>(x.peers[r] + x.off_acc) + par * kXaWords;
+}
+__device__ __forceinline__ unsigned* x_ctr(const XArgs& x, int r, int par, int b) {
+  return reinterpret_cast<unsigned*>(x.peers[r] + x.off_ctr) + (par * 4 + b) * 32;
+}
+__device__ __forceinline__ long long* x_vsum(const XArgs& x, int r, int par, int64_t n) {
+  return reinterpret_cast<long long*>(x.peers[r] + x.off_vsum) + par * n * x.vwords;
+}
+// cross-rank barrier b of this iteration: every CTA of every rank adds one to
+// every rank's counter (release, system scope) and waits for world * G on its own
+__device__ __forceinline__ void xrank_barrier(const XArgs& x, int par, int b, unsigned want,
+                                              unsigned long long* stamps, int64_t it_stamp) {
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < x.world; ++r) red_release_sys_u32(x_ctr(x, r, par, b), 1u);
+    const unsigned* mine = x_ctr(x, x.rank, par, b);
+    while (static_cast<int>(ld_relaxed_sys(mine) - want) < 0) {
+    }
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    if (stamps) timeline_point(stamps, it_stamp, 10, global_ns());
+  }
+  __syncthreads();
+}
+
+// red_cta_hilo with a destination per sum: sums whose bit is set in
+// all_mask (row-side sums of this rank's rows) go to every rank's
+// accumulator, the others (replicated column-side sums) to this rank's only
+template <int K>
+__device__ __forceinline__ void red_cta_hilo_x(HiLo (&v)[K], int word0, int all_mask,
+                                               const XArgs& x, int par, long long* local,
+                                               long long* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    v[k].hi = warp_sum_ll(v[k].hi);
+    v[k].lo = warp_sum_ll(v[k].lo);
+  }
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      sh[(2 * k) * kTW + warp] = v[k].hi;
+      sh[(2 * k + 1) * kTW + warp] = v[k].lo;
+    }
+  __syncthreads();
+  if (threadIdx.x < 2 * K) {
+    long long s = 0;
+#pragma unroll
+    for (int w = 0; w < kTW; ++w) s += sh[threadIdx.x * kTW + w];
+    const int word = word0 + threadIdx.x;
+    if (x.world > 1 && ((all_mask >> (threadIdx.x >> 1)) & 1)) {
+      for (int r = 0; r < x.world; ++r) red_sys_u64(x_acc(x, r, par) + word, s);
+    } else {
+      red_add_u64(local + word, s);
+    }
+  }
+}
+
 // red_cta_hilo over the update warps only (warps kUW..): named barrier 1,
 // so the sums leave while warp 0 still runs the scalar logic
 template <int K>
-__device__ __forceinline__ void red_upd_hilo(HiLo (&v)[K], long long* acc, long long* sh) {
+__device__ __forceinline__ void red_upd_hilo(HiLo (&v)[K], int word0, int all_mask,
+                                             const XArgs& x, int par, long long* local,
+                                             long long* sh) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
@@ -335,7 +413,12 @@ __device__ __forceinline__ void red_upd_hilo(HiLo (&v)[K], long long* acc, long 
     long long s = 0;
 #pragma unroll
     for (int w = kUW; w < kTW; ++w) s += sh[t * kTW + w];
-    red_add_u64(acc + t, s);
+    const int word = word0 + t;
+    if (x.world > 1 && ((all_mask >> (t >> 1)) & 1)) {
+      for (int r = 0; r < x.world; ++r) red_sys_u64(x_acc(x, r, par) + word, s);
+    } else {
+      red_add_u64(local + word, s);
+    }
   }
 }
 
@@ -364,20 +447,60 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x;
   const int par = t.tpar & 1;
+  const XArgs& X = t.x;
+  const bool multi = X.world > 1;  // row shards: counters / sums on every rank
   unsigned* ctr = bar + (par ? kCtr1 : kCtr0);
-  long long* xa = t.xacc + par * kXaWords;          // this iteration's accumulators
-  long long* xn = t.xacc + (par ^ 1) * kXaWords;    // the previous / next iteration's
-  // CTA 0 prepares what others only touch after barrier 1 or in the next
-  // launch: the next tail's counter and sweep / merge sums (A of the other
-  // parity), this iteration's update and report sums (P, R of this parity)
+  // this iteration's accumulators and the other parity's (the previous
+  // iteration's pending update sums, the next iteration's sweep / merge sums)
+  long long* xa = multi ? x_acc(X, X.rank, par) : t.xacc + par * kXaWords;
+  long long* xn = multi ? x_acc(X, X.rank, par ^ 1) : t.xacc + (par ^ 1) * kXaWords;
+  // CTA 0 prepares what others (of every rank) only touch after barrier 1
+  // or in the next launch: the next tail's counters and sweep / merge sums
+  // (A of the other parity), this iteration's update and report sums (P, R)
   if (blockIdx.x == 0) {
     if (tid == 0) bar[par ? kCtr0 : kCtr1] = 0u;
+    if (multi && tid < 4) *x_ctr(X, X.rank, par ^ 1, tid) = 0u;
     if (tid < kXaP) xn[tid] = 0;
     else if (tid < kXaWords) xa[tid] = 0;
   }
   const int64_t it_stamp = t.stamps ? *reinterpret_cast<volatile int64_t*>(&bk->iter) : 0;
   TAIL_STAMP(2);
   if (*reinterpret_cast<volatile int*>(&bk->stop)) return;
+  if (multi) {
+    // row shards: this rank's sweep left fixed-point column partials in vfx
+    // and its scalars in xloc -- add both into every rank's sums (integer
+    // atomics over NVLink: exact, so the totals do not depend on the rank
+    // count or order), then a cross-rank barrier
+    const int64_t n_ = t.n;
+    const int vw = X.vwords;
+    for (int64_t j = static_cast<int64_t>(blockIdx.x) * kTT + tid; j < n_;
+         j += static_cast<int64_t>(gridDim.x) * kTT) {
+      for (int w = 0; w < vw; ++w) {
+        const long long q = __ldcg(t.vfx + w * n_ + j);
+        t.vfx[w * n_ + j] = 0;
+        if (q != 0)
+          for (int r = 0; r < X.world; ++r) red_sys_u64(x_vsum(X, r, par, n_) + w * n_ + j, q);
+      }
+    }
+    if (blockIdx.x == 0 && tid < 2 * kXaDx + 2) {  // cost, prev, dual, dx (hi / lo)
+      long long* src = t.xloc + par * kXaWords + tid;
+      const long long q = __ldcg(src);
+      *src = 0;
+      for (int r = 0; r < X.world; ++r) red_sys_u64(x_acc(X, r, par) + tid, q);
+    } else if (blockIdx.x == 0 && (tid == 32 || tid == 33)) {  // max |t|, non-finite count
+      const int word = tid == 32 ? kXaMax : kXaBad;
+      long long* src = t.xloc + par * kXaWords + word;
+      const long long q = __ldcg(src);
+      *src = 0;
+      for (int r = 0; r < X.world; ++r) {
+        if (tid == 32)
+          red_sys_max_u64(x_acc(X, r, par) + word, q);
+        else
+          red_sys_u64(x_acc(X, r, par) + word, q);
+      }
+    }
+    xrank_barrier(X, par, 0, static_cast<unsigned>(X.world) * gridDim.x, nullptr, 0);
+  }
   __shared__ __align__(16) T red[kTT * R];  // strip merge partition sums [P][CV][R]
   __shared__ Book<T> sbk;
   __shared__ long long shL[2 * 8 * kTW];
@@ -456,7 +579,8 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned
           const int64_t jj = e - m;
           const T qj = first ? f_pq : ld_keep(t.q + jj);
           const T bj = first ? f_ab : ld_keep(t.b + jj);
-          const T sv = col_terms(jj, fx_take<T>(t.vfx, jj, n), qj, bj);
+          const T sv = col_terms(
+              jj, fx_take<T>(multi ? x_vsum(X, X.rank, par, n) : t.vfx, jj, n), qj, bj);
           if (first) f_rs = sv;
         }
       }
@@ -541,10 +665,13 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned
     }
   }
   TAIL_STAMP(8);
-  red_cta_hilo<7>(hm, xa + 2 * kXaSumR, shL);
+  red_cta_hilo_x<7>(hm, 2 * kXaSumR, 0x1B, X, par, xa, shL);
   TAIL_STAMP(3);
   // ---- barrier 1: every CTA reads the exact totals -------------------------
-  count_barrier(ctr, static_cast<unsigned>(G), t.stamps, it_stamp);
+  if (multi)
+    xrank_barrier(X, par, 1, static_cast<unsigned>(X.world) * G, t.stamps, it_stamp);
+  else
+    count_barrier(ctr, static_cast<unsigned>(G), t.stamps, it_stamp);
   const bool fg = t.fused_gate != 0;
   // s_tot: [0, 11) the A sums, [11] max|t|, [12] non-finite count,
   // [13, 21) the previous iteration's P sums
@@ -647,7 +774,7 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned
       }
     }
   }
-  if (warp >= kUW && !pass_bad) red_upd_hilo<8>(hp, xa + kXaP, shP);
+  if (warp >= kUW && !pass_bad) red_upd_hilo<8>(hp, kXaP, 0x0F, X, par, xa, shP);
   __syncthreads();
   if (tid == 0) {
     if (fg && s_pvalid && !s_gate_ran) {  // gate did not run: the patch stands
@@ -669,7 +796,10 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned
     return;
   }
   // ---- barrier 2 (only when needed): exact dual value / exact gate ----------
-  count_barrier(ctr, 2u * static_cast<unsigned>(G), nullptr, 0);
+  if (multi)
+    xrank_barrier(X, par, 2, static_cast<unsigned>(X.world) * G, nullptr, 0);
+  else
+    count_barrier(ctr, 2u * static_cast<unsigned>(G), nullptr, 0);
   if (tid < 8) s_tot[13 + tid] = hilo_value(__ldcg(xa + kXaP + 2 * tid), __ldcg(xa + kXaP + 2 * tid + 1));
   __syncthreads();
   if (tid == 0) {
@@ -714,9 +844,12 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned
             report_elem_exact<T>(xv[k], cv[k], mu[k], nu_j, t.rho, folded, hr);
       }
     }
-    red_cta_hilo<2>(hr, xa + kXaR, shL);
+    red_cta_hilo_x<2>(hr, kXaR, 0x3, X, par, xa, shL);
   }
-  count_barrier(ctr, 3u * static_cast<unsigned>(G), nullptr, 0);
+  if (multi)
+    xrank_barrier(X, par, 3, static_cast<unsigned>(X.world) * G, nullptr, 0);
+  else
+    count_barrier(ctr, 3u * static_cast<unsigned>(G), nullptr, 0);
   if (tid < 2) s_tot[tid] = hilo_value(__ldcg(xa + kXaR + 2 * tid), __ldcg(xa + kXaR + 2 * tid + 1));
   __syncthreads();
   if (tid == 0) report_decide<T>(&sbk, s_tot[0], s_tot[1], 0);
@@ -804,366 +937,6 @@ __global__ void __launch_bounds__(1024) xallreduce_kernel(const U* in, U* out, i
 }
 
 template <class T>
-__global__ void __launch_bounds__(kTT) shard_tail_kernel(const TailArgs<T> t, T* cpart,
-                                                         double* dpart, unsigned* bar,
-                                                         const XArgs x) {
-  Book<T>* bk = t.book;
-  if (*reinterpret_cast<volatile int*>(&bk->stop)) return;
-  __shared__ T red[kTW][32];
-  __shared__ Book<T> sbk;
-  __shared__ T shT[16 * kTW];
-  __shared__ double shD[16 * kTW];
-  __shared__ unsigned s_gen0;
-  __shared__ long long s_k;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int G = gridDim.x;
-  const int64_t m = t.m, n = t.n;
-  if (tid == 0) {
-    s_gen0 = ld_acquire(bar + 1);
-    s_k = *reinterpret_cast<volatile long long*>(&bk->iter);
-  }
-  __syncthreads();
-  unsigned my_gen = s_gen0;
-  const int64_t k = s_k;
-  const int pb = static_cast<int>(k & 1);
-  const unsigned long long gen = static_cast<unsigned long long>(k + 1);
-
-  // ---- A: local merge; v partials go straight to every peer ---------------
-  {
-    T pr[3] = {T(0), T(0), T(0)};
-    double pd[2] = {0, 0};
-    const int64_t ngr = (m + 31) / 32, ngc = (n + 31) / 32;
-    for (int64_t grp = blockIdx.x; grp < ngr + ngc; grp += G) {
-      T acc = T(0);
-      if (grp < ngr) {
-        const int64_t idx = grp * 32 + lane;
-        if (idx < m) {
-          int64_t g = warp;
-          for (; g + 7 * kTW < t.grid_cols; g += 8 * kTW) {
-            T v8[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) v8[q] = t.ustrip[(g + q * kTW) * t.ld + idx];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) acc += v8[q];
-          }
-          for (; g < t.grid_cols; g += kTW) acc += t.ustrip[g * t.ld + idx];
-        }
-      } else {
-        const int64_t j = (grp - ngr) * 32 + lane;
-        if (j < n) {
-          int64_t g = warp;
-          for (; g + 7 * kTW < t.grid_rows64; g += 8 * kTW) {
-            T v8[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) v8[q] = t.vstrip[(g + q * kTW) * n + j];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) acc += v8[q];
-          }
-          for (; g < t.grid_rows64; g += kTW) acc += t.vstrip[g * n + j];
-        }
-      }
-      red[warp][lane] = acc;
-      __syncthreads();
-      if (warp == 0) {
-        T tot = T(0);
-#pragma unroll
-        for (int w = 0; w < kTW; ++w) tot += red[w][lane];
-        if (grp < ngr) {
-          const int64_t idx = grp * 32 + lane;
-          if (idx < m) {
-            const T pi = t.p[idx];
-            const T r = tot - pi;
-            t.r_new[idx] = r;
-            pr[0] += r;
-            pr[1] += r * r;
-            pd[0] += static_cast<double>(pi) * static_cast<double>(t.a[idx]);
-            pd[1] += static_cast<double>(pi) * static_cast<double>(r);
-          }
-        } else {
-          const int64_t j = (grp - ngr) * 32 + lane;
-          if (j < n)
-            for (int r = 0; r < x.world; ++r)
-              reinterpret_cast<T*>(xslot(x, r, pb, x.rank))[j] = tot;
-        }
-      }
-      __syncthreads();
-    }
-    __threadfence_system();  // this CTA's peer stores before its arrival
-    const int64_t np = t.n_pass_partials;
-    const int64_t k0 = static_cast<int64_t>(blockIdx.x) * np / G;
-    const int64_t k1 = static_cast<int64_t>(blockIdx.x + 1) * np / G;
-    T ps[4] = {T(0), T(0), T(0), T(0)};
-    T mx = T(0), bad = T(0);
-    for (int64_t q = k0 + tid; q < k1; q += kTT) {
-      const PassPartial<T> sc = t.pass_partials[q];
-      ps[0] += sc.cost;
-      ps[1] += sc.prev;
-      ps[2] += sc.dual;
-      ps[3] += sc.dx;
-      mx = fmax(mx, sc.max_abs);
-      bad += sc.bad ? T(1) : T(0);
-    }
-    mx = warp_max(mx);
-    if (lane == 0) shT[warp] = mx;
-    __syncthreads();
-    T cmx = T(0);
-#pragma unroll
-    for (int w = 0; w < kTW; ++w) cmx = fmax(cmx, shT[w]);
-    __syncthreads();
-    T v8[8] = {ps[0], ps[1], ps[2], ps[3], bad, pr[0], pr[1], pr[2]};
-    store_partials<T, 8>(v8, cpart, 0, shT);
-    if (tid == 0) cpart[blockIdx.x * kTSlots + 8] = cmx;
-    store_partials<double, 2>(pd, dpart, 10, shD);
-  }
-  reduce_barrier(bar, my_gen, [&] {
-    // local totals -> the 16-double scalar payload of this rank
-    const bool pend = *reinterpret_cast<volatile int*>(&bk->pend_valid) != 0;
-    T acc[8];
-    double dd[6];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = T(0);
-#pragma unroll
-    for (int q = 0; q < 6; ++q) dd[q] = 0.0;
-    T m1 = T(0);
-    for (int b = tid; b < G; b += kTT) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) acc[q] += __ldcg(cpart + b * kTSlots + q);
-      m1 = fmax(m1, __ldcg(cpart + b * kTSlots + 8));
-#pragma unroll
-      for (int q = 0; q < 2; ++q) dd[q] += __ldcg(dpart + b * kTSlots + 10 + q);
-      if (pend)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) dd[2 + q] += __ldcg(dpart + b * kTSlots + q);  // row part
-    }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = warp_sum(acc[q]);
-    m1 = warp_max(m1);
-#pragma unroll
-    for (int q = 0; q < 6; ++q) dd[q] = warp_sum(dd[q]);
-    if (lane == 0) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) shT[q * kTW + warp] = acc[q];
-      shT[8 * kTW + warp] = m1;
-#pragma unroll
-      for (int q = 0; q < 6; ++q) shD[q * kTW + warp] = dd[q];
-    }
-    __syncthreads();
-    __shared__ double payload[16];
-    if (tid < 16) {
-      double v = 0.0;
-      if (tid < 8) {
-        T sum = T(0);
-#pragma unroll
-        for (int w = 0; w < kTW; ++w) sum += shT[tid * kTW + w];
-        v = static_cast<double>(sum);  // cost prev dual dx bad sum_r |r|^2 |s|^2(unused)
-      } else if (tid == 8) {
-        T mm = T(0);
-#pragma unroll
-        for (int w = 0; w < kTW; ++w) mm = fmax(mm, shT[8 * kTW + w]);
-        v = static_cast<double>(mm);
-      } else if (tid < 15) {
-        double sum = 0.0;
-#pragma unroll
-        for (int w = 0; w < kTW; ++w) sum += shD[(tid - 9) * kTW + w];
-        v = sum;  // 9: sum p a, 10: sum p r, 11..14: pending row part
-      }
-      payload[tid] = v;
-    }
-    __syncthreads();
-    if (tid < 16)
-      for (int r = 0; r < x.world; ++r)
-        reinterpret_cast<double*>(xslot(x, r, pb, x.rank) + x.vec_bytes)[tid] = payload[tid];
-    __threadfence_system();
-    __syncthreads();
-    if (tid == 0) {
-      for (int r = 0; r < x.world; ++r)
-        st_release_sys_u64(reinterpret_cast<unsigned long long*>(x.peers[r]) + x.rank, gen);
-      const unsigned long long* mine = reinterpret_cast<const unsigned long long*>(x.peers[x.rank]);
-      for (int r = 0; r < x.world; ++r)
-        while (ld_acquire_sys_u64(mine + r) < gen) {
-        }
-    }
-    __syncthreads();
-  });
-
-  // ---- B: global column sums in rank order; s = v - q (replicated) --------
-  {
-    T ps2 = T(0);
-    double pq[2] = {0, 0};
-    for (int64_t j = static_cast<int64_t>(blockIdx.x) * kTT + tid; j < n;
-         j += static_cast<int64_t>(G) * kTT) {
-      T v = T(0);
-      for (int r = 0; r < x.world; ++r)
-        v += __ldcg(reinterpret_cast<const T*>(xslot(x, x.rank, pb, r)) + j);
-      const T qj = t.q[j];
-      const T sv = v - qj;
-      t.s_new[j] = sv;
-      ps2 += sv * sv;
-      pq[0] += static_cast<double>(qj) * static_cast<double>(t.b[j]);
-      pq[1] += static_cast<double>(qj) * static_cast<double>(sv);
-    }
-    T one[1] = {ps2};
-    store_partials<T, 1>(one, cpart, 9, shT);
-    store_partials<double, 2>(pq, dpart, 14, shD);
-  }
-  reduce_barrier(bar, my_gen, [&] {
-    constexpr int BW = static_cast<int>(sizeof(Book<T>) / 8);
-    unsigned long long bw = tid < BW ? __ldcg(reinterpret_cast<const unsigned long long*>(bk) + tid)
-                                     : 0ull;
-    T s2 = T(0);
-    double dc[6] = {0, 0, 0, 0, 0, 0};  // q.b, q.s, pending column part (4)
-    for (int b = tid; b < G; b += kTT) {
-      s2 += __ldcg(cpart + b * kTSlots + 9);
-      dc[0] += __ldcg(dpart + b * kTSlots + 14);
-      dc[1] += __ldcg(dpart + b * kTSlots + 15);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) dc[2 + q] += __ldcg(dpart + b * kTSlots + 4 + q);
-    }
-    if (tid < BW) reinterpret_cast<unsigned long long*>(&sbk)[tid] = bw;
-    s2 = warp_sum(s2);
-#pragma unroll
-    for (int q = 0; q < 6; ++q) dc[q] = warp_sum(dc[q]);
-    if (lane == 0) {
-      shT[warp] = s2;
-#pragma unroll
-      for (int q = 0; q < 6; ++q) shD[q * kTW + warp] = dc[q];
-    }
-    __syncthreads();
-    if (tid == 0) {
-      T ss = T(0);
-#pragma unroll
-      for (int w = 0; w < kTW; ++w) ss += shT[w];
-      double c6[6];
-#pragma unroll
-      for (int q = 0; q < 6; ++q) {
-        double sum = 0.0;
-#pragma unroll
-        for (int w = 0; w < kTW; ++w) sum += shD[q * kTW + w];
-        c6[q] = sum;
-      }
-      // global scalars: the ranks' payloads summed in rank order
-      double g16[16];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) g16[q] = 0.0;
-      double gmax = 0.0;
-      for (int r = 0; r < x.world; ++r) {
-        const double* pl =
-            reinterpret_cast<const double*>(xslot(x, x.rank, pb, r) + x.vec_bytes);
-        for (int q = 0; q < 16; ++q) {
-          const double v = __ldcg(pl + q);
-          if (q == 8)
-            gmax = fmax(gmax, v);
-          else
-            g16[q] += v;
-        }
-      }
-      // the previous iteration's exact dual value / fixed-point terms
-      const double d8[8] = {g16[11], g16[12], g16[13], g16[14], c6[2], c6[3], c6[4], c6[5]};
-      patch_pending<T>(&sbk, t, d8);
-      const T tot[8] = {static_cast<T>(g16[0]), static_cast<T>(g16[1]), static_cast<T>(g16[2]),
-                        static_cast<T>(g16[3]), static_cast<T>(gmax),   static_cast<T>(g16[5]),
-                        static_cast<T>(g16[6]), ss};
-      merge_scalars<T>(&sbk, t, tot, g16[4] > 0.0 ? 1 : 0);
-      if (!sbk.stop) {
-        const double coef = static_cast<double>(sbk.coef);
-        const double inv_n = 1.0 / static_cast<double>(t.n_global);
-        const double inv_m = 1.0 / static_cast<double>(t.m_global);
-        const double dual_alg = ((g16[9] - 2.0 * g16[10] + coef * sbk.sum_p) * inv_n +
-                                 (c6[0] - 2.0 * c6[1] + coef * sbk.sum_q) * inv_m) /
-                                static_cast<double>(t.rho);
-        gate_fused<T>(&sbk, t, dual_alg);
-        if (sbk.confirm && !sbk.stop) sbk.stop = 2;  // pause: collective confirm on the host
-      }
-    }
-    book_store(bk, &sbk);
-  });
-  if (*reinterpret_cast<volatile int*>(&bk->failed)) return;
-
-  // ---- C: phi (local rows), varphi (all columns), a, b + pending partials ---
-  {
-    const T coef = *reinterpret_cast<volatile T*>(&bk->coef);
-    const T inv_n = T(1) / static_cast<T>(t.n_global);
-    const T inv_m = T(1) / static_cast<T>(t.m_global);
-    const double drho = static_cast<double>(t.rho);
-    const bool fp = bk->record_trace != 0;
-    double part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const int64_t TT = static_cast<int64_t>(G) * kTT;
-    // rows and columns in separate loops: the column mapping (and so the
-    // rounding of the replicated column sums) must not depend on the
-    // rank's row count
-    const int64_t g0 = static_cast<int64_t>(blockIdx.x) * kTT + tid;
-    for (int64_t idx = g0; idx < m; idx += TT) {
-      {
-        const T r = __ldcg(t.r_new + idx);
-        const T ph_old = t.phi[idx];
-        const T ai = t.a[idx];
-        const T ph = (ai - T(2) * r + coef) * inv_n;  // solver.hpp:280-282
-        t.phi[idx] = ph;
-        t.a[idx] = ai - r;  // solver.hpp:287
-        part[0] += static_cast<double>(t.p[idx]) * static_cast<double>(ph) / drho;
-        if (fp) {
-          const double d = static_cast<double>(ph) - static_cast<double>(ph_old);
-          part[1] += d * d;
-          part[2] += d;
-          part[3] += d * (static_cast<double>(r) - static_cast<double>(t.r_old[idx]));
-        }
-      }
-    }
-    for (int64_t j = g0; j < n; j += TT) {
-      {
-        const T sv = __ldcg(t.s_new + j);
-        const T vp_old = t.varphi[j];
-        const T bj = t.b[j];
-        const T vp = (bj - T(2) * sv + coef) * inv_m;  // solver.hpp:283-285
-        t.varphi[j] = vp;
-        t.b[j] = bj - sv;  // solver.hpp:288
-        part[4] += static_cast<double>(t.q[j]) * static_cast<double>(vp) / drho;
-        if (fp) {
-          const double d = static_cast<double>(vp) - static_cast<double>(vp_old);
-          part[5] += d * d;
-          part[6] += d;
-          part[7] += d * (static_cast<double>(sv) - static_cast<double>(t.s_old[j]));
-        }
-      }
-    }
-    store_partials<double, 8>(part, dpart, 0, shD);
-  }
-}
-
-// pause / finish helpers: the pending update partials of the last iteration
-template <class T>
-__global__ void __launch_bounds__(kTT) shard_pending_local_kernel(const TailArgs<T> t,
-                                                                  const double* dpart, int G,
-                                                                  double* out4) {
-  __shared__ double shD[16 * kTW];
-  Book<T>* bk = t.book;
-  const bool pend = *reinterpret_cast<volatile int*>(&bk->pend_valid) != 0;
-  double d4[4];
-  totals<double, 4>(dpart, G, 0, d4, shD);
-  if (threadIdx.x == 0)
-    for (int q = 0; q < 4; ++q) out4[q] = pend ? d4[q] : 0.0;
-}
-
-template <class T>
-__global__ void __launch_bounds__(kTT) shard_pending_patch_kernel(const TailArgs<T> t,
-                                                                  const double* dpart, int G,
-                                                                  const double* glob4) {
-  __shared__ double shD[16 * kTW];
-  Book<T>* bk = t.book;
-  if (!*reinterpret_cast<volatile int*>(&bk->pend_valid)) return;
-  double c4[4];
-  totals<double, 4>(dpart, G, 4, c4, shD);
-  if (threadIdx.x == 0) {
-    Book<T> lb = *bk;
-    const double d8[8] = {glob4[0], glob4[1], glob4[2], glob4[3], c4[0], c4[1], c4[2], c4[3]};
-    const bool paused = lb.confirm && lb.stop == 2;
-    patch_pending<T>(&lb, t, d8);
-    if (paused) gate_recheck<T>(&lb);  // exact gap (replicated on every rank)
-    *bk = lb;
-  }
-}
-
-template <class T>
 __global__ void __launch_bounds__(kTT) tail_finalize_kernel(const TailArgs<T> t) {
   Book<T>* bk = t.book;
   if (threadIdx.x != 0 || !*reinterpret_cast<volatile int*>(&bk->pend_valid)) return;
@@ -1196,8 +969,6 @@ int tail_grid(int device) {
   // that is a deadlock.  The tails ask for the maximum carveout, K1's.
   cudaFuncSetAttribute(tail_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
                        cudaSharedmemCarveoutMaxShared);
-  cudaFuncSetAttribute(shard_tail_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                       cudaSharedmemCarveoutMaxShared);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tail_kernel<T>, kTT, 0);
   // one CTA per SM: the last CTA reduces half as many partial rows; measured
   // 35 vs 39 us per iteration at 1000^2 fp64, equal at 10k^2 (r1n)
@@ -1226,6 +997,11 @@ cudaError_t launch_tail(const TailArgs<T>& t, T* cpart, double* dpart, unsigned*
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = t.pdl ? 2 : 1;  // t.pdl: a programmatic dependent of the sweep
+  // test aid: several shards of ONE process on ONE device run their tails
+  // concurrently; the driver does not overlap two cooperative grids, so the
+  // in-process test launches ordinary grids small enough to be co-resident
+  const char* nc = std::getenv("DROTB_TAIL_NONCOOP");
+  if (nc && nc[0] == '1' && t.x.world > 1) cfg.numAttrs = 0;
   count_launch();
   (void)cpart;
   (void)dpart;
@@ -1247,55 +1023,6 @@ template void launch_xallreduce<double>(const double*, double*, int64_t, int, ch
 template void launch_xallreduce<int32_t>(const int32_t*, int32_t*, int64_t, int, char* const*,
                                          int, int, int64_t, int64_t, unsigned long long,
                                          cudaStream_t);
-
-template <class T>
-cudaError_t launch_shard_tail(const TailArgs<T>& t, T* cpart, double* dpart, unsigned* bar,
-                              const XArgs& x, int grid, cudaStream_t st) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(grid));
-  cfg.blockDim = dim3(kTT);
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  // test aid: several shards of ONE process on ONE device run their tails
-  // concurrently; the driver does not overlap two cooperative grids, so the
-  // in-process test launches ordinary grids small enough to be co-resident
-  const char* nc = std::getenv("DROTB_TAIL_NONCOOP");
-  const bool noncoop = nc && nc[0] == '1';
-  if (noncoop) cfg.numAttrs = 0;
-  count_launch();
-  return cudaLaunchKernelEx(&cfg, shard_tail_kernel<T>, t, cpart, dpart, bar, x);
-}
-
-template <class T>
-void launch_shard_pending_local(const TailArgs<T>& t, const double* dpart, int grid,
-                                double* out4, cudaStream_t st) {
-  shard_pending_local_kernel<T><<<1, kTT, 0, st>>>(t, dpart, grid, out4);
-  count_launch();
-}
-
-template <class T>
-void launch_shard_pending_patch(const TailArgs<T>& t, const double* dpart, int grid,
-                                const double* glob4, cudaStream_t st) {
-  shard_pending_patch_kernel<T><<<1, kTT, 0, st>>>(t, dpart, grid, glob4);
-  count_launch();
-}
-
-template cudaError_t launch_shard_tail<float>(const TailArgs<float>&, float*, double*,
-                                              unsigned*, const XArgs&, int, cudaStream_t);
-template cudaError_t launch_shard_tail<double>(const TailArgs<double>&, double*, double*,
-                                               unsigned*, const XArgs&, int, cudaStream_t);
-template void launch_shard_pending_local<float>(const TailArgs<float>&, const double*, int,
-                                                double*, cudaStream_t);
-template void launch_shard_pending_local<double>(const TailArgs<double>&, const double*, int,
-                                                 double*, cudaStream_t);
-template void launch_shard_pending_patch<float>(const TailArgs<float>&, const double*, int,
-                                                const double*, cudaStream_t);
-template void launch_shard_pending_patch<double>(const TailArgs<double>&, const double*, int,
-                                                 const double*, cudaStream_t);
 
 template <class T>
 void launch_tail_finalize(const TailArgs<T>& t, const double* dpart, int grid, cudaStream_t st) {
