@@ -362,9 +362,13 @@ def run_b200(args, rank, world, local_rank):
     # ---- config C2 in fp64 (the north_star keeps fp32 and fp64) -------------
     if world == 1 and rank == 0 and not args.no_f64:
         out["c2_f64"] = c2_f64(drot, torch, m, n)
-    # ---- config C5 at N = 1: m = n = 100 000 fp32 (X + C = 80 GB) ----------
+    # ---- config C5: m = n = 100 000 fp32 (X + C = 80 GB) ---------------------
     if world == 1 and rank == 0 and not args.no_c5:
         out["c5_single_gpu"] = c5_single(args, drot, torch)
+    if world > 1 and not args.no_c5:
+        c5 = c5_strong(args, drot, torch, dist, rank, world, local_rank)
+        if out is not None:
+            out["c5_strong"] = c5
     # ---- e2e through the public API with host buffers -----------------------
     if not args.no_e2e:
         e2e = run_e2e(args, drot, torch, m, n, local_rank)
@@ -506,14 +510,70 @@ def c5_single(args, drot, torch, size=100000, iters=20):
             "setup_s_generation_validation_init": setup, "timed_iterations": iters}
 
 
+def c5_strong(args, drot, torch, dist, rank, world, local_rank, size=100000, iters=10):
+    """The north_star scaling config (BASELINE configs[4]): m = n = 10^5 fp32
+    Gaussian, rows sharded over the N GPUs (strong scaling; each rank
+    generates its rows on the device), `iters` timed iterations after 2
+    warm-up ones; CUDA events on each rank's stream, max over ranks.  Per-GPU
+    HBM rate = the rank's algorithmic bytes (2.5 * 4 * m_rank * n per
+    iteration) / time."""
+    cfg = drot.DrotConfig(tol_primal=-1.0, max_iters=10 ** 12, device=local_rank)
+    free, _ = torch.cuda.mem_get_info()
+    r0, r1 = drot.shard_rows(size, world, rank)
+    need = 2 * 4 * (r1 - r0) * size * 1.05
+    ok = torch.tensor([1.0 if free >= need else 0.0],
+                      device="cpu" if os.environ.get("DROTB_BENCH_SHARE_GPU") == "1" else "cuda")
+    if dist is not None:
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if float(ok.item()) < 1.0:
+        return {"skipped": f"a rank needs {need / 1e9:.0f} GB, {free / 1e9:.0f} GB free"}
+    sess = make_shard(drot, dist, args, size, size, np.float32, cfg, rank, world)
+    stream = torch.cuda.Stream()
+    sess.set_stream(stream.cuda_stream)
+    sess.gen_gaussian(5.0, 0, "dyadic")
+    sess.init()
+    sess.enqueue(2)
+    sess.prepare(iters)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    sess.enqueue(iters)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    if dist is not None:
+        share = os.environ.get("DROTB_BENCH_SHARE_GPU") == "1"
+        t = torch.tensor([ms], device="cpu" if share else "cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    sess.close()
+    peak, _ = measured_hbm_peak()
+    rank_bytes = 2.5 * 4 * (r1 - r0) * size
+    return {"config": f"C5 {size}x{size} fp32 Gaussian seed 0 (rows generated on each rank's "
+                      f"device), dyadic-uniform marginals, {world} GPU(s), rows sharded "
+                      "(strong scaling)",
+            "ms_per_iteration": ms, "iterations_per_s": 1e3 / ms,
+            "rank0_rows": r1 - r0, "hbm_gbs_per_gpu_rank0": rank_bytes / (ms / 1e3) / 1e9,
+            "frac_of_peak_per_gpu_rank0": rank_bytes / (ms / 1e3) / 1e9 / peak,
+            "hbm_gbs_aggregate": 2.5 * 4 * size * size / (ms / 1e3) / 1e9,
+            "timed_iterations": iters,
+            "time_to_tol": "not run by default (~1e5+ iterations at this size): "
+                           "scripts/c5_time_to_tol.py under torchrun"}
+
+
 def time_to_tol_c2(args, drot, torch, dist, m, n, m_global, rank, world, local_rank):
     """Time-to-1e-4 (BASELINE metric) on the headline C2 instance: the full
     gated solve loop (reference defaults: rho0 = 2, tol 1e-4 x 3, skip_cost,
     exact confirm) from X0 = p q^T until the device-side gate + confirm stop
-    it, capped at --ttt-max-iters.  At N > 1 the same row-sharded
-    (N*size) x size problem as the throughput run.  Device time = CUDA events
-    on the session stream around run(), max over ranks."""
+    it, capped at --ttt-max-iters.  At N > 1 the SAME size x size instance,
+    row-sharded over the N GPUs (strong scaling): the sharded solve is
+    bit-identical to the one-GPU solve, so the iteration count is the N = 1
+    count and the time is directly comparable.  Device time = CUDA events on
+    the session stream around run(), max over ranks."""
     cfg = drot.DrotConfig(max_iters=args.ttt_max_iters, record_trace=False, device=local_rank)
+    m_global = m
     if world > 1:
         sess = make_shard(drot, dist, args, m_global, n, np.float32, cfg, rank, world)
     else:
@@ -542,7 +602,7 @@ def time_to_tol_c2(args, drot, torch, dist, m, n, m_global, rank, world, local_r
     sess.close()
     return {"config": f"C2 {m_global}x{n} fp32 Gaussian seed 0, dyadic-uniform marginals, "
                       f"reference defaults (rho0=2, tol 1e-4 x3), {world} GPU(s)"
-                      + (", row-sharded" if world > 1 else ""),
+                      + (", row-sharded (same instance as N = 1)" if world > 1 else ""),
             "seconds": sec, "wall_seconds_rank0": wall, "iterations": iters,
             "status": st.name, "ms_per_iteration": 1e3 * sec / max(iters, 1),
             "objective": rep.objective, "r_primal": rep.r_primal, "r_dual": rep.r_dual,
