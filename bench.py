@@ -648,7 +648,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--size", type=int, default=10000)
     ap.add_argument("--order", default="fast", choices=["fast", "reference"])
-    ap.add_argument("--e2e-iters", type=int, default=200)
+    ap.add_argument("--e2e-iters", type=int, default=1000)
     ap.add_argument("--cpu-iters", type=int, default=20)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -77,77 +77,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_ASYNC_MINB)
   const int64_t it_stamp = a.stamps ? *reinterpret_cast<const volatile int64_t*>(a.iter) : 0;
   if (a.stamps && threadIdx.x == 0) timeline_point(a.stamps, it_stamp, 0, t_entry);
 
-  T ph[R], u[R];
-  if (nvalid > 0) {
-    unpack(ld_keep(reinterpret_cast<const V*>(a.phi + row0)), ph);
-  } else {
-#pragma unroll
-    for (int t = 0; t < R; ++t) ph[t] = T(0);
-  }
-#pragma unroll
-  for (int t = 0; t < R; ++t) u[t] = T(0);
-  PassAcc<T> acc{T(0), T(0), T(0), T(0), T(0), false};
-  const bool full = __all_sync(0xffffffffu, nvalid == R);
-  if (a.pdl) {
-    if (full)
-      pass_tile_async<T, MODE, DUAL, DX, false, true>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc,
-                                                      wbuf, ring, lane);
-    else
-      pass_tile_async<T, MODE, DUAL, DX, true, true>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc,
-                                                     wbuf, ring, lane);
-  } else {
-    if (full)
-      pass_tile_async<T, MODE, DUAL, DX, false>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc, wbuf,
-                                                ring, lane);
-    else
-      pass_tile_async<T, MODE, DUAL, DX, true>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc, wbuf,
-                                               ring, lane);
-  }
-  if (a.fx) {
-#pragma unroll
-    for (int t = 0; t < R; ++t)
-      if (t < nvalid) red_fx<T>(a.ufx, row0 + t, a.ld, u[t]);
-  } else if (nvalid > 0) {
-    st_keep(reinterpret_cast<V*>(a.ustrip + gc * a.ld + row0), pack4(u), a.l2hint);
-  }
-
-  acc.cost = warp_sum(acc.cost);
-  acc.prev = warp_sum(acc.prev);
-  acc.dual = warp_sum(acc.dual);
-  acc.dx = warp_sum(acc.dx);
-  acc.mx = warp_max(acc.mx);
-  const bool wbad = __any_sync(0xffffffffu, acc.bad);
-  if (lane == 0) {
-    acc.bad = wbad;
-    wacc[warp] = acc;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    PassPartial<T> out{T(0), T(0), T(0), T(0), T(0), 0, 0};
-#pragma unroll
-    for (int w = 0; w < kWarpsPerCta; ++w) {
-      out.cost += wacc[w].cost;
-      out.prev += wacc[w].prev;
-      out.dual += wacc[w].dual;
-      out.dx += wacc[w].dx;
-      out.max_abs = fmax(out.max_abs, wacc[w].mx);
-      out.bad |= wacc[w].bad ? 1 : 0;
-    }
-    if (a.xacc) {  // exact accumulators (the per-CTA sums rounded, then summed exactly)
-      red_hilo(a.xacc + 2 * kXaCost, to_hilo(static_cast<double>(out.cost)));
-      red_hilo(a.xacc + 2 * kXaPrev, to_hilo(static_cast<double>(out.prev)));
-      red_hilo(a.xacc + 2 * kXaDual, to_hilo(static_cast<double>(out.dual)));
-      red_hilo(a.xacc + 2 * kXaDx, to_hilo(static_cast<double>(out.dx)));
-      atomicMax(reinterpret_cast<unsigned long long*>(a.xacc + kXaMax),
-                static_cast<unsigned long long>(
-                    __double_as_longlong(static_cast<double>(out.max_abs))));
-      if (out.bad) red_add_u64(a.xacc + kXaBad, 1);
-    } else {
-      st_partial_keep(a.partials + static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x,
-                      out);
-    }
-    if (a.stamps) timeline_point(a.stamps, it_stamp, 1, global_ns());
-  }
+  k1_tile<T, MODE, DUAL, DX>(a, blockIdx.x, blockIdx.y, gridDim.x, dyn_smem, wacc, a.pdl != 0,
+                             it_stamp);
 }
 
 // The shared-memory opt-in is a per-device function attribute: set it once

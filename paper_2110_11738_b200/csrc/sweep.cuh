@@ -578,6 +578,102 @@ __device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0
 }
 
 
+// One K1 tile (row block bx, column tile by): the body of pass_kernel_async
+// after its prologue, shared with the small-problem solver kernel (tail.cu),
+// which walks the same tiles -- so both produce the same per-tile sums.
+// primed: the first ring stages were issued (ring_prime) by the caller.
+template <class T, int MODE, bool DUAL, bool DX>
+__device__ __forceinline__ void k1_tile(const PassArgs<T>& a, int64_t bx, int64_t by,
+                                        int64_t gridx, unsigned char* dyn_smem,
+                                        PassAcc<T>* wacc, bool primed, int64_t it_stamp) {
+  using V = typename V16<T>::type;
+  constexpr int R = 16 / sizeof(T);
+  constexpr int ROWS_W = 32 * R;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr size_t ring_v = static_cast<size_t>(kAsyncS) * 2 * kAsyncG * 32;  // V per warp
+  V* ring = reinterpret_cast<V*>(dyn_smem) + warp * ring_v;
+  T* wbuf = reinterpret_cast<T*>(reinterpret_cast<V*>(dyn_smem) + kWarpsPerCta * ring_v) +
+            warp * kChunkCols * ROWS_W;
+  const int64_t wrow0 = (bx * kWarpsPerCta + warp) * ROWS_W;
+  const int64_t row0 = wrow0 + static_cast<int64_t>(lane) * R;
+  const int64_t gc = by;
+  const int64_t c0 = gc * a.tc;
+  const int64_t c1 = imin64(a.n, c0 + a.tc);
+  const int64_t nv = a.m - row0;
+  const int nvalid = nv <= 0 ? 0 : (nv >= R ? R : static_cast<int>(nv));
+  T ph[R], u[R];
+  if (nvalid > 0) {
+    unpack(ld_keep(reinterpret_cast<const V*>(a.phi + row0)), ph);
+  } else {
+#pragma unroll
+    for (int t = 0; t < R; ++t) ph[t] = T(0);
+  }
+#pragma unroll
+  for (int t = 0; t < R; ++t) u[t] = T(0);
+  PassAcc<T> acc{T(0), T(0), T(0), T(0), T(0), false};
+  const bool full = __all_sync(0xffffffffu, nvalid == R);
+  if (primed) {
+    if (full)
+      pass_tile_async<T, MODE, DUAL, DX, false, true>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc,
+                                                      wbuf, ring, lane);
+    else
+      pass_tile_async<T, MODE, DUAL, DX, true, true>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc,
+                                                     wbuf, ring, lane);
+  } else {
+    if (full)
+      pass_tile_async<T, MODE, DUAL, DX, false>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc, wbuf,
+                                                ring, lane);
+    else
+      pass_tile_async<T, MODE, DUAL, DX, true>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc, wbuf,
+                                               ring, lane);
+  }
+  if (a.fx) {
+#pragma unroll
+    for (int t = 0; t < R; ++t)
+      if (t < nvalid) red_fx<T>(a.ufx, row0 + t, a.ld, u[t]);
+  } else if (nvalid > 0) {
+    st_keep(reinterpret_cast<V*>(a.ustrip + gc * a.ld + row0), pack4(u), a.l2hint);
+  }
+
+  acc.cost = warp_sum(acc.cost);
+  acc.prev = warp_sum(acc.prev);
+  acc.dual = warp_sum(acc.dual);
+  acc.dx = warp_sum(acc.dx);
+  acc.mx = warp_max(acc.mx);
+  const bool wbad = __any_sync(0xffffffffu, acc.bad);
+  if (lane == 0) {
+    acc.bad = wbad;
+    wacc[warp] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    PassPartial<T> out{T(0), T(0), T(0), T(0), T(0), 0, 0};
+#pragma unroll
+    for (int w = 0; w < kWarpsPerCta; ++w) {
+      out.cost += wacc[w].cost;
+      out.prev += wacc[w].prev;
+      out.dual += wacc[w].dual;
+      out.dx += wacc[w].dx;
+      out.max_abs = fmax(out.max_abs, wacc[w].mx);
+      out.bad |= wacc[w].bad ? 1 : 0;
+    }
+    if (a.xacc) {  // exact accumulators (the per-CTA sums rounded, then summed exactly)
+      red_hilo(a.xacc + 2 * kXaCost, to_hilo(static_cast<double>(out.cost)));
+      red_hilo(a.xacc + 2 * kXaPrev, to_hilo(static_cast<double>(out.prev)));
+      red_hilo(a.xacc + 2 * kXaDual, to_hilo(static_cast<double>(out.dual)));
+      red_hilo(a.xacc + 2 * kXaDx, to_hilo(static_cast<double>(out.dx)));
+      atomicMax(reinterpret_cast<unsigned long long*>(a.xacc + kXaMax),
+                static_cast<unsigned long long>(
+                    __double_as_longlong(static_cast<double>(out.max_abs))));
+      if (out.bad) red_add_u64(a.xacc + kXaBad, 1);
+    } else {
+      st_partial_keep(a.partials + gc * gridx + bx, out);
+    }
+    if (a.stamps) timeline_point(a.stamps, it_stamp, 1, global_ns());
+  }
+  __syncthreads();  // wacc and the ring / staging buffers are reused by the next tile
+}
+
 // ---------------------------------------------------------------------------
 // Solve-loop scalar logic shared by the tail kernels and the persistent
 // solver kernel (operates on a Book<T>, in global or shared memory)

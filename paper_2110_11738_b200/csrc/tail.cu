@@ -358,10 +358,11 @@ __device__ __forceinline__ void xrank_barrier(const XArgs& x, int par, int b, un
 // red_cta_hilo with a destination per sum: sums whose bit is set in
 // all_mask (row-side sums of this rank's rows) go to every rank's
 // accumulator, the others (replicated column-side sums) to this rank's only
-template <int K>
+template <int NT, int K>
 __device__ __forceinline__ void red_cta_hilo_x(HiLo (&v)[K], int word0, int all_mask,
                                                const XArgs& x, int par, long long* local,
                                                long long* sh) {
+  constexpr int kTW = NT / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
@@ -391,10 +392,12 @@ __device__ __forceinline__ void red_cta_hilo_x(HiLo (&v)[K], int word0, int all_
 
 // red_cta_hilo over the update warps only (warps kUW..): named barrier 1,
 // so the sums leave while warp 0 still runs the scalar logic
-template <int K>
+template <int NT, int K>
 __device__ __forceinline__ void red_upd_hilo(HiLo (&v)[K], int word0, int all_mask,
                                              const XArgs& x, int par, long long* local,
                                              long long* sh) {
+  constexpr int kTW = NT / 32;
+  constexpr int kUT = NT - 32 * kUW;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
@@ -434,16 +437,17 @@ __device__ __forceinline__ T fx_take(long long* fxa, int64_t i, int64_t len) {
   return static_cast<T>(static_cast<double>(hi) * kFxInv + static_cast<double>(lo) * kFxLoInv);
 }
 
-template <class T>
-__global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned* bar) {
+// One iteration's tail on NT-thread CTAs (the whole grid): the body of
+// tail_kernel, and of the small-problem solver's loop.  Returns whether the
+// solve stops (the decision every CTA holds identically).
+template <class T, int NT>
+__device__ __forceinline__ bool tail_body(const TailArgs<T>& t, unsigned* bar) {
   using V = typename V16<T>::type;
   constexpr int R = 16 / sizeof(T);
   constexpr int BW = static_cast<int>(sizeof(Book<T>) / 8);
+  constexpr int TW = NT / 32;            // warps per CTA
+  constexpr int UT = NT - 32 * kUW;      // update threads per CTA
   Book<T>* bk = t.book;
-  // the next sweep (a programmatic dependent) may be scheduled now; it waits
-  // in griddepcontrol.wait for this grid's completion
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // (t.pdl: after the sweep)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x;
   const int par = t.tpar & 1;
@@ -465,7 +469,7 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned
   }
   const int64_t it_stamp = t.stamps ? *reinterpret_cast<volatile int64_t*>(&bk->iter) : 0;
   TAIL_STAMP(2);
-  if (*reinterpret_cast<volatile int*>(&bk->stop)) return;
+  if (*reinterpret_cast<volatile int*>(&bk->stop)) return true;
   if (multi) {
     // row shards: this rank's sweep left fixed-point column partials in vfx
     // and its scalars in xloc -- add both into every rank's sums (integer
@@ -473,8 +477,8 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned
     // count or order), then a cross-rank barrier
     const int64_t n_ = t.n;
     const int vw = X.vwords;
-    for (int64_t j = static_cast<int64_t>(blockIdx.x) * kTT + tid; j < n_;
-         j += static_cast<int64_t>(gridDim.x) * kTT) {
+    for (int64_t j = static_cast<int64_t>(blockIdx.x) * NT + tid; j < n_;
+         j += static_cast<int64_t>(gridDim.x) * NT) {
       for (int w = 0; w < vw; ++w) {
         const long long q = __ldcg(t.vfx + w * n_ + j);
         t.vfx[w * n_ + j] = 0;
@@ -501,10 +505,10 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned
     }
     xrank_barrier(X, par, 0, static_cast<unsigned>(X.world) * gridDim.x, nullptr, 0);
   }
-  __shared__ __align__(16) T red[kTT * R];  // strip merge partition sums [P][CV][R]
+  __shared__ __align__(16) T red[NT * R];  // strip merge partition sums [P][CV][R]
   __shared__ Book<T> sbk;
-  __shared__ long long shL[2 * 8 * kTW];
-  __shared__ long long shP[2 * 8 * kTW];  // update sums (named-barrier reduction)
+  __shared__ long long shL[2 * 8 * 8];
+  __shared__ long long shP[2 * 8 * 8];  // update sums (named-barrier reduction)
   __shared__ double s_tot[24];
   __shared__ double s_patch[3];
   __shared__ int s_gate_ran, s_pvalid;
@@ -517,7 +521,7 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned
   const bool fp = bk->record_trace != 0;  // configuration: constant over the solve
 
   // this CTA's balanced range of [0, m + n): the update, and the merge in
-  // fixed-point mode; update thread ut takes e0 + ut, e0 + ut + kUT, ...
+  // fixed-point mode; update thread ut takes e0 + ut, e0 + ut + UT, ...
   const int64_t E = m + n;
   const int64_t e0 = static_cast<int64_t>(blockIdx.x) * E / G;
   const int64_t e1 = static_cast<int64_t>(blockIdx.x + 1) * E / G;
@@ -568,7 +572,7 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned
     // complete after the sweep: one read (and reset) per index, by the
     // update thread that owns it
     if (ut >= 0) {
-      for (int64_t e = ef; e < e1; e += kUT) {
+      for (int64_t e = ef; e < e1; e += UT) {
         const bool first = e == ef;
         if (e < m) {
           const T pi = first ? f_pq : ld_keep(t.p + e);
@@ -597,9 +601,9 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned
     const int64_t v0 = static_cast<int64_t>(blockIdx.x) * NV / G;
     const int64_t v1 = static_cast<int64_t>(blockIdx.x + 1) * NV / G;
     const int64_t cnt = v1 - v0;
-    int P = cnt > 0 ? static_cast<int>(kTT / cnt) : 8;
+    int P = cnt > 0 ? static_cast<int>(NT / cnt) : 8;
     P = P < 1 ? 1 : (P > 8 ? 8 : P);
-    const int CV = kTT / P;
+    const int CV = NT / P;
     T* redv = red;
     for (int64_t c0 = v0; c0 < v1; c0 += CV) {
       const int64_t vec = c0 + tid % CV;
@@ -665,7 +669,7 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned
     }
   }
   TAIL_STAMP(8);
-  red_cta_hilo_x<7>(hm, 2 * kXaSumR, 0x1B, X, par, xa, shL);
+  red_cta_hilo_x<NT, 7>(hm, 2 * kXaSumR, 0x1B, X, par, xa, shL);
   TAIL_STAMP(3);
   // ---- barrier 1: every CTA reads the exact totals -------------------------
   if (multi)
@@ -736,7 +740,7 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned
     const T inv_n = T(1) / static_cast<T>(t.n_global);
     const T inv_m = T(1) / static_cast<T>(t.m_global);
     const double drho = static_cast<double>(t.rho);
-    for (int64_t e = ef; e < e1; e += kUT) {
+    for (int64_t e = ef; e < e1; e += UT) {
       const bool first = e == ef && t.fx;
       if (e < m) {
         const T r = first ? f_rs : ld_keep_cg(t.r_new + e);
@@ -774,7 +778,7 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned
       }
     }
   }
-  if (warp >= kUW && !pass_bad) red_upd_hilo<8>(hp, kXaP, 0x0F, X, par, xa, shP);
+  if (warp >= kUW && !pass_bad) red_upd_hilo<NT, 8>(hp, kXaP, 0x0F, X, par, xa, shP);
   __syncthreads();
   if (tid == 0) {
     if (fg && s_pvalid && !s_gate_ran) {  // gate did not run: the patch stands
@@ -790,10 +794,10 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned
   TAIL_STAMP(4);
   __syncthreads();
   TAIL_STAMP(5);
-  if (sbk.failed) return;  // non-finite pass
+  if (sbk.failed) return true;  // non-finite pass
   if (fg && (!sbk.confirm || sbk.stop == 1)) {
     TAIL_STAMP(6);
-    return;
+    return sbk.stop != 0;
   }
   // ---- barrier 2 (only when needed): exact dual value / exact gate ----------
   if (multi)
@@ -815,18 +819,18 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned
   }
   book_store_cta0(bk, &sbk);
   __syncthreads();
-  if (!sbk.confirm || sbk.stop == 1) return;
+  if (!sbk.confirm || sbk.stop == 1) return sbk.stop != 0;
 
   // ---- C: exact confirm report (only when the gate fired) ------------------
   {
     const bool folded = sbk.folded != 0;
     const double drho = static_cast<double>(t.rho);
-    const int64_t ngx = (m + int64_t(kTT) * R - 1) / (int64_t(kTT) * R);
+    const int64_t ngx = (m + int64_t(NT) * R - 1) / (int64_t(NT) * R);
     const int64_t ncs = imin64(n, (2 * static_cast<int64_t>(G) + ngx - 1) / ngx);
     HiLo hr[2] = {HiLo{0, 0}, HiLo{0, 0}};
     for (int64_t unit = blockIdx.x; unit < ngx * ncs; unit += G) {
       const int64_t rx = unit % ngx, cs = unit / ngx;
-      const int64_t row0 = (rx * kTT + tid) * R;
+      const int64_t row0 = (rx * NT + tid) * R;
       if (row0 >= m) continue;
       const int nvalid = static_cast<int>(imin64(R, m - row0));
       double mu[R];
@@ -844,7 +848,7 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned
             report_elem_exact<T>(xv[k], cv[k], mu[k], nu_j, t.rho, folded, hr);
       }
     }
-    red_cta_hilo_x<2>(hr, kXaR, 0x3, X, par, xa, shL);
+    red_cta_hilo_x<NT, 2>(hr, kXaR, 0x3, X, par, xa, shL);
   }
   if (multi)
     xrank_barrier(X, par, 3, static_cast<unsigned>(X.world) * G, nullptr, 0);
@@ -854,6 +858,79 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned
   __syncthreads();
   if (tid == 0) report_decide<T>(&sbk, s_tot[0], s_tot[1], 0);
   book_store_cta0(bk, &sbk);
+  return sbk.stop != 0;
+}
+
+template <class T>
+__global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned* bar) {
+  // the next sweep (a programmatic dependent) may be scheduled now; it waits
+  // in griddepcontrol.wait for this grid's completion
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (t.pdl: after the sweep)
+  tail_body<T, kTT>(t, bar);
+}
+
+// ---------------------------------------------------------------------------
+// KS -- small problems (X and C resident in L2): the whole loop in ONE
+// cooperative launch of co-resident 128-thread CTAs, `nb` iterations per
+// launch.  Per iteration: the K1 tiles (k1_tile: the same tiles, in any
+// order, with the same per-tile sums as pass_kernel_async), a grid barrier,
+// the tail (tail_body on 128-thread CTAs), a grid barrier.  Every cross-CTA
+// sum is exact, so the trajectory is bit-identical to the per-launch loop;
+// what goes away is two kernel boundaries and their launch gaps per
+// iteration, which dominate below ~2000^2.
+// ---------------------------------------------------------------------------
+constexpr int kCtrSmall = 512;  // bar word of the loop's grid barriers (host-reset per launch)
+
+__device__ __forceinline__ void grid_barrier_mono(unsigned* ctr, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    red_release_add(ctr, 1u);
+    while (static_cast<int>(ld_relaxed(ctr) - target) < 0) {
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+template <class T, int MODE, bool DUAL, bool DX>
+__device__ __forceinline__ void small_sweep(const PassArgs<T>& pa, const SmallArgs& sa,
+                                            unsigned char* dyn_smem, PassAcc<T>* wacc) {
+  for (int64_t tile = blockIdx.x; tile < sa.n_tiles; tile += gridDim.x)
+    k1_tile<T, MODE, DUAL, DX>(pa, tile % sa.gx, tile / sa.gx, sa.gx, dyn_smem, wacc, false, 0);
+}
+
+template <class T>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, 3)
+    small_solve_kernel(const PassArgs<T> pa0, const PassArgs<T> pa1, const TailArgs<T> ta0,
+                       const TailArgs<T> ta1, unsigned* bar, const SmallArgs sa) {
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  __shared__ PassAcc<T> wacc[kWarpsPerCta];
+  const unsigned G = gridDim.x;
+  for (int b = 0; b < sa.nb; ++b) {
+    const int par = b & 1;
+    const PassArgs<T>& pa = par ? pa1 : pa0;
+    if (*reinterpret_cast<const volatile int*>(pa.stop)) break;  // uniform: the Book
+    const int mode = sa.mode[par];
+    const bool dual = sa.dual != 0, dx = sa.dx != 0;
+    if (mode == kSkip) {
+      small_sweep<T, kSkip, false, false>(pa, sa, dyn_smem, wacc);
+    } else if (mode == kFold) {
+      if (dx) small_sweep<T, kFold, true, true>(pa, sa, dyn_smem, wacc);
+      else small_sweep<T, kFold, true, false>(pa, sa, dyn_smem, wacc);
+    } else if (mode == kPlain0) {
+      if (dual && dx) small_sweep<T, kPlain0, true, true>(pa, sa, dyn_smem, wacc);
+      else if (dual) small_sweep<T, kPlain0, true, false>(pa, sa, dyn_smem, wacc);
+      else small_sweep<T, kPlain0, false, false>(pa, sa, dyn_smem, wacc);
+    } else {
+      if (dual && dx) small_sweep<T, kPlain1, true, true>(pa, sa, dyn_smem, wacc);
+      else if (dual) small_sweep<T, kPlain1, true, false>(pa, sa, dyn_smem, wacc);
+      else small_sweep<T, kPlain1, false, false>(pa, sa, dyn_smem, wacc);
+    }
+    grid_barrier_mono(bar + kCtrSmall, G * static_cast<unsigned>(2 * b + 1));
+    if (tail_body<T, kWarpsPerCta * 32>(par ? ta1 : ta0, bar)) break;
+    grid_barrier_mono(bar + kCtrSmall, G * static_cast<unsigned>(2 * b + 2));
+  }
 }
 
 }  // namespace
@@ -1042,5 +1119,50 @@ template cudaError_t launch_tail<float>(const TailArgs<float>&, float*, double*,
                                         cudaStream_t);
 template cudaError_t launch_tail<double>(const TailArgs<double>&, double*, double*, unsigned*,
                                          int, cudaStream_t);
+
+
+template <class T>
+int small_grid(int device) {
+  int sms = 0, per = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  const int smem = static_cast<int>(async_smem_bytes<T>());
+  cudaFuncSetAttribute(small_solve_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, small_solve_kernel<T>,
+                                                    kWarpsPerCta * 32, smem) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 0;
+  }
+  return sms * per;
+}
+
+template <class T>
+cudaError_t launch_small_solve(const PassArgs<T>& pa0, const PassArgs<T>& pa1,
+                               const TailArgs<T>& ta0, const TailArgs<T>& ta1, unsigned* bar,
+                               const SmallArgs& sa, int grid, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(bar + kCtrSmall, 0, sizeof(unsigned), st);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kWarpsPerCta * 32);
+  cfg.dynamicSmemBytes = async_smem_bytes<T>();
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  count_launch();
+  return cudaLaunchKernelEx(&cfg, small_solve_kernel<T>, pa0, pa1, ta0, ta1, bar, sa);
+}
+template int small_grid<float>(int);
+template int small_grid<double>(int);
+template cudaError_t launch_small_solve<float>(const PassArgs<float>&, const PassArgs<float>&,
+                                               const TailArgs<float>&, const TailArgs<float>&,
+                                               unsigned*, const SmallArgs&, int, cudaStream_t);
+template cudaError_t launch_small_solve<double>(const PassArgs<double>&,
+                                                const PassArgs<double>&,
+                                                const TailArgs<double>&,
+                                                const TailArgs<double>&, unsigned*,
+                                                const SmallArgs&, int, cudaStream_t);
 
 }  // namespace drotb

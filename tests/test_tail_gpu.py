@@ -131,3 +131,41 @@ def test_l2_policies_do_not_change_results(drot, dt):
     assert a[0][1] == b[0][1] == 40
     for x, y in zip(a[1:], b[1:]):
         np.testing.assert_array_equal(x, y)
+
+
+def _session_solve(drot, m, n, dt, cfg, seed, small_mb):
+    old = os.environ.get("DROTB_SMALL_MB")
+    os.environ["DROTB_SMALL_MB"] = small_mb
+    try:
+        s = drot.Session(m, n, dt, cfg)
+        s.gen_gaussian(5.0, seed, "dyadic")
+        s.init()
+        s.run()
+        st = s.status()
+        plan, mu, nu = s.plan()
+        s.close()
+    finally:
+        if old is None:
+            os.environ.pop("DROTB_SMALL_MB", None)
+        else:
+            os.environ["DROTB_SMALL_MB"] = old
+    return st, plan, mu, nu
+
+
+@pytest.mark.parametrize("dt,shape,max_iters", [(np.float64, (300, 200), 100000),
+                                                (np.float32, (500, 400), 100000),
+                                                (np.float64, (1000, 1000), 3000)])
+def test_small_solver_bitwise(drot, dt, shape, max_iters):
+    """The small-problem solver (the whole loop in one cooperative launch per
+    batch, tail.cu small_solve_kernel) against the per-launch loop: same
+    tiles, exact sums -- bit-identical status, iterations, report, plan."""
+    m, n = shape
+    cfg = drot.DrotConfig(max_iters=max_iters)
+    a = _session_solve(drot, m, n, dt, cfg, 11, "0")
+    b = _session_solve(drot, m, n, dt, cfg, 11, "1000")
+    (sa, ia, ra), (sb, ib, rb) = a[0], b[0]
+    assert sa == sb and ia == ib
+    assert (ra.objective, ra.r_primal, ra.r_dual, ra.gap) == (rb.objective, rb.r_primal,
+                                                              rb.r_dual, rb.gap)
+    for x, y in zip(a[1:], b[1:]):
+        assert np.array_equal(x, y)
