@@ -271,22 +271,6 @@ void launch_xallreduce(const U* in, U* out, int64_t count, int op, char* const* 
 template <class T>
 void launch_tail_finalize(const TailArgs<T>& t, const double* dpart, int grid, cudaStream_t st);
 
-// Small problems (tail.cu small_solve_kernel): the whole loop in one
-// cooperative launch, nb iterations; per parity the sweep mode, the pass /
-// tail arguments of iterations k0 + even and k0 + odd
-struct SmallArgs {
-  int64_t gx, n_tiles;  // the K1 tile grid (row blocks, total tiles)
-  int32_t nb;           // iterations in this launch (even)
-  int32_t mode[2];
-  int32_t dual, dx;
-};
-template <class T>
-int small_grid(int device);
-template <class T>
-cudaError_t launch_small_solve(const PassArgs<T>& pa0, const PassArgs<T>& pa1,
-                               const TailArgs<T>& ta0, const TailArgs<T>& ta1, unsigned* bar,
-                               const SmallArgs& sa, int grid, cudaStream_t st);
-
 // ---- kernel launchers (kernels.cu) ---------------------------------------
 void launch_spin(unsigned long long ns, cudaStream_t st);
 template <class T>

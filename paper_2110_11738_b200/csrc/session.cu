@@ -922,80 +922,10 @@ int Session<T>::run_timed(int64_t n_iters, double* total_ms, double* pass_ms, in
 }
 
 
-// Small problems: X and C resident in L2 (<= DROTB_SMALL_MB, default 48 MB),
-// fast order, one GPU, fixed-point sums -- the loop in one cooperative
-// launch per batch (tail.cu small_solve_kernel), bit-identical to the
-// per-launch loop.  DROTB_SMALL_MB=0 disables.
-template <class T>
-bool Session<T>::small_ok() {
-  if (!coop || exact || sharded || !fx || !xacc || tstamps) return false;
-  double mb = 48.0;
-  if (const char* e = std::getenv("DROTB_SMALL_MB")) mb = std::atof(e);
-  if (2.0 * sizeof(T) * static_cast<double>(ld) * static_cast<double>(n) > mb * 1e6) return false;
-  if (small_grid_n == 0) small_grid_n = small_grid<T>(device);
-  return small_grid_n > 0;
-}
-
-template <class T>
-int Session<T>::run_small() {
-  const int64_t nb = std::max<int64_t>(2, 2 * (std::max<int64_t>(batch_iters(), 32) / 2));
-  const int64_t limit = std::max<int64_t>(cfg.max_iters, 0) + 4 * nb + 4;
-  constexpr int R = 16 / sizeof(T);
-  SmallArgs sa{};
-  sa.gx = (m + int64_t(kWarpsPerCta) * 32 * R - 1) / (int64_t(kWarpsPerCta) * 32 * R);
-  sa.n_tiles = sa.gx * ((n + tc - 1) / tc);
-  sa.nb = static_cast<int32_t>(nb);
-  sa.dual = want_dual ? 1 : 0;
-  sa.dx = want_dx ? 1 : 0;
-  int slot = 0;
-  bool pending = false;
-  int64_t launched = 0;
-  while (true) {
-    // iterations k0 (even parity of the launch) and k0 + 1: modes, fold states
-    PassArgs<T> pa[2];
-    TailArgs<T> ta[2];
-    int64_t k = h_iter;
-    bool folded = h_folded;
-    for (int q = 0; q < 2; ++q, ++k) {
-      int mode;
-      bool folded_after;
-      RC_TRY(pass_mode(k, folded, &mode, &folded_after));
-      sa.mode[q] = mode;
-      pa[q] = pass_args(k);
-      pa[q].pdl = 0;
-      pa[q].trigger = 0;
-      pa[q].stamps = nullptr;
-      ta[q] = tail_args(k, mode, folded_after, true);
-      ta[q].stamps = nullptr;
-      folded = folded_after;
-    }
-    CUDA_TRY(launch_small_solve<T>(pa[0], pa[1], ta[0], ta[1], tbar, sa, small_grid_n, stream));
-    h_iter += nb;  // nb is even: the fold state repeats
-    launched += nb;
-    CUDA_TRY(cudaMemcpyAsync(&h_stop[slot], &book->stop, sizeof(int32_t),
-                             cudaMemcpyDeviceToHost, stream));
-    CUDA_TRY(cudaEventRecord(ev[slot], stream));
-    if (pending) {
-      CUDA_TRY(cudaEventSynchronize(ev[slot ^ 1]));
-      if (h_stop[slot ^ 1]) break;
-    }
-    pending = true;
-    slot ^= 1;
-    if (launched > limit) break;  // the device sets stop at max_iters
-  }
-  CUDA_TRY(cudaStreamSynchronize(stream));
-  Book<T> hb;
-  RC_TRY(read_book(&hb));
-  h_iter = hb.iter;  // resync (the launch after the stop ran no iteration)
-  h_folded = hb.folded != 0;
-  return 0;
-}
-
 template <class T>
 int Session<T>::run() {
   if (!initialized) return set_error(DROTB_ERRC_BAD_CONFIG, "session not initialized");
   if (sharded && xmode != 1) return run_sharded();  // NCCL: host-driven confirm pauses
-  if (small_ok()) return run_small();
   const int64_t bi = batch_iters();
   int slot = 0;
   bool pending = false;
@@ -1152,10 +1082,6 @@ template void Session<double>::release();
 template int Session<float>::create(int64_t m_, int64_t n_, const drotb_config& c, bool engine);
 template int Session<double>::create(int64_t m_, int64_t n_, const drotb_config& c, bool engine);
 template int Session<float>::setup_coop_tail();
-template bool Session<float>::small_ok();
-template bool Session<double>::small_ok();
-template int Session<float>::run_small();
-template int Session<double>::run_small();
 template int Session<double>::setup_coop_tail();
 template int64_t Session<float>::fast_tile_cols()const;
 template int64_t Session<double>::fast_tile_cols()const;

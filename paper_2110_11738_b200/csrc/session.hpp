@@ -322,10 +322,7 @@ struct Session {
   int run_sharded();
 
   int run();
-  // small problems: the whole loop in one cooperative launch per batch
-  bool small_ok();
-  int run_small();
-  int small_grid_n = 0;
+
 
   // Small transfers through pinned staging: a pageable copy blocks inside the
   // CUDA call until the stream drains, which must not happen while another

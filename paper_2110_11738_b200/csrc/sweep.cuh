@@ -423,23 +423,10 @@ constexpr int kSkipS = 2 * kAsyncS, kSkipG = kAsyncG;
 constexpr int kSkipS = kAsyncS, kSkipG = 2 * kAsyncG;
 #endif
 
-// L2 eviction policy of the streamed X / C reads: evict_first keeps the
-// small per-iteration data (strips, records, the Book, kernel code) resident
-// in L2 across the 0.4-80 GB sweep (PassArgs::l2hint; evict_normal otherwise)
-__device__ __forceinline__ uint64_t stream_policy(int evict_first) {
-  uint64_t pol;
-  if (evict_first & 5)
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  else
-    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, uint64_t pol) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(sa),
-               "l"(gmem), "l"(pol)
-               : "memory");
-}
+// The streamed X / C reads use plain cp.async.cg: the cache-hinted form
+// (an evict_first createpolicy operand, formerly DROTB_L2HINT bits 0 / 2)
+// measured slower and mis-compiled in r2 (an uninitialized policy
+// descriptor: illegal-instruction traps and wrong loads), so it is gone.
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
@@ -470,7 +457,7 @@ __device__ __forceinline__ void ring_prime(const PassArgs<T>& a, int64_t c0, int
   constexpr bool RC = MODE != kSkip;
   constexpr int S = RC ? kAsyncS : kSkipS, G = RC ? kAsyncG : kSkipG;
   constexpr int SLOTS = 2 * kAsyncG * kAsyncS / S;  // 16-B slots per lane and stage
-  const uint64_t pol = stream_policy(a.l2hint);
+  // the same copies as pass_tile_async's issue()
 #pragma unroll
   for (int st = 0; st < S - 1; ++st) {
 #pragma unroll
@@ -478,9 +465,8 @@ __device__ __forceinline__ void ring_prime(const PassArgs<T>& a, int64_t c0, int
       const int64_t col = c0 + st * G + k;
       if (col < c1 && live) {
         const int64_t off = col * a.ld + row0;
-        cp_async16_hint(ring + (st * SLOTS + k) * 32 + lane, a.xy + off, pol);
-        if (RC) cp_async16_hint(ring + (st * SLOTS + kAsyncG + k) * 32 + lane, a.cost + off,
-                                pol);
+        cp_async16(ring + (st * SLOTS + k) * 32 + lane, a.xy + off);
+        if (RC) cp_async16(ring + (st * SLOTS + kAsyncG + k) * 32 + lane, a.cost + off);
       }
     }
     cp_async_commit();
@@ -507,7 +493,6 @@ __device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0
   static_assert(SLOTS >= G * (RC ? 2 : 1), "ring slots per stage");
   const bool live = !MASK || nvalid > 0;
   T vb[S][G];
-  const uint64_t pol = stream_policy(a.l2hint);
   auto xslot = [&](int st, int k) { return ring + (st * SLOTS + k) * 32 + lane; };
   auto cslot = [&](int st, int k) { return ring + (st * SLOTS + kAsyncG + k) * 32 + lane; };
   auto issue = [&](int st, int64_t jg) {
@@ -518,17 +503,8 @@ __device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0
       if (col < c1) {
         if (live) {
           const int64_t off = col * a.ld + row0;
-          // bit 0: evict_first on X and C; bit 2: on C only (read-only here)
-          if (a.l2hint & 1)
-            cp_async16_hint(xslot(st, k), a.xy + off, pol);
-          else
-            cp_async16(xslot(st, k), a.xy + off);
-          if (RC) {
-            if (a.l2hint & 5)
-              cp_async16_hint(cslot(st, k), a.cost + off, pol);
-            else
-              cp_async16(cslot(st, k), a.cost + off);
-          }
+          cp_async16(xslot(st, k), a.xy + off);
+          if (RC) cp_async16(cslot(st, k), a.cost + off);
         }
         vb[st][k] = __ldg(a.varphi + col);
       }

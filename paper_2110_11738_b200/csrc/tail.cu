@@ -458,6 +458,10 @@ __device__ __forceinline__ bool tail_body(const TailArgs<T>& t, unsigned* bar) {
   // iteration's pending update sums, the next iteration's sweep / merge sums)
   long long* xa = multi ? x_acc(X, X.rank, par) : t.xacc + par * kXaWords;
   long long* xn = multi ? x_acc(X, X.rank, par ^ 1) : t.xacc + (par ^ 1) * kXaWords;
+  // a stopped loop (graph batches run on past the stop): nothing to do, and
+  // nothing may be reset -- the last iteration's pending update sums (P)
+  // are still to be read by the finalize kernel
+  if (*reinterpret_cast<volatile int*>(&bk->stop)) return true;
   // CTA 0 prepares what others (of every rank) only touch after barrier 1
   // or in the next launch: the next tail's counters and sweep / merge sums
   // (A of the other parity), this iteration's update and report sums (P, R)
@@ -469,7 +473,6 @@ __device__ __forceinline__ bool tail_body(const TailArgs<T>& t, unsigned* bar) {
   }
   const int64_t it_stamp = t.stamps ? *reinterpret_cast<volatile int64_t*>(&bk->iter) : 0;
   TAIL_STAMP(2);
-  if (*reinterpret_cast<volatile int*>(&bk->stop)) return true;
   if (multi) {
     // row shards: this rank's sweep left fixed-point column partials in vfx
     // and its scalars in xloc -- add both into every rank's sums (integer
@@ -870,69 +873,6 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned
   tail_body<T, kTT>(t, bar);
 }
 
-// ---------------------------------------------------------------------------
-// KS -- small problems (X and C resident in L2): the whole loop in ONE
-// cooperative launch of co-resident 128-thread CTAs, `nb` iterations per
-// launch.  Per iteration: the K1 tiles (k1_tile: the same tiles, in any
-// order, with the same per-tile sums as pass_kernel_async), a grid barrier,
-// the tail (tail_body on 128-thread CTAs), a grid barrier.  Every cross-CTA
-// sum is exact, so the trajectory is bit-identical to the per-launch loop;
-// what goes away is two kernel boundaries and their launch gaps per
-// iteration, which dominate below ~2000^2.
-// ---------------------------------------------------------------------------
-constexpr int kCtrSmall = 512;  // bar word of the loop's grid barriers (host-reset per launch)
-
-__device__ __forceinline__ void grid_barrier_mono(unsigned* ctr, unsigned target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    red_release_add(ctr, 1u);
-    while (static_cast<int>(ld_relaxed(ctr) - target) < 0) {
-    }
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-  }
-  __syncthreads();
-}
-
-template <class T, int MODE, bool DUAL, bool DX>
-__device__ __forceinline__ void small_sweep(const PassArgs<T>& pa, const SmallArgs& sa,
-                                            unsigned char* dyn_smem, PassAcc<T>* wacc) {
-  for (int64_t tile = blockIdx.x; tile < sa.n_tiles; tile += gridDim.x)
-    k1_tile<T, MODE, DUAL, DX>(pa, tile % sa.gx, tile / sa.gx, sa.gx, dyn_smem, wacc, false, 0);
-}
-
-template <class T>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, 3)
-    small_solve_kernel(const PassArgs<T> pa0, const PassArgs<T> pa1, const TailArgs<T> ta0,
-                       const TailArgs<T> ta1, unsigned* bar, const SmallArgs sa) {
-  extern __shared__ __align__(16) unsigned char dyn_smem[];
-  __shared__ PassAcc<T> wacc[kWarpsPerCta];
-  const unsigned G = gridDim.x;
-  for (int b = 0; b < sa.nb; ++b) {
-    const int par = b & 1;
-    const PassArgs<T>& pa = par ? pa1 : pa0;
-    if (*reinterpret_cast<const volatile int*>(pa.stop)) break;  // uniform: the Book
-    const int mode = sa.mode[par];
-    const bool dual = sa.dual != 0, dx = sa.dx != 0;
-    if (mode == kSkip) {
-      small_sweep<T, kSkip, false, false>(pa, sa, dyn_smem, wacc);
-    } else if (mode == kFold) {
-      if (dx) small_sweep<T, kFold, true, true>(pa, sa, dyn_smem, wacc);
-      else small_sweep<T, kFold, true, false>(pa, sa, dyn_smem, wacc);
-    } else if (mode == kPlain0) {
-      if (dual && dx) small_sweep<T, kPlain0, true, true>(pa, sa, dyn_smem, wacc);
-      else if (dual) small_sweep<T, kPlain0, true, false>(pa, sa, dyn_smem, wacc);
-      else small_sweep<T, kPlain0, false, false>(pa, sa, dyn_smem, wacc);
-    } else {
-      if (dual && dx) small_sweep<T, kPlain1, true, true>(pa, sa, dyn_smem, wacc);
-      else if (dual) small_sweep<T, kPlain1, true, false>(pa, sa, dyn_smem, wacc);
-      else small_sweep<T, kPlain1, false, false>(pa, sa, dyn_smem, wacc);
-    }
-    grid_barrier_mono(bar + kCtrSmall, G * static_cast<unsigned>(2 * b + 1));
-    if (tail_body<T, kWarpsPerCta * 32>(par ? ta1 : ta0, bar)) break;
-    grid_barrier_mono(bar + kCtrSmall, G * static_cast<unsigned>(2 * b + 2));
-  }
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -1120,49 +1060,5 @@ template cudaError_t launch_tail<float>(const TailArgs<float>&, float*, double*,
 template cudaError_t launch_tail<double>(const TailArgs<double>&, double*, double*, unsigned*,
                                          int, cudaStream_t);
 
-
-template <class T>
-int small_grid(int device) {
-  int sms = 0, per = 0;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  const int smem = static_cast<int>(async_smem_bytes<T>());
-  cudaFuncSetAttribute(small_solve_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, small_solve_kernel<T>,
-                                                    kWarpsPerCta * 32, smem) != cudaSuccess) {
-    (void)cudaGetLastError();
-    return 0;
-  }
-  return sms * per;
-}
-
-template <class T>
-cudaError_t launch_small_solve(const PassArgs<T>& pa0, const PassArgs<T>& pa1,
-                               const TailArgs<T>& ta0, const TailArgs<T>& ta1, unsigned* bar,
-                               const SmallArgs& sa, int grid, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(bar + kCtrSmall, 0, sizeof(unsigned), st);
-  if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(grid));
-  cfg.blockDim = dim3(kWarpsPerCta * 32);
-  cfg.dynamicSmemBytes = async_smem_bytes<T>();
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  count_launch();
-  return cudaLaunchKernelEx(&cfg, small_solve_kernel<T>, pa0, pa1, ta0, ta1, bar, sa);
-}
-template int small_grid<float>(int);
-template int small_grid<double>(int);
-template cudaError_t launch_small_solve<float>(const PassArgs<float>&, const PassArgs<float>&,
-                                               const TailArgs<float>&, const TailArgs<float>&,
-                                               unsigned*, const SmallArgs&, int, cudaStream_t);
-template cudaError_t launch_small_solve<double>(const PassArgs<double>&,
-                                                const PassArgs<double>&,
-                                                const TailArgs<double>&,
-                                                const TailArgs<double>&, unsigned*,
-                                                const SmallArgs&, int, cudaStream_t);
 
 }  // namespace drotb
