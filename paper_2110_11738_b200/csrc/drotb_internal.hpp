@@ -146,7 +146,14 @@ struct Book {
   // cooperative tail: which of its two pending-partial buffers holds the
   // partials of pend_valid (tail.cu)
   int32_t pend_buf, pad_pm;
+  // deferred bookkeeping of the cooperative tail (gate.cuh tail_decide /
+  // tail_commit): what the last decided iteration still has to record
+  int32_t cm_valid, cm_flags;  // flags: kCm* bits
+  int64_t cm_k;                // the iteration (0-based) the record is of
+  double cm_tot[5];            // pass totals {cost, prev, dual, dx, max|t|}
+  double cm_r_primal, cm_r_dual, cm_gap, cm_dual, cm_last_cost;
 };
+constexpr int kCmCost = 1, kCmDual = 2, kCmFired = 4, kCmTrace = 8, kCmUseDx = 16, kCmFail = 32;
 
 struct TraceRowDev {
   int64_t iter;

@@ -65,32 +65,125 @@ __device__ void patch_pending(Book<T>* bk, const TailArgs<T>& t, const double (&
   bk->pend_row = -1;
 }
 
+// ---- the fused-gate tail's scalar logic, split (tail.cu) --------------------
+// tail_decide: what the next steps depend on -- the recursions' scalars, the
+// stale residuals and the gate's control flow (merge_scalars + gate_fused,
+// solver.hpp:266-289, 418-504) -- and a record of the rest; tail_commit:
+// the rest (pass diagnostics, ergodic mean, result iteration count, the trace
+// row, the pending-patch state), applied beside the NEXT iteration's decision
+// (warp 1 of the next tail), by the confirm path, or by the finalize kernel.
+// The decision reads nothing the commit writes, so the commit is off the
+// critical path and the results are those of the sequential logic.
 template <class T>
-__device__ void gate_fused(Book<T>* bk, const TailArgs<T>& t, double dual_alg,
-                           bool write_trace = true) {
-  bk->alpha = bk->alpha - bk->beta;  // solver.hpp:289
+__device__ void tail_decide(Book<T>* bk, const TailArgs<T>& t, const T (&tot)[8], int totbad,
+                            double sum_pa, double sum_pr, double sum_qb, double sum_qs) {
   const int64_t k = bk->iter;
+  bk->folded = t.folded_after;
+  bk->cm_k = k;
+#pragma unroll
+  for (int q = 0; q < 5; ++q) bk->cm_tot[q] = static_cast<double>(tot[q]);
+  bk->cm_valid = 1;
+  if (totbad) {  // solver.hpp:266, 418-422
+    bk->failed = 1;
+    bk->stop = 1;
+    bk->cm_flags = kCmFail;
+    return;
+  }
+  const T beta = tot[5] / static_cast<T>(t.m_global + t.n_global);
+  bk->beta = beta;
+  bk->coef = T(2) * beta - bk->alpha;
+  bk->nr2 = tot[6];
+  bk->ns2 = tot[7];
+  const bool cost_valid = t.reads_cost != 0;
+  const bool dual_valid = t.reads_cost && t.want_dual;
+  if (cost_valid) bk->last_cost = static_cast<double>(tot[0]);
+  if (dual_valid)
+    bk->last_r_dual = sqrt(static_cast<double>(tot[2])) / static_cast<double>(t.rho);
+  bk->alpha = bk->alpha - bk->beta;  // solver.hpp:289
   bk->iter = k + 1;
-  const double nan = __longlong_as_double(0x7ff8000000000000ULL);
+  const double dcoef = static_cast<double>(bk->coef);
+  const double dual_alg = ((sum_pa - 2.0 * sum_pr + dcoef * bk->sum_p) * t.inv_n_d +
+                           (sum_qb - 2.0 * sum_qs + dcoef * bk->sum_q) * t.inv_m_d) /
+                          static_cast<double>(t.rho);
   const double r_primal = sqrt(static_cast<double>(bk->nr2) + static_cast<double>(bk->ns2));
   const double gap = fabs(bk->last_cost - dual_alg);
   const double gap_scale = bk->relative ? 1.0 / (1.0 + fabs(bk->last_cost)) : 1.0;
-  bk->r_primal = r_primal;
-  bk->dual_value = dual_alg;
-  bk->gap = gap;
-  bk->fp_residual = nan;
   const bool check = every(k + 1, bk->check_every);
   const bool trace_row = bk->record_trace && every(k + 1, bk->trace_every);
+  // pre-filter with a slack above the closed form's rounding; gate_recheck
+  // applies the reference's exact test before any confirm report
+  const double slack = 1e-6 * bk->tol_gap + 1e-12 * fabs(bk->last_cost);
+  const bool fire = check && r_primal * bk->primal_scale <= bk->tol_primal &&
+                    bk->last_r_dual <= bk->tol_dual && gap * gap_scale <= bk->tol_gap + slack;
+  if (fire)
+    bk->confirm = 1;
+  else if (k + 1 >= bk->max_iters)
+    bk->stop = 1;
+  bk->cm_flags = (cost_valid ? kCmCost : 0) | (dual_valid ? kCmDual : 0) |
+                 (fire ? kCmFired : 0) | (trace_row ? kCmTrace : 0) |
+                 ((t.reads_cost && t.want_dx) ? kCmUseDx : 0);
+  bk->cm_r_primal = r_primal;
+  bk->cm_r_dual = bk->last_r_dual;
+  bk->cm_gap = gap;
+  bk->cm_dual = dual_alg;
+  bk->cm_last_cost = bk->last_cost;
+}
+
+// the commit record, copied before tail_decide of the next iteration
+// overwrites it (the two run concurrently in the next tail)
+struct CommitRec {
+  int32_t valid, flags;
+  int64_t k;
+  double tot[5];
+  double r_primal, r_dual, gap, dual, last_cost;
+};
+template <class T>
+__device__ __forceinline__ CommitRec commit_snap(const Book<T>& b) {
+  CommitRec c;
+  c.valid = b.cm_valid;
+  c.flags = b.cm_flags;
+  c.k = b.cm_k;
+#pragma unroll
+  for (int q = 0; q < 5; ++q) c.tot[q] = b.cm_tot[q];
+  c.r_primal = b.cm_r_primal;
+  c.r_dual = b.cm_r_dual;
+  c.gap = b.cm_gap;
+  c.dual = b.cm_dual;
+  c.last_cost = b.cm_last_cost;
+  return c;
+}
+
+template <class T>
+__device__ void tail_commit(Book<T>* bk, const TailArgs<T>& t, const CommitRec& c,
+                            bool write_trace) {
+  if (!c.valid) return;
+  bk->pass_cost = static_cast<T>(c.tot[0]);
+  bk->pass_prev = static_cast<T>(c.tot[1]);
+  bk->pass_dual = static_cast<T>(c.tot[2]);
+  bk->pass_dx = static_cast<T>(c.tot[3]);
+  bk->pass_max_abs = static_cast<T>(c.tot[4]);
+  bk->pass_bad = (c.flags & kCmFail) ? 1 : 0;
+  bk->iterations = c.k + 1;
+  if (c.flags & kCmFail) return;
+  const bool cost_valid = (c.flags & kCmCost) != 0;
+  if (!bk->prev_pass_had_cost && cost_valid) erg_update(bk, c.tot[1]);
+  if (cost_valid) erg_update(bk, c.tot[0]);
+  bk->prev_pass_had_cost = cost_valid ? 1 : 0;
+  const double nan = __longlong_as_double(0x7ff8000000000000ULL);
+  bk->r_primal = c.r_primal;
+  bk->dual_value = c.dual;
+  bk->gap = c.gap;
+  bk->fp_residual = nan;
   bk->pend_row = -1;
-  if (trace_row) {
+  if (c.flags & kCmTrace) {
     if (t.trace && bk->trace_rows < bk->trace_cap) {
       if (write_trace) {
         TraceRowDev& row = t.trace[bk->trace_rows];
-        row.iter = k + 1;
-        row.r_primal = r_primal;
-        row.r_dual = bk->last_r_dual;
-        row.gap = gap;  // patched with the exact dual value later
-        row.objective = bk->last_cost;
+        row.iter = c.k + 1;
+        row.r_primal = c.r_primal;
+        row.r_dual = c.r_dual;
+        row.gap = c.gap;  // patched with the exact dual value later
+        row.objective = c.last_cost;
         row.ergodic_objective = bk->erg_mean;
         row.fixed_point_residual = nan;  // patched later
       }
@@ -99,22 +192,10 @@ __device__ void gate_fused(Book<T>* bk, const TailArgs<T>& t, double dual_alg,
     bk->trace_rows += 1;
   }
   bk->pend_valid = 1;
-  bk->pend_last_cost = bk->last_cost;
-  bk->pend_use_dx = (t.reads_cost && t.want_dx) ? 1 : 0;
-  bk->pend_dx = static_cast<double>(bk->pass_dx);
-  // pre-filter: the closed-form dual value differs from the reference's sum
-  // by rounding only, so the gap test gets a slack far above that rounding
-  // (and far below tol_gap); gate_recheck then applies the reference's exact
-  // test (solver.hpp:498-504) before any confirm report runs
-  const double slack = 1e-6 * bk->tol_gap + 1e-12 * fabs(bk->last_cost);
-  const bool fire = check && r_primal * bk->primal_scale <= bk->tol_primal &&
-                    bk->last_r_dual <= bk->tol_dual && gap * gap_scale <= bk->tol_gap + slack;
-  if (fire) {
-    bk->confirm = 1;
-    bk->gate_hits += 1;
-  } else if (k + 1 >= bk->max_iters) {
-    bk->stop = 1;
-  }
+  bk->pend_last_cost = c.last_cost;
+  bk->pend_use_dx = (c.flags & kCmUseDx) ? 1 : 0;
+  bk->pend_dx = c.tot[3];
+  if (c.flags & kCmFired) bk->gate_hits += 1;
 }
 
 // After patch_pending has put the EXACT dual value of the gated iteration in

@@ -43,122 +43,6 @@ constexpr int kTSlots = 16;         // per-CTA partial slots
     if (t.stamps && threadIdx.x == 0) timeline_point(t.stamps, it_stamp, pt, global_ns()); \
   } while (0)
 
-// Every CTA has published its partials; the last CTA to arrive runs fn()
-// (whole CTA) and then releases the others.  bar = {count, generation}.
-// The arrival is one acq_rel atomic (releases this CTA's partials, acquires
-// everyone's for the last CTA), the release a red.release on the
-// generation, the wait an ld.acquire spin -- no full membar.gl on the path.
-__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
-  unsigned old;
-  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
-}
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// bar layout (unsigned words): [0] top count, [1] generation, and
-// kBarSub group counters at [kBarStride * (1 + g)] (one 128-B line each).
-// Arrival is hierarchical -- CTA b increments group counter b % kBarSub;
-// the last of its group increments the top counter -- so no address sees
-// more than ~G/kBarSub serialized atomics.  The generation a CTA waits on
-// is tracked in shared memory from one read at kernel start.
-constexpr int kBarSub = 16;
-constexpr int kBarStride = 32;
-
-__constant__ int c_bar_flat = 1;  // 1: one arrival counter (DROTB_BAR_FLAT)
-
-template <class F>
-__device__ __forceinline__ void reduce_barrier(unsigned* bar, unsigned& my_gen, F&& fn,
-                                               unsigned long long* stamps = nullptr,
-                                               int64_t it_stamp = 0) {
-  __shared__ int s_last;
-  __syncthreads();  // this CTA's partials are written (CTA scope)
-  if (threadIdx.x == 0) {
-    const unsigned G = gridDim.x;
-    const unsigned grp = blockIdx.x % kBarSub;
-    const unsigned ngrp = G < kBarSub ? G : kBarSub;
-    const unsigned members = G / kBarSub + (grp < G % kBarSub ? 1u : 0u);
-    int last = 0;
-    if (c_bar_flat)
-      last = atom_add_acq_rel(bar, 1u) == G - 1;
-    else if (atom_add_acq_rel(bar + kBarStride * (1 + grp), 1u) == members - 1)
-      last = atom_add_acq_rel(bar, 1u) == ngrp - 1;
-    s_last = last;
-  }
-  __syncthreads();
-  if (s_last) {
-    if (stamps && threadIdx.x == 0) timeline_point(stamps, it_stamp, 10, global_ns());
-    fn();
-    __syncthreads();
-    if (threadIdx.x < kBarSub) bar[kBarStride * (1 + threadIdx.x)] = 0u;
-    if (threadIdx.x == 0) bar[0] = 0u;
-    __syncthreads();
-    if (threadIdx.x == 0) red_release_add(bar + 1, 1u);
-  } else if (threadIdx.x == 0) {
-    while (ld_acquire(bar + 1) == my_gen) {
-    }
-    if (stamps) timeline_point(stamps, it_stamp, 13, global_ns());
-  }
-  ++my_gen;
-  __syncthreads();
-}
-
-// Fixed-order sum over the G per-CTA slots [off, off+K): thread t takes
-// CTAs t, t+kTT, ...; then a fixed warp tree and the warps in order.
-// Result valid in thread 0.
-template <class U, int K>
-__device__ __forceinline__ void totals(const U* part, int nb, int off, U (&out)[K], U* sh) {
-  U acc[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) acc[k] = U(0);
-  for (int b = threadIdx.x; b < nb; b += kTT)
-#pragma unroll
-    for (int k = 0; k < K; ++k) acc[k] += __ldcg(part + b * kTSlots + off + k);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int k = 0; k < K; ++k) acc[k] = warp_sum(acc[k]);
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < K; ++k) sh[k * kTW + warp] = acc[k];
-  __syncthreads();
-  if (threadIdx.x == 0)
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      U s = U(0);
-#pragma unroll
-      for (int w = 0; w < kTW; ++w) s += sh[k * kTW + w];
-      out[k] = s;
-    }
-  __syncthreads();
-}
-
-template <class U, int K>
-__device__ __forceinline__ void store_partials(U (&v)[K], U* part, int off, U* sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
-  __syncthreads();
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < K; ++k) sh[k * kTW + warp] = v[k];
-  __syncthreads();
-  if (threadIdx.x < K) {
-    U s = U(0);
-#pragma unroll
-    for (int w = 0; w < kTW; ++w) s += sh[threadIdx.x * kTW + w];
-    part[blockIdx.x * kTSlots + off + threadIdx.x] = s;
-  }
-  __syncthreads();
-}
-
-// book_load / book_store / patch_pending / gate_fused: gate.cuh
-
 // Counter barrier of the cooperative tail: every CTA arrives with one
 // release-add on the counter of this launch and spins (relaxed loads, no
 // cache invalidation per poll) until all G arrivals are visible, then
@@ -169,6 +53,9 @@ __device__ __forceinline__ void store_partials(U (&v)[K], U* part, int off, U* s
 // Counters: bar[kCtr0] / bar[kCtr1] by iteration parity; a launch resets the
 // other parity's counter for the next launch (consecutive tails alternate).
 constexpr int kCtr0 = 768, kCtr1 = 896;
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -187,55 +74,6 @@ __device__ __forceinline__ void count_barrier(unsigned* ctr, unsigned target,
   __syncthreads();
 }
 
-// Partials are stored value-major -- part[k * Gp + b] for value k of CTA b,
-// Gp = G rounded up to 32 -- so that reading all of them is a few coalesced
-// 128-B requests per value instead of one request per (CTA, value): every
-// CTA reads every partial after a counter barrier (the L2 would otherwise
-// serve ~G^2 * K small requests).
-__device__ __forceinline__ int padded_grid(int G) { return (G + 31) & ~31; }
-
-template <class U, int K>
-__device__ __forceinline__ void store_partials_vm(U (&v)[K], U* part, int Gp, int off, U* sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
-  __syncthreads();
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < K; ++k) sh[k * kTW + warp] = v[k];
-  __syncthreads();
-  if (threadIdx.x < K) {
-    U s = U(0);
-#pragma unroll
-    for (int w = 0; w < kTW; ++w) s += sh[threadIdx.x * kTW + w];
-    part[(off + threadIdx.x) * Gp + blockIdx.x] = s;
-  }
-}
-
-// Fixed-order totals of K value-major partials: warp w sums values
-// w, w + kTW, ...: lane l adds CTAs l, l + 32, ... in order, then the warp
-// tree.  out[k] valid in every thread after the call (through sh).
-template <class U, int K>
-__device__ __forceinline__ void all_totals_vm(const U* part, int G, int Gp, int off,
-                                              U (&out)[K], U* sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int k = warp; k < K; k += kTW) {
-    U acc = U(0);
-    for (int b = lane; b < G; b += 32) acc += __ldcg(part + (off + k) * Gp + b);
-    acc = warp_sum(acc);
-    if (lane == 0) sh[k] = acc;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < K; ++k) out[k] = sh[k];
-  __syncthreads();
-}
-
-// dpart values: [0, 8) pending update partials of parity 0, [8, 10) confirm
-// report, [10, 14) fused-gate merge sums, [16, 24) pending partials of parity 1
-constexpr int kDS = kTailDSlots;
-__device__ __forceinline__ int pend_off(int par) { return par ? 16 : 0; }
-
 template <class T>
 __device__ __forceinline__ void book_store_cta0(Book<T>* dst, const Book<T>* src) {
   constexpr int W = static_cast<int>(sizeof(Book<T>) / 8);
@@ -246,72 +84,10 @@ __device__ __forceinline__ void book_store_cta0(Book<T>* dst, const Book<T>* src
           reinterpret_cast<const unsigned long long*>(src)[k];
 }
 
-// The pending exact dual value / fixed-point residual of the previous
-// iteration (gate.cuh patch_pending), split so that it can run beside the
-// current iteration's gate: snapshot the pending fields, compute, apply.
-struct PendSnap {
-  int valid, use_dx, record;
-  int64_t row, cap;
-  double last_cost, dx;
-};
-template <class T>
-__device__ __forceinline__ PendSnap pend_snap(const Book<T>& b) {
-  return PendSnap{b.pend_valid, b.pend_use_dx, b.record_trace, b.pend_row, b.trace_cap,
-                  b.pend_last_cost, b.pend_dx};
-}
-template <class T>
-__device__ __forceinline__ void pend_compute(const PendSnap& ps, const TailArgs<T>& t,
-                                             const double (&d8)[8], bool write_trace,
-                                             double* out3) {
-  const double dual = d8[0] + d8[4];
-  double fpr = __longlong_as_double(0x7ff8000000000000ULL);
-  if (ps.record) {  // rank-two identity (solver.hpp:443-472)
-    double fp_sq = static_cast<double>(t.n_global) * d8[1] +
-                   static_cast<double>(t.m_global) * d8[5] + 2.0 * d8[2] * d8[6];
-    if (ps.use_dx) fp_sq += ps.dx + 2.0 * (d8[3] + d8[7]);
-    fpr = sqrt(fmax(fp_sq, 0.0));
-  }
-  const double gap = fabs(ps.last_cost - dual);
-  if (write_trace && t.trace && ps.row >= 0 && ps.row < ps.cap) {
-    TraceRowDev& row = t.trace[ps.row];
-    row.gap = gap;
-    row.fixed_point_residual = fpr;
-  }
-  out3[0] = dual;
-  out3[1] = gap;
-  out3[2] = fpr;
-}
-
 // update-phase threads: warps kUW.. (warps 0 and 1 run the scalar logic of
 // barrier 1 meanwhile)
 constexpr int kUW = 2;
 constexpr int kUT = kTT - 32 * kUW;
-
-// K exact sums (HiLo pairs) of one CTA: fixed-order int64 trees (exact, so
-// the order does not matter anyway), then one red per word into acc[0, 2K)
-template <int K>
-__device__ __forceinline__ void red_cta_hilo(HiLo (&v)[K], long long* acc, long long* sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    v[k].hi = warp_sum_ll(v[k].hi);
-    v[k].lo = warp_sum_ll(v[k].lo);
-  }
-  __syncthreads();
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      sh[(2 * k) * kTW + warp] = v[k].hi;
-      sh[(2 * k + 1) * kTW + warp] = v[k].lo;
-    }
-  __syncthreads();
-  if (threadIdx.x < 2 * K) {
-    long long s = 0;
-#pragma unroll
-    for (int w = 0; w < kTW; ++w) s += sh[threadIdx.x * kTW + w];
-    red_add_u64(acc + threadIdx.x, s);
-  }
-}
 
 // ---- row shards (TailArgs::x, world > 1) ----------------------------------
 __device__ __forceinline__ void red_sys_u64(long long* p, long long v) {
@@ -513,8 +289,6 @@ __device__ __forceinline__ bool tail_body(const TailArgs<T>& t, unsigned* bar) {
   __shared__ long long shL[2 * 8 * 8];
   __shared__ long long shP[2 * 8 * 8];  // update sums (named-barrier reduction)
   __shared__ double s_tot[24];
-  __shared__ double s_patch[3];
-  __shared__ int s_gate_ran, s_pvalid;
   const int64_t m = t.m, n = t.n;
   // the Book as this launch found it (CTA 0 of the previous tail or the host
   // wrote it; nobody writes it before barrier 1)
@@ -704,35 +478,29 @@ __device__ __forceinline__ bool tail_body(const TailArgs<T>& t, unsigned* bar) {
   const T beta_all = tot8[5] / static_cast<T>(t.m_global + t.n_global);
   const T coef = T(2) * beta_all - sbk.alpha;
   const bool pass_bad = s_tot[12] > 0.0;
-  PendSnap snap{};
-  if (tid == 32) {
-    snap = pend_snap(sbk);
-    s_pvalid = snap.valid;
-  }
+  // the previous iteration's commit record, before warp 0 overwrites it
+  CommitRec crec{};
+  if (tid == 32) crec = commit_snap(sbk);
   __syncthreads();
-  // warp 0: recursions + gate; warp 1: the previous iteration's exact dual /
-  // fixed-point patch; warps 2..7: the update (solver.hpp:279-289)
+  // warp 0: this iteration's decision (gate.cuh tail_decide); warp 1: the
+  // previous iteration's commit and exact dual / fixed-point patch; warps
+  // 2..: the update (solver.hpp:279-289) -- concurrently
   if (warp == 0) {
     if (lane == 0) {
-      merge_scalars<T>(&sbk, t, tot8, pass_bad ? 1 : 0);
-      int ran = 0;
-      if (fg && !sbk.stop) {
-        const double dcoef = static_cast<double>(sbk.coef);
-        const double dual_alg =
-            ((s_tot[kXaPA] - 2.0 * s_tot[kXaPR] + dcoef * sbk.sum_p) * t.inv_n_d +
-             (s_tot[kXaQB] - 2.0 * s_tot[kXaQS] + dcoef * sbk.sum_q) * t.inv_m_d) /
-            static_cast<double>(t.rho);
-        gate_fused<T>(&sbk, t, dual_alg, blockIdx.x == 0);
+      if (fg) {
+        tail_decide<T>(&sbk, t, tot8, pass_bad ? 1 : 0, s_tot[kXaPA], s_tot[kXaPR],
+                       s_tot[kXaQB], s_tot[kXaQS]);
         sbk.pend_buf = par;
-        ran = 1;
+      } else {
+        merge_scalars<T>(&sbk, t, tot8, pass_bad ? 1 : 0);
       }
-      s_gate_ran = ran;
     }
   } else if (warp == 1) {
-    if (lane == 0 && fg && snap.valid) {
+    if (lane == 0 && fg && crec.valid) {
+      tail_commit<T>(&sbk, t, crec, blockIdx.x == 0);
       const double d8[8] = {s_tot[13], s_tot[14], s_tot[15], s_tot[16],
                             s_tot[17], s_tot[18], s_tot[19], s_tot[20]};
-      pend_compute<T>(snap, t, d8, blockIdx.x == 0, s_patch);
+      patch_pending<T>(&sbk, t, d8, blockIdx.x == 0);
     }
   }
   // ---- B: phi / varphi / a / b + exact dual-value and fixed-point sums ------
@@ -783,15 +551,6 @@ __device__ __forceinline__ bool tail_body(const TailArgs<T>& t, unsigned* bar) {
   }
   if (warp >= kUW && !pass_bad) red_upd_hilo<NT, 8>(hp, kXaP, 0x0F, X, par, xa, shP);
   __syncthreads();
-  if (tid == 0) {
-    if (fg && s_pvalid && !s_gate_ran) {  // gate did not run: the patch stands
-      sbk.dual_value = s_patch[0];
-      sbk.gap = s_patch[1];
-      sbk.fp_residual = s_patch[2];
-      sbk.pend_valid = 0;
-      sbk.pend_row = -1;
-    }
-  }
   TAIL_STAMP(12);
   book_store_cta0(bk, &sbk);
   TAIL_STAMP(4);
@@ -813,8 +572,14 @@ __device__ __forceinline__ bool tail_body(const TailArgs<T>& t, unsigned* bar) {
     const double d8[8] = {s_tot[13], s_tot[14], s_tot[15], s_tot[16],
                           s_tot[17], s_tot[18], s_tot[19], s_tot[20]};
     if (fg) {
+      // this iteration's commit now (its record is consumed: the next tail
+      // must not apply it again), then its exact dual value and the
+      // reference's gap test before the report
+      const CommitRec c = commit_snap(sbk);
+      tail_commit<T>(&sbk, t, c, blockIdx.x == 0);
+      sbk.cm_valid = 0;
       patch_pending<T>(&sbk, t, d8, blockIdx.x == 0);
-      gate_recheck<T>(&sbk);  // exact gap before the report
+      gate_recheck<T>(&sbk);
     } else {
       gate_logic<T>(&sbk, t, d8[0] + d8[4], d8[1], d8[2], d8[5], d8[6], d8[3] + d8[7],
                     blockIdx.x == 0);
@@ -955,29 +720,31 @@ __global__ void __launch_bounds__(1024) xallreduce_kernel(const U* in, U* out, i
 
 template <class T>
 __global__ void __launch_bounds__(kTT) tail_finalize_kernel(const TailArgs<T> t) {
+  // end of a run: the last iteration's commit and exact dual / fixed-point patch
   Book<T>* bk = t.book;
-  if (threadIdx.x != 0 || !*reinterpret_cast<volatile int*>(&bk->pend_valid)) return;
-  const int buf = *reinterpret_cast<volatile int*>(&bk->pend_buf);
-  const long long* xp = t.xacc + buf * kXaWords + kXaP;
-  double d8[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) d8[k] = hilo_value(xp[2 * k], xp[2 * k + 1]);
+  if (threadIdx.x != 0) return;
+  if (!*reinterpret_cast<volatile int*>(&bk->cm_valid) &&
+      !*reinterpret_cast<volatile int*>(&bk->pend_valid))
+    return;
   Book<T> lb = *bk;
-  patch_pending<T>(&lb, t, d8);
+  if (lb.cm_valid) {
+    const CommitRec c = commit_snap(lb);
+    tail_commit<T>(&lb, t, c, true);
+    lb.cm_valid = 0;
+  }
+  if (lb.pend_valid) {
+    const long long* xp = t.xacc + lb.pend_buf * kXaWords + kXaP;
+    double d8[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) d8[k] = hilo_value(xp[2 * k], xp[2 * k + 1]);
+    patch_pending<T>(&lb, t, d8);
+  }
   *bk = lb;
 }
 
 template <class T>
 int tail_grid(int device) {
   int sms = 0, per = 0;
-  {
-    // one arrival counter (default): one atomic round trip for the last
-    // arriver instead of two; measured -0.5 us per iteration at 148 CTAs.
-    // DROTB_BAR_FLAT=0 restores the 16-group hierarchy (for large grids)
-    const char* e = std::getenv("DROTB_BAR_FLAT");
-    const int v = (e && e[0] == '0') ? 0 : 1;
-    cudaMemcpyToSymbol(c_bar_flat, &v, sizeof(v));
-  }
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   // An SM runs CTAs of kernels with different shared-memory carveouts only
   // after reconfiguring, i.e. once it is empty: a spinning tail CTA on an
