@@ -491,6 +491,7 @@ __device__ __forceinline__ bool tail_body(const TailArgs<T>& t, unsigned* bar) {
         tail_decide<T>(&sbk, t, tot8, pass_bad ? 1 : 0, s_tot[kXaPA], s_tot[kXaPR],
                        s_tot[kXaQB], s_tot[kXaQS]);
         sbk.pend_buf = par;
+        TAIL_STAMP(15);
       } else {
         merge_scalars<T>(&sbk, t, tot8, pass_bad ? 1 : 0);
       }
@@ -549,7 +550,9 @@ __device__ __forceinline__ bool tail_body(const TailArgs<T>& t, unsigned* bar) {
       }
     }
   }
+  if (t.stamps && tid == 32 * kUW) timeline_point(t.stamps, it_stamp, 13, global_ns());
   if (warp >= kUW && !pass_bad) red_upd_hilo<NT, 8>(hp, kXaP, 0x0F, X, par, xa, shP);
+  if (t.stamps && tid == 32 * kUW) timeline_point(t.stamps, it_stamp, 14, global_ns());
   __syncthreads();
   TAIL_STAMP(12);
   book_store_cta0(bk, &sbk);

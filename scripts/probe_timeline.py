@@ -39,7 +39,7 @@ a = np.array(list(buf), dtype=np.float64).reshape(64, 16, 2)
 it0 = 8
 names = ["K1 entry", "K1 exit", "tail entry", "merge done", "book stored", "update done", "tail exit",
          "strips loaded", "r/s stored", "K1 slice ld", "barrier passed", "totals loaded",
-         "scalars done", "(unused)"]
+         "join (all roles)", "update done(w2)", "upd sums red(w2)", "decide done(w0)"]
 NP = len(names)
 rows = []
 for k in range(it0 + 2, it0 + K - 1):
@@ -54,7 +54,7 @@ r = np.array(rows)
 mean = r.mean(axis=0)
 print(f"{m}x{m} {np.dtype(dt).name}: {len(r)} iterations, graph-timed "
       f"{e0.elapsed_time(e1) * 1e3 / K:.1f} us/iter; mean us after the first K1 CTA entry:")
-order = [0, 1, 2, 7, 8, 9, 3, 10, 11, 12, 4, 5, 6]
+order = [0, 1, 2, 7, 8, 9, 3, 10, 11, 15, 13, 14, 12, 4, 5, 6]
 for p in order:
     if mean[p] > 1e9:  # point not recorded
         continue
