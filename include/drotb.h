@@ -357,10 +357,10 @@ int drotb_session_gen_uniform(drotb_session* s, uint64_t seed, double lo, double
 int drotb_session_support(drotb_session* s, double rel_tau, double abs_tau, int64_t* nnz,
                           double* xmax);
 /* Profiling aid (DROTB_TAIL_STAMPS=1 at session creation): copies and resets
- * the device timeline of the solve loop, 64 iterations deep: out[2048] =
- * [slot = iteration & 63][point 0..15][min, max over CTAs] %globaltimer ns
+ * the device timeline of the solve loop, 64 iterations deep: out[3072] =
+ * [slot = iteration & 63][point 0..23][min, max over CTAs] %globaltimer ns
  * (points: csrc/drotb_internal.hpp kStampPts). */
-int drotb_session_tail_stamps(drotb_session* s, uint64_t* out2048);
+int drotb_session_tail_stamps(drotb_session* s, uint64_t* out3072);
 /* Debug aid: device addresses of the book, the tail barrier words and the
  * exchange buffer, and the tail grid size. */
 int drotb_session_debug_ptrs(drotb_session* s, uint64_t* out4);

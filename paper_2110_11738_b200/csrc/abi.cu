@@ -148,7 +148,9 @@ int step_t(T* xy, int32_t* folded, T* rs, T* cs, T* ya, T* yb, T* alpha, T* r,
     CUDA_TRY(cudaGetLastError());
     drotb::Book<T> hb;
     RC_TRY(ss->read_book(&hb));
-    if (hb.pass_bad) {
+    // (the cooperative tail records pass_bad with the deferred commit, at
+    // store_state; its decision sets failed at once)
+    if (hb.pass_bad || hb.failed) {
       RC_TRY(ss->store_state(xy, folded, rs, cs, ya, yb, alpha, r, s, beta, iter, false));
       return drotb::set_error(DROTB_ERRC_NON_FINITE_ITERATE,
                               "non-finite value in iterate update");

@@ -66,7 +66,7 @@ enum XAcc : int {
 };
 
 constexpr int kStampSlots = 64;
-constexpr int kStampPts = 16;
+constexpr int kStampPts = 24;
 constexpr int kStampWords = kStampSlots * kStampPts * 2;
 
 template <class T>
@@ -254,7 +254,7 @@ struct TailArgs {
   XArgs x;
   long long* xloc;
   int32_t pdl;                 // tail launched as a programmatic dependent of the sweep
-  int32_t pad_pdl;
+  int32_t ctail;               // cluster tail allowed: max CTAs per cluster (0: grid tail)
 };
 
 // Cooperative per-iteration tail (tail.cu): merge + recursions + update +

@@ -42,27 +42,33 @@ __device__ __forceinline__ void book_store(Book<T>* dst, const Book<T>* src) {
 // fixed_point_residual) are reduced one iteration later -- or by the
 // finalize kernel at the end of a run -- and patched into its trace row.
 template <class T>
-__device__ void patch_pending(Book<T>* bk, const TailArgs<T>& t, const double (&d8)[8],
-                              bool write_trace = true) {
+__device__ __forceinline__ void patch_pending(Book<T>* bk, TraceRowDev* trace, int64_t n_global,
+                                              int64_t m_global, const double* d8,
+                                              bool write_trace) {
   if (!bk->pend_valid) return;
   const double dual = d8[0] + d8[4];
   double fpr = __longlong_as_double(0x7ff8000000000000ULL);
   if (bk->record_trace) {  // rank-two identity (solver.hpp:443-472)
-    double fp_sq = static_cast<double>(t.n_global) * d8[1] +
-                   static_cast<double>(t.m_global) * d8[5] + 2.0 * d8[2] * d8[6];
+    double fp_sq = static_cast<double>(n_global) * d8[1] +
+                   static_cast<double>(m_global) * d8[5] + 2.0 * d8[2] * d8[6];
     if (bk->pend_use_dx) fp_sq += bk->pend_dx + 2.0 * (d8[3] + d8[7]);
     fpr = sqrt(fmax(fp_sq, 0.0));
   }
   bk->dual_value = dual;
   bk->gap = fabs(bk->pend_last_cost - dual);
   bk->fp_residual = fpr;
-  if (write_trace && t.trace && bk->pend_row >= 0 && bk->pend_row < bk->trace_cap) {
-    TraceRowDev& row = t.trace[bk->pend_row];
+  if (write_trace && trace && bk->pend_row >= 0 && bk->pend_row < bk->trace_cap) {
+    TraceRowDev& row = trace[bk->pend_row];
     row.gap = bk->gap;
     row.fixed_point_residual = fpr;
   }
   bk->pend_valid = 0;
   bk->pend_row = -1;
+}
+template <class T>
+__device__ __forceinline__ void patch_pending(Book<T>* bk, const TailArgs<T>& t,
+                                              const double (&d8)[8], bool write_trace = true) {
+  patch_pending<T>(bk, t.trace, t.n_global, t.m_global, d8, write_trace);
 }
 
 // ---- the fused-gate tail's scalar logic, split (tail.cu) --------------------
@@ -74,37 +80,59 @@ __device__ void patch_pending(Book<T>* bk, const TailArgs<T>& t, const double (&
 // (warp 1 of the next tail), by the confirm path, or by the finalize kernel.
 // The decision reads nothing the commit writes, so the commit is off the
 // critical path and the results are those of the sequential logic.
+// tail_decide's inputs, in shared memory (the launch constants are set in
+// the tail's prologue, off the critical path; the call passes two pointers)
 template <class T>
-__device__ void tail_decide(Book<T>* bk, const TailArgs<T>& t, const T (&tot)[8], int totbad,
-                            double sum_pa, double sum_pr, double sum_qb, double sum_qs) {
+struct DecideIn {
+  T tot[8];                            // pass totals {cost, prev, dual, dx, max|t|, sum r, |r|^2, |s|^2}
+  double sum_pa, sum_pr, sum_qb, sum_qs;  // exact merge sums
+  double inv_n_d, inv_m_d;
+  int64_t mn;                          // m_global + n_global
+  T rho;
+  int32_t totbad, folded_after, reads_cost, want_dual, want_dx;
+};
+template <class T>
+__device__ __forceinline__ void decide_consts(DecideIn<T>* in, const TailArgs<T>& t) {
+  in->inv_n_d = t.inv_n_d;
+  in->inv_m_d = t.inv_m_d;
+  in->mn = t.m_global + t.n_global;
+  in->rho = t.rho;
+  in->folded_after = t.folded_after;
+  in->reads_cost = t.reads_cost;
+  in->want_dual = t.want_dual;
+  in->want_dx = t.want_dx;
+}
+template <class T>
+__device__ __noinline__ void tail_decide(Book<T>* bk, const DecideIn<T>* in) {
+  const T (&tot)[8] = in->tot;
   const int64_t k = bk->iter;
-  bk->folded = t.folded_after;
+  bk->folded = in->folded_after;
   bk->cm_k = k;
 #pragma unroll
   for (int q = 0; q < 5; ++q) bk->cm_tot[q] = static_cast<double>(tot[q]);
   bk->cm_valid = 1;
-  if (totbad) {  // solver.hpp:266, 418-422
+  if (in->totbad) {  // solver.hpp:266, 418-422
     bk->failed = 1;
     bk->stop = 1;
     bk->cm_flags = kCmFail;
     return;
   }
-  const T beta = tot[5] / static_cast<T>(t.m_global + t.n_global);
+  const T beta = tot[5] / static_cast<T>(in->mn);
   bk->beta = beta;
   bk->coef = T(2) * beta - bk->alpha;
   bk->nr2 = tot[6];
   bk->ns2 = tot[7];
-  const bool cost_valid = t.reads_cost != 0;
-  const bool dual_valid = t.reads_cost && t.want_dual;
+  const bool cost_valid = in->reads_cost != 0;
+  const bool dual_valid = in->reads_cost && in->want_dual;
   if (cost_valid) bk->last_cost = static_cast<double>(tot[0]);
   if (dual_valid)
-    bk->last_r_dual = sqrt(static_cast<double>(tot[2])) / static_cast<double>(t.rho);
+    bk->last_r_dual = sqrt(static_cast<double>(tot[2])) / static_cast<double>(in->rho);
   bk->alpha = bk->alpha - bk->beta;  // solver.hpp:289
   bk->iter = k + 1;
   const double dcoef = static_cast<double>(bk->coef);
-  const double dual_alg = ((sum_pa - 2.0 * sum_pr + dcoef * bk->sum_p) * t.inv_n_d +
-                           (sum_qb - 2.0 * sum_qs + dcoef * bk->sum_q) * t.inv_m_d) /
-                          static_cast<double>(t.rho);
+  const double dual_alg = ((in->sum_pa - 2.0 * in->sum_pr + dcoef * bk->sum_p) * in->inv_n_d +
+                           (in->sum_qb - 2.0 * in->sum_qs + dcoef * bk->sum_q) * in->inv_m_d) /
+                          static_cast<double>(in->rho);
   const double r_primal = sqrt(static_cast<double>(bk->nr2) + static_cast<double>(bk->ns2));
   const double gap = fabs(bk->last_cost - dual_alg);
   const double gap_scale = bk->relative ? 1.0 / (1.0 + fabs(bk->last_cost)) : 1.0;
@@ -121,7 +149,7 @@ __device__ void tail_decide(Book<T>* bk, const TailArgs<T>& t, const T (&tot)[8]
     bk->stop = 1;
   bk->cm_flags = (cost_valid ? kCmCost : 0) | (dual_valid ? kCmDual : 0) |
                  (fire ? kCmFired : 0) | (trace_row ? kCmTrace : 0) |
-                 ((t.reads_cost && t.want_dx) ? kCmUseDx : 0);
+                 ((in->reads_cost && in->want_dx) ? kCmUseDx : 0);
   bk->cm_r_primal = r_primal;
   bk->cm_r_dual = bk->last_r_dual;
   bk->cm_gap = gap;
@@ -154,8 +182,8 @@ __device__ __forceinline__ CommitRec commit_snap(const Book<T>& b) {
 }
 
 template <class T>
-__device__ void tail_commit(Book<T>* bk, const TailArgs<T>& t, const CommitRec& c,
-                            bool write_trace) {
+__device__ __forceinline__ void tail_commit(Book<T>* bk, TraceRowDev* trace, const CommitRec& c,
+                                            bool write_trace) {
   if (!c.valid) return;
   bk->pass_cost = static_cast<T>(c.tot[0]);
   bk->pass_prev = static_cast<T>(c.tot[1]);
@@ -176,9 +204,9 @@ __device__ void tail_commit(Book<T>* bk, const TailArgs<T>& t, const CommitRec& 
   bk->fp_residual = nan;
   bk->pend_row = -1;
   if (c.flags & kCmTrace) {
-    if (t.trace && bk->trace_rows < bk->trace_cap) {
+    if (trace && bk->trace_rows < bk->trace_cap) {
       if (write_trace) {
-        TraceRowDev& row = t.trace[bk->trace_rows];
+        TraceRowDev& row = trace[bk->trace_rows];
         row.iter = c.k + 1;
         row.r_primal = c.r_primal;
         row.r_dual = c.r_dual;
@@ -196,6 +224,27 @@ __device__ void tail_commit(Book<T>* bk, const TailArgs<T>& t, const CommitRec& 
   bk->pend_use_dx = (c.flags & kCmUseDx) ? 1 : 0;
   bk->pend_dx = c.tot[3];
   if (c.flags & kCmFired) bk->gate_hits += 1;
+}
+template <class T>
+__device__ __forceinline__ void tail_commit(Book<T>* bk, const TailArgs<T>& t, const CommitRec& c,
+                                            bool write_trace) {
+  tail_commit<T>(bk, t.trace, c, write_trace);
+}
+
+// the previous iteration's commit + exact dual / fixed-point patch as one
+// out-of-line call on shared-memory inputs (the cluster tail runs it once
+// on a scratch Book to cache its code, then for real -- see tail.cu)
+struct CommitIn {
+  CommitRec c;
+  double d8[8];
+  TraceRowDev* trace;
+  int64_t n_global, m_global;
+  int32_t write_trace, pad;
+};
+template <class T>
+__device__ __noinline__ void commit_patch(Book<T>* bk, const CommitIn* in) {
+  tail_commit<T>(bk, in->trace, in->c, in->write_trace != 0);
+  patch_pending<T>(bk, in->trace, in->n_global, in->m_global, in->d8, in->write_trace != 0);
 }
 
 // After patch_pending has put the EXACT dual value of the gated iteration in

@@ -75,7 +75,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_ASYNC_MINB)
     return;
   }
   const int64_t it_stamp = a.stamps ? *reinterpret_cast<const volatile int64_t*>(a.iter) : 0;
-  if (a.stamps && threadIdx.x == 0) timeline_point(a.stamps, it_stamp, 0, t_entry);
+  if (a.stamps && threadIdx.x == 0) {
+    timeline_point(a.stamps, it_stamp, 0, t_entry);
+    timeline_point(a.stamps, it_stamp, 9, global_ns());  // released by the tail
+  }
 
   k1_tile<T, MODE, DUAL, DX>(a, blockIdx.x, blockIdx.y, gridDim.x, dyn_smem, wacc, a.pdl != 0,
                              it_stamp);

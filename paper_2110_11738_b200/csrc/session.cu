@@ -104,6 +104,10 @@ int Session<T>::setup_coop_tail() {
   // 1000^2 fp64 (r2 timeline) -- tail CTAs parked beside the last sweep wave
   tail_pdl = false;
   if (const char* e = std::getenv("DROTB_TAIL_PDL")) tail_pdl = e[0] == '1';
+  // the tail as one thread-block cluster where m + n fits it (tail.cu KC);
+  // DROTB_CTAIL=0: always the grid tail, =8: clusters of at most 8 CTAs
+  ctail_cap = 16;
+  if (const char* e = std::getenv("DROTB_CTAIL")) ctail_cap = std::atoi(e) >= 16 ? 16 : (std::atoi(e) >= 8 ? 8 : 0);
   tgrid = tail_grid<T>(device);
   if (tgrid <= 0) return 0;
   const size_t gp = static_cast<size_t>((tgrid + 31) / 32 * 32);  // value-major partials (tail.cu)
@@ -633,6 +637,7 @@ TailArgs<T> Session<T>::tail_args(int64_t k, int mode, bool folded_after, bool s
   t.vfx = vfx;
   t.fx = fx ? 1 : 0;
   t.pdl = (coop && tail_pdl && !exact && !sharded) ? 1 : 0;
+  t.ctail = ctail_cap;
   t.xacc = xacc;
   std::memset(&t.x, 0, sizeof(t.x));
   t.x.world = 1;

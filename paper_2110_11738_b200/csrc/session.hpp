@@ -134,6 +134,7 @@ struct Session {
 
   // cooperative tail kernel (fast order, one GPU; tail.cu)
   bool coop = false, coop_graphs = false, fused_gate = true, pdl_ok = false, tail_pdl = false;
+  int ctail_cap = 16;  // cluster tail: max CTAs per cluster (DROTB_CTAIL; 0 = grid tail only)
   // L2 policies (sweep.cuh): bit 0 evict_first on the streamed X / C reads
   // (measured slower: off), bit 1 evict_last on the row / column strips K1
   // leaves for the tail (default: +2 % per iteration at 10k^2, r1n)

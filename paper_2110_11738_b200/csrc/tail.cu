@@ -22,6 +22,7 @@
 // the barrier itself: no CTA re-reads all partials (a G^2 L2 hot spot) and no
 // second barrier is needed to broadcast the totals.  Deterministic: every
 // reduction runs in a fixed order independent of which CTA arrives last.
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 
@@ -34,8 +35,6 @@ namespace drotb {
 namespace {
 
 constexpr int kTT = 256;            // threads per CTA
-constexpr int kTW = kTT / 32;       // warps per CTA = strip partitions in A
-constexpr int kTSlots = 16;         // per-CTA partial slots
 
 // profiling aid (DROTB_TAIL_STAMPS): timeline points (drotb_internal.hpp)
 #define TAIL_STAMP(pt)                                                          \
@@ -87,7 +86,6 @@ __device__ __forceinline__ void book_store_cta0(Book<T>* dst, const Book<T>* src
 // update-phase threads: warps kUW.. (warps 0 and 1 run the scalar logic of
 // barrier 1 meanwhile)
 constexpr int kUW = 2;
-constexpr int kUT = kTT - 32 * kUW;
 
 // ---- row shards (TailArgs::x, world > 1) ----------------------------------
 __device__ __forceinline__ void red_sys_u64(long long* p, long long v) {
@@ -139,24 +137,22 @@ __device__ __forceinline__ void red_cta_hilo_x(HiLo (&v)[K], int word0, int all_
                                                const XArgs& x, int par, long long* local,
                                                long long* sh) {
   constexpr int kTW = NT / 32;
+  static_assert(K <= 8, "16 words per lane");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  long long w[16];
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    v[k].hi = warp_sum_ll(v[k].hi);
-    v[k].lo = warp_sum_ll(v[k].lo);
+  for (int k = 0; k < 8; ++k) {
+    w[2 * k] = k < K ? v[k].hi : 0;
+    w[2 * k + 1] = k < K ? v[k].lo : 0;
   }
+  const long long ws = bfly16(w, lane);
   __syncthreads();
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      sh[(2 * k) * kTW + warp] = v[k].hi;
-      sh[(2 * k + 1) * kTW + warp] = v[k].lo;
-    }
+  if ((lane & 1) == 0) sh[bfly16_word(lane) * kTW + warp] = ws;
   __syncthreads();
   if (threadIdx.x < 2 * K) {
     long long s = 0;
 #pragma unroll
-    for (int w = 0; w < kTW; ++w) s += sh[threadIdx.x * kTW + w];
+    for (int q = 0; q < kTW; ++q) s += sh[threadIdx.x * kTW + q];
     const int word = word0 + threadIdx.x;
     if (x.world > 1 && ((all_mask >> (threadIdx.x >> 1)) & 1)) {
       for (int r = 0; r < x.world; ++r) red_sys_u64(x_acc(x, r, par) + word, s);
@@ -174,24 +170,22 @@ __device__ __forceinline__ void red_upd_hilo(HiLo (&v)[K], int word0, int all_ma
                                              long long* sh) {
   constexpr int kTW = NT / 32;
   constexpr int kUT = NT - 32 * kUW;
+  static_assert(K <= 8, "16 words per lane");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  long long w[16];
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    v[k].hi = warp_sum_ll(v[k].hi);
-    v[k].lo = warp_sum_ll(v[k].lo);
+  for (int k = 0; k < 8; ++k) {
+    w[2 * k] = k < K ? v[k].hi : 0;
+    w[2 * k + 1] = k < K ? v[k].lo : 0;
   }
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      sh[(2 * k) * kTW + warp] = v[k].hi;
-      sh[(2 * k + 1) * kTW + warp] = v[k].lo;
-    }
+  const long long ws = bfly16(w, lane);
+  if ((lane & 1) == 0) sh[bfly16_word(lane) * kTW + warp] = ws;
   asm volatile("bar.sync 1, %0;" ::"n"(kUT) : "memory");
   const int t = threadIdx.x - 32 * kUW;
   if (t < 2 * K) {
     long long s = 0;
 #pragma unroll
-    for (int w = kUW; w < kTW; ++w) s += sh[t * kTW + w];
+    for (int w2 = kUW; w2 < kTW; ++w2) s += sh[t * kTW + w2];
     const int word = word0 + t;
     if (x.world > 1 && ((all_mask >> (t >> 1)) & 1)) {
       for (int r = 0; r < x.world; ++r) red_sys_u64(x_acc(x, r, par) + word, s);
@@ -221,7 +215,6 @@ __device__ __forceinline__ bool tail_body(const TailArgs<T>& t, unsigned* bar) {
   using V = typename V16<T>::type;
   constexpr int R = 16 / sizeof(T);
   constexpr int BW = static_cast<int>(sizeof(Book<T>) / 8);
-  constexpr int TW = NT / 32;            // warps per CTA
   constexpr int UT = NT - 32 * kUW;      // update threads per CTA
   Book<T>* bk = t.book;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -289,13 +282,17 @@ __device__ __forceinline__ bool tail_body(const TailArgs<T>& t, unsigned* bar) {
   __shared__ long long shL[2 * 8 * 8];
   __shared__ long long shP[2 * 8 * 8];  // update sums (named-barrier reduction)
   __shared__ double s_tot[24];
+  __shared__ DecideIn<T> s_din;  // tail_decide's inputs (thread 0 only)
   const int64_t m = t.m, n = t.n;
+  const bool fg = t.fused_gate != 0;
   // the Book as this launch found it (CTA 0 of the previous tail or the host
   // wrote it; nobody writes it before barrier 1)
   if (tid < BW)
     reinterpret_cast<unsigned long long*>(&sbk)[tid] =
         __ldcg(reinterpret_cast<const unsigned long long*>(bk) + tid);
   const bool fp = bk->record_trace != 0;  // configuration: constant over the solve
+  // tail_decide's launch constants (thread 0 runs the decision)
+  if (fg && tid == 0) decide_consts<T>(&s_din, t);
 
   // this CTA's balanced range of [0, m + n): the update, and the merge in
   // fixed-point mode; update thread ut takes e0 + ut, e0 + ut + UT, ...
@@ -453,7 +450,6 @@ __device__ __forceinline__ bool tail_body(const TailArgs<T>& t, unsigned* bar) {
     xrank_barrier(X, par, 1, static_cast<unsigned>(X.world) * G, t.stamps, it_stamp);
   else
     count_barrier(ctr, static_cast<unsigned>(G), t.stamps, it_stamp);
-  const bool fg = t.fused_gate != 0;
   // s_tot: [0, 11) the A sums, [11] max|t|, [12] non-finite count,
   // [13, 21) the previous iteration's P sums
   if (tid < 11) {
@@ -488,8 +484,14 @@ __device__ __forceinline__ bool tail_body(const TailArgs<T>& t, unsigned* bar) {
   if (warp == 0) {
     if (lane == 0) {
       if (fg) {
-        tail_decide<T>(&sbk, t, tot8, pass_bad ? 1 : 0, s_tot[kXaPA], s_tot[kXaPR],
-                       s_tot[kXaQB], s_tot[kXaQS]);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s_din.tot[q] = tot8[q];
+        s_din.totbad = pass_bad ? 1 : 0;
+        s_din.sum_pa = s_tot[kXaPA];
+        s_din.sum_pr = s_tot[kXaPR];
+        s_din.sum_qb = s_tot[kXaQB];
+        s_din.sum_qs = s_tot[kXaQS];
+        tail_decide<T>(&sbk, &s_din);
         sbk.pend_buf = par;
         TAIL_STAMP(15);
       } else {
@@ -641,6 +643,390 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned
   tail_body<T, kTT>(t, bar);
 }
 
+// ---------------------------------------------------------------------------
+// KC: the same tail as ONE thread-block cluster (16 -- or 8 -- CTAs of
+// kCT threads in one GPC), for a single GPU in fixed-point mode when
+// m + n fits the cluster's update threads (kCK elements each: 28 672 at 16
+// CTAs).  The grid tail's two global round trips per reduction (arrival
+// atomics + spin on an L2 counter, then a load of the totals) become a
+// hardware cluster barrier and distributed-shared-memory reads; the 16 CTAs
+// leave 132 SMs to the next sweep, whose CTAs (programmatic dependents)
+// become resident and prime their rings while the tail runs.  The exact
+// integer sums make the totals independent of the partition, so KC and the
+// grid tail give bit-identical iterations (tests/test_tail_gpu.py).
+//   prologue  Book, the sweep's exact totals (complete: kernel boundary) and
+//             the previous iteration's update sums; each update thread loads
+//             its <= kCK elements' inputs at once
+//   A  merge  r = u - p, s = v - q from the fixed-point sums; CTA partials of
+//             the 7 merge sums -> cluster barrier 1 -> every CTA adds the C
+//             partials over DSMEM (same totals everywhere)
+//   B  warp 0: the decision; warp 1: the previous iteration's commit and
+//      patch; warps 2..: the update + its 8 exact sums, added into CTA 0's
+//      shared memory (DSMEM atomics) -> cluster barrier 2 -> CTA 0 stores the
+//      sums and the Book
+//   C  (only when the gate fired) exact dual value, recheck and the exact
+//      report, reduced the same way
+// ---------------------------------------------------------------------------
+constexpr int kCT = 512;                 // threads per cluster CTA
+constexpr int kCUT = kCT - 32 * kUW;     // update threads per cluster CTA
+constexpr int kCK = 4;                   // elements per update thread (at most)
+
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cluster_ctas() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+// every thread of every CTA of the cluster; release / acquire at cluster scope
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+               "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// address of this CTA's shared variable `p` in CTA `r` of the cluster
+__device__ __forceinline__ uint32_t dsmem(const void* p, unsigned r) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(a), "r"(r));
+  return out;
+}
+__device__ __forceinline__ long long ld_dsmem(uint32_t a) {
+  long long v;
+  asm volatile("ld.relaxed.cluster.shared::cluster.s64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_dsmem_s32(uint32_t a, int v) {
+  asm volatile("st.relaxed.cluster.shared::cluster.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_dsmem(uint32_t a, long long v) {
+  asm volatile("red.relaxed.cluster.shared::cluster.add.u64 [%0], %1;" ::"r"(a), "l"(v)
+               : "memory");
+}
+
+// per-CTA sums of K <= 8 HiLo values over the threads [32 * W0, NT): a warp
+// reduce-scatter (bfly16), then thread 32 * W0 + w adds word w over the
+// warps.  sync(): the barrier over exactly those threads.
+template <int NT, int K, int W0, class Sync>
+__device__ __forceinline__ long long cta_sum_hilo(HiLo (&v)[K], long long* sh, Sync sync) {
+  constexpr int kW = NT / 32;
+  static_assert(K <= 8, "16 words per lane");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  long long w[16];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    w[2 * k] = k < K ? v[k].hi : 0;
+    w[2 * k + 1] = k < K ? v[k].lo : 0;
+  }
+  const long long ws = bfly16(w, lane);
+  if ((lane & 1) == 0) sh[bfly16_word(lane) * kW + warp] = ws;
+  sync();
+  const int t = threadIdx.x - 32 * W0;
+  long long s = 0;
+  if (t >= 0 && t < 2 * K)
+#pragma unroll
+    for (int q = W0; q < kW; ++q) s += sh[t * kW + q];
+  return s;
+}
+
+template <class T>
+__global__ void __launch_bounds__(kCT, 1) ctail_kernel(const TailArgs<T> t) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  constexpr int BW = static_cast<int>(sizeof(Book<T>) / 8);
+  constexpr int kW = kCT / 32;
+  Book<T>* bk = t.book;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const unsigned C = cluster_ctas(), cr = cluster_rank();
+  const bool lead = cr == 0;  // CTA 0 decides and keeps the Book; CTAs 1.. update
+  const int par = t.tpar & 1;
+  long long* xa = t.xacc + par * kXaWords;
+  long long* xn = t.xacc + (par ^ 1) * kXaWords;
+  // a stopped loop: nothing to do (every CTA reads the same flag: the Book
+  // is only written after cluster barrier 2)
+  if (*reinterpret_cast<volatile int*>(&bk->stop)) return;
+  __shared__ Book<T> sbk;
+  __shared__ DecideIn<T> s_din;
+  __shared__ double s_tot[24];
+  __shared__ long long sh[2 * 8 * kW];
+  __shared__ long long s_part[16];  // this CTA's 7 merge sums (hi / lo)
+  __shared__ long long s_word[16];  // their cluster totals
+  __shared__ long long s_P[16];     // CTA 0: the cluster's 8 update sums
+  __shared__ long long s_R[4];      // CTA 0: the 2 report sums
+  __shared__ int s_flags;           // CTA 0's decision: failed | confirm << 1 | stop << 2
+  __shared__ CommitIn s_cin;        // CTA 0: commit_patch's inputs
+  const int64_t it_stamp = t.stamps ? *reinterpret_cast<volatile int64_t*>(&bk->iter) : 0;
+  TAIL_STAMP(2);
+  if (tid < BW) {
+    const unsigned long long w = __ldcg(reinterpret_cast<const unsigned long long*>(bk) + tid);
+    reinterpret_cast<unsigned long long*>(&sbk)[tid] = w;
+  }
+  if (lead) {
+    if (tid < kXaP) xn[tid] = 0;  // the next sweep's accumulators
+    if (tid >= 32 && tid < 48) s_P[tid - 32] = 0;
+    if (tid >= 64 && tid < 68) s_R[tid - 64] = 0;
+  }
+  // the sweep's totals (complete: kernel boundary) and the previous
+  // iteration's update sums (P of the other parity)
+  if (tid < 4) {
+    s_tot[tid] = hilo_value(__ldcg(xa + 2 * tid), __ldcg(xa + 2 * tid + 1));
+  } else if (tid == 4) {
+    s_tot[11] = __longlong_as_double(__ldcg(xa + kXaMax));
+  } else if (tid == 5) {
+    s_tot[12] = static_cast<double>(__ldcg(xa + kXaBad));
+  } else if (tid == 6 && lead) {
+    decide_consts<T>(&s_din, t);
+  } else if (tid >= 32 && tid < 40 && lead) {
+    const int k = tid - 32;
+    s_tot[13 + k] = hilo_value(__ldcg(xn + kXaP + 2 * k), __ldcg(xn + kXaP + 2 * k + 1));
+  }
+  const bool fp = bk->record_trace != 0;
+  const int64_t m = t.m, n = t.n, E = m + n;
+  // CTAs 1..C-1 share [0, m + n); update thread ut takes e0 + ut + k * kCUT
+  const int64_t e0 = lead ? 0 : static_cast<int64_t>(cr - 1) * E / (C - 1);
+  const int64_t e1 = lead ? 0 : static_cast<int64_t>(cr) * E / (C - 1);
+  const int ut = tid - 32 * kUW;
+  // element e is row e (e < m) or column e - m: the same code for both, on
+  // selected pointers (one compact body -- the tail's code is fetched cold
+  // every iteration, so its size is latency)
+  T f_ab[kCK], f_pq[kCK], f_old[kCK], f_rso[kCK], f_rs[kCK];
+  long long fxh[kCK], fxl[kCK];
+#pragma unroll
+  for (int k = 0; k < kCK; ++k) {
+    f_ab[k] = f_pq[k] = f_old[k] = f_rso[k] = f_rs[k] = T(0);
+    fxh[k] = fxl[k] = 0;
+    const int64_t e = e0 + ut + static_cast<int64_t>(k) * kCUT;
+    if (ut < 0 || e >= e1) continue;
+    const bool row = e < m;
+    const int64_t i = row ? e : e - m;
+    const long long* fxa = row ? t.ufx : t.vfx;
+    fxh[k] = __ldcg(fxa + i);
+    if (sizeof(T) == 8) fxl[k] = __ldcg(fxa + (row ? t.ld : n) + i);
+    f_ab[k] = ld_keep((row ? t.a : t.b) + i);
+    f_pq[k] = ld_keep((row ? t.p : t.q) + i);
+    f_old[k] = ld_keep((row ? t.phi : t.varphi) + i);
+    if (fp) f_rso[k] = ld_keep((row ? t.r_old : t.s_old) + i);
+  }
+  TAIL_STAMP(8);
+  // ---- A: merge (solver.hpp:269-272) and its exact sums ----------------------
+  // {sum r, |r|^2, |s|^2, sum p a, sum p r, sum q b, sum q s}
+  // (the updating CTAs' path first: the code of a kernel is fetched on
+  // demand, and the hot path placed first in the text measured ~3 us faster
+  // per tail than behind CTA 0's block)
+  if (!lead) {
+    HiLo hm[7];
+#pragma unroll
+    for (int k = 0; k < 7; ++k) hm[k] = HiLo{0, 0};
+#pragma unroll
+    for (int k = 0; k < kCK; ++k) {
+      const int64_t e = e0 + ut + static_cast<int64_t>(k) * kCUT;
+      if (ut < 0 || e >= e1) continue;
+      const bool row = e < m;
+      const int64_t i = row ? e : e - m;
+      long long* fxa = row ? t.ufx : t.vfx;
+      const double fv = sizeof(T) == 4 ? static_cast<double>(fxh[k]) * kFxInv
+                                       : static_cast<double>(fxh[k]) * kFxInv +
+                                             static_cast<double>(fxl[k]) * kFxLoInv;
+      fxa[i] = 0;
+      if (sizeof(T) == 8) fxa[(row ? t.ld : n) + i] = 0;
+      const T rs = static_cast<T>(fv) - f_pq[k];  // r = u - p, s = v - q
+      st_keep((row ? t.r_new : t.s_new) + i, rs, 2);
+      // rows: sum r, |r|^2, sum p a, sum p r; columns: |s|^2, sum q b, sum q s
+      const HiLo h0 = to_hilo(static_cast<double>(rs));
+      const HiLo h1 = to_hilo(static_cast<double>(rs * rs));
+      const HiLo h2 = to_hilo(static_cast<double>(f_pq[k]) * static_cast<double>(f_ab[k]));
+      const HiLo h3 = to_hilo(static_cast<double>(f_pq[k]) * static_cast<double>(rs));
+      if (row) {
+        hm[0].hi += h0.hi; hm[0].lo += h0.lo;
+        hm[1].hi += h1.hi; hm[1].lo += h1.lo;
+        hm[3].hi += h2.hi; hm[3].lo += h2.lo;
+        hm[4].hi += h3.hi; hm[4].lo += h3.lo;
+      } else {
+        hm[2].hi += h1.hi; hm[2].lo += h1.lo;
+        hm[5].hi += h2.hi; hm[5].lo += h2.lo;
+        hm[6].hi += h3.hi; hm[6].lo += h3.lo;
+      }
+      f_rs[k] = rs;
+    }
+    const long long s = cta_sum_hilo<kCT, 7, 0>(hm, sh, [] { __syncthreads(); });
+    if (tid < 14) s_part[tid] = s;
+    TAIL_STAMP(3);
+    cluster_sync_all();  // (1) every CTA's merge partials are in its shared memory
+  } else {
+    // CTA 0 has no elements (it runs the scalar logic after the barrier)
+    if (tid < 16) s_part[tid] = 0;
+    TAIL_STAMP(3);
+    cluster_sync_all();
+  }
+  TAIL_STAMP(10);
+  if (tid < 14) {  // word tid over the C CTAs: 16 loads in flight (C = 8 or 16)
+    long long v[16];
+#pragma unroll
+    for (unsigned c = 0; c < 16; ++c) v[c] = ld_dsmem(dsmem(&s_part[tid], c & (C - 1)));
+    long long sum = 0;
+#pragma unroll
+    for (unsigned c = 0; c < 16; ++c) sum += c < C ? v[c] : 0;
+    s_word[tid] = sum;
+  }
+  __syncthreads();
+  if (tid < 7) s_tot[kXaSumR + tid] = hilo_value(s_word[2 * tid], s_word[2 * tid + 1]);
+  __syncthreads();
+  TAIL_STAMP(11);
+  const T tot8[8] = {static_cast<T>(s_tot[kXaCost]), static_cast<T>(s_tot[kXaPrev]),
+                     static_cast<T>(s_tot[kXaDual]), static_cast<T>(s_tot[kXaDx]),
+                     static_cast<T>(s_tot[11]),      static_cast<T>(s_tot[kXaSumR]),
+                     static_cast<T>(s_tot[kXaR2]),   static_cast<T>(s_tot[kXaS2])};
+  const bool pass_bad = s_tot[12] > 0.0;
+  // the previous iteration's commit record, before the decision overwrites it
+  CommitRec crec{};
+  if (lead && tid == 32) crec = commit_snap(sbk);
+  __syncthreads();
+  // ---- B: CTA 0: decision (warp 0) | commit + patch (warp 1);
+  //         CTAs 1..: the update (warps 2..) ------------------------------------
+  if (!lead) {
+    if (warp >= kUW) {
+      // coef as merge_scalars forms it (solver.hpp:273-277)
+      const T beta_all = tot8[5] / static_cast<T>(t.m_global + t.n_global);
+      const T coef = T(2) * beta_all - sbk.alpha;
+      HiLo hp[8];
+  #pragma unroll
+      for (int k = 0; k < 8; ++k) hp[k] = HiLo{0, 0};
+      if (!pass_bad) {
+        const T inv_n = T(1) / static_cast<T>(t.n_global);
+        const T inv_m = T(1) / static_cast<T>(t.m_global);
+        const double drho = static_cast<double>(t.rho);
+#pragma unroll
+        for (int k = 0; k < kCK; ++k) {
+          const int64_t e = e0 + ut + static_cast<int64_t>(k) * kCUT;
+          if (e >= e1) continue;
+          const bool row = e < m;
+          const int64_t i = row ? e : e - m;
+          // phi = (a - 2 r + coef) / n, varphi = (b - 2 s + coef) / m
+          // (solver.hpp:280-285); a -= r, b -= s (solver.hpp:287-288)
+          const T ph = (f_ab[k] - T(2) * f_rs[k] + coef) * (row ? inv_n : inv_m);
+          st_keep((row ? t.phi : t.varphi) + i, ph, 2);
+          st_keep((row ? t.a : t.b) + i, f_ab[k] - f_rs[k], 2);
+          const double d = static_cast<double>(ph) - static_cast<double>(f_old[k]);
+          const HiLo g0 = to_hilo(static_cast<double>(f_pq[k]) * static_cast<double>(ph) / drho);
+          const int o = row ? 0 : 4;
+#pragma unroll
+          for (int q = 0; q < 8; q += 4)
+            if (o == q) {
+              hp[q].hi += g0.hi;
+              hp[q].lo += g0.lo;
+            }
+          if (fp) {
+            const HiLo g1 = to_hilo(d * d), g2 = to_hilo(d);
+            const HiLo g3 = to_hilo(d * (static_cast<double>(f_rs[k]) - static_cast<double>(f_rso[k])));
+#pragma unroll
+            for (int q = 0; q < 8; q += 4)
+              if (o == q) {
+                hp[q + 1].hi += g1.hi; hp[q + 1].lo += g1.lo;
+                hp[q + 2].hi += g2.hi; hp[q + 2].lo += g2.lo;
+                hp[q + 3].hi += g3.hi; hp[q + 3].lo += g3.lo;
+              }
+          }
+        }
+      }
+      if (t.stamps && tid == 32 * kUW) timeline_point(t.stamps, it_stamp, 13, global_ns());
+      const long long s = cta_sum_hilo<kCT, 8, kUW>(hp, sh, [] {
+        asm volatile("bar.sync 1, %0;" ::"n"(kCUT) : "memory");
+      });
+      if (ut < 16 && s != 0) red_dsmem(dsmem(&s_P[ut], 0), s);
+      if (t.stamps && tid == 32 * kUW) timeline_point(t.stamps, it_stamp, 14, global_ns());
+    }
+  } else {
+    if (tid == 0) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s_din.tot[q] = tot8[q];
+      s_din.totbad = pass_bad ? 1 : 0;
+      s_din.sum_pa = s_tot[kXaPA];
+      s_din.sum_pr = s_tot[kXaPR];
+      s_din.sum_qb = s_tot[kXaQB];
+      s_din.sum_qs = s_tot[kXaQS];
+      tail_decide<T>(&sbk, &s_din);
+      sbk.pend_buf = par;
+      const int f = (sbk.failed ? 1 : 0) | (sbk.confirm ? 2 : 0) | (sbk.stop << 2);
+      for (unsigned c = 0; c < C; ++c) st_dsmem_s32(dsmem(&s_flags, c), f);
+      TAIL_STAMP(15);
+    } else if (tid == 32 && crec.valid) {
+      // the previous iteration's commit and exact dual / fixed-point patch
+      // (it reads nothing the decision writes)
+      s_cin.c = crec;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s_cin.d8[k] = s_tot[13 + k];
+      s_cin.trace = t.trace;
+      s_cin.n_global = t.n_global;
+      s_cin.m_global = t.m_global;
+      s_cin.write_trace = 1;
+      commit_patch<T>(&sbk, &s_cin);
+    }
+  }
+  cluster_sync_all();  // (2) the update sums are in CTA 0, the decision everywhere
+  TAIL_STAMP(12);
+  if (lead && tid < 16) xa[kXaP + tid] = s_P[tid];
+  book_store_cta0(bk, &sbk);
+  TAIL_STAMP(4);
+  if ((s_flags & 1) || !(s_flags & 2) || (s_flags >> 2) == 1) {
+    TAIL_STAMP(6);
+    return;  // (no CTA reads another's shared memory after barrier 2)
+  }
+  // ---- C: the gate fired: exact dual value and the reference's gap test -----
+  if (lead && tid == 0) {
+    double d8[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) d8[k] = hilo_value(s_P[2 * k], s_P[2 * k + 1]);
+    const CommitRec c = commit_snap(sbk);
+    tail_commit<T>(&sbk, t, c, true);
+    sbk.cm_valid = 0;
+    patch_pending<T>(&sbk, t, d8, true);
+    gate_recheck<T>(&sbk);
+    const int f = (sbk.confirm ? 2 : 0) | (sbk.stop << 2);
+    for (unsigned cc = 0; cc < C; ++cc) st_dsmem_s32(dsmem(&s_flags, cc), f);
+  }
+  book_store_cta0(bk, &sbk);
+  cluster_sync_all();  // (3) the recheck's flags are everywhere
+  if (!(s_flags & 2) || (s_flags >> 2) == 1) return;
+  // exact confirm report of (X_{k+1}, phi / rho, varphi / rho) over the cluster
+  {
+    using V = typename V16<T>::type;
+    constexpr int R = 16 / sizeof(T);
+    const bool folded = t.folded_after != 0;
+    const double drho = static_cast<double>(t.rho);
+    const int64_t ngx = (m + int64_t(kCT) * R - 1) / (int64_t(kCT) * R);
+    const int64_t ncs = imin64(n, (2 * static_cast<int64_t>(C) + ngx - 1) / ngx);
+    HiLo hr[2] = {HiLo{0, 0}, HiLo{0, 0}};
+    for (int64_t unit = cr; unit < ngx * ncs; unit += C) {
+      const int64_t rx = unit % ngx, cs = unit / ngx;
+      const int64_t row0 = (rx * kCT + tid) * R;
+      if (row0 >= m) continue;
+      const int nvalid = static_cast<int>(imin64(R, m - row0));
+      double mu[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+        mu[k] = k < nvalid ? static_cast<double>(__ldcg(t.phi + row0 + k)) / drho : 0.0;
+      for (int64_t j = cs; j < n; j += ncs) {
+        const double nu_j = static_cast<double>(__ldcg(t.varphi + j)) / drho;
+        T xv[R], cv[R];
+        unpack(__ldcs(reinterpret_cast<const V*>(t.report_x + j * t.ld + row0)), xv);
+        unpack(__ldcs(reinterpret_cast<const V*>(t.report_c + j * t.ld + row0)), cv);
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+          if (k < nvalid) report_elem_exact<T>(xv[k], cv[k], mu[k], nu_j, t.rho, folded, hr);
+      }
+    }
+    __syncthreads();  // sh is reused
+    const long long s = cta_sum_hilo<kCT, 2, 0>(hr, sh, [] { __syncthreads(); });
+    if (tid < 4 && s != 0) red_dsmem(dsmem(&s_R[tid], 0), s);
+  }
+  cluster_sync_all();  // (4) the report sums are in CTA 0
+  if (!lead) return;
+  if (tid == 0)
+    report_decide<T>(&sbk, hilo_value(s_R[0], s_R[1]), hilo_value(s_R[2], s_R[3]), 0);
+  book_store_cta0(bk, &sbk);
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -769,9 +1155,67 @@ int tail_grid(int device) {
   return sms * (per < want ? per : want);
 }
 
+// CTAs per cluster of the cluster tail on `device`: 16 (a non-portable
+// size) when such a cluster of kCT-thread CTAs can be resident, else 8, else 0
+template <class T>
+int ctail_ctas(int device) {
+  static std::atomic<int> cache[64];  // per device: 0 unknown, else size + 1
+  std::atomic<int>& slot = cache[device & 63];
+  const int got = slot.load(std::memory_order_acquire);
+  if (got > 0) return got - 1;
+  int size = 0;
+  cudaFuncSetAttribute(ctail_kernel<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  // max carveout, as the grid tail and K1 (see tail_grid)
+  cudaFuncSetAttribute(ctail_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
+  for (const int c : {16, 8}) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(c));
+    cfg.blockDim = dim3(kCT);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = static_cast<unsigned>(c);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, ctail_kernel<T>, &cfg) == cudaSuccess && nc > 0) {
+      size = c;
+      break;
+    }
+  }
+  (void)cudaGetLastError();
+  slot.store(size + 1, std::memory_order_release);
+  return size;
+}
+
 template <class T>
 cudaError_t launch_tail(const TailArgs<T>& t, T* cpart, double* dpart, unsigned* bar, int grid,
                         cudaStream_t st) {
+  // one GPU, fixed-point sums, fused gate, m + n within the cluster's update
+  // threads: the cluster tail (same results, shorter critical path)
+  if (t.ctail > 0 && t.x.world <= 1 && !t.sharded && t.fx && t.fused_gate && !t.pdl) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int hw = ctail_ctas<T>(dev);
+    const int c = hw < t.ctail ? hw : t.ctail;
+    if (c > 0 && t.m + t.n <= static_cast<int64_t>(c - 1) * kCUT * kCK) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(static_cast<unsigned>(c));
+      cfg.blockDim = dim3(kCT);
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = static_cast<unsigned>(c);
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      count_launch();
+      return cudaLaunchKernelEx(&cfg, ctail_kernel<T>, t);
+    }
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
   cfg.blockDim = dim3(kTT);

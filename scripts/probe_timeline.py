@@ -1,5 +1,7 @@
 """Dev aid: device timeline of the solve loop (DROTB_TAIL_STAMPS=1), CUDA
-graphs as in the bench.  Per iteration (averaged over 60): K1 entry / exit,
+graphs as in the bench.  The stamps are global atomics: they slow the tail
+by several us -- read the phases' order and relative length here, and time
+iterations with scripts/probe_iter.py.  Per iteration (averaged over 60): K1 entry / exit,
 tail entry, merge done, scalar section done, update done, tail exit, all
 relative to the first K1 CTA entry of that iteration.
 usage: python scripts/probe_timeline.py [m] [dtype] [iters]"""
@@ -27,7 +29,7 @@ s.init()
 s.enqueue(8)
 s.prepare(K)
 s.synchronize()
-buf = (C.c_uint64 * 2048)()
+buf = (C.c_uint64 * 3072)()
 _lib.load().drotb_session_tail_stamps(s.handle, buf)  # reset
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(st)
@@ -35,11 +37,12 @@ s.enqueue(K)
 e1.record(st)
 torch.cuda.synchronize()
 _lib.load().drotb_session_tail_stamps(s.handle, buf)
-a = np.array(list(buf), dtype=np.float64).reshape(64, 16, 2)
+a = np.array(list(buf), dtype=np.float64).reshape(64, 24, 2)
 it0 = 8
 names = ["K1 entry", "K1 exit", "tail entry", "merge done", "book stored", "update done", "tail exit",
-         "strips loaded", "r/s stored", "K1 slice ld", "barrier passed", "totals loaded",
-         "join (all roles)", "update done(w2)", "upd sums red(w2)", "decide done(w0)"]
+         "K1 swept/strips", "r/s stored", "K1 released", "barrier passed", "totals loaded",
+         "join (all roles)", "update done(w2)", "upd sums red(w2)", "decide done(w0)",
+         "pt16", "pt17", "pt18", "pt19", "pt20", "pt21", "pt22", "pt23"]
 NP = len(names)
 rows = []
 for k in range(it0 + 2, it0 + K - 1):
@@ -54,7 +57,7 @@ r = np.array(rows)
 mean = r.mean(axis=0)
 print(f"{m}x{m} {np.dtype(dt).name}: {len(r)} iterations, graph-timed "
       f"{e0.elapsed_time(e1) * 1e3 / K:.1f} us/iter; mean us after the first K1 CTA entry:")
-order = [0, 1, 2, 7, 8, 9, 3, 10, 11, 15, 13, 14, 12, 4, 5, 6]
+order = [0, 9, 7, 1, 2, 8, 3, 10, 11, 15, 13, 14, 12, 4, 5, 6]
 for p in order:
     if mean[p] > 1e9:  # point not recorded
         continue
@@ -64,8 +67,10 @@ print(f"  next K1 entry      {nx:8.1f}")
 print(f"  gaps: K1 last exit -> tail first entry {mean[2] - mean[NP + 1]:.1f} us; "
       f"tail last exit -> next K1 entry {nx - mean[NP + 6]:.1f} us; "
       f"tail span {mean[NP + 6] - mean[2]:.1f} us; K1 span {mean[NP + 1] - mean[0]:.1f} us")
-for k in (0, 1):  # fold / skip iterations separately
+for k in (0, 1):  # the two iteration parities (fold / skip-cost sweeps) separately
     sub = r[k::2]
+    mk = sub.mean(axis=0)
     print(f"  parity {k}: K1 span {np.mean(sub[:, NP + 1] - sub[:, 0]):.1f} us, "
-          f"iteration {np.mean(sub[:, 2 * NP]):.1f} us")
+          f"iteration {np.mean(sub[:, 2 * NP]):.1f} us; " +
+          ", ".join(f"{names[p]} {mk[p]:.1f}/{mk[NP + p]:.1f}" for p in order if mk[p] < 1e9))
 s.close()

@@ -33,10 +33,10 @@ class _env:
                 os.environ[k] = v
 
 
-def _run(drot, m, n, dt, iters=None, legacy=False, **kw):
-    with _env(DROTB_TAIL="legacy" if legacy else "coop"):
+def _run(drot, m, n, dt, iters=None, legacy=False, ctail="16", gen=4, **kw):
+    with _env(DROTB_TAIL="legacy" if legacy else "coop", DROTB_CTAIL=ctail):
         s = drot.Session(m, n, dt, drot.DrotConfig(**kw))
-    s.gen_gaussian(5.0, 4, "dyadic")
+    s.gen_gaussian(5.0, gen, "dyadic")
     s.init()
     if iters is None:
         s.run()
@@ -154,3 +154,36 @@ def test_max_iters_report_gap(drot, dt):
     dual = float(p @ mu.astype(np.float64) + q @ nu.astype(np.float64))
     assert abs(rep.gap - abs(rep.objective - dual)) <= 1e-9 * abs(rep.objective) + 1e-12, \
         (rep.gap, rep.objective, dual)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("shape", [(700, 500), (3000, 2000), (9000, 7000)])
+def test_cluster_tail_equals_grid_tail(drot, dt, shape):
+    """The cluster tail (KC, tail.cu: one 16- or 8-CTA cluster, DSMEM
+    reductions) and the grid tail (148 CTAs, counter barriers) sum the same
+    exact integers: bitwise identical iterates, duals and reports.  9000 +
+    7000 elements exceed an 8-CTA cluster (7 updating CTAs: 12 544 slots,
+    so the grid tail runs) but fit 16 (26 880)."""
+    m, n = shape
+    kw = dict(iters=30, tol_primal=-1.0, max_iters=10 ** 9)
+    grid = _run(drot, m, n, dt, ctail="0", **kw)
+    for cap in ("16", "8"):
+        clu = _run(drot, m, n, dt, ctail=cap, **kw)
+        assert grid[0][1] == clu[0][1] == 30
+        for x, y in zip(grid[1:], clu[1:]):
+            np.testing.assert_array_equal(x, y)
+        assert grid[0][2].objective == clu[0][2].objective
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_cluster_tail_solve_equals_grid_tail(drot, dt):
+    """To convergence (the fused gate fires, the confirm report runs inside
+    the cluster): same status, iteration count and report, bitwise."""
+    a = _run(drot, 500, 400, dt, ctail="0", max_iters=80000)
+    b = _run(drot, 500, 400, dt, ctail="16", max_iters=80000)
+    assert a[0][0] == b[0][0] == drot.SolveStatus.converged
+    assert a[0][1] == b[0][1]
+    for f in ("objective", "r_primal", "r_dual", "gap"):
+        assert getattr(a[0][2], f) == getattr(b[0][2], f), f
+    for x, y in zip(a[1:], b[1:]):
+        np.testing.assert_array_equal(x, y)
