@@ -581,8 +581,7 @@ __device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0
 
 
 // One K1 tile (row block bx, column tile by): the body of pass_kernel_async
-// after its prologue, shared with the small-problem solver kernel (tail.cu),
-// which walks the same tiles -- so both produce the same per-tile sums.
+// after its prologue (one tile per CTA).
 // primed: the first ring stages were issued (ring_prime) by the caller.
 template <class T, int MODE, bool DUAL, bool DX>
 __device__ __forceinline__ void k1_tile(const PassArgs<T>& a, int64_t bx, int64_t by,
@@ -674,7 +673,7 @@ __device__ __forceinline__ void k1_tile(const PassArgs<T>& a, int64_t bx, int64_
     }
     if (a.stamps) timeline_point(a.stamps, it_stamp, 1, global_ns());
   }
-  __syncthreads();  // wacc and the ring / staging buffers are reused by the next tile
+  // (one tile per CTA: nothing reuses wacc or the ring after this)
 }
 
 // ---------------------------------------------------------------------------

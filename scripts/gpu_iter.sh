@@ -1,6 +1,5 @@
 #!/bin/bash
-# graph-timed us/iteration: cluster tail vs grid tail
+# graph-timed us/iteration
 for cfg in "1000 f64" "10000 f32" "2000 f64"; do
-  DROTB_CTAIL=16 timeout 300 python scripts/probe_iter.py $cfg 2>&1 | tail -1
-  DROTB_CTAIL=0 timeout 300 python scripts/probe_iter.py $cfg 2>&1 | tail -1
+  timeout 300 python scripts/probe_iter.py $cfg 2>&1 | tail -1
 done

@@ -1,4 +1,5 @@
-"""Dev aid: C1 drot.solve() wall time, first and repeated calls."""
+"""Dev aid: C1 drot.solve() wall time (first and repeated calls) and the
+fixed per-call overhead (max_iters 1 / 1000 calls of the same shape)."""
 import os
 import sys
 import time
@@ -15,3 +16,10 @@ for k in range(3):
     t0 = time.perf_counter()
     res = drot.solve(prob, drot.DrotConfig())
     print(f"call {k}: {time.perf_counter() - t0:.3f} s, {res.trace.iterations} iterations", flush=True)
+for it in (1, 1000, 10000):
+    ts = []
+    for k in range(3):
+        t0 = time.perf_counter()
+        res = drot.solve(prob, drot.DrotConfig(max_iters=it))
+        ts.append(time.perf_counter() - t0)
+    print(f"max_iters {it}: {min(ts) * 1e3:.2f} ms ({res.trace.iterations} iterations)", flush=True)

@@ -17,7 +17,10 @@ K = int(sys.argv[3]) if len(sys.argv) > 3 else 400
 s = drot.Session(m, m, dt, drot.DrotConfig(tol_primal=-1.0, max_iters=10 ** 12))
 st = torch.cuda.Stream()
 s.set_stream(st.cuda_stream)
-s.gen_gaussian(5.0, 0, "dyadic")
+if os.environ.get("PROBE_UNIFORM"):
+    s.gen_uniform(1, 0.0, 1.0, "uniform")
+else:
+    s.gen_gaussian(5.0, 0, "dyadic")
 s.init()
 s.enqueue(16)
 s.prepare(K)
