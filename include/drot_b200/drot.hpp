@@ -569,7 +569,8 @@ SolveResult<T> sinkhorn_solve(const TransportProblem<T>& pr, T eta, double tol,
   res.cert.nu.assign(n, T(0));
   res.cert.rho = eta;
   const std::int64_t ce = check_every < 1 ? 1 : check_every;
-  const std::int64_t cap = (max_iters > 0 ? max_iters : 0) / ce + 2;
+  const std::int64_t cap =
+      std::min<std::int64_t>((max_iters > 0 ? max_iters : 0) / ce + 2, std::int64_t(1) << 23);
   std::vector<drotb_trace_row> tr(static_cast<std::size_t>(cap));
   drotb_report r{};
   int64_t tlen = 0, iters = 0;

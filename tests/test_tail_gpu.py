@@ -187,3 +187,28 @@ def test_cluster_tail_solve_equals_grid_tail(drot, dt):
         assert getattr(a[0][2], f) == getattr(b[0][2], f), f
     for x, y in zip(a[1:], b[1:]):
         np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_cluster_tail_trace_equals_grid_tail(drot, dt):
+    """The trace rows (written by the tail's deferred commit and patched with
+    the exact dual value / fixed-point residual one iteration later, or by
+    the finalize kernel) are identical for the cluster and the grid tail."""
+    m, n = 260, 300
+    C = np.asfortranarray(drot.random_matrix(m, n, 5).astype(dt))
+    prob = drot.TransportProblem(C, drot.dyadic_marginal(m, dt), drot.dyadic_marginal(n, dt))
+    res = []
+    for ct in ("0", "16"):
+        with _env(DROTB_TAIL="coop", DROTB_CTAIL=ct):
+            drot.release_device_cache()
+            res.append(drot.solve(prob, drot.DrotConfig(max_iters=60000, trace_every=7)))
+            drot.release_device_cache()
+    a, b = res
+    assert a.status == b.status and a.trace.iterations == b.trace.iterations
+    assert len(a.trace.rows) == len(b.trace.rows) > 10
+    for ra, rb in zip(a.trace.rows, b.trace.rows):
+        for f in ("iter", "r_primal", "r_dual", "gap", "objective", "ergodic_objective",
+                  "fixed_point_residual"):
+            x, y = getattr(ra, f), getattr(rb, f)
+            assert x == y or (np.isnan(x) and np.isnan(y)), (ra.iter, f, x, y)
+    np.testing.assert_array_equal(a.plan.x, b.plan.x)
