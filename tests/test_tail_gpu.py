@@ -157,19 +157,21 @@ def test_max_iters_report_gap(drot, dt):
 
 
 @pytest.mark.parametrize("dt", [np.float32, np.float64])
-@pytest.mark.parametrize("shape", [(700, 500), (3000, 2000), (9000, 7000)])
+@pytest.mark.parametrize("shape", [(700, 500), (3000, 2000), (9000, 7000), (13440, 13440),
+                                   (13441, 13440)])
 def test_cluster_tail_equals_grid_tail(drot, dt, shape):
     """The cluster tail (KC, tail.cu: one 16- or 8-CTA cluster, DSMEM
     reductions) and the grid tail (148 CTAs, counter barriers) sum the same
     exact integers: bitwise identical iterates, duals and reports.  9000 +
     7000 elements exceed an 8-CTA cluster (7 updating CTAs: 12 544 slots,
-    so the grid tail runs) but fit 16 (26 880)."""
+    so the grid tail runs) but fit 16 (26 880: 13 440 + 13 440 uses every
+    slot, one more row falls back to the grid tail)."""
     m, n = shape
-    kw = dict(iters=30, tol_primal=-1.0, max_iters=10 ** 9)
+    kw = dict(iters=30 if m < 10000 else 12, tol_primal=-1.0, max_iters=10 ** 9)
     grid = _run(drot, m, n, dt, ctail="0", **kw)
     for cap in ("16", "8"):
         clu = _run(drot, m, n, dt, ctail=cap, **kw)
-        assert grid[0][1] == clu[0][1] == 30
+        assert grid[0][1] == clu[0][1] == kw["iters"]
         for x, y in zip(grid[1:], clu[1:]):
             np.testing.assert_array_equal(x, y)
         assert grid[0][2].objective == clu[0][2].objective
