@@ -7,6 +7,6 @@ for f in test_tail_gpu test_report_gpu test_probgen_gpu test_sinkhorn_gpu test_s
   echo "== $f"; grep -E "ERROR SUMMARY|passed|failed|^rc" gpurun_out/mc_$f.log | tail -4
 done
 for tool in racecheck synccheck; do
-  timeout 900 compute-sanitizer --tool $tool --print-limit 10 python -m pytest tests/test_tail_gpu.py -m gpu -q -x -k "cluster and 700" --timeout 900 > gpurun_out/${tool}_tail.log 2>&1; echo "rc $?" >> gpurun_out/${tool}_tail.log
+  timeout 900 compute-sanitizer --tool $tool --print-limit 10 python -m pytest tests/test_tail_gpu.py -m gpu -q -x -k "cluster_tail_equals_grid_tail and shape0" --timeout 900 > gpurun_out/${tool}_tail.log 2>&1; echo "rc $?" >> gpurun_out/${tool}_tail.log
   echo "== $tool tail"; grep -E "ERROR SUMMARY|RACECHECK SUMMARY|passed|failed|^rc" gpurun_out/${tool}_tail.log | tail -4
 done
