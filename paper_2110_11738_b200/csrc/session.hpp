@@ -304,10 +304,17 @@ struct Session {
                 int64_t* n_pass, double* pass_bytes, int64_t* launches);
 
   int64_t batch_iters() const {
-    // ~1 ms of pass traffic per batch at ~6 TB/s, at least 8 iterations
-    const double bytes = 3.0 * sizeof(T) * static_cast<double>(m) * n;
-    const double t_iter = bytes / 6.0e12 + 20e-6;
-    int64_t bi = static_cast<int64_t>(1e-3 / t_iter) + 1;
+    // ~3.5 ms of work per graph: each graph boundary breaks the sweep's
+    // programmatic-launch chain and the run loop adds a stop-flag copy per
+    // batch; the host reads the flag one batch behind, so a stop costs at
+    // most two batches of early-exit launches.  At least 8 iterations.
+    if (const char* e = std::getenv("DROTB_BATCH")) {  // tuning aid
+      const int64_t v = std::atoll(e);
+      if (v >= 2) return v + (v & 1);
+    }
+    const double bytes = 2.5 * sizeof(T) * static_cast<double>(m) * n;
+    const double t_iter = bytes / 6.0e12 + 10e-6;
+    int64_t bi = static_cast<int64_t>(3.5e-3 / t_iter) + 1;
     bi = std::max<int64_t>(8, std::min<int64_t>(bi, 256));
     return bi + (bi & 1);
   }

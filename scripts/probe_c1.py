@@ -23,3 +23,11 @@ for it in (1, 1000, 10000):
         res = drot.solve(prob, drot.DrotConfig(max_iters=it))
         ts.append(time.perf_counter() - t0)
     print(f"max_iters {it}: {min(ts) * 1e3:.2f} ms ({res.trace.iterations} iterations)", flush=True)
+# the same iteration count without the gate (tol -1): the gate / confirm cost
+for label, kw in (("gated", {}), ("no gate", {"tol_primal": -1.0})):
+    ts = []
+    for k in range(2):
+        t0 = time.perf_counter()
+        res = drot.solve(prob, drot.DrotConfig(max_iters=36041, **kw))
+        ts.append(time.perf_counter() - t0)
+    print(f"{label}: {min(ts):.3f} s ({res.trace.iterations} iterations)", flush=True)
