@@ -374,6 +374,11 @@ def run_b200(args, rank, world, local_rank):
         e2e = run_e2e(args, drot, torch, m, n, local_rank)
         if out is not None:
             out["e2e"] = e2e
+    # ---- time to tolerance (C1: 1000x1000 fp64, the results-oracle config) --
+    # (before the CPU baseline: the reference's host thread pool would compete
+    # with the solve loop's host thread)
+    if rank == 0 and not args.no_ttt:
+        out["time_to_tol"] = time_to_tol(drot)
     # ---- CPU baseline (rank 0, N = 1 only) ----------------------------------
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ips, cores, kind, k_run, total = reference_iters_per_s(m, n, args.cpu_iters, 1)
@@ -382,9 +387,6 @@ def run_b200(args, rank, world, local_rank):
             "sample": f"{k_run} iterations of reference solve<float> on the same 10k x 10k fp32 "
                       f"instance, record_trace on (solve(max_iters={1 + k_run}) - "
                       f"solve(max_iters=1)), {total:.1f} s wall, {cores} host threads"}
-    # ---- time to tolerance (C1: 1000x1000 fp64, the results-oracle config) --
-    if rank == 0 and not args.no_ttt:
-        out["time_to_tol"] = time_to_tol(drot)
     if out is not None:
         print(json.dumps(out), flush=True)
     if dist is not None:

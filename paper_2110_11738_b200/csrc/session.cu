@@ -182,9 +182,9 @@ int Session<T>::setup_coop_tail() {
 // latency), in multiples of the 16-column staging chunk, at most 256.
 template <class T>
 int64_t Session<T>::fast_tile_cols() const {
-  if (const char* e = std::getenv("DROTB_TC")) {  // tuning aid
+  if (const char* e = std::getenv("DROTB_TC")) {  // tuning aid (any even width)
     const int64_t v = std::atoll(e);
-    if (v >= kChunkCols) return round_up(v, kChunkCols);
+    if (v >= 2) return round_up(v, 2);
   }
   constexpr int R = 16 / sizeof(T);
   const int64_t rows_cta = int64_t(kWarpsPerCta) * 32 * R;
