@@ -70,10 +70,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, DROTB_ASYNC_MINB)
   // sweep CTAs per SM and waits in its own griddepcontrol.wait
   if (a.trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (a.stop != nullptr && *reinterpret_cast<const volatile int*>(a.stop)) {
-    cp_async_wait<0>();
-    return;
-  }
+  // (the stop flag is read inside the tile, once phi / varphi are in flight)
   const int64_t it_stamp = a.stamps ? *reinterpret_cast<const volatile int64_t*>(a.iter) : 0;
   if (a.stamps && threadIdx.x == 0) {
     timeline_point(a.stamps, it_stamp, 0, t_entry);

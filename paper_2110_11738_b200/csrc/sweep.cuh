@@ -500,8 +500,11 @@ __device__ __forceinline__ void ring_prime(const PassArgs<T>& a, int64_t c0, int
 }
 
 // PRIMED: the caller issued the first S-1 stages (ring_prime)
+// Returns true when the loop's stop flag (a.stop) is set: read only after
+// the first loads of the tile are in flight (its latency overlaps theirs),
+// and before anything is written.
 template <class T, int MODE, bool DUAL, bool DX, bool MASK, bool PRIMED = false>
-__device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0, int64_t c1,
+__device__ __forceinline__ bool pass_tile_async(const PassArgs<T>& a, int64_t c0, int64_t c1,
                                                 int64_t wrow0, int64_t row0, int nvalid,
                                                 const T (&ph)[16 / sizeof(T)],
                                                 T (&u)[16 / sizeof(T)], PassAcc<T>& acc,
@@ -549,6 +552,10 @@ __device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0
         vb[st][k] = col < c1 ? __ldg(a.varphi + col) : T(0);
       }
   }
+  if (a.stop != nullptr && *reinterpret_cast<const volatile int*>(a.stop)) {
+    cp_async_wait<0>();
+    return true;
+  }
   for (int64_t j0 = c0; j0 < c1; j0 += CH) {
 #pragma unroll
     for (int gg = 0; gg < NG; ++gg) {
@@ -577,6 +584,7 @@ __device__ __forceinline__ void pass_tile_async(const PassArgs<T>& a, int64_t c0
     __syncwarp();
   }
   cp_async_wait<0>();
+  return false;
 }
 
 
@@ -613,21 +621,23 @@ __device__ __forceinline__ void k1_tile(const PassArgs<T>& a, int64_t bx, int64_
   for (int t = 0; t < R; ++t) u[t] = T(0);
   PassAcc<T> acc{T(0), T(0), T(0), T(0), T(0), false};
   const bool full = __all_sync(0xffffffffu, nvalid == R);
+  bool stopped;
   if (primed) {
     if (full)
-      pass_tile_async<T, MODE, DUAL, DX, false, true>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc,
-                                                      wbuf, ring, lane);
+      stopped = pass_tile_async<T, MODE, DUAL, DX, false, true>(a, c0, c1, wrow0, row0, nvalid,
+                                                                ph, u, acc, wbuf, ring, lane);
     else
-      pass_tile_async<T, MODE, DUAL, DX, true, true>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc,
-                                                     wbuf, ring, lane);
+      stopped = pass_tile_async<T, MODE, DUAL, DX, true, true>(a, c0, c1, wrow0, row0, nvalid,
+                                                               ph, u, acc, wbuf, ring, lane);
   } else {
     if (full)
-      pass_tile_async<T, MODE, DUAL, DX, false>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc, wbuf,
-                                                ring, lane);
+      stopped = pass_tile_async<T, MODE, DUAL, DX, false>(a, c0, c1, wrow0, row0, nvalid, ph, u,
+                                                          acc, wbuf, ring, lane);
     else
-      pass_tile_async<T, MODE, DUAL, DX, true>(a, c0, c1, wrow0, row0, nvalid, ph, u, acc, wbuf,
-                                               ring, lane);
+      stopped = pass_tile_async<T, MODE, DUAL, DX, true>(a, c0, c1, wrow0, row0, nvalid, ph, u,
+                                                         acc, wbuf, ring, lane);
   }
+  if (stopped) return;  // (every thread reads the same flag)
   if (a.stamps && threadIdx.x == 0) timeline_point(a.stamps, it_stamp, 7, global_ns());
   if (a.fx) {
 #pragma unroll

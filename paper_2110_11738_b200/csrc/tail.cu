@@ -743,9 +743,6 @@ __global__ void __launch_bounds__(kCT, 1) ctail_kernel(const TailArgs<T> t) {
   const int par = t.tpar & 1;
   long long* xa = t.xacc + par * kXaWords;
   long long* xn = t.xacc + (par ^ 1) * kXaWords;
-  // a stopped loop: nothing to do (every CTA reads the same flag: the Book
-  // is only written after cluster barrier 2)
-  if (*reinterpret_cast<volatile int*>(&bk->stop)) return;
   __shared__ Book<T> sbk;
   __shared__ DecideIn<T> s_din;
   __shared__ double s_tot[24];
@@ -763,7 +760,6 @@ __global__ void __launch_bounds__(kCT, 1) ctail_kernel(const TailArgs<T> t) {
     reinterpret_cast<unsigned long long*>(&sbk)[tid] = w;
   }
   if (lead) {
-    if (tid < kXaP) xn[tid] = 0;  // the next sweep's accumulators
     if (tid >= 32 && tid < 48) s_P[tid - 32] = 0;
     if (tid >= 64 && tid < 68) s_R[tid - 64] = 0;
   }
@@ -806,8 +802,13 @@ __global__ void __launch_bounds__(kCT, 1) ctail_kernel(const TailArgs<T> t) {
     f_ab[k] = ld_keep((row ? t.a : t.b) + i);
     f_pq[k] = ld_keep((row ? t.p : t.q) + i);
     f_old[k] = ld_keep((row ? t.phi : t.varphi) + i);
-    if (fp) f_rso[k] = ld_keep((row ? t.r_old : t.s_old) + i);
+    f_rso[k] = ld_keep((row ? t.r_old : t.s_old) + i);  // (used when fp)
   }
+  // a stopped loop: nothing to do and nothing may be written (every CTA reads
+  // the same flag: the Book is only written after cluster barrier 2).  Read
+  // after the loads above are in flight, so its latency overlaps theirs.
+  if (*reinterpret_cast<volatile int*>(&bk->stop)) return;
+  if (lead && tid < kXaP) xn[tid] = 0;  // the next sweep's accumulators
   TAIL_STAMP(8);
   // ---- A: merge (solver.hpp:269-272) and its exact sums ----------------------
   // {sum r, |r|^2, |s|^2, sum p a, sum p r, sum q b, sum q s}
