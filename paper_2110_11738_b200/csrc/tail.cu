@@ -645,27 +645,29 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned
 
 // ---------------------------------------------------------------------------
 // KC: the same tail as ONE thread-block cluster (16 -- or 8 -- CTAs of
-// kCT threads in one GPC), for a single GPU in fixed-point mode when
-// m + n fits the cluster's update threads (kCK elements each: 28 672 at 16
-// CTAs).  The grid tail's two global round trips per reduction (arrival
-// atomics + spin on an L2 counter, then a load of the totals) become a
-// hardware cluster barrier and distributed-shared-memory reads; the 16 CTAs
-// leave 132 SMs to the next sweep, whose CTAs (programmatic dependents)
-// become resident and prime their rings while the tail runs.  The exact
-// integer sums make the totals independent of the partition, so KC and the
-// grid tail give bit-identical iterations (tests/test_tail_gpu.py).
+// kCT threads in one GPC), for a single GPU in fixed-point mode when m + n
+// fits the updating CTAs' threads (kCK elements each: 26 880 at 16 CTAs).
+// The grid tail's global round trips per reduction (arrival atomics + spin on
+// an L2 counter, then a load of the totals) become hardware cluster barriers
+// and distributed-shared-memory reads; the 16 CTAs leave 132 SMs to the next
+// sweep, whose CTAs (programmatic dependents) become resident and prime their
+// rings while the tail runs.  The exact integer sums make the totals
+// independent of the partition, so KC and the grid tail give bit-identical
+// iterations (tests/test_tail_gpu.py).
 //   prologue  Book, the sweep's exact totals (complete: kernel boundary) and
-//             the previous iteration's update sums; each update thread loads
-//             its <= kCK elements' inputs at once
-//   A  merge  r = u - p, s = v - q from the fixed-point sums; CTA partials of
-//             the 7 merge sums -> cluster barrier 1 -> every CTA adds the C
-//             partials over DSMEM (same totals everywhere)
-//   B  warp 0: the decision; warp 1: the previous iteration's commit and
-//      patch; warps 2..: the update + its 8 exact sums, added into CTA 0's
-//      shared memory (DSMEM atomics) -> cluster barrier 2 -> CTA 0 stores the
-//      sums and the Book
+//             the previous iteration's update sums; each update thread of
+//             CTAs 1.. loads its <= kCK elements' inputs at once; then the
+//             stop flag
+//   A  merge  (CTAs 1..) r = u - p, s = v - q from the fixed-point sums; CTA
+//             partials of the 7 merge sums -> cluster barrier 1 -> every CTA
+//             adds the C partials over DSMEM (same totals everywhere)
+//   B  CTA 0, thread 0: the decision, pushed to every CTA's shared memory;
+//      thread 32: the previous iteration's commit and patch.  CTAs 1..,
+//      warps 2..: the update + its 8 exact sums, added into CTA 0's shared
+//      memory (DSMEM atomics) -> cluster barrier 2 -> CTA 0 stores the sums
+//      and the Book
 //   C  (only when the gate fired) exact dual value, recheck and the exact
-//      report, reduced the same way
+//      report over the cluster, reduced the same way
 // ---------------------------------------------------------------------------
 constexpr int kCT = 512;                 // threads per cluster CTA
 constexpr int kCUT = kCT - 32 * kUW;     // update threads per cluster CTA
