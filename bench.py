@@ -574,7 +574,9 @@ def time_to_tol_c2(args, drot, torch, dist, m, n, m_global, rank, world, local_r
     bit-identical to the one-GPU solve, so the iteration count is the N = 1
     count and the time is directly comparable.  Device time = CUDA events on
     the session stream around run(), max over ranks."""
-    cfg = drot.DrotConfig(max_iters=args.ttt_max_iters, record_trace=False, device=local_rank)
+    # reference defaults throughout, record_trace included (solver.hpp:72):
+    # the same per-iteration work as the headline step
+    cfg = drot.DrotConfig(max_iters=args.ttt_max_iters, device=local_rank)
     m_global = m
     if world > 1:
         sess = make_shard(drot, dist, args, m_global, n, np.float32, cfg, rank, world)

@@ -781,6 +781,10 @@ int Session<T>::build_graph(int64_t n_iters, bool timed, cudaGraphExec_t* exec_o
   h_folded = save_folded;
   if (rc) return rc;
   CUDA_TRY(cudaGraphInstantiate(exec_out, g, 0));
+  // upload now: a graph's first launch otherwise carries the upload of its
+  // nodes to the device (measured ~100 us for a 20-iteration graph at 10k^2,
+  // inside the first timed region that launches it)
+  CUDA_TRY(cudaGraphUpload(*exec_out, stream));
   ++graph_builds;
   *launches_out = kernel_launch_count() - before;
   count_launch(-*launches_out);  // captured, not launched
