@@ -669,8 +669,7 @@ __global__ void __launch_bounds__(kTT) tail_kernel(const TailArgs<T> t, unsigned
 //   C  (only when the gate fired) exact dual value, recheck and the exact
 //      report over the cluster, reduced the same way
 // ---------------------------------------------------------------------------
-constexpr int kCT = 512;                 // threads per cluster CTA
-constexpr int kCUT = kCT - 32 * kUW;     // update threads per cluster CTA
+constexpr int kCT = 512;                 // threads per cluster CTA (256 for small m + n)
 constexpr int kCK = 4;                   // elements per update thread (at most)
 
 __device__ __forceinline__ unsigned cluster_rank() {
@@ -733,8 +732,10 @@ __device__ __forceinline__ long long cta_sum_hilo(HiLo (&v)[K], long long* sh, S
   return s;
 }
 
-template <class T>
-__global__ void __launch_bounds__(kCT, 1) ctail_kernel(const TailArgs<T> t) {
+template <class T, int NT>
+__global__ void __launch_bounds__(NT, 1) ctail_kernel(const TailArgs<T> t) {
+  constexpr int kCT = NT;
+  constexpr int kCUT = NT - 32 * kUW;  // update threads per CTA
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr int BW = static_cast<int>(sizeof(Book<T>) / 8);
   constexpr int kW = kCT / 32;
@@ -1162,15 +1163,17 @@ int tail_grid(int device) {
 // size) when such a cluster of kCT-thread CTAs can be resident, else 8, else 0
 template <class T>
 int ctail_ctas(int device) {
+  for (void* f : {reinterpret_cast<void*>(ctail_kernel<T, kCT>),
+                  reinterpret_cast<void*>(ctail_kernel<T, kCT / 2>)}) {
+    cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+  }
   static std::atomic<int> cache[64];  // per device: 0 unknown, else size + 1
   std::atomic<int>& slot = cache[device & 63];
   const int got = slot.load(std::memory_order_acquire);
   if (got > 0) return got - 1;
   int size = 0;
-  cudaFuncSetAttribute(ctail_kernel<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  // max carveout, as the grid tail and K1 (see tail_grid)
-  cudaFuncSetAttribute(ctail_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                       cudaSharedmemCarveoutMaxShared);
   for (const int c : {16, 8}) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(c));
@@ -1183,7 +1186,8 @@ int ctail_ctas(int device) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int nc = 0;
-    if (cudaOccupancyMaxActiveClusters(&nc, ctail_kernel<T>, &cfg) == cudaSuccess && nc > 0) {
+    if (cudaOccupancyMaxActiveClusters(&nc, ctail_kernel<T, kCT>, &cfg) == cudaSuccess &&
+        nc > 0) {
       size = c;
       break;
     }
@@ -1203,10 +1207,16 @@ cudaError_t launch_tail(const TailArgs<T>& t, T* cpart, double* dpart, unsigned*
     cudaGetDevice(&dev);
     const int hw = ctail_ctas<T>(dev);
     const int c = hw < t.ctail ? hw : t.ctail;
-    if (c > 0 && t.m + t.n <= static_cast<int64_t>(c - 1) * kCUT * kCK) {
+    // half-size CTAs when every element still gets its own thread (cheaper
+    // CTA barriers and reductions where the tail is latency-bound: 14.3 vs
+    // 14.5 us per iteration at 1000^2 fp64; with more elements per thread
+    // they lose, 61.9 vs 59.6 at 5000^2 fp32 -- same-box A/B)
+    const int64_t need = t.m + t.n;
+    const int nt = need <= static_cast<int64_t>(c - 1) * (kCT / 2 - 32 * kUW) ? kCT / 2 : kCT;
+    if (c > 0 && need <= static_cast<int64_t>(c - 1) * (kCT - 32 * kUW) * kCK) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(static_cast<unsigned>(c));
-      cfg.blockDim = dim3(kCT);
+      cfg.blockDim = dim3(nt);
       cfg.stream = st;
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1216,7 +1226,8 @@ cudaError_t launch_tail(const TailArgs<T>& t, T* cpart, double* dpart, unsigned*
       cfg.attrs = at;
       cfg.numAttrs = 1;
       count_launch();
-      return cudaLaunchKernelEx(&cfg, ctail_kernel<T>, t);
+      return nt == kCT ? cudaLaunchKernelEx(&cfg, ctail_kernel<T, kCT>, t)
+                       : cudaLaunchKernelEx(&cfg, ctail_kernel<T, kCT / 2>, t);
     }
   }
   cudaLaunchConfig_t cfg = {};

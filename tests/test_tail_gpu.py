@@ -157,12 +157,14 @@ def test_max_iters_report_gap(drot, dt):
 
 
 @pytest.mark.parametrize("dt", [np.float32, np.float64])
-@pytest.mark.parametrize("shape", [(700, 500), (3000, 2000), (9000, 7000), (13440, 13440),
-                                   (13441, 13440)])
+@pytest.mark.parametrize("shape", [(700, 500), (1500, 1380), (3000, 2000), (9000, 7000),
+                                   (13440, 13440), (13441, 13440)])
 def test_cluster_tail_equals_grid_tail(drot, dt, shape):
     """The cluster tail (KC, tail.cu: one 16- or 8-CTA cluster, DSMEM
     reductions) and the grid tail (148 CTAs, counter barriers) sum the same
-    exact integers: bitwise identical iterates, duals and reports.  9000 +
+    exact integers: bitwise identical iterates, duals and reports.  Up to
+    15 * 192 = 2880 elements the cluster's CTAs have 256 threads (1500 + 1380
+    is the last such size), then 512.  9000 +
     7000 elements exceed an 8-CTA cluster (7 updating CTAs: 12 544 slots,
     so the grid tail runs) but fit 16 (26 880: 13 440 + 13 440 uses every
     slot, one more row falls back to the grid tail)."""
